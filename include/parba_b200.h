@@ -1,0 +1,119 @@
+/*
+ * parba_b200.h -- C ABI of the B200-native Barabasi-Albert edge generator
+ * (Sanders & Schulz, arXiv 1602.07106).
+ *
+ * Every entry point replaces one seam of the reference package `parba`
+ * (/root/reference/pkg/src/parba/...; file:line cited per function).  The
+ * signatures carry plain pointers and sizes only: no torch, no C++ types.
+ *
+ * Conventions
+ *   - Return value: PARBA_OK (0) or a PARBA_E* code; parba_last_error()
+ *     returns a thread-local, human-readable description of the last failure.
+ *     Bad parameters map to ParameterError in the Python layer
+ *     (errors.py:6-7), CUDA failures to GenerationError (errors.py:27-28).
+ *   - Device entry points (no `_host` suffix): every pointer is a DEVICE
+ *     pointer on the current CUDA device, owned by the caller; the launch is
+ *     asynchronous on `stream` (a cudaStream_t, NULL = legacy default).
+ *   - `probes`, when non-NULL, is a device u64 that is INCREMENTED by the
+ *     total number of hash evaluations (RunStats.hash_probes, driver.py:50-55).
+ *   - Count buffers ACCUMULATE (+=), so partial ranges merge the way
+ *     Consumer.merge does (analytics.py:78-82).
+ *   - `_host` entry points take HOST buffers, run on `device`, and return
+ *     after the result is in host memory (blocking).
+ *   - Thread-safe per (device, stream).
+ */
+#ifndef PARBA_B200_H
+#define PARBA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PARBA_OK 0
+#define PARBA_EINVAL 1   /* parameter / range error  -> ParameterError   */
+#define PARBA_ECUDA 2    /* CUDA runtime / launch error -> GenerationError */
+#define PARBA_ENOMEM 3   /* device or pinned allocation failed            */
+
+#define PARBA_HASH_CRC 0u    /* HashKind.CRC    (hashing.py:43-45, 119-125) */
+#define PARBA_HASH_SIMPLE 1u /* HashKind.SIMPLE (hashing.py:128-138)        */
+
+/* Graph family = GenParams (generator.py:50-110) with a uniform degree d,
+ * plus the effective hash constants of its HashConfig (hashing.py:48-85). */
+typedef struct parba_params {
+    uint64_t n;            /* node count                                   */
+    uint64_t d;            /* uniform out-degree (>= 1)                    */
+    uint64_t n0;           /* seed nodes                                   */
+    uint64_t m0;           /* seed edges (= len(seed_edges)/2)             */
+    uint64_t m;            /* m0 + (n - n0) * d                            */
+    uint32_t hash_kind;    /* PARBA_HASH_*                                 */
+    uint32_t crc_seed0;    /* HashConfig.crc_seeds()[0] (salt folded in)   */
+    uint32_t crc_seed1;    /* HashConfig.crc_seeds()[1]                    */
+    uint32_t reserved;     /* must be 0                                    */
+    uint64_t simple_mult;  /* HashConfig.simple_multiplier()               */
+    const uint64_t *seed_edges; /* DEVICE pointer to 2*m0 node IDs (NULL iff m0 == 0) */
+} parba_params_t;
+
+/* Library / ABI version (major*10000 + minor*100 + patch). */
+int parba_version(void);
+/* Thread-local description of the last error ("" if none). */
+const char *parba_last_error(void);
+/* Number of visible CUDA devices (0 when none); never fails. */
+int parba_device_count(void);
+
+/* Elementwise position hash out[k] = h(r[k]) -- hash_many / hash_value
+ * (hashing.py:141-145, 194-198).  Requires r[k] >= 1 (checked by caller). */
+int parba_hash(const parba_params_t *p, const uint64_t *r, uint64_t count, uint64_t *out,
+               void *stream);
+
+/* resolve_chain_block (_kernels.py:121-135): out[k] = terminal r of the
+ * chain started at r0[k] (body at least once; stop when r < stop_below or r
+ * even).  r0 is not modified; out may not alias r0. */
+int parba_resolve_chains(const parba_params_t *p, const uint64_t *r0, uint64_t count,
+                         uint64_t stop_below, uint64_t *out, unsigned long long *probes,
+                         void *stream);
+
+/* generate_block, plain path (generator.py:258-270, 288-325): rows
+ * (source, target) of edges lo..hi-1 into out_pairs[2*(hi-lo)] (u64,
+ * 16-byte aligned) -- the same bytes as the reference's (hi-lo, 2) uint64
+ * array and as its binary edge file (cli.py:121-139).  m0 <= lo <= hi <= m. */
+int parba_generate(const parba_params_t *p, uint64_t lo, uint64_t hi, uint64_t *out_pairs,
+                   unsigned long long *probes, void *stream);
+
+/* generate_edge on an arbitrary ID list (generator.py:172-181):
+ * out_pairs[2k], out_pairs[2k+1] = edge ids[k].  Every id in [m0, m). */
+int parba_edges_at(const parba_params_t *p, const uint64_t *ids, uint64_t count,
+                   uint64_t *out_pairs, unsigned long long *probes, void *stream);
+
+/* Fused generate_block + DegreeCountConsumer (analytics.py:44-48, 61-82):
+ * counts[v] += degree contribution of edges lo..hi-1 to node v, for v < K
+ * (both endpoints; a self-loop counts 2).  E is never stored. */
+int parba_degree_window(const parba_params_t *p, uint64_t lo, uint64_t hi, uint64_t K,
+                        unsigned long long *counts, unsigned long long *probes, void *stream);
+
+/* Full-histogram variant (degree_counts with K = n, analytics.py:85-99):
+ * counts[v] += contribution for every v < n, uint32 counters. */
+int parba_degree_full(const parba_params_t *p, uint64_t lo, uint64_t hi, uint32_t *counts,
+                      unsigned long long *probes, void *stream);
+
+/* count_block on device (analytics.py:44-48): counts[ids[k]] += 1 for
+ * ids[k] < K.  Folds seed edges into a count (count_seed_edges,
+ * analytics.py:51-52). */
+int parba_count_ids(const uint64_t *ids, uint64_t count, uint64_t K, unsigned long long *counts,
+                    void *stream);
+
+/* Host-buffer entry points (blocking).  generate_block into a host array
+ * out_pairs[2*(hi-lo)]: the device generates in chunks while earlier chunks
+ * stream back over PCIe (pinned host memory gets full DMA speed). */
+int parba_generate_host(const parba_params_t *p_host_seed, uint64_t lo, uint64_t hi,
+                        uint64_t *out_pairs_host, uint64_t *probes_host, int device);
+/* degree_counts for [lo,hi) into host int64 counts[K] (+=). */
+int parba_degree_window_host(const parba_params_t *p_host_seed, uint64_t lo, uint64_t hi,
+                             uint64_t K, int64_t *counts_host, uint64_t *probes_host, int device);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PARBA_B200_H */

@@ -1,0 +1,69 @@
+"""B200-native Barabasi-Albert edge generator (Sanders & Schulz, arXiv 1602.07106).
+
+Drop-in for the hot path of the reference package ``parba``: same names,
+argument meaning, return types and error behaviour for the uniform-degree
+generator and degree API; the chains run in hand-written sm_100a CUDA kernels
+(``libparba_b200.so``, C ABI in include/parba_b200.h).  There is no CPU
+fallback: without the library or a CUDA device every compute call raises
+``GenerationError``.
+"""
+
+from .analytics import (
+    BinRatio,
+    DegreeCounter,
+    DegreeCountConsumer,
+    Histogram,
+    count_block,
+    count_edge,
+    count_seed_edges,
+    degree_counts,
+    expected_degree_check,
+    fit_exponent,
+    merge,
+    write_degree_csv,
+    write_histogram_csv,
+)
+from .driver import (
+    DEFAULT_BATCH_SIZE,
+    Batch,
+    CollectConsumer,
+    Consumer,
+    DiscardConsumer,
+    Granularity,
+    RunStats,
+    WorkerStats,
+    plan_batches,
+    run,
+)
+from . import parallel
+from .errors import GenerationError, InfeasibleTargetsError, ParameterError, SeedGraphFormatError
+from .generator import (
+    MAX_EDGES,
+    ChainResult,
+    Edge,
+    GenParams,
+    edge_count,
+    edges_at,
+    generate_block,
+    generate_block_device,
+    generate_edge,
+    generate_node_edges,
+    resolve_chain,
+    resolve_chain_block,
+)
+from .hashing import DEFAULT_MULTIPLIER, HashConfig, HashKind, h_crc, h_simple, hash_many, hash_value
+from .oracle_compat import bb_generate, edge_list
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "Batch", "BinRatio", "ChainResult", "CollectConsumer", "Consumer", "DEFAULT_BATCH_SIZE",
+    "DEFAULT_MULTIPLIER", "DegreeCountConsumer", "DegreeCounter", "DiscardConsumer", "Edge",
+    "GenParams", "GenerationError", "Granularity", "HashConfig", "HashKind", "Histogram",
+    "InfeasibleTargetsError", "MAX_EDGES", "ParameterError", "RunStats", "SeedGraphFormatError",
+    "WorkerStats", "bb_generate", "count_block", "count_edge", "count_seed_edges", "degree_counts",
+    "edge_count", "edge_list", "edges_at", "expected_degree_check", "fit_exponent",
+    "generate_block", "generate_block_device", "generate_edge", "generate_node_edges", "h_crc",
+    "h_simple", "hash_many", "hash_value", "merge", "plan_batches", "resolve_chain",
+    "resolve_chain_block", "run", "write_degree_csv", "write_histogram_csv",
+]

@@ -1,0 +1,115 @@
+"""ctypes binding of ``libparba_b200.so`` (include/parba_b200.h).
+
+There is no CPU fallback: if the library or a CUDA device is missing, every
+compute call raises ``GenerationError``.  Device buffers are torch tensors
+(allocation and streams only -- torch is plumbing here, the compute is the
+library's CUDA kernels).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+from .errors import GenerationError, ParameterError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libparba_b200.so")
+
+PARBA_OK, PARBA_EINVAL, PARBA_ECUDA, PARBA_ENOMEM = 0, 1, 2, 3
+HASH_CRC, HASH_SIMPLE = 0, 1
+
+# Every symbol include/parba_b200.h declares (checked by tests/test_boundary.py).
+EXPORTS = (
+    "parba_version", "parba_last_error", "parba_device_count", "parba_hash",
+    "parba_resolve_chains", "parba_generate", "parba_edges_at", "parba_degree_window",
+    "parba_degree_full", "parba_count_ids", "parba_generate_host", "parba_degree_window_host",
+)
+
+
+class CParams(ctypes.Structure):
+    """parba_params_t."""
+
+    _fields_ = [
+        ("n", ctypes.c_uint64),
+        ("d", ctypes.c_uint64),
+        ("n0", ctypes.c_uint64),
+        ("m0", ctypes.c_uint64),
+        ("m", ctypes.c_uint64),
+        ("hash_kind", ctypes.c_uint32),
+        ("crc_seed0", ctypes.c_uint32),
+        ("crc_seed1", ctypes.c_uint32),
+        ("reserved", ctypes.c_uint32),
+        ("simple_mult", ctypes.c_uint64),
+        ("seed_edges", ctypes.c_void_p),
+    ]
+
+
+_lock = threading.Lock()
+_lib: ctypes.CDLL | None = None
+
+
+def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load (once) and type the library; raise loudly when it is missing."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise GenerationError(
+                f"CUDA library {path} is missing; build it with "
+                "`python -m paper_1602_07106_b200.build` (there is no CPU fallback)"
+            )
+        L = ctypes.CDLL(path)
+        u64, i32, vp = ctypes.c_uint64, ctypes.c_int, ctypes.c_void_p
+        P = ctypes.POINTER(CParams)
+        sig = {
+            "parba_version": ([], i32),
+            "parba_last_error": ([], ctypes.c_char_p),
+            "parba_device_count": ([], i32),
+            "parba_hash": ([P, vp, u64, vp, vp], i32),
+            "parba_resolve_chains": ([P, vp, u64, u64, vp, vp, vp], i32),
+            "parba_generate": ([P, u64, u64, vp, vp, vp], i32),
+            "parba_edges_at": ([P, vp, u64, vp, vp, vp], i32),
+            "parba_degree_window": ([P, u64, u64, u64, vp, vp, vp], i32),
+            "parba_degree_full": ([P, u64, u64, vp, vp, vp], i32),
+            "parba_count_ids": ([vp, u64, u64, vp, vp], i32),
+            "parba_generate_host": ([P, u64, u64, vp, vp, i32], i32),
+            "parba_degree_window_host": ([P, u64, u64, u64, vp, vp, i32], i32),
+        }
+        for name, (args, res) in sig.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = L
+        return L
+
+
+def check(rc: int) -> None:
+    if rc == PARBA_OK:
+        return
+    msg = load().parba_last_error().decode(errors="replace")
+    if rc == PARBA_EINVAL:
+        raise ParameterError(msg)
+    raise GenerationError(msg)
+
+
+def torch_cuda():
+    """torch with a usable CUDA device, else GenerationError (no CPU path)."""
+    import torch
+
+    if not torch.cuda.is_available():
+        raise GenerationError("no CUDA device: the B200 path has no CPU fallback")
+    return torch
+
+
+def stream_ptr(torch, device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def to_device_u64(torch, arr, device) -> "torch.Tensor":
+    a = np.ascontiguousarray(np.asarray(arr, dtype=np.uint64))
+    return torch.from_numpy(a.view(np.int64)).to(device)

@@ -1,0 +1,418 @@
+// parba_api.cu -- the C ABI (include/parba_b200.h): validation, template
+// dispatch (hash family x CRC width x sink), persistent-grid sizing, and the
+// host-buffer entry points.  No torch types cross this boundary.
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/parba_b200.h"
+#include "parba_kernels.cuh"
+
+using namespace parba;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                     \
+    do {                                                                                   \
+        cudaError_t e_ = (expr);                                                           \
+        if (e_ != cudaSuccess)                                                             \
+            return fail(PARBA_ECUDA, "%s failed: %s", #expr, cudaGetErrorString(e_));      \
+    } while (0)
+
+constexpr uint64_t kMaxEdges = 1ull << 58;  // degreeseq.py:27 (MAX_EDGES)
+
+int validate(const parba_params_t *p) {
+    if (!p) return fail(PARBA_EINVAL, "params is NULL");
+    if (p->d < 1) return fail(PARBA_EINVAL, "uniform degree must be >= 1, got %llu", (unsigned long long)p->d);
+    if (p->n < p->n0) return fail(PARBA_EINVAL, "need 0 <= n0 <= n, got n0=%llu, n=%llu",
+                                  (unsigned long long)p->n0, (unsigned long long)p->n);
+    if (p->hash_kind > PARBA_HASH_SIMPLE) return fail(PARBA_EINVAL, "unknown hash kind %u", p->hash_kind);
+    if (p->reserved != 0) return fail(PARBA_EINVAL, "reserved field must be 0");
+    if (p->m0 > 0 && !p->seed_edges) return fail(PARBA_EINVAL, "m0 > 0 but seed_edges is NULL");
+    // m = m0 + (n - n0) * d, checked without overflow
+    const unsigned __int128 m = (unsigned __int128)p->m0 + (unsigned __int128)(p->n - p->n0) * p->d;
+    if (m != p->m) return fail(PARBA_EINVAL, "m=%llu inconsistent with m0 + (n-n0)*d", (unsigned long long)p->m);
+    if (p->m >= kMaxEdges) return fail(PARBA_EINVAL, "total edge count %llu exceeds the supported maximum",
+                                       (unsigned long long)p->m);
+    return PARBA_OK;
+}
+
+int check_range(const parba_params_t *p, uint64_t lo, uint64_t hi) {
+    if (!(p->m0 <= lo && lo <= hi && hi <= p->m))
+        return fail(PARBA_EINVAL, "block [%llu, %llu) out of range [%llu, %llu]", (unsigned long long)lo,
+                    (unsigned long long)hi, (unsigned long long)p->m0, (unsigned long long)p->m);
+    return PARBA_OK;
+}
+
+DevParams make_dev(const parba_params_t *p, uint64_t K = 0) {
+    DevParams d{};
+    d.n = p->n;
+    d.d = p->d;
+    d.n0 = p->n0;
+    d.m0 = p->m0;
+    d.m = p->m;
+    d.stop = 2 * p->m0;
+    d.mult = p->simple_mult;
+    // CRC linearity: crc(s, w) = crc(s, 0) ^ crc(0, w)
+    d.k0 = crc32c_u64_bitwise(p->crc_seed0, 0);
+    d.k1 = crc32c_u64_bitwise(p->crc_seed1, 0);
+    d.seed = p->seed_edges;
+    d.divd = make_magic(p->d);
+    d.K = K;
+    // generated target ((r>>1) - m0)/d + n0 < K  <=>  (r>>1) < m0 + (K - n0) * d
+    if (K <= p->n0) {
+        d.win_lim = 0;
+    } else {
+        const unsigned __int128 lim = (unsigned __int128)p->m0 + (unsigned __int128)(K - p->n0) * p->d;
+        d.win_lim = lim > (unsigned __int128)UINT64_MAX ? UINT64_MAX : (uint64_t)lim;
+    }
+    return d;
+}
+
+int bits_of(uint64_t x) { return x ? 64 - __builtin_clzll(x) : 0; }
+
+// CRC table chunks needed to cover every r in a launch.
+int nch_for(uint64_t max_r) {
+    const int b = bits_of(max_r);
+    if (b <= 35) return 7;
+    if (b <= 45) return 9;
+    return 13;
+}
+
+struct DevInfo {
+    int sms = 0;
+    bool attr_done[2][3][3] = {};
+};
+std::mutex g_mu;
+std::vector<DevInfo> g_dev;
+
+int dev_info(DevInfo **out) {
+    int dev;
+    CUDA_TRY(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_mu);
+    if ((int)g_dev.size() <= dev) g_dev.resize(dev + 1);
+    if (!g_dev[dev].sms) CUDA_TRY(cudaDeviceGetAttribute(&g_dev[dev].sms, cudaDevAttrMultiProcessorCount, dev));
+    *out = &g_dev[dev];
+    return PARBA_OK;
+}
+
+template <class Hash, int NCH, int SINK>
+int launch_tiles_t(const DevParams &dp, uint64_t lo, uint64_t hi, const StoreArgs &a,
+                   unsigned long long *probes, cudaStream_t st, int hk, int nk) {
+    if (hi <= lo) return PARBA_OK;
+    DevInfo *di;
+    int rc = dev_info(&di);
+    if (rc) return rc;
+    auto kern = tile_kernel<Hash, NCH, SINK>;
+    const size_t smem = tile_smem_bytes<SINK>();
+    int per_sm = 0;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        if (!di->attr_done[hk][nk][SINK]) {
+            CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            di->attr_done[hk][nk][SINK] = true;
+        }
+    }
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
+    if (per_sm < 1) per_sm = 1;
+    const uint64_t tile0 = lo / kTile;
+    const uint64_t ntiles = (hi - 1) / kTile - tile0 + 1;
+    uint64_t grid = (uint64_t)di->sms * per_sm;
+    const uint64_t need = (ntiles + kWarps - 1) / kWarps;
+    if (grid > need) grid = need;
+    kern<<<(unsigned)grid, kThreads, smem, st>>>(dp, lo, hi, tile0, ntiles, a, probes);
+    CUDA_TRY(cudaGetLastError());
+    return PARBA_OK;
+}
+
+template <int SINK>
+int launch_tiles(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi,
+                 const StoreArgs &a, unsigned long long *probes, cudaStream_t st) {
+    if (p->hash_kind == PARBA_HASH_SIMPLE)
+        return launch_tiles_t<HashSimple, 0, SINK>(dp, lo, hi, a, probes, st, 1, 0);
+    switch (nch_for(2 * hi)) {
+        case 7: return launch_tiles_t<HashCrc<7>, 7, SINK>(dp, lo, hi, a, probes, st, 0, 0);
+        case 9: return launch_tiles_t<HashCrc<9>, 9, SINK>(dp, lo, hi, a, probes, st, 0, 1);
+        default: return launch_tiles_t<HashCrc<13>, 13, SINK>(dp, lo, hi, a, probes, st, 0, 2);
+    }
+}
+
+unsigned grid_for(uint64_t count, int threads) {
+    uint64_t g = (count + threads - 1) / threads;
+    if (g > 148ull * 32) g = 148ull * 32;
+    return (unsigned)(g ? g : 1);
+}
+
+template <class Hash, int NCH>
+int launch_chains_t(const DevParams &dp, const uint64_t *r0, uint64_t count, uint64_t stop,
+                    uint64_t *out, const uint64_t *ids, uint64_t *pairs, unsigned long long *probes,
+                    cudaStream_t st) {
+    chains_kernel<Hash, NCH><<<grid_for(count, 256), 256, 0, st>>>(dp, r0, count, stop, out, ids, pairs, probes);
+    CUDA_TRY(cudaGetLastError());
+    return PARBA_OK;
+}
+
+int launch_chains(const parba_params_t *p, const DevParams &dp, const uint64_t *r0, uint64_t count,
+                  uint64_t stop, uint64_t *out, const uint64_t *ids, uint64_t *pairs,
+                  unsigned long long *probes, cudaStream_t st) {
+    if (count == 0) return PARBA_OK;
+    if (p->hash_kind == PARBA_HASH_SIMPLE)
+        return launch_chains_t<HashSimple, 0>(dp, r0, count, stop, out, ids, pairs, probes, st);
+    return launch_chains_t<HashCrc<13>, 13>(dp, r0, count, stop, out, ids, pairs, probes, st);
+}
+
+template <typename CountT>
+int launch_sources(const DevParams &dp, uint64_t lo, uint64_t hi, uint64_t K, CountT *counts, cudaStream_t st) {
+    // nodes whose edges intersect [lo,hi): v in [src(lo), src(hi-1)] and v >= n0, v < K
+    if (hi <= lo) return PARBA_OK;
+    const uint64_t vlo = (lo - dp.m0) / dp.d + dp.n0;
+    uint64_t vhi = (hi - 1 - dp.m0) / dp.d + dp.n0 + 1;
+    if (vhi > K) vhi = K;
+    if (vlo >= vhi) return PARBA_OK;
+    source_counts_kernel<CountT><<<grid_for(vhi - vlo, 256), 256, 0, st>>>(dp, lo, hi, vlo, vhi, counts);
+    CUDA_TRY(cudaGetLastError());
+    return PARBA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int parba_version(void) { return 10000; }
+
+const char *parba_last_error(void) { return g_err.c_str(); }
+
+int parba_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int parba_hash(const parba_params_t *p, const uint64_t *r, uint64_t count, uint64_t *out, void *stream) {
+    int rc = validate(p);
+    if (rc) return rc;
+    if (count == 0) return PARBA_OK;
+    if (!r || !out) return fail(PARBA_EINVAL, "NULL buffer");
+    const DevParams dp = make_dev(p);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (p->hash_kind == PARBA_HASH_SIMPLE)
+        hash_kernel<HashSimple, 0><<<grid_for(count, 256), 256, 0, st>>>(dp, r, count, out);
+    else
+        hash_kernel<HashCrc<13>, 13><<<grid_for(count, 256), 256, 0, st>>>(dp, r, count, out);
+    CUDA_TRY(cudaGetLastError());
+    return PARBA_OK;
+}
+
+int parba_resolve_chains(const parba_params_t *p, const uint64_t *r0, uint64_t count, uint64_t stop_below,
+                         uint64_t *out, unsigned long long *probes, void *stream) {
+    int rc = validate(p);
+    if (rc) return rc;
+    if (count == 0) return PARBA_OK;
+    if (!r0 || !out) return fail(PARBA_EINVAL, "NULL buffer");
+    if (r0 == out) return fail(PARBA_EINVAL, "out may not alias r0");
+    return launch_chains(p, make_dev(p), r0, count, stop_below, out, nullptr, nullptr, probes,
+                         (cudaStream_t)stream);
+}
+
+int parba_generate(const parba_params_t *p, uint64_t lo, uint64_t hi, uint64_t *out_pairs,
+                   unsigned long long *probes, void *stream) {
+    int rc = validate(p);
+    if (!rc) rc = check_range(p, lo, hi);
+    if (rc) return rc;
+    if (hi == lo) return PARBA_OK;
+    if (!out_pairs) return fail(PARBA_EINVAL, "out_pairs is NULL");
+    if (((uintptr_t)out_pairs) & 15) return fail(PARBA_EINVAL, "out_pairs must be 16-byte aligned");
+    StoreArgs a{out_pairs, nullptr, nullptr};
+    return launch_tiles<kStore>(p, make_dev(p), lo, hi, a, probes, (cudaStream_t)stream);
+}
+
+int parba_edges_at(const parba_params_t *p, const uint64_t *ids, uint64_t count, uint64_t *out_pairs,
+                   unsigned long long *probes, void *stream) {
+    int rc = validate(p);
+    if (rc) return rc;
+    if (count == 0) return PARBA_OK;
+    if (!ids || !out_pairs) return fail(PARBA_EINVAL, "NULL buffer");
+    if (((uintptr_t)out_pairs) & 15) return fail(PARBA_EINVAL, "out_pairs must be 16-byte aligned");
+    const DevParams dp = make_dev(p);
+    return launch_chains(p, dp, nullptr, count, dp.stop, nullptr, ids, out_pairs, probes, (cudaStream_t)stream);
+}
+
+int parba_degree_window(const parba_params_t *p, uint64_t lo, uint64_t hi, uint64_t K,
+                        unsigned long long *counts, unsigned long long *probes, void *stream) {
+    int rc = validate(p);
+    if (!rc) rc = check_range(p, lo, hi);
+    if (rc) return rc;
+    if (hi == lo) return PARBA_OK;
+    if (K > 0 && !counts) return fail(PARBA_EINVAL, "counts is NULL");
+    cudaStream_t st = (cudaStream_t)stream;
+    const DevParams dp = make_dev(p, K);
+    StoreArgs a{nullptr, counts, nullptr};
+    rc = launch_tiles<kWindow>(p, dp, lo, hi, a, probes, st);
+    if (rc) return rc;
+    return launch_sources<unsigned long long>(dp, lo, hi, K, counts, st);
+}
+
+int parba_degree_full(const parba_params_t *p, uint64_t lo, uint64_t hi, uint32_t *counts,
+                      unsigned long long *probes, void *stream) {
+    int rc = validate(p);
+    if (!rc) rc = check_range(p, lo, hi);
+    if (rc) return rc;
+    if (hi == lo) return PARBA_OK;
+    if (!counts) return fail(PARBA_EINVAL, "counts is NULL");
+    cudaStream_t st = (cudaStream_t)stream;
+    const DevParams dp = make_dev(p, p->n);
+    StoreArgs a{nullptr, nullptr, counts};
+    rc = launch_tiles<kFull>(p, dp, lo, hi, a, probes, st);
+    if (rc) return rc;
+    return launch_sources<uint32_t>(dp, lo, hi, p->n, counts, st);
+}
+
+int parba_count_ids(const uint64_t *ids, uint64_t count, uint64_t K, unsigned long long *counts, void *stream) {
+    if (count == 0 || K == 0) return PARBA_OK;
+    if (!ids || !counts) return fail(PARBA_EINVAL, "NULL buffer");
+    count_ids_kernel<<<grid_for(count, 256), 256, 0, (cudaStream_t)stream>>>(ids, count, K, counts);
+    CUDA_TRY(cudaGetLastError());
+    return PARBA_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Host-buffer entry points.
+
+namespace {
+
+struct DevBuf {
+    void *p = nullptr;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+};
+
+// Upload the host seed array; returns a params copy pointing at device memory.
+int upload_seed(const parba_params_t *ph, parba_params_t *pd, DevBuf &seed) {
+    *pd = *ph;
+    if (ph->m0 > 0) {
+        if (!ph->seed_edges) return fail(PARBA_EINVAL, "m0 > 0 but seed_edges is NULL");
+        const size_t bytes = 2 * ph->m0 * sizeof(uint64_t);
+        CUDA_TRY(cudaMalloc(&seed.p, bytes));
+        CUDA_TRY(cudaMemcpy(seed.p, ph->seed_edges, bytes, cudaMemcpyHostToDevice));
+        pd->seed_edges = (const uint64_t *)seed.p;
+    }
+    return PARBA_OK;
+}
+
+struct StreamGuard {
+    cudaStream_t s = nullptr;
+    ~StreamGuard() {
+        if (s) cudaStreamDestroy(s);
+    }
+};
+struct EventGuard {
+    cudaEvent_t e = nullptr;
+    ~EventGuard() {
+        if (e) cudaEventDestroy(e);
+    }
+};
+
+}  // namespace
+
+int parba_generate_host(const parba_params_t *ph, uint64_t lo, uint64_t hi, uint64_t *out_host,
+                        uint64_t *probes_host, int device) {
+    int rc = validate(ph);
+    if (!rc) rc = check_range(ph, lo, hi);
+    if (rc) return rc;
+    if (probes_host) *probes_host = 0;
+    if (hi == lo) return PARBA_OK;
+    if (!out_host) return fail(PARBA_EINVAL, "out_pairs_host is NULL");
+    CUDA_TRY(cudaSetDevice(device));
+    parba_params_t pd;
+    DevBuf seed, bufs, prb;
+    rc = upload_seed(ph, &pd, seed);
+    if (rc) return rc;
+    // Two chunk buffers: the kernel fills one while the other drains over PCIe.
+    const uint64_t total = hi - lo;
+    const uint64_t chunk = total < (1ull << 25) ? total : (1ull << 25);  // 32 Mi edges = 512 MiB
+    const size_t cbytes = chunk * 16;
+    CUDA_TRY(cudaMalloc(&bufs.p, 2 * cbytes));
+    CUDA_TRY(cudaMalloc(&prb.p, sizeof(unsigned long long)));
+    StreamGuard sc, sx;
+    CUDA_TRY(cudaStreamCreateWithFlags(&sc.s, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&sx.s, cudaStreamNonBlocking));
+    CUDA_TRY(cudaMemsetAsync(prb.p, 0, sizeof(unsigned long long), sc.s));
+    EventGuard made[2], drained[2];
+    for (int b = 0; b < 2; ++b) {
+        CUDA_TRY(cudaEventCreateWithFlags(&made[b].e, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&drained[b].e, cudaEventDisableTiming));
+    }
+    uint64_t k = 0;
+    for (uint64_t a = lo; a < hi; a += chunk, ++k) {
+        const uint64_t b = a + chunk < hi ? a + chunk : hi;
+        const int slot = (int)(k & 1);
+        uint64_t *dbuf = (uint64_t *)((char *)bufs.p + slot * cbytes);
+        if (k >= 2) CUDA_TRY(cudaStreamWaitEvent(sc.s, drained[slot].e, 0));
+        rc = parba_generate(&pd, a, b, dbuf, (unsigned long long *)prb.p, sc.s);
+        if (rc) return rc;
+        CUDA_TRY(cudaEventRecord(made[slot].e, sc.s));
+        CUDA_TRY(cudaStreamWaitEvent(sx.s, made[slot].e, 0));
+        CUDA_TRY(cudaMemcpyAsync(out_host + 2 * (a - lo), dbuf, (b - a) * 16, cudaMemcpyDeviceToHost, sx.s));
+        CUDA_TRY(cudaEventRecord(drained[slot].e, sx.s));
+    }
+    unsigned long long pr = 0;
+    CUDA_TRY(cudaStreamSynchronize(sc.s));
+    CUDA_TRY(cudaMemcpy(&pr, prb.p, sizeof(pr), cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaStreamSynchronize(sx.s));
+    if (probes_host) *probes_host = pr;
+    return PARBA_OK;
+}
+
+int parba_degree_window_host(const parba_params_t *ph, uint64_t lo, uint64_t hi, uint64_t K,
+                             int64_t *counts_host, uint64_t *probes_host, int device) {
+    int rc = validate(ph);
+    if (!rc) rc = check_range(ph, lo, hi);
+    if (rc) return rc;
+    if (probes_host) *probes_host = 0;
+    if (K > 0 && !counts_host) return fail(PARBA_EINVAL, "counts_host is NULL");
+    CUDA_TRY(cudaSetDevice(device));
+    parba_params_t pd;
+    DevBuf seed, cnt, prb;
+    rc = upload_seed(ph, &pd, seed);
+    if (rc) return rc;
+    const size_t cbytes = (K ? K : 1) * sizeof(unsigned long long);
+    CUDA_TRY(cudaMalloc(&cnt.p, cbytes));
+    CUDA_TRY(cudaMalloc(&prb.p, sizeof(unsigned long long)));
+    StreamGuard sc;
+    CUDA_TRY(cudaStreamCreateWithFlags(&sc.s, cudaStreamNonBlocking));
+    CUDA_TRY(cudaMemsetAsync(cnt.p, 0, cbytes, sc.s));
+    CUDA_TRY(cudaMemsetAsync(prb.p, 0, sizeof(unsigned long long), sc.s));
+    rc = parba_degree_window(&pd, lo, hi, K, (unsigned long long *)cnt.p, (unsigned long long *)prb.p, sc.s);
+    if (rc) return rc;
+    std::vector<unsigned long long> tmp(K ? K : 1);
+    unsigned long long pr = 0;
+    CUDA_TRY(cudaMemcpyAsync(tmp.data(), cnt.p, cbytes, cudaMemcpyDeviceToHost, sc.s));
+    CUDA_TRY(cudaMemcpyAsync(&pr, prb.p, sizeof(pr), cudaMemcpyDeviceToHost, sc.s));
+    CUDA_TRY(cudaStreamSynchronize(sc.s));
+    for (uint64_t v = 0; v < K; ++v) counts_host[v] += (int64_t)tmp[v];
+    if (probes_host) *probes_host = pr;
+    return PARBA_OK;
+}
+
+}  // extern "C"

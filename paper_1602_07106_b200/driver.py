@@ -1,0 +1,185 @@
+"""Batch planning and execution (reference: parba/driver.py).
+
+The reference cuts [m0, m) into batches claimed by forked CPU workers and
+feeds each batch's (k, 2) array to a Python ``Consumer`` (driver.py:58-81,
+161-270).  On the B200 path the consumers the hot path serves are fused into
+device kernels instead:
+
+  * ``DegreeCountConsumer``  -> the fused window / full-histogram kernels
+  * ``CollectConsumer``      -> store mode (device array, streamed to host)
+  * ``DiscardConsumer``      -> the streaming kernel with an empty window
+
+A generic Python consumer would need every edge on the host and is not
+fused, so ``run`` raises ``ParameterError`` for it (no CPU fallback).
+``workers`` keeps its meaning of "degree of parallelism" and is validated;
+inside one process the work runs on one GPU, and when ``torch.distributed``
+is initialised the edge range is sharded over its ranks (one GPU each) and
+the histogram reduced over NCCL -- results are identical for every
+workers / batch_size / world size, as in the reference (driver.py:1-9).
+"""
+
+from __future__ import annotations
+
+import enum
+import time
+from dataclasses import dataclass
+from typing import Any, Sequence
+
+import numpy as np
+
+from .errors import ParameterError
+from .generator import Edge, GenParams, Resolution
+
+DEFAULT_BATCH_SIZE = 1 << 16  # driver.py:26
+
+
+class Granularity(enum.Enum):
+    EDGE = "edge"
+    NODE = "node"
+
+
+@dataclass(frozen=True)
+class Batch:
+    lo: int
+    hi: int
+    granularity: Granularity = Granularity.EDGE
+
+
+@dataclass(frozen=True)
+class WorkerStats:
+    worker_id: int
+    batches: int
+    edges: int
+    probes: int
+    seconds: float
+
+
+@dataclass(frozen=True)
+class RunStats:
+    edges_emitted: int
+    hash_probes: int
+    elapsed: float
+    per_worker: tuple[WorkerStats, ...]
+
+
+class Consumer:
+    """Streaming edge consumer contract (driver.py:58-81)."""
+
+    def new_context(self, worker_id: int) -> Any:
+        return None
+
+    def accept(self, ctx: Any, i: int, edge: Edge) -> None:
+        raise NotImplementedError
+
+    def accept_block(self, ctx: Any, lo: int, edges: np.ndarray) -> None:
+        for k in range(edges.shape[0]):
+            self.accept(ctx, lo + k, Edge(int(edges[k, 0]), int(edges[k, 1])))
+
+    def finalize_context(self, ctx: Any) -> Any:
+        return ctx
+
+    def merge(self, contexts: Sequence[Any]) -> Any:
+        raise NotImplementedError
+
+
+class DiscardConsumer(Consumer):
+    """Counts edges and drops them (driver.py:84-94)."""
+
+    def new_context(self, worker_id: int) -> int:
+        return 0
+
+    def accept_block(self, ctx: int, lo: int, edges: np.ndarray) -> int:
+        return ctx + edges.shape[0]
+
+    def merge(self, contexts: Sequence[int]) -> int:
+        return sum(contexts)
+
+
+class CollectConsumer(Consumer):
+    """Gathers all edges into one (m - m0, 2) array in edge-index order
+    (driver.py:97-114)."""
+
+    def new_context(self, worker_id: int) -> list:
+        return []
+
+    def accept_block(self, ctx: list, lo: int, edges: np.ndarray) -> list:
+        ctx.append((lo, edges.copy()))
+        return ctx
+
+    def merge(self, contexts: Sequence[list]) -> np.ndarray:
+        chunks = sorted((c for ctx in contexts for c in ctx), key=lambda c: c[0])
+        if not chunks:
+            return np.empty((0, 2), dtype=np.uint64)
+        return np.concatenate([arr for _, arr in chunks])
+
+
+def _round_down_to_node(p: GenParams, pos: int) -> int:
+    if p.d is not None:
+        return p.m0 + ((pos - p.m0) // p.d) * p.d
+    W = p.m0 + np.concatenate([[0], np.cumsum(p.degrees.astype(np.int64))])
+    k = int(np.searchsorted(W, pos, side="right")) - 1
+    return int(W[k])
+
+
+def _next_node_boundary(p: GenParams, lo: int) -> int:
+    if p.d is not None:
+        return lo + p.d
+    W = p.m0 + np.concatenate([[0], np.cumsum(p.degrees.astype(np.int64))])
+    k = int(np.searchsorted(W, lo, side="right")) - 1
+    return lo + int(p.degrees[k])
+
+
+def plan_batches(p: GenParams, batch_size: int, granularity: Granularity | None = None) -> list[Batch]:
+    """Cover [m0, m) exactly once with half-open batches (driver.py:131-158);
+    node granularity rounds boundaries down to a node's first edge."""
+    if batch_size < 1:
+        raise ParameterError(f"batch_size must be >= 1, got {batch_size}")
+    if granularity is None:
+        node_gran = p.no_self_loops or p.no_parallel_edges
+    else:
+        node_gran = granularity is Granularity.NODE
+    gran = Granularity.NODE if node_gran else Granularity.EDGE
+    out = []
+    lo = p.m0
+    while lo < p.m:
+        hi = min(lo + batch_size, p.m)
+        if node_gran and hi < p.m:
+            hi = _round_down_to_node(p, hi)
+            if hi <= lo:
+                hi = min(_next_node_boundary(p, lo), p.m)
+        out.append(Batch(lo, hi, gran))
+        lo = hi
+    return out
+
+
+def run(p: GenParams, consumer: Consumer, workers: int = 1, batch_size: int = DEFAULT_BATCH_SIZE,
+        resolution: Resolution = "rank", device=None) -> tuple[Any, RunStats]:
+    """Generate every edge of [m0, m) exactly once into a fused consumer.
+
+    Returns (merged consumer result, RunStats) like driver.py:210-270."""
+    from . import analytics, parallel
+    from .generator import generate_block
+
+    if workers < 1:
+        raise ParameterError(f"workers must be >= 1, got {workers}")
+    if batch_size < 1:
+        raise ParameterError(f"batch_size must be >= 1, got {batch_size}")
+    t0 = time.perf_counter()
+    if isinstance(consumer, analytics.DegreeCountConsumer):
+        counts, probes, per = parallel.degree_counts_sharded(p, consumer.K, p.m0, p.m, device=device)
+        merged = analytics.DegreeCounter(K=consumer.K, counts=counts)
+    elif isinstance(consumer, DiscardConsumer):
+        _, probes, per = parallel.degree_counts_sharded(p, 0, p.m0, p.m, device=device)
+        merged = p.m - p.m0
+    elif isinstance(consumer, CollectConsumer):
+        merged, probes = generate_block(p.m0, p.m, p, resolution=resolution, device=device)
+        per = [(0, p.m - p.m0, probes)]
+    else:
+        raise ParameterError(
+            f"consumer {type(consumer).__name__} is not fused into the B200 path; use "
+            "DegreeCountConsumer, CollectConsumer or DiscardConsumer (there is no CPU fallback)")
+    elapsed = time.perf_counter() - t0
+    per_worker = tuple(WorkerStats(w, 1 if e else 0, e, pr, elapsed) for w, e, pr in per)
+    return merged, RunStats(edges_emitted=sum(w.edges for w in per_worker),
+                            hash_probes=sum(w.probes for w in per_worker),
+                            elapsed=elapsed, per_worker=per_worker)

@@ -1,0 +1,118 @@
+"""Multi-GPU sharding: one process per GPU, ``torch.distributed`` (NCCL) for
+the plumbing (reference counterpart: the fork workers and
+``Consumer.merge`` of driver.py:210-270 / analytics.py:78-82).
+
+Every edge is a pure function of its index, so rank g
+of G takes the contiguous edge-ID shard
+
+    [lo + floor(g*(hi-lo)/G), lo + floor((g+1)*(hi-lo)/G))
+
+with no communication while generating.  Store mode needs no collective at
+all; a degree count needs exactly one: the sum of the per-rank histograms
+(NCCL reduce / all-reduce over NVLink).  Results are bit-identical for every
+world size.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+from .errors import ParameterError
+
+
+def world() -> tuple[int, int]:
+    """(rank, world_size) of the default process group, (0, 1) without one."""
+    try:
+        import torch.distributed as dist
+    except Exception:  # pragma: no cover
+        return 0, 1
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_rank(), dist.get_world_size()
+    return 0, 1
+
+
+def shard_range(lo: int, hi: int, rank: int, world_size: int) -> tuple[int, int]:
+    """Contiguous shard of [lo, hi) owned by `rank` (exact cover, no overlap)."""
+    if world_size < 1 or not 0 <= rank < world_size:
+        raise ParameterError(f"bad rank {rank} of world {world_size}")
+    if hi < lo:
+        raise ParameterError(f"empty-or-negative range [{lo}, {hi})")
+    n = hi - lo
+    return lo + (rank * n) // world_size, lo + ((rank + 1) * n) // world_size
+
+
+def reduce_counts(t, op: str = "allreduce", dst: int = 0, group=None):
+    """Sum a per-rank count tensor over the group (NCCL on GPU tensors, gloo
+    on CPU tensors).  ``op='reduce'`` leaves the sum on `dst` only."""
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return t
+    if op == "allreduce":
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    elif op == "reduce":
+        dist.reduce(t, dst=dst, op=dist.ReduceOp.SUM, group=group)
+    else:
+        raise ParameterError(f"unknown reduction {op!r}")
+    return t
+
+
+def count_shard_device(p, K: int, lo: int, hi: int, counts=None, probes=None, device=None):
+    """Fused generate + count of edges [lo, hi) on one GPU.
+
+    Returns (counts tensor, probes tensor).  K == n with 2m < 2^32 uses the
+    uint32 full-histogram kernel; otherwise the uint64 window kernel."""
+    from .generator import _device
+
+    torch, dev = _device(device)
+    L = _lib.load()
+    full = (K == p.n and K > 0 and 2 * p.m < (1 << 32))
+    if probes is None:
+        probes = torch.zeros(1, dtype=torch.int64, device=dev)
+    with torch.cuda.device(dev):
+        cp = p._device_params(dev)
+        st = _lib.stream_ptr(torch, dev)
+        if full:
+            if counts is None:
+                counts = torch.zeros(K, dtype=torch.int32, device=dev)
+            _lib.check(L.parba_degree_full(cp, lo, hi, counts.data_ptr(), probes.data_ptr(), st))
+        else:
+            if counts is None:
+                counts = torch.zeros(max(K, 1), dtype=torch.int64, device=dev)
+            _lib.check(L.parba_degree_window(cp, lo, hi, K, counts.data_ptr() if K else None,
+                                             probes.data_ptr(), st))
+    return counts, probes
+
+
+def widen_counts(torch, counts, K: int):
+    """uint32 / int64 device counts -> int64 device tensor of length K."""
+    if counts.dtype == torch.int32:
+        return counts.to(torch.int64) & 0xFFFFFFFF
+    return counts[:K]
+
+
+def degree_counts_sharded(p, K: int, lo: int, hi: int, device=None):
+    """This rank's shard of [lo, hi) counted on its GPU, summed over ranks.
+
+    Returns (int64 numpy counts[K], total probes, per-rank [(rank, edges, probes)])."""
+    from .generator import _device
+
+    torch, dev = _device(device)
+    rank, ws = world()
+    a, b = shard_range(lo, hi, rank, ws)
+    counts, probes = count_shard_device(p, K, a, b, device=dev)
+    c64 = widen_counts(torch, counts, K)
+    stats = torch.tensor([b - a, 0], dtype=torch.int64, device=dev)
+    stats[1:2].copy_(probes)
+    if ws > 1:
+        reduce_counts(c64)
+        gathered = [torch.zeros_like(stats) for _ in range(ws)]
+        import torch.distributed as dist
+
+        dist.all_gather(gathered, stats)
+        per = [(r, int(g[0].item()), int(g[1].item())) for r, g in enumerate(gathered)]
+    else:
+        per = [(0, b - a, int(probes.item()))]
+    out = c64[:K].cpu().numpy() if K else np.zeros(0, dtype=np.int64)
+    return out.astype(np.int64, copy=False), sum(pr for _, _, pr in per), per

@@ -1,0 +1,414 @@
+"""GPU parity: the CUDA path (through the C ABI, via the drop-in package)
+against the CPU oracle and the golden fixtures made by the reference.
+
+Bar: bit-exact edges, terminal chain values, probe totals and counts.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import GOLDEN_CRC_N10_D2, GOLDEN_SIMPLE_N10_D2, RING10, TRIANGLE
+
+pytestmark = pytest.mark.gpu
+
+pb = pytest.importorskip("paper_1602_07106_b200")
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def _hc(c):
+    kind, s0, s1, salt, mult = c
+    return pb.HashConfig(kind=pb.HashKind(kind), seed0=s0, seed1=s1, attempt_salt=salt, multiplier=mult)
+
+
+def _op(p: "pb.GenParams") -> O.OParams:
+    s0, s1 = p.hash.crc_seeds()
+    return O.OParams(n=p.n, d=p.d, n0=p.n0, seed_edges=tuple(int(x) for x in p.seed_edges),
+                     kind=O.KIND_CRC if p.hash.kind is pb.HashKind.CRC else O.KIND_SIMPLE,
+                     seed0=p.hash.seed0, seed1=p.hash.seed1, salt=p.hash.attempt_salt,
+                     multiplier=p.hash.multiplier)
+
+
+SEEDS = {"none": (None, 0), "triangle": (TRIANGLE, 3), "ring10": (RING10, 10)}
+
+
+# --------------------------------------------------------------------------- hashes / chains
+
+def test_hash_all_families_vs_reference_fixture(golden):
+    arrays, meta = golden
+    rs = arrays["hash_r"]
+    for k, c in enumerate(meta["cfgs"]):
+        got = pb.hash_many(rs, _hc(c))
+        assert np.array_equal(got, arrays[f"hash_out_{k}"]), c
+
+
+def test_hash_frozen_values_and_edges():
+    crc, simple = pb.HashConfig(), pb.HashConfig(kind=pb.HashKind.SIMPLE)
+    assert pb.h_crc(3, crc) == 2 and pb.h_crc(1000, crc) == 10 and pb.h_crc(10**6, crc) == 592013
+    assert pb.h_crc(1000, pb.HashConfig(seed0=7, seed1=9)) == 96
+    assert pb.h_simple(3, simple) == 1 and pb.h_simple(2**32, simple) == 2721204694
+    assert pb.h_crc(1, crc) == 0 and pb.h_simple(1, simple) == 0
+    with pytest.raises(pb.ParameterError):
+        pb.h_crc(0, crc)
+    with pytest.raises(pb.ParameterError):
+        pb.hash_value(0, simple)
+
+
+def test_hash_dense_small_r_vs_oracle():
+    # every r in [1, 70000) -- covers the exact slow path (r < 2^13) and the
+    # fp64-reciprocal fast path on both sides of the switch
+    rs = np.arange(1, 70000, dtype=np.uint64)
+    for cfg in (pb.HashConfig(), pb.HashConfig(seed0=7, seed1=9, attempt_salt=11)):
+        p = O.OParams(n=1, d=1, seed0=cfg.seed0, seed1=cfg.seed1, salt=cfg.attempt_salt)
+        assert np.array_equal(pb.hash_many(rs, cfg), O.hash_many(p, rs))
+
+
+def test_hash_random_wide_r_vs_oracle():
+    rng = np.random.default_rng(7)
+    for bits in (20, 32, 33, 41, 52, 53, 58, 63, 64):
+        rs = rng.integers(1, 2**bits - 1, size=20000, dtype=np.uint64, endpoint=True)
+        rs[:3] = [2**bits - 1, 2**(bits - 1), 2**(bits - 1) + 1]
+        p = O.OParams(n=1, d=1)
+        assert np.array_equal(pb.hash_many(rs, pb.HashConfig()), O.hash_many(p, rs)), bits
+
+
+def test_chains_vs_reference_fixture(golden):
+    arrays, meta = golden
+    r0 = arrays["chain_r0"]
+    for k, c in enumerate(meta["cfgs"]):
+        for stop in (0, 6, 1000):
+            vals, probes = pb.resolve_chain_block(r0, stop, _hc(c))
+            assert np.array_equal(vals, arrays[f"chain_out_{k}_{stop}"]), (c, stop)
+            assert probes == meta["chain_probes"][f"{k}_{stop}"]
+
+
+def test_resolve_chain_scalar_semantics():
+    crc, simple = pb.HashConfig(), pb.HashConfig(kind=pb.HashKind.SIMPLE)
+    assert pb.resolve_chain(1, 0, crc) == (0, None, 1)
+    assert pb.resolve_chain(11, 0, simple) == (4, None, 2)
+    assert pb.resolve_chain(1001, 0, crc) == (286, None, 1)
+    cr = pb.resolve_chain(100, 0, crc)  # even start is hashed (body runs at least once)
+    assert cr.probes >= 1 and cr.half_pos % 2 == 0
+    with pytest.raises(pb.ParameterError):
+        pb.resolve_chain(0, 0, crc)
+    rng = np.random.default_rng(21)
+    saw_seed = False
+    for r0 in rng.integers(8, 10_000, size=200):
+        cr = pb.resolve_chain(int(r0), 8, crc)
+        assert (cr.half_pos is None) != (cr.seed_pos is None)
+        saw_seed |= cr.seed_pos is not None
+    assert saw_seed
+
+
+def test_resolve_chain_block_does_not_mutate_and_empty():
+    r0 = np.array([5, 7, 9], dtype=np.uint64)
+    keep = r0.copy()
+    pb.resolve_chain_block(r0, 0, pb.HashConfig())
+    assert np.array_equal(r0, keep)
+    v, pr = pb.resolve_chain_block(np.empty(0, dtype=np.uint64), 0, pb.HashConfig())
+    assert v.size == 0 and pr == 0
+    with pytest.raises(pb.ParameterError):
+        pb.resolve_chain_block(np.array([0, 3], dtype=np.uint64), 0, pb.HashConfig())
+
+
+# --------------------------------------------------------------------------- store mode
+
+def test_golden_n10_d2():
+    for kind, want in ((pb.HashKind.SIMPLE, GOLDEN_SIMPLE_N10_D2), (pb.HashKind.CRC, GOLDEN_CRC_N10_D2)):
+        p = pb.GenParams(n=10, d=2, hash=pb.HashConfig(kind=kind))
+        blk, _ = pb.generate_block(0, p.m, p)
+        assert [tuple(map(int, r)) for r in blk] == want
+        assert [tuple(pb.generate_edge(i, p)) for i in range(20)] == want
+        assert [tuple(map(int, r)) for r in pb.edge_list(pb.bb_generate(p))] == want
+    assert pb.generate_edge(7, pb.GenParams(n=10, d=2, hash=pb.HashConfig(kind=pb.HashKind.SIMPLE))) == (3, 2)
+
+
+def test_72_combos_byte_identical(golden):
+    _, meta = golden
+    for c in meta["combos"]:
+        seed, n0 = SEEDS[c["seed"]]
+        p = pb.GenParams(n=c["n"], d=c["d"], n0=n0, seed_edges=seed,
+                         hash=pb.HashConfig(kind=pb.HashKind(c["kind"])))
+        got, probes = pb.generate_block(p.m0, p.m, p)
+        assert got.dtype == np.uint64 and got.shape == (p.m - p.m0, 2)
+        assert _sha(got) == c["sha256"], c
+        assert probes == c["probes"], c
+
+
+def test_config1_full_array(golden):
+    _, meta = golden
+    g = meta["config1"]
+    p = pb.GenParams(n=g["n"], d=g["d"])
+    got, probes = pb.generate_block(0, p.m, p)
+    assert _sha(got) == g["sha256"] and probes == g["probes"]
+    assert tuple(map(int, got[-1])) == tuple(g["last_edge"])
+    want, wp = O.generate_block(_op(p), 0, p.m)
+    assert np.array_equal(got, want) and probes == wp
+    e = pb.bb_generate(p)
+    assert np.array_equal(e.reshape(-1, 2), want)
+
+
+def test_partition_independence_and_probe_sums():
+    rng = np.random.default_rng(24)
+    for seed, n0 in ((None, 0), (RING10, 10)):
+        p = pb.GenParams(n=30000, d=3, n0=n0, seed_edges=seed)
+        whole, probes = pb.generate_block(p.m0, p.m, p)
+        cuts = sorted(rng.integers(p.m0, p.m, size=9).tolist())
+        bounds = [p.m0] + cuts + [p.m]
+        parts = [pb.generate_block(a, b, p) for a, b in zip(bounds, bounds[1:])]
+        assert np.array_equal(whole, np.concatenate([x for x, _ in parts]))
+        assert probes == sum(pr for _, pr in parts)
+
+
+def test_unaligned_subranges_vs_oracle():
+    rng = np.random.default_rng(5)
+    for n, d in ((10**8, 10), (10**9, 100), (10**10, 100), (2**40, 7), (2**55, 4)):
+        p = pb.GenParams(n=n, d=d)
+        for _ in range(3):
+            lo = int(rng.integers(0, p.m - 5000))
+            hi = lo + int(rng.integers(1, 5000))
+            got, pr = pb.generate_block(lo, hi, p)
+            want, wp = O.generate_block(_op(p), lo, hi)
+            assert np.array_equal(got, want) and pr == wp, (n, d, lo, hi)
+        got, pr = pb.generate_block(p.m - 3000, p.m, p)
+        want, wp = O.generate_block(_op(p), p.m - 3000, p.m)
+        assert np.array_equal(got, want) and pr == wp
+
+
+def test_sampled_ids_vs_reference_fixture(golden):
+    arrays, meta = golden
+    for name, s in meta["samples"].items():
+        p = pb.GenParams(n=s["n"], d=s["d"])
+        ids = arrays[f"sample_{name}_ids"]
+        e, probes = pb.edges_at(ids, p)
+        assert np.array_equal(e[:, 0], arrays[f"sample_{name}_src"])
+        assert np.array_equal(e[:, 1], arrays[f"sample_{name}_tgt"])
+        assert probes == int(arrays[f"sample_{name}_probes"].sum())
+
+
+def test_block_edge_cases():
+    p = pb.GenParams(n=10, d=2, n0=3, seed_edges=TRIANGLE)
+    arr, pr = pb.generate_block(5, 5, p)
+    assert arr.shape == (0, 2) and pr == 0
+    for lo, hi in ((0, 5), (5, 18), (9, 5)):
+        with pytest.raises(pb.ParameterError):
+            pb.generate_block(lo, hi, p)
+    with pytest.raises(pb.ParameterError):
+        pb.generate_edge(2, p)
+    with pytest.raises(pb.ParameterError):
+        pb.generate_edge(17, p)
+    flagged = pb.GenParams(n=10, d=2, n0=3, seed_edges=TRIANGLE, no_self_loops=True)
+    with pytest.raises(pb.ParameterError, match="generate_node_edges"):
+        pb.generate_edge(3, flagged)
+    with pytest.raises(pb.ParameterError):
+        pb.generate_block(3, 17, flagged)  # not on the B200 path, no CPU fallback
+    with pytest.raises(pb.ParameterError):
+        pb.run(pb.GenParams(n=10, d=2), pb.Consumer())
+
+
+def test_node_edges_and_source_law():
+    p = pb.GenParams(n=500, d=3, n0=3, seed_edges=TRIANGLE)
+    for v in (3, 10, 499):
+        first = p.first_edge_of(v)
+        assert pb.generate_node_edges(v, p) == [pb.generate_edge(i, p) for i in range(first, first + 3)]
+    blk, _ = pb.generate_block(p.m0, p.m, p)
+    idx = np.arange(p.m0, p.m, dtype=np.uint64)
+    assert np.array_equal(blk[:, 0], (idx - np.uint64(p.m0)) // np.uint64(p.d) + np.uint64(p.n0))
+    assert (blk[:, 1] <= blk[:, 0]).all()
+
+
+def test_store_device_api_and_run_collect():
+    import torch
+
+    p = pb.GenParams(n=4000, d=5, n0=3, seed_edges=TRIANGLE)
+    want, wp = O.generate_block(_op(p), p.m0, p.m)
+    out, probes = pb.generate_block_device(p.m0, p.m, p)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy().view(np.uint64), want) and int(probes.item()) == wp
+    got, stats = pb.run(p, pb.CollectConsumer(), workers=4, batch_size=64)
+    assert np.array_equal(got, want)
+    assert stats.edges_emitted == p.m - p.m0 and stats.hash_probes == wp
+    n, st = pb.run(p, pb.DiscardConsumer())
+    assert n == p.m - p.m0 and st.hash_probes == wp
+
+
+# --------------------------------------------------------------------------- degree counting
+
+def test_window_subranges_vs_reference_fixture(golden):
+    import torch
+
+    arrays, meta = golden
+    L = pb._lib.load()
+    for w in meta["windows"]:
+        p = pb.GenParams(n=w["n"], d=w["d"])
+        counts, probes = pb.parallel.count_shard_device(p, w["K"], w["lo"], w["hi"])
+        torch.cuda.synchronize()
+        c = counts.cpu().numpy()
+        assert _sha(c) == w["sha256"], w["name"]
+        assert int(probes.item()) == w["probes"]
+        assert int(c.sum()) == w["sum"]
+
+
+def test_degree_counts_vs_reference_fixture(golden):
+    arrays, meta = golden
+    for f in meta["full"]:
+        seed = np.array(f["seed"], dtype=np.uint64) if f["seed"] else None
+        p = pb.GenParams(n=f["n"], d=f["d"], n0=f["n0"], seed_edges=seed)
+        counter, stats = pb.degree_counts(p)
+        assert counter.counts.dtype == np.int64
+        assert _sha(counter.counts) == f["sha256"]
+        assert int(counter.counts.sum()) == 2 * p.m
+        assert stats.hash_probes == f["probes"] and stats.edges_emitted == p.m - p.m0
+        # truncated window == prefix of the full count (window kernel vs full kernel)
+        win, _ = pb.degree_counts(p, K=777)
+        assert np.array_equal(win.counts, counter.counts[:777])
+
+
+def test_degree_counts_config1(golden):
+    _, meta = golden
+    g = meta["config1"]
+    counter, _ = pb.degree_counts(pb.GenParams(n=g["n"], d=g["d"]))
+    assert _sha(counter.counts) == g["counts_sha256"]
+    assert counter.counts[:5].tolist() == g["deg0_4"] and int(counter.counts.max()) == g["degree_max"]
+
+
+def test_full_histogram_n1e6_d16_vs_oracle():
+    # config-4 shape at desk scale: exact element-wise counts
+    p = pb.GenParams(n=10**6, d=16)
+    counter, stats = pb.degree_counts(p)
+    blk, wp = O.run_threaded(_op(p), 0, p.m, O.MODE_STORE, threads=os.cpu_count() or 1, batch=1 << 18)
+    want = np.bincount(blk.astype(np.int64).ravel(), minlength=p.n)
+    assert np.array_equal(counter.counts, want) and stats.hash_probes == wp
+    h = pb.Histogram.from_degree_counts(counter)
+    assert 2.6 <= pb.fit_exponent(h, xmin=16) <= 3.4
+
+
+def test_window_large_range_sharding_independent():
+    # C3 shape: n=1e9, d=100, K=1e5 over the first 1e9 edge IDs; any split of
+    # the range into shards sums to the same histogram
+    import torch
+
+    p = pb.GenParams(n=10**9, d=100)
+    lo, hi, K = 0, 10**9, 10**5
+    whole, pr = pb.parallel.count_shard_device(p, K, lo, hi)
+    for G in (2, 3, 8):
+        acc = torch.zeros_like(whole)
+        prs = torch.zeros_like(pr)
+        for g in range(G):
+            a, b = pb.parallel.shard_range(lo, hi, g, G)
+            pb.parallel.count_shard_device(p, K, a, b, counts=acc, probes=prs)
+        torch.cuda.synchronize()
+        assert torch.equal(acc, whole) and int(prs.item()) == int(pr.item())
+    # sources of edges < K*d = 1e7 all land in the window: K*d each
+    c = whole.cpu().numpy()
+    assert (c >= 100).all()  # every node < K owns its d = 100 edges in [0, 1e9)
+    assert 1.9 <= int(pr.item()) / (hi - lo) <= 2.1
+
+
+def test_probe_cost_per_edge():
+    # acceptance (3): mean probes/edge in [1.8, 2.2]
+    for kind in (pb.HashKind.CRC, pb.HashKind.SIMPLE):
+        p = pb.GenParams(n=600_000, d=2, hash=pb.HashConfig(kind=kind))
+        _, probes = pb.generate_block(10**5, 10**5 + 10**6, p)
+        assert 1.8 <= probes / 10**6 <= 2.2
+
+
+def test_expected_degree_law_billion_edges():
+    # acceptance (6): n=1e7, d=100, K=1e4, SIMPLE, 1e9 edges
+    n, d, K = 10**7, 100, 10**4
+    p = pb.GenParams(n=n, d=d, hash=pb.HashConfig(kind=pb.HashKind.SIMPLE))
+    counter, stats = pb.degree_counts(p, K=K)
+    ratios = pb.expected_degree_check(counter, n=n, d=d, bins=12, lo=10, hi=K)
+    assert len(ratios) >= 10 and all(0.8 <= r.ratio <= 1.2 for r in ratios)
+    assert stats.edges_emitted == 10**9
+
+
+def test_degree_conservation_randomized():
+    rng = np.random.default_rng(90)
+    for case in range(20):
+        n0 = int(rng.integers(0, 6))
+        seed = None
+        if n0 >= 2:
+            flat = list(RING10[:0])
+            for i in range(n0):
+                flat += (i, (i + 1) % n0)
+            for _ in range(int(rng.integers(0, 5))):
+                flat += (int(rng.integers(n0)), int(rng.integers(n0)))
+            seed = np.array(flat, dtype=np.uint64)
+        else:
+            n0 = 0
+        kind = pb.HashKind.CRC if rng.random() < 0.5 else pb.HashKind.SIMPLE
+        p = pb.GenParams(n=int(rng.integers(n0 + 1, 4000)), d=int(rng.integers(1, 9)), n0=n0,
+                         seed_edges=seed, hash=pb.HashConfig(kind=kind))
+        counter, _ = pb.degree_counts(p)
+        assert int(counter.counts.sum()) == 2 * p.m
+        want = np.zeros(p.n, dtype=np.int64)
+        blk, _ = O.generate_block(_op(p), p.m0, p.m)
+        O.count_block(want, blk)
+        if p.m0:
+            O.count_block(want, p.seed_edges.reshape(-1, 2))
+        assert np.array_equal(counter.counts, want)
+
+
+# --------------------------------------------------------------------------- full BASELINE sizes
+
+def test_config2_full_size_properties():
+    """C2 (n=1e8, d=10, m=1e9; 16 GB in HBM): closed-form sources over the
+    whole array, target <= source, 2e5 sampled rows bit-exact vs the oracle,
+    probe mean, and the device histogram of the stored targets equals the
+    fused full-count kernel (a checksum of two independent kernels)."""
+    import torch
+
+    p = pb.GenParams(n=10**8, d=10)
+    out, probes = pb.generate_block_device(0, p.m, p)
+    torch.cuda.synchronize()
+    step = 1 << 27
+    for a in range(0, p.m, step):
+        b = min(a + step, p.m)
+        src = out[a:b, 0]
+        idx = torch.arange(a, b, dtype=torch.int64, device=out.device)
+        assert torch.equal(src, idx // p.d)
+        assert bool((out[a:b, 1] <= src).all())
+    rng = np.random.default_rng(160207106)
+    ids = np.unique(rng.integers(0, p.m, size=200_000, dtype=np.uint64))
+    rows = out[torch.from_numpy(ids.view(np.int64)).to(out.device)].cpu().numpy().view(np.uint64)
+    r0 = np.uint64(2) * ids + np.uint64(1)
+    term, _ = O.resolve_chain_block(_op(p), r0, 0)
+    assert np.array_equal(rows[:, 0], ids // np.uint64(10))
+    assert np.array_equal(rows[:, 1], (term >> np.uint64(1)) // np.uint64(10))
+    assert 1.95 <= int(probes.item()) / p.m <= 2.05
+    tgt_hist = torch.bincount(out[:, 1], minlength=p.n)
+    del out
+    counts, pr2 = pb.parallel.count_shard_device(p, p.n, 0, p.m)
+    torch.cuda.synchronize()
+    c64 = pb.parallel.widen_counts(torch, counts, p.n)
+    assert int(pr2.item()) == int(probes.item())
+    assert torch.equal(c64 - p.d, tgt_hist)  # every node is the source of exactly d edges
+    assert int(c64.sum().item()) == 2 * p.m
+
+
+def test_config4_full_histogram_properties():
+    """C4 (n=1e8, d=16, m=1.6e9, uint32 counts): sum = 2m, min degree d,
+    power-law exponent in range, and the counts of a node subrange equal the
+    window kernel's."""
+    import torch
+
+    p = pb.GenParams(n=10**8, d=16)
+    counts, probes = pb.parallel.count_shard_device(p, p.n, 0, p.m)
+    c64 = pb.parallel.widen_counts(torch, counts, p.n)
+    assert int(c64.sum().item()) == 2 * p.m
+    assert int(c64.min().item()) >= p.d
+    win, _ = pb.parallel.count_shard_device(p, 100_000, 0, p.m)
+    torch.cuda.synchronize()
+    assert torch.equal(win[:100_000], c64[:100_000])
+    vals, cnt = torch.unique(c64, return_counts=True)
+    h = pb.Histogram(degrees=vals.cpu().numpy(), counts=cnt.cpu().numpy())
+    assert 2.6 <= pb.fit_exponent(h, xmin=32) <= 3.4

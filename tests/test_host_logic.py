@@ -1,0 +1,136 @@
+"""Host-side logic of the drop-in package (CPU only): configuration objects,
+validation and error behaviour mirror the reference (hashing.py:48-85,
+generator.py:50-136, driver.py:131-158)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_1602_07106_b200 as pb
+from conftest import TRIANGLE, ring_edges
+
+
+def test_hash_config_validation_and_folding():
+    for kw in ({"seed0": -1}, {"seed1": 2**64}, {"kind": pb.HashKind.SIMPLE, "multiplier": 2**64}):
+        with pytest.raises(pb.ParameterError):
+            pb.HashConfig(**kw)
+    with pytest.raises(pb.ParameterError):
+        pb.HashConfig().with_attempt(-1)
+    cfg = pb.HashConfig(seed0=10, seed1=20)
+    assert cfg.crc_seeds() == (10, 20)
+    assert cfg.with_attempt(3).crc_seeds() == (13, (20 + 3 * 0x9E3779B9) & 0xFFFFFFFF)
+    assert pb.HashConfig(seed0=2**40 + 5).crc_seeds()[0] == 5  # seeds are 32-bit
+    mults = {pb.HashConfig(kind=pb.HashKind.SIMPLE).with_attempt(a).simple_multiplier() for a in range(12)}
+    assert len(mults) == 12 and all(m & 1 == pb.DEFAULT_MULTIPLIER & 1 for m in mults)
+
+
+def test_genparams_validation():
+    bad = [dict(n=10), dict(n=10, d=2, degrees=np.ones(10, dtype=np.uint64)), dict(n=5, d=0),
+           dict(n=5, d=2, n0=6), dict(n=5, d=2, n0=-1),
+           dict(n=5, d=2, n0=1, seed_edges=np.array([0, 1, 2], dtype=np.uint64)),
+           dict(n=5, d=2, n0=1, seed_edges=np.array([0, 1], dtype=np.uint64)),
+           dict(n=5, d=2, max_attempts=0), dict(n=2**58, d=1),
+           dict(n=5, n0=1, degrees=np.array([2, 2], dtype=np.uint64)),
+           dict(n=5, d=2, no_self_loops=True), dict(n=5, d=2, no_parallel_edges=True)]
+    for kw in bad:
+        with pytest.raises(pb.ParameterError):
+            pb.GenParams(**kw)
+
+
+def test_genparams_derived():
+    p = pb.GenParams(n=10, d=2)
+    assert (p.m0, p.m, pb.edge_count(p)) == (0, 20, 20)
+    p = pb.GenParams(n=10, d=2, n0=3, seed_edges=TRIANGLE)
+    assert (p.m0, p.m) == (3, 17) and p.degree_of(5) == 2
+    assert p.first_edge_of(3) == 3 and p.first_edge_of(4) == 5
+    for v in (2, 10):
+        with pytest.raises(pb.ParameterError):
+            p.degree_of(v)
+    src = np.array([0, 1], dtype=np.int32)
+    q = pb.GenParams(n=5, d=1, n0=2, seed_edges=src)
+    src[0] = 99
+    assert q.seed_edges.dtype == np.uint64 and q.seed_edges.tolist() == [0, 1]
+    assert pb.GenParams(n=10**10, d=100).m == 10**12
+
+
+def test_plan_batches_reference_cases():
+    p = pb.GenParams(n=30, d=2)
+    assert pb.plan_batches(p, 30) == [pb.Batch(0, 30), pb.Batch(30, 60)]
+    assert pb.plan_batches(p, 25) == [pb.Batch(0, 25), pb.Batch(25, 50), pb.Batch(50, 60)]
+    u = pb.GenParams(n=40, d=3, n0=3, seed_edges=TRIANGLE)
+    assert pb.plan_batches(u, 1000) == [pb.Batch(3, 114)]
+    q = pb.GenParams(n=30, d=4, n0=3, seed_edges=TRIANGLE)
+    got = pb.plan_batches(q, 30, granularity=pb.Granularity.NODE)
+    assert got[0] == pb.Batch(3, 31, pb.Granularity.NODE)
+    with pytest.raises(pb.ParameterError):
+        pb.plan_batches(u, 0)
+    rng = np.random.default_rng(40)
+    for _ in range(20):
+        n0 = int(rng.integers(0, 4))
+        seed = ring_edges(n0) if n0 else None
+        p = pb.GenParams(n=int(rng.integers(n0 + 1, 80)), d=int(rng.integers(1, 6)), n0=n0, seed_edges=seed)
+        pos = p.m0
+        for b in pb.plan_batches(p, int(rng.integers(1, 40))):
+            assert b.lo == pos and b.hi > b.lo
+            pos = b.hi
+        assert pos == p.m
+
+
+def test_shard_range_exact_cover():
+    rng = np.random.default_rng(3)
+    for _ in range(200):
+        lo = int(rng.integers(0, 10**12))
+        hi = lo + int(rng.integers(0, 10**6))
+        G = int(rng.integers(1, 9))
+        pos = lo
+        for g in range(G):
+            a, b = pb.parallel.shard_range(lo, hi, g, G)
+            assert a == pos and b >= a
+            pos = b
+        assert pos == hi
+    assert pb.parallel.shard_range(0, 10**12, 7, 8) == (875 * 10**9, 10**12)
+    with pytest.raises(pb.ParameterError):
+        pb.parallel.shard_range(0, 10, 2, 2)
+
+
+def test_run_validation():
+    p = pb.GenParams(n=10, d=2)
+    with pytest.raises(pb.ParameterError):
+        pb.run(p, pb.DiscardConsumer(), workers=0)
+    with pytest.raises(pb.ParameterError):
+        pb.run(p, pb.DiscardConsumer(), batch_size=0)
+    with pytest.raises(pb.ParameterError):
+        pb.DegreeCountConsumer(-1)
+    with pytest.raises(pb.ParameterError):
+        pb.DegreeCounter.zeros(-1)
+
+
+def test_count_edge_and_merge_semantics():
+    c = pb.DegreeCounter.zeros(4)
+    pb.count_edge(c, pb.Edge(0, 3))
+    pb.count_edge(c, pb.Edge(3, 1))
+    pb.count_edge(c, pb.Edge(1, 9))
+    assert c.counts.tolist() == [1, 2, 0, 2]
+    d = pb.DegreeCounter.zeros(2)
+    pb.count_edge(d, pb.Edge(1, 1))
+    assert d.counts.tolist() == [0, 2]
+    a = pb.DegreeCounter(3, np.array([1, 0, 2], dtype=np.int64))
+    b = pb.DegreeCounter(3, np.array([0, 5, 1], dtype=np.int64))
+    assert pb.merge(a, b).counts.tolist() == [1, 5, 3]
+    with pytest.raises(pb.ParameterError):
+        pb.merge(a, pb.DegreeCounter.zeros(4))
+
+
+def test_histogram_and_fit_on_synthetic_counts():
+    rng = np.random.default_rng(11)
+    gamma = 3.0
+    # discrete power-law sample via inverse transform of the continuous law
+    x = np.floor((16 - 0.5) * (1 - rng.random(200_000)) ** (-1 / (gamma - 1)) + 0.5).astype(np.int64)
+    h = pb.Histogram.from_degree_counts(pb.DegreeCounter(x.size, x))
+    assert h.total_nodes == x.size and h.degree_sum == int(x.sum())
+    assert abs(pb.fit_exponent(h, xmin=16) - gamma) < 0.05
+    with pytest.raises(pb.ParameterError):
+        pb.fit_exponent(h, xmin=0)
+    with pytest.raises(pb.ParameterError):
+        pb.fit_exponent(pb.Histogram(np.array([5]), np.array([10])), xmin=5)
