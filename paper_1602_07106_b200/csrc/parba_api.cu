@@ -74,31 +74,33 @@ DevParams make_dev(const parba_params_t *p, uint64_t K = 0) {
     d.k0 = crc32c_u64_bitwise(p->crc_seed0, 0);
     d.k1 = crc32c_u64_bitwise(p->crc_seed1, 0);
     d.seed = p->seed_edges;
-    d.divd = make_magic(p->d);
+    d.div64 = make_magic64(p->d);
+    d.div32 = make_magic32(p->d);
     d.K = K;
-    // generated target ((r>>1) - m0)/d + n0 < K  <=>  (r>>1) < m0 + (K - n0) * d
+    // generated target ((r>>1) - m0)/d + n0 < K  <=>  r < 2*(m0 + (K - n0)*d)
     if (K <= p->n0) {
-        d.win_lim = 0;
+        d.win_rlim = 0;
     } else {
-        const unsigned __int128 lim = (unsigned __int128)p->m0 + (unsigned __int128)(K - p->n0) * p->d;
-        d.win_lim = lim > (unsigned __int128)UINT64_MAX ? UINT64_MAX : (uint64_t)lim;
+        const unsigned __int128 lim = 2 * ((unsigned __int128)p->m0 + (unsigned __int128)(K - p->n0) * p->d);
+        d.win_rlim = lim > (unsigned __int128)UINT64_MAX ? UINT64_MAX : (uint64_t)lim;
     }
     return d;
 }
 
 int bits_of(uint64_t x) { return x ? 64 - __builtin_clzll(x) : 0; }
 
-// CRC table chunks needed to cover every r in a launch.
-int nch_for(uint64_t max_r) {
-    const int b = bits_of(max_r);
-    if (b <= 35) return 7;
-    if (b <= 45) return 9;
-    return 13;
+// Byte tables needed to cover every chain value of a launch (r < 2*hi).
+int nb_for(uint64_t two_hi) {
+    const int b = bits_of(two_hi);
+    if (b <= 32) return 4;
+    if (b <= 40) return 5;
+    if (b <= 48) return 6;
+    return 8;
 }
 
 struct DevInfo {
     int sms = 0;
-    bool attr_done[2][3][3] = {};
+    bool attr_done[8][3][2] = {};
 };
 std::mutex g_mu;
 std::vector<DevInfo> g_dev;
@@ -113,21 +115,21 @@ int dev_info(DevInfo **out) {
     return PARBA_OK;
 }
 
-template <class Hash, int NCH, int SINK>
-int launch_tiles_t(const DevParams &dp, uint64_t lo, uint64_t hi, const StoreArgs &a,
-                   unsigned long long *probes, cudaStream_t st, int hk, int nk) {
+template <class Hash, int SINK, bool SEED>
+int launch_tiles_t(const DevParams &dp, uint64_t lo, uint64_t hi, const SinkArgs &a,
+                   unsigned long long *probes, cudaStream_t st, int variant) {
     if (hi <= lo) return PARBA_OK;
     DevInfo *di;
     int rc = dev_info(&di);
     if (rc) return rc;
-    auto kern = tile_kernel<Hash, NCH, SINK>;
-    const size_t smem = tile_smem_bytes<SINK>();
+    auto kern = tile_kernel<Hash, SINK, SEED>;
+    const size_t smem = tile_smem_bytes<Hash, SINK>();
     int per_sm = 0;
     {
         std::lock_guard<std::mutex> lk(g_mu);
-        if (!di->attr_done[hk][nk][SINK]) {
+        if (!di->attr_done[variant][SINK][SEED]) {
             CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            di->attr_done[hk][nk][SINK] = true;
+            di->attr_done[variant][SINK][SEED] = true;
         }
     }
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
@@ -142,15 +144,26 @@ int launch_tiles_t(const DevParams &dp, uint64_t lo, uint64_t hi, const StoreArg
     return PARBA_OK;
 }
 
+template <class Hash, int SINK>
+int launch_tiles_s(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi,
+                   const SinkArgs &a, unsigned long long *probes, cudaStream_t st, int variant) {
+    if (p->m0 > 0 || p->n0 > 0) return launch_tiles_t<Hash, SINK, true>(dp, lo, hi, a, probes, st, variant);
+    return launch_tiles_t<Hash, SINK, false>(dp, lo, hi, a, probes, st, variant);
+}
+
 template <int SINK>
 int launch_tiles(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi,
-                 const StoreArgs &a, unsigned long long *probes, cudaStream_t st) {
-    if (p->hash_kind == PARBA_HASH_SIMPLE)
-        return launch_tiles_t<HashSimple, 0, SINK>(dp, lo, hi, a, probes, st, 1, 0);
-    switch (nch_for(2 * hi)) {
-        case 7: return launch_tiles_t<HashCrc<7>, 7, SINK>(dp, lo, hi, a, probes, st, 0, 0);
-        case 9: return launch_tiles_t<HashCrc<9>, 9, SINK>(dp, lo, hi, a, probes, st, 0, 1);
-        default: return launch_tiles_t<HashCrc<13>, 13, SINK>(dp, lo, hi, a, probes, st, 0, 2);
+                 const SinkArgs &a, unsigned long long *probes, cudaStream_t st) {
+    const int nb = nb_for(2 * hi);
+    if (p->hash_kind == PARBA_HASH_SIMPLE) {
+        if (nb == 4) return launch_tiles_s<HashSimple<true>, SINK>(p, dp, lo, hi, a, probes, st, 4);
+        return launch_tiles_s<HashSimple<false>, SINK>(p, dp, lo, hi, a, probes, st, 5);
+    }
+    switch (nb) {
+        case 4: return launch_tiles_s<HashCrc<4>, SINK>(p, dp, lo, hi, a, probes, st, 0);
+        case 5: return launch_tiles_s<HashCrc<5>, SINK>(p, dp, lo, hi, a, probes, st, 1);
+        case 6: return launch_tiles_s<HashCrc<6>, SINK>(p, dp, lo, hi, a, probes, st, 2);
+        default: return launch_tiles_s<HashCrc<8>, SINK>(p, dp, lo, hi, a, probes, st, 3);
     }
 }
 
@@ -160,11 +173,11 @@ unsigned grid_for(uint64_t count, int threads) {
     return (unsigned)(g ? g : 1);
 }
 
-template <class Hash, int NCH>
+template <class Hash>
 int launch_chains_t(const DevParams &dp, const uint64_t *r0, uint64_t count, uint64_t stop,
                     uint64_t *out, const uint64_t *ids, uint64_t *pairs, unsigned long long *probes,
                     cudaStream_t st) {
-    chains_kernel<Hash, NCH><<<grid_for(count, 256), 256, 0, st>>>(dp, r0, count, stop, out, ids, pairs, probes);
+    chains_kernel<Hash><<<grid_for(count, 256), 256, 0, st>>>(dp, r0, count, stop, out, ids, pairs, probes);
     CUDA_TRY(cudaGetLastError());
     return PARBA_OK;
 }
@@ -174,8 +187,8 @@ int launch_chains(const parba_params_t *p, const DevParams &dp, const uint64_t *
                   unsigned long long *probes, cudaStream_t st) {
     if (count == 0) return PARBA_OK;
     if (p->hash_kind == PARBA_HASH_SIMPLE)
-        return launch_chains_t<HashSimple, 0>(dp, r0, count, stop, out, ids, pairs, probes, st);
-    return launch_chains_t<HashCrc<13>, 13>(dp, r0, count, stop, out, ids, pairs, probes, st);
+        return launch_chains_t<HashSimple<false>>(dp, r0, count, stop, out, ids, pairs, probes, st);
+    return launch_chains_t<HashCrc<8>>(dp, r0, count, stop, out, ids, pairs, probes, st);
 }
 
 template <typename CountT>
@@ -216,9 +229,9 @@ int parba_hash(const parba_params_t *p, const uint64_t *r, uint64_t count, uint6
     const DevParams dp = make_dev(p);
     cudaStream_t st = (cudaStream_t)stream;
     if (p->hash_kind == PARBA_HASH_SIMPLE)
-        hash_kernel<HashSimple, 0><<<grid_for(count, 256), 256, 0, st>>>(dp, r, count, out);
+        hash_kernel<HashSimple<false>><<<grid_for(count, 256), 256, 0, st>>>(dp, r, count, out);
     else
-        hash_kernel<HashCrc<13>, 13><<<grid_for(count, 256), 256, 0, st>>>(dp, r, count, out);
+        hash_kernel<HashCrc<8>><<<grid_for(count, 256), 256, 0, st>>>(dp, r, count, out);
     CUDA_TRY(cudaGetLastError());
     return PARBA_OK;
 }
@@ -242,7 +255,7 @@ int parba_generate(const parba_params_t *p, uint64_t lo, uint64_t hi, uint64_t *
     if (hi == lo) return PARBA_OK;
     if (!out_pairs) return fail(PARBA_EINVAL, "out_pairs is NULL");
     if (((uintptr_t)out_pairs) & 15) return fail(PARBA_EINVAL, "out_pairs must be 16-byte aligned");
-    StoreArgs a{out_pairs, nullptr, nullptr};
+    SinkArgs a{out_pairs, nullptr, nullptr};
     return launch_tiles<kStore>(p, make_dev(p), lo, hi, a, probes, (cudaStream_t)stream);
 }
 
@@ -266,7 +279,7 @@ int parba_degree_window(const parba_params_t *p, uint64_t lo, uint64_t hi, uint6
     if (K > 0 && !counts) return fail(PARBA_EINVAL, "counts is NULL");
     cudaStream_t st = (cudaStream_t)stream;
     const DevParams dp = make_dev(p, K);
-    StoreArgs a{nullptr, counts, nullptr};
+    SinkArgs a{nullptr, counts, nullptr};
     rc = launch_tiles<kWindow>(p, dp, lo, hi, a, probes, st);
     if (rc) return rc;
     return launch_sources<unsigned long long>(dp, lo, hi, K, counts, st);
@@ -281,7 +294,7 @@ int parba_degree_full(const parba_params_t *p, uint64_t lo, uint64_t hi, uint32_
     if (!counts) return fail(PARBA_EINVAL, "counts is NULL");
     cudaStream_t st = (cudaStream_t)stream;
     const DevParams dp = make_dev(p, p->n);
-    StoreArgs a{nullptr, nullptr, counts};
+    SinkArgs a{nullptr, nullptr, counts};
     rc = launch_tiles<kFull>(p, dp, lo, hi, a, probes, st);
     if (rc) return rc;
     return launch_sources<uint32_t>(dp, lo, hi, p->n, counts, st);

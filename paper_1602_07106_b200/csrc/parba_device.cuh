@@ -1,31 +1,32 @@
 // parba_device.cuh -- device-side building blocks of the B200 hot path.
 //
-//   crc0(w)       CRC32-C of one 64-bit word with zero seed, from 5-bit chunk
-//                 tables in shared memory (32 entries per table = exactly the
-//                 32 smem banks, so every lookup is bank-conflict free).
+//   crc0<NB>(w)   CRC32-C of one 64-bit word with zero seed, w < 2^(8*NB):
+//                 slicing tables tab[k][b] = crc(0, b << 8k) in shared memory,
+//                 one lookup per significant byte (4 for 2m <= 2^32, 5 for the
+//                 paper-scale 1e11-edge graph).  Byte extraction is one PRMT
+//                 (ALU pipe) and the scaled address one IMAD (FMA pipe).
 //   h_crc(r)      the reference hash ((crc(s0,r)<<32) + crc(s1,r)) % r
 //                 (hashing.py:119-125, _kernels.py:32-42) rewritten through
 //                 CRC linearity: crc(s,w) = crc(s,0) ^ crc(0,w), so one table
-//                 CRC per probe instead of two.
-//   mod_u64(h,r)  exact h % r via an fp64 reciprocal estimate (the FP64 pipe
-//                 is otherwise idle) and one integer correction; a rare slow
-//                 path (r < 2^13 or a failed correction) uses the exact
-//                 integer remainder.
+//                 CRC per probe instead of the reference's two.
+//   mod_fp(h,r)   exact h % r for r < 2^52, computed on the FP64 pipe (64
+//                 lanes/SM/clk on B200, otherwise idle), which keeps the ALU
+//                 and FMA pipes free for the CRC and the chain bookkeeping.
+//   mod_int(h,r)  exact h % r for any 64-bit r (generic kernels).
 //   h_simple(r)   umulhi((r*M) mod 2^64, r)  (hashing.py:128-138).
-//   MagicDiv      division by the launch-constant d (source/target closed
-//                 forms, generator.py:157-169) by multiply-high.
+//   Magic32/64    division by the launch-constant d (closed forms for
+//                 source/target, generator.py:157-169) by multiply-high.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace parba {
 
 constexpr uint32_t kCrcPoly = 0x82F63B78u;  // hashing.py:40 (reflected 0x1EDC6F41)
-constexpr int kChunkBits = 5;
-constexpr int kMaxChunks = 13;              // ceil(64 / 5)
 
-// Bit-serial CRC32-C of one LE 64-bit word (host + device); used only to
-// build tables and constants.
+// Bit-serial CRC32-C of one LE 64-bit word (host + device); builds tables
+// and the seed constants only.
 __host__ __device__ inline uint32_t crc32c_u64_bitwise(uint32_t seed, uint64_t word) {
     uint32_t c = seed;
     for (int b = 0; b < 64; ++b) {
@@ -35,18 +36,25 @@ __host__ __device__ inline uint32_t crc32c_u64_bitwise(uint32_t seed, uint64_t w
     return c;
 }
 
-// Branch-free unsigned 64-bit division by a runtime-invariant d >= 1
-// (Granlund-Montgomery round-up variant).
-struct MagicDiv {
+// ---------------------------------------------------------------------------
+// Division by a runtime-invariant d >= 1.
+//   Magic64: Granlund-Montgomery round-up form for any 64-bit n:
+//            t = mulhi(mul, n);  q = (t + ((n - t) >> sh1)) >> sh2
+//   Magic32: n < 2^32, d < 2^32: q = mulhi64(n, M) with M = floor(2^64/d)+1
+//            (error n*(M - 2^64/d)/2^64 < 2^-32 <= 1/d, so the floor is
+//            exact): two IMAD.WIDE on the FMA pipe, no shifts.
+struct Magic64 {
     uint64_t mul;
     uint32_t sh1, sh2;
 };
+struct Magic32 {
+    uint64_t mul;
+};
 
-inline MagicDiv make_magic(uint64_t d) {
-    MagicDiv m{};
+inline Magic64 make_magic64(uint64_t d) {
+    Magic64 m{};
     int l = 0;
     while (l < 64 && (1ull << l) < d) ++l;  // l = ceil(log2 d)
-    // mul = floor(2^64 * (2^l - d) / d) + 1
     unsigned __int128 num = ((unsigned __int128)1 << 64) * (((unsigned __int128)1 << l) - d);
     m.mul = (uint64_t)(num / d) + 1;
     m.sh1 = l > 0 ? 1u : 0u;
@@ -54,9 +62,21 @@ inline MagicDiv make_magic(uint64_t d) {
     return m;
 }
 
-__device__ __forceinline__ uint64_t magic_div(uint64_t n, const MagicDiv &m) {
+inline Magic32 make_magic32(uint64_t d) {
+    Magic32 m{};
+    if (d < 2 || d >= (1ull << 32)) return m;  // d == 1 handled by the caller's template
+    m.mul = (uint64_t)((((unsigned __int128)1) << 64) / d) + 1;
+    return m;
+}
+
+__device__ __forceinline__ uint64_t magic_div(uint64_t n, const Magic64 &m) {
     uint64_t t = __umul64hi(m.mul, n);
     return (t + ((n - t) >> m.sh1)) >> m.sh2;
+}
+// n < 2^32; d >= 2 (mul != 0) or d == 1 (mul == 0: quotient is n)
+__device__ __forceinline__ uint32_t magic_div32(uint32_t n, const Magic32 &m) {
+    if (m.mul == 0) return n;
+    return (uint32_t)__umul64hi((uint64_t)n, m.mul);
 }
 
 // Launch-constant description of one graph family (plain uniform-d mode).
@@ -66,96 +86,148 @@ struct DevParams {
     uint64_t mult;         // SIMPLE multiplier
     uint32_t k0, k1;       // crc(s0,0), crc(s1,0)
     const uint64_t *seed;  // 2*m0 seed endpoints (device)
-    MagicDiv divd;
-    uint64_t win_lim;      // window mode: generated target < K  <=>  (r>>1) < win_lim
+    Magic64 div64;         // by d (wide)
+    Magic32 div32;         // by d (narrow: positions < 2^32)
+    uint64_t win_rlim;     // window mode: generated target < K  <=>  r < win_rlim
     uint64_t K;
 };
 
 // Closed forms (generator.py:157-169): source of edge i, target of terminal r.
+template <bool NARROW, bool SEED>
 __device__ __forceinline__ uint64_t source_of(uint64_t i, const DevParams &p) {
-    return magic_div(i - p.m0, p.divd) + p.n0;
+    if constexpr (NARROW) {
+        if constexpr (SEED) return (uint64_t)magic_div32((uint32_t)(i - p.m0), p.div32) + p.n0;
+        else return (uint64_t)magic_div32((uint32_t)i, p.div32);
+    } else {
+        if constexpr (SEED) return magic_div(i - p.m0, p.div64) + p.n0;
+        else return magic_div(i, p.div64);
+    }
 }
+template <bool NARROW, bool SEED>
 __device__ __forceinline__ uint64_t target_of(uint64_t r, const DevParams &p) {
-    if (r < p.stop) return __ldg(p.seed + r);
-    return magic_div((r >> 1) - p.m0, p.divd) + p.n0;
+    if constexpr (SEED) {
+        if (r < p.stop) return __ldg(p.seed + r);
+    }
+    return source_of<NARROW, SEED>(r >> 1, p);
 }
 
 // ---------------------------------------------------------------------------
-// Exact 64-bit remainder.
+// Exact remainder.
 
-__device__ __forceinline__ double u64_to_f64_exact52(uint64_t x) {  // x < 2^52
+__device__ __forceinline__ double u32_to_f64(uint32_t x) {
+    return __hiloint2double(0x43300000, (int)x) - 0x1p52;
+}
+__device__ __forceinline__ double u52_to_f64(uint64_t x) {  // x < 2^52
     return __longlong_as_double((long long)(x | 0x4330000000000000ull)) - 0x1p52;
 }
 
-// h = hi:lo (two u32 halves) -> nearest double (one rounding).
+// hi:lo -> nearest double (one rounding).
 __device__ __forceinline__ double u64_halves_to_f64(uint32_t hi, uint32_t lo) {
     double dh = __hiloint2double(0x45300000, (int)hi);  // 2^84 + hi*2^32
     double dl = __hiloint2double(0x43300000, (int)lo);  // 2^52 + lo
     return (dh - 0x1.00000001p84) + dl;                  // 2^84 + 2^52 exactly
 }
 
-template <bool kWide>
-__device__ __forceinline__ uint64_t mod_u64(uint32_t hhi, uint32_t hlo, uint64_t r) {
-    const uint64_t h = ((uint64_t)hhi << 32) | hlo;
-    if (r < (1ull << 13)) return h % r;  // q would exceed 2^51: exact slow path (rare)
-    double rd = kWide ? __ull2double_rn(r) : u64_to_f64_exact52(r);
+// y ~ 1/rd: rcp.approx.ftz.f64 (max relative error 2^-19.9 measured on
+// B200 by tools/micro) plus one Newton step: relative error < 2^-39.
+__device__ __forceinline__ double recip_approx(double rd) {
     double y;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(rd));
-    double e = fma(-rd, y, 1.0);
-    y = fma(y, e, y);
-    e = fma(-rd, y, 1.0);
-    y = fma(y, e, y);
-    double qd = u64_halves_to_f64(hhi, hlo) * y;   // ~ h / r, |err| < 2 for r >= 2^13
-    uint64_t q = (uint64_t)__double_as_longlong(qd + 0x1p52) & 0x000FFFFFFFFFFFFFull;
-    uint64_t t = h - q * r;                        // exact h mod r up to +-r
-    if ((int64_t)t < 0) t += r;
-    else if (t >= r) t -= r;
-    if (t >= r) t = h % r;                         // estimate off by > 1: exact fallback
-    return t;
+    const double e = fma(-rd, y, 1.0);
+    return fma(y, e, y);
+}
+
+// h % r for 1 <= r < 2^52, h = hhi:hlo, entirely in fp64.
+//   A: qa = round(hhi*y) is floor(hhi/r) or +1 (hhi/r < 2^32, error < 2^-7);
+//      x = fma(-qa, r, hhi) is EXACT (the true value lies in [-r, r), which
+//      a double holds exactly since r < 2^52) -- no correction needed yet.
+//   B: v = x*2^32 + hlo (|v| < r*2^32); qb = round(v*y) is floor(v/r) or +1;
+//      t = fma(-qb, r, x*2^32) + hlo is again exact, t in [-r, r);
+//      one "if negative add r" gives h % r (= v % r, since v = h - qa*r*2^32).
+// The 1.5*2^52 offset rounds q to an integer for |q| < 2^51 of either sign.
+__device__ __forceinline__ uint64_t mod_fp(uint32_t hhi, uint32_t hlo, double rd) {
+    const double y = recip_approx(rd);
+    const double ha = u32_to_f64(hhi);
+    const double hl = u32_to_f64(hlo);
+    const double qa = fma(ha, y, 0x1.8p52) - 0x1.8p52;
+    const double x = fma(-qa, rd, ha);
+    const double qb = fma(fma(x, 0x1p32, hl), y, 0x1.8p52) - 0x1.8p52;
+    double t = fma(-qb, rd, x * 0x1p32) + hl;
+    t = (t < 0.0) ? t + rd : t;
+    return (uint64_t)__double_as_longlong(t + 0x1p52) & 0x000FFFFFFFFFFFFFull;
+}
+
+// h % r for any 1 <= r < 2^64 (generic kernels; integer corrections).
+__device__ __forceinline__ uint64_t mod_int(uint32_t hhi, uint32_t hlo, uint64_t r) {
+    const uint64_t h = ((uint64_t)hhi << 32) | hlo;
+    if (r > (1ull << 63)) return h >= r ? h - r : h;   // h < 2^64 < 2r
+    const double rd = u64_halves_to_f64((uint32_t)(r >> 32), (uint32_t)r);
+    const double y = recip_approx(rd);
+    const uint32_t qa = (uint32_t)__double2loint(fma(u32_to_f64(hhi), y, 0x1p52));
+    int64_t x = (int64_t)((uint64_t)hhi - (uint64_t)qa * r);
+    x += (x < 0) ? (int64_t)r : 0;                     // x = hhi mod r < 2^32
+    const uint64_t v = ((uint64_t)x << 32) | hlo;      // < r * 2^32, no overflow
+    const uint32_t qb = (uint32_t)__double2loint(fma(u64_halves_to_f64((uint32_t)x, hlo), y, 0x1p52));
+    int64_t t = (int64_t)(v - (uint64_t)qb * r);       // in [-r, r): fits for r <= 2^63
+    t += (t < 0) ? (int64_t)r : 0;
+    return (uint64_t)t;
 }
 
 // ---------------------------------------------------------------------------
-// Shared-memory CRC tables: tab[k][x] = crc(0, x << 5k).
+// Byte-sliced CRC tables in shared memory: tab[k][b] = crc(0, b << 8k).
 
+template <int NB>
 struct CrcTables {
-    uint32_t t[kMaxChunks][32];
+    uint32_t t[NB][256];
 };
 
-__device__ __forceinline__ void build_crc_tables(CrcTables &s) {
-    for (int e = threadIdx.x; e < kMaxChunks * 32; e += blockDim.x) {
-        int k = e >> 5, x = e & 31;
-        s.t[k][x] = crc32c_u64_bitwise(0u, (uint64_t)x << (kChunkBits * k));
+template <int NB>
+__device__ __forceinline__ void build_crc_tables(CrcTables<NB> &s) {
+    for (int e = threadIdx.x; e < NB * 256; e += blockDim.x) {
+        const int k = e >> 8, b = e & 255;
+        s.t[k][b] = crc32c_u64_bitwise(0u, (uint64_t)b << (8 * k));
     }
 }
 
-// crc(0, w) for w < 2^(5*NCH).
-template <int NCH>
-__device__ __forceinline__ uint32_t crc0(const CrcTables &s, uint64_t w) {
+template <int NB>
+__device__ __forceinline__ uint32_t crc0(const CrcTables<NB> &s, uint64_t w) {
+    const uint32_t lo = (uint32_t)w, hi = (uint32_t)(w >> 32);
     uint32_t c = 0;
 #pragma unroll
-    for (int k = 0; k < NCH; ++k) c ^= s.t[k][(uint32_t)(w >> (kChunkBits * k)) & 31u];
+    for (int k = 0; k < NB; ++k) {
+        const uint32_t b = __byte_perm(k < 4 ? lo : hi, 0u, 0x4440u | (k & 3));
+        c ^= s.t[k][b];
+    }
     return c;
 }
 
 // ---------------------------------------------------------------------------
-// Hash policies.  probe(r) = h(r); first(...) = h(2i+1) given crc(0,2i+1).
+// Hash policies.  R is the chain-value type (u32 when every position < 2^32).
 
-template <int NCH>
+template <int NB>
 struct HashCrc {
-    static constexpr bool kWide = (NCH * kChunkBits) > 52;
     static constexpr bool kHasCrc = true;
-    __device__ __forceinline__ static uint64_t from_crc(uint32_t c, uint64_t r, const DevParams &p) {
-        return mod_u64<kWide>(c ^ p.k0, c ^ p.k1, r);
+    static constexpr bool kNarrow = NB <= 4;
+    static constexpr int kTables = NB;
+    using R = typename std::conditional<kNarrow, uint32_t, uint64_t>::type;
+    __device__ __forceinline__ static R from_crc(uint32_t c, R r, const DevParams &p) {
+        if constexpr (kNarrow) return (R)mod_fp(c ^ p.k0, c ^ p.k1, u32_to_f64(r));
+        else if constexpr (NB * 8 <= 52) return mod_fp(c ^ p.k0, c ^ p.k1, u52_to_f64(r));
+        else return mod_int(c ^ p.k0, c ^ p.k1, r);
     }
-    __device__ __forceinline__ static uint64_t probe(const CrcTables &s, uint64_t r, const DevParams &p) {
-        return from_crc(crc0<NCH>(s, r), r, p);
+    __device__ __forceinline__ static R probe(const CrcTables<NB> &s, R r, const DevParams &p) {
+        return from_crc(crc0<NB>(s, r), r, p);
     }
 };
 
+template <bool NARROW>
 struct HashSimple {
     static constexpr bool kHasCrc = false;
-    __device__ __forceinline__ static uint64_t probe(const CrcTables &, uint64_t r, const DevParams &p) {
-        return __umul64hi(r * p.mult, r);
+    static constexpr bool kNarrow = NARROW;
+    static constexpr int kTables = 1;
+    using R = typename std::conditional<NARROW, uint32_t, uint64_t>::type;
+    __device__ __forceinline__ static R probe(const CrcTables<1> &, R r, const DevParams &p) {
+        return (R)__umul64hi((uint64_t)r * p.mult, (uint64_t)r);
     }
 };
 

@@ -22,8 +22,11 @@
 //            increments its target's counter directly (E never stored).
 //
 // Persistent grid: one resident wave of CTAs, warps stride over tiles.
+// Template axes: Hash (CRC with NB table bytes / SIMPLE; narrow = every chain
+// value < 2^32), SINK, SEED (m0 > 0 or n0 > 0: offsets and the seed stop).
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "parba_device.cuh"
@@ -36,94 +39,106 @@ constexpr int kWarps = 8;                  // warps per CTA
 constexpr int kThreads = kWarps * 32;
 
 enum SinkKind { kStore = 0, kWindow = 1, kFull = 2 };
-constexpr int kTabBytes = (sizeof(CrcTables) + 15) / 16 * 16;
 
-struct StoreArgs {
-    uint64_t *out;                         // 2*(hi-lo) u64, 16-byte aligned
+struct SinkArgs {
+    uint64_t *out;                         // store: 2*(hi-lo) u64, 16-byte aligned
     unsigned long long *win;               // window counts (K)
     uint32_t *full;                        // full counts (n)
 };
 
-template <int SINK>
-struct WarpSmem;
-
-template <>
-struct WarpSmem<kStore> {
-    uint64_t stage[2][kTile];  // targets of the two tiles in flight
-    uint64_t qr[kTile];        // pending chain values
-    uint16_t qs[kTile];        // pending slots: buf*kTile + j
+// Per-warp shared state.  R = chain value type (u32 in narrow mode).
+template <int SINK, class R>
+struct WarpSmem {
+    R qr[kTile];               // pending chain values (ring)
+    uint16_t qs[kTile];        // pending slots: buf*kTile + j   (store only)
+    R stage[2][kTile];         // targets of the two tiles in flight (store only)
 };
-template <>
-struct WarpSmem<kWindow> {
-    uint64_t qr[kTile];
+template <class R>
+struct WarpSmem<kWindow, R> {
+    R qr[kTile];
 };
-template <>
-struct WarpSmem<kFull> {
-    uint64_t qr[kTile];
+template <class R>
+struct WarpSmem<kFull, R> {
+    R qr[kTile];
 };
 
-template <int SINK>
-constexpr size_t tile_smem_bytes() { return kTabBytes + kWarps * sizeof(WarpSmem<SINK>); }
+template <class Hash, int SINK>
+constexpr size_t tile_smem_bytes() {
+    return kWarps * sizeof(WarpSmem<SINK, typename Hash::R>);
+}
 
-template <int SINK>
-__device__ __forceinline__ void finish(WarpSmem<SINK> &w, uint32_t slot, uint64_t r,
-                                       const DevParams &p, const StoreArgs &a) {
+// A chain finished with terminal value r: hand its target to the sink.
+template <bool NARROW, bool SEED, int SINK, class W>
+__device__ __forceinline__ void finish(W &w, uint32_t slot, uint64_t r, const DevParams &p,
+                                       const SinkArgs &a) {
     if constexpr (SINK == kStore) {
-        (&w.stage[0][0])[slot] = target_of(r, p);  // slot spans both ring buffers
+        using RS = std::remove_reference_t<decltype(w.stage[0][0])>;
+        (&w.stage[0][0])[slot] = (RS)target_of<NARROW, SEED>(r, p);
     } else if constexpr (SINK == kWindow) {
-        // target < K  <=>  (r>>1) < win_lim for generated positions
-        if (r >= p.stop) {
-            if ((r >> 1) < p.win_lim) atomicAdd(a.win + target_of(r, p), 1ull);
-        } else {
-            uint64_t t = __ldg(p.seed + r);
+        if (SEED && r < p.stop) {
+            const uint64_t t = __ldg(p.seed + r);
             if (t < p.K) atomicAdd(a.win + t, 1ull);
+        } else if (r < p.win_rlim) {  // generated target < K  <=>  r < win_rlim
+            atomicAdd(a.win + source_of<NARROW, SEED>(r >> 1, p), 1ull);
         }
     } else {
-        atomicAdd(a.full + target_of(r, p), 1u);
+        atomicAdd(a.full + target_of<NARROW, SEED>(r, p), 1u);
     }
 }
 
-template <class Hash, int NCH, int SINK>
-__global__ void __launch_bounds__(kThreads, 3)
+template <class Hash, int SINK, bool SEED>
+__global__ void __launch_bounds__(kThreads, 4)
 tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntiles,
-            StoreArgs a, unsigned long long *probes_out) {
+            SinkArgs a, unsigned long long *probes_out) {
+    using R = typename Hash::R;
+    constexpr bool NARROW = Hash::kNarrow;
+    constexpr int NB = Hash::kTables;
+    __shared__ CrcTables<NB> tabs;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    CrcTables &tabs = *reinterpret_cast<CrcTables *>(smem_raw);
-    WarpSmem<SINK> *wsm = reinterpret_cast<WarpSmem<SINK> *>(smem_raw + kTabBytes);
-    build_crc_tables(tabs);
+    WarpSmem<SINK, R> *wsm = reinterpret_cast<WarpSmem<SINK, R> *>(smem_raw);
+    if constexpr (Hash::kHasCrc) build_crc_tables<NB>(tabs);
     __syncthreads();
 
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
-    WarpSmem<SINK> &w = wsm[wib];
+    WarpSmem<SINK, R> &w = wsm[wib];
     const unsigned ltmask = lanemask_lt();
     const uint64_t gw = (uint64_t)blockIdx.x * kWarps + wib;
     const uint64_t nw = (uint64_t)gridDim.x * kWarps;
 
     // crc(0, 2j+1) for this lane's phase-1 edges j = lane + 32k (2j+1 < 512).
     uint32_t clow[kEpl];
+    if constexpr (Hash::kHasCrc) {
 #pragma unroll
-    for (int k = 0; k < kEpl; ++k) clow[k] = crc0<2>(tabs, 2u * (lane + 32u * k) + 1u);
+        for (int k = 0; k < kEpl; ++k)
+            clow[k] = crc0<2>(*reinterpret_cast<const CrcTables<2> *>(&tabs), 2u * (lane + 32u * k) + 1u);
+    }
 
-    bool act = false;        // lane holds a running chain
-    uint64_t r = 0;
+    int act = 0;                  // lane holds a running chain
+    R r = 0;
     uint32_t slot = 0;
     uint32_t head = 0, tail = 0;  // queue cursors (warp-uniform)
-    unsigned long long probes = 0;
+    uint32_t probes = 0;          // per lane (< 2^32 per launch and lane)
     uint64_t prev_base = 0;
     bool have_prev = false;
     uint32_t buf = 0;
+
+    auto is_done = [&](R v) -> bool {
+        if constexpr (SEED) return ((uint32_t)v & 1u) == 0 || (uint64_t)v < p.stop;
+        else return ((uint32_t)v & 1u) == 0;
+    };
 
     // Write a finished tile out of buffer b (store mode).
     auto flush = [&](uint32_t b, uint64_t base) {
         if constexpr (SINK == kStore) {
             __syncwarp();
+            const bool full_tile = base >= lo && base + kTile <= hi;
 #pragma unroll
             for (int k = 0; k < kEpl; ++k) {
                 const uint32_t j = lane + 32u * k;
                 const uint64_t i = base + j;
-                if (i >= lo && i < hi) {
-                    ulonglong2 v = make_ulonglong2(source_of(i, p), w.stage[b][j]);
+                if (full_tile || (i >= lo && i < hi)) {
+                    ulonglong2 v = make_ulonglong2(source_of<NARROW, SEED>(i, p), (uint64_t)w.stage[b][j]);
                     __stcs(reinterpret_cast<ulonglong2 *>(a.out + 2 * (i - lo)), v);
                 }
             }
@@ -136,32 +151,30 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
         if (act) {
             r = Hash::probe(tabs, r, p);
             ++probes;
-            if (r < p.stop || (r & 1ull) == 0) {
-                finish<SINK>(w, slot, r, p, a);
-                act = false;
+            if (is_done(r)) {
+                finish<NARROW, SEED, SINK>(w, slot, (uint64_t)r, p, a);
+                act = 0;
             }
         }
     };
 
     for (uint64_t t = gw; t < ntiles; t += nw) {
         const uint64_t base = (tile0 + t) * kTile;
+        const bool full_tile = base >= lo && base + kTile <= hi;
         // ---- phase 1: first probe of all edges of the tile
         uint32_t cb = 0;
-        if constexpr (Hash::kHasCrc) cb = crc0<NCH>(tabs, 2 * base);
+        if constexpr (Hash::kHasCrc) cb = crc0<NB>(tabs, 2 * base);
 #pragma unroll
         for (int k = 0; k < kEpl; ++k) {
             const uint32_t j = lane + 32u * k;
             const uint64_t i = base + j;
-            const bool valid = (i >= lo) && (i < hi);
-            const uint64_t r0 = 2 * i + 1;
-            uint64_t r1;
+            const bool valid = full_tile || ((i >= lo) && (i < hi));
+            const R r0 = (R)(2 * i + 1);
+            R r1;
             if constexpr (Hash::kHasCrc) r1 = Hash::from_crc(cb ^ clow[k], r0, p);
             else r1 = Hash::probe(tabs, r0, p);
-            const bool done = (r1 < p.stop) || ((r1 & 1ull) == 0);
-            if (valid) {
-                ++probes;
-                if (done) finish<SINK>(w, buf * kTile + j, r1, p, a);
-            }
+            const bool done = is_done(r1);
+            if (valid && done) finish<NARROW, SEED, SINK>(w, buf * kTile + j, (uint64_t)r1, p, a);
             const bool pend = valid && !done;
             const unsigned m = __ballot_sync(0xffffffffu, pend);
             if (pend) {
@@ -170,23 +183,21 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
                 if constexpr (SINK == kStore) w.qs[pos] = (uint16_t)(buf * kTile + j);
             }
             tail += __popc(m);
+            probes += valid ? 1u : 0u;
         }
         __syncwarp();
         // ---- phase 2: drain the queue with lane refill
         while (tail != head) {
             const unsigned idle = __ballot_sync(0xffffffffu, !act);
             const uint32_t avail = tail - head;
-            if (!act) {
-                const uint32_t rank = __popc(idle & ltmask);
-                if (rank < avail) {
-                    const uint32_t pos = (head + rank) & (kTile - 1);
-                    r = w.qr[pos];
-                    if constexpr (SINK == kStore) slot = w.qs[pos];
-                    act = true;
-                }
+            const uint32_t rank = __popc(idle & ltmask);
+            if (!act && rank < avail) {
+                const uint32_t pos = (head + rank) & (kTile - 1);
+                r = w.qr[pos];
+                if constexpr (SINK == kStore) slot = w.qs[pos];
+                act = 1;
             }
-            const uint32_t took = min((uint32_t)__popc(idle), avail);
-            head += took;
+            head += min((uint32_t)__popc(idle), avail);
             step();
         }
         // ---- store: flush the previous tile once none of its chains runs
@@ -208,22 +219,24 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
     }
     // ---- probes: warp reduce, one atomic per warp
     if (probes_out) {
+        unsigned long long pr = probes;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) probes += __shfl_xor_sync(0xffffffffu, probes, o);
-        if (lane == 0) atomicAdd(probes_out, probes);
+        for (int o = 16; o > 0; o >>= 1) pr += __shfl_xor_sync(0xffffffffu, pr, o);
+        if (lane == 0) atomicAdd(probes_out, pr);
     }
 }
 
 // ---------------------------------------------------------------------------
-// Generic kernels (not the bench path): arbitrary chain starts / ID lists.
+// Generic kernels (not the bench path): arbitrary chain starts / ID lists,
+// full 64-bit values.
 
-template <class Hash, int NCH>
+template <class Hash>
 __global__ void __launch_bounds__(256)
 chains_kernel(DevParams p, const uint64_t *__restrict__ r0, uint64_t count, uint64_t stop,
               uint64_t *__restrict__ out, const uint64_t *__restrict__ ids,
               uint64_t *__restrict__ pairs, unsigned long long *probes_out) {
-    __shared__ CrcTables tabs;
-    build_crc_tables(tabs);
+    __shared__ CrcTables<Hash::kTables> tabs;
+    if constexpr (Hash::kHasCrc) build_crc_tables<Hash::kTables>(tabs);
     __syncthreads();
     unsigned long long probes = 0;
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count;
@@ -234,7 +247,8 @@ chains_kernel(DevParams p, const uint64_t *__restrict__ r0, uint64_t count, uint
             ++probes;
         } while (!(r < stop || (r & 1ull) == 0));
         if (ids) {
-            reinterpret_cast<ulonglong2 *>(pairs)[k] = make_ulonglong2(source_of(ids[k], p), target_of(r, p));
+            reinterpret_cast<ulonglong2 *>(pairs)[k] =
+                make_ulonglong2(source_of<false, true>(ids[k], p), target_of<false, true>(r, p));
         } else {
             out[k] = r;
         }
@@ -245,11 +259,11 @@ chains_kernel(DevParams p, const uint64_t *__restrict__ r0, uint64_t count, uint
     }
 }
 
-template <class Hash, int NCH>
+template <class Hash>
 __global__ void __launch_bounds__(256)
 hash_kernel(DevParams p, const uint64_t *__restrict__ r, uint64_t count, uint64_t *__restrict__ out) {
-    __shared__ CrcTables tabs;
-    build_crc_tables(tabs);
+    __shared__ CrcTables<Hash::kTables> tabs;
+    if constexpr (Hash::kHasCrc) build_crc_tables<Hash::kTables>(tabs);
     __syncthreads();
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count;
          k += (uint64_t)gridDim.x * blockDim.x)
@@ -268,10 +282,6 @@ __global__ void source_counts_kernel(DevParams p, uint64_t lo, uint64_t hi, uint
         if (y > x) counts[v] += (CountT)(y - x);
     }
 }
-
-}  // namespace parba
-
-namespace parba {
 
 // count_block on device (analytics.py:44-48): counts[id] += 1 for id < K.
 __global__ void count_ids_kernel(const uint64_t *__restrict__ ids, uint64_t count, uint64_t K,
