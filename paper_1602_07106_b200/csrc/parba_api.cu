@@ -72,7 +72,7 @@ DevParams make_dev(const parba_params_t *p, uint64_t K = 0) {
     d.mult = p->simple_mult;
     // CRC linearity: crc(s, w) = crc(s, 0) ^ crc(0, w)
     d.k0 = crc32c_u64_bitwise(p->crc_seed0, 0);
-    d.k1 = crc32c_u64_bitwise(p->crc_seed1, 0);
+    d.k01 = d.k0 ^ crc32c_u64_bitwise(p->crc_seed1, 0);
     d.seed = p->seed_edges;
     d.div64 = make_magic64(p->d);
     d.div32 = make_magic32(p->d);
@@ -84,6 +84,8 @@ DevParams make_dev(const parba_params_t *p, uint64_t K = 0) {
         const unsigned __int128 lim = 2 * ((unsigned __int128)p->m0 + (unsigned __int128)(K - p->n0) * p->d);
         d.win_rlim = lim > (unsigned __int128)UINT64_MAX ? UINT64_MAX : (uint64_t)lim;
     }
+    // narrow launches hold r < 2^32; 2^32-1 is odd, so never a terminal value
+    d.win_rlim32 = d.win_rlim > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)d.win_rlim;
     return d;
 }
 

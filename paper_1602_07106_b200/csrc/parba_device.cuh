@@ -84,11 +84,12 @@ struct DevParams {
     uint64_t n, d, n0, m0, m;
     uint64_t stop;         // 2*m0: chains stop when r < stop (seed region)
     uint64_t mult;         // SIMPLE multiplier
-    uint32_t k0, k1;       // crc(s0,0), crc(s1,0)
+    uint32_t k0, k01;      // crc(s0,0) and crc(s0,0)^crc(s1,0): h = (c0<<32)|(c0^k01)
     const uint64_t *seed;  // 2*m0 seed endpoints (device)
     Magic64 div64;         // by d (wide)
     Magic32 div32;         // by d (narrow: positions < 2^32)
     uint64_t win_rlim;     // window mode: generated target < K  <=>  r < win_rlim
+    uint32_t win_rlim32;   // min(win_rlim, 2^32 - 1) for narrow launches
     uint64_t K;
 };
 
@@ -145,7 +146,8 @@ __device__ __forceinline__ double recip_approx(double rd) {
 //      t = fma(-qb, r, x*2^32) + hlo is again exact, t in [-r, r);
 //      one "if negative add r" gives h % r (= v % r, since v = h - qa*r*2^32).
 // The 1.5*2^52 offset rounds q to an integer for |q| < 2^51 of either sign.
-__device__ __forceinline__ uint64_t mod_fp(uint32_t hhi, uint32_t hlo, double rd) {
+template <class R>
+__device__ __forceinline__ R mod_fp(uint32_t hhi, uint32_t hlo, double rd) {
     const double y = recip_approx(rd);
     const double ha = u32_to_f64(hhi);
     const double hl = u32_to_f64(hlo);
@@ -154,7 +156,14 @@ __device__ __forceinline__ uint64_t mod_fp(uint32_t hhi, uint32_t hlo, double rd
     const double qb = fma(fma(x, 0x1p32, hl), y, 0x1.8p52) - 0x1.8p52;
     double t = fma(-qb, rd, x * 0x1p32) + hl;
     t = (t < 0.0) ? t + rd : t;
-    return (uint64_t)__double_as_longlong(t + 0x1p52) & 0x000FFFFFFFFFFFFFull;
+    const double tt = t + 0x1p52;  // t < 2^52: the mantissa holds t exactly
+    const uint32_t lo = (uint32_t)__double2loint(tt);
+    if constexpr (sizeof(R) == 4) {
+        return lo;
+    } else {
+        const uint32_t hi = (uint32_t)__double2hiint(tt) & 0x000FFFFFu;
+        return ((uint64_t)hi << 32) | lo;
+    }
 }
 
 // h % r for any 1 <= r < 2^64 (generic kernels; integer corrections).
@@ -181,11 +190,13 @@ struct CrcTables {
     uint32_t t[NB][256];
 };
 
+// Table 0 carries k0 = crc(s0, 0): every crc0() XORs exactly one table-0
+// entry, so crc0() returns crc(s0, w) directly (CRC linearity).
 template <int NB>
-__device__ __forceinline__ void build_crc_tables(CrcTables<NB> &s) {
+__device__ __forceinline__ void build_crc_tables(CrcTables<NB> &s, uint32_t k0) {
     for (int e = threadIdx.x; e < NB * 256; e += blockDim.x) {
         const int k = e >> 8, b = e & 255;
-        s.t[k][b] = crc32c_u64_bitwise(0u, (uint64_t)b << (8 * k));
+        s.t[k][b] = crc32c_u64_bitwise(0u, (uint64_t)b << (8 * k)) ^ (k == 0 ? k0 : 0u);
     }
 }
 
@@ -210,10 +221,11 @@ struct HashCrc {
     static constexpr bool kNarrow = NB <= 4;
     static constexpr int kTables = NB;
     using R = typename std::conditional<kNarrow, uint32_t, uint64_t>::type;
-    __device__ __forceinline__ static R from_crc(uint32_t c, R r, const DevParams &p) {
-        if constexpr (kNarrow) return (R)mod_fp(c ^ p.k0, c ^ p.k1, u32_to_f64(r));
-        else if constexpr (NB * 8 <= 52) return mod_fp(c ^ p.k0, c ^ p.k1, u52_to_f64(r));
-        else return mod_int(c ^ p.k0, c ^ p.k1, r);
+    // c0 = crc(s0, r) (k0 already folded into table 0); crc(s1, r) = c0 ^ k01.
+    __device__ __forceinline__ static R from_crc(uint32_t c0, R r, const DevParams &p) {
+        if constexpr (kNarrow) return mod_fp<R>(c0, c0 ^ p.k01, u32_to_f64(r));
+        else if constexpr (NB * 8 <= 52) return mod_fp<R>(c0, c0 ^ p.k01, u52_to_f64(r));
+        else return mod_int(c0, c0 ^ p.k01, r);
     }
     __device__ __forceinline__ static R probe(const CrcTables<NB> &s, R r, const DevParams &p) {
         return from_crc(crc0<NB>(s, r), r, p);

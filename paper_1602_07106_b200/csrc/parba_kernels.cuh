@@ -9,8 +9,9 @@
 //   phase 1  every lane takes the first probe of 8 edges of a 256-edge,
 //            256-aligned warp tile.  r0 = 2i+1 = 2B + (2j+1), so by CRC
 //            linearity crc(0,r0) = crc(0,2B) ^ crc(0,2j+1): a warp-uniform
-//            value per tile XOR a per-lane register constant -- the first
-//            probe (half of all probes) needs no table lookup.  About half
+//            value per tile XOR a constant read from a 1 KB smem table
+//            (conflict-free, lane-consecutive) -- the first probe (half of
+//            all probes) needs one lookup instead of NB.  About half
 //            the edges finish here; the rest go to a per-warp smem queue.
 //   phase 2  lanes pop queued chains (ballot/popc refill) and probe until
 //            the queue is empty; chains still running stay in registers and
@@ -78,7 +79,8 @@ __device__ __forceinline__ void finish(W &w, uint32_t slot, uint64_t r, const De
         if (SEED && r < p.stop) {
             const uint64_t t = __ldg(p.seed + r);
             if (t < p.K) atomicAdd(a.win + t, 1ull);
-        } else if (r < p.win_rlim) {  // generated target < K  <=>  r < win_rlim
+        } else if (NARROW ? ((uint32_t)r < p.win_rlim32) : (r < p.win_rlim)) {
+            // generated target < K  <=>  r < win_rlim
             atomicAdd(a.win + source_of<NARROW, SEED>(r >> 1, p), 1ull);
         }
     } else {
@@ -87,16 +89,21 @@ __device__ __forceinline__ void finish(W &w, uint32_t slot, uint64_t r, const De
 }
 
 template <class Hash, int SINK, bool SEED>
-__global__ void __launch_bounds__(kThreads, 4)
+__global__ void __launch_bounds__(kThreads, SINK == kStore ? 5 : 6)
 tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntiles,
             SinkArgs a, unsigned long long *probes_out) {
     using R = typename Hash::R;
     constexpr bool NARROW = Hash::kNarrow;
     constexpr int NB = Hash::kTables;
     __shared__ CrcTables<NB> tabs;
+    __shared__ uint32_t clow_s[kTile];  // crc(0, 2j+1) for j < kTile (2j+1 < 512)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     WarpSmem<SINK, R> *wsm = reinterpret_cast<WarpSmem<SINK, R> *>(smem_raw);
-    if constexpr (Hash::kHasCrc) build_crc_tables<NB>(tabs);
+    if constexpr (Hash::kHasCrc) {
+        build_crc_tables<NB>(tabs, p.k0);
+        for (int j = threadIdx.x; j < kTile; j += blockDim.x)
+            clow_s[j] = crc32c_u64_bitwise(0u, 2u * (uint32_t)j + 1u);
+    }
     __syncthreads();
 
     const int lane = threadIdx.x & 31;
@@ -105,14 +112,6 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
     const unsigned ltmask = lanemask_lt();
     const uint64_t gw = (uint64_t)blockIdx.x * kWarps + wib;
     const uint64_t nw = (uint64_t)gridDim.x * kWarps;
-
-    // crc(0, 2j+1) for this lane's phase-1 edges j = lane + 32k (2j+1 < 512).
-    uint32_t clow[kEpl];
-    if constexpr (Hash::kHasCrc) {
-#pragma unroll
-        for (int k = 0; k < kEpl; ++k)
-            clow[k] = crc0<2>(*reinterpret_cast<const CrcTables<2> *>(&tabs), 2u * (lane + 32u * k) + 1u);
-    }
 
     int act = 0;                  // lane holds a running chain
     R r = 0;
@@ -146,16 +145,16 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
         }
     };
 
-    // One probe on every active lane; finished chains go to the sink.
+    // One probe on every lane (idle lanes hash a harmless stale value and
+    // discard it: no divergent branch around the probe); finished chains go
+    // to the sink.
     auto step = [&]() {
-        if (act) {
-            r = Hash::probe(tabs, r, p);
-            ++probes;
-            if (is_done(r)) {
-                finish<NARROW, SEED, SINK>(w, slot, (uint64_t)r, p, a);
-                act = 0;
-            }
-        }
+        const R nr = Hash::probe(tabs, r, p);
+        probes += (uint32_t)act;
+        const bool fin = act && is_done(nr);
+        r = nr;
+        if (fin) finish<NARROW, SEED, SINK>(w, slot, (uint64_t)nr, p, a);
+        act = act && !fin;
     };
 
     for (uint64_t t = gw; t < ntiles; t += nw) {
@@ -171,7 +170,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
             const bool valid = full_tile || ((i >= lo) && (i < hi));
             const R r0 = (R)(2 * i + 1);
             R r1;
-            if constexpr (Hash::kHasCrc) r1 = Hash::from_crc(cb ^ clow[k], r0, p);
+            if constexpr (Hash::kHasCrc) r1 = Hash::from_crc(cb ^ clow_s[j], r0, p);
             else r1 = Hash::probe(tabs, r0, p);
             const bool done = is_done(r1);
             if (valid && done) finish<NARROW, SEED, SINK>(w, buf * kTile + j, (uint64_t)r1, p, a);
@@ -236,7 +235,7 @@ chains_kernel(DevParams p, const uint64_t *__restrict__ r0, uint64_t count, uint
               uint64_t *__restrict__ out, const uint64_t *__restrict__ ids,
               uint64_t *__restrict__ pairs, unsigned long long *probes_out) {
     __shared__ CrcTables<Hash::kTables> tabs;
-    if constexpr (Hash::kHasCrc) build_crc_tables<Hash::kTables>(tabs);
+    if constexpr (Hash::kHasCrc) build_crc_tables<Hash::kTables>(tabs, p.k0);
     __syncthreads();
     unsigned long long probes = 0;
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count;
@@ -263,7 +262,7 @@ template <class Hash>
 __global__ void __launch_bounds__(256)
 hash_kernel(DevParams p, const uint64_t *__restrict__ r, uint64_t count, uint64_t *__restrict__ out) {
     __shared__ CrcTables<Hash::kTables> tabs;
-    if constexpr (Hash::kHasCrc) build_crc_tables<Hash::kTables>(tabs);
+    if constexpr (Hash::kHasCrc) build_crc_tables<Hash::kTables>(tabs, p.k0);
     __syncthreads();
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count;
          k += (uint64_t)gridDim.x * blockDim.x)
