@@ -156,7 +156,8 @@ int launch_tiles_s(const parba_params_t *p, const DevParams &dp, uint64_t lo, ui
 template <int SINK>
 int launch_tiles(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi,
                  const SinkArgs &a, unsigned long long *probes, cudaStream_t st) {
-    const int nb = nb_for(2 * hi);
+    int nb = nb_for(2 * hi);
+    if (nb == 4 && p->d >= (1ull << 31)) nb = 5;  // narrow closed forms need d < 2^31
     if (p->hash_kind == PARBA_HASH_SIMPLE) {
         if (nb == 4) return launch_tiles_s<HashSimple<true>, SINK>(p, dp, lo, hi, a, probes, st, 4);
         return launch_tiles_s<HashSimple<false>, SINK>(p, dp, lo, hi, a, probes, st, 5);

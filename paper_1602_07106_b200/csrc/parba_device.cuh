@@ -40,15 +40,16 @@ __host__ __device__ inline uint32_t crc32c_u64_bitwise(uint32_t seed, uint64_t w
 // Division by a runtime-invariant d >= 1.
 //   Magic64: Granlund-Montgomery round-up form for any 64-bit n:
 //            t = mulhi(mul, n);  q = (t + ((n - t) >> sh1)) >> sh2
-//   Magic32: n < 2^32, d < 2^32: q = mulhi64(n, M) with M = floor(2^64/d)+1
-//            (error n*(M - 2^64/d)/2^64 < 2^-32 <= 1/d, so the floor is
-//            exact): two IMAD.WIDE on the FMA pipe, no shifts.
+//   Magic32: n < 2^31 (every narrow position), d < 2^31: with
+//            l = ceil(log2 d), m = floor(2^(31+l)/d) + 1 < 2^32,
+//            q = (n*m) >> (31+l) exactly (Granlund-Montgomery, N = 31):
+//            one IMAD.WIDE.U32 and one funnel shift.
 struct Magic64 {
     uint64_t mul;
     uint32_t sh1, sh2;
 };
 struct Magic32 {
-    uint64_t mul;
+    uint32_t mul, shift;
 };
 
 inline Magic64 make_magic64(uint64_t d) {
@@ -64,8 +65,11 @@ inline Magic64 make_magic64(uint64_t d) {
 
 inline Magic32 make_magic32(uint64_t d) {
     Magic32 m{};
-    if (d < 2 || d >= (1ull << 32)) return m;  // d == 1 handled by the caller's template
-    m.mul = (uint64_t)((((unsigned __int128)1) << 64) / d) + 1;
+    if (d < 1 || d >= (1ull << 31)) return m;  // narrow launches need d < 2^31
+    int l = 0;
+    while ((1ull << l) < d) ++l;
+    m.mul = (uint32_t)((1ull << (31 + l)) / d + 1);
+    m.shift = (uint32_t)(31 + l);
     return m;
 }
 
@@ -73,10 +77,9 @@ __device__ __forceinline__ uint64_t magic_div(uint64_t n, const Magic64 &m) {
     uint64_t t = __umul64hi(m.mul, n);
     return (t + ((n - t) >> m.sh1)) >> m.sh2;
 }
-// n < 2^32; d >= 2 (mul != 0) or d == 1 (mul == 0: quotient is n)
+// n < 2^31
 __device__ __forceinline__ uint32_t magic_div32(uint32_t n, const Magic32 &m) {
-    if (m.mul == 0) return n;
-    return (uint32_t)__umul64hi((uint64_t)n, m.mul);
+    return (uint32_t)(((uint64_t)n * m.mul) >> m.shift);
 }
 
 // Launch-constant description of one graph family (plain uniform-d mode).

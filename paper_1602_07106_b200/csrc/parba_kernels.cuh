@@ -52,7 +52,7 @@ template <int SINK, class R>
 struct WarpSmem {
     R qr[kTile];               // pending chain values (ring)
     uint16_t qs[kTile];        // pending slots: buf*kTile + j   (store only)
-    R stage[2][kTile];         // targets of the two tiles in flight (store only)
+    R stage[2][kTile];         // terminal chain values of the two tiles in flight (store only)
 };
 template <class R>
 struct WarpSmem<kWindow, R> {
@@ -74,7 +74,7 @@ __device__ __forceinline__ void finish(W &w, uint32_t slot, uint64_t r, const De
                                        const SinkArgs &a) {
     if constexpr (SINK == kStore) {
         using RS = std::remove_reference_t<decltype(w.stage[0][0])>;
-        (&w.stage[0][0])[slot] = (RS)target_of<NARROW, SEED>(r, p);
+        (&w.stage[0][0])[slot] = (RS)r;  // target computed at flush, all lanes busy
     } else if constexpr (SINK == kWindow) {
         if (SEED && r < p.stop) {
             const uint64_t t = __ldg(p.seed + r);
@@ -127,20 +127,29 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
         else return ((uint32_t)v & 1u) == 0;
     };
 
-    // Write a finished tile out of buffer b (store mode).
-    auto flush = [&](uint32_t b, uint64_t base) {
+    // Write a finished tile out of buffer b (store mode): (source, target)
+    // pairs from the staged terminal values, 16-byte streaming stores.
+    // Interior tiles (all but the range ends) skip the per-edge bounds test.
+    auto flush_t = [&](auto full_c, uint32_t b, uint64_t base) {
+        constexpr bool FULL = decltype(full_c)::value;
         if constexpr (SINK == kStore) {
-            __syncwarp();
-            const bool full_tile = base >= lo && base + kTile <= hi;
+            ulonglong2 *o = reinterpret_cast<ulonglong2 *>(a.out) + (int64_t)(base - lo);
 #pragma unroll
             for (int k = 0; k < kEpl; ++k) {
                 const uint32_t j = lane + 32u * k;
                 const uint64_t i = base + j;
-                if (full_tile || (i >= lo && i < hi)) {
-                    ulonglong2 v = make_ulonglong2(source_of<NARROW, SEED>(i, p), (uint64_t)w.stage[b][j]);
-                    __stcs(reinterpret_cast<ulonglong2 *>(a.out + 2 * (i - lo)), v);
+                if (FULL || (i >= lo && i < hi)) {
+                    const uint64_t tgt = target_of<NARROW, SEED>((uint64_t)w.stage[b][j], p);
+                    __stcs(o + j, make_ulonglong2(source_of<NARROW, SEED>(i, p), tgt));
                 }
             }
+        }
+    };
+    auto flush = [&](uint32_t b, uint64_t base) {
+        if constexpr (SINK == kStore) {
+            __syncwarp();
+            if (base >= lo && base + kTile <= hi) flush_t(std::true_type{}, b, base);
+            else flush_t(std::false_type{}, b, base);
             __syncwarp();
         }
     };
@@ -157,23 +166,21 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
         act = act && !fin;
     };
 
-    for (uint64_t t = gw; t < ntiles; t += nw) {
-        const uint64_t base = (tile0 + t) * kTile;
-        const bool full_tile = base >= lo && base + kTile <= hi;
-        // ---- phase 1: first probe of all edges of the tile
-        uint32_t cb = 0;
-        if constexpr (Hash::kHasCrc) cb = crc0<NB>(tabs, 2 * base);
+    // First probe of every edge of a tile (FULL: interior tile, no bounds test).
+    auto phase1 = [&](auto full_c, uint64_t base, uint32_t cb) {
+        constexpr bool FULL = decltype(full_c)::value;
 #pragma unroll
         for (int k = 0; k < kEpl; ++k) {
             const uint32_t j = lane + 32u * k;
             const uint64_t i = base + j;
-            const bool valid = full_tile || ((i >= lo) && (i < hi));
-            const R r0 = (R)(2 * i + 1);
+            const bool valid = FULL || ((i >= lo) && (i < hi));
+            const R r0 = (R)(2 * base) + (R)(2 * j + 1);
             R r1;
             if constexpr (Hash::kHasCrc) r1 = Hash::from_crc(cb ^ clow_s[j], r0, p);
             else r1 = Hash::probe(tabs, r0, p);
             const bool done = is_done(r1);
-            if (valid && done) finish<NARROW, SEED, SINK>(w, buf * kTile + j, (uint64_t)r1, p, a);
+            if constexpr (SINK == kStore) w.stage[buf][j] = r1;  // final unless pending
+            if constexpr (SINK != kStore) if (valid && done) finish<NARROW, SEED, SINK>(w, buf * kTile + j, (uint64_t)r1, p, a);
             const bool pend = valid && !done;
             const unsigned m = __ballot_sync(0xffffffffu, pend);
             if (pend) {
@@ -184,6 +191,15 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
             tail += __popc(m);
             probes += valid ? 1u : 0u;
         }
+    };
+
+    for (uint64_t t = gw; t < ntiles; t += nw) {
+        const uint64_t base = (tile0 + t) * kTile;
+        // ---- phase 1: first probe of all edges of the tile
+        uint32_t cb = 0;
+        if constexpr (Hash::kHasCrc) cb = crc0<NB>(tabs, 2 * base);
+        if (base >= lo && base + kTile <= hi) phase1(std::true_type{}, base, cb);
+        else phase1(std::false_type{}, base, cb);
         __syncwarp();
         // ---- phase 2: drain the queue with lane refill
         while (tail != head) {
