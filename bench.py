@@ -47,29 +47,54 @@ def _peaks() -> tuple[float, str]:
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clock and throttle reasons sampled (NVML, every ~5 ms) DURING the
+    timed region; falls back to nvidia-smi when NVML is unavailable."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-
-    def __init__(self, index: int):
+    def __init__(self, index: int, period: float = 0.005):
         self.index = index
-        self.rows: list[list[str]] = []
+        self.period = period
+        self.sm: list[float] = []
+        self.max_sm: float | None = None
+        self.reasons: set[str] = set()
+        self.n = 0
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
 
     def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_sm = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            bits = {"hw_slowdown": nv.nvmlClocksThrottleReasonHwSlowdown,
+                    "hw_thermal_slowdown": getattr(nv, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40),
+                    "sw_thermal_slowdown": getattr(nv, "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20),
+                    "sw_power_cap": nv.nvmlClocksThrottleReasonSwPowerCap}
+            while True:
+                self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+                r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                self.reasons |= {k for k, b in bits.items() if r & b}
+                self.n += 1
+                if self._stop.wait(self.period):
+                    break
+        except Exception:
+            Q = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.sw_power_cap"
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={Q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip().split(",")
+                    self.sm.append(float(out[0]))
+                    self.max_sm = float(out[1])
+                    if out[2].strip() == "Active":
+                        self.reasons.add("hw_slowdown")
+                    if out[3].strip() == "Active":
+                        self.reasons.add("sw_power_cap")
+                    self.n += 1
+                except Exception:
+                    pass
+                self._stop.wait(0.1)
 
     def __enter__(self):
         self._t.start()
@@ -80,14 +105,8 @@ class ClockSampler:
         self._t.join(timeout=10)
 
     def summary(self) -> dict:
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in self.rows for k in range(4) if len(r) > 5 + k and r[5 + k] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None, "sm_max_mhz": self.max_sm,
+                "reasons": sorted(self.reasons), "samples": self.n}
 
 
 def _dist():
@@ -99,7 +118,9 @@ def _dist():
 
 def cpu_baseline(sample_edges: int | None = None, budget_s: float = 12.0) -> dict:
     """The reference algorithm (C port in oracle/) on the host cores, store
-    mode into host memory over a bounded sample of C2's edge range."""
+    mode into host memory over a bounded sample of C2's edge range: chunks of
+    at most 1e8 edges (1.6 GB buffer, reused) walking down from the top of
+    the ID space until about `budget_s` of CPU work is done."""
     import numpy as np
 
     import oracle as O
@@ -111,16 +132,24 @@ def cpu_baseline(sample_edges: int | None = None, budget_s: float = 12.0) -> dic
     O.run_threaded(p, p.m - 2_000_000, p.m, O.MODE_STORE, threads=threads, batch=1 << 16)
     rate = 2_000_000 / (time.perf_counter() - t0)
     if sample_edges is None:
-        sample_edges = int(min(max(rate * budget_s, 4_000_000), 200_000_000))
-    lo = p.m - sample_edges
-    out = np.empty((sample_edges, 2), dtype=np.uint64)
+        sample_edges = int(min(max(rate * budget_s, 4_000_000), p.m))
+    chunk = min(sample_edges, 100_000_000)
+    out = np.empty((chunk, 2), dtype=np.uint64)
+    done = probes = 0
+    hi = p.m
     t0 = time.perf_counter()
-    _, probes = O.run_threaded(p, lo, p.m, O.MODE_STORE, threads=threads, batch=1 << 16, out=out)
+    while done < sample_edges:
+        n = min(chunk, sample_edges - done)
+        _, pr = O.run_threaded(p, hi - n, hi, O.MODE_STORE, threads=threads, batch=1 << 16, out=out[:n])
+        probes += pr
+        done += n
+        hi -= n
     dt = time.perf_counter() - t0
     return {"value": sample_edges / dt, "unit": "edges/s", "cores": threads, "kind": "port",
-            "sample": f"C2 (n=1e8, d=10) edge IDs [{lo}, {p.m}) = {sample_edges} edges, store mode into "
-                      f"host memory, oracle/parba_oracle.c (reference table-CRC + u64 %), {threads} threads, "
-                      f"{dt:.2f} s", "probes_per_edge": probes / sample_edges}
+            "sample": f"C2 (n=1e8, d=10) edge IDs [{p.m - sample_edges}, {p.m}) = {sample_edges} edges, "
+                      f"store mode into a reused host buffer, oracle/parba_oracle.c (the reference's "
+                      f"table CRC + u64 %), {threads} threads, {dt:.2f} s",
+            "sample_edges": sample_edges, "probes_per_edge": probes / sample_edges}
 
 
 def run_reference(args) -> None:
@@ -131,7 +160,7 @@ def run_reference(args) -> None:
     n_edges = None
     for k in range(args.warmup + args.steps):
         cb = cpu_baseline(sample_edges=n_edges, budget_s=4.0)
-        n_edges = n_edges or int(cb["sample"].split("= ")[1].split(" ")[0])
+        n_edges = n_edges or cb["sample_edges"]
         if k >= args.warmup:
             samples.append(cb)
     value = statistics.median(s["value"] for s in samples)
@@ -295,13 +324,14 @@ def main() -> None:
     if rank != 0:
         dist.destroy_process_group() if ws > 1 else None
         return
+    # DRAM bytes per launch from the committed `ncu --set full` capture of this
+    # kernel (profiles/store_traffic.json: dram__bytes_read+write per edge)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "store_traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as fh:
-            tj = json.load(fh)
-            traffic = tj.get("bytes_per_launch_per_edge", None)
-            traffic = traffic * shard if traffic else None
+            per_edge = json.load(fh).get("dram_bytes_per_edge")
+            traffic = per_edge * shard if per_edge else None
     line = {
         "metric": "edges generated/sec (device-timed) at 1/2/4/8 B200; % of HBM/int roofline",
         "value": value, "unit": "edges/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
