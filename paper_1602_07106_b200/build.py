@@ -35,18 +35,23 @@ def stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None,
+          defines: dict | None = None) -> str:
+    """Compile the library (default: in-tree LIB).  `out`/`defines` build
+    tuning variants (e.g. {"PARBA_WARPS": 8}) for tools/ab.py."""
+    target = out or LIB
+    if out is None and not force and not stale():
         return LIB
     cmd = [_nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
-           "-shared", "-cudart", "static", "-o", LIB + ".tmp",
+           "-shared", "-cudart", "static", "-o", target + ".tmp",
+           *[f"-D{k}={v}" for k, v in (defines or {}).items()],
            *[os.path.join(CSRC, s) for s in SOURCES]]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(target + ".tmp", target)
+    return target
 
 
 if __name__ == "__main__":

@@ -74,6 +74,7 @@ DevParams make_dev(const parba_params_t *p, uint64_t K = 0) {
     d.k0 = crc32c_u64_bitwise(p->crc_seed0, 0);
     d.k01 = d.k0 ^ crc32c_u64_bitwise(p->crc_seed1, 0);
     d.seed = p->seed_edges;
+    d.cm = ChunkMul{1u << 21, 1u << 13, 1u << 23, 1u << 10, 4u};
     d.div64 = make_magic64(p->d);
     d.div32 = make_magic32(p->d);
     d.K = K;
@@ -91,13 +92,14 @@ DevParams make_dev(const parba_params_t *p, uint64_t K = 0) {
 
 int bits_of(uint64_t x) { return x ? 64 - __builtin_clzll(x) : 0; }
 
-// Byte tables needed to cover every chain value of a launch (r < 2*hi).
-int nb_for(uint64_t two_hi) {
+// CRC chunk tables needed to cover every chain value of a launch (r < 2*hi):
+// 3 -> r < 2^32 (narrow), 4 -> < 2^43, 5 -> < 2^52, 6 -> any.
+int nc_for(uint64_t two_hi) {
     const int b = bits_of(two_hi);
-    if (b <= 32) return 4;
-    if (b <= 40) return 5;
-    if (b <= 48) return 6;
-    return 8;
+    if (b <= 32) return 3;
+    if (b <= 43) return 4;
+    if (b <= 52) return 5;
+    return 6;
 }
 
 struct DevInfo {
@@ -156,17 +158,17 @@ int launch_tiles_s(const parba_params_t *p, const DevParams &dp, uint64_t lo, ui
 template <int SINK>
 int launch_tiles(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi,
                  const SinkArgs &a, unsigned long long *probes, cudaStream_t st) {
-    int nb = nb_for(2 * hi);
-    if (nb == 4 && p->d >= (1ull << 31)) nb = 5;  // narrow closed forms need d < 2^31
+    int nc = nc_for(2 * hi);
+    if (nc == 3 && p->d >= (1ull << 31)) nc = 4;  // narrow closed forms need d < 2^31
     if (p->hash_kind == PARBA_HASH_SIMPLE) {
-        if (nb == 4) return launch_tiles_s<HashSimple<true>, SINK>(p, dp, lo, hi, a, probes, st, 4);
+        if (nc == 3) return launch_tiles_s<HashSimple<true>, SINK>(p, dp, lo, hi, a, probes, st, 4);
         return launch_tiles_s<HashSimple<false>, SINK>(p, dp, lo, hi, a, probes, st, 5);
     }
-    switch (nb) {
-        case 4: return launch_tiles_s<HashCrc<4>, SINK>(p, dp, lo, hi, a, probes, st, 0);
-        case 5: return launch_tiles_s<HashCrc<5>, SINK>(p, dp, lo, hi, a, probes, st, 1);
-        case 6: return launch_tiles_s<HashCrc<6>, SINK>(p, dp, lo, hi, a, probes, st, 2);
-        default: return launch_tiles_s<HashCrc<8>, SINK>(p, dp, lo, hi, a, probes, st, 3);
+    switch (nc) {
+        case 3: return launch_tiles_s<HashCrc<3>, SINK>(p, dp, lo, hi, a, probes, st, 0);
+        case 4: return launch_tiles_s<HashCrc<4>, SINK>(p, dp, lo, hi, a, probes, st, 1);
+        case 5: return launch_tiles_s<HashCrc<5>, SINK>(p, dp, lo, hi, a, probes, st, 2);
+        default: return launch_tiles_s<HashCrc<6>, SINK>(p, dp, lo, hi, a, probes, st, 3);
     }
 }
 
@@ -191,7 +193,7 @@ int launch_chains(const parba_params_t *p, const DevParams &dp, const uint64_t *
     if (count == 0) return PARBA_OK;
     if (p->hash_kind == PARBA_HASH_SIMPLE)
         return launch_chains_t<HashSimple<false>>(dp, r0, count, stop, out, ids, pairs, probes, st);
-    return launch_chains_t<HashCrc<8>>(dp, r0, count, stop, out, ids, pairs, probes, st);
+    return launch_chains_t<HashCrcBytes>(dp, r0, count, stop, out, ids, pairs, probes, st);
 }
 
 template <typename CountT>
@@ -234,7 +236,7 @@ int parba_hash(const parba_params_t *p, const uint64_t *r, uint64_t count, uint6
     if (p->hash_kind == PARBA_HASH_SIMPLE)
         hash_kernel<HashSimple<false>><<<grid_for(count, 256), 256, 0, st>>>(dp, r, count, out);
     else
-        hash_kernel<HashCrc<8>><<<grid_for(count, 256), 256, 0, st>>>(dp, r, count, out);
+        hash_kernel<HashCrcBytes><<<grid_for(count, 256), 256, 0, st>>>(dp, r, count, out);
     CUDA_TRY(cudaGetLastError());
     return PARBA_OK;
 }

@@ -1,10 +1,9 @@
 // parba_device.cuh -- device-side building blocks of the B200 hot path.
 //
-//   crc0<NB>(w)   CRC32-C of one 64-bit word with zero seed, w < 2^(8*NB):
-//                 slicing tables tab[k][b] = crc(0, b << 8k) in shared memory,
-//                 one lookup per significant byte (4 for 2m <= 2^32, 5 for the
-//                 paper-scale 1e11-edge graph).  Byte extraction is one PRMT
-//                 (ALU pipe) and the scaled address one IMAD (FMA pipe).
+//   crc_chunks    CRC32-C of one 64-bit word with seed s0 from 11-bit chunk
+//                 tables in shared memory: 3 lookups for positions < 2^32, 4
+//                 for < 2^43; offsets formed on the FMA pipe.
+//   crc_bytes     byte-sliced variant for the generic kernels (any 64-bit value).
 //   h_crc(r)      the reference hash ((crc(s0,r)<<32) + crc(s1,r)) % r
 //                 (hashing.py:119-125, _kernels.py:32-42) rewritten through
 //                 CRC linearity: crc(s,w) = crc(s,0) ^ crc(0,w), so one table
@@ -82,6 +81,12 @@ __device__ __forceinline__ uint32_t magic_div32(uint32_t n, const Magic32 &m) {
     return (uint32_t)(((uint64_t)n * m.mul) >> m.shift);
 }
 
+// Opaque powers of two (kernel parameters, so the compiler cannot turn the
+// multiplies into ALU shifts): m21 = 2^21, m13 = 2^13, m23 = 2^23, m10 = 2^10, m4 = 4.
+struct ChunkMul {
+    uint32_t m21, m13, m23, m10, m4;
+};
+
 // Launch-constant description of one graph family (plain uniform-d mode).
 struct DevParams {
     uint64_t n, d, n0, m0, m;
@@ -94,6 +99,7 @@ struct DevParams {
     uint64_t win_rlim;     // window mode: generated target < K  <=>  r < win_rlim
     uint32_t win_rlim32;   // min(win_rlim, 2^32 - 1) for narrow launches
     uint64_t K;
+    ChunkMul cm;           // opaque powers of two for the chunk CRC
 };
 
 // Closed forms (generator.py:157-169): source of edge i, target of terminal r.
@@ -186,52 +192,114 @@ __device__ __forceinline__ uint64_t mod_int(uint32_t hhi, uint32_t hlo, uint64_t
 }
 
 // ---------------------------------------------------------------------------
-// Byte-sliced CRC tables in shared memory: tab[k][b] = crc(0, b << 8k).
+// CRC tables in shared memory.  Table 0 of every layout carries
+// k0 = crc(s0, 0): each crc() XORs exactly one table-0 entry, so it returns
+// crc(s0, w) directly (CRC linearity).
+//
+// Byte layout (generic kernels, any 64-bit value): tab[k*256 + b] = crc(0, b << 8k).
+// Chunk layout (tile kernels): 11/11/10-bit chunks aligned to each 32-bit
+// word, chunk k covers bits [kShift[k], kShift[k] + width) and has a
+// 2048-entry table at tab[k*2048].  Three lookups cover 32-bit positions, four
+// cover 43 bits.  The byte offset (chunk << 2) of every chunk is formed on the
+// FMA pipe by integer multiplies with launch-constant (opaque) powers of two,
+// so the CRC costs one LOP3 per word on the ALU pipe instead of one PRMT per
+// byte.
 
-template <int NB>
-struct CrcTables {
-    uint32_t t[NB][256];
-};
+// chunk k covers bits [chunk_shift(k), chunk_shift(k) + chunk_width(k)): 0, 11, 22, 32, 43, 54
+__host__ __device__ __forceinline__ uint32_t chunk_shift(int k) { return 32u * (k / 3) + 11u * (k % 3); }
+__host__ __device__ __forceinline__ uint32_t chunk_width(int k) { return (k % 3 == 2) ? 10u : 11u; }
 
-// Table 0 carries k0 = crc(s0, 0): every crc0() XORs exactly one table-0
-// entry, so crc0() returns crc(s0, w) directly (CRC linearity).
-template <int NB>
-__device__ __forceinline__ void build_crc_tables(CrcTables<NB> &s, uint32_t k0) {
-    for (int e = threadIdx.x; e < NB * 256; e += blockDim.x) {
+__device__ __forceinline__ void build_byte_tables(uint32_t *tab, int nb, uint32_t k0) {
+    for (int e = threadIdx.x; e < nb * 256; e += blockDim.x) {
         const int k = e >> 8, b = e & 255;
-        s.t[k][b] = crc32c_u64_bitwise(0u, (uint64_t)b << (8 * k)) ^ (k == 0 ? k0 : 0u);
+        tab[e] = crc32c_u64_bitwise(0u, (uint64_t)b << (8 * k)) ^ (k == 0 ? k0 : 0u);
+    }
+}
+
+__device__ __forceinline__ void build_chunk_tables(uint32_t *tab, int nc, uint32_t k0) {
+    for (int e = threadIdx.x; e < nc * 2048; e += blockDim.x) {
+        const int k = e >> 11, x = e & 2047;
+        uint32_t v = 0;
+        if ((uint32_t)x < (1u << chunk_width(k)))
+            v = crc32c_u64_bitwise(0u, (uint64_t)x << chunk_shift(k)) ^ (k == 0 ? k0 : 0u);
+        tab[e] = v;
     }
 }
 
 template <int NB>
-__device__ __forceinline__ uint32_t crc0(const CrcTables<NB> &s, uint64_t w) {
+__device__ __forceinline__ uint32_t crc_bytes(const uint32_t *tab, uint64_t w) {
     const uint32_t lo = (uint32_t)w, hi = (uint32_t)(w >> 32);
     uint32_t c = 0;
 #pragma unroll
     for (int k = 0; k < NB; ++k) {
         const uint32_t b = __byte_perm(k < 4 ? lo : hi, 0u, 0x4440u | (k & 3));
-        c ^= s.t[k][b];
+        c ^= tab[k * 256 + b];
+    }
+    return c;
+}
+
+__device__ __forceinline__ uint32_t lds_u32(const uint32_t *base, uint32_t byte_off) {
+    return *reinterpret_cast<const uint32_t *>(reinterpret_cast<const char *>(base) + byte_off);
+}
+
+// crc of the three chunks of one 32-bit word, tables t0..t2 (2048 entries each)
+__device__ __forceinline__ uint32_t crc_word3(const uint32_t *t, uint32_t x, const ChunkMul &m) {
+    const uint32_t o0 = __umulhi(x * m.m21, m.m13);    // (x & 0x7ff) << 2
+    const uint32_t o1 = __umulhi(x, m.m23) & 0x1ffcu;   // ((x >> 11) & 0x7ff) << 2
+    const uint32_t o2 = __umulhi(x, m.m10) * m.m4;      // (x >> 22) << 2
+    return lds_u32(t, o0) ^ lds_u32(t + 2048, o1) ^ lds_u32(t + 4096, o2);
+}
+
+template <int NC>
+__device__ __forceinline__ uint32_t crc_chunks(const uint32_t *tab, uint64_t w, const ChunkMul &m) {
+    uint32_t c = crc_word3(tab, (uint32_t)w, m);
+    if constexpr (NC > 3) {
+        const uint32_t hi = (uint32_t)(w >> 32);
+        c ^= lds_u32(tab + 3 * 2048, __umulhi(hi * m.m21, m.m13));
+        if constexpr (NC > 4) c ^= lds_u32(tab + 4 * 2048, __umulhi(hi, m.m23) & 0x1ffcu);
+        if constexpr (NC > 5) c ^= lds_u32(tab + 5 * 2048, __umulhi(hi, m.m10) * m.m4);
     }
     return c;
 }
 
 // ---------------------------------------------------------------------------
 // Hash policies.  R is the chain-value type (u32 when every position < 2^32).
+// probe(tab, r) = h(r); from_crc(c0, r) finishes h from c0 = crc(s0, r).
 
-template <int NB>
+// Tile kernels: chunk tables; NC = 3 (every r < 2^32), 4 (< 2^43),
+// 5 (< 2^52), 6 (any).
+template <int NC>
 struct HashCrc {
     static constexpr bool kHasCrc = true;
-    static constexpr bool kNarrow = NB <= 4;
-    static constexpr int kTables = NB;
+    static constexpr bool kNarrow = NC == 3;
+    static constexpr bool kPack = NC <= 5;       // every value < 2^52
+    static constexpr int kTableWords = NC * 2048;
     using R = typename std::conditional<kNarrow, uint32_t, uint64_t>::type;
-    // c0 = crc(s0, r) (k0 already folded into table 0); crc(s1, r) = c0 ^ k01.
+    __device__ __forceinline__ static void build(uint32_t *tab, uint32_t k0) { build_chunk_tables(tab, NC, k0); }
     __device__ __forceinline__ static R from_crc(uint32_t c0, R r, const DevParams &p) {
         if constexpr (kNarrow) return mod_fp<R>(c0, c0 ^ p.k01, u32_to_f64(r));
-        else if constexpr (NB * 8 <= 52) return mod_fp<R>(c0, c0 ^ p.k01, u52_to_f64(r));
+        else if constexpr (NC <= 5) return mod_fp<R>(c0, c0 ^ p.k01, u52_to_f64(r));
         else return mod_int(c0, c0 ^ p.k01, r);
     }
-    __device__ __forceinline__ static R probe(const CrcTables<NB> &s, R r, const DevParams &p) {
-        return from_crc(crc0<NB>(s, r), r, p);
+    __device__ __forceinline__ static uint32_t crc(const uint32_t *tab, uint64_t w, const DevParams &p) {
+        return crc_chunks<NC>(tab, w, p.cm);
+    }
+    __device__ __forceinline__ static R probe(const uint32_t *tab, R r, const DevParams &p) {
+        return from_crc(crc(tab, r, p), r, p);
+    }
+};
+
+// Generic kernels: byte tables, any 64-bit value.
+struct HashCrcBytes {
+    static constexpr bool kHasCrc = true;
+    static constexpr bool kNarrow = false;
+    static constexpr bool kPack = false;
+    static constexpr int kTableWords = 8 * 256;
+    using R = uint64_t;
+    __device__ __forceinline__ static void build(uint32_t *tab, uint32_t k0) { build_byte_tables(tab, 8, k0); }
+    __device__ __forceinline__ static R probe(const uint32_t *tab, R r, const DevParams &p) {
+        const uint32_t c0 = crc_bytes<8>(tab, r);
+        return mod_int(c0, c0 ^ p.k01, r);
     }
 };
 
@@ -239,9 +307,11 @@ template <bool NARROW>
 struct HashSimple {
     static constexpr bool kHasCrc = false;
     static constexpr bool kNarrow = NARROW;
-    static constexpr int kTables = 1;
+    static constexpr bool kPack = NARROW;
+    static constexpr int kTableWords = 0;
     using R = typename std::conditional<NARROW, uint32_t, uint64_t>::type;
-    __device__ __forceinline__ static R probe(const CrcTables<1> &, R r, const DevParams &p) {
+    __device__ __forceinline__ static void build(uint32_t *, uint32_t) {}
+    __device__ __forceinline__ static R probe(const uint32_t *, R r, const DevParams &p) {
         return (R)__umul64hi((uint64_t)r * p.mult, (uint64_t)r);
     }
 };

@@ -36,7 +36,16 @@ namespace parba {
 
 constexpr int kTile = 256;                 // edges per warp tile (power of two)
 constexpr int kEpl = kTile / 32;           // edges per lane in phase 1
-constexpr int kWarps = 8;                  // warps per CTA
+#ifndef PARBA_WARPS
+#define PARBA_WARPS 32
+#endif
+#ifndef PARBA_MINB_STORE
+#define PARBA_MINB_STORE 1
+#endif
+#ifndef PARBA_MINB_STREAM
+#define PARBA_MINB_STREAM 1
+#endif
+constexpr int kWarps = PARBA_WARPS;        // warps per CTA
 constexpr int kThreads = kWarps * 32;
 
 enum SinkKind { kStore = 0, kWindow = 1, kFull = 2 };
@@ -48,11 +57,14 @@ struct SinkArgs {
 };
 
 // Per-warp shared state.  R = chain value type (u32 in narrow mode).
+// Store queue entries pack the chain value and its stage slot (9 bits) into
+// one u64 -- value in the low 55 bits -- when every position is < 2^52
+// (Hash::kPack); otherwise the slot goes to a separate u16 ring.
 template <int SINK, class R>
 struct WarpSmem {
-    R qr[kTile];               // pending chain values (ring)
-    uint16_t qs[kTile];        // pending slots: buf*kTile + j   (store only)
-    R stage[2][kTile];         // terminal chain values of the two tiles in flight (store only)
+    uint64_t qe[kTile];        // pending (slot << 55) | value   (ring)
+    uint16_t qs[kTile];        // pending slots when !kPack
+    R stage[2][kTile];         // terminal chain values of the two tiles in flight
 };
 template <class R>
 struct WarpSmem<kWindow, R> {
@@ -63,10 +75,13 @@ struct WarpSmem<kFull, R> {
     R qr[kTile];
 };
 
+// Dynamic shared memory: [CRC tables][crc(0,2j+1) table][per-warp state].
 template <class Hash, int SINK>
 constexpr size_t tile_smem_bytes() {
-    return kWarps * sizeof(WarpSmem<SINK, typename Hash::R>);
+    return (Hash::kHasCrc ? (Hash::kTableWords + kTile) * 4 : 0) +
+           kWarps * sizeof(WarpSmem<SINK, typename Hash::R>);
 }
+constexpr uint64_t kValueMask = (1ull << 55) - 1;
 
 // A chain finished with terminal value r: hand its target to the sink.
 template <bool NARROW, bool SEED, int SINK, class W>
@@ -89,18 +104,18 @@ __device__ __forceinline__ void finish(W &w, uint32_t slot, uint64_t r, const De
 }
 
 template <class Hash, int SINK, bool SEED>
-__global__ void __launch_bounds__(kThreads, SINK == kStore ? 5 : 6)
+__global__ void __launch_bounds__(kThreads, SINK == kStore ? PARBA_MINB_STORE : PARBA_MINB_STREAM)
 tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntiles,
             SinkArgs a, unsigned long long *probes_out) {
     using R = typename Hash::R;
     constexpr bool NARROW = Hash::kNarrow;
-    constexpr int NB = Hash::kTables;
-    __shared__ CrcTables<NB> tabs;
-    __shared__ uint32_t clow_s[kTile];  // crc(0, 2j+1) for j < kTile (2j+1 < 512)
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    WarpSmem<SINK, R> *wsm = reinterpret_cast<WarpSmem<SINK, R> *>(smem_raw);
+    uint32_t *tabs = reinterpret_cast<uint32_t *>(smem_raw);
+    uint32_t *clow_s = tabs + Hash::kTableWords;  // crc(0, 2j+1), j < kTile (2j+1 < 512)
+    WarpSmem<SINK, R> *wsm = reinterpret_cast<WarpSmem<SINK, R> *>(
+        smem_raw + (Hash::kHasCrc ? (Hash::kTableWords + kTile) * 4 : 0));
     if constexpr (Hash::kHasCrc) {
-        build_crc_tables<NB>(tabs, p.k0);
+        Hash::build(tabs, p.k0);
         for (int j = threadIdx.x; j < kTile; j += blockDim.x)
             clow_s[j] = crc32c_u64_bitwise(0u, 2u * (uint32_t)j + 1u);
     }
@@ -131,7 +146,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
     // pairs from the staged terminal values, 16-byte streaming stores.
     // Interior tiles (all but the range ends) skip the per-edge bounds test.
     auto flush_t = [&](auto full_c, uint32_t b, uint64_t base) {
-        constexpr bool FULL = decltype(full_c)::value;
+        [[maybe_unused]] constexpr bool FULL = decltype(full_c)::value;
         if constexpr (SINK == kStore) {
             ulonglong2 *o = reinterpret_cast<ulonglong2 *>(a.out) + (int64_t)(base - lo);
 #pragma unroll
@@ -185,8 +200,16 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
             const unsigned m = __ballot_sync(0xffffffffu, pend);
             if (pend) {
                 const uint32_t pos = (tail + __popc(m & ltmask)) & (kTile - 1);
-                w.qr[pos] = r1;
-                if constexpr (SINK == kStore) w.qs[pos] = (uint16_t)(buf * kTile + j);
+                if constexpr (SINK == kStore) {
+                    if constexpr (Hash::kPack) {
+                        w.qe[pos] = ((uint64_t)(buf * kTile + j) << 55) | (uint64_t)r1;
+                    } else {
+                        w.qe[pos] = (uint64_t)r1;
+                        w.qs[pos] = (uint16_t)(buf * kTile + j);
+                    }
+                } else {
+                    w.qr[pos] = r1;
+                }
             }
             tail += __popc(m);
             probes += valid ? 1u : 0u;
@@ -197,7 +220,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
         const uint64_t base = (tile0 + t) * kTile;
         // ---- phase 1: first probe of all edges of the tile
         uint32_t cb = 0;
-        if constexpr (Hash::kHasCrc) cb = crc0<NB>(tabs, 2 * base);
+        if constexpr (Hash::kHasCrc) cb = Hash::crc(tabs, 2 * base, p);
         if (base >= lo && base + kTile <= hi) phase1(std::true_type{}, base, cb);
         else phase1(std::false_type{}, base, cb);
         __syncwarp();
@@ -208,8 +231,18 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
             const uint32_t rank = __popc(idle & ltmask);
             if (!act && rank < avail) {
                 const uint32_t pos = (head + rank) & (kTile - 1);
-                r = w.qr[pos];
-                if constexpr (SINK == kStore) slot = w.qs[pos];
+                if constexpr (SINK == kStore) {
+                    const uint64_t e = w.qe[pos];
+                    if constexpr (Hash::kPack) {
+                        r = (R)(e & kValueMask);
+                        slot = (uint32_t)(e >> 55);
+                    } else {
+                        r = (R)e;
+                        slot = w.qs[pos];
+                    }
+                } else {
+                    r = w.qr[pos];
+                }
                 act = 1;
             }
             head += min((uint32_t)__popc(idle), avail);
@@ -250,8 +283,8 @@ __global__ void __launch_bounds__(256)
 chains_kernel(DevParams p, const uint64_t *__restrict__ r0, uint64_t count, uint64_t stop,
               uint64_t *__restrict__ out, const uint64_t *__restrict__ ids,
               uint64_t *__restrict__ pairs, unsigned long long *probes_out) {
-    __shared__ CrcTables<Hash::kTables> tabs;
-    if constexpr (Hash::kHasCrc) build_crc_tables<Hash::kTables>(tabs, p.k0);
+    __shared__ uint32_t tabs[Hash::kTableWords > 0 ? Hash::kTableWords : 1];
+    Hash::build(tabs, p.k0);
     __syncthreads();
     unsigned long long probes = 0;
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count;
@@ -277,8 +310,8 @@ chains_kernel(DevParams p, const uint64_t *__restrict__ r0, uint64_t count, uint
 template <class Hash>
 __global__ void __launch_bounds__(256)
 hash_kernel(DevParams p, const uint64_t *__restrict__ r, uint64_t count, uint64_t *__restrict__ out) {
-    __shared__ CrcTables<Hash::kTables> tabs;
-    if constexpr (Hash::kHasCrc) build_crc_tables<Hash::kTables>(tabs, p.k0);
+    __shared__ uint32_t tabs[Hash::kTableWords > 0 ? Hash::kTableWords : 1];
+    Hash::build(tabs, p.k0);
     __syncthreads();
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count;
          k += (uint64_t)gridDim.x * blockDim.x)
