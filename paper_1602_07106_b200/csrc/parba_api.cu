@@ -93,9 +93,11 @@ DevParams make_dev(const parba_params_t *p, uint64_t K = 0) {
 int bits_of(uint64_t x) { return x ? 64 - __builtin_clzll(x) : 0; }
 
 // CRC chunk tables needed to cover every chain value of a launch (r < 2*hi):
-// 3 -> r < 2^32 (narrow), 4 -> < 2^43, 5 -> < 2^52, 6 -> any.
+// 2 -> r < 2^31 (narrow, 32-bit remainder), 3 -> r < 2^32, 4 -> < 2^43,
+// 5 -> < 2^52, 6 -> any.
 int nc_for(uint64_t two_hi) {
     const int b = bits_of(two_hi);
+    if (b <= 31) return 2;
     if (b <= 32) return 3;
     if (b <= 43) return 4;
     if (b <= 52) return 5;
@@ -104,7 +106,8 @@ int nc_for(uint64_t two_hi) {
 
 struct DevInfo {
     int sms = 0;
-    bool attr_done[8][3][2] = {};
+    int smem_optin = 0;  // max dynamic shared memory per block
+    bool attr_done[8][3][2] = {};  // [hash variant][sink][seed]
 };
 std::mutex g_mu;
 std::vector<DevInfo> g_dev;
@@ -114,7 +117,10 @@ int dev_info(DevInfo **out) {
     CUDA_TRY(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lk(g_mu);
     if ((int)g_dev.size() <= dev) g_dev.resize(dev + 1);
-    if (!g_dev[dev].sms) CUDA_TRY(cudaDeviceGetAttribute(&g_dev[dev].sms, cudaDevAttrMultiProcessorCount, dev));
+    if (!g_dev[dev].sms) {
+        CUDA_TRY(cudaDeviceGetAttribute(&g_dev[dev].sms, cudaDevAttrMultiProcessorCount, dev));
+        CUDA_TRY(cudaDeviceGetAttribute(&g_dev[dev].smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    }
     *out = &g_dev[dev];
     return PARBA_OK;
 }
@@ -127,23 +133,27 @@ int launch_tiles_t(const DevParams &dp, uint64_t lo, uint64_t hi, const SinkArgs
     int rc = dev_info(&di);
     if (rc) return rc;
     auto kern = tile_kernel<Hash, SINK, SEED>;
-    const size_t smem = tile_smem_bytes<Hash, SINK>();
+    // as many warps per CTA (<= kWarps) as the shared memory allows
+    const size_t fixed = tile_smem_fixed<Hash>(), per_warp = tile_smem_per_warp<Hash, SINK>();
+    int warps = kWarps;
+    while (warps > 1 && fixed + warps * per_warp > (size_t)di->smem_optin) --warps;
+    const size_t smem = fixed + warps * per_warp;
     int per_sm = 0;
     {
         std::lock_guard<std::mutex> lk(g_mu);
         if (!di->attr_done[variant][SINK][SEED]) {
-            CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(fixed + kWarps * per_warp > (size_t)di->smem_optin ? di->smem_optin : fixed + kWarps * per_warp)));
             di->attr_done[variant][SINK][SEED] = true;
         }
     }
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem));
     if (per_sm < 1) per_sm = 1;
     const uint64_t tile0 = lo / kTile;
     const uint64_t ntiles = (hi - 1) / kTile - tile0 + 1;
     uint64_t grid = (uint64_t)di->sms * per_sm;
-    const uint64_t need = (ntiles + kWarps - 1) / kWarps;
+    const uint64_t need = (ntiles + warps - 1) / warps;
     if (grid > need) grid = need;
-    kern<<<(unsigned)grid, kThreads, smem, st>>>(dp, lo, hi, tile0, ntiles, a, probes);
+    kern<<<(unsigned)grid, warps * 32, smem, st>>>(dp, lo, hi, tile0, ntiles, a, probes);
     CUDA_TRY(cudaGetLastError());
     return PARBA_OK;
 }
@@ -159,12 +169,13 @@ template <int SINK>
 int launch_tiles(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi,
                  const SinkArgs &a, unsigned long long *probes, cudaStream_t st) {
     int nc = nc_for(2 * hi);
-    if (nc == 3 && p->d >= (1ull << 31)) nc = 4;  // narrow closed forms need d < 2^31
+    if (nc <= 3 && p->d >= (1ull << 31)) nc = 4;  // narrow closed forms need d < 2^31
     if (p->hash_kind == PARBA_HASH_SIMPLE) {
-        if (nc == 3) return launch_tiles_s<HashSimple<true>, SINK>(p, dp, lo, hi, a, probes, st, 4);
+        if (nc <= 3) return launch_tiles_s<HashSimple<true>, SINK>(p, dp, lo, hi, a, probes, st, 4);
         return launch_tiles_s<HashSimple<false>, SINK>(p, dp, lo, hi, a, probes, st, 5);
     }
     switch (nc) {
+        case 2: return launch_tiles_s<HashCrc<2>, SINK>(p, dp, lo, hi, a, probes, st, 6);
         case 3: return launch_tiles_s<HashCrc<3>, SINK>(p, dp, lo, hi, a, probes, st, 0);
         case 4: return launch_tiles_s<HashCrc<4>, SINK>(p, dp, lo, hi, a, probes, st, 1);
         case 5: return launch_tiles_s<HashCrc<5>, SINK>(p, dp, lo, hi, a, probes, st, 2);

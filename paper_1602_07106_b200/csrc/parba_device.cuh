@@ -175,6 +175,24 @@ __device__ __forceinline__ R mod_fp(uint32_t hhi, uint32_t hlo, double rd) {
     }
 }
 
+// h % r for 1 <= r < 2^31 (h = hhi:hlo): stage A as in mod_fp, then the
+// final remainder in 32-bit integer arithmetic.  t = v - qb*r lies in [-r, r)
+// and v = x*2^32 + hlo == hlo (mod 2^32), so t = hlo - qb*r (mod 2^32) read as
+// int32 is exact (|t| < 2^31); t < 0 ? t + r : t == min_u32(t, t + r).  qb is
+// the low word of fma(v, y, 1.5*2^52) (two's complement for negative qb).
+// 10 FP64 instructions + 1 IMAD + 2 ALU, no FP64 -> integer conversion.
+__device__ __forceinline__ uint32_t mod_fp31(uint32_t hhi, uint32_t hlo, uint32_t r) {
+    const double rd = u32_to_f64(r);
+    const double y = recip_approx(rd);
+    const double ha = u32_to_f64(hhi);
+    const double qa = fma(ha, y, 0x1.8p52) - 0x1.8p52;
+    const double x = fma(-qa, rd, ha);                          // exact, in [-r, r)
+    const double v = fma(x, 0x1p32, u32_to_f64(hlo));           // ~ x*2^32 + hlo
+    const uint32_t qb = (uint32_t)__double2loint(fma(v, y, 0x1.8p52));
+    const uint32_t t = hlo - qb * r;                            // exact mod 2^32
+    return min(t, t + r);
+}
+
 // h % r for any 1 <= r < 2^64 (generic kernels; integer corrections).
 __device__ __forceinline__ uint64_t mod_int(uint32_t hhi, uint32_t hlo, uint64_t r) {
     const uint64_t h = ((uint64_t)hhi << 32) | hlo;
@@ -266,23 +284,25 @@ __device__ __forceinline__ uint32_t crc_chunks(const uint32_t *tab, uint64_t w, 
 // Hash policies.  R is the chain-value type (u32 when every position < 2^32).
 // probe(tab, r) = h(r); from_crc(c0, r) finishes h from c0 = crc(s0, r).
 
-// Tile kernels: chunk tables; NC = 3 (every r < 2^32), 4 (< 2^43),
-// 5 (< 2^52), 6 (any).
+// Tile kernels: chunk tables; NC = 2 (every r < 2^31; 3 tables), 3 (< 2^32),
+// 4 (< 2^43), 5 (< 2^52), 6 (any).
 template <int NC>
 struct HashCrc {
     static constexpr bool kHasCrc = true;
-    static constexpr bool kNarrow = NC == 3;
+    static constexpr int kChunks = NC < 3 ? 3 : NC;
+    static constexpr bool kNarrow = NC <= 3;
     static constexpr bool kPack = NC <= 5;       // every value < 2^52
-    static constexpr int kTableWords = NC * 2048;
+    static constexpr int kTableWords = kChunks * 2048;
     using R = typename std::conditional<kNarrow, uint32_t, uint64_t>::type;
-    __device__ __forceinline__ static void build(uint32_t *tab, uint32_t k0) { build_chunk_tables(tab, NC, k0); }
+    __device__ __forceinline__ static void build(uint32_t *tab, uint32_t k0) { build_chunk_tables(tab, kChunks, k0); }
     __device__ __forceinline__ static R from_crc(uint32_t c0, R r, const DevParams &p) {
-        if constexpr (kNarrow) return mod_fp<R>(c0, c0 ^ p.k01, u32_to_f64(r));
+        if constexpr (NC == 2) return mod_fp31(c0, c0 ^ p.k01, r);
+        else if constexpr (kNarrow) return mod_fp<R>(c0, c0 ^ p.k01, u32_to_f64(r));
         else if constexpr (NC <= 5) return mod_fp<R>(c0, c0 ^ p.k01, u52_to_f64(r));
         else return mod_int(c0, c0 ^ p.k01, r);
     }
     __device__ __forceinline__ static uint32_t crc(const uint32_t *tab, uint64_t w, const DevParams &p) {
-        return crc_chunks<NC>(tab, w, p.cm);
+        return crc_chunks<kChunks>(tab, w, p.cm);
     }
     __device__ __forceinline__ static R probe(const uint32_t *tab, R r, const DevParams &p) {
         return from_crc(crc(tab, r, p), r, p);

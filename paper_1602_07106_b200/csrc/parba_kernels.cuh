@@ -76,10 +76,13 @@ struct WarpSmem<kFull, R> {
 };
 
 // Dynamic shared memory: [CRC tables][crc(0,2j+1) table][per-warp state].
+template <class Hash>
+constexpr size_t tile_smem_fixed() {
+    return Hash::kHasCrc ? (Hash::kTableWords + kTile) * 4 : 0;
+}
 template <class Hash, int SINK>
-constexpr size_t tile_smem_bytes() {
-    return (Hash::kHasCrc ? (Hash::kTableWords + kTile) * 4 : 0) +
-           kWarps * sizeof(WarpSmem<SINK, typename Hash::R>);
+constexpr size_t tile_smem_per_warp() {
+    return sizeof(WarpSmem<SINK, typename Hash::R>);
 }
 constexpr uint64_t kValueMask = (1ull << 55) - 1;
 
@@ -123,10 +126,11 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
 
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
+    const int wpc = blockDim.x >> 5;  // warps per CTA (<= kWarps; fewer when smem is tight)
     WarpSmem<SINK, R> &w = wsm[wib];
     const unsigned ltmask = lanemask_lt();
-    const uint64_t gw = (uint64_t)blockIdx.x * kWarps + wib;
-    const uint64_t nw = (uint64_t)gridDim.x * kWarps;
+    const uint64_t gw = (uint64_t)blockIdx.x * wpc + wib;
+    const uint64_t nw = (uint64_t)gridDim.x * wpc;
 
     int act = 0;                  // lane holds a running chain
     R r = 0;
