@@ -244,38 +244,46 @@ __device__ __forceinline__ void build_chunk_tables(uint32_t *tab, int nc, uint32
     }
 }
 
+// Shared-space (32-bit) addressing: the tables are reached through a
+// shared-window address kept in a register, so the compiler does not
+// rematerialise the generic->shared conversion inside the loop.
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
 template <int NB>
-__device__ __forceinline__ uint32_t crc_bytes(const uint32_t *tab, uint64_t w) {
+__device__ __forceinline__ uint32_t crc_bytes(uint32_t tab, uint64_t w) {
     const uint32_t lo = (uint32_t)w, hi = (uint32_t)(w >> 32);
     uint32_t c = 0;
 #pragma unroll
     for (int k = 0; k < NB; ++k) {
         const uint32_t b = __byte_perm(k < 4 ? lo : hi, 0u, 0x4440u | (k & 3));
-        c ^= tab[k * 256 + b];
+        c ^= lds_u32(tab + (k * 256 + b) * 4);
     }
     return c;
 }
 
-__device__ __forceinline__ uint32_t lds_u32(const uint32_t *base, uint32_t byte_off) {
-    return *reinterpret_cast<const uint32_t *>(reinterpret_cast<const char *>(base) + byte_off);
-}
-
-// crc of the three chunks of one 32-bit word, tables t0..t2 (2048 entries each)
-__device__ __forceinline__ uint32_t crc_word3(const uint32_t *t, uint32_t x, const ChunkMul &m) {
+// crc of the three chunks of one 32-bit word, tables at t, t+8K, t+16K
+__device__ __forceinline__ uint32_t crc_word3(uint32_t t, uint32_t x, const ChunkMul &m) {
     const uint32_t o0 = __umulhi(x * m.m21, m.m13);    // (x & 0x7ff) << 2
     const uint32_t o1 = __umulhi(x, m.m23) & 0x1ffcu;   // ((x >> 11) & 0x7ff) << 2
     const uint32_t o2 = __umulhi(x, m.m10) * m.m4;      // (x >> 22) << 2
-    return lds_u32(t, o0) ^ lds_u32(t + 2048, o1) ^ lds_u32(t + 4096, o2);
+    return lds_u32(t + o0) ^ lds_u32(t + 8192 + o1) ^ lds_u32(t + 16384 + o2);
 }
 
 template <int NC>
-__device__ __forceinline__ uint32_t crc_chunks(const uint32_t *tab, uint64_t w, const ChunkMul &m) {
+__device__ __forceinline__ uint32_t crc_chunks(uint32_t tab, uint64_t w, const ChunkMul &m) {
     uint32_t c = crc_word3(tab, (uint32_t)w, m);
     if constexpr (NC > 3) {
         const uint32_t hi = (uint32_t)(w >> 32);
-        c ^= lds_u32(tab + 3 * 2048, __umulhi(hi * m.m21, m.m13));
-        if constexpr (NC > 4) c ^= lds_u32(tab + 4 * 2048, __umulhi(hi, m.m23) & 0x1ffcu);
-        if constexpr (NC > 5) c ^= lds_u32(tab + 5 * 2048, __umulhi(hi, m.m10) * m.m4);
+        c ^= lds_u32(tab + 3 * 8192 + __umulhi(hi * m.m21, m.m13));
+        if constexpr (NC > 4) c ^= lds_u32(tab + 4 * 8192 + (__umulhi(hi, m.m23) & 0x1ffcu));
+        if constexpr (NC > 5) c ^= lds_u32(tab + 5 * 8192 + __umulhi(hi, m.m10) * m.m4);
     }
     return c;
 }
@@ -301,10 +309,10 @@ struct HashCrc {
         else if constexpr (NC <= 5) return mod_fp<R>(c0, c0 ^ p.k01, u52_to_f64(r));
         else return mod_int(c0, c0 ^ p.k01, r);
     }
-    __device__ __forceinline__ static uint32_t crc(const uint32_t *tab, uint64_t w, const DevParams &p) {
+    __device__ __forceinline__ static uint32_t crc(uint32_t tab, uint64_t w, const DevParams &p) {
         return crc_chunks<kChunks>(tab, w, p.cm);
     }
-    __device__ __forceinline__ static R probe(const uint32_t *tab, R r, const DevParams &p) {
+    __device__ __forceinline__ static R probe(uint32_t tab, R r, const DevParams &p) {
         return from_crc(crc(tab, r, p), r, p);
     }
 };
@@ -317,7 +325,7 @@ struct HashCrcBytes {
     static constexpr int kTableWords = 8 * 256;
     using R = uint64_t;
     __device__ __forceinline__ static void build(uint32_t *tab, uint32_t k0) { build_byte_tables(tab, 8, k0); }
-    __device__ __forceinline__ static R probe(const uint32_t *tab, R r, const DevParams &p) {
+    __device__ __forceinline__ static R probe(uint32_t tab, R r, const DevParams &p) {
         const uint32_t c0 = crc_bytes<8>(tab, r);
         return mod_int(c0, c0 ^ p.k01, r);
     }
@@ -331,10 +339,18 @@ struct HashSimple {
     static constexpr int kTableWords = 0;
     using R = typename std::conditional<NARROW, uint32_t, uint64_t>::type;
     __device__ __forceinline__ static void build(uint32_t *, uint32_t) {}
-    __device__ __forceinline__ static R probe(const uint32_t *, R r, const DevParams &p) {
+    __device__ __forceinline__ static R probe(uint32_t, R r, const DevParams &p) {
         return (R)__umul64hi((uint64_t)r * p.mult, (uint64_t)r);
     }
 };
+
+// Full-warp ballot (callers guarantee convergence).
+__device__ __forceinline__ unsigned ballot_all(bool pred) {
+    unsigned m;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\tvote.sync.ballot.b32 %0, q, 0xffffffff;\n\t}"
+                 : "=r"(m) : "r"((unsigned)pred));
+    return m;
+}
 
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned m;

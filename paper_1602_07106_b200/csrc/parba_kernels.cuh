@@ -113,12 +113,13 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
     using R = typename Hash::R;
     constexpr bool NARROW = Hash::kNarrow;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    uint32_t *tabs = reinterpret_cast<uint32_t *>(smem_raw);
-    uint32_t *clow_s = tabs + Hash::kTableWords;  // crc(0, 2j+1), j < kTile (2j+1 < 512)
+    uint32_t *tabs_p = reinterpret_cast<uint32_t *>(smem_raw);
+    uint32_t *clow_s = tabs_p + Hash::kTableWords;  // crc(0, 2j+1), j < kTile (2j+1 < 512)
+    const uint32_t tabs = smem_addr(tabs_p);
     WarpSmem<SINK, R> *wsm = reinterpret_cast<WarpSmem<SINK, R> *>(
         smem_raw + (Hash::kHasCrc ? (Hash::kTableWords + kTile) * 4 : 0));
     if constexpr (Hash::kHasCrc) {
-        Hash::build(tabs, p.k0);
+        Hash::build(tabs_p, p.k0);
         for (int j = threadIdx.x; j < kTile; j += blockDim.x)
             clow_s[j] = crc32c_u64_bitwise(0u, 2u * (uint32_t)j + 1u);
     }
@@ -132,7 +133,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
     const uint64_t gw = (uint64_t)blockIdx.x * wpc + wib;
     const uint64_t nw = (uint64_t)gridDim.x * wpc;
 
-    int act = 0;                  // lane holds a running chain
+    uint32_t act = 0;             // 1: lane holds a running chain
     R r = 0;
     uint32_t slot = 0;
     uint32_t head = 0, tail = 0;  // queue cursors (warp-uniform)
@@ -179,10 +180,12 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
     auto step = [&]() {
         const R nr = Hash::probe(tabs, r, p);
         probes += (uint32_t)act;
-        const bool fin = act && is_done(nr);
+        uint32_t cont = (uint32_t)nr & 1u;  // odd: the chain continues
+        if constexpr (SEED) cont &= (uint64_t)nr >= p.stop ? 1u : 0u;
+        const uint32_t fin = act & (cont ^ 1u);
+        act &= cont;
         r = nr;
         if (fin) finish<NARROW, SEED, SINK>(w, slot, (uint64_t)nr, p, a);
-        act = act && !fin;
     };
 
     // First probe of every edge of a tile (FULL: interior tile, no bounds test).
@@ -201,7 +204,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
             if constexpr (SINK == kStore) w.stage[buf][j] = r1;  // final unless pending
             if constexpr (SINK != kStore) if (valid && done) finish<NARROW, SEED, SINK>(w, buf * kTile + j, (uint64_t)r1, p, a);
             const bool pend = valid && !done;
-            const unsigned m = __ballot_sync(0xffffffffu, pend);
+            const unsigned m = ballot_all(pend);
             if (pend) {
                 const uint32_t pos = (tail + __popc(m & ltmask)) & (kTile - 1);
                 if constexpr (SINK == kStore) {
@@ -230,7 +233,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
         __syncwarp();
         // ---- phase 2: drain the queue with lane refill
         while (tail != head) {
-            const unsigned idle = __ballot_sync(0xffffffffu, !act);
+            const unsigned idle = ballot_all(!act);
             const uint32_t avail = tail - head;
             const uint32_t rank = __popc(idle & ltmask);
             if (!act && rank < avail) {
@@ -287,9 +290,10 @@ __global__ void __launch_bounds__(256)
 chains_kernel(DevParams p, const uint64_t *__restrict__ r0, uint64_t count, uint64_t stop,
               uint64_t *__restrict__ out, const uint64_t *__restrict__ ids,
               uint64_t *__restrict__ pairs, unsigned long long *probes_out) {
-    __shared__ uint32_t tabs[Hash::kTableWords > 0 ? Hash::kTableWords : 1];
-    Hash::build(tabs, p.k0);
+    __shared__ uint32_t tabs_p[Hash::kTableWords > 0 ? Hash::kTableWords : 1];
+    Hash::build(tabs_p, p.k0);
     __syncthreads();
+    const uint32_t tabs = smem_addr(tabs_p);
     unsigned long long probes = 0;
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count;
          k += (uint64_t)gridDim.x * blockDim.x) {
@@ -314,9 +318,10 @@ chains_kernel(DevParams p, const uint64_t *__restrict__ r0, uint64_t count, uint
 template <class Hash>
 __global__ void __launch_bounds__(256)
 hash_kernel(DevParams p, const uint64_t *__restrict__ r, uint64_t count, uint64_t *__restrict__ out) {
-    __shared__ uint32_t tabs[Hash::kTableWords > 0 ? Hash::kTableWords : 1];
-    Hash::build(tabs, p.k0);
+    __shared__ uint32_t tabs_p[Hash::kTableWords > 0 ? Hash::kTableWords : 1];
+    Hash::build(tabs_p, p.k0);
     __syncthreads();
+    const uint32_t tabs = smem_addr(tabs_p);
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count;
          k += (uint64_t)gridDim.x * blockDim.x)
         out[k] = Hash::probe(tabs, r[k], p);
