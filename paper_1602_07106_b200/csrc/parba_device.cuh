@@ -255,6 +255,42 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
     return v;
 }
+__device__ __forceinline__ uint64_t lds_u64(uint32_t addr) {
+    uint64_t v;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint16_t lds_u16(uint32_t addr) {
+    uint16_t v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" :: "r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts_u64(uint32_t addr, uint64_t v) {
+    asm volatile("st.shared.u64 [%0], %1;" :: "r"(addr), "l"(v) : "memory");
+}
+__device__ __forceinline__ void sts_u16(uint32_t addr, uint16_t v) {
+    asm volatile("st.shared.u16 [%0], %1;" :: "r"(addr), "h"(v) : "memory");
+}
+// Loop-invariant value the compiler must keep in a register (it would
+// otherwise rematerialise shared-window bases inside the hot loop).
+__device__ __forceinline__ uint32_t opaque(uint32_t x) {
+    uint32_t y;
+    asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
+    return y;
+}
+template <class T>
+__device__ __forceinline__ T lds_t(uint32_t addr) {
+    if constexpr (sizeof(T) == 4) return (T)lds_u32(addr);
+    else return (T)lds_u64(addr);
+}
+template <class T>
+__device__ __forceinline__ void sts_t(uint32_t addr, T v) {
+    if constexpr (sizeof(T) == 4) sts_u32(addr, (uint32_t)v);
+    else sts_u64(addr, (uint64_t)v);
+}
 
 template <int NB>
 __device__ __forceinline__ uint32_t crc_bytes(uint32_t tab, uint64_t w) {

@@ -87,12 +87,11 @@ constexpr size_t tile_smem_per_warp() {
 constexpr uint64_t kValueMask = (1ull << 55) - 1;
 
 // A chain finished with terminal value r: hand its target to the sink.
-template <bool NARROW, bool SEED, int SINK, class W>
-__device__ __forceinline__ void finish(W &w, uint32_t slot, uint64_t r, const DevParams &p,
+template <bool NARROW, bool SEED, int SINK, class R>
+__device__ __forceinline__ void finish(uint32_t stage_s, uint32_t slot, uint64_t r, const DevParams &p,
                                        const SinkArgs &a) {
     if constexpr (SINK == kStore) {
-        using RS = std::remove_reference_t<decltype(w.stage[0][0])>;
-        (&w.stage[0][0])[slot] = (RS)r;  // target computed at flush, all lanes busy
+        sts_t<R>(stage_s + slot * (uint32_t)sizeof(R), (R)r);  // target computed at flush, all lanes busy
     } else if constexpr (SINK == kWindow) {
         if (SEED && r < p.stop) {
             const uint64_t t = __ldg(p.seed + r);
@@ -115,7 +114,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint32_t *tabs_p = reinterpret_cast<uint32_t *>(smem_raw);
     uint32_t *clow_s = tabs_p + Hash::kTableWords;  // crc(0, 2j+1), j < kTile (2j+1 < 512)
-    const uint32_t tabs = smem_addr(tabs_p);
+    const uint32_t tabs = opaque(smem_addr(tabs_p));
     WarpSmem<SINK, R> *wsm = reinterpret_cast<WarpSmem<SINK, R> *>(
         smem_raw + (Hash::kHasCrc ? (Hash::kTableWords + kTile) * 4 : 0));
     if constexpr (Hash::kHasCrc) {
@@ -129,6 +128,15 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
     const int wib = threadIdx.x >> 5;
     const int wpc = blockDim.x >> 5;  // warps per CTA (<= kWarps; fewer when smem is tight)
     WarpSmem<SINK, R> &w = wsm[wib];
+    // shared-window addresses of this warp's queue and stage (kept in registers)
+    uint32_t qe_s, qs_s = 0, stage_s = 0;
+    if constexpr (SINK == kStore) {
+        qe_s = opaque(smem_addr(&w.qe[0]));
+        qs_s = opaque(smem_addr(&w.qs[0]));
+        stage_s = opaque(smem_addr(&w.stage[0][0]));
+    } else {
+        qe_s = opaque(smem_addr(&w.qr[0]));
+    }
     const unsigned ltmask = lanemask_lt();
     const uint64_t gw = (uint64_t)blockIdx.x * wpc + wib;
     const uint64_t nw = (uint64_t)gridDim.x * wpc;
@@ -159,7 +167,8 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
                 const uint32_t j = lane + 32u * k;
                 const uint64_t i = base + j;
                 if (FULL || (i >= lo && i < hi)) {
-                    const uint64_t tgt = target_of<NARROW, SEED>((uint64_t)w.stage[b][j], p);
+                    const uint64_t tgt = target_of<NARROW, SEED>(
+                        (uint64_t)lds_t<R>(stage_s + (b * kTile + j) * (uint32_t)sizeof(R)), p);
                     __stcs(o + j, make_ulonglong2(source_of<NARROW, SEED>(i, p), tgt));
                 }
             }
@@ -185,7 +194,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
         const uint32_t fin = act & (cont ^ 1u);
         act &= cont;
         r = nr;
-        if (fin) finish<NARROW, SEED, SINK>(w, slot, (uint64_t)nr, p, a);
+        if (fin) finish<NARROW, SEED, SINK, R>(stage_s, slot, (uint64_t)nr, p, a);
     };
 
     // First probe of every edge of a tile (FULL: interior tile, no bounds test).
@@ -201,21 +210,22 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
             if constexpr (Hash::kHasCrc) r1 = Hash::from_crc(cb ^ clow_s[j], r0, p);
             else r1 = Hash::probe(tabs, r0, p);
             const bool done = is_done(r1);
-            if constexpr (SINK == kStore) w.stage[buf][j] = r1;  // final unless pending
-            if constexpr (SINK != kStore) if (valid && done) finish<NARROW, SEED, SINK>(w, buf * kTile + j, (uint64_t)r1, p, a);
+            if constexpr (SINK == kStore)  // final unless pending
+                sts_t<R>(stage_s + (buf * kTile + j) * (uint32_t)sizeof(R), r1);
+            if constexpr (SINK != kStore) if (valid && done) finish<NARROW, SEED, SINK, R>(stage_s, buf * kTile + j, (uint64_t)r1, p, a);
             const bool pend = valid && !done;
             const unsigned m = ballot_all(pend);
             if (pend) {
                 const uint32_t pos = (tail + __popc(m & ltmask)) & (kTile - 1);
                 if constexpr (SINK == kStore) {
                     if constexpr (Hash::kPack) {
-                        w.qe[pos] = ((uint64_t)(buf * kTile + j) << 55) | (uint64_t)r1;
+                        sts_u64(qe_s + pos * 8, ((uint64_t)(buf * kTile + j) << 55) | (uint64_t)r1);
                     } else {
-                        w.qe[pos] = (uint64_t)r1;
-                        w.qs[pos] = (uint16_t)(buf * kTile + j);
+                        sts_u64(qe_s + pos * 8, (uint64_t)r1);
+                        sts_u16(qs_s + pos * 2, (uint16_t)(buf * kTile + j));
                     }
                 } else {
-                    w.qr[pos] = r1;
+                    sts_t<R>(qe_s + pos * (uint32_t)sizeof(R), r1);
                 }
             }
             tail += __popc(m);
@@ -239,16 +249,16 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
             if (!act && rank < avail) {
                 const uint32_t pos = (head + rank) & (kTile - 1);
                 if constexpr (SINK == kStore) {
-                    const uint64_t e = w.qe[pos];
+                    const uint64_t e = lds_u64(qe_s + pos * 8);
                     if constexpr (Hash::kPack) {
                         r = (R)(e & kValueMask);
                         slot = (uint32_t)(e >> 55);
                     } else {
                         r = (R)e;
-                        slot = w.qs[pos];
+                        slot = lds_u16(qs_s + pos * 2);
                     }
                 } else {
-                    r = w.qr[pos];
+                    r = lds_t<R>(qe_s + pos * (uint32_t)sizeof(R));
                 }
                 act = 1;
             }
@@ -293,7 +303,7 @@ chains_kernel(DevParams p, const uint64_t *__restrict__ r0, uint64_t count, uint
     __shared__ uint32_t tabs_p[Hash::kTableWords > 0 ? Hash::kTableWords : 1];
     Hash::build(tabs_p, p.k0);
     __syncthreads();
-    const uint32_t tabs = smem_addr(tabs_p);
+    const uint32_t tabs = opaque(smem_addr(tabs_p));
     unsigned long long probes = 0;
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count;
          k += (uint64_t)gridDim.x * blockDim.x) {
@@ -321,7 +331,7 @@ hash_kernel(DevParams p, const uint64_t *__restrict__ r, uint64_t count, uint64_
     __shared__ uint32_t tabs_p[Hash::kTableWords > 0 ? Hash::kTableWords : 1];
     Hash::build(tabs_p, p.k0);
     __syncthreads();
-    const uint32_t tabs = smem_addr(tabs_p);
+    const uint32_t tabs = opaque(smem_addr(tabs_p));
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count;
          k += (uint64_t)gridDim.x * blockDim.x)
         out[k] = Hash::probe(tabs, r[k], p);
