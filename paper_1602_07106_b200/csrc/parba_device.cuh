@@ -124,11 +124,21 @@ __device__ __forceinline__ uint64_t target_of(uint64_t r, const DevParams &p) {
 // ---------------------------------------------------------------------------
 // Exact remainder.
 
+// Exact integer -> double (I2F.F64: one instruction, measured slightly faster
+// on B200 than the 0x4330... magic-exponent trick, which needs a MOV + DADD).
 __device__ __forceinline__ double u32_to_f64(uint32_t x) {
+#ifdef PARBA_MAGIC_CVT
     return __hiloint2double(0x43300000, (int)x) - 0x1p52;
+#else
+    return __uint2double_rn(x);
+#endif
 }
 __device__ __forceinline__ double u52_to_f64(uint64_t x) {  // x < 2^52
+#ifdef PARBA_MAGIC_CVT
     return __longlong_as_double((long long)(x | 0x4330000000000000ull)) - 0x1p52;
+#else
+    return __ull2double_rn(x);
+#endif
 }
 
 // hi:lo -> nearest double (one rounding).
