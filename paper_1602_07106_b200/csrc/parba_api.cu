@@ -77,6 +77,7 @@ DevParams make_dev(const parba_params_t *p, uint64_t K = 0) {
     d.cm = ChunkMul{1u << 21, 1u << 13, 1u << 23, 1u << 10, 4u};
     d.div64 = make_magic64(p->d);
     d.div32 = make_magic32(p->d);
+    d.div32_2d = make_magic32(2 * p->d);
     d.K = K;
     // generated target ((r>>1) - m0)/d + n0 < K  <=>  r < 2*(m0 + (K - n0)*d)
     if (K <= p->n0) {

@@ -95,7 +95,8 @@ struct DevParams {
     uint32_t k0, k01;      // crc(s0,0) and crc(s0,0)^crc(s1,0): h = (c0<<32)|(c0^k01)
     const uint64_t *seed;  // 2*m0 seed endpoints (device)
     Magic64 div64;         // by d (wide)
-    Magic32 div32;         // by d (narrow: positions < 2^32)
+    Magic32 div32;         // by d (narrow: positions < 2^31)
+    Magic32 div32_2d;      // by 2d (every r < 2^31: target = (r - 2m0) / 2d + n0)
     uint64_t win_rlim;     // window mode: generated target < K  <=>  r < win_rlim
     uint32_t win_rlim32;   // min(win_rlim, 2^32 - 1) for narrow launches
     uint64_t K;
@@ -113,10 +114,16 @@ __device__ __forceinline__ uint64_t source_of(uint64_t i, const DevParams &p) {
         else return magic_div(i, p.div64);
     }
 }
-template <bool NARROW, bool SEED>
+// R31: every chain value < 2^31, so floor(((r>>1) - m0)/d) = floor((r - 2m0)/(2d))
+// is one 32-bit multiply-high division.
+template <bool NARROW, bool SEED, bool R31 = false>
 __device__ __forceinline__ uint64_t target_of(uint64_t r, const DevParams &p) {
     if constexpr (SEED) {
         if (r < p.stop) return __ldg(p.seed + r);
+    }
+    if constexpr (R31) {
+        if constexpr (SEED) return (uint64_t)magic_div32((uint32_t)(r - p.stop), p.div32_2d) + p.n0;
+        else return (uint64_t)magic_div32((uint32_t)r, p.div32_2d);
     }
     return source_of<NARROW, SEED>(r >> 1, p);
 }
@@ -281,6 +288,10 @@ __device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) {
 __device__ __forceinline__ void sts_u64(uint32_t addr, uint64_t v) {
     asm volatile("st.shared.u64 [%0], %1;" :: "r"(addr), "l"(v) : "memory");
 }
+__device__ __forceinline__ void sts_u64_if(bool pred, uint32_t addr, uint64_t v) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q st.shared.u64 [%1], %2;\n\t}"
+                 :: "r"((unsigned)pred), "r"(addr), "l"(v) : "memory");
+}
 __device__ __forceinline__ void sts_u16(uint32_t addr, uint16_t v) {
     asm volatile("st.shared.u16 [%0], %1;" :: "r"(addr), "h"(v) : "memory");
 }
@@ -345,6 +356,7 @@ struct HashCrc {
     static constexpr bool kHasCrc = true;
     static constexpr int kChunks = NC < 3 ? 3 : NC;
     static constexpr bool kNarrow = NC <= 3;
+    static constexpr bool kR31 = NC == 2;
     static constexpr bool kPack = NC <= 5;       // every value < 2^52
     static constexpr int kTableWords = kChunks * 2048;
     using R = typename std::conditional<kNarrow, uint32_t, uint64_t>::type;
@@ -367,6 +379,7 @@ struct HashCrc {
 struct HashCrcBytes {
     static constexpr bool kHasCrc = true;
     static constexpr bool kNarrow = false;
+    static constexpr bool kR31 = false;
     static constexpr bool kPack = false;
     static constexpr int kTableWords = 8 * 256;
     using R = uint64_t;
@@ -381,6 +394,7 @@ template <bool NARROW>
 struct HashSimple {
     static constexpr bool kHasCrc = false;
     static constexpr bool kNarrow = NARROW;
+    static constexpr bool kR31 = false;
     static constexpr bool kPack = NARROW;
     static constexpr int kTableWords = 0;
     using R = typename std::conditional<NARROW, uint32_t, uint64_t>::type;

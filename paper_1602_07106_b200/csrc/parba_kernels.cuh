@@ -167,7 +167,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
                 const uint32_t j = lane + 32u * k;
                 const uint64_t i = base + j;
                 if (FULL || (i >= lo && i < hi)) {
-                    const uint64_t tgt = target_of<NARROW, SEED>(
+                    const uint64_t tgt = target_of<NARROW, SEED, Hash::kR31>(
                         (uint64_t)lds_t<R>(stage_s + (b * kTile + j) * (uint32_t)sizeof(R)), p);
                     __stcs(o + j, make_ulonglong2(source_of<NARROW, SEED>(i, p), tgt));
                 }
@@ -215,11 +215,15 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
             if constexpr (SINK != kStore) if (valid && done) finish<NARROW, SEED, SINK, R>(stage_s, buf * kTile + j, (uint64_t)r1, p, a);
             const bool pend = valid && !done;
             const unsigned m = ballot_all(pend);
-            if (pend) {
+            if constexpr (SINK == kStore && Hash::kPack) {
+                // predicated store, no branch: (slot << 55) | value
+                const uint32_t pos = (tail + __popc(m & ltmask)) & (kTile - 1);
+                const uint32_t slot_hi = ((buf * kTile + j) << 23);
+                sts_u64_if(pend, qe_s + pos * 8, ((uint64_t)slot_hi << 32) | (uint64_t)r1);
+            } else if (pend) {
                 const uint32_t pos = (tail + __popc(m & ltmask)) & (kTile - 1);
                 if constexpr (SINK == kStore) {
                     if constexpr (Hash::kPack) {
-                        sts_u64(qe_s + pos * 8, ((uint64_t)(buf * kTile + j) << 55) | (uint64_t)r1);
                     } else {
                         sts_u64(qe_s + pos * 8, (uint64_t)r1);
                         sts_u16(qs_s + pos * 2, (uint16_t)(buf * kTile + j));
