@@ -292,6 +292,15 @@ __device__ __forceinline__ void sts_u64_if(bool pred, uint32_t addr, uint64_t v)
     asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q st.shared.u64 [%1], %2;\n\t}"
                  :: "r"((unsigned)pred), "r"(addr), "l"(v) : "memory");
 }
+__device__ __forceinline__ void sts_u32_if(bool pred, uint32_t addr, uint32_t v) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q st.shared.u32 [%1], %2;\n\t}"
+                 :: "r"((unsigned)pred), "r"(addr), "r"(v) : "memory");
+}
+template <class T>
+__device__ __forceinline__ void sts_t_if(bool pred, uint32_t addr, T v) {
+    if constexpr (sizeof(T) == 4) sts_u32_if(pred, addr, (uint32_t)v);
+    else sts_u64_if(pred, addr, (uint64_t)v);
+}
 __device__ __forceinline__ void sts_u16(uint32_t addr, uint16_t v) {
     asm volatile("st.shared.u16 [%0], %1;" :: "r"(addr), "h"(v) : "memory");
 }

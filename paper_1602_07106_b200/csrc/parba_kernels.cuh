@@ -215,22 +215,18 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
             if constexpr (SINK != kStore) if (valid && done) finish<NARROW, SEED, SINK, R>(stage_s, buf * kTile + j, (uint64_t)r1, p, a);
             const bool pend = valid && !done;
             const unsigned m = ballot_all(pend);
-            if constexpr (SINK == kStore && Hash::kPack) {
-                // predicated store, no branch: (slot << 55) | value
-                const uint32_t pos = (tail + __popc(m & ltmask)) & (kTile - 1);
-                const uint32_t slot_hi = ((buf * kTile + j) << 23);
-                sts_u64_if(pend, qe_s + pos * 8, ((uint64_t)slot_hi << 32) | (uint64_t)r1);
-            } else if (pend) {
-                const uint32_t pos = (tail + __popc(m & ltmask)) & (kTile - 1);
-                if constexpr (SINK == kStore) {
-                    if constexpr (Hash::kPack) {
-                    } else {
-                        sts_u64(qe_s + pos * 8, (uint64_t)r1);
-                        sts_u16(qs_s + pos * 2, (uint16_t)(buf * kTile + j));
-                    }
-                } else {
-                    sts_t<R>(qe_s + pos * (uint32_t)sizeof(R), r1);
+            const uint32_t pos = (tail + __popc(m & ltmask)) & (kTile - 1);
+            if constexpr (SINK == kStore) {
+                if constexpr (Hash::kPack) {
+                    // predicated store, no branch: (slot << 55) | value
+                    const uint32_t slot_hi = ((buf * kTile + j) << 23);
+                    sts_u64_if(pend, qe_s + pos * 8, ((uint64_t)slot_hi << 32) | (uint64_t)r1);
+                } else if (pend) {
+                    sts_u64(qe_s + pos * 8, (uint64_t)r1);
+                    sts_u16(qs_s + pos * 2, (uint16_t)(buf * kTile + j));
                 }
+            } else {
+                sts_t_if<R>(pend, qe_s + pos * (uint32_t)sizeof(R), r1);
             }
             tail += __popc(m);
             probes += valid ? 1u : 0u;
