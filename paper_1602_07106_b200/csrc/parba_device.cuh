@@ -131,8 +131,21 @@ __device__ __forceinline__ uint64_t target_of(uint64_t r, const DevParams &p) {
 // ---------------------------------------------------------------------------
 // Exact remainder.
 
-// Exact integer -> double (I2F.F64: one instruction, measured slightly faster
-// on B200 than the 0x4330... magic-exponent trick, which needs a MOV + DADD).
+// Exact integer -> double: I2F.F64 (one XU instruction) or the magic-exponent
+// trick (MOV + DADD on the FP64 pipe).  The mix used by mod_fp31 is a tuning
+// knob (PARBA_CVT31, bit k = operand k via magic: 1 r, 2 hhi, 4 hlo).
+__device__ __forceinline__ double u32_to_f64_magic(uint32_t x) {
+    return __hiloint2double(0x43300000, (int)x) - 0x1p52;
+}
+__device__ __forceinline__ double u32_to_f64_i2f(uint32_t x) { return __uint2double_rn(x); }
+#ifndef PARBA_CVT31
+#define PARBA_CVT31 6
+#endif
+template <int BIT>
+__device__ __forceinline__ double cvt31(uint32_t x) {
+    if constexpr ((PARBA_CVT31 >> BIT) & 1) return u32_to_f64_magic(x);
+    else return u32_to_f64_i2f(x);
+}
 __device__ __forceinline__ double u32_to_f64(uint32_t x) {
 #ifdef PARBA_MAGIC_CVT
     return __hiloint2double(0x43300000, (int)x) - 0x1p52;
@@ -199,12 +212,12 @@ __device__ __forceinline__ R mod_fp(uint32_t hhi, uint32_t hlo, double rd) {
 // the low word of fma(v, y, 1.5*2^52) (two's complement for negative qb).
 // 10 FP64 instructions + 1 IMAD + 2 ALU, no FP64 -> integer conversion.
 __device__ __forceinline__ uint32_t mod_fp31(uint32_t hhi, uint32_t hlo, uint32_t r) {
-    const double rd = u32_to_f64(r);
+    const double rd = cvt31<0>(r);
     const double y = recip_approx(rd);
-    const double ha = u32_to_f64(hhi);
+    const double ha = cvt31<1>(hhi);
     const double qa = fma(ha, y, 0x1.8p52) - 0x1.8p52;
     const double x = fma(-qa, rd, ha);                          // exact, in [-r, r)
-    const double v = fma(x, 0x1p32, u32_to_f64(hlo));           // ~ x*2^32 + hlo
+    const double v = fma(x, 0x1p32, cvt31<2>(hlo));             // ~ x*2^32 + hlo
     const uint32_t qb = (uint32_t)__double2loint(fma(v, y, 0x1.8p52));
     const uint32_t t = hlo - qb * r;                            // exact mod 2^32
     return min(t, t + r);
