@@ -35,6 +35,7 @@
 namespace parba {
 
 constexpr int kTile = 256;                 // edges per warp tile (power of two)
+constexpr int kQueue = 512;                // per-warp pending ring (>= kTile + 31)
 constexpr int kEpl = kTile / 32;           // edges per lane in phase 1
 #ifndef PARBA_WARPS
 #define PARBA_WARPS 32
@@ -62,17 +63,17 @@ struct SinkArgs {
 // (Hash::kPack); otherwise the slot goes to a separate u16 ring.
 template <int SINK, class R>
 struct WarpSmem {
-    uint64_t qe[kTile];        // pending (slot << 55) | value   (ring)
-    uint16_t qs[kTile];        // pending slots when !kPack
+    uint64_t qe[kQueue];       // pending (slot << 55) | value   (ring)
+    uint16_t qs[kQueue];       // pending slots when !kPack
     R stage[2][kTile];         // terminal chain values of the two tiles in flight
 };
 template <class R>
 struct WarpSmem<kWindow, R> {
-    R qr[kTile];
+    R qr[kQueue];
 };
 template <class R>
 struct WarpSmem<kFull, R> {
-    R qr[kTile];
+    R qr[kQueue];
 };
 
 // Dynamic shared memory: [CRC tables][crc(0,2j+1) table][per-warp state].
@@ -145,6 +146,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
     R r = 0;
     uint32_t slot = 0;
     uint32_t head = 0, tail = 0;  // queue cursors (warp-uniform)
+    uint32_t tile_q0 = 0;         // queue cursor at the start of the current tile
     uint32_t probes = 0;          // per lane (< 2^32 per launch and lane)
     uint64_t prev_base = 0;
     bool have_prev = false;
@@ -197,6 +199,33 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
         if (fin) finish<NARROW, SEED, SINK, R>(stage_s, slot, (uint64_t)nr, p, a);
     };
 
+    // Pop queued chains into idle lanes.  FULLQ: at least 32 entries queued,
+    // so every idle lane takes one (no availability test).
+    auto refill = [&](auto fullq_c) {
+        constexpr bool FULLQ = decltype(fullq_c)::value;
+        const unsigned idle = ballot_all(!act);
+        const uint32_t rank = __popc(idle & ltmask);
+        const uint32_t avail = tail - head;
+        if (!act && (FULLQ || rank < avail)) {
+            const uint32_t pos = (head + rank) & (kQueue - 1);
+            if constexpr (SINK == kStore) {
+                const uint64_t e = lds_u64(qe_s + pos * 8);
+                if constexpr (Hash::kPack) {
+                    r = (R)(e & kValueMask);
+                    slot = (uint32_t)(e >> 55);
+                } else {
+                    r = (R)e;
+                    slot = lds_u16(qs_s + pos * 2);
+                }
+            } else {
+                r = lds_t<R>(qe_s + pos * (uint32_t)sizeof(R));
+            }
+            act = 1;
+        }
+        if constexpr (FULLQ) head += (uint32_t)__popc(idle);
+        else head += min((uint32_t)__popc(idle), avail);
+    };
+
     // First probe of every edge of a tile (FULL: interior tile, no bounds test).
     auto phase1 = [&](auto full_c, uint64_t base, uint32_t cb) {
         constexpr bool FULL = decltype(full_c)::value;
@@ -215,7 +244,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
             if constexpr (SINK != kStore) if (valid && done) finish<NARROW, SEED, SINK, R>(stage_s, buf * kTile + j, (uint64_t)r1, p, a);
             const bool pend = valid && !done;
             const unsigned m = ballot_all(pend);
-            const uint32_t pos = (tail + __popc(m & ltmask)) & (kTile - 1);
+            const uint32_t pos = (tail + __popc(m & ltmask)) & (kQueue - 1);
             if constexpr (SINK == kStore) {
                 if constexpr (Hash::kPack) {
                     // predicated store, no branch: (slot << 55) | value
@@ -236,39 +265,29 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
     for (uint64_t t = gw; t < ntiles; t += nw) {
         const uint64_t base = (tile0 + t) * kTile;
         // ---- phase 1: first probe of all edges of the tile
+        tile_q0 = tail;  // queue position where this tile's entries start
         uint32_t cb = 0;
         if constexpr (Hash::kHasCrc) cb = Hash::crc(tabs, 2 * base, p);
         if (base >= lo && base + kTile <= hi) phase1(std::true_type{}, base, cb);
         else phase1(std::false_type{}, base, cb);
         __syncwarp();
-        // ---- phase 2: drain the queue with lane refill
-        while (tail != head) {
-            const unsigned idle = ballot_all(!act);
-            const uint32_t avail = tail - head;
-            const uint32_t rank = __popc(idle & ltmask);
-            if (!act && rank < avail) {
-                const uint32_t pos = (head + rank) & (kTile - 1);
-                if constexpr (SINK == kStore) {
-                    const uint64_t e = lds_u64(qe_s + pos * 8);
-                    if constexpr (Hash::kPack) {
-                        r = (R)(e & kValueMask);
-                        slot = (uint32_t)(e >> 55);
-                    } else {
-                        r = (R)e;
-                        slot = lds_u16(qs_s + pos * 2);
-                    }
-                } else {
-                    r = lds_t<R>(qe_s + pos * (uint32_t)sizeof(R));
-                }
-                act = 1;
-            }
-            head += min((uint32_t)__popc(idle), avail);
+        // ---- phase 2: pop queued chains into idle lanes and probe while at
+        // least a full warp of entries is queued (the < 32 newest entries
+        // carry over to the next tile, so every refill can fill every idle lane)
+        while (tail - head >= 32u) {
+            refill(std::true_type{});
             step();
         }
         // ---- store: flush the previous tile once none of its chains runs
         if constexpr (SINK == kStore) {
             if (have_prev) {
                 const uint32_t pb = buf ^ 1u;
+                // entries of the previous tile still queued (only when this
+                // tile pushed fewer than 32): pop them first
+                while ((int32_t)(tile_q0 - head) > 0) {
+                    refill(std::false_type{});
+                    step();
+                }
                 while (__any_sync(0xffffffffu, act && (slot / kTile) == pb)) step();
                 flush(pb, prev_base);
             }
@@ -277,7 +296,11 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
             buf ^= 1u;
         }
     }
-    // ---- drain the chains still running, then flush the last tile
+    // ---- drain the queue and the chains still running, then flush the last tile
+    while (tail != head) {
+        refill(std::false_type{});
+        step();
+    }
     while (__any_sync(0xffffffffu, act)) step();
     if constexpr (SINK == kStore) {
         if (have_prev) flush(buf ^ 1u, prev_base);
