@@ -35,7 +35,7 @@ from .driver import (
     plan_batches,
     run,
 )
-from . import parallel
+from . import io, parallel
 from .errors import GenerationError, InfeasibleTargetsError, ParameterError, SeedGraphFormatError
 from .generator import (
     MAX_EDGES,
@@ -51,6 +51,7 @@ from .generator import (
     resolve_chain,
     resolve_chain_block,
 )
+from .io import EdgeFileWriter, write_edges_binary
 from .hashing import DEFAULT_MULTIPLIER, HashConfig, HashKind, h_crc, h_simple, hash_many, hash_value
 from .oracle_compat import bb_generate, edge_list
 
@@ -58,7 +59,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "Batch", "BinRatio", "ChainResult", "CollectConsumer", "Consumer", "DEFAULT_BATCH_SIZE",
-    "DEFAULT_MULTIPLIER", "DegreeCountConsumer", "DegreeCounter", "DiscardConsumer", "Edge",
+    "DEFAULT_MULTIPLIER", "DegreeCountConsumer", "EdgeFileWriter", "write_edges_binary", "DegreeCounter", "DiscardConsumer", "Edge",
     "GenParams", "GenerationError", "Granularity", "HashConfig", "HashKind", "Histogram",
     "InfeasibleTargetsError", "MAX_EDGES", "ParameterError", "RunStats", "SeedGraphFormatError",
     "WorkerStats", "bb_generate", "count_block", "count_edge", "count_seed_edges", "degree_counts",

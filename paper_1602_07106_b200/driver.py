@@ -8,6 +8,8 @@ device kernels instead:
   * ``DegreeCountConsumer``  -> the fused window / full-histogram kernels
   * ``CollectConsumer``      -> store mode (device array, streamed to host)
   * ``DiscardConsumer``      -> the streaming kernel with an empty window
+  * ``io.EdgeFileWriter``    -> store mode streamed into the positional
+                                binary file (cli.py:121-145)
 
 A generic Python consumer would need every edge on the host and is not
 fused, so ``run`` raises ``ParameterError`` for it (no CPU fallback).
@@ -157,7 +159,7 @@ def run(p: GenParams, consumer: Consumer, workers: int = 1, batch_size: int = DE
     """Generate every edge of [m0, m) exactly once into a fused consumer.
 
     Returns (merged consumer result, RunStats) like driver.py:210-270."""
-    from . import analytics, parallel
+    from . import analytics, io, parallel
     from .generator import generate_block
 
     if workers < 1:
@@ -171,13 +173,35 @@ def run(p: GenParams, consumer: Consumer, workers: int = 1, batch_size: int = DE
     elif isinstance(consumer, DiscardConsumer):
         _, probes, per = parallel.degree_counts_sharded(p, 0, p.m0, p.m, device=device)
         merged = p.m - p.m0
+    elif isinstance(consumer, io.EdgeFileWriter):
+        rank, ws = parallel.world()
+        a, b = parallel.shard_range(p.m0, p.m, rank, ws)
+        if ws > 1:
+            import torch.distributed as dist
+
+            dist.barrier()  # every rank has opened (and rank 0 sized) the file
+        nbytes, probes = consumer.write_range(p, a, b, device=device)
+        per = [(rank, b - a, probes)]
+        merged = nbytes
+        if ws > 1:
+            from .generator import _device
+
+            torch, dev = _device(device)
+            t = torch.tensor([nbytes, b - a, probes], dtype=torch.int64, device=dev)
+            gathered = [torch.zeros_like(t) for _ in range(ws)]
+            dist.all_gather(gathered, t)
+            per = [(r, int(g[1].item()), int(g[2].item())) for r, g in enumerate(gathered)]
+            merged = sum(int(g[0].item()) for g in gathered)
+            probes = sum(pr for _, _, pr in per)
+            dist.barrier()  # the file is complete on return
     elif isinstance(consumer, CollectConsumer):
         merged, probes = generate_block(p.m0, p.m, p, resolution=resolution, device=device)
         per = [(0, p.m - p.m0, probes)]
     else:
         raise ParameterError(
             f"consumer {type(consumer).__name__} is not fused into the B200 path; use "
-            "DegreeCountConsumer, CollectConsumer or DiscardConsumer (there is no CPU fallback)")
+            "DegreeCountConsumer, CollectConsumer, DiscardConsumer or EdgeFileWriter "
+            "(there is no CPU fallback)")
     elapsed = time.perf_counter() - t0
     per_worker = tuple(WorkerStats(w, 1 if e else 0, e, pr, elapsed) for w, e, pr in per)
     return merged, RunStats(edges_emitted=sum(w.edges for w in per_worker),

@@ -1,0 +1,147 @@
+"""Positional binary edge files fed from the device.
+
+Reference: ``EdgeFileWriter`` / ``_pwrite_all`` (parba/cli.py:109-145): edge i
+is stored as two little-endian u64 at byte offset 16*(i - m0), so any range
+of edges can be written by any worker in any order and the file is
+byte-identical for every schedule.
+
+Here a range is generated on the GPU in chunks (the store kernel), each chunk
+is copied into a pinned host buffer while the next one is generated, and a
+writer thread ``pwrite``s the pinned buffer at the edge's file offset --
+device generation, PCIe and the file system overlap.
+"""
+
+from __future__ import annotations
+
+import os
+import queue
+import threading
+
+import numpy as np
+
+from . import _lib, driver
+from .errors import GenerationError, ParameterError
+from .generator import GenParams, _check_block, _device, _require_plain
+
+# edges per device chunk (16 B each: 64 MiB chunks, two pinned buffers)
+FILE_CHUNK_EDGES = 1 << 22
+
+
+def _pwrite_all(fd: int, data, offset: int) -> None:
+    """pwrite every byte of `data` at `offset` (cli.py:109-118)."""
+    view = memoryview(data).cast("B")
+    pos = offset
+    try:
+        while view:
+            k = os.pwrite(fd, view, pos)
+            pos += k
+            view = view[k:]
+    except OSError as e:
+        raise GenerationError(f"write failed at byte offset {pos}: {e}") from e
+
+
+class EdgeFileWriter(driver.Consumer):
+    """Positional binary writer (cli.py:121-145): edge i lands at byte offset
+    16*(i - m0).  ``create=False`` opens an existing file without truncating
+    it (other ranks of a multi-process run)."""
+
+    def __init__(self, path: str, m0: int, total_edges: int, create: bool = True):
+        if total_edges < 0:
+            raise ParameterError(f"total_edges must be >= 0, got {total_edges}")
+        self.path = path
+        self.m0 = m0
+        self.total_edges = total_edges
+        flags = os.O_RDWR | os.O_CREAT | (os.O_TRUNC if create else 0)
+        self.fd = os.open(path, flags, 0o644)
+        if create:
+            os.ftruncate(self.fd, 16 * total_edges)
+
+    def new_context(self, worker_id: int) -> int:
+        return 0
+
+    def accept_block(self, ctx: int, lo: int, edges: np.ndarray) -> int:
+        data = np.ascontiguousarray(edges, dtype="<u8")
+        _pwrite_all(self.fd, data, 16 * (lo - self.m0))
+        return ctx + data.nbytes
+
+    def merge(self, contexts) -> int:
+        return sum(contexts)
+
+    def write_range(self, p: GenParams, lo: int, hi: int, device=None) -> tuple[int, int]:
+        """Generate edges lo..hi-1 on the GPU and write them at their file
+        offsets.  Returns (bytes written, hash probes)."""
+        _check_block(lo, hi, p)
+        _require_plain(p)
+        if lo == hi:
+            return 0, 0
+        torch, dev = _device(device)
+        L = _lib.load()
+        total = hi - lo
+        chunk = min(total, FILE_CHUNK_EDGES)
+        nbuf = 2
+        work: queue.Queue = queue.Queue(maxsize=nbuf)
+        free: queue.Queue = queue.Queue()
+        errors: list[BaseException] = []
+
+        def writer():
+            while True:
+                item = work.get()
+                if item is None:
+                    return
+                k, a, n, host, ev = item
+                try:
+                    ev.synchronize()
+                    _pwrite_all(self.fd, host[: 2 * n].numpy(), 16 * (a - self.m0))
+                except BaseException as e:  # surfaced after the loop
+                    errors.append(e)
+                free.put(k)
+
+        with torch.cuda.device(dev):
+            comp = torch.cuda.current_stream(dev)
+            copy = torch.cuda.Stream(dev)
+            dbufs = [torch.empty(2 * chunk, dtype=torch.int64, device=dev) for _ in range(nbuf)]
+            hbufs = [torch.empty(2 * chunk, dtype=torch.int64, pin_memory=True) for _ in range(nbuf)]
+            for k in range(nbuf):
+                free.put(k)
+            probes = torch.zeros(1, dtype=torch.int64, device=dev)
+            cp = p._device_params(dev)
+            th = threading.Thread(target=writer, daemon=True)
+            th.start()
+            try:
+                for a in range(lo, hi, chunk):
+                    n = min(chunk, hi - a)
+                    k = free.get()  # host buffer k (and device buffer k) are free again
+                    _lib.check(L.parba_generate(cp, a, a + n, dbufs[k].data_ptr(), probes.data_ptr(),
+                                                comp.cuda_stream))
+                    made = torch.cuda.Event()
+                    made.record(comp)
+                    copy.wait_event(made)
+                    with torch.cuda.stream(copy):
+                        hbufs[k][: 2 * n].copy_(dbufs[k][: 2 * n], non_blocking=True)
+                        ev = torch.cuda.Event()
+                        ev.record(copy)
+                    work.put((k, a, n, hbufs[k], ev))
+                    if errors:
+                        break
+            finally:
+                work.put(None)
+                th.join()
+            if errors:
+                raise errors[0]
+            return 16 * total, int(probes.item())
+
+    def close(self) -> None:
+        os.close(self.fd)
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def write_edges_binary(path: str, p: GenParams, device=None) -> tuple[int, int]:
+    """Whole-graph binary file (`parba generate -o`, cli.py:279-297): edges
+    m0..m-1 at offsets 16*(i - m0).  Returns (bytes, probes)."""
+    with EdgeFileWriter(path, p.m0, p.m - p.m0) as w:
+        return w.write_range(p, p.m0, p.m, device=device)

@@ -412,3 +412,41 @@ def test_config4_full_histogram_properties():
     vals, cnt = torch.unique(c64, return_counts=True)
     h = pb.Histogram(degrees=vals.cpu().numpy(), counts=cnt.cpu().numpy())
     assert 2.6 <= pb.fit_exponent(h, xmin=32) <= 3.4
+
+
+# --------------------------------------------------------------------------- binary file writer (f2)
+
+def test_binary_file_equals_oracle_and_is_schedule_independent(tmp_path):
+    import hashlib as _h
+
+    from paper_1602_07106_b200 import io as pio
+
+    p = pb.GenParams(n=10**5, d=8)  # reference acceptance (2): n=1e5, d=8
+    want, _ = O.generate_block(_op(p), 0, p.m)
+    path = tmp_path / "edges.bin"
+    nbytes, probes = pb.write_edges_binary(str(path), p)
+    data = path.read_bytes()
+    assert nbytes == len(data) == 16 * p.m
+    assert data == np.ascontiguousarray(want, dtype="<u8").tobytes()
+    digests = {_h.sha256(data).hexdigest()}
+    old = pio.FILE_CHUNK_EDGES
+    try:
+        for chunk in (1 << 10, 12345):
+            pio.FILE_CHUNK_EDGES = chunk
+            w = pb.EdgeFileWriter(str(path), p.m0, p.m - p.m0)
+            merged, stats = pb.run(p, w, workers=4, batch_size=1 << 10)
+            w.close()
+            assert merged == 16 * p.m and stats.hash_probes == probes
+            digests.add(_h.sha256(path.read_bytes()).hexdigest())
+    finally:
+        pio.FILE_CHUNK_EDGES = old
+    assert len(digests) == 1
+    # seeded family, partial range written by two "workers" in reverse order
+    q = pb.GenParams(n=3000, d=3, n0=10, seed_edges=RING10)
+    w = pb.EdgeFileWriter(str(path), q.m0, q.m - q.m0)
+    mid = (q.m0 + q.m) // 2 + 1
+    w.write_range(q, mid, q.m)
+    w.write_range(q, q.m0, mid)
+    w.close()
+    blk, _ = O.generate_block(_op(q), q.m0, q.m)
+    assert path.read_bytes() == np.ascontiguousarray(blk, dtype="<u8").tobytes()

@@ -134,3 +134,20 @@ def test_histogram_and_fit_on_synthetic_counts():
         pb.fit_exponent(h, xmin=0)
     with pytest.raises(pb.ParameterError):
         pb.fit_exponent(pb.Histogram(np.array([5]), np.array([10])), xmin=5)
+
+
+def test_edge_file_writer_positional_semantics(tmp_path):
+    # cli.py:121-145: edge i at byte offset 16*(i - m0), file pre-sized, LE u64
+    path = tmp_path / "edges.bin"
+    w = pb.EdgeFileWriter(str(path), 3, 10)
+    ctx = w.new_context(0)
+    ctx = w.accept_block(ctx, 8, np.array([[7, 1], [7, 2]], dtype=np.uint64))
+    ctx = w.accept_block(ctx, 3, np.array([[3, 0]], dtype=np.uint64))
+    w.close()
+    assert w.merge([ctx]) == 48
+    data = np.frombuffer(path.read_bytes(), dtype="<u8").reshape(-1, 2)
+    assert data.shape == (10, 2)
+    assert data[0].tolist() == [3, 0] and data[5].tolist() == [7, 1] and data[6].tolist() == [7, 2]
+    assert (data[1:5] == 0).all()
+    with pytest.raises(pb.ParameterError):
+        pb.EdgeFileWriter(str(tmp_path / "x.bin"), 0, -1)
