@@ -450,3 +450,36 @@ def test_binary_file_equals_oracle_and_is_schedule_independent(tmp_path):
     w.close()
     blk, _ = O.generate_block(_op(q), q.m0, q.m)
     assert path.read_bytes() == np.ascontiguousarray(blk, dtype="<u8").tobytes()
+
+
+# --------------------------------------------------------------------------- C ABI, host-buffer entry points
+
+def test_c_abi_host_entry_points():
+    import ctypes
+
+    from paper_1602_07106_b200 import _lib, hashing
+
+    L = _lib.load()
+    # seeded family: the _host variants take a HOST seed pointer
+    seed = np.ascontiguousarray(RING10, dtype=np.uint64)
+    p = pb.GenParams(n=5000, d=4, n0=10, seed_edges=seed)
+    cp = hashing.c_params(p.hash, p.n, p.d, p.n0, p.m0, seed.ctypes.data)
+    lo, hi = p.m0 + 7, p.m - 3
+    out = np.empty((hi - lo, 2), dtype=np.uint64)
+    probes = ctypes.c_uint64(0)
+    rc = L.parba_generate_host(ctypes.byref(cp), lo, hi, out.ctypes.data, ctypes.addressof(probes), 0)
+    assert rc == 0, L.parba_last_error()
+    want, wp = O.generate_block(_op(p), lo, hi)
+    assert np.array_equal(out, want) and probes.value == wp
+    K = 777
+    counts = np.full(K, 5, dtype=np.int64)  # accumulates (+=)
+    rc = L.parba_degree_window_host(ctypes.byref(cp), p.m0, p.m, K, counts.ctypes.data,
+                                    ctypes.addressof(probes), 0)
+    assert rc == 0, L.parba_last_error()
+    ref = np.zeros(K, dtype=np.int64)
+    blk, _ = O.generate_block(_op(p), p.m0, p.m)
+    O.count_block(ref, blk)
+    assert np.array_equal(counts, ref + 5)
+    # errors map to status codes, no exception crosses the ABI
+    assert L.parba_generate_host(ctypes.byref(cp), 0, 5, out.ctypes.data, None, 0) == _lib.PARBA_EINVAL
+    assert b"out of range" in L.parba_last_error()
