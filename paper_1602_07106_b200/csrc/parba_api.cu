@@ -74,7 +74,6 @@ DevParams make_dev(const parba_params_t *p, uint64_t K = 0) {
     d.k0 = crc32c_u64_bitwise(p->crc_seed0, 0);
     d.k01 = d.k0 ^ crc32c_u64_bitwise(p->crc_seed1, 0);
     d.seed = p->seed_edges;
-    d.cm = ChunkMul{1u << 21, 1u << 13, 1u << 23, 1u << 10, 4u};
     d.div64 = make_magic64(p->d);
     d.div32 = make_magic32(p->d);
     d.div32_2d = make_magic32(2 * p->d);
@@ -135,7 +134,7 @@ int launch_tiles_t(const DevParams &dp, uint64_t lo, uint64_t hi, const SinkArgs
     if (rc) return rc;
     auto kern = tile_kernel<Hash, SINK, SEED>;
     // as many warps per CTA (<= kWarps) as the shared memory allows
-    const size_t fixed = tile_smem_fixed<Hash>(), per_warp = tile_smem_per_warp<Hash, SINK>();
+    const size_t fixed = TileLayout<Hash, SINK>::fixed, per_warp = TileLayout<Hash, SINK>::per_warp;
     int warps = kWarps;
     while (warps > 1 && fixed + warps * per_warp > (size_t)di->smem_optin) --warps;
     const size_t smem = fixed + warps * per_warp;
@@ -149,13 +148,24 @@ int launch_tiles_t(const DevParams &dp, uint64_t lo, uint64_t hi, const SinkArgs
     }
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem));
     if (per_sm < 1) per_sm = 1;
-    const uint64_t tile0 = lo / kTile;
-    const uint64_t ntiles = (hi - 1) / kTile - tile0 + 1;
-    uint64_t grid = (uint64_t)di->sms * per_sm;
-    const uint64_t need = (ntiles + warps - 1) / warps;
-    if (grid > need) grid = need;
-    kern<<<(unsigned)grid, warps * 32, smem, st>>>(dp, lo, hi, tile0, ntiles, a, probes);
-    CUDA_TRY(cudaGetLastError());
+    // launches of at most kLaunchEdgesPerWarp edges per warp (tile-aligned
+    // cuts), so the kernel's 32-bit queue cursors never wrap
+    const uint64_t max_grid = (uint64_t)di->sms * per_sm;
+    const uint64_t cap = max_grid * warps * kLaunchEdgesPerWarp;
+    for (uint64_t a0 = lo; a0 < hi;) {
+        uint64_t a1 = hi;
+        if (hi - a0 > cap) a1 = (a0 / kTile) * kTile + cap;
+        const uint64_t tile0 = a0 / kTile;
+        const uint64_t ntiles = (a1 - 1) / kTile - tile0 + 1;
+        uint64_t grid = max_grid;
+        const uint64_t need = (ntiles + warps - 1) / warps;
+        if (grid > need) grid = need;
+        SinkArgs ac = a;
+        if (SINK == kStore) ac.out = a.out + 2 * (a0 - lo);
+        kern<<<(unsigned)grid, warps * 32, smem, st>>>(dp, a0, a1, tile0, ntiles, ac, probes);
+        CUDA_TRY(cudaGetLastError());
+        a0 = a1;
+    }
     return PARBA_OK;
 }
 

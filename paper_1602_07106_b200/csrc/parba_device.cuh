@@ -2,7 +2,7 @@
 //
 //   crc_chunks    CRC32-C of one 64-bit word with seed s0 from 11-bit chunk
 //                 tables in shared memory: 3 lookups for positions < 2^32, 4
-//                 for < 2^43; offsets formed on the FMA pipe.
+//                 for < 2^43; offsets by shift+mask on the ALU pipe.
 //   crc_bytes     byte-sliced variant for the generic kernels (any 64-bit value).
 //   h_crc(r)      the reference hash ((crc(s0,r)<<32) + crc(s1,r)) % r
 //                 (hashing.py:119-125, _kernels.py:32-42) rewritten through
@@ -81,12 +81,6 @@ __device__ __forceinline__ uint32_t magic_div32(uint32_t n, const Magic32 &m) {
     return (uint32_t)(((uint64_t)n * m.mul) >> m.shift);
 }
 
-// Opaque powers of two (kernel parameters, so the compiler cannot turn the
-// multiplies into ALU shifts): m21 = 2^21, m13 = 2^13, m23 = 2^23, m10 = 2^10, m4 = 4.
-struct ChunkMul {
-    uint32_t m21, m13, m23, m10, m4;
-};
-
 // Launch-constant description of one graph family (plain uniform-d mode).
 struct DevParams {
     uint64_t n, d, n0, m0, m;
@@ -100,7 +94,6 @@ struct DevParams {
     uint64_t win_rlim;     // window mode: generated target < K  <=>  r < win_rlim
     uint32_t win_rlim32;   // min(win_rlim, 2^32 - 1) for narrow launches
     uint64_t K;
-    ChunkMul cm;           // opaque powers of two for the chunk CRC
 };
 
 // Closed forms (generator.py:157-169): source of edge i, target of terminal r.
@@ -186,8 +179,7 @@ __device__ __forceinline__ double recip_approx(double rd) {
 //      one "if negative add r" gives h % r (= v % r, since v = h - qa*r*2^32).
 // The 1.5*2^52 offset rounds q to an integer for |q| < 2^51 of either sign.
 template <class R>
-__device__ __forceinline__ R mod_fp(uint32_t hhi, uint32_t hlo, double rd) {
-    const double y = recip_approx(rd);
+__device__ __forceinline__ R mod_fp_y(uint32_t hhi, uint32_t hlo, double rd, double y) {
     const double ha = u32_to_f64(hhi);
     const double hl = u32_to_f64(hlo);
     const double qa = fma(ha, y, 0x1.8p52) - 0x1.8p52;
@@ -204,23 +196,31 @@ __device__ __forceinline__ R mod_fp(uint32_t hhi, uint32_t hlo, double rd) {
         return ((uint64_t)hi << 32) | lo;
     }
 }
+template <class R>
+__device__ __forceinline__ R mod_fp(uint32_t hhi, uint32_t hlo, double rd) {
+    return mod_fp_y<R>(hhi, hlo, rd, recip_approx(rd));
+}
 
 // h % r for 1 <= r < 2^31 (h = hhi:hlo): stage A as in mod_fp, then the
 // final remainder in 32-bit integer arithmetic.  t = v - qb*r lies in [-r, r)
 // and v = x*2^32 + hlo == hlo (mod 2^32), so t = hlo - qb*r (mod 2^32) read as
-// int32 is exact (|t| < 2^31); t < 0 ? t + r : t == min_u32(t, t + r).  qb is
-// the low word of fma(v, y, 1.5*2^52) (two's complement for negative qb).
+// int32 is exact (|t| < 2^31); t < 0 ? t + r : t == min_u32(t, t + r).  -qb is
+// the low word of fma(-v, y, 1.5*2^52) (round-to-nearest is symmetric), so
+// t = hlo + (-qb)*r needs no negation.
 // 10 FP64 instructions + 1 IMAD + 2 ALU, no FP64 -> integer conversion.
-__device__ __forceinline__ uint32_t mod_fp31(uint32_t hhi, uint32_t hlo, uint32_t r) {
-    const double rd = cvt31<0>(r);
-    const double y = recip_approx(rd);
+__device__ __forceinline__ uint32_t mod_fp31_y(uint32_t hhi, uint32_t hlo, uint32_t r, double rd,
+                                               double y) {
     const double ha = cvt31<1>(hhi);
     const double qa = fma(ha, y, 0x1.8p52) - 0x1.8p52;
     const double x = fma(-qa, rd, ha);                          // exact, in [-r, r)
     const double v = fma(x, 0x1p32, cvt31<2>(hlo));             // ~ x*2^32 + hlo
-    const uint32_t qb = (uint32_t)__double2loint(fma(v, y, 0x1.8p52));
-    const uint32_t t = hlo - qb * r;                            // exact mod 2^32
+    const uint32_t nqb = (uint32_t)__double2loint(fma(-v, y, 0x1.8p52));  // -qb mod 2^32
+    const uint32_t t = hlo + nqb * r;                           // exact mod 2^32
     return min(t, t + r);
+}
+__device__ __forceinline__ uint32_t mod_fp31(uint32_t hhi, uint32_t hlo, uint32_t r) {
+    const double rd = cvt31<0>(r);
+    return mod_fp31_y(hhi, hlo, r, rd, recip_approx(rd));
 }
 
 // h % r for any 1 <= r < 2^64 (generic kernels; integer corrections).
@@ -348,21 +348,23 @@ __device__ __forceinline__ uint32_t crc_bytes(uint32_t tab, uint64_t w) {
 }
 
 // crc of the three chunks of one 32-bit word, tables at t, t+8K, t+16K
-__device__ __forceinline__ uint32_t crc_word3(uint32_t t, uint32_t x, const ChunkMul &m) {
-    const uint32_t o0 = __umulhi(x * m.m21, m.m13);    // (x & 0x7ff) << 2
-    const uint32_t o1 = __umulhi(x, m.m23) & 0x1ffcu;   // ((x >> 11) & 0x7ff) << 2
-    const uint32_t o2 = __umulhi(x, m.m10) * m.m4;      // (x >> 22) << 2
+// Byte offsets of the three 11/11/10-bit chunks of x (shift + mask on the
+// ALU pipe: the FMA-heavy pipe that would take IMAD forms is the busier one).
+__device__ __forceinline__ uint32_t crc_word3(uint32_t t, uint32_t x) {
+    const uint32_t o0 = (x << 2) & 0x1ffcu;   // (x & 0x7ff) << 2
+    const uint32_t o1 = (x >> 9) & 0x1ffcu;   // ((x >> 11) & 0x7ff) << 2
+    const uint32_t o2 = (x >> 20) & 0xffcu;   // (x >> 22) << 2
     return lds_u32(t + o0) ^ lds_u32(t + 8192 + o1) ^ lds_u32(t + 16384 + o2);
 }
 
 template <int NC>
-__device__ __forceinline__ uint32_t crc_chunks(uint32_t tab, uint64_t w, const ChunkMul &m) {
-    uint32_t c = crc_word3(tab, (uint32_t)w, m);
+__device__ __forceinline__ uint32_t crc_chunks(uint32_t tab, uint64_t w) {
+    uint32_t c = crc_word3(tab, (uint32_t)w);
     if constexpr (NC > 3) {
         const uint32_t hi = (uint32_t)(w >> 32);
-        c ^= lds_u32(tab + 3 * 8192 + __umulhi(hi * m.m21, m.m13));
-        if constexpr (NC > 4) c ^= lds_u32(tab + 4 * 8192 + (__umulhi(hi, m.m23) & 0x1ffcu));
-        if constexpr (NC > 5) c ^= lds_u32(tab + 5 * 8192 + __umulhi(hi, m.m10) * m.m4);
+        c ^= lds_u32(tab + 3 * 8192 + ((hi << 2) & 0x1ffcu));
+        if constexpr (NC > 4) c ^= lds_u32(tab + 4 * 8192 + ((hi >> 9) & 0x1ffcu));
+        if constexpr (NC > 5) c ^= lds_u32(tab + 5 * 8192 + ((hi >> 20) & 0xffcu));
     }
     return c;
 }
@@ -389,8 +391,16 @@ struct HashCrc {
         else if constexpr (NC <= 5) return mod_fp<R>(c0, c0 ^ p.k01, u52_to_f64(r));
         else return mod_int(c0, c0 ^ p.k01, r);
     }
+    // Same, with rd = (double)r and y ~ 1/r (relative error < 2^-34) supplied
+    // by the caller (first probes of a tile: series around the tile's centre).
+    static constexpr bool kHasRy = NC <= 5;
+    __device__ __forceinline__ static R from_crc_ry(uint32_t c0, R r, double rd, double y,
+                                                    const DevParams &p) {
+        if constexpr (NC == 2) return mod_fp31_y(c0, c0 ^ p.k01, r, rd, y);
+        else return mod_fp_y<R>(c0, c0 ^ p.k01, rd, y);
+    }
     __device__ __forceinline__ static uint32_t crc(uint32_t tab, uint64_t w, const DevParams &p) {
-        return crc_chunks<kChunks>(tab, w, p.cm);
+        return crc_chunks<kChunks>(tab, w);
     }
     __device__ __forceinline__ static R probe(uint32_t tab, R r, const DevParams &p) {
         return from_crc(crc(tab, r, p), r, p);
@@ -400,6 +410,9 @@ struct HashCrc {
 // Generic kernels: byte tables, any 64-bit value.
 struct HashCrcBytes {
     static constexpr bool kHasCrc = true;
+    static constexpr bool kHasRy = false;
+    template <class T>
+    __device__ __forceinline__ static T from_crc_ry(uint32_t, T r, double, double, const DevParams &) { return r; }
     static constexpr bool kNarrow = false;
     static constexpr bool kR31 = false;
     static constexpr bool kPack = false;
@@ -415,6 +428,9 @@ struct HashCrcBytes {
 template <bool NARROW>
 struct HashSimple {
     static constexpr bool kHasCrc = false;
+    static constexpr bool kHasRy = false;
+    template <class T>
+    __device__ __forceinline__ static T from_crc_ry(uint32_t, T r, double, double, const DevParams &) { return r; }
     static constexpr bool kNarrow = NARROW;
     static constexpr bool kR31 = false;
     static constexpr bool kPack = NARROW;

@@ -37,6 +37,8 @@ namespace parba {
 constexpr int kTile = 256;                 // edges per warp tile (power of two)
 constexpr int kQueue = 512;                // per-warp pending ring (>= kTile + 31)
 constexpr int kEpl = kTile / 32;           // edges per lane in phase 1
+// first probes use the per-tile reciprocal series from 2*base >= 2^27 on
+constexpr uint64_t kRyMin = 1ull << 27;
 #ifndef PARBA_WARPS
 #define PARBA_WARPS 32
 #endif
@@ -57,42 +59,40 @@ struct SinkArgs {
     uint32_t *full;                        // full counts (n)
 };
 
-// Per-warp shared state.  R = chain value type (u32 in narrow mode).
-// Store queue entries pack the chain value and its stage slot (9 bits) into
-// one u64 -- value in the low 55 bits -- when every position is < 2^52
-// (Hash::kPack); otherwise the slot goes to a separate u16 ring.
-template <int SINK, class R>
-struct WarpSmem {
-    uint64_t qe[kQueue];       // pending (slot << 55) | value   (ring)
-    uint16_t qs[kQueue];       // pending slots when !kPack
-    R stage[2][kTile];         // terminal chain values of the two tiles in flight
-};
-template <class R>
-struct WarpSmem<kWindow, R> {
-    R qr[kQueue];
-};
-template <class R>
-struct WarpSmem<kFull, R> {
-    R qr[kQueue];
-};
-
-// Dynamic shared memory: [CRC tables][crc(0,2j+1) table][per-warp state].
-template <class Hash>
-constexpr size_t tile_smem_fixed() {
-    return Hash::kHasCrc ? (Hash::kTableWords + kTile) * 4 : 0;
-}
+// Shared-memory layout of a tile CTA (dynamic smem, W warps):
+//   [pad][queue 0] .. [queue W-1] [CRC tables][crc(0,2j+1)] [stage 0] .. [stage W-1] [slots]
+// Each warp's pending queue is a ring of kQueue entries of kEB bytes aligned
+// to its own size kQB, so an entry address is qbase | (cursor & (kQB - 1))
+// with byte cursors.  Store-mode entries carry the chain value and where its
+// terminal value goes (the stage cell):
+//   narrow (values < 2^32):  (smem address of the cell << 32) | value
+//   kPack  (values < 2^52):  (cell offset in the warp's stage << 52) | value
+//   otherwise:               value, offsets in a separate u16 ring (slots).
+// The stage holds the terminal values of the two tiles in flight.
 template <class Hash, int SINK>
-constexpr size_t tile_smem_per_warp() {
-    return sizeof(WarpSmem<SINK, typename Hash::R>);
-}
-constexpr uint64_t kValueMask = (1ull << 55) - 1;
+struct TileLayout {
+    using R = typename Hash::R;
+    static constexpr uint32_t kEB = SINK == kStore ? 8u : (uint32_t)sizeof(R);
+    static constexpr uint32_t kLgEB = kEB == 8 ? 3u : 2u;
+    static constexpr uint32_t kQB = kQueue * kEB;
+    static constexpr uint32_t kTB = kTile * (uint32_t)sizeof(R);  // one stage buffer
+    static constexpr uint32_t kStageB = SINK == kStore ? 2 * kTB : 0;
+    static constexpr bool kSlots = SINK == kStore && !Hash::kPack;
+    static constexpr uint32_t kSlotB = kSlots ? kQueue * 2 : 0;
+    static constexpr size_t kTabB = Hash::kHasCrc ? (Hash::kTableWords + kTile) * 4 : 0;
+    static constexpr size_t fixed = kQB /* alignment pad */ + kTabB;
+    static constexpr size_t per_warp = kQB + kStageB + kSlotB;
+};
+constexpr uint64_t kValueMask52 = (1ull << 52) - 1;
+// Byte cursors of one launch stay below 2^31 when a launch covers at most
+// kLaunchEdgesPerWarp edges per warp (the host splits larger ranges).
+constexpr uint64_t kLaunchEdgesPerWarp = 1ull << 27;
 
 // A chain finished with terminal value r: hand its target to the sink.
 template <bool NARROW, bool SEED, int SINK, class R>
-__device__ __forceinline__ void finish(uint32_t stage_s, uint32_t slot, uint64_t r, const DevParams &p,
-                                       const SinkArgs &a) {
+__device__ __forceinline__ void finish(uint32_t saddr, uint64_t r, const DevParams &p, const SinkArgs &a) {
     if constexpr (SINK == kStore) {
-        sts_t<R>(stage_s + slot * (uint32_t)sizeof(R), (R)r);  // target computed at flush, all lanes busy
+        sts_t<R>(saddr, (R)r);  // stage cell; the target is computed at flush
     } else if constexpr (SINK == kWindow) {
         if (SEED && r < p.stop) {
             const uint64_t t = __ldg(p.seed + r);
@@ -112,12 +112,18 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
             SinkArgs a, unsigned long long *probes_out) {
     using R = typename Hash::R;
     constexpr bool NARROW = Hash::kNarrow;
+    using L = TileLayout<Hash, SINK>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    uint32_t *tabs_p = reinterpret_cast<uint32_t *>(smem_raw);
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    const int wpc = blockDim.x >> 5;  // warps per CTA (<= kWarps; fewer when smem is tight)
+    // queues first, each aligned to its size (the launch reserves kQB of padding)
+    const uint32_t raw_s = smem_addr(smem_raw);
+    const uint32_t pad = (L::kQB - (raw_s & (L::kQB - 1))) & (L::kQB - 1);
+    unsigned char *tab_raw = smem_raw + pad + (size_t)wpc * L::kQB;
+    uint32_t *tabs_p = reinterpret_cast<uint32_t *>(tab_raw);
     uint32_t *clow_s = tabs_p + Hash::kTableWords;  // crc(0, 2j+1), j < kTile (2j+1 < 512)
     const uint32_t tabs = opaque(smem_addr(tabs_p));
-    WarpSmem<SINK, R> *wsm = reinterpret_cast<WarpSmem<SINK, R> *>(
-        smem_raw + (Hash::kHasCrc ? (Hash::kTableWords + kTile) * 4 : 0));
     if constexpr (Hash::kHasCrc) {
         Hash::build(tabs_p, p.k0);
         for (int j = threadIdx.x; j < kTile; j += blockDim.x)
@@ -125,32 +131,27 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
     }
     __syncthreads();
 
-    const int lane = threadIdx.x & 31;
-    const int wib = threadIdx.x >> 5;
-    const int wpc = blockDim.x >> 5;  // warps per CTA (<= kWarps; fewer when smem is tight)
-    WarpSmem<SINK, R> &w = wsm[wib];
-    // shared-window addresses of this warp's queue and stage (kept in registers)
-    uint32_t qe_s, qs_s = 0, stage_s = 0;
-    if constexpr (SINK == kStore) {
-        qe_s = opaque(smem_addr(&w.qe[0]));
-        qs_s = opaque(smem_addr(&w.qs[0]));
-        stage_s = opaque(smem_addr(&w.stage[0][0]));
-    } else {
-        qe_s = opaque(smem_addr(&w.qr[0]));
-    }
+    // shared-window addresses of this warp's queue, stage and slot ring
+    const uint32_t qbase = opaque(raw_s + pad + (uint32_t)wib * L::kQB);
+    const uint32_t st_all = raw_s + pad + (uint32_t)wpc * L::kQB + (uint32_t)L::kTabB;
+    [[maybe_unused]] const uint32_t stage_s = opaque(st_all + (uint32_t)wib * L::kStageB);
+    [[maybe_unused]] const uint32_t qs_s =
+        opaque(st_all + (uint32_t)wpc * L::kStageB + (uint32_t)wib * L::kSlotB);
     const unsigned ltmask = lanemask_lt();
     const uint64_t gw = (uint64_t)blockIdx.x * wpc + wib;
     const uint64_t nw = (uint64_t)gridDim.x * wpc;
 
-    uint32_t act = 0;             // 1: lane holds a running chain
+    uint32_t act = 0;               // 1: lane holds a running chain
     R r = 0;
-    uint32_t slot = 0;
-    uint32_t head = 0, tail = 0;  // queue cursors (warp-uniform)
-    uint32_t tile_q0 = 0;         // queue cursor at the start of the current tile
-    uint32_t probes = 0;          // per lane (< 2^32 per launch and lane)
+    uint32_t saddr = 0;             // store: smem address of the chain's stage cell
+    uint32_t headb = 0, tailb = 0;  // queue byte cursors (warp-uniform)
+    uint32_t tile_q0 = 0;           // tail cursor at the start of the current tile
+    uint32_t probes = 0;            // per lane (< 2^32 per launch and lane)
     uint64_t prev_base = 0;
     bool have_prev = false;
     uint32_t buf = 0;
+
+    auto qaddr = [&](uint32_t cur) -> uint32_t { return qbase | (cur & (L::kQB - 1)); };
 
     auto is_done = [&](R v) -> bool {
         if constexpr (SEED) return ((uint32_t)v & 1u) == 0 || (uint64_t)v < p.stop;
@@ -196,7 +197,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
         const uint32_t fin = act & (cont ^ 1u);
         act &= cont;
         r = nr;
-        if (fin) finish<NARROW, SEED, SINK, R>(stage_s, slot, (uint64_t)nr, p, a);
+        if (fin) finish<NARROW, SEED, SINK, R>(saddr, (uint64_t)nr, p, a);
     };
 
     // Pop queued chains into idle lanes.  FULLQ: at least 32 entries queued,
@@ -205,30 +206,43 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
         constexpr bool FULLQ = decltype(fullq_c)::value;
         const unsigned idle = ballot_all(!act);
         const uint32_t rank = __popc(idle & ltmask);
-        const uint32_t avail = tail - head;
-        if (!act && (FULLQ || rank < avail)) {
-            const uint32_t pos = (head + rank) & (kQueue - 1);
+        const uint32_t availb = tailb - headb;
+        if (!act && (FULLQ || (rank << L::kLgEB) < availb)) {
+            const uint32_t cur = headb + (rank << L::kLgEB);
             if constexpr (SINK == kStore) {
-                const uint64_t e = lds_u64(qe_s + pos * 8);
-                if constexpr (Hash::kPack) {
-                    r = (R)(e & kValueMask);
-                    slot = (uint32_t)(e >> 55);
+                const uint64_t e = lds_u64(qaddr(cur));
+                if constexpr (NARROW) {
+                    r = (R)(uint32_t)e;
+                    saddr = (uint32_t)(e >> 32);
+                } else if constexpr (Hash::kPack) {
+                    r = (R)(e & kValueMask52);
+                    saddr = stage_s + (uint32_t)(e >> 52);
                 } else {
                     r = (R)e;
-                    slot = lds_u16(qs_s + pos * 2);
+                    saddr = stage_s + lds_u16(qs_s + ((cur & (L::kQB - 1)) >> 2));
                 }
             } else {
-                r = lds_t<R>(qe_s + pos * (uint32_t)sizeof(R));
+                r = lds_t<R>(qaddr(cur));
             }
             act = 1;
         }
-        if constexpr (FULLQ) head += (uint32_t)__popc(idle);
-        else head += min((uint32_t)__popc(idle), avail);
+        if constexpr (FULLQ) headb += (uint32_t)__popc(idle) << L::kLgEB;
+        else headb += min((uint32_t)__popc(idle) << L::kLgEB, availb);
     };
 
-    // First probe of every edge of a tile (FULL: interior tile, no bounds test).
-    auto phase1 = [&](auto full_c, uint64_t base, uint32_t cb) {
+    // RY: large tile (2*base >= kRyMin): the lane's 8 start values differ by
+    // multiples of 64, so 1/r0 comes from one reciprocal per lane and tile,
+    // c = 1/rc at the centre rc, and the first-order series
+    // 1/(rc + e) ~ c - e*c^2 (relative error (e/rc)^2 < 2^-38 for |e| <= 224).
+    auto phase1 = [&](auto full_c, auto ry_c, uint64_t base, uint32_t cb) {
         constexpr bool FULL = decltype(full_c)::value;
+        constexpr bool RY = decltype(ry_c)::value;
+        [[maybe_unused]] double rc = 0.0, c = 0.0, s64 = 0.0;
+        if constexpr (RY) {
+            rc = u52_to_f64(2 * base + 2 * lane + 1 + 224);
+            c = recip_approx(rc);
+            s64 = 64.0 * c * c;
+        }
 #pragma unroll
         for (int k = 0; k < kEpl; ++k) {
             const uint32_t j = lane + 32u * k;
@@ -236,28 +250,36 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
             const bool valid = FULL || ((i >= lo) && (i < hi));
             const R r0 = (R)(2 * base) + (R)(2 * j + 1);
             R r1;
-            if constexpr (Hash::kHasCrc) r1 = Hash::from_crc(cb ^ clow_s[j], r0, p);
-            else r1 = Hash::probe(tabs, r0, p);
+            if constexpr (RY) {
+                static_assert(kEpl == 8, "series centre assumes 8 edges per lane");
+            const double e = 64.0 * k - 224.0;
+                r1 = Hash::from_crc_ry(cb ^ clow_s[j], r0, rc + e, fma(-(k - 3.5), s64, c), p);
+            } else if constexpr (Hash::kHasCrc) {
+                r1 = Hash::from_crc(cb ^ clow_s[j], r0, p);
+            } else {
+                r1 = Hash::probe(tabs, r0, p);
+            }
             const bool done = is_done(r1);
+            [[maybe_unused]] const uint32_t cell = stage_s + (buf * kTile + j) * (uint32_t)sizeof(R);
             if constexpr (SINK == kStore)  // final unless pending
-                sts_t<R>(stage_s + (buf * kTile + j) * (uint32_t)sizeof(R), r1);
-            if constexpr (SINK != kStore) if (valid && done) finish<NARROW, SEED, SINK, R>(stage_s, buf * kTile + j, (uint64_t)r1, p, a);
+                sts_t<R>(cell, r1);
+            if constexpr (SINK != kStore) if (valid && done) finish<NARROW, SEED, SINK, R>(0u, (uint64_t)r1, p, a);
             const bool pend = valid && !done;
             const unsigned m = ballot_all(pend);
-            const uint32_t pos = (tail + __popc(m & ltmask)) & (kQueue - 1);
+            const uint32_t cur = tailb + (__popc(m & ltmask) << L::kLgEB);
             if constexpr (SINK == kStore) {
-                if constexpr (Hash::kPack) {
-                    // predicated store, no branch: (slot << 55) | value
-                    const uint32_t slot_hi = ((buf * kTile + j) << 23);
-                    sts_u64_if(pend, qe_s + pos * 8, ((uint64_t)slot_hi << 32) | (uint64_t)r1);
+                if constexpr (NARROW) {
+                    sts_u64_if(pend, qaddr(cur), ((uint64_t)cell << 32) | (uint64_t)r1);
+                } else if constexpr (Hash::kPack) {
+                    sts_u64_if(pend, qaddr(cur), ((uint64_t)(cell - stage_s) << 52) | (uint64_t)r1);
                 } else if (pend) {
-                    sts_u64(qe_s + pos * 8, (uint64_t)r1);
-                    sts_u16(qs_s + pos * 2, (uint16_t)(buf * kTile + j));
+                    sts_u64(qaddr(cur), (uint64_t)r1);
+                    sts_u16(qs_s + ((cur & (L::kQB - 1)) >> 2), (uint16_t)(cell - stage_s));
                 }
             } else {
-                sts_t_if<R>(pend, qe_s + pos * (uint32_t)sizeof(R), r1);
+                sts_t_if<R>(pend, qaddr(cur), r1);
             }
-            tail += __popc(m);
+            tailb += __popc(m) << L::kLgEB;
             probes += valid ? 1u : 0u;
         }
     };
@@ -265,18 +287,29 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
     for (uint64_t t = gw; t < ntiles; t += nw) {
         const uint64_t base = (tile0 + t) * kTile;
         // ---- phase 1: first probe of all edges of the tile
-        tile_q0 = tail;  // queue position where this tile's entries start
+        tile_q0 = tailb;  // queue position where this tile's entries start
         uint32_t cb = 0;
         if constexpr (Hash::kHasCrc) cb = Hash::crc(tabs, 2 * base, p);
-        if (base >= lo && base + kTile <= hi) phase1(std::true_type{}, base, cb);
-        else phase1(std::false_type{}, base, cb);
+        if (base >= lo && base + kTile <= hi) {
+            if constexpr (Hash::kHasRy) {
+                if (2 * base >= kRyMin) phase1(std::true_type{}, std::true_type{}, base, cb);
+                else phase1(std::true_type{}, std::false_type{}, base, cb);
+            } else {
+                phase1(std::true_type{}, std::false_type{}, base, cb);
+            }
+        } else {
+            phase1(std::false_type{}, std::false_type{}, base, cb);
+        }
         __syncwarp();
         // ---- phase 2: pop queued chains into idle lanes and probe while at
         // least a full warp of entries is queued (the < 32 newest entries
         // carry over to the next tile, so every refill can fill every idle lane)
-        while (tail - head >= 32u) {
-            refill(std::true_type{});
-            step();
+        if (tailb - headb >= (32u << L::kLgEB)) {
+            const uint32_t lim = tailb - (32u << L::kLgEB);
+            do {
+                refill(std::true_type{});
+                step();
+            } while (headb <= lim);
         }
         // ---- store: flush the previous tile once none of its chains runs
         if constexpr (SINK == kStore) {
@@ -284,11 +317,11 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
                 const uint32_t pb = buf ^ 1u;
                 // entries of the previous tile still queued (only when this
                 // tile pushed fewer than 32): pop them first
-                while ((int32_t)(tile_q0 - head) > 0) {
+                while ((int32_t)(tile_q0 - headb) > 0) {
                     refill(std::false_type{});
                     step();
                 }
-                while (__any_sync(0xffffffffu, act && (slot / kTile) == pb)) step();
+                while (__any_sync(0xffffffffu, act && (saddr - stage_s) / L::kTB == pb)) step();
                 flush(pb, prev_base);
             }
             prev_base = base;
@@ -297,7 +330,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
         }
     }
     // ---- drain the queue and the chains still running, then flush the last tile
-    while (tail != head) {
+    while (tailb != headb) {
         refill(std::false_type{});
         step();
     }

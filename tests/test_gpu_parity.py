@@ -183,6 +183,19 @@ def test_unaligned_subranges_vs_oracle():
         assert np.array_equal(got, want) and pr == wp
 
 
+def test_first_probe_series_threshold_vs_oracle():
+    """Tiles at and around 2*base = 2^27, where the first probes switch to the
+    per-tile reciprocal series, for the 31-bit and the wide remainder paths."""
+    for n, d in ((10**8, 10), (10**9, 100), (2**40, 7)):
+        p = pb.GenParams(n=n, d=d)
+        for c in (1 << 26, 1 << 29):
+            lo, hi = c - 4096 - 17, c + 4096 + 5
+            assert hi <= p.m
+            got, pr = pb.generate_block(lo, hi, p)
+            want, wp = O.generate_block(_op(p), lo, hi)
+            assert np.array_equal(got, want) and pr == wp, (n, d, c)
+
+
 def test_sampled_ids_vs_reference_fixture(golden):
     arrays, meta = golden
     for name, s in meta["samples"].items():
