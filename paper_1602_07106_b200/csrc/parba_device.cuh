@@ -131,6 +131,9 @@ __device__ __forceinline__ double u32_to_f64_magic(uint32_t x) {
     return __hiloint2double(0x43300000, (int)x) - 0x1p52;
 }
 __device__ __forceinline__ double u32_to_f64_i2f(uint32_t x) { return __uint2double_rn(x); }
+#ifndef PARBA_ROT
+#define PARBA_ROT 0
+#endif
 #ifndef PARBA_CVT31
 #define PARBA_CVT31 6
 #endif
@@ -351,7 +354,11 @@ __device__ __forceinline__ uint32_t crc_bytes(uint32_t tab, uint64_t w) {
 // Byte offsets of the three 11/11/10-bit chunks of x (shift + mask on the
 // ALU pipe: the FMA-heavy pipe that would take IMAD forms is the busier one).
 __device__ __forceinline__ uint32_t crc_word3(uint32_t t, uint32_t x) {
+#if PARBA_ROT
+    const uint32_t o0 = __funnelshift_l(x, x, 2) & 0x1ffcu;   // rotate: SHF on the ALU
+#else
     const uint32_t o0 = (x << 2) & 0x1ffcu;   // (x & 0x7ff) << 2
+#endif
     const uint32_t o1 = (x >> 9) & 0x1ffcu;   // ((x >> 11) & 0x7ff) << 2
     const uint32_t o2 = (x >> 20) & 0xffcu;   // (x >> 22) << 2
     return lds_u32(t + o0) ^ lds_u32(t + 8192 + o1) ^ lds_u32(t + 16384 + o2);
