@@ -36,11 +36,24 @@ extern "C" {
 #define PARBA_ECUDA 2    /* CUDA runtime / launch error -> GenerationError */
 #define PARBA_ENOMEM 3   /* device or pinned allocation failed            */
 
+#define PARBA_EINFEASIBLE 4 /* no fresh target within max_attempts -> InfeasibleTargetsError (errors.py:19-24) */
+
 #define PARBA_HASH_CRC 0u    /* HashKind.CRC    (hashing.py:43-45, 119-125) */
 #define PARBA_HASH_SIMPLE 1u /* HashKind.SIMPLE (hashing.py:128-138)        */
 
-/* Graph family = GenParams (generator.py:50-110) with a uniform degree d,
- * plus the effective hash constants of its HashConfig (hashing.py:48-85). */
+/* GenParams option flags (generator.py:61-62, 184-246). */
+#define PARBA_FLAG_NO_SELF_LOOPS 1u
+#define PARBA_FLAG_NO_PARALLEL_EDGES 2u
+
+/* Owner-lookup methods of a degree sequence (generator.py:30, 248-255). */
+#define PARBA_RESOLVE_RANK 0u
+#define PARBA_RESOLVE_BISECT 1u
+#define PARBA_RESOLVE_DEFERRED 2u
+
+/* Graph family = GenParams (generator.py:50-110): a uniform degree d or a
+ * degree sequence, the seed graph, the option flags, plus the effective hash
+ * constants of its HashConfig (hashing.py:48-85).  Zero-initialise the
+ * fields after seed_edges for the plain uniform-d family. */
 typedef struct parba_params {
     uint64_t n;            /* node count                                   */
     uint64_t d;            /* uniform out-degree (>= 1)                    */
@@ -53,6 +66,18 @@ typedef struct parba_params {
     uint32_t reserved;     /* must be 0                                    */
     uint64_t simple_mult;  /* HashConfig.simple_multiplier()               */
     const uint64_t *seed_edges; /* DEVICE pointer to 2*m0 node IDs (NULL iff m0 == 0) */
+    /* option flags (f3) */
+    uint32_t flags;        /* PARBA_FLAG_* (both require m0 >= 1)          */
+    uint32_t reserved2;    /* must be 0                                    */
+    uint64_t max_attempts; /* no_parallel_edges retry cap; 0 = 64 * degree */
+    uint32_t base_seed0;   /* seed0 & 0xFFFFFFFF: retry attempt a >= 1 uses  */
+    uint32_t base_seed1;   /* seed1 & 0xFFFFFFFF  the family with salt a     */
+    uint64_t base_mult;    /* HashConfig.multiplier    (with_attempt, hashing.py:69-85) */
+    /* degree sequence (f4): d == 0 and these three set (DEVICE pointers,
+     * built by parba_degseq_prefix / parba_degseq_rank); m = W[n - n0]   */
+    const uint64_t *degree_prefix; /* W: n - n0 + 1 entries               */
+    const void *rank;              /* rank directory, (m + 63) / 64 x 16 B */
+    const uint64_t *owners;        /* rank -> node; NULL iff every degree >= 1 */
 } parba_params_t;
 
 /* Library / ABI version (major*10000 + minor*100 + patch). */
@@ -103,7 +128,39 @@ int parba_degree_full(const parba_params_t *p, uint64_t lo, uint64_t hi, uint32_
 int parba_count_ids(const uint64_t *ids, uint64_t count, uint64_t K, unsigned long long *counts,
                     void *stream);
 
-/* Host-buffer entry points (blocking).  generate_block into a host array
+/* ---- Degree sequences (f4; degreeseq.py) ------------------------------
+ * build_prefix (degreeseq.py:87-115): W[k] = m0 + degrees[0] + ... +
+ * degrees[k-1] for k <= count (W[count] = m), by a device scan.  The caller
+ * validates the degrees (non-negative, no overflow, m < 2^58). */
+int parba_degseq_prefix(const uint64_t *degrees, uint64_t count, uint64_t m0, uint64_t *W, void *stream);
+/* build_rank_bits (degreeseq.py:118-151): rank directory over positions
+ * [0, m) -- ((m + 63) / 64) 16-byte entries {start bits, ones before} -- and,
+ * when owners != NULL, owners[j] = node of the j-th node with degree >= 1.
+ * n_ones (host, optional) receives the number of such nodes. */
+int parba_degseq_rank(const uint64_t *W, uint64_t count, uint64_t m, uint64_t n0, void *rank,
+                      uint64_t *owners, uint64_t *n_ones, void *stream);
+/* rank1_many (degreeseq.py:154-162): out[k] = ones at positions 0..es[k]. */
+int parba_rank1(const void *rank, const uint64_t *es, uint64_t count, uint64_t *out, void *stream);
+/* node_of_edge_many / node_of_edge_bisect_many / owners_of_edges_deferred
+ * (degreeseq.py:165-216): out[k] = owning node of position es[k] (every
+ * es[k] in [m0, m)), by PARBA_RESOLVE_* -- identical results. */
+int parba_node_of_edges(const parba_params_t *p, const uint64_t *es, uint64_t count, uint64_t *out,
+                        uint32_t method, void *stream);
+
+/* ---- Option flags (f3) --------------------------------------------------
+ * With p->flags set, parba_generate / parba_degree_window / parba_degree_full
+ * are node-granular: lo and hi must be node boundaries (hi may be m), as in
+ * generate_block (generator.py:272-302), and the call synchronises `stream`
+ * to report PARBA_EINFEASIBLE (no fresh target within max_attempts).
+ * generate_node_edges(v) = parba_generate over [W_v, W_v + d_v). */
+
+/* count_block over stored pairs (analytics.py:44-48): counts[x] += 1 for
+ * each endpoint x < K of pairs[0..count). */
+int parba_count_pairs(const uint64_t *pairs, uint64_t count, uint64_t K, unsigned long long *counts,
+                      void *stream);
+
+/* Host-buffer entry points (blocking; uniform degree only -- a degree
+ * sequence's index lives on the device).  generate_block into a host array
  * out_pairs[2*(hi-lo)]: the device generates in chunks while earlier chunks
  * stream back over PCIe (pinned host memory gets full DMA speed). */
 int parba_generate_host(const parba_params_t *p_host_seed, uint64_t lo, uint64_t hi,

@@ -45,6 +45,13 @@ class _Params(ctypes.Structure):
         ("s1", ctypes.c_uint32),
         ("mult", ctypes.c_uint64),
         ("seed_edges", ctypes.POINTER(ctypes.c_uint64)),
+        ("W", ctypes.POINTER(ctypes.c_uint64)),
+        ("flags", ctypes.c_uint32),
+        ("pad", ctypes.c_uint32),
+        ("max_attempts", ctypes.c_uint64),
+        ("base_seed0", ctypes.c_uint64),
+        ("base_seed1", ctypes.c_uint64),
+        ("base_mult", ctypes.c_uint64),
     ]
 
 
@@ -87,16 +94,19 @@ def lib() -> ctypes.CDLL:
         L.po_run_threaded.restype = u64
         L.po_crc32c_table.argtypes = [pu64]
         L.po_crc32c_table.restype = None
+        L.po_generate_nodes.argtypes = [P, u64, u64, pu64, ctypes.POINTER(u64), ctypes.POINTER(u64)]
+        L.po_generate_nodes.restype = i32
         _lib = L
     return _lib
 
 
 @dataclass(frozen=True)
 class OParams:
-    """Uniform-degree graph family (generator.py:50-110 restated)."""
+    """Graph family (generator.py:50-110 restated): uniform d, or a degree
+    sequence ``degrees`` (d = None); option flags."""
 
     n: int
-    d: int
+    d: int | None
     n0: int = 0
     seed_edges: tuple = ()
     kind: int = KIND_CRC
@@ -104,6 +114,10 @@ class OParams:
     seed1: int = 1
     salt: int = 0
     multiplier: int = DEFAULT_MULTIPLIER
+    degrees: tuple | None = None
+    no_self_loops: bool = False
+    no_parallel_edges: bool = False
+    max_attempts: int | None = None
 
     @property
     def m0(self) -> int:
@@ -111,7 +125,22 @@ class OParams:
 
     @property
     def m(self) -> int:  # generator.py:107-110
+        if self.degrees is not None:
+            return self.m0 + int(sum(int(x) for x in self.degrees))
         return self.m0 + (self.n - self.n0) * self.d
+
+    def W(self) -> np.ndarray:
+        """Prefix sums (degreeseq.py:109-115), n-n0+1 entries (last = m)."""
+        deg = np.array(self.degrees, dtype=np.uint64)
+        W = np.empty(deg.size + 1, dtype=np.uint64)
+        W[0] = self.m0
+        np.cumsum(deg, out=W[1:])
+        W[1:] += np.uint64(self.m0)
+        return W
+
+    @property
+    def flags(self) -> int:
+        return (1 if self.no_self_loops else 0) | (2 if self.no_parallel_edges else 0)
 
     def crc_seeds(self) -> tuple[int, int]:  # hashing.py:73-77
         return (self.seed0 + self.salt) & MASK32, (self.seed1 + self.salt * _GOLDEN32) & MASK32
@@ -122,10 +151,14 @@ class OParams:
     def _c(self):
         seed = np.ascontiguousarray(np.array(self.seed_edges, dtype=np.uint64))
         s0, s1 = self.crc_seeds()
-        st = _Params(self.n, self.d, self.n0, self.m0, self.m, self.kind, s0, s1,
+        W = self.W() if self.degrees is not None else None
+        st = _Params(self.n, self.d or 0, self.n0, self.m0, self.m, self.kind, s0, s1,
                      self.simple_multiplier(),
-                     seed.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)) if seed.size else None)
-        return st, seed  # keep seed alive alongside the struct
+                     seed.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)) if seed.size else None,
+                     W.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)) if W is not None else None,
+                     self.flags, 0, self.max_attempts or 0, self.seed0 & MASK64, self.seed1 & MASK64,
+                     self.multiplier & MASK64)
+        return st, (seed, W)  # keep the arrays alive alongside the struct
 
 
 def _ptr(a: np.ndarray) -> int:
@@ -169,9 +202,29 @@ def resolve_chain_block(p: OParams, r0: np.ndarray, stop_below: int) -> tuple[np
     return out, int(probes)
 
 
+class NotNodeBoundary(ValueError):
+    pass
+
+
+class Infeasible(RuntimeError):
+    def __init__(self, edge: int):
+        super().__init__(f"edge {edge}: no fresh target")
+        self.edge = edge
+
+
 def generate_block(p: OParams, lo: int, hi: int) -> tuple[np.ndarray, int]:
+    """generate_block (generator.py:258-325); flag modes are node-granular
+    (raise NotNodeBoundary / Infeasible like the reference's errors)."""
     out = np.empty((hi - lo, 2), dtype=np.uint64)
     st, _keep = p._c()
+    if p.flags:
+        probes, fail = ctypes.c_uint64(0), ctypes.c_uint64(0)
+        rc = lib().po_generate_nodes(ctypes.byref(st), lo, hi, _ptr(out), ctypes.byref(probes), ctypes.byref(fail))
+        if rc == 1:
+            raise NotNodeBoundary(f"[{lo}, {hi}) is not node-aligned")
+        if rc == 2:
+            raise Infeasible(int(fail.value))
+        return out, int(probes.value)
     probes = lib().po_generate_block(ctypes.byref(st), lo, hi, _ptr(out))
     return out, int(probes)
 

@@ -39,6 +39,16 @@ typedef struct {
     uint32_t s0, s1;     /* effective CRC seeds (HashConfig.crc_seeds) */
     uint64_t mult;       /* effective SIMPLE multiplier */
     const uint64_t *seed_edges; /* 2*m0 node IDs (may be NULL when m0 == 0) */
+    /* degree sequence (generator.py:54-91, degreeseq.py:87-115): W[k] =
+     * first edge of node n0+k, k <= n-n0 (W[n-n0] = m); NULL = uniform d */
+    const uint64_t *W;
+    /* option flags (generator.py:61-62): bit 0 no_self_loops, bit 1
+     * no_parallel_edges; retry cap (0 = 64 * degree, generator.py:205) */
+    uint32_t flags, pad;
+    uint64_t max_attempts;
+    /* raw HashConfig seed0 / seed1 / multiplier: retry attempt a >= 1 uses
+     * the family with attempt_salt = a (HashConfig.with_attempt, hashing.py:69-71) */
+    uint64_t base_seed0, base_seed1, base_mult;
 } po_params_t;
 
 static uint32_t g_table[256];
@@ -135,11 +145,99 @@ uint64_t po_resolve_chain_block(const po_params_t *p, const uint64_t *r0, uint64
     return probes;
 }
 
-/* generator.py:157-169 -- closed forms, uniform degree. */
-static inline uint64_t po_source(const po_params_t *p, uint64_t i) { return (i - p->m0) / p->d + p->n0; }
+/* degreeseq.py:188-196 -- node_of_edge_bisect: the rightmost k with
+ * W[k] <= e (zero-degree nodes share their successor's W and are skipped). */
+static inline uint64_t po_node_bisect(const po_params_t *p, uint64_t e) {
+    uint64_t lo = 0, hi = p->n - p->n0;
+    while (lo < hi) {
+        uint64_t mid = lo + (hi - lo) / 2;
+        if (p->W[mid] <= e) lo = mid + 1;
+        else hi = mid;
+    }
+    return p->n0 + lo - 1;
+}
+
+/* generator.py:157-169 -- closed forms (uniform d) or owner lookup. */
+static inline uint64_t po_source(const po_params_t *p, uint64_t i) {
+    if (p->W) return po_node_bisect(p, i);
+    return (i - p->m0) / p->d + p->n0;
+}
 static inline uint64_t po_target(const po_params_t *p, uint64_t term) {
     if (term < 2 * p->m0) return p->seed_edges[term];          /* generator.py:164-165, 312-318 */
+    if (p->W) return po_node_bisect(p, term >> 1);              /* generator.py:168-169 */
     return ((term >> 1) - p->m0) / p->d + p->n0;                /* generator.py:166-168, 320-322 */
+}
+
+static inline uint64_t po_first_edge(const po_params_t *p, uint64_t v) {
+    return p->W ? p->W[v - p->n0] : p->m0 + (v - p->n0) * p->d;
+}
+static inline uint64_t po_degree(const po_params_t *p, uint64_t v) {
+    return p->W ? p->W[v - p->n0 + 1] - p->W[v - p->n0] : p->d;
+}
+
+/* hashing.py:69-85 -- the family of retry attempt a (a = 0: the configured one). */
+static po_params_t po_family(const po_params_t *p, uint64_t attempt) {
+    po_params_t f = *p;
+    if (attempt) {
+        po_crc_seeds(p->base_seed0, p->base_seed1, attempt, &f.s0, &f.s1);
+        f.mult = po_simple_multiplier(p->base_mult, attempt);
+    }
+    return f;
+}
+
+/* generator.py:184-217 -- _node_edges_with_probes: node v's edges, in edge
+ * order, into rows[dv][2].  Returns 0, or -1 with *fail_edge set when
+ * no_parallel_edges finds no fresh target within the cap. */
+int po_node_edges(const po_params_t *p, uint64_t v, uint64_t *rows, uint64_t *probes, uint64_t *fail_edge) {
+    po_build_table();
+    const uint64_t first = po_first_edge(p, v), dv = po_degree(p, v);
+    const uint64_t stop = 2 * p->m0;
+    const int nsl = p->flags & 1u, npe = (p->flags >> 1) & 1u;
+    for (uint64_t i = first; i < first + dv; ++i) {
+        const uint64_t r0 = nsl ? 2 * first : 2 * i + 1;
+        uint64_t term, t = 0;
+        if (!npe) {
+            *probes += po_chain(p, r0, stop, &term);
+            t = po_target(p, term);
+        } else {
+            const uint64_t cap = p->max_attempts ? p->max_attempts : 64 * dv;
+            int fresh = 0;
+            for (uint64_t a = 0; a < cap && !fresh; ++a) {
+                const po_params_t f = po_family(p, a);
+                *probes += po_chain(&f, r0, stop, &term);
+                t = po_target(p, term);
+                fresh = 1;
+                for (uint64_t j = first; j < i; ++j)
+                    if (rows[2 * (j - first) + 1] == t) { fresh = 0; break; }
+            }
+            if (!fresh) { *fail_edge = i; return -1; }
+        }
+        rows[2 * (i - first)] = v;
+        rows[2 * (i - first) + 1] = t;
+    }
+    return 0;
+}
+
+/* generator.py:231-245 -- node whose first edge is exactly pos (n at m). */
+static int po_boundary_node(const po_params_t *p, uint64_t pos, uint64_t *v) {
+    if (pos == p->m) { *v = p->n; return 0; }
+    uint64_t u = po_source(p, pos);
+    if (po_first_edge(p, u) != pos) return -1;
+    *v = u;
+    return 0;
+}
+
+/* generator.py:258-302, flag modes -- node-granular generate_block.
+ * Returns 0, 1 (lo or hi is not a node boundary), 2 (infeasible: *fail_edge). */
+int po_generate_nodes(const po_params_t *p, uint64_t lo, uint64_t hi, uint64_t *out_pairs,
+                      uint64_t *probes, uint64_t *fail_edge) {
+    uint64_t vlo, vhi;
+    *probes = 0;
+    if (lo == hi) return 0;
+    if (po_boundary_node(p, lo, &vlo) || po_boundary_node(p, hi, &vhi)) return 1;
+    for (uint64_t v = vlo; v < vhi; ++v)
+        if (po_node_edges(p, v, out_pairs + 2 * (po_first_edge(p, v) - lo), probes, fail_edge)) return 2;
+    return 0;
 }
 
 /* generator.py:258-325 (plain path, uniform d) -- rows (src, tgt) of edges

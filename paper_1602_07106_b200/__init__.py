@@ -1,8 +1,9 @@
 """B200-native Barabasi-Albert edge generator (Sanders & Schulz, arXiv 1602.07106).
 
 Drop-in for the hot path of the reference package ``parba``: same names,
-argument meaning, return types and error behaviour for the uniform-degree
-generator and degree API; the chains run in hand-written sm_100a CUDA kernels
+argument meaning, return types and error behaviour for the generator (uniform
+degree or degree sequence, option flags) and the degree API; the chains and
+the degree-sequence index run in hand-written sm_100a CUDA kernels
 (``libparba_b200.so``, C ABI in include/parba_b200.h).  There is no CPU
 fallback: without the library or a CUDA device every compute call raises
 ``GenerationError``.
@@ -35,7 +36,18 @@ from .driver import (
     plan_batches,
     run,
 )
-from . import io, parallel
+from . import degreeseq, io, parallel
+from .degreeseq import (
+    PrefixIndex,
+    RankBits,
+    build_prefix,
+    build_rank_bits,
+    first_half_pos,
+    node_of_edge,
+    node_of_edge_bisect,
+    read_degree_file,
+    resolve_targets_deferred,
+)
 from .errors import GenerationError, InfeasibleTargetsError, ParameterError, SeedGraphFormatError
 from .generator import (
     MAX_EDGES,
@@ -61,7 +73,9 @@ __all__ = [
     "Batch", "BinRatio", "ChainResult", "CollectConsumer", "Consumer", "DEFAULT_BATCH_SIZE",
     "DEFAULT_MULTIPLIER", "DegreeCountConsumer", "EdgeFileWriter", "write_edges_binary", "DegreeCounter", "DiscardConsumer", "Edge",
     "GenParams", "GenerationError", "Granularity", "HashConfig", "HashKind", "Histogram",
-    "InfeasibleTargetsError", "MAX_EDGES", "ParameterError", "RunStats", "SeedGraphFormatError",
+    "InfeasibleTargetsError", "MAX_EDGES", "ParameterError", "PrefixIndex", "RankBits", "RunStats",
+    "SeedGraphFormatError", "build_prefix", "build_rank_bits", "first_half_pos", "node_of_edge",
+    "node_of_edge_bisect", "read_degree_file", "resolve_targets_deferred",
     "WorkerStats", "bb_generate", "count_block", "count_edge", "count_seed_edges", "degree_counts",
     "edge_count", "edge_list", "edges_at", "expected_degree_check", "fit_exponent",
     "generate_block", "generate_block_device", "generate_edge", "generate_node_edges", "h_crc",

@@ -19,14 +19,16 @@ from .errors import GenerationError, ParameterError
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libparba_b200.so")
 
-PARBA_OK, PARBA_EINVAL, PARBA_ECUDA, PARBA_ENOMEM = 0, 1, 2, 3
+PARBA_OK, PARBA_EINVAL, PARBA_ECUDA, PARBA_ENOMEM, PARBA_EINFEASIBLE = 0, 1, 2, 3, 4
 HASH_CRC, HASH_SIMPLE = 0, 1
+FLAG_NO_SELF_LOOPS, FLAG_NO_PARALLEL_EDGES = 1, 2
 
 # Every symbol include/parba_b200.h declares (checked by tests/test_boundary.py).
 EXPORTS = (
     "parba_version", "parba_last_error", "parba_device_count", "parba_hash",
     "parba_resolve_chains", "parba_generate", "parba_edges_at", "parba_degree_window",
     "parba_degree_full", "parba_count_ids", "parba_generate_host", "parba_degree_window_host",
+    "parba_degseq_prefix", "parba_degseq_rank", "parba_rank1", "parba_node_of_edges", "parba_count_pairs",
 )
 
 
@@ -45,6 +47,15 @@ class CParams(ctypes.Structure):
         ("reserved", ctypes.c_uint32),
         ("simple_mult", ctypes.c_uint64),
         ("seed_edges", ctypes.c_void_p),
+        ("flags", ctypes.c_uint32),
+        ("reserved2", ctypes.c_uint32),
+        ("max_attempts", ctypes.c_uint64),
+        ("base_seed0", ctypes.c_uint32),
+        ("base_seed1", ctypes.c_uint32),
+        ("base_mult", ctypes.c_uint64),
+        ("degree_prefix", ctypes.c_void_p),
+        ("rank", ctypes.c_void_p),
+        ("owners", ctypes.c_void_p),
     ]
 
 
@@ -79,9 +90,16 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
             "parba_count_ids": ([vp, u64, u64, vp, vp], i32),
             "parba_generate_host": ([P, u64, u64, vp, vp, i32], i32),
             "parba_degree_window_host": ([P, u64, u64, u64, vp, vp, i32], i32),
+            "parba_degseq_prefix": ([vp, u64, u64, vp, vp], i32),
+            "parba_degseq_rank": ([vp, u64, u64, u64, vp, vp, ctypes.POINTER(u64), vp], i32),
+            "parba_rank1": ([vp, vp, u64, vp, vp], i32),
+            "parba_node_of_edges": ([P, vp, u64, vp, ctypes.c_uint32, vp], i32),
+            "parba_count_pairs": ([vp, u64, u64, vp, vp], i32),
         }
         for name, (args, res) in sig.items():
-            fn = getattr(L, name)
+            fn = getattr(L, name, None)
+            if fn is None:  # older builds (tools/ab.py A/B); tests check every export
+                continue
             fn.argtypes = args
             fn.restype = res
         _lib = L
@@ -94,6 +112,10 @@ def check(rc: int) -> None:
     msg = load().parba_last_error().decode(errors="replace")
     if rc == PARBA_EINVAL:
         raise ParameterError(msg)
+    if rc == PARBA_EINFEASIBLE:
+        from .errors import InfeasibleTargetsError
+
+        raise InfeasibleTargetsError(msg)
     raise GenerationError(msg)
 
 

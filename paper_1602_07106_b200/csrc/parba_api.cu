@@ -10,8 +10,12 @@
 #include <string>
 #include <vector>
 
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
 #include "../../include/parba_b200.h"
 #include "parba_kernels.cuh"
+#include "parba_nodes.cuh"
 
 using namespace parba;
 
@@ -38,8 +42,29 @@ int fail(int code, const char *fmt, ...) {
 
 constexpr uint64_t kMaxEdges = 1ull << 58;  // degreeseq.py:27 (MAX_EDGES)
 
+bool is_deg(const parba_params_t *p) { return p->degree_prefix != nullptr; }
+
 int validate(const parba_params_t *p) {
     if (!p) return fail(PARBA_EINVAL, "params is NULL");
+    if (p->flags & ~(PARBA_FLAG_NO_SELF_LOOPS | PARBA_FLAG_NO_PARALLEL_EDGES))
+        return fail(PARBA_EINVAL, "unknown option flags 0x%x", p->flags);
+    if (p->reserved2 != 0) return fail(PARBA_EINVAL, "reserved2 field must be 0");
+    if (p->flags && p->m0 < 1)
+        return fail(PARBA_EINVAL, "no_self_loops / no_parallel_edges require a seed graph (m0 >= 1): "
+                                  "with an empty seed the first edge is the forced self-loop (0, 0)");
+    if (is_deg(p)) {
+        if (p->d != 0) return fail(PARBA_EINVAL, "exactly one of d and degrees must be given");
+        if (!p->rank) return fail(PARBA_EINVAL, "degree sequence without its rank directory");
+        if (p->n < p->n0) return fail(PARBA_EINVAL, "need 0 <= n0 <= n, got n0=%llu, n=%llu",
+                                      (unsigned long long)p->n0, (unsigned long long)p->n);
+        if (p->hash_kind > PARBA_HASH_SIMPLE) return fail(PARBA_EINVAL, "unknown hash kind %u", p->hash_kind);
+        if (p->reserved != 0) return fail(PARBA_EINVAL, "reserved field must be 0");
+        if (p->m0 > 0 && !p->seed_edges) return fail(PARBA_EINVAL, "m0 > 0 but seed_edges is NULL");
+        if (p->m < p->m0 || p->m >= kMaxEdges)
+            return fail(PARBA_EINVAL, "total edge count %llu out of range", (unsigned long long)p->m);
+        return PARBA_OK;
+    }
+    if (p->rank || p->owners) return fail(PARBA_EINVAL, "rank/owners given without a degree sequence");
     if (p->d < 1) return fail(PARBA_EINVAL, "uniform degree must be >= 1, got %llu", (unsigned long long)p->d);
     if (p->n < p->n0) return fail(PARBA_EINVAL, "need 0 <= n0 <= n, got n0=%llu, n=%llu",
                                   (unsigned long long)p->n0, (unsigned long long)p->n);
@@ -74,10 +99,14 @@ DevParams make_dev(const parba_params_t *p, uint64_t K = 0) {
     d.k0 = crc32c_u64_bitwise(p->crc_seed0, 0);
     d.k01 = d.k0 ^ crc32c_u64_bitwise(p->crc_seed1, 0);
     d.seed = p->seed_edges;
-    d.div64 = make_magic64(p->d);
-    d.div32 = make_magic32(p->d);
-    d.div32_2d = make_magic32(2 * p->d);
+    const uint64_t dd = p->d ? p->d : 1;  // degree sequences: closed forms unused
+    d.div64 = make_magic64(dd);
+    d.div32 = make_magic32(dd);
+    d.div32_2d = make_magic32(2 * dd);
     d.K = K;
+    d.W = p->degree_prefix;
+    d.rank = (const ulonglong2 *)p->rank;
+    d.owners = p->owners;
     // generated target ((r>>1) - m0)/d + n0 < K  <=>  r < 2*(m0 + (K - n0)*d)
     if (K <= p->n0) {
         d.win_rlim = 0;
@@ -107,7 +136,7 @@ int nc_for(uint64_t two_hi) {
 struct DevInfo {
     int sms = 0;
     int smem_optin = 0;  // max dynamic shared memory per block
-    bool attr_done[8][3][2] = {};  // [hash variant][sink][seed]
+    bool attr_done[12][3][2] = {};  // [hash variant][sink][seed]
 };
 std::mutex g_mu;
 std::vector<DevInfo> g_dev;
@@ -125,14 +154,14 @@ int dev_info(DevInfo **out) {
     return PARBA_OK;
 }
 
-template <class Hash, int SINK, bool SEED>
+template <class Hash, int SINK, bool SEED, bool DEG = false>
 int launch_tiles_t(const DevParams &dp, uint64_t lo, uint64_t hi, const SinkArgs &a,
                    unsigned long long *probes, cudaStream_t st, int variant) {
     if (hi <= lo) return PARBA_OK;
     DevInfo *di;
     int rc = dev_info(&di);
     if (rc) return rc;
-    auto kern = tile_kernel<Hash, SINK, SEED>;
+    auto kern = tile_kernel<Hash, SINK, SEED, DEG>;
     // as many warps per CTA (<= kWarps) as the shared memory allows
     const size_t fixed = TileLayout<Hash, SINK>::fixed, per_warp = TileLayout<Hash, SINK>::per_warp;
     int warps = kWarps;
@@ -180,6 +209,13 @@ template <int SINK>
 int launch_tiles(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi,
                  const SinkArgs &a, unsigned long long *probes, cudaStream_t st) {
     int nc = nc_for(2 * hi);
+    if (is_deg(p)) {  // degree sequence: owner lookups instead of closed forms
+        if (p->hash_kind == PARBA_HASH_SIMPLE)
+            return launch_tiles_t<HashSimple<false>, SINK, true, true>(dp, lo, hi, a, probes, st, 8);
+        if (nc <= 3) return launch_tiles_t<HashCrc<3>, SINK, true, true>(dp, lo, hi, a, probes, st, 9);
+        if (nc <= 5) return launch_tiles_t<HashCrc<5>, SINK, true, true>(dp, lo, hi, a, probes, st, 10);
+        return launch_tiles_t<HashCrc<6>, SINK, true, true>(dp, lo, hi, a, probes, st, 11);
+    }
     if (nc <= 3 && p->d >= (1ull << 31)) nc = 4;  // narrow closed forms need d < 2^31
     if (p->hash_kind == PARBA_HASH_SIMPLE) {
         if (nc <= 3) return launch_tiles_s<HashSimple<true>, SINK>(p, dp, lo, hi, a, probes, st, 4);
@@ -204,7 +240,10 @@ template <class Hash>
 int launch_chains_t(const DevParams &dp, const uint64_t *r0, uint64_t count, uint64_t stop,
                     uint64_t *out, const uint64_t *ids, uint64_t *pairs, unsigned long long *probes,
                     cudaStream_t st) {
-    chains_kernel<Hash><<<grid_for(count, 256), 256, 0, st>>>(dp, r0, count, stop, out, ids, pairs, probes);
+    if (dp.W)
+        chains_kernel<Hash, true><<<grid_for(count, 256), 256, 0, st>>>(dp, r0, count, stop, out, ids, pairs, probes);
+    else
+        chains_kernel<Hash><<<grid_for(count, 256), 256, 0, st>>>(dp, r0, count, stop, out, ids, pairs, probes);
     CUDA_TRY(cudaGetLastError());
     return PARBA_OK;
 }
@@ -222,6 +261,13 @@ template <typename CountT>
 int launch_sources(const DevParams &dp, uint64_t lo, uint64_t hi, uint64_t K, CountT *counts, cudaStream_t st) {
     // nodes whose edges intersect [lo,hi): v in [src(lo), src(hi-1)] and v >= n0, v < K
     if (hi <= lo) return PARBA_OK;
+    if (dp.W) {  // degree sequence: every generated node below K, overlap from W
+        const uint64_t vhi = K < dp.n ? K : dp.n;
+        if (dp.n0 >= vhi) return PARBA_OK;
+        source_counts_kernel<CountT, true><<<grid_for(vhi - dp.n0, 256), 256, 0, st>>>(dp, lo, hi, dp.n0, vhi, counts);
+        CUDA_TRY(cudaGetLastError());
+        return PARBA_OK;
+    }
     const uint64_t vlo = (lo - dp.m0) / dp.d + dp.n0;
     uint64_t vhi = (hi - 1 - dp.m0) / dp.d + dp.n0 + 1;
     if (vhi > K) vhi = K;
@@ -231,11 +277,171 @@ int launch_sources(const DevParams &dp, uint64_t lo, uint64_t hi, uint64_t K, Co
     return PARBA_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Degree sequences and option flags (host side of parba_nodes.cuh)
+
+// Stream-ordered scratch, freed on the same stream.
+struct AsyncBuf {
+    void *p = nullptr;
+    cudaStream_t st = nullptr;
+    ~AsyncBuf() {
+        if (p) cudaFreeAsync(p, st);
+    }
+    int alloc(size_t bytes, cudaStream_t s) {
+        st = s;
+        CUDA_TRY(cudaMallocAsync(&p, bytes ? bytes : 8, s));
+        return PARBA_OK;
+    }
+};
+
+int read_u64s(const uint64_t *dptr, uint64_t *out, size_t n, cudaStream_t st) {
+    CUDA_TRY(cudaMemcpyAsync(out, dptr, n * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return PARBA_OK;
+}
+
+// Degree sequence: node of position pos (m0 <= pos < m) and its edge span.
+int owner_span(const DevParams &dp, uint64_t pos, uint64_t span[3], cudaStream_t st) {
+    AsyncBuf b;
+    int rc = b.alloc(3 * sizeof(uint64_t), st);
+    if (rc) return rc;
+    owner_span_kernel<<<1, 32, 0, st>>>(dp, pos, (uint64_t *)b.p);
+    CUDA_TRY(cudaGetLastError());
+    return read_u64s((const uint64_t *)b.p, span, 3, st);
+}
+
+// Window test of a degree sequence: node < K  <=>  r < 2 * W[K - n0].
+int win_rlim_deg(const parba_params_t *p, DevParams &dp, uint64_t K, cudaStream_t st) {
+    if (K <= p->n0) {
+        dp.win_rlim = 0;
+    } else if (K >= p->n) {
+        dp.win_rlim = 2 * p->m;
+    } else {
+        uint64_t w;
+        int rc = read_u64s(p->degree_prefix + (K - p->n0), &w, 1, st);
+        if (rc) return rc;
+        dp.win_rlim = 2 * w;
+    }
+    dp.win_rlim32 = dp.win_rlim > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)dp.win_rlim;
+    return PARBA_OK;
+}
+
+// Node whose first edge is exactly pos (n when pos == m), else EINVAL
+// (_owner_at_boundary / _check_node_boundary, generator.py:231-245).
+int boundary_node(const parba_params_t *p, const DevParams &dp, uint64_t pos, uint64_t *v, cudaStream_t st) {
+    if (pos == p->m) {
+        *v = p->n;
+        return PARBA_OK;
+    }
+    if (!is_deg(p)) {
+        if ((pos - p->m0) % p->d)
+            return fail(PARBA_EINVAL, "batch boundary %llu is not a node boundary", (unsigned long long)pos);
+        *v = p->n0 + (pos - p->m0) / p->d;
+        return PARBA_OK;
+    }
+    uint64_t span[3];
+    int rc = owner_span(dp, pos, span, st);
+    if (rc) return rc;
+    if (span[1] != pos)
+        return fail(PARBA_EINVAL, "batch boundary %llu is not a node boundary", (unsigned long long)pos);
+    *v = span[0];
+    return PARBA_OK;
+}
+
+uint64_t node_first_edge(const parba_params_t *p, uint64_t v) { return p->m0 + (v - p->n0) * p->d; }
+
+// Edges of nodes [vlo, vhi) (first edge lo) into out, honouring the flags;
+// synchronises st to report an infeasible node (InfeasibleTargetsError).
+int generate_nodes(const parba_params_t *p, const DevParams &dp, uint64_t vlo, uint64_t vhi, uint64_t lo,
+                   uint64_t *out, unsigned long long *probes, cudaStream_t st) {
+    if (vhi <= vlo) return PARBA_OK;
+    NodeArgs na{};
+    na.no_self_loops = (p->flags & PARBA_FLAG_NO_SELF_LOOPS) ? 1u : 0u;
+    na.no_parallel_edges = (p->flags & PARBA_FLAG_NO_PARALLEL_EDGES) ? 1u : 0u;
+    na.max_attempts = p->max_attempts;
+    na.base_seed0 = p->base_seed0;
+    na.base_seed1 = p->base_seed1;
+    na.base_mult = p->base_mult;
+    na.simple = p->hash_kind == PARBA_HASH_SIMPLE ? 1u : 0u;
+    AsyncBuf fe;
+    int rc = fe.alloc(sizeof(unsigned long long), st);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemsetAsync(fe.p, 0xFF, sizeof(unsigned long long), st));
+    const unsigned grid = grid_for(vhi - vlo, 256);
+    if (is_deg(p))
+        node_kernel<true><<<grid, 256, 0, st>>>(dp, na, vlo, vhi, lo, (ulonglong2 *)out, probes,
+                                                (unsigned long long *)fe.p);
+    else
+        node_kernel<false><<<grid, 256, 0, st>>>(dp, na, vlo, vhi, lo, (ulonglong2 *)out, probes,
+                                                 (unsigned long long *)fe.p);
+    CUDA_TRY(cudaGetLastError());
+    uint64_t edge;
+    rc = read_u64s((const uint64_t *)fe.p, &edge, 1, st);
+    if (rc) return rc;
+    if (edge == UINT64_MAX) return PARBA_OK;
+    uint64_t v, deg;
+    if (is_deg(p)) {
+        uint64_t span[3];
+        rc = owner_span(dp, edge, span, st);
+        if (rc) return rc;
+        v = span[0];
+        deg = span[2] - span[1];
+    } else {
+        v = p->n0 + (edge - p->m0) / p->d;
+        deg = p->d;
+    }
+    const uint64_t cap = p->max_attempts ? p->max_attempts : 64 * deg;
+    return fail(PARBA_EINFEASIBLE,
+                "edge %llu of node %llu: no fresh target in %llu attempts "
+                "(distinct-target pool may be smaller than the degree)",
+                (unsigned long long)edge, (unsigned long long)v, (unsigned long long)cap);
+}
+
+// Degree counts of [lo, hi) with option flags: node-aligned chunks generated
+// into scratch, then counted (both endpoints < K).
+template <typename CountT>
+int count_nodes(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi, uint64_t K,
+                CountT *counts, unsigned long long *probes, cudaStream_t st) {
+    uint64_t vlo, vhi;
+    int rc = boundary_node(p, dp, lo, &vlo, st);
+    if (!rc) rc = boundary_node(p, dp, hi, &vhi, st);
+    if (rc) return rc;
+    const uint64_t step = is_deg(p) ? (1ull << 20) : ((1ull << 24) / p->d > 0 ? (1ull << 24) / p->d : 1);
+    for (uint64_t v = vlo; v < vhi;) {
+        const uint64_t v1 = vhi - v > step ? v + step : vhi;
+        uint64_t a, b;
+        if (is_deg(p)) {
+            uint64_t w[2];
+            rc = read_u64s(p->degree_prefix + (v - p->n0), &w[0], 1, st);
+            if (!rc) rc = read_u64s(p->degree_prefix + (v1 - p->n0), &w[1], 1, st);
+            if (rc) return rc;
+            a = w[0];
+            b = w[1];
+        } else {
+            a = node_first_edge(p, v);
+            b = node_first_edge(p, v1);
+        }
+        if (b > a) {
+            AsyncBuf scratch;
+            rc = scratch.alloc((b - a) * 16, st);
+            if (!rc) rc = generate_nodes(p, dp, v, v1, a, (uint64_t *)scratch.p, probes, st);
+            if (rc) return rc;
+            if (K > 0) {
+                count_pairs_kernel<CountT><<<grid_for(b - a, 256), 256, 0, st>>>(
+                    (const ulonglong2 *)scratch.p, b - a, K, counts);
+                CUDA_TRY(cudaGetLastError());
+            }
+        }
+        v = v1;
+    }
+    return PARBA_OK;
+}
+
 }  // namespace
 
 extern "C" {
 
-int parba_version(void) { return 10000; }
+int parba_version(void) { return 20000; }
 
 const char *parba_last_error(void) { return g_err.c_str(); }
 
@@ -282,8 +488,17 @@ int parba_generate(const parba_params_t *p, uint64_t lo, uint64_t hi, uint64_t *
     if (hi == lo) return PARBA_OK;
     if (!out_pairs) return fail(PARBA_EINVAL, "out_pairs is NULL");
     if (((uintptr_t)out_pairs) & 15) return fail(PARBA_EINVAL, "out_pairs must be 16-byte aligned");
+    cudaStream_t st = (cudaStream_t)stream;
+    const DevParams dp = make_dev(p);
+    if (p->flags) {  // node-granular (generator.py:272-302)
+        uint64_t vlo, vhi;
+        rc = boundary_node(p, dp, lo, &vlo, st);
+        if (!rc) rc = boundary_node(p, dp, hi, &vhi, st);
+        if (rc) return rc;
+        return generate_nodes(p, dp, vlo, vhi, lo, out_pairs, probes, st);
+    }
     SinkArgs a{out_pairs, nullptr, nullptr};
-    return launch_tiles<kStore>(p, make_dev(p), lo, hi, a, probes, (cudaStream_t)stream);
+    return launch_tiles<kStore>(p, dp, lo, hi, a, probes, st);
 }
 
 int parba_edges_at(const parba_params_t *p, const uint64_t *ids, uint64_t count, uint64_t *out_pairs,
@@ -293,6 +508,8 @@ int parba_edges_at(const parba_params_t *p, const uint64_t *ids, uint64_t count,
     if (count == 0) return PARBA_OK;
     if (!ids || !out_pairs) return fail(PARBA_EINVAL, "NULL buffer");
     if (((uintptr_t)out_pairs) & 15) return fail(PARBA_EINVAL, "out_pairs must be 16-byte aligned");
+    if (p->flags)
+        return fail(PARBA_EINVAL, "option flags need whole-node processing; use generate_node_edges");
     const DevParams dp = make_dev(p);
     return launch_chains(p, dp, nullptr, count, dp.stop, nullptr, ids, out_pairs, probes, (cudaStream_t)stream);
 }
@@ -305,7 +522,12 @@ int parba_degree_window(const parba_params_t *p, uint64_t lo, uint64_t hi, uint6
     if (hi == lo) return PARBA_OK;
     if (K > 0 && !counts) return fail(PARBA_EINVAL, "counts is NULL");
     cudaStream_t st = (cudaStream_t)stream;
-    const DevParams dp = make_dev(p, K);
+    DevParams dp = make_dev(p, K);
+    if (p->flags) return count_nodes<unsigned long long>(p, dp, lo, hi, K, counts, probes, st);
+    if (is_deg(p)) {
+        rc = win_rlim_deg(p, dp, K, st);
+        if (rc) return rc;
+    }
     SinkArgs a{nullptr, counts, nullptr};
     rc = launch_tiles<kWindow>(p, dp, lo, hi, a, probes, st);
     if (rc) return rc;
@@ -321,6 +543,7 @@ int parba_degree_full(const parba_params_t *p, uint64_t lo, uint64_t hi, uint32_
     if (!counts) return fail(PARBA_EINVAL, "counts is NULL");
     cudaStream_t st = (cudaStream_t)stream;
     const DevParams dp = make_dev(p, p->n);
+    if (p->flags) return count_nodes<uint32_t>(p, dp, lo, hi, p->n, counts, probes, st);
     SinkArgs a{nullptr, nullptr, counts};
     rc = launch_tiles<kFull>(p, dp, lo, hi, a, probes, st);
     if (rc) return rc;
@@ -331,6 +554,133 @@ int parba_count_ids(const uint64_t *ids, uint64_t count, uint64_t K, unsigned lo
     if (count == 0 || K == 0) return PARBA_OK;
     if (!ids || !counts) return fail(PARBA_EINVAL, "NULL buffer");
     count_ids_kernel<<<grid_for(count, 256), 256, 0, (cudaStream_t)stream>>>(ids, count, K, counts);
+    CUDA_TRY(cudaGetLastError());
+    return PARBA_OK;
+}
+
+int parba_count_pairs(const uint64_t *pairs, uint64_t count, uint64_t K, unsigned long long *counts,
+                      void *stream) {
+    if (count == 0 || K == 0) return PARBA_OK;
+    if (!pairs || !counts) return fail(PARBA_EINVAL, "NULL buffer");
+    count_pairs_kernel<unsigned long long><<<grid_for(count, 256), 256, 0, (cudaStream_t)stream>>>(
+        (const ulonglong2 *)pairs, count, K, counts);
+    CUDA_TRY(cudaGetLastError());
+    return PARBA_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Degree-sequence index (f4).
+
+int parba_degseq_prefix(const uint64_t *degrees, uint64_t count, uint64_t m0, uint64_t *W, void *stream) {
+    if (!W) return fail(PARBA_EINVAL, "W is NULL");
+    if (count > 0 && !degrees) return fail(PARBA_EINVAL, "degrees is NULL");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (count > 0) {
+        size_t tmp_bytes = 0;
+        CUDA_TRY(cub::DeviceScan::ExclusiveScan(nullptr, tmp_bytes, degrees, W, cub::Sum(), (uint64_t)m0,
+                                                (int64_t)count, st));
+        AsyncBuf tmp;
+        int rc = tmp.alloc(tmp_bytes, st);
+        if (rc) return rc;
+        CUDA_TRY(cub::DeviceScan::ExclusiveScan(tmp.p, tmp_bytes, degrees, W, cub::Sum(), (uint64_t)m0,
+                                                (int64_t)count, st));
+    }
+    degseq_last_kernel<<<1, 32, 0, st>>>(degrees, count, m0, W);
+    CUDA_TRY(cudaGetLastError());
+    return PARBA_OK;
+}
+
+int parba_degseq_rank(const uint64_t *W, uint64_t count, uint64_t m, uint64_t n0, void *rank,
+                      uint64_t *owners, uint64_t *n_ones, void *stream) {
+    if (!W) return fail(PARBA_EINVAL, "W is NULL");
+    if (m >= kMaxEdges) return fail(PARBA_EINVAL, "total edge count %llu exceeds the supported maximum",
+                                    (unsigned long long)m);
+    cudaStream_t st = (cudaStream_t)stream;
+    const uint64_t words = (m + 63) / 64;
+    if (words == 0) {
+        if (n_ones) *n_ones = 0;
+        return PARBA_OK;
+    }
+    if (!rank) return fail(PARBA_EINVAL, "rank is NULL");
+    ulonglong2 *rk = (ulonglong2 *)rank;
+    CUDA_TRY(cudaMemsetAsync(rk, 0, words * sizeof(ulonglong2), st));
+    if (count > 0) {
+        rank_mark_kernel<<<grid_for(count, 256), 256, 0, st>>>(W, count, rk);
+        CUDA_TRY(cudaGetLastError());
+    }
+    AsyncBuf cnt, before, tmp;
+    int rc = cnt.alloc(words * sizeof(uint64_t), st);
+    if (!rc) rc = before.alloc(words * sizeof(uint64_t), st);
+    if (rc) return rc;
+    rank_popc_kernel<<<grid_for(words, 256), 256, 0, st>>>(rk, words, (uint64_t *)cnt.p);
+    CUDA_TRY(cudaGetLastError());
+    size_t tmp_bytes = 0;
+    CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, (const uint64_t *)cnt.p, (uint64_t *)before.p,
+                                           (int64_t)words, st));
+    rc = tmp.alloc(tmp_bytes, st);
+    if (rc) return rc;
+    CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, (const uint64_t *)cnt.p, (uint64_t *)before.p,
+                                           (int64_t)words, st));
+    rank_before_kernel<<<grid_for(words, 256), 256, 0, st>>>(rk, (const uint64_t *)before.p, words);
+    CUDA_TRY(cudaGetLastError());
+    if (owners && count > 0) {
+        owners_kernel<<<grid_for(count, 256), 256, 0, st>>>(W, count, n0, rk, owners);
+        CUDA_TRY(cudaGetLastError());
+    }
+    if (n_ones) {
+        uint64_t v[2];
+        rc = read_u64s((const uint64_t *)before.p + (words - 1), &v[0], 1, st);
+        if (!rc) rc = read_u64s((const uint64_t *)cnt.p + (words - 1), &v[1], 1, st);
+        if (rc) return rc;
+        *n_ones = v[0] + v[1];
+    }
+    return PARBA_OK;
+}
+
+int parba_rank1(const void *rank, const uint64_t *es, uint64_t count, uint64_t *out, void *stream) {
+    if (count == 0) return PARBA_OK;
+    if (!rank || !es || !out) return fail(PARBA_EINVAL, "NULL buffer");
+    rank1_kernel<<<grid_for(count, 256), 256, 0, (cudaStream_t)stream>>>((const ulonglong2 *)rank, es, count, out);
+    CUDA_TRY(cudaGetLastError());
+    return PARBA_OK;
+}
+
+int parba_node_of_edges(const parba_params_t *p, const uint64_t *es, uint64_t count, uint64_t *out,
+                        uint32_t method, void *stream) {
+    int rc = validate(p);
+    if (rc) return rc;
+    if (method > PARBA_RESOLVE_DEFERRED) return fail(PARBA_EINVAL, "unknown resolution %u", method);
+    if (!is_deg(p)) return fail(PARBA_EINVAL, "uniform-degree parameters have no prefix index");
+    if (count == 0) return PARBA_OK;
+    if (!es || !out) return fail(PARBA_EINVAL, "NULL buffer");
+    cudaStream_t st = (cudaStream_t)stream;
+    const DevParams dp = make_dev(p);
+    const uint64_t n_nodes = p->n - p->n0;
+    if (method == PARBA_RESOLVE_RANK) {
+        node_of_rank_kernel<<<grid_for(count, 256), 256, 0, st>>>(dp, es, count, out);
+    } else if (method == PARBA_RESOLVE_BISECT) {
+        node_of_bisect_kernel<<<grid_for(count, 256), 256, 0, st>>>(dp, es, count, n_nodes, out);
+    } else {
+        AsyncBuf idx, skeys, sidx, tmp;
+        rc = idx.alloc(count * 8, st);
+        if (!rc) rc = skeys.alloc(count * 8, st);
+        if (!rc) rc = sidx.alloc(count * 8, st);
+        if (rc) return rc;
+        iota_kernel<<<grid_for(count, 256), 256, 0, st>>>((uint64_t *)idx.p, count);
+        CUDA_TRY(cudaGetLastError());
+        size_t tmp_bytes = 0;
+        CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, es, (uint64_t *)skeys.p,
+                                                 (const uint64_t *)idx.p, (uint64_t *)sidx.p, (int64_t)count,
+                                                 0, 64, st));
+        rc = tmp.alloc(tmp_bytes, st);
+        if (rc) return rc;
+        CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, es, (uint64_t *)skeys.p,
+                                                 (const uint64_t *)idx.p, (uint64_t *)sidx.p, (int64_t)count,
+                                                 0, 64, st));
+        const uint64_t runs = (count + kMergeRun - 1) / kMergeRun;
+        merge_owner_kernel<<<grid_for(runs, 128), 128, 0, st>>>(dp, (const uint64_t *)skeys.p,
+                                                                (const uint64_t *)sidx.p, count, n_nodes, out);
+    }
     CUDA_TRY(cudaGetLastError());
     return PARBA_OK;
 }
@@ -377,6 +727,7 @@ struct EventGuard {
 
 int parba_generate_host(const parba_params_t *ph, uint64_t lo, uint64_t hi, uint64_t *out_host,
                         uint64_t *probes_host, int device) {
+    if (ph && is_deg(ph)) return fail(PARBA_EINVAL, "host entry points take uniform-degree families only");
     int rc = validate(ph);
     if (!rc) rc = check_range(ph, lo, hi);
     if (rc) return rc;
@@ -426,6 +777,7 @@ int parba_generate_host(const parba_params_t *ph, uint64_t lo, uint64_t hi, uint
 
 int parba_degree_window_host(const parba_params_t *ph, uint64_t lo, uint64_t hi, uint64_t K,
                              int64_t *counts_host, uint64_t *probes_host, int device) {
+    if (ph && is_deg(ph)) return fail(PARBA_EINVAL, "host entry points take uniform-degree families only");
     int rc = validate(ph);
     if (!rc) rc = check_range(ph, lo, hi);
     if (rc) return rc;

@@ -94,11 +94,34 @@ struct DevParams {
     uint64_t win_rlim;     // window mode: generated target < K  <=>  r < win_rlim
     uint32_t win_rlim32;   // min(win_rlim, 2^32 - 1) for narrow launches
     uint64_t K;
+    // degree sequences (f4): node of a position by rank (degreeseq.py:145-178)
+    const uint64_t *W;         // W[k] = first edge of node n0+k, W[n-n0] = m
+    const ulonglong2 *rank;    // per 64 positions: {start bits, ones before}
+    const uint64_t *owners;    // rank -> node, NULL when every degree >= 1
 };
 
+// Rank directory of a degree sequence: one 16-byte entry per 64 positions,
+// x = bit j set iff a node with degree >= 1 starts at position 64w+j,
+// y = number of such starts before position 64w.  One LDG.128 per lookup
+// (the reference's two-level 512-bit superblock directory, degreeseq.py:
+// 118-151, traded for a single sector read).
+__device__ __forceinline__ uint64_t rank1_dev(const ulonglong2 *rank, uint64_t e) {
+    const ulonglong2 w = __ldg(rank + (e >> 6));
+    const uint64_t mask = ~(0xFFFFFFFFFFFFFFFEull << (e & 63));  // bits 0..e&63
+    return w.y + (uint64_t)__popcll(w.x & mask);
+}
+// Owning node of generated position e (m0 <= e < m): node_of_edge
+// (degreeseq.py:165-178) -- the last node with W <= e and degree >= 1.
+__device__ __forceinline__ uint64_t node_of(uint64_t e, const DevParams &p) {
+    const uint64_t r = rank1_dev(p.rank, e);
+    return p.owners ? __ldg(p.owners + r - 1) : p.n0 + r - 1;
+}
+
 // Closed forms (generator.py:157-169): source of edge i, target of terminal r.
-template <bool NARROW, bool SEED>
+// DEG: degree sequence, node_of instead of the division by d.
+template <bool NARROW, bool SEED, bool DEG = false>
 __device__ __forceinline__ uint64_t source_of(uint64_t i, const DevParams &p) {
+    if constexpr (DEG) return node_of(i, p);
     if constexpr (NARROW) {
         if constexpr (SEED) return (uint64_t)magic_div32((uint32_t)(i - p.m0), p.div32) + p.n0;
         else return (uint64_t)magic_div32((uint32_t)i, p.div32);
@@ -109,11 +132,12 @@ __device__ __forceinline__ uint64_t source_of(uint64_t i, const DevParams &p) {
 }
 // R31: every chain value < 2^31, so floor(((r>>1) - m0)/d) = floor((r - 2m0)/(2d))
 // is one 32-bit multiply-high division.
-template <bool NARROW, bool SEED, bool R31 = false>
+template <bool NARROW, bool SEED, bool R31 = false, bool DEG = false>
 __device__ __forceinline__ uint64_t target_of(uint64_t r, const DevParams &p) {
     if constexpr (SEED) {
         if (r < p.stop) return __ldg(p.seed + r);
     }
+    if constexpr (DEG) return node_of(r >> 1, p);
     if constexpr (R31) {
         if constexpr (SEED) return (uint64_t)magic_div32((uint32_t)(r - p.stop), p.div32_2d) + p.n0;
         else return (uint64_t)magic_div32((uint32_t)r, p.div32_2d);

@@ -89,7 +89,7 @@ constexpr uint64_t kValueMask52 = (1ull << 52) - 1;
 constexpr uint64_t kLaunchEdgesPerWarp = 1ull << 27;
 
 // A chain finished with terminal value r: hand its target to the sink.
-template <bool NARROW, bool SEED, int SINK, class R>
+template <bool NARROW, bool SEED, int SINK, class R, bool DEG = false>
 __device__ __forceinline__ void finish(uint32_t saddr, uint64_t r, const DevParams &p, const SinkArgs &a) {
     if constexpr (SINK == kStore) {
         sts_t<R>(saddr, (R)r);  // stage cell; the target is computed at flush
@@ -99,14 +99,14 @@ __device__ __forceinline__ void finish(uint32_t saddr, uint64_t r, const DevPara
             if (t < p.K) atomicAdd(a.win + t, 1ull);
         } else if (NARROW ? ((uint32_t)r < p.win_rlim32) : (r < p.win_rlim)) {
             // generated target < K  <=>  r < win_rlim
-            atomicAdd(a.win + source_of<NARROW, SEED>(r >> 1, p), 1ull);
+            atomicAdd(a.win + source_of<NARROW, SEED, DEG>(r >> 1, p), 1ull);
         }
     } else {
-        atomicAdd(a.full + target_of<NARROW, SEED>(r, p), 1u);
+        atomicAdd(a.full + target_of<NARROW, SEED, false, DEG>(r, p), 1u);
     }
 }
 
-template <class Hash, int SINK, bool SEED>
+template <class Hash, int SINK, bool SEED, bool DEG = false>
 __global__ void __launch_bounds__(kThreads, SINK == kStore ? PARBA_MINB_STORE : PARBA_MINB_STREAM)
 tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntiles,
             SinkArgs a, unsigned long long *probes_out) {
@@ -170,9 +170,9 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
                 const uint32_t j = lane + 32u * k;
                 const uint64_t i = base + j;
                 if (FULL || (i >= lo && i < hi)) {
-                    const uint64_t tgt = target_of<NARROW, SEED, Hash::kR31>(
+                    const uint64_t tgt = target_of<NARROW, SEED, Hash::kR31 && !DEG, DEG>(
                         (uint64_t)lds_t<R>(stage_s + (b * kTile + j) * (uint32_t)sizeof(R)), p);
-                    __stcs(o + j, make_ulonglong2(source_of<NARROW, SEED>(i, p), tgt));
+                    __stcs(o + j, make_ulonglong2(source_of<NARROW, SEED, DEG>(i, p), tgt));
                 }
             }
         }
@@ -197,7 +197,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
         const uint32_t fin = act & (cont ^ 1u);
         act &= cont;
         r = nr;
-        if (fin) finish<NARROW, SEED, SINK, R>(saddr, (uint64_t)nr, p, a);
+        if (fin) finish<NARROW, SEED, SINK, R, DEG>(saddr, (uint64_t)nr, p, a);
     };
 
     // Pop queued chains into idle lanes.  FULLQ: at least 32 entries queued,
@@ -263,7 +263,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
             [[maybe_unused]] const uint32_t cell = stage_s + (buf * kTile + j) * (uint32_t)sizeof(R);
             if constexpr (SINK == kStore)  // final unless pending
                 sts_t<R>(cell, r1);
-            if constexpr (SINK != kStore) if (valid && done) finish<NARROW, SEED, SINK, R>(0u, (uint64_t)r1, p, a);
+            if constexpr (SINK != kStore) if (valid && done) finish<NARROW, SEED, SINK, R, DEG>(0u, (uint64_t)r1, p, a);
             const bool pend = valid && !done;
             const unsigned m = ballot_all(pend);
             const uint32_t cur = tailb + (__popc(m & ltmask) << L::kLgEB);
@@ -351,7 +351,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
 // Generic kernels (not the bench path): arbitrary chain starts / ID lists,
 // full 64-bit values.
 
-template <class Hash>
+template <class Hash, bool DEG = false>
 __global__ void __launch_bounds__(256)
 chains_kernel(DevParams p, const uint64_t *__restrict__ r0, uint64_t count, uint64_t stop,
               uint64_t *__restrict__ out, const uint64_t *__restrict__ ids,
@@ -370,7 +370,7 @@ chains_kernel(DevParams p, const uint64_t *__restrict__ r0, uint64_t count, uint
         } while (!(r < stop || (r & 1ull) == 0));
         if (ids) {
             reinterpret_cast<ulonglong2 *>(pairs)[k] =
-                make_ulonglong2(source_of<false, true>(ids[k], p), target_of<false, true>(r, p));
+                make_ulonglong2(source_of<false, true, DEG>(ids[k], p), target_of<false, true, false, DEG>(r, p));
         } else {
             out[k] = r;
         }
@@ -394,13 +394,21 @@ hash_kernel(DevParams p, const uint64_t *__restrict__ r, uint64_t count, uint64_
 }
 
 // Source endpoints of a window/full count in closed form: node v owns edges
-// [m0+(v-n0)d, m0+(v-n0+1)d); its count grows by the overlap with [lo,hi).
-template <typename CountT>
+// [m0+(v-n0)d, m0+(v-n0+1)d) (degree sequence: [W[v-n0], W[v-n0+1])); its
+// count grows by the overlap with [lo,hi).
+template <typename CountT, bool DEG = false>
 __global__ void source_counts_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t vlo,
                                      uint64_t vhi, CountT *counts) {
     for (uint64_t v = vlo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < vhi;
          v += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t a = p.m0 + (v - p.n0) * p.d, b = a + p.d;
+        uint64_t a, b;
+        if constexpr (DEG) {
+            a = __ldg(p.W + (v - p.n0));
+            b = __ldg(p.W + (v - p.n0) + 1);
+        } else {
+            a = p.m0 + (v - p.n0) * p.d;
+            b = a + p.d;
+        }
         const uint64_t x = a > lo ? a : lo, y = b < hi ? b : hi;
         if (y > x) counts[v] += (CountT)(y - x);
     }

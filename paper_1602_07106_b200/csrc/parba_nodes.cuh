@@ -1,0 +1,263 @@
+// parba_nodes.cuh -- node-granular kernels: the degree-sequence index (f4)
+// and the option flags no_self_loops / no_parallel_edges (f3).
+//
+// Degree sequences (degreeseq.py): W[k] = m0 + sum of the degrees of nodes
+// n0..n0+k-1 (exclusive scan on the device), W[n-n0] = m.  The owner of a
+// position is found by rank over a bit vector with a one at every first edge
+// of a node of degree >= 1 (parba_device.cuh: rank1_dev / node_of); the
+// reference's binary search and deferred sort-and-merge lookups run here too
+// (identical results, exercised by the parity tests).
+//
+// Option flags (generator.py:184-246): chains become node-granular.  With
+// no_self_loops every edge of node v starts at r0 = 2*W_v (so all d chains of
+// v coincide and resolve strictly before v); with no_parallel_edges edge i
+// re-runs its chain under attempt-salted families 0, 1, 2, ... until its
+// target is not among the node's earlier targets.  One thread walks one node
+// in edge order -- exactly the reference's sequential rule -- while nodes
+// run in parallel; a node's accepted targets live in the output it writes.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "parba_device.cuh"
+
+namespace parba {
+
+// ---------------------------------------------------------------------------
+// Degree-sequence index
+
+// W[count] = W[count-1] + deg[count-1] (m0 when count == 0).
+__global__ void degseq_last_kernel(const uint64_t *deg, uint64_t count, uint64_t m0, uint64_t *W) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) W[count] = count ? W[count - 1] + deg[count - 1] : m0;
+}
+
+// One bit per first edge of a node with degree >= 1 (degreeseq.py:118-124).
+__global__ void rank_mark_kernel(const uint64_t *__restrict__ W, uint64_t count, ulonglong2 *rank) {
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t a = W[k], b = W[k + 1];
+        if (b > a) atomicOr(reinterpret_cast<unsigned long long *>(&rank[a >> 6].x), 1ull << (a & 63));
+    }
+}
+
+__global__ void rank_popc_kernel(const ulonglong2 *__restrict__ rank, uint64_t words, uint64_t *cnt) {
+    for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words;
+         w += (uint64_t)gridDim.x * blockDim.x)
+        cnt[w] = (uint64_t)__popcll(rank[w].x);
+}
+
+__global__ void rank_before_kernel(ulonglong2 *rank, const uint64_t *__restrict__ before, uint64_t words) {
+    for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words;
+         w += (uint64_t)gridDim.x * blockDim.x)
+        rank[w].y = before[w];
+}
+
+// owners[rank - 1] = node, for nodes of degree >= 1 (degreeseq.py:136-139).
+__global__ void owners_kernel(const uint64_t *__restrict__ W, uint64_t count, uint64_t n0,
+                              const ulonglong2 *__restrict__ rank, uint64_t *owners) {
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t a = W[k], b = W[k + 1];
+        if (b > a) owners[rank1_dev(rank, a) - 1] = n0 + k;
+    }
+}
+
+__global__ void rank1_kernel(const ulonglong2 *__restrict__ rank, const uint64_t *__restrict__ es,
+                             uint64_t count, uint64_t *out) {
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count;
+         k += (uint64_t)gridDim.x * blockDim.x)
+        out[k] = rank1_dev(rank, es[k]);
+}
+
+// node_of_edge_many (degreeseq.py:181-185): rank path.
+__global__ void node_of_rank_kernel(DevParams p, const uint64_t *__restrict__ es, uint64_t count,
+                                    uint64_t *out) {
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count;
+         k += (uint64_t)gridDim.x * blockDim.x)
+        out[k] = node_of(es[k], p);
+}
+
+// Rightmost k in [lo, hi) with W[k] <= e (W sorted; zero-degree nodes share
+// their successor's W and are skipped by the right bias), degreeseq.py:188-196.
+__device__ __forceinline__ uint64_t upper_bound_m1(const uint64_t *W, uint64_t lo, uint64_t hi, uint64_t e) {
+    while (lo < hi) {
+        const uint64_t mid = lo + (hi - lo) / 2;
+        if (__ldg(W + mid) <= e) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo - 1;
+}
+
+__global__ void node_of_bisect_kernel(DevParams p, const uint64_t *__restrict__ es, uint64_t count,
+                                      uint64_t n_nodes, uint64_t *out) {
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count;
+         k += (uint64_t)gridDim.x * blockDim.x)
+        out[k] = p.n0 + upper_bound_m1(p.W, 0, n_nodes, es[k]);
+}
+
+// Deferred path (degreeseq.py:204-216, _kernels.py:101-118): keys sorted on
+// the device (CUB radix sort), then each thread merges a run of kMergeRun
+// consecutive sorted keys against W -- one binary search for the run's first
+// key, then a forward walk (bounded; a long gap falls back to a search) --
+// and scatters the owners back to the keys' original slots.
+constexpr int kMergeRun = 64;
+__global__ void merge_owner_kernel(DevParams p, const uint64_t *__restrict__ skeys,
+                                   const uint64_t *__restrict__ sidx, uint64_t count, uint64_t n_nodes,
+                                   uint64_t *out) {
+    const uint64_t runs = (count + kMergeRun - 1) / kMergeRun;
+    for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < runs;
+         r += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t a = r * kMergeRun, b = a + kMergeRun < count ? a + kMergeRun : count;
+        uint64_t k = upper_bound_m1(p.W, 0, n_nodes, skeys[a]);
+        for (uint64_t j = a; j < b; ++j) {
+            const uint64_t e = skeys[j];
+            int steps = 0;
+            while (k + 1 < n_nodes && __ldg(p.W + k + 1) <= e && steps < 16) {
+                ++k;
+                ++steps;
+            }
+            if (steps == 16) k = upper_bound_m1(p.W, k, n_nodes, e);
+            out[sidx[j]] = p.n0 + k;
+        }
+    }
+}
+
+__global__ void iota_kernel(uint64_t *v, uint64_t count) {
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count;
+         k += (uint64_t)gridDim.x * blockDim.x)
+        v[k] = k;
+}
+
+// out[0] = node owning position pos (m0 <= pos < m), out[1] = its first edge,
+// out[2] = its end (first edge + degree).
+__global__ void owner_span_kernel(DevParams p, uint64_t pos, uint64_t *out) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        const uint64_t v = node_of(pos, p);
+        out[0] = v;
+        out[1] = p.W[v - p.n0];
+        out[2] = p.W[v - p.n0 + 1];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Option flags
+
+struct NodeArgs {
+    uint32_t no_self_loops, no_parallel_edges;
+    uint64_t max_attempts;  // 0: 64 * degree (generator.py:205)
+    uint32_t base_seed0, base_seed1;  // attempt a >= 1: salt a on the unsalted seeds
+    uint64_t base_mult;
+    uint32_t simple;
+};
+
+// One hash family of the retry sequence (HashConfig.with_attempt,
+// hashing.py:69-85): attempt 0 is the configured family itself.
+struct Family {
+    uint32_t k0, k01;
+    uint64_t mult;
+};
+
+__device__ __forceinline__ Family family_of(uint64_t attempt, const DevParams &p, const NodeArgs &na) {
+    if (attempt == 0) return Family{p.k0, p.k01, p.mult};
+    const uint32_t s0 = na.base_seed0 + (uint32_t)attempt;
+    const uint32_t s1 = na.base_seed1 + (uint32_t)attempt * 0x9E3779B9u;
+    Family f;
+    f.k0 = crc32c_u64_bitwise(s0, 0);
+    f.k01 = f.k0 ^ crc32c_u64_bitwise(s1, 0);
+    f.mult = na.base_mult + 2ull * attempt * 0x9E3779B97F4A7C15ull;
+    return f;
+}
+
+// h(r) under family f; tab = seed-free byte tables (crc(0, .)).
+__device__ __forceinline__ uint64_t hash_family(uint32_t tab, uint64_t r, const Family &f, bool simple) {
+    if (simple) return __umul64hi(r * f.mult, r);
+    const uint32_t c0 = crc_bytes<8>(tab, r) ^ f.k0;
+    return mod_int(c0, c0 ^ f.k01, r);
+}
+
+// resolve_chain (generator.py:139-154): body at least once.
+__device__ __forceinline__ uint64_t chain_family(uint32_t tab, uint64_t r, const Family &f, bool simple,
+                                                 uint64_t stop, uint64_t &probes) {
+    do {
+        r = hash_family(tab, r, f, simple);
+        ++probes;
+    } while (!(r < stop || (r & 1ull) == 0));
+    return r;
+}
+
+// Edges of nodes [vlo, vhi) into out (row i - lo), honouring the flags
+// (_node_edges_with_probes, generator.py:184-217).  fail_edge receives the
+// smallest edge index that found no fresh target (InfeasibleTargetsError).
+template <bool DEG>
+__global__ void __launch_bounds__(256)
+node_kernel(DevParams p, NodeArgs na, uint64_t vlo, uint64_t vhi, uint64_t lo, ulonglong2 *out,
+            unsigned long long *probes_out, unsigned long long *fail_edge) {
+    __shared__ uint32_t tabs_p[8 * 256];
+    build_byte_tables(tabs_p, 8, 0u);
+    __syncthreads();
+    const uint32_t tab = opaque(smem_addr(tabs_p));
+    const bool simple = na.simple != 0;
+    uint64_t probes = 0;
+    for (uint64_t v = vlo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < vhi;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t first, dv;
+        if constexpr (DEG) {
+            first = __ldg(p.W + (v - p.n0));
+            dv = __ldg(p.W + (v - p.n0) + 1) - first;
+        } else {
+            first = p.m0 + (v - p.n0) * p.d;
+            dv = p.d;
+        }
+        if (dv == 0) continue;
+        if (!na.no_parallel_edges) {
+            // no_self_loops alone: every edge of v runs the same chain
+            uint64_t pr = 0;
+            const Family f0{p.k0, p.k01, p.mult};
+            const uint64_t r = chain_family(tab, 2 * first, f0, simple, p.stop, pr);
+            probes += pr * dv;
+            const uint64_t t = target_of<false, true, false, DEG>(r, p);
+            for (uint64_t i = first; i < first + dv; ++i) out[i - lo] = make_ulonglong2(v, t);
+            continue;
+        }
+        const uint64_t cap = na.max_attempts ? na.max_attempts : 64 * dv;
+        for (uint64_t i = first; i < first + dv; ++i) {
+            const uint64_t r0 = na.no_self_loops ? 2 * first : 2 * i + 1;
+            uint64_t t = 0;
+            bool fresh = false;
+            for (uint64_t attempt = 0; attempt < cap && !fresh; ++attempt) {
+                const Family f = family_of(attempt, p, na);
+                const uint64_t r = chain_family(tab, r0, f, simple, p.stop, probes);
+                t = target_of<false, true, false, DEG>(r, p);
+                fresh = true;
+                for (uint64_t j = first; j < i; ++j)  // the node's accepted targets so far
+                    if (out[j - lo].y == t) {
+                        fresh = false;
+                        break;
+                    }
+            }
+            if (!fresh) {
+                atomicMin(fail_edge, (unsigned long long)i);
+                break;
+            }
+            out[i - lo] = make_ulonglong2(v, t);
+        }
+    }
+    if (probes_out) {
+        for (int o = 16; o > 0; o >>= 1) probes += __shfl_xor_sync(0xffffffffu, probes, o);
+        if ((threadIdx.x & 31) == 0 && probes) atomicAdd(probes_out, (unsigned long long)probes);
+    }
+}
+
+// count_block over stored pairs (analytics.py:44-48): both endpoints < K.
+template <typename CountT>
+__global__ void count_pairs_kernel(const ulonglong2 *__restrict__ pairs, uint64_t count, uint64_t K,
+                                   CountT *counts) {
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        const ulonglong2 e = pairs[k];
+        if (e.x < K) atomicAdd(counts + e.x, (CountT)1);
+        if (e.y < K) atomicAdd(counts + e.y, (CountT)1);
+    }
+}
+
+}  // namespace parba

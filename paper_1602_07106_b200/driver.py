@@ -175,7 +175,7 @@ def run(p: GenParams, consumer: Consumer, workers: int = 1, batch_size: int = DE
         merged = p.m - p.m0
     elif isinstance(consumer, io.EdgeFileWriter):
         rank, ws = parallel.world()
-        a, b = parallel.shard_range(p.m0, p.m, rank, ws)
+        a, b = parallel.shard_range_for(p, p.m0, p.m, rank, ws)
         if ws > 1:
             import torch.distributed as dist
 

@@ -8,9 +8,10 @@ generator.py:139-181).  Here the chains run in the CUDA kernels of
 argument meaning and return types so it is a drop-in for the plain
 (uniform-degree) path.
 
-Not on the B200 path (raise ``ParameterError`` instead
-of falling back to a CPU implementation): degree sequences (f4) and the
-option flags no_self_loops / no_parallel_edges (f3).
+Degree sequences (f4) run in the same tile kernels with owner lookups by
+rank instead of the division by d (index built on the device by
+``degreeseq``); the option flags no_self_loops / no_parallel_edges (f3) run in
+the node-granular kernel (include/parba_b200.h, "Option flags").
 """
 
 from __future__ import annotations
@@ -20,7 +21,7 @@ from typing import Literal, NamedTuple
 
 import numpy as np
 
-from . import _lib
+from . import _lib, degreeseq
 from .errors import ParameterError
 from .hashing import HashConfig, c_params
 
@@ -82,11 +83,13 @@ class GenParams:
             raise ParameterError("seed graph references node IDs >= n0")
         object.__setattr__(self, "seed_edges", seed)
         if self.degrees is not None:
-            degrees = np.array(self.degrees, dtype=np.uint64, copy=True)
+            degrees = np.asarray(self.degrees)
             if degrees.size != self.n - self.n0:
                 raise ParameterError(
                     f"degree sequence length {degrees.size} != n - n0 = {self.n - self.n0}")
-            object.__setattr__(self, "degrees", degrees)
+            degrees, m = degreeseq.validate_degrees(degrees, self.m0, self.n0)
+            object.__setattr__(self, "degrees", np.array(degrees, dtype=np.uint64, copy=True))
+            self.__dict__["_m"] = m
         if (self.no_self_loops or self.no_parallel_edges) and self.m0 < 1:
             raise ParameterError(
                 "no_self_loops / no_parallel_edges require a seed graph (m0 >= 1): "
@@ -104,7 +107,41 @@ class GenParams:
     def m(self) -> int:
         if self.d is not None:
             return self.m0 + (self.n - self.n0) * self.d
-        return self.m0 + int(self.degrees.sum())
+        return self.__dict__["_m"]
+
+    @property
+    def prefix(self) -> "degreeseq.PrefixIndex":
+        """Device prefix index of the degree sequence (generator.py:113-115)."""
+        if self.d is not None:
+            raise ParameterError("uniform-degree parameters have no prefix index")
+        return self._index()[0]
+
+    @property
+    def rank_bits(self) -> "degreeseq.RankBits":
+        if self.d is not None:
+            raise ParameterError("uniform-degree parameters have no prefix index")
+        return self._index()[1]
+
+    def _index(self, device=None):
+        torch = _lib.torch_cuda()
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        cache = self.__dict__.setdefault("_index_dev", {})
+        key = (dev.type, dev.index)
+        if key not in cache:
+            pi = degreeseq.build_prefix(self.degrees, self.m0, self.n0, device=dev)
+            cache[key] = (pi, degreeseq.build_rank_bits(pi, device=dev))
+        return cache[key]
+
+    def _host_W(self) -> np.ndarray:
+        """Host prefix (node starts + m) for batch planning only."""
+        W = self.__dict__.get("_W_host")
+        if W is None:
+            W = np.empty(self.degrees.size + 1, dtype=np.uint64)
+            W[0] = self.m0
+            np.cumsum(self.degrees, out=W[1:])
+            W[1:] += np.uint64(self.m0)
+            self.__dict__["_W_host"] = W
+        return W
 
     def degree_of(self, v: int) -> int:
         if not self.n0 <= v < self.n:
@@ -118,12 +155,16 @@ class GenParams:
             raise ParameterError(f"node {v} outside generated range [{self.n0}, {self.n})")
         if self.d is not None:
             return self.m0 + (v - self.n0) * self.d
-        return self.m0 + int(self.degrees[: v - self.n0].sum())
+        return int(self._host_W()[v - self.n0])
+
+    @property
+    def has_flags(self) -> bool:
+        return self.no_self_loops or self.no_parallel_edges
 
     # -- device plumbing -----------------------------------------------------
     def _device_params(self, device) -> _lib.CParams:
-        """parba_params_t with the seed graph resident on `device` (cached)."""
-        _require_plain(self)
+        """parba_params_t with the seed graph (and a degree sequence's index)
+        resident on `device` (cached)."""
         torch = _lib.torch_cuda()
         dev = torch.device(device)
         cache = self.__dict__.setdefault("_seed_dev", {})
@@ -133,20 +174,57 @@ class GenParams:
             if key not in cache:
                 cache[key] = _lib.to_device_u64(torch, self.seed_edges, dev)
             seed_ptr = cache[key].data_ptr()
-        return c_params(self.hash, self.n, self.d, self.n0, self.m0, seed_ptr)
+        if self.d is not None:
+            cp = c_params(self.hash, self.n, self.d, self.n0, self.m0, seed_ptr)
+        else:
+            cp = c_params(self.hash, self.n, 1, self.n0, self.m0, seed_ptr)
+            pi, rb = self._index(dev)
+            cp.d = 0
+            cp.m = self.m
+            cp.degree_prefix = pi.W_dev.data_ptr()
+            cp.rank = rb.rank_dev.data_ptr() if rb.rank_dev is not None else None
+            cp.owners = rb.owners_dev.data_ptr() if rb.owners_dev is not None else None
+        cp.flags = ((_lib.FLAG_NO_SELF_LOOPS if self.no_self_loops else 0)
+                    | (_lib.FLAG_NO_PARALLEL_EDGES if self.no_parallel_edges else 0))
+        cp.max_attempts = self.max_attempts or 0
+        return cp
 
 
 def edge_count(p: GenParams) -> int:
     return p.m
 
 
-def _require_plain(p: GenParams) -> None:
-    if p.d is None:
-        raise ParameterError("degree sequences are not on the B200 path (SURVEY.md 8f: f4)")
-    if p.no_self_loops or p.no_parallel_edges:
-        raise ParameterError(
-            "option flags need whole-node processing; they are not on the B200 path "
-            "(SURVEY.md 8f: f3)")
+def _check_resolution(resolution: str) -> None:
+    if resolution not in degreeseq.RESOLVE:
+        raise ParameterError(f"unknown resolution {resolution!r}")
+
+
+def _cuts(p: GenParams, lo: int, hi: int, chunk: int) -> list[int]:
+    """Chunk boundaries lo = c0 < c1 < ... = hi; node boundaries when an
+    option flag makes generation node-granular (driver.py:131-158)."""
+    if not p.has_flags:
+        return list(range(lo, hi, chunk)) + [hi]
+    cuts = [lo]
+    if p.d is not None:
+        step = max(p.d, (chunk // p.d) * p.d)
+        a = lo
+        while hi - a > step:
+            a += step
+            cuts.append(a)
+    else:
+        W = p._host_W()
+        a = lo
+        while hi - a > chunk:
+            k = int(np.searchsorted(W, np.uint64(a + chunk), side="right")) - 1
+            b = int(W[k])
+            if b <= a:  # one node larger than a chunk
+                k = int(np.searchsorted(W, np.uint64(a), side="right"))
+                b = int(W[k]) if k < W.size else hi
+            if b >= hi:
+                break
+            cuts.append(b)
+            a = b
+    return cuts + [hi]
 
 
 def _device(device=None):
@@ -200,7 +278,8 @@ def edges_at(ids, p: GenParams, device=None) -> tuple[np.ndarray, int]:
     """(k, 2) uint64 edges for an arbitrary list of edge IDs in [m0, m), plus
     total probes -- generate_edge vectorised (generator.py:172-181)."""
     ids = np.ascontiguousarray(np.asarray(ids, dtype=np.uint64)).reshape(-1)
-    _require_plain(p)
+    if p.has_flags:
+        raise ParameterError("option flags need whole-node processing; use generate_node_edges")
     if ids.size == 0:
         return np.empty((0, 2), dtype=np.uint64), 0
     lo_i, hi_i = int(ids.min()), int(ids.max())
@@ -229,12 +308,17 @@ def generate_edge(i: int, p: GenParams) -> Edge:
 
 
 def generate_node_edges(v: int, p: GenParams) -> list[Edge]:
-    """All edges of node v in edge-index order (generator.py:220-228), plain mode."""
+    """All edges of node v in edge-index order, honouring the option flags
+    (generator.py:220-228)."""
     if not p.n0 <= v < p.n:
         raise ParameterError(f"node {v} outside generated range [{p.n0}, {p.n})")
-    _require_plain(p)
-    first = p.first_edge_of(v)
-    e, _ = edges_at(np.arange(first, first + p.d, dtype=np.uint64), p)
+    first, dv = p.first_edge_of(v), p.degree_of(v)
+    if dv == 0:
+        return []
+    if p.has_flags:
+        e, _ = generate_block(first, first + dv, p)
+    else:
+        e, _ = edges_at(np.arange(first, first + dv, dtype=np.uint64), p)
     return [Edge(int(a), int(b)) for a, b in e]
 
 
@@ -270,23 +354,24 @@ def generate_block(lo: int, hi: int, p: GenParams, resolution: Resolution = "ran
     probes (generator.py:258-325).  The device generates in chunks while the
     previous chunk streams into pinned host memory."""
     _check_block(lo, hi, p)
-    _require_plain(p)
+    _check_resolution(resolution)
     if lo == hi:
         return np.empty((0, 2), dtype=np.uint64), 0
     torch, dev = _device(device)
     total = hi - lo
     out_host = torch.empty(2 * total, dtype=torch.int64, pin_memory=True)
-    chunk = min(total, HOST_CHUNK_EDGES)
+    cuts = _cuts(p, lo, hi, min(total, HOST_CHUNK_EDGES))
+    spans = list(zip(cuts, cuts[1:]))
+    chunk = max(b - a for a, b in spans)
     L = _lib.load()
     with torch.cuda.device(dev):
         comp = torch.cuda.current_stream(dev)
         copy = torch.cuda.Stream(dev)
-        bufs = [torch.empty(2 * chunk, dtype=torch.int64, device=dev) for _ in range(min(2, -(-total // chunk)))]
+        bufs = [torch.empty(2 * chunk, dtype=torch.int64, device=dev) for _ in range(min(2, len(spans)))]
         probes = torch.zeros(1, dtype=torch.int64, device=dev)
         cp = p._device_params(dev)
         drained = [None, None]
-        for k, a in enumerate(range(lo, hi, chunk)):
-            b = min(a + chunk, hi)
+        for k, (a, b) in enumerate(spans):
             buf = bufs[k % len(bufs)]
             if drained[k % 2] is not None:
                 comp.wait_event(drained[k % 2])

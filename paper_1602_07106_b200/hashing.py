@@ -63,11 +63,17 @@ class HashConfig:
 
 def c_params(cfg: HashConfig, n: int = 1, d: int = 1, n0: int = 0, m0: int = 0,
              seed_ptr: int | None = None) -> _lib.CParams:
-    """parba_params_t for a family (a 1-node dummy graph when only h is needed)."""
+    """parba_params_t for a family (a 1-node dummy graph when only h is needed).
+    The base seeds / multiplier feed the retry families of no_parallel_edges
+    (HashConfig.with_attempt: attempt a >= 1 replaces the salt by a)."""
     s0, s1 = cfg.crc_seeds()
-    return _lib.CParams(n, d, n0, m0, m0 + (n - n0) * d,
-                        _lib.HASH_CRC if cfg.kind is HashKind.CRC else _lib.HASH_SIMPLE,
-                        s0, s1, 0, cfg.simple_multiplier(), seed_ptr)
+    p = _lib.CParams(n, d, n0, m0, m0 + (n - n0) * d,
+                     _lib.HASH_CRC if cfg.kind is HashKind.CRC else _lib.HASH_SIMPLE,
+                     s0, s1, 0, cfg.simple_multiplier(), seed_ptr)
+    p.base_seed0 = cfg.seed0 & MASK32
+    p.base_seed1 = cfg.seed1 & MASK32
+    p.base_mult = cfg.multiplier & MASK64
+    return p
 
 
 def hash_many(r, cfg: HashConfig, device=None) -> np.ndarray:

@@ -21,7 +21,7 @@ import numpy as np
 
 from . import _lib, driver
 from .errors import GenerationError, ParameterError
-from .generator import GenParams, _check_block, _device, _require_plain
+from .generator import GenParams, _check_block, _cuts, _device
 
 # edges per device chunk (16 B each: 64 MiB chunks, two pinned buffers)
 FILE_CHUNK_EDGES = 1 << 22
@@ -71,13 +71,14 @@ class EdgeFileWriter(driver.Consumer):
         """Generate edges lo..hi-1 on the GPU and write them at their file
         offsets.  Returns (bytes written, hash probes)."""
         _check_block(lo, hi, p)
-        _require_plain(p)
         if lo == hi:
             return 0, 0
         torch, dev = _device(device)
         L = _lib.load()
         total = hi - lo
-        chunk = min(total, FILE_CHUNK_EDGES)
+        cuts = _cuts(p, lo, hi, min(total, FILE_CHUNK_EDGES))  # node-aligned under option flags
+        spans = list(zip(cuts, cuts[1:]))
+        chunk = max(b - a for a, b in spans)
         nbuf = 2
         work: queue.Queue = queue.Queue(maxsize=nbuf)
         free: queue.Queue = queue.Queue()
@@ -108,8 +109,8 @@ class EdgeFileWriter(driver.Consumer):
             th = threading.Thread(target=writer, daemon=True)
             th.start()
             try:
-                for a in range(lo, hi, chunk):
-                    n = min(chunk, hi - a)
+                for a, b in spans:
+                    n = b - a
                     k = free.get()  # host buffer k (and device buffer k) are free again
                     _lib.check(L.parba_generate(cp, a, a + n, dbufs[k].data_ptr(), probes.data_ptr(),
                                                 comp.cuda_stream))

@@ -42,6 +42,26 @@ def shard_range(lo: int, hi: int, rank: int, world_size: int) -> tuple[int, int]
     return lo + (rank * n) // world_size, lo + ((rank + 1) * n) // world_size
 
 
+def node_floor(p, x: int) -> int:
+    """Largest node boundary <= x (x in [m0, m]); m is a boundary."""
+    if x >= p.m:
+        return p.m
+    if p.d is not None:
+        return p.m0 + ((x - p.m0) // p.d) * p.d
+    W = p._host_W()
+    return int(W[int(np.searchsorted(W, np.uint64(x), side="right")) - 1])
+
+
+def shard_range_for(p, lo: int, hi: int, rank: int, world_size: int) -> tuple[int, int]:
+    """shard_range, with the cuts moved down to node boundaries when an
+    option flag makes generation node-granular (lo, hi must be boundaries)."""
+    a, b = shard_range(lo, hi, rank, world_size)
+    if p.has_flags:
+        a = lo if rank == 0 else max(lo, node_floor(p, a))
+        b = hi if rank == world_size - 1 else max(lo, node_floor(p, b))
+    return a, b
+
+
 def reduce_counts(t, op: str = "allreduce", dst: int = 0, group=None):
     """Sum a per-rank count tensor over the group (NCCL on GPU tensors, gloo
     on CPU tensors).  ``op='reduce'`` leaves the sum on `dst` only."""
@@ -100,7 +120,7 @@ def degree_counts_sharded(p, K: int, lo: int, hi: int, device=None):
 
     torch, dev = _device(device)
     rank, ws = world()
-    a, b = shard_range(lo, hi, rank, ws)
+    a, b = shard_range_for(p, lo, hi, rank, ws)
     counts, probes = count_shard_device(p, K, a, b, device=dev)
     c64 = widen_counts(torch, counts, K)
     stats = torch.tensor([b - a, 0], dtype=torch.int64, device=dev)

@@ -34,6 +34,15 @@ def golden():
     return arrays, meta
 
 
+@pytest.fixture(scope="session")
+def golden_nodes():
+    """f3 / f4 fixtures (tests/golden/make_golden_nodes.py)."""
+    arrays = np.load(os.path.join(GOLDEN_DIR, "golden_nodes.npz"))
+    with open(os.path.join(GOLDEN_DIR, "golden_nodes.json")) as fh:
+        meta = json.load(fh)
+    return arrays, meta
+
+
 # Reference test fixtures (pkg/tests/helpers.py:7-18 of the reference).
 TRIANGLE = np.array([0, 1, 1, 2, 2, 0], dtype=np.uint64)
 GOLDEN_SIMPLE_N10_D2 = [

@@ -21,7 +21,7 @@ HEADER = os.path.join(ROOT, "include", "parba_b200.h")
 
 def _declared_symbols() -> set[str]:
     src = open(HEADER).read()
-    return set(re.findall(r"\b(parba_[a-z_]+)\s*\(", src))
+    return set(re.findall(r"\b(parba_[a-z0-9_]+)\s*\(", src))
 
 
 @pytest.fixture(scope="module")
@@ -53,7 +53,7 @@ def test_library_loads_and_answers_without_gpu(lib_path):
     from paper_1602_07106_b200 import _lib
 
     L = _lib.load(lib_path)
-    assert L.parba_version() == 10000
+    assert L.parba_version() == 20000
     assert L.parba_device_count() >= 0  # 0 here (no GPU); never fails
 
 
@@ -71,6 +71,40 @@ def test_abi_validation_errors_without_launch(lib_path):
     assert b"inconsistent" in L.parba_last_error()
     seedless = hashing.c_params(hashing.HashConfig(), n=10, d=2, n0=3, m0=3)
     assert L.parba_degree_window(ctypes.byref(seedless), 3, 4, 5, None, None, None) == _lib.PARBA_EINVAL
+
+
+def test_abi_option_flag_and_degree_sequence_validation(lib_path):
+    # f3 / f4 parameter errors, all raised before any CUDA call
+    from paper_1602_07106_b200 import _lib, hashing
+
+    L = _lib.load(lib_path)
+    fake = ctypes.c_void_p(256)  # never dereferenced: validation fails first
+    p = hashing.c_params(hashing.HashConfig(), n=10, d=2)
+    p.flags = _lib.FLAG_NO_SELF_LOOPS
+    assert L.parba_generate(ctypes.byref(p), 0, 2, fake, None, None) == _lib.PARBA_EINVAL
+    assert b"require a seed graph" in L.parba_last_error()
+    p.flags = 4
+    assert L.parba_generate(ctypes.byref(p), 0, 2, fake, None, None) == _lib.PARBA_EINVAL
+    assert b"unknown option flags" in L.parba_last_error()
+    q = hashing.c_params(hashing.HashConfig(), n=10, d=3, n0=3, m0=3, seed_ptr=512)
+    q.flags = _lib.FLAG_NO_PARALLEL_EDGES
+    assert L.parba_generate(ctypes.byref(q), 4, q.m, fake, None, None) == _lib.PARBA_EINVAL
+    assert b"not a node boundary" in L.parba_last_error()
+    assert L.parba_generate(ctypes.byref(q), 3, q.m - 1, fake, None, None) == _lib.PARBA_EINVAL
+    assert b"not a node boundary" in L.parba_last_error()
+    assert L.parba_edges_at(ctypes.byref(q), fake, 1, fake, None, None) == _lib.PARBA_EINVAL
+    assert b"generate_node_edges" in L.parba_last_error()
+    r = hashing.c_params(hashing.HashConfig(), n=10, d=2)
+    r.degree_prefix = 512
+    assert L.parba_generate(ctypes.byref(r), 0, 2, fake, None, None) == _lib.PARBA_EINVAL
+    assert b"exactly one of d and degrees" in L.parba_last_error()
+    r.d = 0
+    assert L.parba_generate(ctypes.byref(r), 0, 2, fake, None, None) == _lib.PARBA_EINVAL
+    assert b"rank directory" in L.parba_last_error()
+    u = hashing.c_params(hashing.HashConfig(), n=10, d=2)
+    assert L.parba_node_of_edges(ctypes.byref(u), fake, 1, fake, 0, None) == _lib.PARBA_EINVAL
+    assert b"no prefix index" in L.parba_last_error()
+    assert L.parba_node_of_edges(ctypes.byref(u), fake, 1, fake, 7, None) == _lib.PARBA_EINVAL
 
 
 def test_product_never_imports_the_oracle():

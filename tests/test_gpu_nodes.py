@@ -1,0 +1,290 @@
+"""GPU parity of the node-granular rows: f4 degree sequences
+(device prefix / rank index, the three owner lookups, generation and degree
+counts in the tile kernels) and f3 option flags (the node kernel), through
+the C ABI, against fixtures made by the reference itself
+(tests/golden/make_golden_nodes.py) and against the CPU oracle.
+
+Bar: bit-exact edges, probe totals, counts and error messages."""
+
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import TRIANGLE
+from test_oracle_nodes import oparams_deg, oparams_flag
+
+pytestmark = pytest.mark.gpu
+
+pb = pytest.importorskip("paper_1602_07106_b200")
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def _hc(kind: str, salt: int = 0):
+    return pb.HashConfig(kind=pb.HashKind(kind), attempt_salt=salt)
+
+
+def params_deg(c, arrays, **kw) -> "pb.GenParams":
+    return pb.GenParams(n=c["n"], n0=c["n0"], degrees=arrays[f"{c['name']}_degrees"],
+                        seed_edges=None if c["seed"] is None else np.array(c["seed"], dtype=np.uint64),
+                        hash=_hc(c["kind"]), **kw)
+
+
+def params_flag(c, arrays) -> "pb.GenParams":
+    kw = dict(n=c["n"], n0=c["n0"], seed_edges=np.array(c["seed"], dtype=np.uint64),
+              no_self_loops=c["nsl"], no_parallel_edges=c["npe"], hash=_hc(c["kind"], c["salt"]))
+    if c["has_degrees"]:
+        kw["degrees"] = arrays[f"{c['name']}_degrees"]
+    else:
+        kw["d"] = c["d"]
+    return pb.GenParams(**kw)
+
+
+# --------------------------------------------------------------------------- f4 index
+
+def test_degree_index_vs_reference(golden_nodes):
+    arrays, meta = golden_nodes
+    g = meta["index"]
+    pi = pb.build_prefix(arrays["index_degrees"], m0=g["m0"], n0=g["n0"])
+    assert np.array_equal(pi.W, arrays["index_W"]) and pi.m == g["m"]
+    rb = pb.build_rank_bits(pi)
+    assert rb.n_ones == g["n_ones"] and rb.nbits == g["m"]
+    assert np.array_equal(rb.words, arrays["index_words"])
+    assert np.array_equal(pb.degreeseq.rank1_many(rb, arrays["index_es"]), arrays["index_rank1"])
+    es, want = arrays["index_gen_es"], arrays["index_owner"]
+    assert np.array_equal(pb.degreeseq.node_of_edge_many(es, rb), want)
+    assert np.array_equal(pb.degreeseq.node_of_edge_bisect_many(es, pi), want)
+    assert np.array_equal(pb.degreeseq.owners_of_edges_deferred(es, pi), want)
+    if g["owners"] is not None:
+        assert [int(x) for x in rb.owners[:8]] == g["owners"]
+
+
+def test_degree_index_reference_unit_cases():
+    # reference tests/test_degreeseq.py:40-178 restated
+    pi = pb.build_prefix(np.array([3, 1, 2], dtype=np.uint64), m0=0, n0=0)
+    assert pi.W.tolist() == [0, 3, 4] and pi.m == 6 and pi.n_nodes == 3
+    rb = pb.build_rank_bits(pb.build_prefix(np.array([1, 2, 1], dtype=np.uint64), m0=0, n0=0))
+    assert rb.nbits == 4 and int(rb.words[0]) == 0b1011 and rb.n_ones == 3 and rb.owners is None
+    assert [pb.degreeseq.rank1(rb, e) for e in range(4)] == [1, 2, 2, 3]
+    rb = pb.build_rank_bits(pb.build_prefix(np.array([2, 2], dtype=np.uint64), m0=2, n0=2))
+    assert rb.nbits == 6 and int(rb.words[0]) == (1 << 2) | (1 << 4)
+    rb = pb.build_rank_bits(pb.build_prefix(np.array([], dtype=np.uint64), m0=0, n0=0))
+    assert rb.nbits == 0 and rb.n_ones == 0
+    pi = pb.build_prefix(np.array([2, 0, 3], dtype=np.uint64), m0=0, n0=0)
+    rb = pb.build_rank_bits(pi)
+    assert rb.owners is not None
+    assert [pb.node_of_edge(e, rb) for e in range(5)] == [0, 0, 2, 2, 2]
+    assert [pb.node_of_edge_bisect(e, pi) for e in range(5)] == [0, 0, 2, 2, 2]
+    pi = pb.build_prefix(np.array([2], dtype=np.uint64), m0=3, n0=1)
+    rb = pb.build_rank_bits(pi)
+    for bad in (2, 5):
+        with pytest.raises(pb.ParameterError):
+            pb.node_of_edge(bad, rb)
+        with pytest.raises(pb.ParameterError):
+            pb.node_of_edge_bisect(bad, pi)
+    with pytest.raises(pb.ParameterError):
+        pb.degreeseq.rank1(rb, 5)
+    pi = pb.build_prefix(np.array([3, 1, 2], dtype=np.uint64), m0=0, n0=0)
+    assert pb.resolve_targets_deferred([(4, 6)], pi) == [(2, 1)]
+    assert pb.resolve_targets_deferred([], pi) == []
+    with pytest.raises(pb.ParameterError):
+        pb.resolve_targets_deferred([(0, 3)], pi)
+    assert [pb.first_half_pos(v, pi) for v in range(3)] == [0, 6, 8]
+    for bad in (np.array([[1]]), np.array([1.5]), np.array([-1, 2])):
+        with pytest.raises(pb.ParameterError):
+            pb.build_prefix(bad, m0=0, n0=0)
+    with pytest.raises(pb.ParameterError):
+        pb.build_prefix(np.array([2**63, 2**63], dtype=np.uint64), m0=0, n0=0)
+
+
+def test_degree_index_random_agreement_and_uniform_reduction():
+    rng = np.random.default_rng(13)
+    for trial in range(6):
+        n_nodes = int(rng.integers(1, 200_000))
+        deg = rng.integers(0, 7, size=n_nodes).astype(np.uint64)
+        deg[0] = max(int(deg[0]), 1)
+        m0, n0 = int(rng.integers(0, 4)), int(rng.integers(0, 4))
+        pi = pb.build_prefix(deg, m0=m0, n0=n0)
+        rb = pb.build_rank_bits(pi)
+        es = rng.integers(pi.m0, pi.m, size=50_000, dtype=np.uint64)
+        W = pi.W
+        want = (np.searchsorted(W, es, side="right") - 1 + n0).astype(np.uint64)
+        assert np.array_equal(pb.degreeseq.node_of_edge_many(es, rb), want)
+        assert np.array_equal(pb.degreeseq.node_of_edge_bisect_many(es, pi), want)
+        assert np.array_equal(pb.degreeseq.owners_of_edges_deferred(es, pi), want)
+    d, m0, n0, n = 4, 3, 3, 40
+    pi = pb.build_prefix(np.full(n - n0, d, dtype=np.uint64), m0=m0, n0=n0)
+    es = np.arange(m0, pi.m, dtype=np.uint64)
+    assert np.array_equal(pb.degreeseq.node_of_edge_many(es, pb.build_rank_bits(pi)),
+                          (es - np.uint64(m0)) // np.uint64(d) + np.uint64(n0))
+
+
+# --------------------------------------------------------------------------- f4 generation
+
+def test_degree_sequence_blocks_vs_reference(golden_nodes):
+    arrays, meta = golden_nodes
+    for c in meta["degseq"]:
+        p = params_deg(c, arrays)
+        assert p.m == c["m"]
+        for res in ("rank", "bisect", "deferred"):
+            got, probes = pb.generate_block(p.m0, p.m, p, resolution=res)
+            assert _sha(got) == c["sha256"] and probes == c["probes"], (c["name"], res)
+        lo, hi, sub_sha, sub_pr = c["sub"]
+        sub, sp = pb.generate_block(lo, hi, p)
+        assert _sha(sub) == sub_sha and sp == sub_pr, c["name"]
+    with pytest.raises(pb.ParameterError, match="unknown resolution"):
+        pb.generate_block(0, 1, params_deg(meta["degseq"][0], arrays), resolution="sideways")
+
+
+def test_degree_sequence_counts_vs_reference(golden_nodes):
+    arrays, meta = golden_nodes
+    for c in meta["counts"]:
+        case = next(x for x in meta["degseq"] if x["name"] == c["case"])
+        p = params_deg(case, arrays)
+        counter, stats = pb.degree_counts(p, K=c["K"]) if c["K"] else pb.degree_counts(p)
+        assert _sha(counter.counts) == c["sha256"] and stats.hash_probes == c["probes"], c
+
+
+def test_degree_sequence_edges_at_and_node_edges(golden_nodes):
+    arrays, meta = golden_nodes
+    c = meta["degseq"][5]
+    p = params_deg(c, arrays)
+    full = arrays[f"{c['name']}_edges"]
+    ids = np.arange(p.m0, p.m, 7, dtype=np.uint64)
+    e, _ = pb.edges_at(ids, p)
+    assert np.array_equal(e, full[(ids - np.uint64(p.m0)).astype(np.int64)])
+    for v in (p.n0, p.n0 + 3, p.n - 1):
+        first, dv = p.first_edge_of(v), p.degree_of(v)
+        got = pb.generate_node_edges(v, p)
+        assert [tuple(x) for x in got] == [tuple(map(int, r)) for r in full[first - p.m0: first - p.m0 + dv]]
+
+
+def test_degree_sequence_large_vs_oracle():
+    """A million-node power-law-like sequence (zeros included): random
+    unaligned subranges bit-exact vs the oracle, full window counts sum."""
+    rng = np.random.default_rng(77)
+    n_nodes = 10**6
+    deg = np.minimum(rng.zipf(2.2, size=n_nodes), 500).astype(np.uint64)
+    deg[rng.random(n_nodes) < 0.05] = 0
+    deg[0] = 2
+    p = pb.GenParams(n=3 + n_nodes, n0=3, degrees=deg, seed_edges=TRIANGLE)
+    op = O.OParams(n=p.n, d=None, n0=3, seed_edges=tuple(int(x) for x in TRIANGLE),
+                   degrees=tuple(int(x) for x in deg))
+    for _ in range(4):
+        lo = int(rng.integers(p.m0, p.m - 20000))
+        hi = lo + int(rng.integers(1, 20000))
+        got, pr = pb.generate_block(lo, hi, p)
+        want, wp = O.generate_block(op, lo, hi)
+        assert np.array_equal(got, want) and pr == wp
+    counter, stats = pb.degree_counts(p)
+    assert int(counter.counts.sum()) == 2 * p.m
+    assert np.array_equal(counter.counts[3:] >= deg.astype(np.int64), np.ones(n_nodes, dtype=bool))
+    K = 1000
+    win, _ = pb.degree_counts(p, K=K)
+    assert np.array_equal(win.counts, counter.counts[:K])
+
+
+# --------------------------------------------------------------------------- f3 option flags
+
+def test_option_flag_blocks_vs_reference(golden_nodes):
+    arrays, meta = golden_nodes
+    for c in meta["flags"]:
+        p = params_flag(c, arrays)
+        got, probes = pb.generate_block(p.m0, p.m, p)
+        assert _sha(got) == c["sha256"] and probes == c["probes"], c["name"]
+        lo, hi, sub_sha, sub_pr = c["sub"]
+        sub, sp = pb.generate_block(lo, hi, p)
+        assert _sha(sub) == sub_sha and sp == sub_pr, c["name"]
+        counter, stats = pb.degree_counts(p)
+        assert _sha(counter.counts) == c["counts_sha256"] and stats.hash_probes == c["counts_probes"], c["name"]
+        if c["nsl"]:
+            assert (got[:, 1] < got[:, 0]).all()
+        if c["npe"] and not c["has_degrees"]:
+            t = np.sort(got[:, 1].reshape(-1, c["d"]), axis=1)
+            assert (np.diff(t, axis=1) != 0).all()
+
+
+def test_option_flag_errors_match_reference(golden_nodes):
+    _, meta = golden_nodes
+    for c in meta["infeasible"]:
+        p = pb.GenParams(n=c["n"], d=c["d"], n0=c["n0"], seed_edges=np.array(c["seed"], dtype=np.uint64),
+                         no_self_loops=True, no_parallel_edges=True, max_attempts=c["max_attempts"])
+        with pytest.raises(pb.InfeasibleTargetsError) as ei:
+            pb.generate_block(p.m0, p.m, p)
+        assert str(ei.value) == c["message"]
+        with pytest.raises(pb.InfeasibleTargetsError, match="node 2"):
+            pb.generate_node_edges(2, p)
+    p = pb.GenParams(n=40, d=3, n0=3, seed_edges=TRIANGLE, no_self_loops=True)
+    with pytest.raises(pb.ParameterError, match="node boundary"):
+        pb.generate_block(4, p.m, p)
+    with pytest.raises(pb.ParameterError, match="node boundary"):
+        pb.generate_block(p.m0, p.m - 1, p)
+    with pytest.raises(pb.ParameterError):
+        pb.generate_edge(5, p)
+    with pytest.raises(pb.ParameterError):
+        pb.edges_at([5], p)
+
+
+def test_option_flags_node_edges_and_chain_sharing():
+    p = pb.GenParams(n=30, d=4, n0=3, seed_edges=TRIANGLE, no_self_loops=True)
+    for v in (3, 17, 29):
+        assert len({e.target for e in pb.generate_node_edges(v, p)}) == 1
+    q = pb.GenParams(n=40, d=3, n0=3, seed_edges=TRIANGLE, no_self_loops=True)
+    block, _ = pb.generate_block(q.m0, q.m, q)
+    want = [tuple(e) for v in range(3, 40) for e in pb.generate_node_edges(v, q)]
+    assert [tuple(map(int, r)) for r in block] == want
+
+
+def test_option_flags_large_vs_oracle_and_chunked(monkeypatch, tmp_path):
+    """1e5-node runs bit-exact vs the oracle; node-aligned host chunks, the
+    binary writer and world-size-independent counts on the flag path."""
+    from paper_1602_07106_b200 import generator as G, io as IO
+
+    seed = np.array([x for u in range(6) for v in range(u + 1, 6) for x in (u, v)], dtype=np.uint64)
+    for nsl, npe in ((True, False), (False, True), (True, True)):
+        p = pb.GenParams(n=10**5, d=4, n0=6, seed_edges=seed, no_self_loops=nsl, no_parallel_edges=npe)
+        op = O.OParams(n=p.n, d=4, n0=6, seed_edges=tuple(int(x) for x in seed), no_self_loops=nsl,
+                       no_parallel_edges=npe)
+        want, wp = O.generate_block(op, p.m0, p.m)
+        got, pr = pb.generate_block(p.m0, p.m, p)
+        assert np.array_equal(got, want) and pr == wp
+        monkeypatch.setattr(G, "HOST_CHUNK_EDGES", 4097)
+        got2, pr2 = pb.generate_block(p.m0, p.m, p)
+        assert np.array_equal(got2, want) and pr2 == wp
+        monkeypatch.setattr(IO, "FILE_CHUNK_EDGES", 10001)
+        path = tmp_path / f"f{int(nsl)}{int(npe)}.bin"
+        nbytes, _ = pb.write_edges_binary(str(path), p)
+        assert nbytes == 16 * (p.m - p.m0)
+        assert np.array_equal(np.fromfile(path, dtype="<u8").reshape(-1, 2), want)
+        counts = np.zeros(p.n, dtype=np.int64)
+        O.count_block(counts, want)
+        counts += np.bincount(seed.astype(np.int64), minlength=p.n)
+        counter, _ = pb.degree_counts(p)
+        assert np.array_equal(counter.counts, counts)
+
+
+def test_option_flags_with_degree_sequence_vs_oracle():
+    rng = np.random.default_rng(5)
+    deg = rng.integers(0, 9, size=50_000).astype(np.uint64)
+    deg[0] = 3
+    seed = np.array([x for u in range(7) for v in range(u + 1, 7) for x in (u, v)], dtype=np.uint64)
+    for kind in ("crc", "simple"):
+        p = pb.GenParams(n=7 + deg.size, n0=7, degrees=deg, seed_edges=seed, no_self_loops=True,
+                         no_parallel_edges=True, hash=_hc(kind))
+        op = O.OParams(n=p.n, d=None, n0=7, seed_edges=tuple(int(x) for x in seed),
+                       kind=O.KIND_CRC if kind == "crc" else O.KIND_SIMPLE, degrees=tuple(int(x) for x in deg),
+                       no_self_loops=True, no_parallel_edges=True)
+        want, wp = O.generate_block(op, p.m0, p.m)
+        got, pr = pb.generate_block(p.m0, p.m, p)
+        assert np.array_equal(got, want) and pr == wp
+        v = 7 + 1234
+        lo = p.first_edge_of(v)
+        hi = p.first_edge_of(v + 500)
+        sub, sp = pb.generate_block(lo, hi, p)
+        assert np.array_equal(sub, want[lo - p.m0: hi - p.m0])

@@ -221,8 +221,8 @@ def test_block_edge_cases():
     flagged = pb.GenParams(n=10, d=2, n0=3, seed_edges=TRIANGLE, no_self_loops=True)
     with pytest.raises(pb.ParameterError, match="generate_node_edges"):
         pb.generate_edge(3, flagged)
-    with pytest.raises(pb.ParameterError):
-        pb.generate_block(3, 17, flagged)  # not on the B200 path, no CPU fallback
+    with pytest.raises(pb.ParameterError, match="node boundary"):
+        pb.generate_block(4, 17, flagged)  # flag modes are node-granular
     with pytest.raises(pb.ParameterError):
         pb.run(pb.GenParams(n=10, d=2), pb.Consumer())
 
