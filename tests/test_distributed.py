@@ -72,3 +72,64 @@ def test_sharded_window_counts_equal_single_process():
     assert np.array_equal(all0, want) and np.array_equal(all1, want)
     assert np.array_equal(red0, want)  # root holds the sum
     assert pr0 == pr1 == wp
+
+
+def _worker_flags(rank: int, world: int, port: int, q) -> None:
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import oracle as O
+    import paper_1602_07106_b200 as pb
+    from paper_1602_07106_b200 import parallel
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        seed = (0, 1, 1, 2, 2, 3, 3, 0, 0, 2)
+        deg = np.random.default_rng(2).integers(0, 6, size=3000).astype(np.uint64)
+        deg[0] = 2
+        p = pb.GenParams(n=3004, n0=4, degrees=deg, seed_edges=np.array(seed, dtype=np.uint64),
+                         no_self_loops=True, no_parallel_edges=True)
+        op = O.OParams(n=p.n, d=None, n0=4, seed_edges=seed, degrees=tuple(int(x) for x in deg),
+                       no_self_loops=True, no_parallel_edges=True)
+        a, b = parallel.shard_range_for(p, p.m0, p.m, rank, world)
+        blk, probes = O.generate_block(op, a, b)  # node-aligned shard: no error
+        counts = np.zeros(p.n, dtype=np.int64)
+        O.count_block(counts, blk)
+        t = torch.from_numpy(counts)
+        parallel.reduce_counts(t, op="allreduce")
+        pr = torch.tensor([probes], dtype=torch.int64)
+        dist.all_reduce(pr)
+        q.put((rank, (a, b), t.numpy().copy(), int(pr.item())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_flag_counts_on_node_boundaries():
+    """Option flags make shards node-granular (parallel.shard_range_for): the
+    world-size-2 sum equals the single-process count of the whole graph."""
+    import oracle as O
+
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker_flags, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = sorted(q.get(timeout=240) for _ in procs)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    seed = (0, 1, 1, 2, 2, 3, 3, 0, 0, 2)
+    deg = np.random.default_rng(2).integers(0, 6, size=3000).astype(np.uint64)
+    deg[0] = 2
+    op = O.OParams(n=3004, d=None, n0=4, seed_edges=seed, degrees=tuple(int(x) for x in deg),
+                   no_self_loops=True, no_parallel_edges=True)
+    whole, wp = O.generate_block(op, op.m0, op.m)
+    want = np.zeros(op.n, dtype=np.int64)
+    O.count_block(want, whole)
+    (r0, s0, c0, p0), (r1, s1, c1, p1) = res
+    assert s0[0] == op.m0 and s0[1] == s1[0] and s1[1] == op.m
+    assert np.array_equal(c0, want) and np.array_equal(c1, want) and p0 == p1 == wp

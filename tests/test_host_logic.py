@@ -151,3 +151,54 @@ def test_edge_file_writer_positional_semantics(tmp_path):
     assert (data[1:5] == 0).all()
     with pytest.raises(pb.ParameterError):
         pb.EdgeFileWriter(str(tmp_path / "x.bin"), 0, -1)
+
+
+def test_degree_sequence_validation_and_host_planning():
+    """build_prefix's checks (degreeseq.py:87-109) on the host; m, first
+    edges and degrees of a degree-sequence family without touching a GPU."""
+    for bad, msg in ((np.array([[1, 2]]), "one-dimensional"), (np.array([1.5]), "integers"),
+                     (np.array([2, -1]), "non-negative"),
+                     (np.array([2**63, 2**63], dtype=np.uint64), "overflows"),
+                     (np.array([2**58], dtype=np.uint64), "maximum")):
+        with pytest.raises(pb.ParameterError, match=msg):
+            pb.degreeseq.validate_degrees(bad, 0, 0)
+    with pytest.raises(pb.ParameterError, match="length"):
+        pb.GenParams(n=5, n0=1, degrees=np.array([1, 2], dtype=np.uint64))
+    p = pb.GenParams(n=6, n0=3, degrees=np.array([2, 0, 3], dtype=np.uint64), seed_edges=TRIANGLE)
+    assert (p.m0, p.m) == (3, 8)
+    assert [p.first_edge_of(v) for v in (3, 4, 5)] == [3, 5, 5]
+    assert [p.degree_of(v) for v in (3, 4, 5)] == [2, 0, 3]
+    with pytest.raises(pb.ParameterError):
+        pb.GenParams(n=10, d=2).prefix
+
+
+def test_node_aligned_cuts_and_shards():
+    """Chunk cuts and rank shards land on node boundaries when an option
+    flag makes generation node-granular (driver.py:131-158)."""
+    from paper_1602_07106_b200 import generator as G, parallel as P
+
+    rng = np.random.default_rng(8)
+    deg = rng.integers(0, 9, size=400).astype(np.uint64)
+    deg[0] = 1
+    fams = [pb.GenParams(n=300, d=7, n0=3, seed_edges=TRIANGLE, no_self_loops=True),
+            pb.GenParams(n=403, n0=3, degrees=deg, seed_edges=TRIANGLE, no_parallel_edges=True)]
+    for p in fams:
+        if p.d is not None:
+            starts = {p.m0 + k * p.d for k in range(p.n - p.n0)} | {p.m}
+        else:
+            starts = set(int(x) for x in p._host_W())
+        for chunk in (1, 5, 37, 1000, 10**6):
+            cuts = G._cuts(p, p.m0, p.m, chunk)
+            assert cuts[0] == p.m0 and cuts[-1] == p.m
+            assert all(a < b for a, b in zip(cuts, cuts[1:]))
+            assert set(cuts) <= starts
+        for ws in range(1, 9):
+            pos = p.m0
+            for r in range(ws):
+                a, b = P.shard_range_for(p, p.m0, p.m, r, ws)
+                assert a == pos and b >= a and b in starts
+                pos = b
+            assert pos == p.m
+    plain = pb.GenParams(n=300, d=7)
+    assert G._cuts(plain, 5, 50, 10) == [5, 15, 25, 35, 45, 50]
+    assert P.shard_range_for(plain, 0, 100, 1, 3) == P.shard_range(0, 100, 1, 3)
