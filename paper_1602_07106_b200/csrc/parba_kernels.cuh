@@ -42,6 +42,16 @@ constexpr uint64_t kRyMin = 1ull << 27;
 #ifndef PARBA_WARPS
 #define PARBA_WARPS 32
 #endif
+// Running chains per lane in phase 2.  Two independent chains per lane help
+// the streaming sinks (+2% at C3) but cost the store sink 17% (twice the
+// chains in flight make the flush of the previous tile wait longer), A/B on
+// one B200 with tools/ab.py.
+#ifndef PARBA_ILP_STORE
+#define PARBA_ILP_STORE 1
+#endif
+#ifndef PARBA_ILP_STREAM
+#define PARBA_ILP_STREAM 2
+#endif
 #ifndef PARBA_MINB_STORE
 #define PARBA_MINB_STORE 1
 #endif
@@ -141,9 +151,17 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
     const uint64_t gw = (uint64_t)blockIdx.x * wpc + wib;
     const uint64_t nw = (uint64_t)gridDim.x * wpc;
 
-    uint32_t act = 0;               // 1: lane holds a running chain
-    R r = 0;
-    uint32_t saddr = 0;             // store: smem address of the chain's stage cell
+    // NS chains per lane in phase 2 (independent probes for the scheduler)
+    constexpr int NS = SINK == kStore ? PARBA_ILP_STORE : PARBA_ILP_STREAM;
+    uint32_t act[NS];               // 1: slot holds a running chain
+    R r[NS];
+    uint32_t saddr[NS];             // store: smem address of the chain's stage cell
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {
+        act[q] = 0;
+        r[q] = 0;
+        saddr[q] = 0;
+    }
     uint32_t headb = 0, tailb = 0;  // queue byte cursors (warp-uniform)
     uint32_t tile_q0 = 0;           // tail cursor at the start of the current tile
     uint32_t probes = 0;            // per lane (< 2^32 per launch and lane)
@@ -190,44 +208,60 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
     // discard it: no divergent branch around the probe); finished chains go
     // to the sink.
     auto step = [&]() {
-        const R nr = Hash::probe(tabs, r, p);
-        probes += (uint32_t)act;
-        uint32_t cont = (uint32_t)nr & 1u;  // odd: the chain continues
-        if constexpr (SEED) cont &= (uint64_t)nr >= p.stop ? 1u : 0u;
-        const uint32_t fin = act & (cont ^ 1u);
-        act &= cont;
-        r = nr;
-        if (fin) finish<NARROW, SEED, SINK, R, DEG>(saddr, (uint64_t)nr, p, a);
+        R nr[NS];
+#pragma unroll
+        for (int q = 0; q < NS; ++q) nr[q] = Hash::probe(tabs, r[q], p);
+#pragma unroll
+        for (int q = 0; q < NS; ++q) {
+            probes += act[q];
+            uint32_t cont = (uint32_t)nr[q] & 1u;  // odd: the chain continues
+            if constexpr (SEED) cont &= (uint64_t)nr[q] >= p.stop ? 1u : 0u;
+            const uint32_t fin = act[q] & (cont ^ 1u);
+            act[q] &= cont;
+            r[q] = nr[q];
+            if (fin) finish<NARROW, SEED, SINK, R, DEG>(saddr[q], (uint64_t)nr[q], p, a);
+        }
     };
 
-    // Pop queued chains into idle lanes.  FULLQ: at least 32 entries queued,
-    // so every idle lane takes one (no availability test).
-    auto refill = [&](auto fullq_c) {
+    // Pop queued chains into idle lanes of slot Q.  FULLQ: at least 32
+    // entries queued, so every idle lane takes one (no availability test).
+    auto refill1 = [&](auto fullq_c, auto slot_c) {
         constexpr bool FULLQ = decltype(fullq_c)::value;
-        const unsigned idle = ballot_all(!act);
+        constexpr int Q = decltype(slot_c)::value;
+        const unsigned idle = ballot_all(!act[Q]);
         const uint32_t rank = __popc(idle & ltmask);
         const uint32_t availb = tailb - headb;
-        if (!act && (FULLQ || (rank << L::kLgEB) < availb)) {
+        if (!act[Q] && (FULLQ || (rank << L::kLgEB) < availb)) {
             const uint32_t cur = headb + (rank << L::kLgEB);
             if constexpr (SINK == kStore) {
                 const uint64_t e = lds_u64(qaddr(cur));
                 if constexpr (NARROW) {
-                    r = (R)(uint32_t)e;
-                    saddr = (uint32_t)(e >> 32);
+                    r[Q] = (R)(uint32_t)e;
+                    saddr[Q] = (uint32_t)(e >> 32);
                 } else if constexpr (Hash::kPack) {
-                    r = (R)(e & kValueMask52);
-                    saddr = stage_s + (uint32_t)(e >> 52);
+                    r[Q] = (R)(e & kValueMask52);
+                    saddr[Q] = stage_s + (uint32_t)(e >> 52);
                 } else {
-                    r = (R)e;
-                    saddr = stage_s + lds_u16(qs_s + ((cur & (L::kQB - 1)) >> 2));
+                    r[Q] = (R)e;
+                    saddr[Q] = stage_s + lds_u16(qs_s + ((cur & (L::kQB - 1)) >> 2));
                 }
             } else {
-                r = lds_t<R>(qaddr(cur));
+                r[Q] = lds_t<R>(qaddr(cur));
             }
-            act = 1;
+            act[Q] = 1;
         }
         if constexpr (FULLQ) headb += (uint32_t)__popc(idle) << L::kLgEB;
         else headb += min((uint32_t)__popc(idle) << L::kLgEB, availb);
+    };
+    auto refill = [&](auto fullq_c) {
+        refill1(fullq_c, std::integral_constant<int, 0>{});
+        if constexpr (NS > 1) refill1(fullq_c, std::integral_constant<int, 1>{});
+    };
+    auto any_act = [&]() -> bool {
+        uint32_t x = 0;
+#pragma unroll
+        for (int q = 0; q < NS; ++q) x |= act[q];
+        return __any_sync(0xffffffffu, x);
     };
 
     // RY: large tile (2*base >= kRyMin): the lane's 8 start values differ by
@@ -304,8 +338,8 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
         // ---- phase 2: pop queued chains into idle lanes and probe while at
         // least a full warp of entries is queued (the < 32 newest entries
         // carry over to the next tile, so every refill can fill every idle lane)
-        if (tailb - headb >= (32u << L::kLgEB)) {
-            const uint32_t lim = tailb - (32u << L::kLgEB);
+        if (tailb - headb >= ((32u * NS) << L::kLgEB)) {
+            const uint32_t lim = tailb - ((32u * NS) << L::kLgEB);
             do {
                 refill(std::true_type{});
                 step();
@@ -321,7 +355,13 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
                     refill(std::false_type{});
                     step();
                 }
-                while (__any_sync(0xffffffffu, act && (saddr - stage_s) / L::kTB == pb)) step();
+                for (;;) {
+                    uint32_t x = 0;
+#pragma unroll
+                    for (int q = 0; q < NS; ++q) x |= act[q] & ((saddr[q] - stage_s) / L::kTB == pb ? 1u : 0u);
+                    if (!__any_sync(0xffffffffu, x)) break;
+                    step();
+                }
                 flush(pb, prev_base);
             }
             prev_base = base;
@@ -334,7 +374,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
         refill(std::false_type{});
         step();
     }
-    while (__any_sync(0xffffffffu, act)) step();
+    while (any_act()) step();
     if constexpr (SINK == kStore) {
         if (have_prev) flush(buf ^ 1u, prev_base);
     }
