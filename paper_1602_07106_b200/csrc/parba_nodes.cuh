@@ -142,6 +142,9 @@ __global__ void owner_span_kernel(DevParams p, uint64_t pos, uint64_t *out) {
 // ---------------------------------------------------------------------------
 // Option flags
 
+constexpr int kFamilies = 256;  // retry families cached in shared memory
+constexpr int kMemo = 16;       // memoised (r0, attempt) targets per node (no_self_loops)
+
 struct NodeArgs {
     uint32_t no_self_loops, no_parallel_edges;
     uint64_t max_attempts;  // 0: 64 * degree (generator.py:205)
@@ -193,7 +196,10 @@ __global__ void __launch_bounds__(256)
 node_kernel(DevParams p, NodeArgs na, uint64_t vlo, uint64_t vhi, uint64_t lo, ulonglong2 *out,
             unsigned long long *probes_out, unsigned long long *fail_edge) {
     __shared__ uint32_t tabs_p[8 * 256];
+    __shared__ Family fams[kFamilies];  // retry families 0..kFamilies-1 (built once per CTA)
     build_byte_tables(tabs_p, 8, 0u);
+    if (na.no_parallel_edges)
+        for (int a = threadIdx.x; a < kFamilies; a += blockDim.x) fams[a] = family_of(a, p, na);
     __syncthreads();
     const uint32_t tab = opaque(smem_addr(tabs_p));
     const bool simple = na.simple != 0;
@@ -220,14 +226,32 @@ node_kernel(DevParams p, NodeArgs na, uint64_t vlo, uint64_t vhi, uint64_t lo, u
             continue;
         }
         const uint64_t cap = na.max_attempts ? na.max_attempts : 64 * dv;
+        // with no_self_loops every edge of v starts at the same r0, so the
+        // target of (r0, attempt a) is the same for all of them: memoised
+        // (probe totals still count every evaluation, as the reference does)
+        uint64_t memo_t[kMemo];
+        uint32_t memo_p[kMemo];
+        uint32_t n_memo = 0;
         for (uint64_t i = first; i < first + dv; ++i) {
             const uint64_t r0 = na.no_self_loops ? 2 * first : 2 * i + 1;
             uint64_t t = 0;
             bool fresh = false;
             for (uint64_t attempt = 0; attempt < cap && !fresh; ++attempt) {
-                const Family f = family_of(attempt, p, na);
-                const uint64_t r = chain_family(tab, r0, f, simple, p.stop, probes);
-                t = target_of<false, true, false, DEG>(r, p);
+                if (na.no_self_loops && attempt < n_memo) {
+                    t = memo_t[attempt];
+                    probes += memo_p[attempt];
+                } else {
+                    const Family f = attempt < kFamilies ? fams[attempt] : family_of(attempt, p, na);
+                    uint64_t pr = 0;
+                    const uint64_t r = chain_family(tab, r0, f, simple, p.stop, pr);
+                    probes += pr;
+                    t = target_of<false, true, false, DEG>(r, p);
+                    if (na.no_self_loops && attempt == n_memo && n_memo < kMemo) {
+                        memo_t[n_memo] = t;
+                        memo_p[n_memo] = (uint32_t)pr;
+                        ++n_memo;
+                    }
+                }
                 fresh = true;
                 for (uint64_t j = first; j < i; ++j)  // the node's accepted targets so far
                     if (out[j - lo].y == t) {
