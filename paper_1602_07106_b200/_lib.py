@@ -17,7 +17,9 @@ import numpy as np
 from .errors import GenerationError, ParameterError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libparba_b200.so")
+# PARBA_LIB selects another build of the same library (e.g. the
+# -DPARBA_DEBUG_CHECKS=1 build of tools/check_build.sh); default: in-tree.
+LIB_PATH = os.environ.get("PARBA_LIB") or os.path.join(HERE, "libparba_b200.so")
 
 PARBA_OK, PARBA_EINVAL, PARBA_ECUDA, PARBA_ENOMEM, PARBA_EINFEASIBLE = 0, 1, 2, 3, 4
 HASH_CRC, HASH_SIMPLE = 0, 1

@@ -17,7 +17,7 @@ LIB = os.path.join(HERE, "libparba_b200.so")
 ROOT = os.path.dirname(HERE)
 
 SOURCES = ["parba_api.cu"]
-DEPS = ["parba_api.cu", "parba_kernels.cuh", "parba_device.cuh"]
+DEPS = ["parba_api.cu", "parba_kernels.cuh", "parba_device.cuh", "parba_nodes.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -353,7 +353,7 @@ uint64_t node_first_edge(const parba_params_t *p, uint64_t v) { return p->m0 + (
 // Edges of nodes [vlo, vhi) (first edge lo) into out, honouring the flags;
 // synchronises st to report an infeasible node (InfeasibleTargetsError).
 int generate_nodes(const parba_params_t *p, const DevParams &dp, uint64_t vlo, uint64_t vhi, uint64_t lo,
-                   uint64_t *out, unsigned long long *probes, cudaStream_t st) {
+                   uint64_t hi, uint64_t *out, unsigned long long *probes, cudaStream_t st) {
     if (vhi <= vlo) return PARBA_OK;
     NodeArgs na{};
     na.no_self_loops = (p->flags & PARBA_FLAG_NO_SELF_LOOPS) ? 1u : 0u;
@@ -369,10 +369,10 @@ int generate_nodes(const parba_params_t *p, const DevParams &dp, uint64_t vlo, u
     CUDA_TRY(cudaMemsetAsync(fe.p, 0xFF, sizeof(unsigned long long), st));
     const unsigned grid = grid_for(vhi - vlo, 256);
     if (is_deg(p))
-        node_kernel<true><<<grid, 256, 0, st>>>(dp, na, vlo, vhi, lo, (ulonglong2 *)out, probes,
+        node_kernel<true><<<grid, 256, 0, st>>>(dp, na, vlo, vhi, lo, hi - lo, (ulonglong2 *)out, probes,
                                                 (unsigned long long *)fe.p);
     else
-        node_kernel<false><<<grid, 256, 0, st>>>(dp, na, vlo, vhi, lo, (ulonglong2 *)out, probes,
+        node_kernel<false><<<grid, 256, 0, st>>>(dp, na, vlo, vhi, lo, hi - lo, (ulonglong2 *)out, probes,
                                                  (unsigned long long *)fe.p);
     CUDA_TRY(cudaGetLastError());
     uint64_t edge;
@@ -424,7 +424,7 @@ int count_nodes(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint6
         if (b > a) {
             AsyncBuf scratch;
             rc = scratch.alloc((b - a) * 16, st);
-            if (!rc) rc = generate_nodes(p, dp, v, v1, a, (uint64_t *)scratch.p, probes, st);
+            if (!rc) rc = generate_nodes(p, dp, v, v1, a, b, (uint64_t *)scratch.p, probes, st);
             if (rc) return rc;
             if (K > 0) {
                 count_pairs_kernel<CountT><<<grid_for(b - a, 256), 256, 0, st>>>(
@@ -495,7 +495,7 @@ int parba_generate(const parba_params_t *p, uint64_t lo, uint64_t hi, uint64_t *
         rc = boundary_node(p, dp, lo, &vlo, st);
         if (!rc) rc = boundary_node(p, dp, hi, &vhi, st);
         if (rc) return rc;
-        return generate_nodes(p, dp, vlo, vhi, lo, out_pairs, probes, st);
+        return generate_nodes(p, dp, vlo, vhi, lo, hi, out_pairs, probes, st);
     }
     SinkArgs a{out_pairs, nullptr, nullptr};
     return launch_tiles<kStore>(p, dp, lo, hi, a, probes, st);

@@ -59,6 +59,19 @@ constexpr uint64_t kRyMin = 1ull << 27;
 #define PARBA_MINB_STREAM 1
 #endif
 constexpr int kWarps = PARBA_WARPS;        // warps per CTA
+
+// Debug builds (-DPARBA_DEBUG_CHECKS=1, tools/check_build.sh) trap on a
+// violated invariant; release builds compile the checks away.
+#if defined(PARBA_DEBUG_CHECKS) && PARBA_DEBUG_CHECKS
+#define PARBA_CHECK(cond)                \
+    do {                                 \
+        if (!(cond)) __trap();           \
+    } while (0)
+#else
+#define PARBA_CHECK(cond) \
+    do {                  \
+    } while (0)
+#endif
 constexpr int kThreads = kWarps * 32;
 
 enum SinkKind { kStore = 0, kWindow = 1, kFull = 2 };
@@ -219,7 +232,10 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
             const uint32_t fin = act[q] & (cont ^ 1u);
             act[q] &= cont;
             r[q] = nr[q];
-            if (fin) finish<NARROW, SEED, SINK, R, DEG>(saddr[q], (uint64_t)nr[q], p, a);
+            if (fin) {
+                if constexpr (SINK == kStore) PARBA_CHECK(saddr[q] - stage_s < L::kStageB);
+                finish<NARROW, SEED, SINK, R, DEG>(saddr[q], (uint64_t)nr[q], p, a);
+            }
         }
     };
 
@@ -314,6 +330,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
                 sts_t_if<R>(pend, qaddr(cur), r1);
             }
             tailb += __popc(m) << L::kLgEB;
+            PARBA_CHECK(tailb - headb <= L::kQB);  // the ring never overflows
             probes += valid ? 1u : 0u;
         }
     };

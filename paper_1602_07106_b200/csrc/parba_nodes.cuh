@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include "parba_device.cuh"
+#include "parba_kernels.cuh"  // PARBA_CHECK
 
 namespace parba {
 
@@ -193,7 +194,7 @@ __device__ __forceinline__ uint64_t chain_family(uint32_t tab, uint64_t r, const
 // smallest edge index that found no fresh target (InfeasibleTargetsError).
 template <bool DEG>
 __global__ void __launch_bounds__(256)
-node_kernel(DevParams p, NodeArgs na, uint64_t vlo, uint64_t vhi, uint64_t lo, ulonglong2 *out,
+node_kernel(DevParams p, NodeArgs na, uint64_t vlo, uint64_t vhi, uint64_t lo, uint64_t n_out, ulonglong2 *out,
             unsigned long long *probes_out, unsigned long long *fail_edge) {
     __shared__ uint32_t tabs_p[8 * 256];
     __shared__ Family fams[kFamilies];  // retry families 0..kFamilies-1 (built once per CTA)
@@ -222,6 +223,7 @@ node_kernel(DevParams p, NodeArgs na, uint64_t vlo, uint64_t vhi, uint64_t lo, u
             const uint64_t r = chain_family(tab, 2 * first, f0, simple, p.stop, pr);
             probes += pr * dv;
             const uint64_t t = target_of<false, true, false, DEG>(r, p);
+            PARBA_CHECK(first - lo + dv <= n_out);
             for (uint64_t i = first; i < first + dv; ++i) out[i - lo] = make_ulonglong2(v, t);
             continue;
         }
@@ -263,6 +265,7 @@ node_kernel(DevParams p, NodeArgs na, uint64_t vlo, uint64_t vhi, uint64_t lo, u
                 atomicMin(fail_edge, (unsigned long long)i);
                 break;
             }
+            PARBA_CHECK(i - lo < n_out);
             out[i - lo] = make_ulonglong2(v, t);
         }
     }
