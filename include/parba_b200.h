@@ -169,6 +169,23 @@ int parba_generate_host(const parba_params_t *p_host_seed, uint64_t lo, uint64_t
 int parba_degree_window_host(const parba_params_t *p_host_seed, uint64_t lo, uint64_t hi,
                              uint64_t K, int64_t *counts_host, uint64_t *probes_host, int device);
 
+/* Single-process multi-GPU run over [m0, m) (parba_multi_run;
+ * the fork workers + Consumer.merge of driver.py:210-270): contiguous shards
+ * on devs[0..ndev), one host thread per device (a device may repeat).
+ *   PARBA_MULTI_STORE   out_host = host u64 pairs [2*(m - m0)] (edge i at row i - m0)
+ *   PARBA_MULTI_WINDOW  out_host = host int64 counts[K], +=
+ *   PARBA_MULTI_FULL    out_host = host int64 counts[n], += (needs 2m < 2^32)
+ *   PARBA_MULTI_DISCARD out_host unused (probes and time only)
+ * Counts are summed on devs[0] (peer copies + an add kernel).  probes_host
+ * and device_seconds (max shard device time + the reduction) are optional.
+ * Uniform degree only (host entry point); option flags cut at node boundaries. */
+#define PARBA_MULTI_STORE 0
+#define PARBA_MULTI_WINDOW 1
+#define PARBA_MULTI_FULL 2
+#define PARBA_MULTI_DISCARD 3
+int parba_multi_run(const parba_params_t *p_host_seed, int ndev, const int *devs, int mode, uint64_t K,
+                    void *out_host, uint64_t *probes_host, double *device_seconds);
+
 #ifdef __cplusplus
 }
 #endif

@@ -136,3 +136,51 @@ def degree_counts_sharded(p, K: int, lo: int, hi: int, device=None):
         per = [(0, b - a, int(probes.item()))]
     out = c64[:K].cpu().numpy() if K else np.zeros(0, dtype=np.int64)
     return out.astype(np.int64, copy=False), sum(pr for _, _, pr in per), per
+
+
+_MULTI_MODES = {"store": _lib.MULTI_STORE, "window": _lib.MULTI_WINDOW, "full": _lib.MULTI_FULL,
+                "discard": _lib.MULTI_DISCARD}
+
+
+def multi_run(p, devices, mode: str = "window", K: int | None = None):
+    """Whole graph [m0, m) on several GPUs from ONE process (C ABI
+    ``parba_multi_run``: a host thread per device, counts summed on
+    devices[0] over peer copies).  Returns (result, probes, device_seconds):
+    result = (m - m0, 2) uint64 edges ('store'), int64 counts[K] ('window'),
+    int64 counts[n] ('full') or None ('discard').  Uniform degree only."""
+    import ctypes
+
+    from .hashing import c_params
+
+    if mode not in _MULTI_MODES:
+        raise ParameterError(f"unknown mode {mode!r}")
+    if p.d is None:
+        raise ParameterError("multi_run takes uniform-degree families (degree sequences: one process per GPU)")
+    devs = np.ascontiguousarray(np.asarray(list(devices), dtype=np.int32))
+    if devs.size < 1:
+        raise ParameterError("need at least one device")
+    seed = np.ascontiguousarray(p.seed_edges, dtype=np.uint64)
+    cp = c_params(p.hash, p.n, p.d, p.n0, p.m0, seed.ctypes.data if seed.size else None)
+    cp.flags = ((_lib.FLAG_NO_SELF_LOOPS if p.no_self_loops else 0)
+                | (_lib.FLAG_NO_PARALLEL_EDGES if p.no_parallel_edges else 0))
+    cp.max_attempts = p.max_attempts or 0
+    if mode == "window":
+        K = p.n if K is None else K
+        out = np.zeros(max(K, 1), dtype=np.int64)
+    elif mode == "full":
+        K = p.n
+        out = np.zeros(max(K, 1), dtype=np.int64)
+    elif mode == "store":
+        K = 0
+        out = np.empty((p.m - p.m0, 2), dtype=np.uint64)
+    else:
+        K, out = 0, None
+    probes = ctypes.c_uint64(0)
+    secs = ctypes.c_double(0.0)
+    L = _lib.load()
+    _lib.check(L.parba_multi_run(ctypes.byref(cp), int(devs.size), devs.ctypes.data, _MULTI_MODES[mode], K,
+                                 out.ctypes.data if out is not None else None, ctypes.byref(probes),
+                                 ctypes.byref(secs)))
+    if mode in ("window", "full"):
+        out = out[:K]
+    return out, int(probes.value), float(secs.value)

@@ -496,3 +496,29 @@ def test_c_abi_host_entry_points():
     # errors map to status codes, no exception crosses the ABI
     assert L.parba_generate_host(ctypes.byref(cp), 0, 5, out.ctypes.data, None, 0) == _lib.PARBA_EINVAL
     assert b"out of range" in L.parba_last_error()
+
+
+def test_multi_run_single_process_shards():
+    """parba_multi_run (one process, a host thread per device; here the same
+    GPU three times): every mode equals the single-device result."""
+    import oracle as O
+
+    p = pb.GenParams(n=20000, d=5, n0=3, seed_edges=TRIANGLE)
+    want, wp = pb.generate_block(p.m0, p.m, p)
+    got, pr, secs = pb.parallel.multi_run(p, [0, 0, 0], mode="store")
+    assert np.array_equal(got, want) and pr == wp and secs > 0
+    full, fp = pb.degree_counts(p)
+    got, pr, _ = pb.parallel.multi_run(p, [0, 0], mode="full")
+    seed_counts = np.bincount(TRIANGLE.astype(np.int64), minlength=p.n)
+    assert np.array_equal(got + seed_counts, full.counts) and pr == wp
+    got, pr, _ = pb.parallel.multi_run(p, [0, 0, 0], mode="window", K=777)
+    assert np.array_equal(got + seed_counts[:777], full.counts[:777])
+    _, pr, _ = pb.parallel.multi_run(p, [0, 0], mode="discard")
+    assert pr == wp
+    f = pb.GenParams(n=5000, d=3, n0=3, seed_edges=TRIANGLE, no_self_loops=True)
+    fw, fwp = pb.generate_block(f.m0, f.m, f)
+    got, pr, _ = pb.parallel.multi_run(f, [0, 0, 0], mode="store")  # node-aligned shards
+    assert np.array_equal(got, fw) and pr == fwp
+    big = pb.GenParams(n=10**9, d=100)
+    with pytest.raises(pb.ParameterError, match="2m < 2"):
+        pb.parallel.multi_run(big, [0], mode="full")
