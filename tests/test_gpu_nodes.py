@@ -288,3 +288,31 @@ def test_option_flags_with_degree_sequence_vs_oracle():
         hi = p.first_edge_of(v + 500)
         sub, sp = pb.generate_block(lo, hi, p)
         assert np.array_equal(sub, want[lo - p.m0: hi - p.m0])
+
+
+def test_degree_count_windows_edge_cases_vs_oracle():
+    """K in {0, 1, n0, n0+1, n, n+17} for uniform, degree-sequence and
+    flagged families, counts of subranges with the seed folded in; the
+    device window / full kernels (and the flag path's chunked counts) must
+    equal count_block over the oracle's edges."""
+    rng = np.random.default_rng(31)
+    deg = rng.integers(0, 6, size=4000).astype(np.uint64)
+    deg[0] = 2
+    seed = np.array([x for u in range(5) for v in range(u + 1, 5) for x in (u, v)], dtype=np.uint64)
+    fams = [
+        (pb.GenParams(n=5000, d=3, n0=5, seed_edges=seed),
+         O.OParams(n=5000, d=3, n0=5, seed_edges=tuple(int(x) for x in seed))),
+        (pb.GenParams(n=4005, n0=5, degrees=deg, seed_edges=seed),
+         O.OParams(n=4005, d=None, n0=5, seed_edges=tuple(int(x) for x in seed), degrees=tuple(int(x) for x in deg))),
+        (pb.GenParams(n=3000, d=4, n0=5, seed_edges=seed, no_self_loops=True, no_parallel_edges=True),
+         O.OParams(n=3000, d=4, n0=5, seed_edges=tuple(int(x) for x in seed), no_self_loops=True,
+                   no_parallel_edges=True)),
+    ]
+    for p, op in fams:
+        want_edges, _ = O.generate_block(op, op.m0, op.m)
+        for K in (0, 1, p.n0, p.n0 + 1, p.n, p.n + 17):
+            want = np.zeros(K, dtype=np.int64)
+            O.count_block(want, want_edges)
+            O.count_block(want, np.asarray(seed, dtype=np.uint64))
+            counter, _ = pb.degree_counts(p, K=K)
+            assert counter.K == K and np.array_equal(counter.counts, want), (p, K)
