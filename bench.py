@@ -34,6 +34,7 @@ C2 = dict(n=10**8, d=10)          # configs[1]: store mode, m = 1e9
 C3 = dict(n=10**9, d=100, K=10**5)  # configs[2]: streaming window, m = 1e11
 C4 = dict(n=10**8, d=16)          # configs[3]: full histogram, m = 1.6e9
 BYTES_PER_EDGE = 16               # algorithmic HBM bytes per stored edge
+WRITE_ONLY_GBS = 6867.6  # write-only HBM peak measured by tools/micro.cu on a B200 of this pool
 INT_OPS_PER_PROBE = 32            # SURVEY 8d convention (64 per edge)
 
 
@@ -345,6 +346,9 @@ def main() -> None:
         "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
                      "frac": achieved_gbs / peak, "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": shard * BYTES_PER_EDGE,
+                     # also against a write-only peak measured on this pool
+                     # (tools/micro.cu, profiles/r01_micro.json: 6867.6 GB/s)
+                     "frac_of_write_only_peak": achieved_gbs / WRITE_ONLY_GBS,
                      "avg_kernel_ms": statistics.mean(kern_ms)},
         "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": args.steps,
         "clocks": clk.summary(), "probes_per_edge": probes_per_edge, "modes": extra,
