@@ -92,6 +92,13 @@ int parba_device_count(void);
 int parba_hash(const parba_params_t *p, const uint64_t *r, uint64_t count, uint64_t *out,
                void *stream);
 
+/* crc32c_u64_many (hashing.py:105-116, 158-165): out[k] = raw reflected
+ * CRC32-C of the 8 little-endian bytes of words[k] accumulated on seed (no
+ * inversion), widened to u64. */
+int parba_crc32c(uint32_t seed, const uint64_t *words, uint64_t count, uint64_t *out, void *stream);
+/* mulhi_u64 (hashing.py:168-176): out[k] = high 64 bits of a[k] * b[k]. */
+int parba_mulhi_u64(const uint64_t *a, const uint64_t *b, uint64_t count, uint64_t *out, void *stream);
+
 /* resolve_chain_block (_kernels.py:121-135): out[k] = terminal r of the
  * chain started at r0[k] (body at least once; stop when r < stop_below or r
  * even).  r0 is not modified; out may not alias r0. */

@@ -64,12 +64,27 @@ from .generator import (
     resolve_chain_block,
 )
 from .io import EdgeFileWriter, write_edges_binary
-from .hashing import DEFAULT_MULTIPLIER, HashConfig, HashKind, h_crc, h_simple, hash_many, hash_value
+from .hashing import (
+    CRC32C_TABLE,
+    DEFAULT_MULTIPLIER,
+    HashConfig,
+    HashKind,
+    crc32c_u64,
+    crc32c_u64_many,
+    h_crc,
+    h_crc_many,
+    h_simple,
+    h_simple_many,
+    hash_many,
+    hash_value,
+    mulhi_u64,
+)
 from .oracle_compat import bb_generate, edge_list
 
 __version__ = "0.1.0"
 
 __all__ = [
+    "CRC32C_TABLE", "crc32c_u64", "crc32c_u64_many", "h_crc_many", "h_simple_many", "mulhi_u64",
     "Batch", "BinRatio", "ChainResult", "CollectConsumer", "Consumer", "DEFAULT_BATCH_SIZE",
     "DEFAULT_MULTIPLIER", "DegreeCountConsumer", "EdgeFileWriter", "write_edges_binary", "DegreeCounter", "DiscardConsumer", "Edge",
     "GenParams", "GenerationError", "Granularity", "HashConfig", "HashKind", "Histogram",

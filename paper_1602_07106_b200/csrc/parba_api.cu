@@ -470,6 +470,23 @@ int parba_hash(const parba_params_t *p, const uint64_t *r, uint64_t count, uint6
     return PARBA_OK;
 }
 
+int parba_crc32c(uint32_t seed, const uint64_t *words, uint64_t count, uint64_t *out, void *stream) {
+    if (count == 0) return PARBA_OK;
+    if (!words || !out) return fail(PARBA_EINVAL, "NULL buffer");
+    crc_kernel<<<grid_for(count, 256), 256, 0, (cudaStream_t)stream>>>(crc32c_u64_bitwise(seed, 0), words, count,
+                                                                      out);
+    CUDA_TRY(cudaGetLastError());
+    return PARBA_OK;
+}
+
+int parba_mulhi_u64(const uint64_t *a, const uint64_t *b, uint64_t count, uint64_t *out, void *stream) {
+    if (count == 0) return PARBA_OK;
+    if (!a || !b || !out) return fail(PARBA_EINVAL, "NULL buffer");
+    mulhi_kernel<<<grid_for(count, 256), 256, 0, (cudaStream_t)stream>>>(a, b, count, out);
+    CUDA_TRY(cudaGetLastError());
+    return PARBA_OK;
+}
+
 int parba_resolve_chains(const parba_params_t *p, const uint64_t *r0, uint64_t count, uint64_t stop_below,
                          uint64_t *out, unsigned long long *probes, void *stream) {
     int rc = validate(p);

@@ -450,6 +450,27 @@ hash_kernel(DevParams p, const uint64_t *__restrict__ r, uint64_t count, uint64_
         out[k] = Hash::probe(tabs, r[k], p);
 }
 
+// crc32c_u64_many (hashing.py:158-165): out[k] = crc(seed, words[k]) via
+// CRC linearity -- byte tables of crc(0, .) with crc(seed, 0) folded in.
+__global__ void __launch_bounds__(256)
+crc_kernel(uint32_t k0, const uint64_t *__restrict__ w, uint64_t count, uint64_t *__restrict__ out) {
+    __shared__ uint32_t tabs_p[8 * 256];
+    build_byte_tables(tabs_p, 8, k0);
+    __syncthreads();
+    const uint32_t tabs = opaque(smem_addr(tabs_p));
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count;
+         k += (uint64_t)gridDim.x * blockDim.x)
+        out[k] = crc_bytes<8>(tabs, w[k]);
+}
+
+// mulhi_u64 (hashing.py:168-176): high 64 bits of a[k] * b[k].
+__global__ void mulhi_kernel(const uint64_t *__restrict__ a, const uint64_t *__restrict__ b, uint64_t count,
+                             uint64_t *__restrict__ out) {
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count;
+         k += (uint64_t)gridDim.x * blockDim.x)
+        out[k] = __umul64hi(a[k], b[k]);
+}
+
 // Source endpoints of a window/full count in closed form: node v owns edges
 // [m0+(v-n0)d, m0+(v-n0+1)d) (degree sequence: [W[v-n0], W[v-n0+1])); its
 // count grows by the overlap with [lo,hi).

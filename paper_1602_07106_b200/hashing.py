@@ -114,3 +114,76 @@ def h_simple(r: int, cfg: HashConfig) -> int:
 
 def hash_value(r: int, cfg: HashConfig) -> int:
     return _scalar(r, cfg)
+
+
+# ---------------------------------------------------------------------------
+# The CRC32-C primitive and the vectorized helpers of hashing.py:88-198.
+
+_CRC32C_POLY = 0x82F63B78  # hashing.py:40
+
+
+def _build_crc32c_table() -> tuple[int, ...]:
+    """The 256-entry reflected table (hashing.py:88-95): a constant of the
+    hash family, built once on the host; every CRC evaluation runs on the GPU."""
+    table = []
+    for i in range(256):
+        c = i
+        for _ in range(8):
+            c = (c >> 1) ^ _CRC32C_POLY if c & 1 else c >> 1
+        table.append(c)
+    return tuple(table)
+
+
+CRC32C_TABLE: tuple[int, ...] = _build_crc32c_table()
+
+
+def _dev_u64(a):
+    torch = _lib.torch_cuda()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    return torch, dev, _lib.to_device_u64(torch, a, dev)
+
+
+def crc32c_u64_many(seed: int, words) -> np.ndarray:
+    """Elementwise crc32c_u64(seed, w) (hashing.py:158-165), on the GPU."""
+    w = np.ascontiguousarray(np.asarray(words, dtype=np.uint64)).reshape(-1)
+    if w.size == 0:
+        return np.zeros(0, dtype=np.uint64)
+    torch, dev, wd = _dev_u64(w)
+    out = torch.empty_like(wd)
+    with torch.cuda.device(dev):
+        _lib.check(_lib.load().parba_crc32c(seed & MASK32, wd.data_ptr(), w.size, out.data_ptr(),
+                                            _lib.stream_ptr(torch, dev)))
+        return out.cpu().numpy().view(np.uint64)
+
+
+def crc32c_u64(seed: int, word: int) -> int:
+    """CRC32-C of one little-endian 64-bit word on `seed`, raw (no
+    inversion): _mm_crc32_u64 semantics (hashing.py:105-116)."""
+    return int(crc32c_u64_many(seed, np.array([word & MASK64], dtype=np.uint64))[0])
+
+
+def mulhi_u64(a, b) -> np.ndarray:
+    """High 64 bits of the elementwise 128-bit product (hashing.py:168-176)."""
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.uint64)).reshape(-1)
+    b = np.ascontiguousarray(np.asarray(b, dtype=np.uint64)).reshape(-1)
+    if a.shape != b.shape:
+        raise ParameterError("mulhi_u64 operands must have the same shape")
+    if a.size == 0:
+        return np.zeros(0, dtype=np.uint64)
+    torch, dev, ad = _dev_u64(a)
+    bd = _lib.to_device_u64(torch, b, dev)
+    out = torch.empty_like(ad)
+    with torch.cuda.device(dev):
+        _lib.check(_lib.load().parba_mulhi_u64(ad.data_ptr(), bd.data_ptr(), a.size, out.data_ptr(),
+                                               _lib.stream_ptr(torch, dev)))
+        return out.cpu().numpy().view(np.uint64)
+
+
+def h_crc_many(r, cfg: HashConfig) -> np.ndarray:
+    """Elementwise h_crc (hashing.py:179-184); every r >= 1."""
+    return hash_many(r, replace(cfg, kind=HashKind.CRC))
+
+
+def h_simple_many(r, cfg: HashConfig) -> np.ndarray:
+    """Elementwise h_simple (hashing.py:187-191); every r >= 1."""
+    return hash_many(r, replace(cfg, kind=HashKind.SIMPLE))

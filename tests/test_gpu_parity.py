@@ -522,3 +522,30 @@ def test_multi_run_single_process_shards():
     big = pb.GenParams(n=10**9, d=100)
     with pytest.raises(pb.ParameterError, match="2m < 2"):
         pb.parallel.multi_run(big, [0], mode="full")
+
+
+def test_crc_primitive_and_vector_helpers(golden):
+    """crc32c_u64(_many), mulhi_u64, h_crc_many / h_simple_many (hashing.py:
+    105-198) on the device vs the reference's fixture and exact integers."""
+    arrays, meta = golden
+    seeds, words, want = arrays["crc_seeds"], arrays["crc_words"], arrays["crc_out"]
+    got = np.array([pb.crc32c_u64_many(int(s), np.array([w]))[0] for s, w in zip(seeds, words)], dtype=np.uint64)
+    assert np.array_equal(got, want)
+    assert pb.crc32c_u64(int(seeds[0]), int(words[0])) == int(want[0])
+    for s in (0, 1, 0xFFFFFFFF):
+        batch = pb.crc32c_u64_many(s, words)
+        assert np.array_equal(batch[:4], [O.crc32c_u64(s, int(w)) for w in words[:4]])
+    rng = np.random.default_rng(9)
+    a = rng.integers(0, 2**64 - 1, size=5000, dtype=np.uint64, endpoint=True)
+    b = rng.integers(0, 2**64 - 1, size=5000, dtype=np.uint64, endpoint=True)
+    hi = pb.mulhi_u64(a, b)
+    assert all(int(h) == (int(x) * int(y)) >> 64 for h, x, y in zip(hi[:500], a[:500], b[:500]))
+    rs = arrays["hash_r"]
+    for k, c in enumerate(meta["cfgs"]):
+        f = pb.h_crc_many if c[0] == "crc" else pb.h_simple_many
+        assert np.array_equal(f(rs, _hc(c)), arrays[f"hash_out_{k}"]), c
+    from paper_1602_07106_b200 import _kernels
+
+    _kernels.warmup()
+    vals, pr = _kernels.resolve_chain_block(np.array([1001], dtype=np.uint64), 0, pb.HashConfig())
+    assert pr >= 1 and int(vals[0]) % 2 == 0

@@ -202,3 +202,8 @@ def test_node_aligned_cuts_and_shards():
     plain = pb.GenParams(n=300, d=7)
     assert G._cuts(plain, 5, 50, 10) == [5, 15, 25, 35, 45, 50]
     assert P.shard_range_for(plain, 0, 100, 1, 3) == P.shard_range(0, 100, 1, 3)
+
+
+def test_crc_table_constant_matches_reference(golden):
+    arrays, _ = golden
+    assert np.array_equal(np.array(pb.CRC32C_TABLE, dtype=np.uint32), arrays["crc_table"])
