@@ -470,6 +470,16 @@ int parba_hash(const parba_params_t *p, const uint64_t *r, uint64_t count, uint6
     return PARBA_OK;
 }
 
+#if PARBA_WARP_TIMES
+// diagnostic build only (not in the header): copy the per-warp start/end
+// timestamps of the last tile launch.
+int parba_debug_warp_times(uint64_t *out, uint64_t nwarps) {
+    if (nwarps > kMaxTimedWarps) nwarps = kMaxTimedWarps;
+    CUDA_TRY(cudaMemcpyFromSymbol(out, g_warp_times, 2 * nwarps * sizeof(uint64_t)));
+    return PARBA_OK;
+}
+#endif
+
 int parba_crc32c(uint32_t seed, const uint64_t *words, uint64_t count, uint64_t *out, void *stream) {
     if (count == 0) return PARBA_OK;
     if (!words || !out) return fail(PARBA_EINVAL, "NULL buffer");

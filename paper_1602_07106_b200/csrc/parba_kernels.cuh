@@ -76,6 +76,15 @@ constexpr int kThreads = kWarps * 32;
 
 enum SinkKind { kStore = 0, kWindow = 1, kFull = 2 };
 
+#ifndef PARBA_WARP_TIMES
+#define PARBA_WARP_TIMES 0
+#endif
+#if PARBA_WARP_TIMES
+// diagnostic build: start/end globaltimer of every warp of the last launch
+constexpr uint64_t kMaxTimedWarps = 148 * 32;
+__device__ unsigned long long g_warp_times[2 * kMaxTimedWarps];
+#endif
+
 struct SinkArgs {
     uint64_t *out;                         // store: 2*(hi-lo) u64, 16-byte aligned
     unsigned long long *win;               // window counts (K)
@@ -161,6 +170,10 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
     [[maybe_unused]] const uint32_t qs_s =
         opaque(st_all + (uint32_t)wpc * L::kStageB + (uint32_t)wib * L::kSlotB);
     const unsigned ltmask = lanemask_lt();
+#if PARBA_WARP_TIMES
+    unsigned long long t_start;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+#endif
     const uint64_t gw = (uint64_t)blockIdx.x * wpc + wib;
     const uint64_t nw = (uint64_t)gridDim.x * wpc;
 
@@ -395,6 +408,17 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
     if constexpr (SINK == kStore) {
         if (have_prev) flush(buf ^ 1u, prev_base);
     }
+#if PARBA_WARP_TIMES
+    {
+        unsigned long long t_end;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        const uint64_t wid = (uint64_t)blockIdx.x * wpc + wib;
+        if (lane == 0 && wid < kMaxTimedWarps) {
+            g_warp_times[2 * wid] = t_start;
+            g_warp_times[2 * wid + 1] = t_end;
+        }
+    }
+#endif
     // ---- probes: warp reduce, one atomic per warp
     if (probes_out) {
         unsigned long long pr = probes;
