@@ -173,6 +173,17 @@ __device__ __forceinline__ double u32_to_f64(uint32_t x) {
     return __uint2double_rn(x);
 #endif
 }
+#ifndef PARBA_CVTW
+#define PARBA_CVTW 0
+#endif
+// chain value (< 2^52) of the wide kernels -> double; PARBA_CVTW bit 1: magic
+__device__ __forceinline__ double r_to_f64w(uint64_t x) {
+#if PARBA_CVTW & 2
+    return __longlong_as_double((long long)(x | 0x4330000000000000ull)) - 0x1p52;
+#else
+    return __ull2double_rn(x);
+#endif
+}
 __device__ __forceinline__ double u52_to_f64(uint64_t x) {  // x < 2^52
 #ifdef PARBA_MAGIC_CVT
     return __longlong_as_double((long long)(x | 0x4330000000000000ull)) - 0x1p52;
@@ -207,8 +218,16 @@ __device__ __forceinline__ double recip_approx(double rd) {
 // The 1.5*2^52 offset rounds q to an integer for |q| < 2^51 of either sign.
 template <class R>
 __device__ __forceinline__ R mod_fp_y(uint32_t hhi, uint32_t hlo, double rd, double y) {
-    const double ha = u32_to_f64(hhi);
-    const double hl = u32_to_f64(hlo);
+    // the hash halves by the magic exponent (DADD) -- the XU pipe is the
+    // busiest one in the wide kernels (I2F, MUFU, POPC); PARBA_CVTW bit 0:
+    // halves via I2F instead
+#if PARBA_CVTW & 1
+    const double ha = u32_to_f64_i2f(hhi);
+    const double hl = u32_to_f64_i2f(hlo);
+#else
+    const double ha = u32_to_f64_magic(hhi);
+    const double hl = u32_to_f64_magic(hlo);
+#endif
     const double qa = fma(ha, y, 0x1.8p52) - 0x1.8p52;
     const double x = fma(-qa, rd, ha);
     const double qb = fma(fma(x, 0x1p32, hl), y, 0x1.8p52) - 0x1.8p52;
@@ -419,7 +438,7 @@ struct HashCrc {
     __device__ __forceinline__ static R from_crc(uint32_t c0, R r, const DevParams &p) {
         if constexpr (NC == 2) return mod_fp31(c0, c0 ^ p.k01, r);
         else if constexpr (kNarrow) return mod_fp<R>(c0, c0 ^ p.k01, u32_to_f64(r));
-        else if constexpr (NC <= 5) return mod_fp<R>(c0, c0 ^ p.k01, u52_to_f64(r));
+        else if constexpr (NC <= 5) return mod_fp<R>(c0, c0 ^ p.k01, r_to_f64w(r));
         else return mod_int(c0, c0 ^ p.k01, r);
     }
     // Same, with rd = (double)r and y ~ 1/r (relative error < 2^-34) supplied
