@@ -310,8 +310,8 @@ def main() -> None:
             for _ in range(steps):
                 counts.zero_()
                 pb.parallel.count_shard_device(q, K, a, b, counts=counts, probes=prb, device=dev)
-                c64 = pb.parallel.widen_counts(torch, counts, K)
-                pb.parallel.reduce_counts(c64, op="reduce")
+                pb.parallel.reduce_counts(counts, op="reduce")  # u32 words for the full histogram
+            c64 = pb.parallel.widen_counts(torch, counts, K)
             e1.record(stream)
             torch.cuda.synchronize(dev)
             t = max_over_ranks(e0.elapsed_time(e1) / 1000.0)

@@ -122,11 +122,12 @@ def degree_counts_sharded(p, K: int, lo: int, hi: int, device=None):
     rank, ws = world()
     a, b = shard_range_for(p, lo, hi, rank, ws)
     counts, probes = count_shard_device(p, K, a, b, device=dev)
-    c64 = widen_counts(torch, counts, K)
     stats = torch.tensor([b - a, 0], dtype=torch.int64, device=dev)
     stats[1:2].copy_(probes)
     if ws > 1:
-        reduce_counts(c64)
+        # full histograms travel as 32-bit words (2m < 2^32, so the wrapped
+        # int32 sum has the exact bits): half the bytes of an int64 reduce
+        reduce_counts(counts)
         gathered = [torch.zeros_like(stats) for _ in range(ws)]
         import torch.distributed as dist
 
@@ -134,6 +135,7 @@ def degree_counts_sharded(p, K: int, lo: int, hi: int, device=None):
         per = [(r, int(g[0].item()), int(g[1].item())) for r, g in enumerate(gathered)]
     else:
         per = [(0, b - a, int(probes.item()))]
+    c64 = widen_counts(torch, counts, K)
     out = c64[:K].cpu().numpy() if K else np.zeros(0, dtype=np.int64)
     return out.astype(np.int64, copy=False), sum(pr for _, _, pr in per), per
 

@@ -46,6 +46,13 @@ def _worker(rank: int, world: int, port: int, q) -> None:
         parallel.reduce_counts(t2, op="reduce", dst=0)
         pr = torch.tensor([probes], dtype=torch.int64)
         dist.all_reduce(pr)
+        # full histograms are reduced as 32-bit words: a per-rank count above
+        # 2^31 wraps in int32 but the summed bits widen back to the exact total
+        per_rank = 3_000_000_000 if rank == 0 else 1_000_000_000  # total 4e9 < 2^32
+        w = torch.tensor([int(np.uint32(per_rank).view(np.int32)), 7], dtype=torch.int32)
+        parallel.reduce_counts(w)
+        wide = parallel.widen_counts(torch, w, 2)
+        assert wide.tolist() == [4_000_000_000, 14]
         q.put((rank, (a, b), t.numpy().copy(), t2.numpy().copy(), int(pr.item())))
     finally:
         dist.destroy_process_group()
