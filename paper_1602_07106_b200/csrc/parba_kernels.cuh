@@ -390,6 +390,8 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
 #pragma unroll
                     for (int q = 0; q < NS; ++q) x |= act[q] & ((saddr[q] - stage_s) / L::kTB == pb ? 1u : 0u);
                     if (!__any_sync(0xffffffffu, x)) break;
+                    // keep the lanes that are free busy with this tile's chains
+                    if (tailb != headb) refill(std::false_type{});
                     step();
                 }
                 flush(pb, prev_base);
