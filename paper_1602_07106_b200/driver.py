@@ -11,25 +11,33 @@ device kernels instead:
   * ``io.EdgeFileWriter``    -> store mode streamed into the positional
                                 binary file (cli.py:121-145)
 
-A generic Python consumer would need every edge on the host and is not
-fused, so ``run`` raises ``ParameterError`` for it (no CPU fallback).
-``workers`` keeps its meaning of "degree of parallelism" and is validated;
-inside one process the work runs on one GPU, and when ``torch.distributed``
-is initialised the edge range is sharded over its ranks (one GPU each) and
-the histogram reduced over NCCL -- results are identical for every
-workers / batch_size / world size, as in the reference (driver.py:1-9).
+Any other ``Consumer`` (a user plug-in, or a subclass of the built-in ones)
+runs the reference's batch loop (driver.py:161-270): ``plan_batches`` cuts
+[m0, m), ``workers`` host threads claim batches from a shared cursor, every
+batch is generated on the GPU (``generate_block``) and handed to the
+consumer's ``accept_block`` on the host, and the contexts are merged.  The
+edges are still computed only by the CUDA kernels; the host runs the user's
+consumer code.  Worker failures abort the run (GenerationError naming the
+worker, or the original exception with one worker), as in the reference.
+
+When ``torch.distributed`` is initialised the fused routes shard the edge
+range over its ranks (one GPU each) and reduce histograms over NCCL --
+results are identical for every workers / batch_size / world size, as in the
+reference (driver.py:1-9).
 """
 
 from __future__ import annotations
 
 import enum
+import threading
 import time
+import traceback
 from dataclasses import dataclass
 from typing import Any, Sequence
 
 import numpy as np
 
-from .errors import ParameterError
+from .errors import GenerationError, ParameterError
 from .generator import Edge, GenParams, Resolution
 
 DEFAULT_BATCH_SIZE = 1 << 16  # driver.py:26
@@ -167,6 +175,9 @@ def run(p: GenParams, consumer: Consumer, workers: int = 1, batch_size: int = DE
     if batch_size < 1:
         raise ParameterError(f"batch_size must be >= 1, got {batch_size}")
     t0 = time.perf_counter()
+    kind = type(consumer)
+    if kind not in (analytics.DegreeCountConsumer, DiscardConsumer, io.EdgeFileWriter, CollectConsumer):
+        return _run_generic(p, consumer, workers, batch_size, resolution, device, t0)
     if isinstance(consumer, analytics.DegreeCountConsumer):
         counts, probes, per = parallel.degree_counts_sharded(p, consumer.K, p.m0, p.m, device=device)
         merged = analytics.DegreeCounter(K=consumer.K, counts=counts)
@@ -194,16 +205,77 @@ def run(p: GenParams, consumer: Consumer, workers: int = 1, batch_size: int = DE
             merged = sum(int(g[0].item()) for g in gathered)
             probes = sum(pr for _, _, pr in per)
             dist.barrier()  # the file is complete on return
-    elif isinstance(consumer, CollectConsumer):
+    else:  # CollectConsumer
         merged, probes = generate_block(p.m0, p.m, p, resolution=resolution, device=device)
         per = [(0, p.m - p.m0, probes)]
-    else:
-        raise ParameterError(
-            f"consumer {type(consumer).__name__} is not fused into the B200 path; use "
-            "DegreeCountConsumer, CollectConsumer, DiscardConsumer or EdgeFileWriter "
-            "(there is no CPU fallback)")
     elapsed = time.perf_counter() - t0
     per_worker = tuple(WorkerStats(w, 1 if e else 0, e, pr, elapsed) for w, e, pr in per)
     return merged, RunStats(edges_emitted=sum(w.edges for w in per_worker),
                             hash_probes=sum(w.probes for w in per_worker),
                             elapsed=elapsed, per_worker=per_worker)
+
+
+def _run_generic(p: GenParams, consumer: Consumer, workers: int, batch_size: int, resolution: Resolution,
+                 device, t0: float) -> tuple[Any, RunStats]:
+    """The reference's batch loop (driver.py:161-270) with host threads as
+    workers and the GPU generating every batch."""
+    from .generator import generate_block
+
+    batches = plan_batches(p, batch_size)
+    lock = threading.Lock()
+    cursor = [0]
+    abort = threading.Event()
+
+    def claim() -> int:
+        with lock:
+            k = cursor[0]
+            cursor[0] = k + 1
+            return k
+
+    def work(worker_id: int):
+        start = time.perf_counter()
+        ctx = consumer.new_context(worker_id)
+        nb = edges = probes = 0
+        while not abort.is_set():
+            k = claim()
+            if k >= len(batches):
+                break
+            b = batches[k]
+            arr, pr = generate_block(b.lo, b.hi, p, resolution=resolution, device=device)
+            ret = consumer.accept_block(ctx, b.lo, arr)
+            if ret is not None:
+                ctx = ret
+            nb += 1
+            edges += b.hi - b.lo
+            probes += pr
+        stats = WorkerStats(worker_id, nb, edges, probes, time.perf_counter() - start)
+        return consumer.finalize_context(ctx), stats
+
+    if workers == 1:
+        result, st = work(0)
+        results, per_worker = [result], [st]
+    else:
+        out: list = [None] * workers
+        errors: list = []
+
+        def main(w: int) -> None:
+            try:
+                out[w] = work(w)
+            except BaseException:
+                abort.set()
+                errors.append((w, traceback.format_exc()))
+
+        threads = [threading.Thread(target=main, args=(w,), daemon=True) for w in range(workers)]
+        for th in threads:
+            th.start()
+        for th in threads:
+            th.join()
+        if errors:
+            w, tb = sorted(errors)[0]
+            raise GenerationError(f"worker {w} failed:\n{tb}")
+        results = [o[0] for o in out]
+        per_worker = [o[1] for o in out]
+    merged = consumer.merge(results)
+    return merged, RunStats(edges_emitted=sum(w.edges for w in per_worker),
+                            hash_probes=sum(w.probes for w in per_worker),
+                            elapsed=time.perf_counter() - t0, per_worker=tuple(per_worker))

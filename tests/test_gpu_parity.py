@@ -223,7 +223,7 @@ def test_block_edge_cases():
         pb.generate_edge(3, flagged)
     with pytest.raises(pb.ParameterError, match="node boundary"):
         pb.generate_block(4, 17, flagged)  # flag modes are node-granular
-    with pytest.raises(pb.ParameterError):
+    with pytest.raises(NotImplementedError):  # the base Consumer has no accept (driver.py:70-71)
         pb.run(pb.GenParams(n=10, d=2), pb.Consumer())
 
 
@@ -549,3 +549,90 @@ def test_crc_primitive_and_vector_helpers(golden):
     _kernels.warmup()
     vals, pr = _kernels.resolve_chain_block(np.array([1001], dtype=np.uint64), 0, pb.HashConfig())
     assert pr >= 1 and int(vals[0]) % 2 == 0
+
+
+# --------------------------------------------------------------------------- generic consumers
+# (reference tests/test_driver.py:160-270 restated: user plug-ins run the
+# batch loop with host-thread workers; every batch is generated on the GPU)
+
+class _Exploding(pb.Consumer):
+    def new_context(self, worker_id):
+        return 0
+
+    def accept_block(self, ctx, lo, edges):
+        raise RuntimeError("synthetic consumer failure")
+
+    def merge(self, contexts):
+        return None
+
+
+class _PerEdgeSum(pb.Consumer):
+    def new_context(self, worker_id):
+        return {"sum": 0, "count": 0}
+
+    def accept(self, ctx, i, edge):
+        ctx["sum"] += edge.source + edge.target
+        ctx["count"] += 1
+
+    def merge(self, contexts):
+        return sum(c["sum"] for c in contexts), sum(c["count"] for c in contexts)
+
+
+class _Bitmap(pb.Consumer):
+    def __init__(self, m0, m):
+        self.m0, self.m = m0, m
+
+    def new_context(self, worker_id):
+        return np.zeros(self.m - self.m0, dtype=np.int64)
+
+    def accept_block(self, ctx, lo, edges):
+        ctx[lo - self.m0: lo - self.m0 + edges.shape[0]] += 1
+        return ctx
+
+    def merge(self, contexts):
+        return sum(contexts)
+
+
+class _Sleepy(pb.Consumer):
+    def __init__(self, slow_lo):
+        self.slow_lo = slow_lo
+
+    def new_context(self, worker_id):
+        return 0
+
+    def accept_block(self, ctx, lo, edges):
+        import time
+
+        if lo == self.slow_lo:
+            time.sleep(0.6)
+        return ctx + 1
+
+    def merge(self, contexts):
+        return list(contexts)
+
+
+def test_generic_consumers_batch_loop():
+    p = pb.GenParams(n=100, d=2)
+    arr, _ = pb.run(p, pb.CollectConsumer())
+    want = (int(arr.sum()), p.m)
+    assert pb.run(p, _PerEdgeSum(), workers=1, batch_size=17)[0] == want
+    assert pb.run(p, _PerEdgeSum(), workers=2, batch_size=17)[0] == want
+    q = pb.GenParams(n=500, d=3, n0=3, seed_edges=TRIANGLE)
+    for workers in (1, 3):
+        seen, st = pb.run(q, _Bitmap(q.m0, q.m), workers=workers, batch_size=97)
+        assert (seen == 1).all() and st.edges_emitted == q.m - q.m0
+        _, wp = O.generate_block(_op(q), q.m0, q.m)
+        assert st.hash_probes == wp
+    with pytest.raises(pb.GenerationError, match="worker .* failed") as ei:
+        pb.run(q, _Exploding(), workers=2, batch_size=10)
+    assert "synthetic consumer failure" in str(ei.value)
+    with pytest.raises(RuntimeError, match="synthetic consumer failure"):
+        pb.run(q, _Exploding(), workers=1)
+    r = pb.GenParams(n=40, d=3, n0=3, seed_edges=TRIANGLE)  # 111 edges, 12 batches
+    counts, st = pb.run(r, _Sleepy(r.m0), workers=2, batch_size=10)
+    assert sum(counts) == 12 and max(counts) >= 10
+    assert sum(w.batches for w in st.per_worker) == 12
+    # option flags: node-granular batches through a generic consumer
+    f = pb.GenParams(n=300, d=3, n0=3, seed_edges=TRIANGLE, no_self_loops=True)
+    seen, _ = pb.run(f, _Bitmap(f.m0, f.m), workers=2, batch_size=10)
+    assert (seen == 1).all()
