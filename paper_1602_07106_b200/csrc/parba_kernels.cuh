@@ -13,18 +13,21 @@
 //            (conflict-free, lane-consecutive) -- the first probe (half of
 //            all probes) needs one lookup instead of NB.  About half
 //            the edges finish here; the rest go to a per-warp smem queue.
-//   phase 2  lanes pop queued chains (ballot/popc refill) and probe until
-//            the queue is empty; chains still running stay in registers and
-//            carry over into the next tile, so lanes never wait for the
-//            longest chain of a tile.
-//   sink     Store: targets land in a 2-deep smem ring of tile buffers; a
-//            tile is written out (16-byte streaming stores, fully coalesced)
-//            once its last chain finished.  Window/Full: a finished chain
-//            increments its target's counter directly (E never stored).
+//   phase 2  lanes pop queued chains (ballot/popc refill) and probe while
+//            a warp's worth of entries is queued; chains still running stay
+//            in registers and carry over into the next tile, so lanes never
+//            wait for the longest chain of a tile (NS running chains per
+//            lane: 1 for the store sink, 2 for the streaming sinks).
+//   sink     Store: terminal values land in a 2-deep smem ring of tile
+//            buffers; a tile is written out (16-byte streaming stores, fully
+//            coalesced, sources and targets computed then) once its last
+//            chain finished.  Window/Full: a finished chain increments its
+//            target's counter directly (E never stored).
 //
 // Persistent grid: one resident wave of CTAs, warps stride over tiles.
-// Template axes: Hash (CRC with NB table bytes / SIMPLE; narrow = every chain
-// value < 2^32), SINK, SEED (m0 > 0 or n0 > 0: offsets and the seed stop).
+// Template axes: Hash (CRC with NC chunk tables / SIMPLE; narrow = every
+// chain value < 2^32), SINK, SEED (m0 > 0 or n0 > 0: offsets and the seed
+// stop), DEG (degree sequence: owner lookups instead of division by d).
 #pragma once
 #include <cstdint>
 #include <type_traits>
