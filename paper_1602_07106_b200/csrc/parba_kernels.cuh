@@ -62,6 +62,13 @@ constexpr uint64_t kRyMin = 1ull << 27;
 #define PARBA_MINB_STREAM 1
 #endif
 constexpr int kWarps = PARBA_WARPS;        // warps per CTA
+// Store-mode stage buffers (tiles in flight): 2 = flush tile t-1 after
+// phase 2 of tile t; 3 = flush tile t-2 (its chains have had a whole tile
+// longer to finish, so the flush rarely waits).
+#ifndef PARBA_NBUF
+#define PARBA_NBUF 2
+#endif
+constexpr int kStageBufs = PARBA_NBUF;
 
 // Debug builds (-DPARBA_DEBUG_CHECKS=1, tools/check_build.sh) trap on a
 // violated invariant; release builds compile the checks away.
@@ -111,7 +118,7 @@ struct TileLayout {
     static constexpr uint32_t kLgEB = kEB == 8 ? 3u : 2u;
     static constexpr uint32_t kQB = kQueue * kEB;
     static constexpr uint32_t kTB = kTile * (uint32_t)sizeof(R);  // one stage buffer
-    static constexpr uint32_t kStageB = SINK == kStore ? 2 * kTB : 0;
+    static constexpr uint32_t kStageB = SINK == kStore ? kStageBufs * kTB : 0;
     static constexpr bool kSlots = SINK == kStore && !Hash::kPack;
     static constexpr uint32_t kSlotB = kSlots ? kQueue * 2 : 0;
     static constexpr size_t kTabB = Hash::kHasCrc ? (Hash::kTableWords + kTile) * 4 : 0;
@@ -194,9 +201,12 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
     uint32_t headb = 0, tailb = 0;  // queue byte cursors (warp-uniform)
     uint32_t tile_q0 = 0;           // tail cursor at the start of the current tile
     uint32_t probes = 0;            // per lane (< 2^32 per launch and lane)
-    uint64_t prev_base = 0;
+    uint64_t prev_base = 0;         // base of the tile the next flush writes
     bool have_prev = false;
-    uint32_t buf = 0;
+    uint32_t buf = 0;               // stage buffer of the current tile
+    [[maybe_unused]] uint64_t mid_base = 0;  // 3 buffers: base of tile t-1
+    [[maybe_unused]] uint32_t q0_prev = 0;   // 3 buffers: queue cursor at the start of tile t-1
+    [[maybe_unused]] uint32_t n_inflight = 0;
 
     auto qaddr = [&](uint32_t cur) -> uint32_t { return qbase | (cur & (L::kQB - 1)); };
 
@@ -272,7 +282,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
                     saddr[Q] = (uint32_t)(e >> 32);
                 } else if constexpr (Hash::kPack) {
                     r[Q] = (R)(e & kValueMask52);
-                    saddr[Q] = stage_s + (uint32_t)(e >> 52);
+                    saddr[Q] = stage_s + (uint32_t)(e >> 52) * (uint32_t)sizeof(R);
                 } else {
                     r[Q] = (R)e;
                     saddr[Q] = stage_s + lds_u16(qs_s + ((cur & (L::kQB - 1)) >> 2));
@@ -337,7 +347,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
                 if constexpr (NARROW) {
                     sts_u64_if(pend, qaddr(cur), ((uint64_t)cell << 32) | (uint64_t)r1);
                 } else if constexpr (Hash::kPack) {
-                    sts_u64_if(pend, qaddr(cur), ((uint64_t)(cell - stage_s) << 52) | (uint64_t)r1);
+                    sts_u64_if(pend, qaddr(cur), ((uint64_t)(buf * kTile + j) << 52) | (uint64_t)r1);
                 } else if (pend) {
                     sts_u64(qaddr(cur), (uint64_t)r1);
                     sts_u16(qs_s + ((cur & (L::kQB - 1)) >> 2), (uint16_t)(cell - stage_s));
@@ -378,13 +388,14 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
                 step();
             } while (headb <= lim);
         }
-        // ---- store: flush the previous tile once none of its chains runs
+        // ---- store: flush the oldest tile in flight once none of its chains runs
         if constexpr (SINK == kStore) {
             if (have_prev) {
-                const uint32_t pb = buf ^ 1u;
-                // entries of the previous tile still queued (only when this
-                // tile pushed fewer than 32): pop them first
-                while ((int32_t)(tile_q0 - headb) > 0) {
+                // oldest tile: t-1 (2 buffers) or t-2 (3 buffers)
+                const uint32_t pb = kStageBufs == 2 ? (buf ^ 1u) : (buf == 2 ? 0u : buf + 1);
+                const uint32_t q_end = kStageBufs == 2 ? tile_q0 : q0_prev;  // its entries end here
+                // entries of that tile still queued: pop them first
+                while ((int32_t)(q_end - headb) > 0) {
                     refill(std::false_type{});
                     step();
                 }
@@ -399,9 +410,18 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
                 }
                 flush(pb, prev_base);
             }
-            prev_base = base;
-            have_prev = true;
-            buf ^= 1u;
+            if constexpr (kStageBufs == 2) {
+                prev_base = base;
+                have_prev = true;
+                buf ^= 1u;
+            } else {
+                have_prev = n_inflight >= 1;  // tile t-1 will be the next tile's t-2
+                if (n_inflight < 2) ++n_inflight;
+                prev_base = mid_base;         // t-1 becomes the oldest
+                mid_base = base;
+                q0_prev = tile_q0;
+                buf = buf == 2 ? 0u : buf + 1;
+            }
         }
     }
     // ---- drain the queue and the chains still running, then flush the last tile
@@ -411,7 +431,15 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
     }
     while (any_act()) step();
     if constexpr (SINK == kStore) {
-        if (have_prev) flush(buf ^ 1u, prev_base);
+        if constexpr (kStageBufs == 2) {
+            if (have_prev) flush(buf ^ 1u, prev_base);
+        } else {
+            // the last two tiles: buffers buf-2 (older) and buf-1 (newer)
+            const uint32_t b1 = buf == 0 ? 2u : buf - 1;
+            const uint32_t b2 = b1 == 0 ? 2u : b1 - 1;
+            if (n_inflight == 2) flush(b2, prev_base);
+            if (n_inflight >= 1) flush(b1, mid_base);
+        }
     }
 #if PARBA_WARP_TIMES
     {
