@@ -636,3 +636,26 @@ def test_generic_consumers_batch_loop():
     f = pb.GenParams(n=300, d=3, n0=3, seed_edges=TRIANGLE, no_self_loops=True)
     seen, _ = pb.run(f, _Bitmap(f.m0, f.m), workers=2, batch_size=10)
     assert (seen == 1).all()
+
+
+def test_huge_degree_and_offsets_vs_oracle():
+    """Closed forms with d >= 2^31 (the narrow 32-bit division does not
+    apply) and large seed offsets, store and window, vs the oracle."""
+    seed = np.array([x for i in range(50) for x in (i, (i + 7) % 50)], dtype=np.uint64)
+    for n, d, n0, sd in ((4, 2**33 + 7, 0, None), (60, 3 * 2**31, 50, seed), (10**6, 2**31 - 1, 50, seed)):
+        p = pb.GenParams(n=n, d=d, n0=n0, seed_edges=sd)
+        op = _op(p)
+        rng = np.random.default_rng(d % 1000)
+        for _ in range(3):
+            lo = int(rng.integers(p.m0, p.m - 3000))
+            hi = lo + 3000
+            got, pr = pb.generate_block(lo, hi, p)
+            want, wp = O.generate_block(op, lo, hi)
+            assert np.array_equal(got, want) and pr == wp, (n, d, lo)
+            K = n0 + 2
+            import torch
+
+            c, prb = pb.parallel.count_shard_device(p, K, lo, hi)
+            torch.cuda.synchronize()
+            w, _ = O.degree_block(op, lo, hi, K)
+            assert np.array_equal(c.cpu().numpy()[:K], w), (n, d, lo, "window")
