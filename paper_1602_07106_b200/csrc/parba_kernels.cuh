@@ -222,6 +222,24 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
         [[maybe_unused]] constexpr bool FULL = decltype(full_c)::value;
         if constexpr (SINK == kStore) {
             ulonglong2 *o = reinterpret_cast<ulonglong2 *>(a.out) + (int64_t)(base - lo);
+            if constexpr (FULL && !NARROW && !DEG) {
+                // 64-bit positions: one 64-bit division per lane and tile, then
+                // the lane's 8 sources from the remainder by the 32-bit magic
+                // (remainder + 32k < d + 224 < 2^31)
+                if (p.d < (1ull << 30)) {
+                    const uint64_t i0 = base + lane - (SEED ? p.m0 : 0);
+                    const uint64_t q0 = magic_div(i0, p.div64) + (SEED ? p.n0 : 0);
+                    const uint32_t r0 = (uint32_t)(i0 - (q0 - (SEED ? p.n0 : 0)) * p.d);
+#pragma unroll
+                    for (int k = 0; k < kEpl; ++k) {
+                        const uint32_t j = lane + 32u * k;
+                        const uint64_t tgt = target_of<NARROW, SEED, false, false>(
+                            (uint64_t)lds_t<R>(stage_s + (b * kTile + j) * (uint32_t)sizeof(R)), p);
+                        __stcs(o + j, make_ulonglong2(q0 + magic_div32(r0 + 32u * k, p.div32), tgt));
+                    }
+                    return;
+                }
+            }
 #pragma unroll
             for (int k = 0; k < kEpl; ++k) {
                 const uint32_t j = lane + 32u * k;
