@@ -659,3 +659,17 @@ def test_huge_degree_and_offsets_vs_oracle():
             torch.cuda.synchronize()
             w, _ = O.degree_block(op, lo, hi, K)
             assert np.array_equal(c.cpu().numpy()[:K], w), (n, d, lo, "window")
+
+
+def test_wide_store_flush_with_seed_vs_oracle():
+    """Store tiles at positions >= 2^32 (64-bit chain values) with and
+    without a seed graph: the per-tile source division path of the flush."""
+    seed = np.array([x for i in range(40) for x in (i, (i + 3) % 40)], dtype=np.uint64)
+    for n0, sd in ((0, None), (40, seed)):
+        p = pb.GenParams(n=10**9, d=10, n0=n0, seed_edges=sd)
+        op = _op(p)
+        for lo in (5 * 10**9 + 13, 2**33 - 1000):
+            hi = lo + 70_000
+            got, pr = pb.generate_block(lo, hi, p)
+            want, wp = O.generate_block(op, lo, hi)
+            assert np.array_equal(got, want) and pr == wp, (n0, lo)
