@@ -31,7 +31,7 @@ EXPORTS = (
     "parba_resolve_chains", "parba_generate", "parba_edges_at", "parba_degree_window",
     "parba_degree_full", "parba_count_ids", "parba_generate_host", "parba_degree_window_host",
     "parba_degseq_prefix", "parba_degseq_rank", "parba_rank1", "parba_node_of_edges", "parba_count_pairs",
-    "parba_multi_run", "parba_crc32c", "parba_mulhi_u64",
+    "parba_multi_run", "parba_crc32c", "parba_mulhi_u64", "parba_degseq_dense",
 )
 MULTI_STORE, MULTI_WINDOW, MULTI_FULL, MULTI_DISCARD = 0, 1, 2, 3
 
@@ -60,6 +60,7 @@ class CParams(ctypes.Structure):
         ("degree_prefix", ctypes.c_void_p),
         ("rank", ctypes.c_void_p),
         ("owners", ctypes.c_void_p),
+        ("dense_owner", ctypes.c_void_p),
     ]
 
 
@@ -101,6 +102,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
             "parba_count_pairs": ([vp, u64, u64, vp, vp], i32),
             "parba_crc32c": ([ctypes.c_uint32, vp, u64, vp, vp], i32),
             "parba_mulhi_u64": ([vp, vp, u64, vp, vp], i32),
+            "parba_degseq_dense": ([vp, u64, u64, vp, vp], i32),
             "parba_multi_run": ([P, i32, vp, i32, u64, vp, ctypes.POINTER(u64), ctypes.POINTER(ctypes.c_double)],
                                 i32),
         }

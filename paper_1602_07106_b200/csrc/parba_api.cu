@@ -108,6 +108,7 @@ DevParams make_dev(const parba_params_t *p, uint64_t K = 0) {
     d.W = p->degree_prefix;
     d.rank = (const ulonglong2 *)p->rank;
     d.owners = p->owners;
+    d.dense = p->dense_owner;
     // generated target ((r>>1) - m0)/d + n0 < K  <=>  r < 2*(m0 + (K - n0)*d)
     if (K <= p->n0) {
         d.win_rlim = 0;
@@ -662,6 +663,15 @@ int parba_degseq_rank(const uint64_t *W, uint64_t count, uint64_t m, uint64_t n0
         if (rc) return rc;
         *n_ones = v[0] + v[1];
     }
+    return PARBA_OK;
+}
+
+int parba_degseq_dense(const uint64_t *W, uint64_t count, uint64_t m0, uint32_t *dense, void *stream) {
+    if (count == 0) return PARBA_OK;
+    if (!W || !dense) return fail(PARBA_EINVAL, "NULL buffer");
+    if (count > 0xFFFFFFFFull) return fail(PARBA_EINVAL, "the dense owner map needs n - n0 < 2^32");
+    dense_fill_kernel<<<grid_for(count * 32, 256), 256, 0, (cudaStream_t)stream>>>(W, count, m0, dense);
+    CUDA_TRY(cudaGetLastError());
     return PARBA_OK;
 }
 

@@ -34,6 +34,11 @@ MAX_EDGES = 1 << 58
 # (32 Mi edges = 512 MiB per buffer, two buffers in flight).
 HOST_CHUNK_EDGES = 1 << 25
 
+# Degree sequences: build the dense owner map (4 bytes per generated edge,
+# one load per owner lookup instead of a rank entry + owners gather) when it
+# fits in this many bytes and in a quarter of the free device memory.
+DENSE_OWNER_MAX_BYTES = 1 << 34
+
 
 class Edge(NamedTuple):
     source: int
@@ -123,13 +128,24 @@ class GenParams:
         return self._index()[1]
 
     def _index(self, device=None):
+        """(prefix, rank bits, dense owner map or None) on `device` (cached)."""
         torch = _lib.torch_cuda()
         dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         cache = self.__dict__.setdefault("_index_dev", {})
         key = (dev.type, dev.index)
         if key not in cache:
             pi = degreeseq.build_prefix(self.degrees, self.m0, self.n0, device=dev)
-            cache[key] = (pi, degreeseq.build_rank_bits(pi, device=dev))
+            rb = degreeseq.build_rank_bits(pi, device=dev)
+            dense = None
+            nbytes = 4 * (self.m - self.m0)
+            if self.n - self.n0 < (1 << 32) and 0 < nbytes <= DENSE_OWNER_MAX_BYTES:
+                free, _ = torch.cuda.mem_get_info(dev)
+                if nbytes <= free // 4:
+                    dense = torch.empty(self.m - self.m0, dtype=torch.int32, device=dev)
+                    with torch.cuda.device(dev):
+                        _lib.check(_lib.load().parba_degseq_dense(pi.W_dev.data_ptr(), pi.n_nodes, self.m0,
+                                                                  dense.data_ptr(), _lib.stream_ptr(torch, dev)))
+            cache[key] = (pi, rb, dense)
         return cache[key]
 
     def _host_W(self) -> np.ndarray:
@@ -178,12 +194,13 @@ class GenParams:
             cp = c_params(self.hash, self.n, self.d, self.n0, self.m0, seed_ptr)
         else:
             cp = c_params(self.hash, self.n, 1, self.n0, self.m0, seed_ptr)
-            pi, rb = self._index(dev)
+            pi, rb, dense = self._index(dev)
             cp.d = 0
             cp.m = self.m
             cp.degree_prefix = pi.W_dev.data_ptr()
             cp.rank = rb.rank_dev.data_ptr() if rb.rank_dev is not None else None
             cp.owners = rb.owners_dev.data_ptr() if rb.owners_dev is not None else None
+            cp.dense_owner = dense.data_ptr() if dense is not None else None
         cp.flags = ((_lib.FLAG_NO_SELF_LOOPS if self.no_self_loops else 0)
                     | (_lib.FLAG_NO_PARALLEL_EDGES if self.no_parallel_edges else 0))
         cp.max_attempts = self.max_attempts or 0

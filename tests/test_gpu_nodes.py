@@ -316,3 +316,22 @@ def test_degree_count_windows_edge_cases_vs_oracle():
             O.count_block(want, np.asarray(seed, dtype=np.uint64))
             counter, _ = pb.degree_counts(p, K=K)
             assert counter.K == K and np.array_equal(counter.counts, want), (p, K)
+
+
+def test_degree_sequence_rank_path_without_dense_map(golden_nodes, monkeypatch):
+    """The generator uses the dense owner map when it fits; with the map
+    disabled the rank-directory lookups must give the same bytes."""
+    from paper_1602_07106_b200 import generator as G
+
+    arrays, meta = golden_nodes
+    monkeypatch.setattr(G, "DENSE_OWNER_MAX_BYTES", 0)
+    for c in meta["degseq"][::5]:
+        p = params_deg(c, arrays)
+        assert p._index()[2] is None
+        got, probes = pb.generate_block(p.m0, p.m, p)
+        assert _sha(got) == c["sha256"] and probes == c["probes"], c["name"]
+    for c in meta["counts"]:
+        case = next(x for x in meta["degseq"] if x["name"] == c["case"])
+        p = params_deg(case, arrays)
+        counter, stats = pb.degree_counts(p, K=c["K"]) if c["K"] else pb.degree_counts(p)
+        assert _sha(counter.counts) == c["sha256"], c
