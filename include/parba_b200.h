@@ -78,9 +78,9 @@ typedef struct parba_params {
     const uint64_t *degree_prefix; /* W: n - n0 + 1 entries               */
     const void *rank;              /* rank directory, (m + 63) / 64 x 16 B */
     const uint64_t *owners;        /* rank -> node; NULL iff every degree >= 1 */
-    const uint32_t *dense_owner;   /* optional (NULL): node - n0 of every position
-                                      m0..m-1 (parba_degseq_dense), 4 B per edge:
-                                      one load per owner lookup */
+    const uint32_t *dense_owner;   /* optional (NULL): owning node of every position
+                                      m0..m-1 (parba_degseq_dense; n < 2^32), 4 B
+                                      per edge: one load per owner lookup */
 } parba_params_t;
 
 /* Library / ABI version (major*10000 + minor*100 + patch). */
@@ -149,10 +149,11 @@ int parba_degseq_prefix(const uint64_t *degrees, uint64_t count, uint64_t m0, ui
  * n_ones (host, optional) receives the number of such nodes. */
 int parba_degseq_rank(const uint64_t *W, uint64_t count, uint64_t m, uint64_t n0, void *rank,
                       uint64_t *owners, uint64_t *n_ones, void *stream);
-/* Optional dense owner map for faster generation: dense[e - m0] = owner(e) -
- * n0 for every generated position (m - m0 entries of 4 bytes; needs
- * n - n0 < 2^32).  Same results as the rank directory. */
-int parba_degseq_dense(const uint64_t *W, uint64_t count, uint64_t m0, uint32_t *dense, void *stream);
+/* Optional dense owner map for faster generation: dense[e - m0] = owner(e)
+ * for every generated position (m - m0 entries of 4 bytes; needs n < 2^32).
+ * Same results as the rank directory. */
+int parba_degseq_dense(const uint64_t *W, uint64_t count, uint64_t m0, uint64_t n0, uint32_t *dense,
+                       void *stream);
 /* rank1_many (degreeseq.py:154-162): out[k] = ones at positions 0..es[k]. */
 int parba_rank1(const void *rank, const uint64_t *es, uint64_t count, uint64_t *out, void *stream);
 /* node_of_edge_many / node_of_edge_bisect_many / owners_of_edges_deferred

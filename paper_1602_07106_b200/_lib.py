@@ -102,7 +102,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
             "parba_count_pairs": ([vp, u64, u64, vp, vp], i32),
             "parba_crc32c": ([ctypes.c_uint32, vp, u64, vp, vp], i32),
             "parba_mulhi_u64": ([vp, vp, u64, vp, vp], i32),
-            "parba_degseq_dense": ([vp, u64, u64, vp, vp], i32),
+            "parba_degseq_dense": ([vp, u64, u64, u64, vp, vp], i32),
             "parba_multi_run": ([P, i32, vp, i32, u64, vp, ctypes.POINTER(u64), ctypes.POINTER(ctypes.c_double)],
                                 i32),
         }

@@ -666,11 +666,12 @@ int parba_degseq_rank(const uint64_t *W, uint64_t count, uint64_t m, uint64_t n0
     return PARBA_OK;
 }
 
-int parba_degseq_dense(const uint64_t *W, uint64_t count, uint64_t m0, uint32_t *dense, void *stream) {
+int parba_degseq_dense(const uint64_t *W, uint64_t count, uint64_t m0, uint64_t n0, uint32_t *dense,
+                       void *stream) {
     if (count == 0) return PARBA_OK;
     if (!W || !dense) return fail(PARBA_EINVAL, "NULL buffer");
-    if (count > 0xFFFFFFFFull) return fail(PARBA_EINVAL, "the dense owner map needs n - n0 < 2^32");
-    dense_fill_kernel<<<grid_for(count * 32, 256), 256, 0, (cudaStream_t)stream>>>(W, count, m0, dense);
+    if (n0 + count > 0xFFFFFFFFull) return fail(PARBA_EINVAL, "the dense owner map needs n < 2^32");
+    dense_fill_kernel<<<grid_for(count * 32, 256), 256, 0, (cudaStream_t)stream>>>(W, count, m0, n0, dense);
     CUDA_TRY(cudaGetLastError());
     return PARBA_OK;
 }

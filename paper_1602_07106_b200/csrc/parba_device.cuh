@@ -98,7 +98,7 @@ struct DevParams {
     const uint64_t *W;         // W[k] = first edge of node n0+k, W[n-n0] = m
     const ulonglong2 *rank;    // per 64 positions: {start bits, ones before}
     const uint64_t *owners;    // rank -> node, NULL when every degree >= 1
-    const uint32_t *dense;     // optional: node - n0 of every generated position (m - m0 entries)
+    const uint32_t *dense;     // optional: owning node of every generated position (m - m0 entries, n < 2^32)
 };
 
 // Rank directory of a degree sequence: one 16-byte entry per 64 positions,
@@ -116,7 +116,7 @@ __device__ __forceinline__ uint64_t rank1_dev(const ulonglong2 *rank, uint64_t e
 // With the dense map (4 bytes per position, parba_degseq_dense) a lookup is
 // one independent 4-byte load instead of a rank entry and an owners gather.
 __device__ __forceinline__ uint64_t node_of(uint64_t e, const DevParams &p) {
-    if (p.dense) return p.n0 + __ldg(p.dense + (e - p.m0));
+    if (p.dense) return __ldg(p.dense + (e - p.m0));
     const uint64_t r = rank1_dev(p.rank, e);
     return p.owners ? __ldg(p.owners + r - 1) : p.n0 + r - 1;
 }

@@ -63,15 +63,16 @@ __global__ void owners_kernel(const uint64_t *__restrict__ W, uint64_t count, ui
     }
 }
 
-// Dense owner map: dense[pos - m0] = node - n0 for every generated position
+// Dense owner map: dense[pos - m0] = owning node of every generated position
 // (one warp per node fills its edge span; spans are contiguous and disjoint).
-__global__ void dense_fill_kernel(const uint64_t *__restrict__ W, uint64_t count, uint64_t m0, uint32_t *dense) {
+__global__ void dense_fill_kernel(const uint64_t *__restrict__ W, uint64_t count, uint64_t m0, uint64_t n0,
+                                  uint32_t *dense) {
     const int lane = threadIdx.x & 31;
     const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t k = warp; k < count; k += nwarps) {
         const uint64_t a = W[k], b = W[k + 1];
-        for (uint64_t e = a + lane; e < b; e += 32) dense[e - m0] = (uint32_t)k;
+        for (uint64_t e = a + lane; e < b; e += 32) dense[e - m0] = (uint32_t)(n0 + k);
     }
 }
 

@@ -138,13 +138,14 @@ class GenParams:
             rb = degreeseq.build_rank_bits(pi, device=dev)
             dense = None
             nbytes = 4 * (self.m - self.m0)
-            if self.n - self.n0 < (1 << 32) and 0 < nbytes <= DENSE_OWNER_MAX_BYTES:
+            if self.n < (1 << 32) and 0 < nbytes <= DENSE_OWNER_MAX_BYTES:
                 free, _ = torch.cuda.mem_get_info(dev)
                 if nbytes <= free // 4:
                     dense = torch.empty(self.m - self.m0, dtype=torch.int32, device=dev)
                     with torch.cuda.device(dev):
                         _lib.check(_lib.load().parba_degseq_dense(pi.W_dev.data_ptr(), pi.n_nodes, self.m0,
-                                                                  dense.data_ptr(), _lib.stream_ptr(torch, dev)))
+                                                                  self.n0, dense.data_ptr(),
+                                                                  _lib.stream_ptr(torch, dev)))
             cache[key] = (pi, rb, dense)
         return cache[key]
 

@@ -78,7 +78,7 @@ def main():
         f = pb.GenParams(n=n // 10, d=10, n0=12, seed_edges=seed, **kw)
         cf = f._device_params(dev)
         out = torch.empty(2 * (f.m - f.m0), dtype=torch.int64, device=dev)
-        t = timeit(lambda: _lib.check(L.parba_generate(cf, f.m0, f.m, out.data_ptr(), prb.data_ptr(), st)), reps=2)
+        t = timeit(lambda: _lib.check(L.parba_generate(cf, f.m0, f.m, out.data_ptr(), prb.data_ptr(), st)), reps=6)
         res[f"flags_{name}_edges_per_s"] = (f.m - f.m0) / t
         del out
     print(json.dumps(res))
