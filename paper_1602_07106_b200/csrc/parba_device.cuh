@@ -111,12 +111,27 @@ __device__ __forceinline__ uint64_t rank1_dev(const ulonglong2 *rank, uint64_t e
     const uint64_t mask = ~(0xFFFFFFFFFFFFFFFEull << (e & 63));  // bits 0..e&63
     return w.y + (uint64_t)__popcll(w.x & mask);
 }
+// Random 4-byte read of the dense owner map.  PARBA_DENSE_LD selects the
+// load form (0: ld.global.nc; 1: no L1 allocation + 64-byte L2 fetch hint).
+#ifndef PARBA_DENSE_LD
+#define PARBA_DENSE_LD 1
+#endif
+__device__ __forceinline__ uint32_t ld_dense(const uint32_t *ptr) {
+#if PARBA_DENSE_LD == 1
+    uint32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::64B.u32 %0, [%1];" : "=r"(v) : "l"(ptr));
+    return v;
+#else
+    return __ldg(ptr);
+#endif
+}
+
 // Owning node of generated position e (m0 <= e < m): node_of_edge
 // (degreeseq.py:165-178) -- the last node with W <= e and degree >= 1.
 // With the dense map (4 bytes per position, parba_degseq_dense) a lookup is
 // one independent 4-byte load instead of a rank entry and an owners gather.
 __device__ __forceinline__ uint64_t node_of(uint64_t e, const DevParams &p) {
-    if (p.dense) return __ldg(p.dense + (e - p.m0));
+    if (p.dense) return ld_dense(p.dense + (e - p.m0));
     const uint64_t r = rank1_dev(p.rank, e);
     return p.owners ? __ldg(p.owners + r - 1) : p.n0 + r - 1;
 }
