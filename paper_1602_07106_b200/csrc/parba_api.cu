@@ -13,6 +13,8 @@
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
 
 #include "../../include/parba_b200.h"
 #include "parba_kernels.cuh"
@@ -352,6 +354,73 @@ int boundary_node(const parba_params_t *p, const DevParams &dp, uint64_t pos, ui
 
 uint64_t node_first_edge(const parba_params_t *p, uint64_t v) { return p->m0 + (v - p->n0) * p->d; }
 
+// no_parallel_edges nodes of degree > kBigDegree: node_big_kernel with a
+// per-node hash set in scratch, in chunks of at most kBigScratchWords words.
+constexpr uint64_t kBigScratchWords = 1ull << 27;  // 1 GiB per chunk
+
+int generate_big_nodes(const parba_params_t *p, const DevParams &dp, const NodeArgs &na, uint64_t vlo,
+                       uint64_t vhi, uint64_t lo, uint64_t hi, uint64_t *out, unsigned long long *probes,
+                       unsigned long long *fail_edge, cudaStream_t st) {
+    int rc;
+    if (!is_deg(p)) {  // uniform degree: every node or none is big
+        if (p->d <= kBigDegree) return PARBA_OK;
+        const uint64_t per = node_big_words(p->d);
+        const uint64_t step = kBigScratchWords / per > 0 ? kBigScratchWords / per : 1;
+        for (uint64_t v = vlo; v < vhi; v += step) {
+            const uint64_t c = vhi - v < step ? vhi - v : step;
+            AsyncBuf scratch;
+            if ((rc = scratch.alloc(c * per * 8, st))) return rc;
+            node_big_kernel<false><<<grid_for(c, 128), 128, 0, st>>>(dp, na, nullptr, v, c, nullptr, 0, per,
+                                                                    (uint64_t *)scratch.p, lo, hi - lo,
+                                                                    (ulonglong2 *)out, probes, fail_edge);
+            CUDA_TRY(cudaGetLastError());
+        }
+        return PARBA_OK;
+    }
+    // degree sequence: list of big nodes (CUB select over node ids), scratch
+    // offsets by an exclusive scan, processed in chunks of the list
+    const uint64_t nv = vhi - vlo;
+    AsyncBuf flags, list, nsel, words, offs, tmp;
+    if ((rc = flags.alloc(nv, st)) || (rc = list.alloc(nv * 8, st)) || (rc = nsel.alloc(8, st))) return rc;
+    big_flags_kernel<<<grid_for(nv, 256), 256, 0, st>>>(dp, vlo, vhi, kBigDegree, (uint8_t *)flags.p);
+    CUDA_TRY(cudaGetLastError());
+    cub::CountingInputIterator<uint64_t> ids(vlo);
+    size_t tb = 0;
+    CUDA_TRY(cub::DeviceSelect::Flagged(nullptr, tb, ids, (const uint8_t *)flags.p, (uint64_t *)list.p,
+                                        (int64_t *)nsel.p, (int64_t)nv, st));
+    if ((rc = tmp.alloc(tb, st))) return rc;
+    CUDA_TRY(cub::DeviceSelect::Flagged(tmp.p, tb, ids, (const uint8_t *)flags.p, (uint64_t *)list.p,
+                                        (int64_t *)nsel.p, (int64_t)nv, st));
+    uint64_t nbig;
+    if ((rc = read_u64s((const uint64_t *)nsel.p, &nbig, 1, st))) return rc;
+    if (nbig == 0) return PARBA_OK;
+    if ((rc = words.alloc(nbig * 8, st)) || (rc = offs.alloc((nbig + 1) * 8, st))) return rc;
+    big_words_kernel<<<grid_for(nbig, 256), 256, 0, st>>>(dp, (const uint64_t *)list.p, nbig, (uint64_t *)words.p);
+    CUDA_TRY(cudaGetLastError());
+    AsyncBuf tmp2;
+    tb = 0;
+    CUDA_TRY(cub::DeviceScan::InclusiveSum(nullptr, tb, (const uint64_t *)words.p, (uint64_t *)offs.p + 1,
+                                           (int64_t)nbig, st));
+    if ((rc = tmp2.alloc(tb, st))) return rc;
+    CUDA_TRY(cudaMemsetAsync(offs.p, 0, 8, st));
+    CUDA_TRY(cub::DeviceScan::InclusiveSum(tmp2.p, tb, (const uint64_t *)words.p, (uint64_t *)offs.p + 1,
+                                           (int64_t)nbig, st));
+    std::vector<uint64_t> off(nbig + 1);
+    if ((rc = read_u64s((const uint64_t *)offs.p, off.data(), nbig + 1, st))) return rc;
+    for (uint64_t k0 = 0; k0 < nbig;) {
+        uint64_t k1 = k0 + 1;
+        while (k1 < nbig && off[k1 + 1] - off[k0] <= kBigScratchWords) ++k1;
+        AsyncBuf scratch;
+        if ((rc = scratch.alloc((off[k1] - off[k0]) * 8, st))) return rc;
+        node_big_kernel<true><<<grid_for(k1 - k0, 128), 128, 0, st>>>(
+            dp, na, (const uint64_t *)list.p + k0, 0, k1 - k0, (const uint64_t *)offs.p + k0, off[k0], 0,
+            (uint64_t *)scratch.p, lo, hi - lo, (ulonglong2 *)out, probes, fail_edge);
+        CUDA_TRY(cudaGetLastError());
+        k0 = k1;
+    }
+    return PARBA_OK;
+}
+
 // Edges of nodes [vlo, vhi) (first edge lo) into out, honouring the flags;
 // synchronises st to report an infeasible node (InfeasibleTargetsError).
 int generate_nodes(const parba_params_t *p, const DevParams &dp, uint64_t vlo, uint64_t vhi, uint64_t lo,
@@ -370,13 +439,17 @@ int generate_nodes(const parba_params_t *p, const DevParams &dp, uint64_t vlo, u
     if (rc) return rc;
     CUDA_TRY(cudaMemsetAsync(fe.p, 0xFF, sizeof(unsigned long long), st));
     const unsigned grid = grid_for(vhi - vlo, 256);
+    const uint64_t big = na.no_parallel_edges ? kBigDegree : UINT64_MAX;
+    unsigned long long *fep = (unsigned long long *)fe.p;
     if (is_deg(p))
-        node_kernel<true><<<grid, 256, 0, st>>>(dp, na, vlo, vhi, lo, hi - lo, (ulonglong2 *)out, probes,
-                                                (unsigned long long *)fe.p);
+        node_kernel<true><<<grid, 256, 0, st>>>(dp, na, vlo, vhi, lo, hi - lo, (ulonglong2 *)out, probes, fep, big);
     else
-        node_kernel<false><<<grid, 256, 0, st>>>(dp, na, vlo, vhi, lo, hi - lo, (ulonglong2 *)out, probes,
-                                                 (unsigned long long *)fe.p);
+        node_kernel<false><<<grid, 256, 0, st>>>(dp, na, vlo, vhi, lo, hi - lo, (ulonglong2 *)out, probes, fep, big);
     CUDA_TRY(cudaGetLastError());
+    if (na.no_parallel_edges) {
+        rc = generate_big_nodes(p, dp, na, vlo, vhi, lo, hi, out, probes, fep, st);
+        if (rc) return rc;
+    }
     uint64_t edge;
     rc = read_u64s((const uint64_t *)fe.p, &edge, 1, st);
     if (rc) return rc;

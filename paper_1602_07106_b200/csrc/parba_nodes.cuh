@@ -157,7 +157,8 @@ __global__ void owner_span_kernel(DevParams p, uint64_t pos, uint64_t *out) {
 // Option flags
 
 constexpr int kFamilies = 256;  // retry families cached in shared memory
-constexpr int kMemo = 16;       // memoised (r0, attempt) targets per node (no_self_loops)
+constexpr int kMemo = 288;      // memoised (r0, attempt) targets per small node (no_self_loops)
+constexpr uint64_t kBigDegree = 256;  // no_parallel_edges: larger nodes use a hash set
 
 struct NodeArgs {
     uint32_t no_self_loops, no_parallel_edges;
@@ -202,71 +203,64 @@ __device__ __forceinline__ uint64_t chain_family(uint32_t tab, uint64_t r, const
     return r;
 }
 
-// Edges of nodes [vlo, vhi) into out (row i - lo), honouring the flags
-// (_node_edges_with_probes, generator.py:184-217).  fail_edge receives the
-// smallest edge index that found no fresh target (InfeasibleTargetsError).
+// Open-addressing set of a node's accepted targets (key t + 1; 0 = empty),
+// capacity a power of two >= 2 * degree, in global scratch (big nodes).
+__device__ __forceinline__ bool set_insert_if_absent(uint64_t *tab, uint32_t lg_cap, uint64_t t) {
+    const uint64_t key = t + 1, mask = (1ull << lg_cap) - 1;
+    uint64_t h = (key * 0x9E3779B97F4A7C15ull) >> (64 - lg_cap);
+    for (;;) {
+        const uint64_t cur = tab[h];
+        if (cur == key) return false;
+        if (cur == 0) {
+            tab[h] = key;
+            return true;
+        }
+        h = (h + 1) & mask;
+    }
+}
+
+// no_parallel_edges for one node (_node_edges_with_probes, generator.py:
+// 199-217): edge i takes the first attempt a whose target is not among the
+// node's accepted targets.  Membership: `set` (hash set, big nodes) or a scan
+// of the node's output rows (small nodes).  With no_self_loops all edges of
+// v share r0, so attempt a has the same target for every edge: targets and
+// cumulative probe counts are memoised, and edge i starts at the attempt after
+// edge i-1's (earlier ones stay rejected: the accepted set only grows) while
+// adding the probes the reference spends re-walking them.
 template <bool DEG>
-__global__ void __launch_bounds__(256)
-node_kernel(DevParams p, NodeArgs na, uint64_t vlo, uint64_t vhi, uint64_t lo, uint64_t n_out, ulonglong2 *out,
-            unsigned long long *probes_out, unsigned long long *fail_edge) {
-    __shared__ uint32_t tabs_p[8 * 256];
-    __shared__ Family fams[kFamilies];  // retry families 0..kFamilies-1 (built once per CTA)
-    build_byte_tables(tabs_p, 8, 0u);
-    if (na.no_parallel_edges)
-        for (int a = threadIdx.x; a < kFamilies; a += blockDim.x) fams[a] = family_of(a, p, na);
-    __syncthreads();
-    const uint32_t tab = opaque(smem_addr(tabs_p));
-    const bool simple = na.simple != 0;
-    uint64_t probes = 0;
-    for (uint64_t v = vlo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < vhi;
-         v += (uint64_t)gridDim.x * blockDim.x) {
-        uint64_t first, dv;
-        if constexpr (DEG) {
-            first = __ldg(p.W + (v - p.n0));
-            dv = __ldg(p.W + (v - p.n0) + 1) - first;
-        } else {
-            first = p.m0 + (v - p.n0) * p.d;
-            dv = p.d;
-        }
-        if (dv == 0) continue;
-        if (!na.no_parallel_edges) {
-            // no_self_loops alone: every edge of v runs the same chain
-            uint64_t pr = 0;
-            const Family f0{p.k0, p.k01, p.mult};
-            const uint64_t r = chain_family(tab, 2 * first, f0, simple, p.stop, pr);
-            probes += pr * dv;
-            const uint64_t t = target_of<false, true, false, DEG>(r, p);
-            PARBA_CHECK(first - lo + dv <= n_out);
-            for (uint64_t i = first; i < first + dv; ++i) out[i - lo] = make_ulonglong2(v, t);
-            continue;
-        }
-        const uint64_t cap = na.max_attempts ? na.max_attempts : 64 * dv;
-        // with no_self_loops every edge of v starts at the same r0, so the
-        // target of (r0, attempt a) is the same for all of them: memoised
-        // (probe totals still count every evaluation, as the reference does)
-        uint64_t memo_t[kMemo];
-        uint32_t memo_p[kMemo];
-        uint32_t n_memo = 0;
-        for (uint64_t i = first; i < first + dv; ++i) {
-            const uint64_t r0 = na.no_self_loops ? 2 * first : 2 * i + 1;
-            uint64_t t = 0;
-            bool fresh = false;
-            for (uint64_t attempt = 0; attempt < cap && !fresh; ++attempt) {
-                if (na.no_self_loops && attempt < n_memo) {
-                    t = memo_t[attempt];
-                    probes += memo_p[attempt];
-                } else {
-                    const Family f = attempt < kFamilies ? fams[attempt] : family_of(attempt, p, na);
-                    uint64_t pr = 0;
-                    const uint64_t r = chain_family(tab, r0, f, simple, p.stop, pr);
-                    probes += pr;
-                    t = target_of<false, true, false, DEG>(r, p);
-                    if (na.no_self_loops && attempt == n_memo && n_memo < kMemo) {
-                        memo_t[n_memo] = t;
-                        memo_p[n_memo] = (uint32_t)pr;
-                        ++n_memo;
-                    }
+__device__ __forceinline__ bool node_npe(uint64_t v, uint64_t first, uint64_t dv, uint64_t lo, ulonglong2 *out,
+                                         uint64_t *set, uint32_t lg_cap, uint64_t *memo_t, uint64_t *memo_c,
+                                         uint32_t memo_cap, const Family *fams, uint32_t tab, bool simple,
+                                         const DevParams &p, const NodeArgs &na, uint64_t &probes,
+                                         unsigned long long *fail_edge) {
+    const bool nsl = na.no_self_loops != 0;
+    const uint64_t cap = na.max_attempts ? na.max_attempts : 64 * dv;
+    uint32_t n_memo = 0;
+    uint64_t a_start = 0;
+    for (uint64_t i = first; i < first + dv; ++i) {
+        const uint64_t r0 = nsl ? 2 * first : 2 * i + 1;
+        const uint64_t a0 = (nsl && a_start <= n_memo) ? a_start : 0;
+        uint64_t pr_acc = (nsl && a0 > 0) ? memo_c[a0 - 1] : 0;
+        uint64_t t = 0, a = a0;
+        bool fresh = false;
+        for (; a < cap; ++a) {
+            if (nsl && a < n_memo) {
+                t = memo_t[a];
+                pr_acc = memo_c[a];
+            } else {
+                const Family f = a < kFamilies ? fams[a] : family_of(a, p, na);
+                uint64_t pr = 0;
+                t = target_of<false, true, false, DEG>(chain_family(tab, r0, f, simple, p.stop, pr), p);
+                pr_acc += pr;
+                if (nsl && a == n_memo && n_memo < memo_cap) {
+                    memo_t[n_memo] = t;
+                    memo_c[n_memo] = pr_acc;
+                    ++n_memo;
                 }
+            }
+            if (set) {
+                fresh = set_insert_if_absent(set, lg_cap, t);
+            } else {
                 fresh = true;
                 for (uint64_t j = first; j < i; ++j)  // the node's accepted targets so far
                     if (out[j - lo].y == t) {
@@ -274,18 +268,139 @@ node_kernel(DevParams p, NodeArgs na, uint64_t vlo, uint64_t vhi, uint64_t lo, u
                         break;
                     }
             }
-            if (!fresh) {
-                atomicMin(fail_edge, (unsigned long long)i);
-                break;
-            }
-            PARBA_CHECK(i - lo < n_out);
-            out[i - lo] = make_ulonglong2(v, t);
+            if (fresh) break;
         }
+        probes += pr_acc;
+        if (!fresh) {
+            atomicMin(fail_edge, (unsigned long long)i);
+            return false;
+        }
+        out[i - lo] = make_ulonglong2(v, t);
+        a_start = a + 1;
     }
+    return true;
+}
+
+// Node-kernel prologue: seed-free CRC byte tables and the retry families.
+#define PARBA_NODE_PROLOGUE                                                                \
+    __shared__ uint32_t tabs_p[8 * 256];                                                   \
+    __shared__ Family fams[kFamilies];                                                     \
+    build_byte_tables(tabs_p, 8, 0u);                                                      \
+    if (na.no_parallel_edges)                                                              \
+        for (int a_ = threadIdx.x; a_ < kFamilies; a_ += blockDim.x) fams[a_] = family_of(a_, p, na); \
+    __syncthreads();                                                                       \
+    const uint32_t tab = opaque(smem_addr(tabs_p));                                        \
+    const bool simple = na.simple != 0;                                                    \
+    uint64_t probes = 0
+
+__device__ __forceinline__ void node_probes_flush(uint64_t probes, unsigned long long *probes_out) {
     if (probes_out) {
         for (int o = 16; o > 0; o >>= 1) probes += __shfl_xor_sync(0xffffffffu, probes, o);
         if ((threadIdx.x & 31) == 0 && probes) atomicAdd(probes_out, (unsigned long long)probes);
     }
+}
+
+template <bool DEG>
+__device__ __forceinline__ void node_span(uint64_t v, const DevParams &p, uint64_t &first, uint64_t &dv) {
+    if constexpr (DEG) {
+        first = __ldg(p.W + (v - p.n0));
+        dv = __ldg(p.W + (v - p.n0) + 1) - first;
+    } else {
+        first = p.m0 + (v - p.n0) * p.d;
+        dv = p.d;
+    }
+}
+
+// Edges of nodes [vlo, vhi) into out (row i - lo), honouring the flags
+// (_node_edges_with_probes, generator.py:184-217), one thread per node.
+// Under no_parallel_edges nodes of degree > big_deg are skipped here (they
+// run in node_big_kernel with a hash set).  fail_edge receives the smallest
+// edge index that found no fresh target (InfeasibleTargetsError).
+template <bool DEG>
+__global__ void __launch_bounds__(256)
+node_kernel(DevParams p, NodeArgs na, uint64_t vlo, uint64_t vhi, uint64_t lo, uint64_t n_out, ulonglong2 *out,
+            unsigned long long *probes_out, unsigned long long *fail_edge, uint64_t big_deg) {
+    PARBA_NODE_PROLOGUE;
+    uint64_t memo_t[kMemo], memo_c[kMemo];
+    for (uint64_t v = vlo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < vhi;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t first, dv;
+        node_span<DEG>(v, p, first, dv);
+        if (dv == 0) continue;
+        PARBA_CHECK(first - lo + dv <= n_out);
+        if (!na.no_parallel_edges) {
+            // no_self_loops alone: every edge of v runs the same chain
+            uint64_t pr = 0;
+            const Family f0{p.k0, p.k01, p.mult};
+            const uint64_t r = chain_family(tab, 2 * first, f0, simple, p.stop, pr);
+            probes += pr * dv;
+            const uint64_t t = target_of<false, true, false, DEG>(r, p);
+            for (uint64_t i = first; i < first + dv; ++i) out[i - lo] = make_ulonglong2(v, t);
+            continue;
+        }
+        if (dv > big_deg) continue;
+        node_npe<DEG>(v, first, dv, lo, out, nullptr, 0, memo_t, memo_c, kMemo, fams, tab, simple, p, na,
+                      probes, fail_edge);
+    }
+    node_probes_flush(probes, probes_out);
+}
+
+// no_parallel_edges for high-degree nodes: one thread per node with an
+// open-addressing set of its targets (and its no_self_loops memo) in global
+// scratch -- O(degree) per node instead of the scan's O(degree^2).  Node k of
+// the launch is nodes[k] (or vlo + k); its scratch starts at off[k] (or k *
+// per_node) words: set (2^lg words) then memo targets and cumulative probes.
+template <bool DEG>
+__global__ void __launch_bounds__(128)
+node_big_kernel(DevParams p, NodeArgs na, const uint64_t *nodes, uint64_t vlo, uint64_t count,
+                const uint64_t *off, uint64_t off_base, uint64_t per_node, uint64_t *scratch, uint64_t lo, uint64_t n_out,
+                ulonglong2 *out, unsigned long long *probes_out, unsigned long long *fail_edge) {
+    PARBA_NODE_PROLOGUE;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t v = nodes ? nodes[k] : vlo + k;
+        uint64_t first, dv;
+        node_span<DEG>(v, p, first, dv);
+        PARBA_CHECK(first - lo + dv <= n_out);
+        uint32_t lg = 1;
+        while ((1ull << lg) < 2 * dv) ++lg;
+        uint64_t *set = scratch + (off ? off[k] - off_base : k * per_node);
+        for (uint64_t q = 0; q < (1ull << lg); ++q) set[q] = 0;
+        const uint32_t memo_cap = (uint32_t)(2 * dv + 64);
+        uint64_t *memo_t = set + (1ull << lg);
+        node_npe<DEG>(v, first, dv, lo, out, set, lg, memo_t, memo_t + memo_cap, memo_cap, fams, tab, simple, p,
+                      na, probes, fail_edge);
+    }
+    node_probes_flush(probes, probes_out);
+}
+
+// Scratch words of a big node: its set (power of two >= 2 * degree) + memo.
+__host__ __device__ inline uint64_t node_big_words(uint64_t dv) {
+    uint64_t c = 2;
+    while (c < 2 * dv) c <<= 1;
+    return c + 2 * (2 * dv + 64);
+}
+
+// Degree-sequence nodes of [vlo, vhi) with degree > big_deg: flags, then a
+// CUB select; their scratch sizes for an exclusive scan.
+__global__ void big_flags_kernel(DevParams p, uint64_t vlo, uint64_t vhi, uint64_t big_deg, uint8_t *flags) {
+    for (uint64_t v = vlo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < vhi;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t dv = __ldg(p.W + (v - p.n0) + 1) - __ldg(p.W + (v - p.n0));
+        flags[v - vlo] = dv > big_deg ? 1 : 0;
+    }
+}
+__global__ void big_words_kernel(DevParams p, const uint64_t *nodes, uint64_t count, uint64_t *words) {
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t v = nodes[k];
+        words[k] = node_big_words(__ldg(p.W + (v - p.n0) + 1) - __ldg(p.W + (v - p.n0)));
+    }
+}
+__global__ void iota_from_kernel(uint64_t *v, uint64_t count, uint64_t start) {
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count;
+         k += (uint64_t)gridDim.x * blockDim.x)
+        v[k] = start + k;
 }
 
 // count_block over stored pairs (analytics.py:44-48): both endpoints < K.

@@ -335,3 +335,31 @@ def test_degree_sequence_rank_path_without_dense_map(golden_nodes, monkeypatch):
         p = params_deg(case, arrays)
         counter, stats = pb.degree_counts(p, K=c["K"]) if c["K"] else pb.degree_counts(p)
         assert _sha(counter.counts) == c["sha256"], c
+
+
+def test_no_parallel_edges_high_degree_nodes_vs_oracle():
+    """Nodes above the hash-set threshold (degree > 64) run node_big_kernel:
+    uniform d = 300 and power-law degree sequences with hubs, with and
+    without no_self_loops, bit-exact (edges and probe totals) vs the oracle."""
+    seed = np.array([x for u in range(320) for v in range(u + 1, 320) for x in (u, v)], dtype=np.uint64)
+    s_t = tuple(int(x) for x in seed)
+    for nsl in (False, True):
+        p = pb.GenParams(n=2000, d=300, n0=320, seed_edges=seed, no_self_loops=nsl, no_parallel_edges=True)
+        op = O.OParams(n=2000, d=300, n0=320, seed_edges=s_t, no_self_loops=nsl, no_parallel_edges=True)
+        got, pr = pb.generate_block(p.m0, p.m, p)
+        want, wp = O.generate_block(op, op.m0, op.m)
+        assert np.array_equal(got, want) and pr == wp, ("uniform", nsl)
+    rng = np.random.default_rng(3)
+    deg = np.sort(np.minimum(rng.zipf(2.0, size=20000) + 1, 700)).astype(np.uint64)  # hubs late
+    for nsl in (False, True):
+        p = pb.GenParams(n=320 + deg.size, n0=320, degrees=deg, seed_edges=seed, no_self_loops=nsl,
+                         no_parallel_edges=True)
+        op = O.OParams(n=p.n, d=None, n0=320, seed_edges=s_t, degrees=tuple(int(x) for x in deg),
+                       no_self_loops=nsl, no_parallel_edges=True)
+        got, pr = pb.generate_block(p.m0, p.m, p)
+        want, wp = O.generate_block(op, op.m0, op.m)
+        assert np.array_equal(got, want) and pr == wp, ("degrees", nsl)
+        t = got[:, 1]
+        for v in (p.n - 1, p.n - 2):  # the hubs: distinct targets
+            a, b = p.first_edge_of(v) - p.m0, p.first_edge_of(v) - p.m0 + p.degree_of(v)
+            assert len(set(t[a:b].tolist())) == b - a
