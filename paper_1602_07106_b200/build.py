@@ -10,14 +10,16 @@ import os
 import shutil
 import subprocess
 import sys
+import tempfile
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libparba_b200.so")
 ROOT = os.path.dirname(HERE)
 
-SOURCES = ["parba_api.cu"]
-DEPS = ["parba_api.cu", "parba_kernels.cuh", "parba_device.cuh", "parba_nodes.cuh"]
+SOURCES = ["parba_api.cu", "parba_nodes_api.cu", "parba_host.cu"]
+DEPS = ["parba_api.cu", "parba_nodes_api.cu", "parba_host.cu", "parba_common.h", "parba_kernels.cuh",
+        "parba_device.cuh", "parba_nodes.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -42,14 +44,26 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
     target = out or LIB
     if out is None and not force and not stale():
         return LIB
-    cmd = [_nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
-           "-shared", "-cudart", "static", "-o", target + ".tmp",
-           *[f"-D{k}={v}" for k, v in (defines or {}).items()],
-           *[os.path.join(CSRC, s) for s in SOURCES]]
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
+             *[f"-D{k}={v}" for k, v in (defines or {}).items()]]
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.run(cmd, check=True)
+        flags.insert(0, "-Xptxas=-v")
+    with tempfile.TemporaryDirectory() as tmp:
+        # one nvcc per translation unit, in parallel, then one link
+        objs, procs = [], []
+        for src in SOURCES:
+            obj = os.path.join(tmp, src.replace(".cu", ".o"))
+            cmd = [_nvcc(), *flags, "-c", "-o", obj, os.path.join(CSRC, src)]
+            if verbose:
+                print(" ".join(cmd), file=sys.stderr)
+            procs.append((cmd, subprocess.Popen(cmd)))
+            objs.append(obj)
+        codes = [(cmd, proc.wait()) for cmd, proc in procs]  # all finish before tmp goes away
+        for cmd, code in codes:
+            if code != 0:
+                raise subprocess.CalledProcessError(code, cmd)
+        subprocess.run([_nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", target + ".tmp", *objs],
+                       check=True)
     os.replace(target + ".tmp", target)
     return target
 

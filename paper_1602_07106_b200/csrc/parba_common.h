@@ -1,0 +1,86 @@
+// parba_common.h -- host-side internals shared by the C-ABI translation
+// units (parba_api.cu, parba_nodes_api.cu, parba_host.cu): error reporting,
+// parameter validation, DevParams construction, scratch helpers.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/parba_b200.h"
+#include "parba_device.cuh"
+
+namespace parba {
+namespace host {
+
+extern thread_local std::string g_err;
+int fail(int code, const char *fmt, ...);
+
+#define CUDA_TRY(expr)                                                                     \
+    do {                                                                                   \
+        cudaError_t e_ = (expr);                                                           \
+        if (e_ != cudaSuccess)                                                             \
+            return ::parba::host::fail(PARBA_ECUDA, "%s failed: %s", #expr, cudaGetErrorString(e_)); \
+    } while (0)
+
+constexpr uint64_t kMaxEdges = 1ull << 58;  // degreeseq.py:27 (MAX_EDGES)
+
+inline bool is_deg(const parba_params_t *p) { return p->degree_prefix != nullptr; }
+// First edge of node v of a uniform-degree family.
+inline uint64_t node_first_edge(const parba_params_t *p, uint64_t v) { return p->m0 + (v - p->n0) * p->d; }
+int validate(const parba_params_t *p);
+int check_range(const parba_params_t *p, uint64_t lo, uint64_t hi);
+DevParams make_dev(const parba_params_t *p, uint64_t K = 0);
+
+inline unsigned grid_for(uint64_t count, int threads) {
+    uint64_t g = (count + threads - 1) / threads;
+    if (g > 148ull * 32) g = 148ull * 32;
+    return (unsigned)(g ? g : 1);
+}
+
+// Stream-ordered scratch, freed on the same stream.
+struct AsyncBuf {
+    void *p = nullptr;
+    cudaStream_t st = nullptr;
+    ~AsyncBuf() {
+        if (p) cudaFreeAsync(p, st);
+    }
+    int alloc(size_t bytes, cudaStream_t s) {
+        st = s;
+        CUDA_TRY(cudaMallocAsync(&p, bytes ? bytes : 8, s));
+        return PARBA_OK;
+    }
+};
+struct DevBuf {
+    void *p = nullptr;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+};
+struct StreamGuard {
+    cudaStream_t s = nullptr;
+    ~StreamGuard() {
+        if (s) cudaStreamDestroy(s);
+    }
+};
+struct EventGuard {
+    cudaEvent_t e = nullptr;
+    ~EventGuard() {
+        if (e) cudaEventDestroy(e);
+    }
+};
+
+int read_u64s(const uint64_t *dptr, uint64_t *out, size_t n, cudaStream_t st);
+
+// Node-granular paths (parba_nodes_api.cu): option flags and degree sequences.
+int win_rlim_deg(const parba_params_t *p, DevParams &dp, uint64_t K, cudaStream_t st);
+int boundary_node(const parba_params_t *p, const DevParams &dp, uint64_t pos, uint64_t *v, cudaStream_t st);
+int generate_nodes(const parba_params_t *p, const DevParams &dp, uint64_t vlo, uint64_t vhi, uint64_t lo,
+                   uint64_t hi, uint64_t *out, unsigned long long *probes, cudaStream_t st);
+int count_nodes_u64(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi, uint64_t K,
+                    unsigned long long *counts, unsigned long long *probes, cudaStream_t st);
+int count_nodes_u32(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi, uint64_t K,
+                    uint32_t *counts, unsigned long long *probes, cudaStream_t st);
+
+}  // namespace host
+}  // namespace parba

@@ -22,6 +22,19 @@
 
 namespace parba {
 
+// Debug builds (-DPARBA_DEBUG_CHECKS=1, tools/check_build.sh) trap on a
+// violated invariant; release builds compile the checks away.
+#if defined(PARBA_DEBUG_CHECKS) && PARBA_DEBUG_CHECKS
+#define PARBA_CHECK(cond)                \
+    do {                                 \
+        if (!(cond)) __trap();           \
+    } while (0)
+#else
+#define PARBA_CHECK(cond) \
+    do {                  \
+    } while (0)
+#endif
+
 constexpr uint32_t kCrcPoly = 0x82F63B78u;  // hashing.py:40 (reflected 0x1EDC6F41)
 
 // Bit-serial CRC32-C of one LE 64-bit word (host + device); builds tables

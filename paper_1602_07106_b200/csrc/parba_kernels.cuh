@@ -70,18 +70,6 @@ constexpr int kWarps = PARBA_WARPS;        // warps per CTA
 #endif
 constexpr int kStageBufs = PARBA_NBUF;
 
-// Debug builds (-DPARBA_DEBUG_CHECKS=1, tools/check_build.sh) trap on a
-// violated invariant; release builds compile the checks away.
-#if defined(PARBA_DEBUG_CHECKS) && PARBA_DEBUG_CHECKS
-#define PARBA_CHECK(cond)                \
-    do {                                 \
-        if (!(cond)) __trap();           \
-    } while (0)
-#else
-#define PARBA_CHECK(cond) \
-    do {                  \
-    } while (0)
-#endif
 constexpr int kThreads = kWarps * 32;
 
 enum SinkKind { kStore = 0, kWindow = 1, kFull = 2 };

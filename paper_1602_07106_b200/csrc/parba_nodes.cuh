@@ -20,7 +20,6 @@
 #include <cuda_runtime.h>
 
 #include "parba_device.cuh"
-#include "parba_kernels.cuh"  // PARBA_CHECK
 
 namespace parba {
 
