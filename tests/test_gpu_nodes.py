@@ -363,3 +363,9 @@ def test_no_parallel_edges_high_degree_nodes_vs_oracle():
         for v in (p.n - 1, p.n - 2):  # the hubs: distinct targets
             a, b = p.first_edge_of(v) - p.m0, p.first_edge_of(v) - p.m0 + p.degree_of(v)
             assert len(set(t[a:b].tolist())) == b - a
+        # degree counts through the flag path's chunked generate + count
+        want_c = np.zeros(p.n, dtype=np.int64)
+        O.count_block(want_c, want)
+        O.count_block(want_c, seed)
+        counter, st = pb.degree_counts(p)
+        assert np.array_equal(counter.counts, want_c) and st.hash_probes == wp
