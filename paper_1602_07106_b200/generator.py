@@ -377,7 +377,10 @@ def generate_block(lo: int, hi: int, p: GenParams, resolution: Resolution = "ran
         return np.empty((0, 2), dtype=np.uint64), 0
     torch, dev = _device(device)
     total = hi - lo
-    out_host = torch.empty(2 * total, dtype=torch.int64, pin_memory=True)
+    try:  # pinned: the D2H copies run at full PCIe speed and overlap generation
+        out_host = torch.empty(2 * total, dtype=torch.int64, pin_memory=True)
+    except RuntimeError:  # pinning refused (host limits): pageable array, staged copies
+        out_host = torch.empty(2 * total, dtype=torch.int64)
     cuts = _cuts(p, lo, hi, min(total, HOST_CHUNK_EDGES))
     spans = list(zip(cuts, cuts[1:]))
     chunk = max(b - a for a, b in spans)
