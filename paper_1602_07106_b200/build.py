@@ -45,7 +45,8 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
     if out is None and not force and not stale():
         return LIB
     flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
-             *[f"-D{k}={v}" for k, v in (defines or {}).items()]]
+             *[f"-D{k}={v}" for k, v in (defines or {}).items()],
+             *os.environ.get("PARBA_NVCC_FLAGS", "").split()]  # experiments (tools/ab.py)
     if verbose:
         flags.insert(0, "-Xptxas=-v")
     with tempfile.TemporaryDirectory() as tmp:
