@@ -673,3 +673,16 @@ def test_wide_store_flush_with_seed_vs_oracle():
             got, pr = pb.generate_block(lo, hi, p)
             want, wp = O.generate_block(op, lo, hi)
             assert np.array_equal(got, want) and pr == wp, (n0, lo)
+
+
+def test_config5_ten_million_sampled_ids_vs_oracle():
+    """SURVEY 8d, configs[4] (n=1e10, d=100, m=1e12): 1e7 uniformly sampled
+    edge IDs through the device chain kernel vs the oracle's chains."""
+    p = pb.GenParams(n=10**10, d=100)
+    rng = np.random.default_rng(160207106)
+    ids = rng.integers(0, p.m, size=10**7, dtype=np.uint64)
+    e, probes = pb.edges_at(ids, p)
+    term, wp = O.resolve_chain_block(_op(p), np.uint64(2) * ids + np.uint64(1), 0)
+    assert np.array_equal(e[:, 0], ids // np.uint64(100))
+    assert np.array_equal(e[:, 1], (term >> np.uint64(1)) // np.uint64(100))
+    assert probes == wp
