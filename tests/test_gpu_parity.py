@@ -375,7 +375,7 @@ def test_degree_conservation_randomized():
 
 def test_config2_full_size_properties():
     """C2 (n=1e8, d=10, m=1e9; 16 GB in HBM): closed-form sources over the
-    whole array, target <= source, 2e5 sampled rows bit-exact vs the oracle,
+    whole array, target <= source, 1e6 sampled rows bit-exact vs the oracle,
     probe mean, and the device histogram of the stored targets equals the
     fused full-count kernel (a checksum of two independent kernels)."""
     import torch
@@ -391,7 +391,7 @@ def test_config2_full_size_properties():
         assert torch.equal(src, idx // p.d)
         assert bool((out[a:b, 1] <= src).all())
     rng = np.random.default_rng(160207106)
-    ids = np.unique(rng.integers(0, p.m, size=200_000, dtype=np.uint64))
+    ids = np.unique(rng.integers(0, p.m, size=10**6, dtype=np.uint64))  # 1e6 sampled IDs
     rows = out[torch.from_numpy(ids.view(np.int64)).to(out.device)].cpu().numpy().view(np.uint64)
     r0 = np.uint64(2) * ids + np.uint64(1)
     term, _ = O.resolve_chain_block(_op(p), r0, 0)
@@ -686,3 +686,22 @@ def test_config5_ten_million_sampled_ids_vs_oracle():
     assert np.array_equal(e[:, 0], ids // np.uint64(100))
     assert np.array_equal(e[:, 1], (term >> np.uint64(1)) // np.uint64(100))
     assert probes == wp
+
+
+def test_config3_window_subranges_1e8_vs_oracle():
+    """SURVEY 8d, configs[2] (n=1e9, d=100, K=1e5): window counts of the
+    1e8-edge subranges [0, 1e8) (every source hit) and [m - 1e8, m) vs the
+    threaded oracle."""
+    import os
+
+    import torch
+
+    p = pb.GenParams(n=10**9, d=100)
+    K = 10**5
+    threads = max(1, len(os.sched_getaffinity(0)))
+    for lo in (0, p.m - 10**8):
+        hi = lo + 10**8
+        c, prb = pb.parallel.count_shard_device(p, K, lo, hi)
+        torch.cuda.synchronize()
+        want, wp = O.run_threaded(_op(p), lo, hi, O.MODE_WINDOW, K=K, threads=threads, batch=1 << 20)
+        assert np.array_equal(c.cpu().numpy()[:K], want) and int(prb.item()) == wp, lo
