@@ -269,6 +269,18 @@ int launch_sources(const DevParams &dp, uint64_t lo, uint64_t hi, uint64_t K, Co
 
 }  // namespace
 
+namespace parba {
+namespace host {
+// The plain store path for [lo, hi) (used by the node path: attempt 0 of
+// no_parallel_edges is exactly the plain edge).
+int launch_store(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi, uint64_t *out,
+                 unsigned long long *probes, cudaStream_t st) {
+    SinkArgs a{out, nullptr, nullptr};
+    return launch_tiles<kStore>(p, dp, lo, hi, a, probes, st);
+}
+}  // namespace host
+}  // namespace parba
+
 extern "C" {
 
 int parba_version(void) { return 20000; }

@@ -72,6 +72,9 @@ struct EventGuard {
 
 int read_u64s(const uint64_t *dptr, uint64_t *out, size_t n, cudaStream_t st);
 
+int launch_store(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi, uint64_t *out,
+                 unsigned long long *probes, cudaStream_t st);
+
 // Node-granular paths (parba_nodes_api.cu): option flags and degree sequences.
 int win_rlim_deg(const parba_params_t *p, DevParams &dp, uint64_t K, cudaStream_t st);
 int boundary_node(const parba_params_t *p, const DevParams &dp, uint64_t pos, uint64_t *v, cudaStream_t st);

@@ -161,6 +161,7 @@ constexpr uint64_t kBigDegree = 256;  // no_parallel_edges: larger nodes use a h
 
 struct NodeArgs {
     uint32_t no_self_loops, no_parallel_edges;
+    uint32_t pre0;          // no_parallel_edges without no_self_loops: out already holds attempt 0
     uint64_t max_attempts;  // 0: 64 * degree (generator.py:205)
     uint32_t base_seed0, base_seed1;  // attempt a >= 1: salt a on the unsalted seeds
     uint64_t base_mult;
@@ -243,7 +244,9 @@ __device__ __forceinline__ bool node_npe(uint64_t v, uint64_t first, uint64_t dv
         uint64_t t = 0, a = a0;
         bool fresh = false;
         for (; a < cap; ++a) {
-            if (nsl && a < n_memo) {
+            if (na.pre0 && a == 0) {
+                t = out[i - lo].y;  // attempt 0 = the plain edge, already generated (and its probes counted)
+            } else if (nsl && a < n_memo) {
                 t = memo_t[a];
                 pr_acc = memo_c[a];
             } else {
@@ -318,7 +321,7 @@ __device__ __forceinline__ void node_span(uint64_t v, const DevParams &p, uint64
 template <bool DEG>
 __global__ void __launch_bounds__(256)
 node_kernel(DevParams p, NodeArgs na, uint64_t vlo, uint64_t vhi, uint64_t lo, uint64_t n_out, ulonglong2 *out,
-            unsigned long long *probes_out, unsigned long long *fail_edge, uint64_t big_deg) {
+            unsigned long long *probes_out, unsigned long long *fail_edge, uint64_t big_deg, const uint8_t *need) {
     PARBA_NODE_PROLOGUE;
     uint64_t memo_t[kMemo], memo_c[kMemo];
     for (uint64_t v = vlo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < vhi;
@@ -337,7 +340,7 @@ node_kernel(DevParams p, NodeArgs na, uint64_t vlo, uint64_t vhi, uint64_t lo, u
             for (uint64_t i = first; i < first + dv; ++i) out[i - lo] = make_ulonglong2(v, t);
             continue;
         }
-        if (dv > big_deg) continue;
+        if (dv > big_deg || (need && !need[v - vlo])) continue;
         node_npe<DEG>(v, first, dv, lo, out, nullptr, 0, memo_t, memo_c, kMemo, fams, tab, simple, p, na,
                       probes, fail_edge);
     }
@@ -371,6 +374,31 @@ node_big_kernel(DevParams p, NodeArgs na, const uint64_t *nodes, uint64_t vlo, u
                       na, probes, fail_edge);
     }
     node_probes_flush(probes, probes_out);
+}
+
+// no_parallel_edges without no_self_loops, after the plain pass: a node
+// whose attempt-0 targets are pairwise distinct is final (the sequential
+// rule accepts every attempt 0).  need[v - vlo] = 1 marks the nodes the node
+// kernels must re-run: a repeated target among <= 16 edges, or more edges.
+template <bool DEG>
+__global__ void npe_dup_kernel(DevParams p, uint64_t vlo, uint64_t vhi, uint64_t lo, const ulonglong2 *out,
+                               uint8_t *need) {
+    for (uint64_t v = vlo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < vhi;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t first, dv;
+        node_span<DEG>(v, p, first, dv);
+        uint8_t f = dv > 16 ? 1 : 0;
+        if (!f && dv >= 2) {
+            uint64_t t[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) t[k] = (uint64_t)k < dv ? out[first - lo + k].y : ~(uint64_t)k;
+#pragma unroll
+            for (int a = 1; a < 16; ++a)
+#pragma unroll
+                for (int b = 0; b < a; ++b) f |= t[a] == t[b] ? 1 : 0;
+        }
+        need[v - vlo] = f;
+    }
 }
 
 // Scratch words of a big node: its set (power of two >= 2 * degree) + memo.

@@ -157,17 +157,36 @@ int generate_nodes(const parba_params_t *p, const DevParams &dp, uint64_t vlo, u
     na.base_seed1 = p->base_seed1;
     na.base_mult = p->base_mult;
     na.simple = p->hash_kind == PARBA_HASH_SIMPLE ? 1u : 0u;
-    AsyncBuf fe;
+    // no_parallel_edges alone: attempt 0 of every edge is the plain edge, so
+    // the tile kernel generates them all first (full speed, probes counted)
+    // and the node kernels only re-run the edges whose target repeats
+    na.pre0 = (na.no_parallel_edges && !na.no_self_loops) ? 1u : 0u;
+    if (na.pre0) {
+        int rc0 = launch_store(p, dp, lo, hi, out, probes, st);
+        if (rc0) return rc0;
+    }
+    AsyncBuf fe, need;
     int rc = fe.alloc(sizeof(unsigned long long), st);
     if (rc) return rc;
     CUDA_TRY(cudaMemsetAsync(fe.p, 0xFF, sizeof(unsigned long long), st));
     const unsigned grid = grid_for(vhi - vlo, 256);
+    if (na.pre0) {  // nodes whose attempt-0 targets are already distinct are final
+        if ((rc = need.alloc(vhi - vlo, st))) return rc;
+        if (is_deg(p))
+            npe_dup_kernel<true><<<grid, 256, 0, st>>>(dp, vlo, vhi, lo, (const ulonglong2 *)out, (uint8_t *)need.p);
+        else
+            npe_dup_kernel<false><<<grid, 256, 0, st>>>(dp, vlo, vhi, lo, (const ulonglong2 *)out, (uint8_t *)need.p);
+        CUDA_TRY(cudaGetLastError());
+    }
     const uint64_t big = na.no_parallel_edges ? kBigDegree : UINT64_MAX;
     unsigned long long *fep = (unsigned long long *)fe.p;
+    const uint8_t *needp = (const uint8_t *)need.p;
     if (is_deg(p))
-        node_kernel<true><<<grid, 256, 0, st>>>(dp, na, vlo, vhi, lo, hi - lo, (ulonglong2 *)out, probes, fep, big);
+        node_kernel<true><<<grid, 256, 0, st>>>(dp, na, vlo, vhi, lo, hi - lo, (ulonglong2 *)out, probes, fep, big,
+                                                needp);
     else
-        node_kernel<false><<<grid, 256, 0, st>>>(dp, na, vlo, vhi, lo, hi - lo, (ulonglong2 *)out, probes, fep, big);
+        node_kernel<false><<<grid, 256, 0, st>>>(dp, na, vlo, vhi, lo, hi - lo, (ulonglong2 *)out, probes, fep, big,
+                                                 needp);
     CUDA_TRY(cudaGetLastError());
     if (na.no_parallel_edges) {
         rc = generate_big_nodes(p, dp, na, vlo, vhi, lo, hi, out, probes, fep, st);
