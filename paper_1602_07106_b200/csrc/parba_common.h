@@ -38,6 +38,22 @@ inline unsigned grid_for(uint64_t count, int threads) {
     return (unsigned)(g ? g : 1);
 }
 
+// Keep memory freed by cudaFreeAsync in the device's default pool instead of
+// returning it to the driver at every synchronisation (the node paths
+// allocate and free GB-sized scratch per call; re-mapping it cost more than
+// the kernels).  Idempotent, once per device.
+inline void retain_async_pool() {
+    static bool done[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    done[dev] = true;
+}
+
 // Stream-ordered scratch, freed on the same stream.
 struct AsyncBuf {
     void *p = nullptr;
@@ -47,6 +63,7 @@ struct AsyncBuf {
     }
     int alloc(size_t bytes, cudaStream_t s) {
         st = s;
+        retain_async_pool();
         CUDA_TRY(cudaMallocAsync(&p, bytes ? bytes : 8, s));
         return PARBA_OK;
     }

@@ -144,6 +144,32 @@ int generate_big_nodes(const parba_params_t *p, const DevParams &dp, const NodeA
     return PARBA_OK;
 }
 
+// PARBA_EINFEASIBLE with the reference's message when a node kernel
+// recorded a failing edge (InfeasibleTargetsError, generator.py:209-213).
+int report_infeasible(const parba_params_t *p, const DevParams &dp, const uint64_t *fail_edge, cudaStream_t st) {
+    int rc;
+    uint64_t edge;
+    rc = read_u64s(fail_edge, &edge, 1, st);
+    if (rc) return rc;
+    if (edge == UINT64_MAX) return PARBA_OK;
+    uint64_t v, deg;
+    if (is_deg(p)) {
+        uint64_t span[3];
+        rc = owner_span(dp, edge, span, st);
+        if (rc) return rc;
+        v = span[0];
+        deg = span[2] - span[1];
+    } else {
+        v = p->n0 + (edge - p->m0) / p->d;
+        deg = p->d;
+    }
+    const uint64_t cap = p->max_attempts ? p->max_attempts : 64 * deg;
+    return fail(PARBA_EINFEASIBLE,
+                "edge %llu of node %llu: no fresh target in %llu attempts "
+                "(distinct-target pool may be smaller than the degree)",
+                (unsigned long long)edge, (unsigned long long)v, (unsigned long long)cap);
+}
+
 // Edges of nodes [vlo, vhi) (first edge lo) into out, honouring the flags;
 // synchronises st to report an infeasible node (InfeasibleTargetsError).
 int generate_nodes(const parba_params_t *p, const DevParams &dp, uint64_t vlo, uint64_t vhi, uint64_t lo,
@@ -192,26 +218,7 @@ int generate_nodes(const parba_params_t *p, const DevParams &dp, uint64_t vlo, u
         rc = generate_big_nodes(p, dp, na, vlo, vhi, lo, hi, out, probes, fep, st);
         if (rc) return rc;
     }
-    uint64_t edge;
-    rc = read_u64s((const uint64_t *)fe.p, &edge, 1, st);
-    if (rc) return rc;
-    if (edge == UINT64_MAX) return PARBA_OK;
-    uint64_t v, deg;
-    if (is_deg(p)) {
-        uint64_t span[3];
-        rc = owner_span(dp, edge, span, st);
-        if (rc) return rc;
-        v = span[0];
-        deg = span[2] - span[1];
-    } else {
-        v = p->n0 + (edge - p->m0) / p->d;
-        deg = p->d;
-    }
-    const uint64_t cap = p->max_attempts ? p->max_attempts : 64 * deg;
-    return fail(PARBA_EINFEASIBLE,
-                "edge %llu of node %llu: no fresh target in %llu attempts "
-                "(distinct-target pool may be smaller than the degree)",
-                (unsigned long long)edge, (unsigned long long)v, (unsigned long long)cap);
+    return report_infeasible(p, dp, (const uint64_t *)fe.p, st);
 }
 
 // Degree counts of [lo, hi) with option flags: node-aligned chunks generated
