@@ -15,6 +15,9 @@
 #include "../../include/parba_b200.h"
 #include "parba_common.h"
 #include "parba_kernels.cuh"
+#include "parba_hist.cuh"
+
+#include <cub/device/device_scan.cuh>
 
 using namespace parba;
 using namespace parba::host;
@@ -132,7 +135,7 @@ int nc_for(uint64_t two_hi) {
 struct DevInfo {
     int sms = 0;
     int smem_optin = 0;  // max dynamic shared memory per block
-    bool attr_done[12][3][2] = {};  // [hash variant][sink][seed]
+    bool attr_done[12][4][2] = {};  // [hash variant][sink][seed]
 };
 std::mutex g_mu;
 std::vector<DevInfo> g_dev;
@@ -187,6 +190,13 @@ int launch_tiles_t(const DevParams &dp, uint64_t lo, uint64_t hi, const SinkArgs
         if (grid > need) grid = need;
         SinkArgs ac = a;
         if (SINK == kStore) ac.out = a.out + 2 * (a0 - lo);
+        if (SINK == kTargets) {  // one launch; every warp owns capw slots
+            if (a1 != hi) return fail(PARBA_ECUDA, "targets pass needs one launch");
+            const uint64_t nw = grid * warps;
+            ac.capw = (ntiles + nw - 1) / nw * kTile;
+            if (nw * ac.capw > a.t32_cap) return fail(PARBA_ECUDA, "targets scratch too small");
+            *a.t32_len = nw * ac.capw;
+        }
         kern<<<(unsigned)grid, warps * 32, smem, st>>>(dp, a0, a1, tile0, ntiles, ac, probes);
         CUDA_TRY(cudaGetLastError());
         a0 = a1;
@@ -403,6 +413,96 @@ int parba_degree_window(const parba_params_t *p, uint64_t lo, uint64_t hi, uint6
     return launch_sources<unsigned long long>(dp, lo, hi, K, counts, st);
 }
 
+}  // extern "C"
+
+namespace {
+
+// Partitioned full histogram (parba_hist.cuh) over batches of at most
+// kHistBatch edges.  Applies when every target fits u32 and a bucket spans
+// at most 8 slices (n <= 1024 * 2^18); the source endpoints stay closed-form.
+constexpr uint64_t kHistBatch = 1ull << 29;
+constexpr uint64_t kHistMinEdges = 1ull << 22;
+
+int hist_shift(uint64_t n) {
+    int shift = kSliceLg;
+    while (((n + (1ull << shift) - 1) >> shift) > (uint64_t)kHistBuckets) ++shift;
+    return shift;
+}
+
+bool use_partitioned(const parba_params_t *p, uint64_t lo, uint64_t hi) {
+    const char *e = getenv("PARBA_FULL_MODE");  // "direct" / "partition" (tests, A/B)
+    const int mode = !e ? 0 : strcmp(e, "direct") == 0 ? 1 : strcmp(e, "partition") == 0 ? 2 : 0;
+    if (p->n >= kEmptyTarget) return false;
+    if (hist_shift(p->n) - kSliceLg > kMaxSliceLgPerBucket) return false;
+    if (mode) return mode == 2;
+    return hi - lo >= kHistMinEdges;
+}
+
+int full_partitioned(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi, uint32_t *counts,
+                     unsigned long long *probes, cudaStream_t st) {
+    DevInfo *di;
+    int rc = dev_info(&di);
+    if (rc) return rc;
+    const uint32_t n = (uint32_t)p->n;
+    const int shift = hist_shift(n);
+    const int nb = (int)((n + (1ull << shift) - 1) >> shift);
+    const int spb_lg = shift - kSliceLg;
+    const uint64_t batch = hi - lo < kHistBatch ? hi - lo : kHistBatch;
+    // a launch fills nw * ceil(ntiles / nw) * kTile slots, nw <= 64 warps per SM
+    const uint64_t cap = (batch / kTile + 2) * kTile + (uint64_t)di->sms * 64 * kTile;
+    const uint32_t nblk = (uint32_t)di->sms * 2;
+    AsyncBuf t32, srt, H, O, tmp;
+    if ((rc = t32.alloc(cap * 4, st)) || (rc = srt.alloc(cap * 4, st)) ||
+        (rc = H.alloc((size_t)nb * nblk * 4, st)) || (rc = O.alloc((size_t)nb * nblk * 4, st)))
+        return rc;
+    size_t tmp_bytes = 0;
+    CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, (const uint32_t *)H.p, (uint32_t *)O.p,
+                                           (int64_t)nb * nblk, st));
+    if ((rc = tmp.alloc(tmp_bytes, st))) return rc;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        static bool attr[64] = {};
+        int dev = 0;
+        CUDA_TRY(cudaGetDevice(&dev));
+        if (dev < 64 && !attr[dev]) {
+            CUDA_TRY(cudaFuncSetAttribute(slice_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          kSliceNodes * 4));
+            attr[dev] = true;
+        }
+    }
+    for (uint64_t b0 = lo; b0 < hi;) {
+        uint64_t b1 = hi - b0 > batch ? (b0 / kTile) * kTile + batch : hi;
+        if (b1 > hi) b1 = hi;
+        uint64_t len = 0;
+        SinkArgs a{};
+        a.t32 = (uint32_t *)t32.p;
+        a.t32_cap = cap;
+        a.t32_len = &len;
+        if ((rc = launch_tiles<kTargets>(p, dp, b0, b1, a, probes, st))) return rc;
+        const uint64_t span = ((len + nblk - 1) / nblk + kScatterTile - 1) / kScatterTile * kScatterTile;
+        const uint32_t used = (uint32_t)((len + span - 1) / span);
+        // H / O are laid out for `used` CTAs (bucket-major, stride used)
+        bucket_hist_kernel<<<used, kHistThreads, 0, st>>>((const uint32_t *)t32.p, len, span, n, shift, nb,
+                                                          (uint32_t *)H.p);
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, (const uint32_t *)H.p, (uint32_t *)O.p,
+                                               (int64_t)nb * used, st));
+        bucket_scatter_kernel<<<used, kHistThreads, 0, st>>>((const uint32_t *)t32.p, len, span, n, shift, nb,
+                                                             (const uint32_t *)O.p, (uint32_t *)srt.p);
+        CUDA_TRY(cudaGetLastError());
+        slice_count_kernel<<<(unsigned)nb << spb_lg, kHistThreads, kSliceNodes * 4, st>>>(
+            (const uint32_t *)srt.p, (const uint32_t *)O.p, (const uint32_t *)H.p, used, nb, n, shift, spb_lg,
+            counts);
+        CUDA_TRY(cudaGetLastError());
+        b0 = b1;
+    }
+    return PARBA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 int parba_degree_full(const parba_params_t *p, uint64_t lo, uint64_t hi, uint32_t *counts,
                       unsigned long long *probes, void *stream) {
     int rc = validate(p);
@@ -413,8 +513,12 @@ int parba_degree_full(const parba_params_t *p, uint64_t lo, uint64_t hi, uint32_
     cudaStream_t st = (cudaStream_t)stream;
     const DevParams dp = make_dev(p, p->n);
     if (p->flags) return count_nodes_u32(p, dp, lo, hi, p->n, counts, probes, st);
-    SinkArgs a{nullptr, nullptr, counts};
-    rc = launch_tiles<kFull>(p, dp, lo, hi, a, probes, st);
+    if (use_partitioned(p, lo, hi)) {
+        rc = full_partitioned(p, dp, lo, hi, counts, probes, st);
+    } else {
+        SinkArgs a{nullptr, nullptr, counts};
+        rc = launch_tiles<kFull>(p, dp, lo, hi, a, probes, st);
+    }
     if (rc) return rc;
     return launch_sources<uint32_t>(dp, lo, hi, p->n, counts, st);
 }

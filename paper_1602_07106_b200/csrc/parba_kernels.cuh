@@ -72,7 +72,10 @@ constexpr int kStageBufs = PARBA_NBUF;
 
 constexpr int kThreads = kWarps * 32;
 
-enum SinkKind { kStore = 0, kWindow = 1, kFull = 2 };
+// kTargets: the full histogram's first pass — each warp appends the u32
+// targets it finishes to its own region of a scratch buffer (order is
+// irrelevant to a histogram); parba_hist.cuh partitions and counts them.
+enum SinkKind { kStore = 0, kWindow = 1, kFull = 2, kTargets = 3 };
 
 #ifndef PARBA_WARP_TIMES
 #define PARBA_WARP_TIMES 0
@@ -87,6 +90,10 @@ struct SinkArgs {
     uint64_t *out;                         // store: 2*(hi-lo) u64, 16-byte aligned
     unsigned long long *win;               // window counts (K)
     uint32_t *full;                        // full counts (n)
+    uint32_t *t32;                         // targets: capw u32 slots per warp
+    uint64_t capw;
+    uint64_t t32_cap;                      // host side: slots of t32
+    uint64_t *t32_len;                     // host side: slots the launch fills
 };
 
 // Shared-memory layout of a tile CTA (dynamic smem, W warps):
@@ -249,6 +256,19 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
         }
     };
 
+    // targets sink: the warp's finished targets go to consecutive slots of its
+    // region (one ballot per step, so a warp's stores are contiguous)
+    [[maybe_unused]] uint32_t *wout = nullptr;
+    [[maybe_unused]] uint32_t wcur = 0;
+    if constexpr (SINK == kTargets) wout = a.t32 + gw * a.capw;
+    auto emit = [&](bool f, uint64_t rv) {
+        if constexpr (SINK == kTargets) {
+            const unsigned m = ballot_all(f);
+            if (f) wout[wcur + __popc(m & ltmask)] = (uint32_t)target_of<NARROW, SEED, false, DEG>(rv, p);
+            wcur += __popc(m);
+        }
+    };
+
     // One probe on every lane (idle lanes hash a harmless stale value and
     // discard it: no divergent branch around the probe); finished chains go
     // to the sink.
@@ -264,7 +284,9 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
             const uint32_t fin = act[q] & (cont ^ 1u);
             act[q] &= cont;
             r[q] = nr[q];
-            if (fin) {
+            if constexpr (SINK == kTargets) {
+                emit(fin != 0, (uint64_t)nr[q]);
+            } else if (fin) {
                 if constexpr (SINK == kStore) PARBA_CHECK(saddr[q] - stage_s < L::kStageB);
                 finish<NARROW, SEED, SINK, R, DEG>(saddr[q], (uint64_t)nr[q], p, a);
             }
@@ -345,7 +367,8 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
             [[maybe_unused]] const uint32_t cell = stage_s + (buf * kTile + j) * (uint32_t)sizeof(R);
             if constexpr (SINK == kStore)  // final unless pending
                 sts_t<R>(cell, r1);
-            if constexpr (SINK != kStore) if (valid && done) finish<NARROW, SEED, SINK, R, DEG>(0u, (uint64_t)r1, p, a);
+            if constexpr (SINK == kTargets) emit(valid && done, (uint64_t)r1);
+            else if constexpr (SINK != kStore) if (valid && done) finish<NARROW, SEED, SINK, R, DEG>(0u, (uint64_t)r1, p, a);
             const bool pend = valid && !done;
             const unsigned m = ballot_all(pend);
             const uint32_t cur = tailb + (__popc(m & ltmask) << L::kLgEB);
@@ -436,6 +459,10 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
         step();
     }
     while (any_act()) step();
+    if constexpr (SINK == kTargets) {  // unused slots of the region: empty
+        PARBA_CHECK(wcur <= a.capw);
+        for (uint64_t j = wcur + lane; j < a.capw; j += 32) wout[j] = 0xffffffffu;
+    }
     if constexpr (SINK == kStore) {
         if constexpr (kStageBufs == 2) {
             if (have_prev) flush(buf ^ 1u, prev_base);

@@ -13,6 +13,7 @@ import numpy as np
 import pytest
 
 import oracle as O
+from paper_1602_07106_b200.hashing import HashConfig, HashKind
 from conftest import GOLDEN_CRC_N10_D2, GOLDEN_SIMPLE_N10_D2, RING10, TRIANGLE
 
 pytestmark = pytest.mark.gpu
@@ -302,6 +303,64 @@ def test_full_histogram_n1e6_d16_vs_oracle():
     assert np.array_equal(counter.counts, want) and stats.hash_probes == wp
     h = pb.Histogram.from_degree_counts(counter)
     assert 2.6 <= pb.fit_exponent(h, xmin=16) <= 3.4
+
+
+def _full_counts(p, lo, hi, mode, monkeypatch):
+    import torch
+
+    monkeypatch.setenv("PARBA_FULL_MODE", mode)
+    counts, probes = pb.parallel.count_shard_device(p, p.n, lo, hi)
+    torch.cuda.synchronize()
+    return counts.cpu().numpy(), int(probes.item())
+
+
+_RAGGED_DEG = np.random.default_rng(7).integers(1, 40, size=200_000)
+
+
+@pytest.mark.parametrize(
+    "case",
+    [
+        ("n1e6_ragged", dict(n=10**6, d=16), 12345, -777),
+        ("tiny_one_bucket", dict(n=1000, d=3), 0, 0),
+        ("seeded", dict(n=300_000, d=5, n0=3, seed_edges=TRIANGLE), 3, 0),
+        ("nb1024_exact", dict(n=1 << 25, d=2), (1 << 25) - (1 << 22) - 5, 0),
+        ("eight_slices", dict(n=2 * 10**8, d=2), 2 * (2 * 10**8) - (1 << 23) - 99, 0),
+        ("simple_hash", dict(n=500_000, d=4, hash=HashConfig(kind=HashKind.SIMPLE, seed0=5)), 0, 0),
+        ("degree_sequence", dict(n=3 + _RAGGED_DEG.size, n0=3, degrees=_RAGGED_DEG, seed_edges=TRIANGLE), 3, 0),
+    ],
+    ids=lambda c: c[0],
+)
+def test_full_partitioned_equals_direct(case, monkeypatch):
+    """The partitioned full histogram (targets -> bucket sort -> shared-memory
+    slices, parba_hist.cuh) equals the direct-atomic kernel element-wise,
+    probes included, on ragged ranges, seeds, degree sequences, a single
+    bucket, exactly 1024 buckets and 8 slices per bucket."""
+    _, kw, lo, hi = case
+    p = pb.GenParams(**kw)
+    hi = p.m + hi if hi <= 0 else hi
+    part, pp = _full_counts(p, lo, hi, "partition", monkeypatch)
+    direct, pd = _full_counts(p, lo, hi, "direct", monkeypatch)
+    assert pp == pd
+    assert np.array_equal(part, direct)
+    assert int(part.astype(np.int64).sum()) == 2 * (hi - lo)
+
+
+def test_full_partitioned_vs_oracle_small(monkeypatch):
+    # forced partition at desk scale, element-wise against the oracle
+    p = pb.GenParams(n=20_000, d=7)
+    got, probes = _full_counts(p, 0, p.m, "partition", monkeypatch)
+    blk, wp = O.generate_block(_op(p), 0, p.m)
+    want = np.bincount(blk.astype(np.int64).ravel(), minlength=p.n)
+    assert np.array_equal(got.astype(np.int64), want) and probes == wp
+
+
+def test_full_partition_too_large_falls_back(monkeypatch):
+    # n > 1024 * 2^18: a bucket would span 16 slices -> direct atomics
+    p = pb.GenParams(n=3 * 10**8, d=2)
+    lo = p.m - (1 << 22)
+    part, pp = _full_counts(p, lo, p.m, "partition", monkeypatch)
+    direct, pd = _full_counts(p, lo, p.m, "direct", monkeypatch)
+    assert pp == pd and np.array_equal(part, direct)
 
 
 def test_window_large_range_sharding_independent():
