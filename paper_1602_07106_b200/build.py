@@ -18,8 +18,7 @@ LIB = os.path.join(HERE, "libparba_b200.so")
 ROOT = os.path.dirname(HERE)
 
 SOURCES = ["parba_api.cu", "parba_nodes_api.cu", "parba_host.cu"]
-DEPS = ["parba_api.cu", "parba_nodes_api.cu", "parba_host.cu", "parba_common.h", "parba_kernels.cuh",
-        "parba_device.cuh", "parba_nodes.cuh"]
+DEPS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cu", ".cuh", ".h")))
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

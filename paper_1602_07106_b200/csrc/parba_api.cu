@@ -196,6 +196,8 @@ int launch_tiles_t(const DevParams &dp, uint64_t lo, uint64_t hi, const SinkArgs
             ac.capw = (ntiles + nw - 1) / nw * kTile;
             if (nw * ac.capw > a.t32_cap) return fail(PARBA_ECUDA, "targets scratch too small");
             *a.t32_len = nw * ac.capw;
+            *a.t32_span = (uint64_t)warps * ac.capw;
+            *a.t32_ctas = (uint32_t)grid;
         }
         kern<<<(unsigned)grid, warps * 32, smem, st>>>(dp, a0, a1, tile0, ntiles, ac, probes);
         CUDA_TRY(cudaGetLastError());
@@ -450,11 +452,14 @@ int full_partitioned(const parba_params_t *p, const DevParams &dp, uint64_t lo, 
     const uint64_t batch = hi - lo < kHistBatch ? hi - lo : kHistBatch;
     // a launch fills nw * ceil(ntiles / nw) * kTile slots, nw <= 64 warps per SM
     const uint64_t cap = (batch / kTile + 2) * kTile + (uint64_t)di->sms * 64 * kTile;
-    const uint32_t nblk = (uint32_t)di->sms * 2;
-    AsyncBuf t32, srt, H, O, tmp;
+    const uint32_t nblk = (uint32_t)di->sms * 4;  // >= CTAs of one tile launch
+    const uint64_t max_items = nb + cap / kCountChunk + 1;
+    AsyncBuf t32, srt, H, O, tmp, items;
     if ((rc = t32.alloc(cap * 4, st)) || (rc = srt.alloc(cap * 4, st)) ||
-        (rc = H.alloc((size_t)nb * nblk * 4, st)) || (rc = O.alloc((size_t)nb * nblk * 4, st)))
+        (rc = H.alloc((size_t)nb * nblk * 4, st)) || (rc = O.alloc((size_t)nb * nblk * 4, st)) ||
+        (rc = items.alloc((max_items + 1) * 4, st)))
         return rc;
+    uint32_t *n_items = (uint32_t *)items.p + max_items;
     size_t tmp_bytes = 0;
     CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, (const uint32_t *)H.p, (uint32_t *)O.p,
                                            (int64_t)nb * nblk, st));
@@ -467,32 +472,40 @@ int full_partitioned(const parba_params_t *p, const DevParams &dp, uint64_t lo, 
         if (dev < 64 && !attr[dev]) {
             CUDA_TRY(cudaFuncSetAttribute(slice_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           kSliceNodes * 4));
+            CUDA_TRY(cudaFuncSetAttribute(bucket_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          kScatterTile * 4));
             attr[dev] = true;
         }
     }
     for (uint64_t b0 = lo; b0 < hi;) {
         uint64_t b1 = hi - b0 > batch ? (b0 / kTile) * kTile + batch : hi;
         if (b1 > hi) b1 = hi;
-        uint64_t len = 0;
+        uint64_t len = 0, span = 0;
+        uint32_t used = 0;
         SinkArgs a{};
         a.t32 = (uint32_t *)t32.p;
+        a.hist = (uint32_t *)H.p;  // the tile launch writes the bucket histogram of each CTA's region
+        a.shift = shift;
+        a.nb = nb;
         a.t32_cap = cap;
         a.t32_len = &len;
+        a.t32_span = &span;
+        a.t32_ctas = &used;
         if ((rc = launch_tiles<kTargets>(p, dp, b0, b1, a, probes, st))) return rc;
-        const uint64_t span = ((len + nblk - 1) / nblk + kScatterTile - 1) / kScatterTile * kScatterTile;
-        const uint32_t used = (uint32_t)((len + span - 1) / span);
-        // H / O are laid out for `used` CTAs (bucket-major, stride used)
-        bucket_hist_kernel<<<used, kHistThreads, 0, st>>>((const uint32_t *)t32.p, len, span, n, shift, nb,
-                                                          (uint32_t *)H.p);
-        CUDA_TRY(cudaGetLastError());
+        if (used > nblk) return fail(PARBA_ECUDA, "targets launch wider than the histogram");
+        // H / O: bucket-major, stride `used` (the tile CTAs; CTA c's region is [c * span, (c + 1) * span))
         CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, (const uint32_t *)H.p, (uint32_t *)O.p,
                                                (int64_t)nb * used, st));
-        bucket_scatter_kernel<<<used, kHistThreads, 0, st>>>((const uint32_t *)t32.p, len, span, n, shift, nb,
+        bucket_scatter_kernel<<<used, kHistThreads, kScatterTile * 4, st>>>((const uint32_t *)t32.p, len, span, n, shift, nb,
                                                              (const uint32_t *)O.p, (uint32_t *)srt.p);
         CUDA_TRY(cudaGetLastError());
-        slice_count_kernel<<<(unsigned)nb << spb_lg, kHistThreads, kSliceNodes * 4, st>>>(
-            (const uint32_t *)srt.p, (const uint32_t *)O.p, (const uint32_t *)H.p, used, nb, n, shift, spb_lg,
-            counts);
+        count_plan_kernel<<<1, kHistThreads, 0, st>>>((const uint32_t *)O.p, (const uint32_t *)H.p, used, nb,
+                                                       (uint32_t *)items.p, n_items);
+        CUDA_TRY(cudaGetLastError());
+        const uint64_t items_ub = nb + len / kCountChunk + 1;  // >= sum of ceil(size_b / chunk)
+        slice_count_kernel<<<(unsigned)(items_ub << spb_lg), kHistThreads, kSliceNodes * 4, st>>>(
+            (const uint32_t *)srt.p, (const uint32_t *)O.p, (const uint32_t *)H.p, used, nb,
+            (const uint32_t *)items.p, n_items, n, shift, spb_lg, counts);
         CUDA_TRY(cudaGetLastError());
         b0 = b1;
     }

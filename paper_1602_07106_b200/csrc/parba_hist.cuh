@@ -5,30 +5,32 @@
 // atomic rate (~4.3e10/s on B200) no matter where the array lives.  The
 // partitioned pass replaces it with shared-memory atomics:
 //   1. tile_kernel<kTargets> appends every finished target (u32) to its
-//      warp's region of a scratch buffer (UINT32_MAX = empty slot);
-//   2. bucket_hist_kernel: per-CTA histogram of bucket = target >> shift
-//      (nb <= kHistBuckets buckets), written bucket-major so one exclusive
-//      scan gives every (bucket, CTA) its output offset;
-//   3. bucket_scatter_kernel: each CTA re-reads its span in sub-tiles,
-//      sorts a sub-tile by bucket in shared memory and writes the bucket
-//      runs contiguously (no global atomics);
-//   4. slice_count_kernel: one CTA per (bucket, 2^15-node slice) counts its
-//      bucket's entries of that slice in shared memory and adds them to the
-//      counts it owns exclusively (plain coalesced read-modify-write).
-// HBM traffic per target: 4 B written + 3 x 4 B read + 4 B written; the
-// bucket reads of step 4 repeat once per slice of the bucket (<= 8) and are
-// served by L2 because a bucket's slices run side by side.
+//      warp's region of a scratch buffer (UINT32_MAX = empty slot) and keeps
+//      a per-CTA histogram of bucket = target >> shift (nb <= kHistBuckets),
+//      written bucket-major so one exclusive scan gives every (bucket, CTA)
+//      its output offset;
+//   2. bucket_scatter_kernel: one CTA per tile CTA re-reads that CTA's
+//      region in sub-tiles, sorts a sub-tile by bucket in shared memory and
+//      writes the bucket runs contiguously (no global atomics);
+//   3. slice_count_kernel: one CTA per (bucket chunk, 2^15-node slice)
+//      counts the chunk's entries of that slice in shared memory and adds
+//      them to counts (plain read-modify-write when it owns the bucket).
+// HBM traffic per target: 4 B written, 4 B read + 4 B written by the
+// scatter, 4 B read by the count; the count's reads repeat once per slice of
+// a bucket (<= 8) and are served by L2 because those CTAs run side by side.
 #pragma once
 #include <cstdint>
 
 namespace parba {
 
-constexpr int kHistBuckets = 1024;          // level-1 buckets (max)
 constexpr int kSliceLg = 15;                // level-2 slice: 2^15 counters
 constexpr int kSliceNodes = 1 << kSliceLg;  // 128 KB of u32 in shared memory
 constexpr int kMaxSliceLgPerBucket = 3;     // <= 8 slices per bucket
 constexpr int kHistThreads = 1024;
-constexpr int kScatterTile = 8192;          // entries per sorted sub-tile
+#ifndef PARBA_SCATTER_TILE
+#define PARBA_SCATTER_TILE 16384
+#endif
+constexpr int kScatterTile = PARBA_SCATTER_TILE;  // entries per sorted sub-tile (dynamic smem)
 constexpr int kScatterPer = kScatterTile / kHistThreads;
 constexpr uint32_t kEmptyTarget = 0xffffffffu;
 
@@ -38,29 +40,6 @@ __device__ __forceinline__ uint4 ld_stream4(const uint4 *p) {
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                  : "l"(p));
     return v;
-}
-
-// Step 2: H[b * gridDim.x + blk] = entries of CTA blk's span in bucket b.
-// len and span are multiples of 4; t is 16-byte aligned.
-__global__ void __launch_bounds__(kHistThreads) bucket_hist_kernel(const uint32_t *__restrict__ t, uint64_t len,
-                                                                   uint64_t span, uint32_t n, int shift, int nb,
-                                                                   uint32_t *__restrict__ H) {
-    __shared__ uint32_t h[kHistBuckets];
-    for (int b = threadIdx.x; b < nb; b += blockDim.x) h[b] = 0;
-    __syncthreads();
-    const uint64_t s0 = (uint64_t)blockIdx.x * span;
-    const uint64_t s1 = s0 + span < len ? s0 + span : len;
-    const uint4 *t4 = reinterpret_cast<const uint4 *>(t + s0);
-    const uint64_t n4 = s1 > s0 ? (s1 - s0) / 4 : 0;
-    for (uint64_t k = threadIdx.x; k < n4; k += blockDim.x) {
-        const uint4 v = __ldg(t4 + k);  // kept in L2 for the scatter re-read
-        if (v.x < n) atomicAdd(&h[v.x >> shift], 1u);
-        if (v.y < n) atomicAdd(&h[v.y >> shift], 1u);
-        if (v.z < n) atomicAdd(&h[v.z >> shift], 1u);
-        if (v.w < n) atomicAdd(&h[v.w >> shift], 1u);
-    }
-    __syncthreads();
-    for (int b = threadIdx.x; b < nb; b += blockDim.x) H[(uint64_t)b * gridDim.x + blockIdx.x] = h[b];
 }
 
 // Block-wide exclusive scan of x (one value per thread, kHistThreads threads).
@@ -87,7 +66,7 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t x, uint32_t *w
     return inc - x + (w > 0 ? warp_sums[w - 1] : 0u);
 }
 
-// Step 3: O = exclusive scan of H (bucket-major).  CTA blk writes its
+// Step 2: O = exclusive scan of H (bucket-major).  CTA blk writes its
 // bucket-b entries to out[O[b * gridDim.x + blk] ...] in sub-tile order.
 __global__ void __launch_bounds__(kHistThreads) bucket_scatter_kernel(const uint32_t *__restrict__ t, uint64_t len,
                                                                       uint64_t span, uint32_t n, int shift, int nb,
@@ -96,28 +75,37 @@ __global__ void __launch_bounds__(kHistThreads) bucket_scatter_kernel(const uint
     __shared__ uint32_t cur[kHistBuckets];    // next output position per bucket
     __shared__ uint32_t cnt[kHistBuckets];    // sub-tile entries per bucket
     __shared__ uint32_t start[kHistBuckets];  // sub-tile run start per bucket
-    __shared__ uint32_t sorted[kScatterTile];
+    extern __shared__ uint32_t sorted[];  // kScatterTile entries
     __shared__ uint32_t warp_sums[32];
     __shared__ uint32_t total_s;
     for (int b = threadIdx.x; b < kHistBuckets; b += blockDim.x)
         cur[b] = b < nb ? O[(uint64_t)b * gridDim.x + blockIdx.x] : 0u;
     const uint64_t s0 = (uint64_t)blockIdx.x * span;
     const uint64_t s1 = s0 + span < len ? s0 + span : len;
-    for (uint64_t base = s0; base < s1; base += kScatterTile) {
-        for (int b = threadIdx.x; b < kHistBuckets; b += blockDim.x) cnt[b] = 0;
-        __syncthreads();
-        uint32_t v[kScatterPer], rk[kScatterPer];
-        // coalesced: thread i takes 16-byte words i and i + kHistThreads
+    // coalesced: thread i takes 16-byte words i and i + kHistThreads of a
+    // sub-tile; the next sub-tile's loads are issued before this one is sorted
+    uint4 nx[kScatterPer / 4];
+    auto load = [&](uint64_t base) {
 #pragma unroll
         for (int h = 0; h < kScatterPer / 4; ++h) {
             const uint64_t e = base + 4ull * (threadIdx.x + (uint64_t)h * kHistThreads);
-            uint4 w = make_uint4(kEmptyTarget, kEmptyTarget, kEmptyTarget, kEmptyTarget);
-            if (e < s1) w = ld_stream4(reinterpret_cast<const uint4 *>(t + e));
-            v[4 * h] = w.x;
-            v[4 * h + 1] = w.y;
-            v[4 * h + 2] = w.z;
-            v[4 * h + 3] = w.w;
+            nx[h] = make_uint4(kEmptyTarget, kEmptyTarget, kEmptyTarget, kEmptyTarget);
+            if (e < s1) nx[h] = ld_stream4(reinterpret_cast<const uint4 *>(t + e));
         }
+    };
+    load(s0);
+    for (uint64_t base = s0; base < s1; base += kScatterTile) {
+        for (int b = threadIdx.x; b < kHistBuckets; b += blockDim.x) cnt[b] = 0;
+        uint32_t v[kScatterPer], rk[kScatterPer];
+#pragma unroll
+        for (int h = 0; h < kScatterPer / 4; ++h) {
+            v[4 * h] = nx[h].x;
+            v[4 * h + 1] = nx[h].y;
+            v[4 * h + 2] = nx[h].z;
+            v[4 * h + 3] = nx[h].w;
+        }
+        load(base + kScatterTile);
+        __syncthreads();
 #pragma unroll
         for (int k = 0; k < kScatterPer; ++k)
             if (v[k] < n) rk[k] = atomicAdd(&cnt[v[k] >> shift], 1u);
@@ -142,33 +130,102 @@ __global__ void __launch_bounds__(kHistThreads) bucket_scatter_kernel(const uint
     }
 }
 
-// Step 4: CTA (b, s) counts bucket b's entries of slice s (nodes
-// (b << shift) + (s << kSliceLg) + [0, 2^kSliceLg)) and adds them to counts.
-// Bucket b's entries are sorted[O[b * nblk] .. O[(b + 1) * nblk]) (the last
-// bucket ends at O[last] + H[last]).
+// Step 3 plan: bucket sizes are skewed (node v draws ~ 1/sqrt(v) of the
+// targets, so the lowest bucket holds several percent of all entries).  A
+// bucket is cut into chunks of at most kCountChunk entries; items[] lists
+// (bucket, chunk) pairs (bucket | chunk << 10).  One CTA of kHistThreads.
+constexpr uint32_t kCountChunk = 1u << 21;
+
+__device__ __forceinline__ void bucket_range(const uint32_t *O, const uint32_t *H, uint32_t nblk, int nb, uint32_t b,
+                                             uint32_t &e0, uint32_t &e1) {
+    const uint64_t last = (uint64_t)nb * nblk - 1;
+    e0 = O[(uint64_t)b * nblk];
+    e1 = (int)b + 1 < nb ? O[(uint64_t)(b + 1) * nblk] : O[last] + H[last];
+}
+
+__global__ void __launch_bounds__(kHistThreads) count_plan_kernel(const uint32_t *__restrict__ O,
+                                                                  const uint32_t *__restrict__ H, uint32_t nblk,
+                                                                  int nb, uint32_t *__restrict__ items,
+                                                                  uint32_t *__restrict__ n_items) {
+    __shared__ uint32_t warp_sums[32];
+    const uint32_t b = threadIdx.x;
+    uint32_t chunks = 0;
+    if ((int)b < nb) {
+        uint32_t e0, e1;
+        bucket_range(O, H, nblk, nb, b, e0, e1);
+        chunks = e1 > e0 ? (e1 - e0 + kCountChunk - 1) / kCountChunk : 0u;
+    }
+    const uint32_t base = block_exclusive_scan(chunks, warp_sums);
+    for (uint32_t c = 0; c < chunks; ++c) items[base + c] = b | (c << 10);
+    if (threadIdx.x == kHistThreads - 1) *n_items = base + chunks;
+}
+
+// Step 3: CTA (item, s) counts the entries of one chunk of bucket b that fall
+// in slice s (nodes (b << shift) + (s << kSliceLg) + [0, 2^kSliceLg)) and
+// adds them to counts: plain read-modify-write when the chunk is the whole
+// bucket (the CTA owns those counters), atomics when the bucket is split.
+// The 2^spb_lg CTAs of an item are adjacent in the grid, so the chunk is
+// read from HBM about once and from L2 by the others.  (A cluster variant
+// that reads the chunk once and routes each entry to the owning CTA with a
+// distributed-shared-memory red.add measured 3x slower.)
 __global__ void __launch_bounds__(kHistThreads) slice_count_kernel(const uint32_t *__restrict__ sorted,
                                                                    const uint32_t *__restrict__ O,
                                                                    const uint32_t *__restrict__ H, uint32_t nblk,
-                                                                   int nb, uint32_t n, int shift, int spb_lg,
+                                                                   int nb, const uint32_t *__restrict__ items,
+                                                                   const uint32_t *__restrict__ n_items, uint32_t n,
+                                                                   int shift, int spb_lg,
                                                                    uint32_t *__restrict__ counts) {
     extern __shared__ uint32_t c[];
-    const uint32_t b = blockIdx.x >> spb_lg;
+    const uint32_t it = blockIdx.x >> spb_lg;
+    if (it >= *n_items) return;
+    const uint32_t item = items[it];
+    const uint32_t b = item & 1023u, chunk = item >> 10;
     const uint32_t s = blockIdx.x & ((1u << spb_lg) - 1);
     for (int k = threadIdx.x; k < kSliceNodes; k += blockDim.x) c[k] = 0;
     __syncthreads();
-    const uint64_t last = (uint64_t)nb * nblk - 1;
-    const uint32_t e0 = O[(uint64_t)b * nblk];
-    const uint32_t e1 = (int)b + 1 < nb ? O[(uint64_t)(b + 1) * nblk] : O[last] + H[last];
+    uint32_t e0, e1;
+    bucket_range(O, H, nblk, nb, b, e0, e1);
+    const bool split = e1 - e0 > kCountChunk;
+    const uint32_t k0 = e0 + chunk * kCountChunk;
+    const uint32_t k1 = e1 - k0 > kCountChunk ? k0 + kCountChunk : e1;
     const uint32_t smask = (1u << spb_lg) - 1;
-    for (uint32_t k = e0 + threadIdx.x; k < e1; k += blockDim.x) {
-        const uint32_t x = __ldg(sorted + k);
+    auto count = [&](uint32_t x) {
         if (((x >> kSliceLg) & smask) == s) atomicAdd(&c[x & (kSliceNodes - 1)], 1u);
+    };
+    auto count4 = [&](const uint4 &w) {
+        count(w.x);
+        count(w.y);
+        count(w.z);
+        count(w.w);
+    };
+    // scalar head to a 16-byte boundary, then 16-byte words with four loads in
+    // flight per thread (the reads are latency-bound), tail
+    const uint32_t a0 = ((k0 + 3u) & ~3u) < k1 ? ((k0 + 3u) & ~3u) : k1;
+    if (k0 + threadIdx.x < a0) count(__ldg(sorted + k0 + threadIdx.x));
+    const uint32_t nv = (k1 - a0) / 4;
+    const uint4 *s4 = reinterpret_cast<const uint4 *>(sorted + a0);
+    const uint32_t bd = blockDim.x;
+    uint32_t j = threadIdx.x;
+    for (; j + 3 * bd < nv; j += 4 * bd) {
+        const uint4 w0 = __ldg(s4 + j), w1 = __ldg(s4 + j + bd), w2 = __ldg(s4 + j + 2 * bd),
+                    w3 = __ldg(s4 + j + 3 * bd);
+        count4(w0);
+        count4(w1);
+        count4(w2);
+        count4(w3);
     }
+    for (; j < nv; j += bd) count4(__ldg(s4 + j));
+    const uint32_t t0 = a0 + 4 * nv;
+    if (t0 + threadIdx.x < k1) count(__ldg(sorted + t0 + threadIdx.x));
     __syncthreads();
     const uint64_t v0 = ((uint64_t)b << shift) + ((uint64_t)s << kSliceLg);
     for (int k = threadIdx.x; k < kSliceNodes; k += blockDim.x) {
         const uint64_t v = v0 + k;
-        if (v < n && c[k]) counts[v] += c[k];
+        const uint32_t x = c[k];
+        if (v < n && x) {
+            if (split) atomicAdd(counts + v, x);
+            else counts[v] += x;
+        }
     }
 }
 

@@ -76,6 +76,7 @@ constexpr int kThreads = kWarps * 32;
 // targets it finishes to its own region of a scratch buffer (order is
 // irrelevant to a histogram); parba_hist.cuh partitions and counts them.
 enum SinkKind { kStore = 0, kWindow = 1, kFull = 2, kTargets = 3 };
+constexpr int kHistBuckets = 1024;  // targets sink: per-CTA bucket histogram (parba_hist.cuh)
 
 #ifndef PARBA_WARP_TIMES
 #define PARBA_WARP_TIMES 0
@@ -92,8 +93,12 @@ struct SinkArgs {
     uint32_t *full;                        // full counts (n)
     uint32_t *t32;                         // targets: capw u32 slots per warp
     uint64_t capw;
+    uint32_t *hist;                        // targets: H[b * gridDim.x + blk] (bucket = target >> shift)
+    int shift, nb;
     uint64_t t32_cap;                      // host side: slots of t32
     uint64_t *t32_len;                     // host side: slots the launch fills
+    uint64_t *t32_span;                    // host side: slots per CTA
+    uint32_t *t32_ctas;                    // host side: CTAs of the launch
 };
 
 // Shared-memory layout of a tile CTA (dynamic smem, W warps):
@@ -117,7 +122,8 @@ struct TileLayout {
     static constexpr bool kSlots = SINK == kStore && !Hash::kPack;
     static constexpr uint32_t kSlotB = kSlots ? kQueue * 2 : 0;
     static constexpr size_t kTabB = Hash::kHasCrc ? (Hash::kTableWords + kTile) * 4 : 0;
-    static constexpr size_t fixed = kQB /* alignment pad */ + kTabB;
+    static constexpr size_t kHistB = SINK == kTargets ? kHistBuckets * 4 : 0;
+    static constexpr size_t fixed = kQB /* alignment pad */ + kTabB + kHistB;
     static constexpr size_t per_warp = kQB + kStageB + kSlotB;
 };
 constexpr uint64_t kValueMask52 = (1ull << 52) - 1;
@@ -166,6 +172,12 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
         for (int j = threadIdx.x; j < kTile; j += blockDim.x)
             clow_s[j] = crc32c_u64_bitwise(0u, 2u * (uint32_t)j + 1u);
     }
+    // targets sink: the CTA's bucket histogram follows the stage area (empty
+    // for this sink), i.e. the last kHistB bytes of the layout
+    [[maybe_unused]] uint32_t *hist_s =
+        reinterpret_cast<uint32_t *>(smem_raw + pad + (size_t)wpc * L::kQB + L::kTabB);
+    if constexpr (SINK == kTargets)
+        for (int b = threadIdx.x; b < a.nb; b += blockDim.x) hist_s[b] = 0;
     __syncthreads();
 
     // shared-window addresses of this warp's queue, stage and slot ring
@@ -264,7 +276,11 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
     auto emit = [&](bool f, uint64_t rv) {
         if constexpr (SINK == kTargets) {
             const unsigned m = ballot_all(f);
-            if (f) wout[wcur + __popc(m & ltmask)] = (uint32_t)target_of<NARROW, SEED, false, DEG>(rv, p);
+            if (f) {
+                const uint32_t tg = (uint32_t)target_of<NARROW, SEED, false, DEG>(rv, p);
+                wout[wcur + __popc(m & ltmask)] = tg;
+                atomicAdd(hist_s + (tg >> a.shift), 1u);
+            }
             wcur += __popc(m);
         }
     };
@@ -462,6 +478,9 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
     if constexpr (SINK == kTargets) {  // unused slots of the region: empty
         PARBA_CHECK(wcur <= a.capw);
         for (uint64_t j = wcur + lane; j < a.capw; j += 32) wout[j] = 0xffffffffu;
+        __syncthreads();
+        for (int b = threadIdx.x; b < a.nb; b += blockDim.x)
+            a.hist[(uint64_t)b * gridDim.x + blockIdx.x] = hist_s[b];
     }
     if constexpr (SINK == kStore) {
         if constexpr (kStageBufs == 2) {
