@@ -195,9 +195,10 @@ int launch_tiles_t(const DevParams &dp, uint64_t lo, uint64_t hi, const SinkArgs
             const uint64_t nw = grid * warps;
             ac.capw = (ntiles + nw - 1) / nw * kTile;
             if (nw * ac.capw > a.t32_cap) return fail(PARBA_ECUDA, "targets scratch too small");
-            *a.t32_len = nw * ac.capw;
-            *a.t32_span = (uint64_t)warps * ac.capw;
-            *a.t32_ctas = (uint32_t)grid;
+            a.t32_geom[0] = nw * ac.capw;
+            a.t32_geom[1] = ac.capw;
+            a.t32_geom[2] = (uint64_t)warps;
+            a.t32_geom[3] = grid;
         }
         kern<<<(unsigned)grid, warps * 32, smem, st>>>(dp, a0, a1, tile0, ntiles, ac, probes);
         CUDA_TRY(cudaGetLastError());
@@ -421,7 +422,8 @@ namespace {
 
 // Partitioned full histogram (parba_hist.cuh) over batches of at most
 // kHistBatch edges.  Applies when every target fits u32 and a bucket spans
-// at most 8 slices (n <= 1024 * 2^18); the source endpoints stay closed-form.
+// at most 8 slices (n <= kHistBuckets * 2^18); the source endpoints stay
+// closed-form.
 constexpr uint64_t kHistBatch = 1ull << 29;
 constexpr uint64_t kHistMinEdges = 1ull << 22;
 
@@ -437,7 +439,8 @@ bool use_partitioned(const parba_params_t *p, uint64_t lo, uint64_t hi) {
     if (p->n >= kEmptyTarget) return false;
     if (hist_shift(p->n) - kSliceLg > kMaxSliceLgPerBucket) return false;
     if (mode) return mode == 2;
-    return hi - lo >= kHistMinEdges;
+    // an L2-resident count array (n < 2^25 words) absorbs direct atomics as fast
+    return hi - lo >= kHistMinEdges && p->n >= (1ull << 25);
 }
 
 int full_partitioned(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi, uint32_t *counts,
@@ -452,7 +455,7 @@ int full_partitioned(const parba_params_t *p, const DevParams &dp, uint64_t lo, 
     const uint64_t batch = hi - lo < kHistBatch ? hi - lo : kHistBatch;
     // a launch fills nw * ceil(ntiles / nw) * kTile slots, nw <= 64 warps per SM
     const uint64_t cap = (batch / kTile + 2) * kTile + (uint64_t)di->sms * 64 * kTile;
-    const uint32_t nblk = (uint32_t)di->sms * 4;  // >= CTAs of one tile launch
+    const uint32_t nblk = (uint32_t)di->sms * 4 * kHistGroups;  // >= warp groups of one tile launch
     const uint64_t max_items = nb + cap / kCountChunk + 1;
     AsyncBuf t32, srt, H, O, tmp, items;
     if ((rc = t32.alloc(cap * 4, st)) || (rc = srt.alloc(cap * 4, st)) ||
@@ -472,32 +475,32 @@ int full_partitioned(const parba_params_t *p, const DevParams &dp, uint64_t lo, 
         if (dev < 64 && !attr[dev]) {
             CUDA_TRY(cudaFuncSetAttribute(slice_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           kSliceNodes * 4));
-            CUDA_TRY(cudaFuncSetAttribute(bucket_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          kScatterTile * 4));
+            CUDA_TRY(cudaFuncSetAttribute(bucket_scatter_kernel<kScatterThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          kScatterSmem));
             attr[dev] = true;
         }
     }
     for (uint64_t b0 = lo; b0 < hi;) {
         uint64_t b1 = hi - b0 > batch ? (b0 / kTile) * kTile + batch : hi;
         if (b1 > hi) b1 = hi;
-        uint64_t len = 0, span = 0;
-        uint32_t used = 0;
+        uint64_t geom[4] = {};
         SinkArgs a{};
         a.t32 = (uint32_t *)t32.p;
         a.hist = (uint32_t *)H.p;  // the tile launch writes the bucket histogram of each CTA's region
         a.shift = shift;
         a.nb = nb;
         a.t32_cap = cap;
-        a.t32_len = &len;
-        a.t32_span = &span;
-        a.t32_ctas = &used;
+        a.t32_geom = geom;
         if ((rc = launch_tiles<kTargets>(p, dp, b0, b1, a, probes, st))) return rc;
+        const uint64_t len = geom[0], capw = geom[1];
+        const uint32_t wpc = (uint32_t)geom[2], used = (uint32_t)geom[3] * kHistGroups;
         if (used > nblk) return fail(PARBA_ECUDA, "targets launch wider than the histogram");
-        // H / O: bucket-major, stride `used` (the tile CTAs; CTA c's region is [c * span, (c + 1) * span))
+        // H / O: bucket-major, stride `used` (one column per warp group)
         CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, (const uint32_t *)H.p, (uint32_t *)O.p,
                                                (int64_t)nb * used, st));
-        bucket_scatter_kernel<<<used, kHistThreads, kScatterTile * 4, st>>>((const uint32_t *)t32.p, len, span, n, shift, nb,
-                                                             (const uint32_t *)O.p, (uint32_t *)srt.p);
+        bucket_scatter_kernel<kScatterThreads><<<used, kScatterThreads, kScatterSmem, st>>>(
+            (const uint32_t *)t32.p, len, wpc, kHistGroups, capw, n, shift, nb, (const uint32_t *)O.p,
+            (uint32_t *)srt.p);
         CUDA_TRY(cudaGetLastError());
         count_plan_kernel<<<1, kHistThreads, 0, st>>>((const uint32_t *)O.p, (const uint32_t *)H.p, used, nb,
                                                        (uint32_t *)items.p, n_items);

@@ -30,8 +30,12 @@ constexpr int kHistThreads = 1024;
 #ifndef PARBA_SCATTER_TILE
 #define PARBA_SCATTER_TILE 16384
 #endif
+#ifndef PARBA_SCATTER_THREADS
+#define PARBA_SCATTER_THREADS 1024
+#endif
+constexpr int kScatterThreads = PARBA_SCATTER_THREADS;
 constexpr int kScatterTile = PARBA_SCATTER_TILE;  // entries per sorted sub-tile (dynamic smem)
-constexpr int kScatterPer = kScatterTile / kHistThreads;
+constexpr int kScatterSmem = (3 * kHistBuckets + kScatterTile) * 4;
 constexpr uint32_t kEmptyTarget = 0xffffffffu;
 
 __device__ __forceinline__ uint4 ld_stream4(const uint4 *p) {
@@ -42,9 +46,10 @@ __device__ __forceinline__ uint4 ld_stream4(const uint4 *p) {
     return v;
 }
 
-// Block-wide exclusive scan of x (one value per thread, kHistThreads threads).
+// Block-wide exclusive scan of x (one value per thread, <= 1024 threads).
 __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t x, uint32_t *warp_sums) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int nw = blockDim.x >> 5;
     uint32_t inc = x;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -54,7 +59,7 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t x, uint32_t *w
     if (lane == 31) warp_sums[w] = inc;
     __syncthreads();
     if (w == 0) {
-        uint32_t s = warp_sums[lane];
+        uint32_t s = lane < nw ? warp_sums[lane] : 0u;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
@@ -66,39 +71,49 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t x, uint32_t *w
     return inc - x + (w > 0 ? warp_sums[w - 1] : 0u);
 }
 
-// Step 2: O = exclusive scan of H (bucket-major).  CTA blk writes its
-// bucket-b entries to out[O[b * gridDim.x + blk] ...] in sub-tile order.
-__global__ void __launch_bounds__(kHistThreads) bucket_scatter_kernel(const uint32_t *__restrict__ t, uint64_t len,
-                                                                      uint64_t span, uint32_t n, int shift, int nb,
-                                                                      const uint32_t *__restrict__ O,
-                                                                      uint32_t *__restrict__ out) {
-    __shared__ uint32_t cur[kHistBuckets];    // next output position per bucket
-    __shared__ uint32_t cnt[kHistBuckets];    // sub-tile entries per bucket
-    __shared__ uint32_t start[kHistBuckets];  // sub-tile run start per bucket
-    extern __shared__ uint32_t sorted[];  // kScatterTile entries
+// Step 2: O = exclusive scan of H (bucket-major).  Scatter CTA c handles
+// warp group c % groups of tile CTA c / groups: slots
+// [(blk * wpc + w0) * capw, (blk * wpc + w1) * capw) with w0..w1 the group's
+// warps, and writes its bucket-b entries to out[O[b * gridDim.x + c] ...] in
+// sub-tile order.  T threads, kScatterTile entries per sub-tile.
+template <int T>
+__global__ void __launch_bounds__(T, 1) bucket_scatter_kernel(const uint32_t *__restrict__ t, uint64_t len,
+                                                           uint32_t wpc, uint32_t groups, uint64_t capw,
+                                                           uint32_t n, int shift, int nb,
+                                                           const uint32_t *__restrict__ O,
+                                                           uint32_t *__restrict__ out) {
+    constexpr int BPT = kHistBuckets / T;  // buckets per thread in the scan
+    constexpr int PER = kScatterTile / T;  // entries per thread and sub-tile
+    static_assert(BPT * T == kHistBuckets && PER % 4 == 0, "scatter shape");
+    extern __shared__ uint32_t scatter_smem[];  // kScatterSmem bytes
+    uint32_t *cur = scatter_smem;                  // next output position per bucket
+    uint32_t *cnt = cur + kHistBuckets;            // sub-tile entries per bucket
+    uint32_t *start = cnt + kHistBuckets;          // sub-tile run start per bucket
+    uint32_t *sorted = start + kHistBuckets;       // kScatterTile entries
     __shared__ uint32_t warp_sums[32];
     __shared__ uint32_t total_s;
-    for (int b = threadIdx.x; b < kHistBuckets; b += blockDim.x)
-        cur[b] = b < nb ? O[(uint64_t)b * gridDim.x + blockIdx.x] : 0u;
-    const uint64_t s0 = (uint64_t)blockIdx.x * span;
-    const uint64_t s1 = s0 + span < len ? s0 + span : len;
-    // coalesced: thread i takes 16-byte words i and i + kHistThreads of a
-    // sub-tile; the next sub-tile's loads are issued before this one is sorted
-    uint4 nx[kScatterPer / 4];
+    const uint32_t c = blockIdx.x, blk = c / groups, g = c % groups;
+    for (int b = threadIdx.x; b < kHistBuckets; b += T) cur[b] = b < nb ? O[(uint64_t)b * gridDim.x + c] : 0u;
+    const uint64_t s0 = ((uint64_t)blk * wpc + g * wpc / groups) * capw;
+    const uint64_t e1 = ((uint64_t)blk * wpc + (g + 1) * wpc / groups) * capw;
+    const uint64_t s1 = e1 < len ? e1 : len;
+    // coalesced: thread i takes 16-byte words i, i + T, ... of a sub-tile; the
+    // next sub-tile's loads are issued before this one is sorted
+    uint4 nx[PER / 4];
     auto load = [&](uint64_t base) {
 #pragma unroll
-        for (int h = 0; h < kScatterPer / 4; ++h) {
-            const uint64_t e = base + 4ull * (threadIdx.x + (uint64_t)h * kHistThreads);
+        for (int h = 0; h < PER / 4; ++h) {
+            const uint64_t e = base + 4ull * (threadIdx.x + (uint64_t)h * T);
             nx[h] = make_uint4(kEmptyTarget, kEmptyTarget, kEmptyTarget, kEmptyTarget);
             if (e < s1) nx[h] = ld_stream4(reinterpret_cast<const uint4 *>(t + e));
         }
     };
     load(s0);
     for (uint64_t base = s0; base < s1; base += kScatterTile) {
-        for (int b = threadIdx.x; b < kHistBuckets; b += blockDim.x) cnt[b] = 0;
-        uint32_t v[kScatterPer], rk[kScatterPer];
+        for (int b = threadIdx.x; b < kHistBuckets; b += T) cnt[b] = 0;
+        uint32_t v[PER], rk[PER];
 #pragma unroll
-        for (int h = 0; h < kScatterPer / 4; ++h) {
+        for (int h = 0; h < PER / 4; ++h) {
             v[4 * h] = nx[h].x;
             v[4 * h + 1] = nx[h].y;
             v[4 * h + 2] = nx[h].z;
@@ -107,33 +122,43 @@ __global__ void __launch_bounds__(kHistThreads) bucket_scatter_kernel(const uint
         load(base + kScatterTile);
         __syncthreads();
 #pragma unroll
-        for (int k = 0; k < kScatterPer; ++k)
+        for (int k = 0; k < PER; ++k)
             if (v[k] < n) rk[k] = atomicAdd(&cnt[v[k] >> shift], 1u);
         __syncthreads();
-        const uint32_t c = cnt[threadIdx.x];  // kHistThreads == kHistBuckets
-        const uint32_t ex = block_exclusive_scan(c, warp_sums);
-        start[threadIdx.x] = ex;
-        if (threadIdx.x == kHistThreads - 1) total_s = ex + c;
+        uint32_t cb[BPT], sum = 0;
+#pragma unroll
+        for (int i = 0; i < BPT; ++i) {
+            cb[i] = cnt[threadIdx.x * BPT + i];
+            sum += cb[i];
+        }
+        uint32_t ex = block_exclusive_scan(sum, warp_sums);
+#pragma unroll
+        for (int i = 0; i < BPT; ++i) {
+            start[threadIdx.x * BPT + i] = ex;
+            ex += cb[i];
+        }
+        if (threadIdx.x == T - 1) total_s = ex;
         __syncthreads();
 #pragma unroll
-        for (int k = 0; k < kScatterPer; ++k)
+        for (int k = 0; k < PER; ++k)
             if (v[k] < n) sorted[start[v[k] >> shift] + rk[k]] = v[k];
         __syncthreads();
         const uint32_t total = total_s;
-        for (uint32_t k = threadIdx.x; k < total; k += blockDim.x) {
+        for (uint32_t k = threadIdx.x; k < total; k += T) {
             const uint32_t x = sorted[k];
             const uint32_t b = x >> shift;
             out[cur[b] + (k - start[b])] = x;
         }
         __syncthreads();
-        cur[threadIdx.x] += c;
+#pragma unroll
+        for (int i = 0; i < BPT; ++i) cur[threadIdx.x * BPT + i] += cb[i];
     }
 }
 
 // Step 3 plan: bucket sizes are skewed (node v draws ~ 1/sqrt(v) of the
 // targets, so the lowest bucket holds several percent of all entries).  A
 // bucket is cut into chunks of at most kCountChunk entries; items[] lists
-// (bucket, chunk) pairs (bucket | chunk << 10).  One CTA of kHistThreads.
+// (bucket, chunk) pairs (bucket | chunk << kBucketBits).  One CTA of kHistThreads.
 constexpr uint32_t kCountChunk = 1u << 21;
 
 __device__ __forceinline__ void bucket_range(const uint32_t *O, const uint32_t *H, uint32_t nblk, int nb, uint32_t b,
@@ -147,17 +172,28 @@ __global__ void __launch_bounds__(kHistThreads) count_plan_kernel(const uint32_t
                                                                   const uint32_t *__restrict__ H, uint32_t nblk,
                                                                   int nb, uint32_t *__restrict__ items,
                                                                   uint32_t *__restrict__ n_items) {
+    constexpr int BPT = kHistBuckets / kHistThreads;
     __shared__ uint32_t warp_sums[32];
-    const uint32_t b = threadIdx.x;
-    uint32_t chunks = 0;
-    if ((int)b < nb) {
-        uint32_t e0, e1;
-        bucket_range(O, H, nblk, nb, b, e0, e1);
-        chunks = e1 > e0 ? (e1 - e0 + kCountChunk - 1) / kCountChunk : 0u;
+    uint32_t chunks[BPT], sum = 0;
+#pragma unroll
+    for (int i = 0; i < BPT; ++i) {
+        const uint32_t b = threadIdx.x * BPT + i;
+        chunks[i] = 0;
+        if ((int)b < nb) {
+            uint32_t e0, e1;
+            bucket_range(O, H, nblk, nb, b, e0, e1);
+            chunks[i] = e1 > e0 ? (e1 - e0 + kCountChunk - 1) / kCountChunk : 0u;
+        }
+        sum += chunks[i];
     }
-    const uint32_t base = block_exclusive_scan(chunks, warp_sums);
-    for (uint32_t c = 0; c < chunks; ++c) items[base + c] = b | (c << 10);
-    if (threadIdx.x == kHistThreads - 1) *n_items = base + chunks;
+    uint32_t base = block_exclusive_scan(sum, warp_sums);
+#pragma unroll
+    for (int i = 0; i < BPT; ++i) {
+        const uint32_t b = threadIdx.x * BPT + i;
+        for (uint32_t c = 0; c < chunks[i]; ++c) items[base + c] = b | (c << kBucketBits);
+        base += chunks[i];
+    }
+    if (threadIdx.x == kHistThreads - 1) *n_items = base;
 }
 
 // Step 3: CTA (item, s) counts the entries of one chunk of bucket b that fall
@@ -179,7 +215,7 @@ __global__ void __launch_bounds__(kHistThreads) slice_count_kernel(const uint32_
     const uint32_t it = blockIdx.x >> spb_lg;
     if (it >= *n_items) return;
     const uint32_t item = items[it];
-    const uint32_t b = item & 1023u, chunk = item >> 10;
+    const uint32_t b = item & (kHistBuckets - 1), chunk = item >> kBucketBits;
     const uint32_t s = blockIdx.x & ((1u << spb_lg) - 1);
     for (int k = threadIdx.x; k < kSliceNodes; k += blockDim.x) c[k] = 0;
     __syncthreads();

@@ -76,7 +76,15 @@ constexpr int kThreads = kWarps * 32;
 // targets it finishes to its own region of a scratch buffer (order is
 // irrelevant to a histogram); parba_hist.cuh partitions and counts them.
 enum SinkKind { kStore = 0, kWindow = 1, kFull = 2, kTargets = 3 };
-constexpr int kHistBuckets = 1024;  // targets sink: per-CTA bucket histogram (parba_hist.cuh)
+#ifndef PARBA_HIST_BUCKETS
+#define PARBA_HIST_BUCKETS 2048
+#endif
+constexpr int kHistBuckets = PARBA_HIST_BUCKETS;  // targets sink: bucket histogram per warp group (parba_hist.cuh)
+constexpr int kBucketBits = kHistBuckets == 1024 ? 10 : kHistBuckets == 2048 ? 11 : 12;
+#ifndef PARBA_HIST_GROUPS
+#define PARBA_HIST_GROUPS 1
+#endif
+constexpr int kHistGroups = PARBA_HIST_GROUPS;  // warp groups (scatter CTAs) per tile CTA
 
 #ifndef PARBA_WARP_TIMES
 #define PARBA_WARP_TIMES 0
@@ -93,12 +101,10 @@ struct SinkArgs {
     uint32_t *full;                        // full counts (n)
     uint32_t *t32;                         // targets: capw u32 slots per warp
     uint64_t capw;
-    uint32_t *hist;                        // targets: H[b * gridDim.x + blk] (bucket = target >> shift)
-    int shift, nb;
+    uint32_t *hist;                        // targets: H[b * G * gridDim.x + G * blk + group]
+    int shift, nb;                         //   (bucket = target >> shift, G = kHistGroups)
     uint64_t t32_cap;                      // host side: slots of t32
-    uint64_t *t32_len;                     // host side: slots the launch fills
-    uint64_t *t32_span;                    // host side: slots per CTA
-    uint32_t *t32_ctas;                    // host side: CTAs of the launch
+    uint64_t *t32_geom;                    // host side: {slots filled, capw, warps per CTA, CTAs}
 };
 
 // Shared-memory layout of a tile CTA (dynamic smem, W warps):
@@ -122,7 +128,7 @@ struct TileLayout {
     static constexpr bool kSlots = SINK == kStore && !Hash::kPack;
     static constexpr uint32_t kSlotB = kSlots ? kQueue * 2 : 0;
     static constexpr size_t kTabB = Hash::kHasCrc ? (Hash::kTableWords + kTile) * 4 : 0;
-    static constexpr size_t kHistB = SINK == kTargets ? kHistBuckets * 4 : 0;
+    static constexpr size_t kHistB = SINK == kTargets ? kHistGroups * kHistBuckets * 4 : 0;
     static constexpr size_t fixed = kQB /* alignment pad */ + kTabB + kHistB;
     static constexpr size_t per_warp = kQB + kStageB + kSlotB;
 };
@@ -177,7 +183,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
     [[maybe_unused]] uint32_t *hist_s =
         reinterpret_cast<uint32_t *>(smem_raw + pad + (size_t)wpc * L::kQB + L::kTabB);
     if constexpr (SINK == kTargets)
-        for (int b = threadIdx.x; b < a.nb; b += blockDim.x) hist_s[b] = 0;
+        for (int b = threadIdx.x; b < kHistGroups * a.nb; b += blockDim.x) hist_s[b] = 0;
     __syncthreads();
 
     // shared-window addresses of this warp's queue, stage and slot ring
@@ -272,14 +278,18 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
     // region (one ballot per step, so a warp's stores are contiguous)
     [[maybe_unused]] uint32_t *wout = nullptr;
     [[maybe_unused]] uint32_t wcur = 0;
-    if constexpr (SINK == kTargets) wout = a.t32 + gw * a.capw;
+    [[maybe_unused]] uint32_t *hist_w = hist_s;  // this warp's group
+    if constexpr (SINK == kTargets) {
+        wout = a.t32 + gw * a.capw;
+        hist_w = hist_s + (uint32_t)(wib * kHistGroups / wpc) * a.nb;
+    }
     auto emit = [&](bool f, uint64_t rv) {
         if constexpr (SINK == kTargets) {
             const unsigned m = ballot_all(f);
             if (f) {
                 const uint32_t tg = (uint32_t)target_of<NARROW, SEED, false, DEG>(rv, p);
                 wout[wcur + __popc(m & ltmask)] = tg;
-                atomicAdd(hist_s + (tg >> a.shift), 1u);
+                atomicAdd(hist_w + (tg >> a.shift), 1u);
             }
             wcur += __popc(m);
         }
@@ -479,8 +489,10 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
         PARBA_CHECK(wcur <= a.capw);
         for (uint64_t j = wcur + lane; j < a.capw; j += 32) wout[j] = 0xffffffffu;
         __syncthreads();
-        for (int b = threadIdx.x; b < a.nb; b += blockDim.x)
-            a.hist[(uint64_t)b * gridDim.x + blockIdx.x] = hist_s[b];
+        for (int i = threadIdx.x; i < kHistGroups * a.nb; i += blockDim.x) {
+            const int g = i / a.nb, b = i - g * a.nb;
+            a.hist[(uint64_t)b * kHistGroups * gridDim.x + (uint64_t)kHistGroups * blockIdx.x + g] = hist_s[i];
+        }
     }
     if constexpr (SINK == kStore) {
         if constexpr (kStageBufs == 2) {

@@ -323,8 +323,9 @@ _RAGGED_DEG = np.random.default_rng(7).integers(1, 40, size=200_000)
         ("n1e6_ragged", dict(n=10**6, d=16), 12345, -777),
         ("tiny_one_bucket", dict(n=1000, d=3), 0, 0),
         ("seeded", dict(n=300_000, d=5, n0=3, seed_edges=TRIANGLE), 3, 0),
-        ("nb1024_exact", dict(n=1 << 25, d=2), (1 << 25) - (1 << 22) - 5, 0),
-        ("eight_slices", dict(n=2 * 10**8, d=2), 2 * (2 * 10**8) - (1 << 23) - 99, 0),
+        ("all_buckets_one_slice", dict(n=1 << 26, d=2), (1 << 26) - (1 << 22) - 5, 0),
+        ("four_slices", dict(n=10**8, d=3), 3 * 10**8 - (1 << 23) - 99, 0),
+        ("eight_slices", dict(n=5 * 10**8, d=2), 2 * (5 * 10**8) - (1 << 23) - 99, 0),
         ("simple_hash", dict(n=500_000, d=4, hash=HashConfig(kind=HashKind.SIMPLE, seed0=5)), 0, 0),
         ("degree_sequence", dict(n=3 + _RAGGED_DEG.size, n0=3, degrees=_RAGGED_DEG, seed_edges=TRIANGLE), 3, 0),
     ],
@@ -334,7 +335,7 @@ def test_full_partitioned_equals_direct(case, monkeypatch):
     """The partitioned full histogram (targets -> bucket sort -> shared-memory
     slices, parba_hist.cuh) equals the direct-atomic kernel element-wise,
     probes included, on ragged ranges, seeds, degree sequences, a single
-    bucket, exactly 1024 buckets and 8 slices per bucket."""
+    bucket, every bucket (2048) of one slice, and 4 or 8 slices per bucket."""
     _, kw, lo, hi = case
     p = pb.GenParams(**kw)
     hi = p.m + hi if hi <= 0 else hi
@@ -355,8 +356,8 @@ def test_full_partitioned_vs_oracle_small(monkeypatch):
 
 
 def test_full_partition_too_large_falls_back(monkeypatch):
-    # n > 1024 * 2^18: a bucket would span 16 slices -> direct atomics
-    p = pb.GenParams(n=3 * 10**8, d=2)
+    # n > 2048 * 2^18: a bucket would span 16 slices -> direct atomics
+    p = pb.GenParams(n=6 * 10**8, d=2)
     lo = p.m - (1 << 22)
     part, pp = _full_counts(p, lo, p.m, "partition", monkeypatch)
     direct, pd = _full_counts(p, lo, p.m, "direct", monkeypatch)
