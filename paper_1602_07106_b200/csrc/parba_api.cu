@@ -424,7 +424,10 @@ namespace {
 // kHistBatch edges.  Applies when every target fits u32 and a bucket spans
 // at most 8 slices (n <= kHistBuckets * 2^18); the source endpoints stay
 // closed-form.
-constexpr uint64_t kHistBatch = 1ull << 29;
+#ifndef PARBA_HIST_BATCH_LG
+#define PARBA_HIST_BATCH_LG 29
+#endif
+constexpr uint64_t kHistBatch = 1ull << PARBA_HIST_BATCH_LG;
 constexpr uint64_t kHistMinEdges = 1ull << 22;
 
 int hist_shift(uint64_t n) {

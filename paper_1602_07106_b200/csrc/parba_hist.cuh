@@ -35,7 +35,7 @@ constexpr int kHistThreads = 1024;
 #endif
 constexpr int kScatterThreads = PARBA_SCATTER_THREADS;
 constexpr int kScatterTile = PARBA_SCATTER_TILE;  // entries per sorted sub-tile (dynamic smem)
-constexpr int kScatterSmem = (3 * kHistBuckets + kScatterTile) * 4;
+constexpr int kScatterSmem = (4 * kHistBuckets + kScatterTile) * 4;
 constexpr uint32_t kEmptyTarget = 0xffffffffu;
 
 __device__ __forceinline__ uint4 ld_stream4(const uint4 *p) {
@@ -89,7 +89,8 @@ __global__ void __launch_bounds__(T, 1) bucket_scatter_kernel(const uint32_t *__
     uint32_t *cur = scatter_smem;                  // next output position per bucket
     uint32_t *cnt = cur + kHistBuckets;            // sub-tile entries per bucket
     uint32_t *start = cnt + kHistBuckets;          // sub-tile run start per bucket
-    uint32_t *sorted = start + kHistBuckets;       // kScatterTile entries
+    uint32_t *delta = start + kHistBuckets;        // output position - sub-tile position
+    uint32_t *sorted = delta + kHistBuckets;       // kScatterTile entries
     __shared__ uint32_t warp_sums[32];
     __shared__ uint32_t total_s;
     const uint32_t c = blockIdx.x, blk = c / groups, g = c % groups;
@@ -134,7 +135,10 @@ __global__ void __launch_bounds__(T, 1) bucket_scatter_kernel(const uint32_t *__
         uint32_t ex = block_exclusive_scan(sum, warp_sums);
 #pragma unroll
         for (int i = 0; i < BPT; ++i) {
-            start[threadIdx.x * BPT + i] = ex;
+            const int b = threadIdx.x * BPT + i;
+            start[b] = ex;
+            delta[b] = cur[b] - ex;  // output position of sorted[k] is delta[b] + k
+            cur[b] += cb[i];
             ex += cb[i];
         }
         if (threadIdx.x == T - 1) total_s = ex;
@@ -147,11 +151,9 @@ __global__ void __launch_bounds__(T, 1) bucket_scatter_kernel(const uint32_t *__
         for (uint32_t k = threadIdx.x; k < total; k += T) {
             const uint32_t x = sorted[k];
             const uint32_t b = x >> shift;
-            out[cur[b] + (k - start[b])] = x;
+            out[delta[b] + k] = x;
         }
         __syncthreads();
-#pragma unroll
-        for (int i = 0; i < BPT; ++i) cur[threadIdx.x * BPT + i] += cb[i];
     }
 }
 
