@@ -151,6 +151,7 @@ __global__ void __launch_bounds__(T, 1) bucket_scatter_kernel(const uint32_t *__
         for (uint32_t k = threadIdx.x; k < total; k += T) {
             const uint32_t x = sorted[k];
             const uint32_t b = x >> shift;
+            PARBA_CHECK(delta[b] + k < len);
             out[delta[b] + k] = x;
         }
         __syncthreads();
@@ -218,6 +219,7 @@ __global__ void __launch_bounds__(kHistThreads) slice_count_kernel(const uint32_
     if (it >= *n_items) return;
     const uint32_t item = items[it];
     const uint32_t b = item & (kHistBuckets - 1), chunk = item >> kBucketBits;
+    PARBA_CHECK((int)b < nb);
     const uint32_t s = blockIdx.x & ((1u << spb_lg) - 1);
     for (int k = threadIdx.x; k < kSliceNodes; k += blockDim.x) c[k] = 0;
     __syncthreads();
