@@ -328,6 +328,10 @@ def main() -> None:
             extra[name] = {"edges_per_s": q.m * steps / t, "ms_per_step": 1000 * t / steps,
                            "n": cfg["n"], "d": cfg["d"], "K": K, "m": q.m,
                            "int_ops_per_s_convention": q.m * steps / t * 2 * INT_OPS_PER_PROBE}
+            if name == "full_c4":
+                extra[name]["path"] = ("partitioned: targets pass with per-CTA bucket histogram, bucket "
+                                       "sort in shared memory, shared-memory slice counts (parba_hist.cuh); "
+                                       "no per-edge global atomics")
             del counts
 
     if rank != 0:
