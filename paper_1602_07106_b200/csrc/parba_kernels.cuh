@@ -58,6 +58,9 @@ constexpr uint64_t kRyMin = 1ull << 27;
 #ifndef PARBA_MINB_STORE
 #define PARBA_MINB_STORE 1
 #endif
+#ifndef PARBA_ILP_TARGETS
+#define PARBA_ILP_TARGETS 2
+#endif
 #ifndef PARBA_MINB_STREAM
 #define PARBA_MINB_STREAM 1
 #endif
@@ -201,7 +204,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
     const uint64_t nw = (uint64_t)gridDim.x * wpc;
 
     // NS chains per lane in phase 2 (independent probes for the scheduler)
-    constexpr int NS = SINK == kStore ? PARBA_ILP_STORE : PARBA_ILP_STREAM;
+    constexpr int NS = SINK == kStore ? PARBA_ILP_STORE : SINK == kTargets ? PARBA_ILP_TARGETS : PARBA_ILP_STREAM;
     uint32_t act[NS];               // 1: slot holds a running chain
     R r[NS];
     uint32_t saddr[NS];             // store: smem address of the chain's stage cell
