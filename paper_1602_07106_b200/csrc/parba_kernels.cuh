@@ -61,6 +61,13 @@ constexpr uint64_t kRyMin = 1ull << 27;
 #ifndef PARBA_ILP_TARGETS
 #define PARBA_ILP_TARGETS 2
 #endif
+// targets sink: finished chain values are staged in a 64-entry per-warp ring
+// and turned into targets 32 at a time with every lane busy (1), or each
+// finishing lane computes and stores its target at once (0; 1 measured 3%
+// slower at C4)
+#ifndef PARBA_TARGET_STAGE
+#define PARBA_TARGET_STAGE 0
+#endif
 #ifndef PARBA_MINB_STREAM
 #define PARBA_MINB_STREAM 1
 #endif
@@ -127,7 +134,9 @@ struct TileLayout {
     static constexpr uint32_t kLgEB = kEB == 8 ? 3u : 2u;
     static constexpr uint32_t kQB = kQueue * kEB;
     static constexpr uint32_t kTB = kTile * (uint32_t)sizeof(R);  // one stage buffer
-    static constexpr uint32_t kStageB = SINK == kStore ? kStageBufs * kTB : 0;
+    static constexpr uint32_t kStageB = SINK == kStore ? kStageBufs * kTB
+                                        : (SINK == kTargets && PARBA_TARGET_STAGE) ? 64u * (uint32_t)sizeof(R)
+                                                                                   : 0;
     static constexpr bool kSlots = SINK == kStore && !Hash::kPack;
     static constexpr uint32_t kSlotB = kSlots ? kQueue * 2 : 0;
     static constexpr size_t kTabB = Hash::kHasCrc ? (Hash::kTableWords + kTile) * 4 : 0;
@@ -181,10 +190,10 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
         for (int j = threadIdx.x; j < kTile; j += blockDim.x)
             clow_s[j] = crc32c_u64_bitwise(0u, 2u * (uint32_t)j + 1u);
     }
-    // targets sink: the CTA's bucket histogram follows the stage area (empty
-    // for this sink), i.e. the last kHistB bytes of the layout
-    [[maybe_unused]] uint32_t *hist_s =
-        reinterpret_cast<uint32_t *>(smem_raw + pad + (size_t)wpc * L::kQB + L::kTabB);
+    // targets sink: the CTA's bucket histograms follow the stage and slot
+    // areas, i.e. the last kHistB bytes of the layout
+    [[maybe_unused]] uint32_t *hist_s = reinterpret_cast<uint32_t *>(
+        smem_raw + pad + (size_t)wpc * (L::kQB + L::kStageB + L::kSlotB) + L::kTabB);
     if constexpr (SINK == kTargets)
         for (int b = threadIdx.x; b < kHistGroups * a.nb; b += blockDim.x) hist_s[b] = 0;
     __syncthreads();
@@ -286,15 +295,35 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
         wout = a.t32 + gw * a.capw;
         hist_w = hist_s + (uint32_t)(wib * kHistGroups / wpc) * a.nb;
     }
+    auto put_target = [&](uint32_t slot, uint64_t rv) {
+        const uint32_t tg = (uint32_t)target_of<NARROW, SEED, false, DEG>(rv, p);
+        wout[slot] = tg;
+        atomicAdd(hist_w + (tg >> a.shift), 1u);
+    };
+    [[maybe_unused]] uint32_t wstaged = 0;  // staged values (wcur = values written)
+    // stage ring -> targets, 32 (or, at the end, the rest) with every lane busy
+    auto drain_stage = [&](bool all) {
+        if constexpr (SINK == kTargets && PARBA_TARGET_STAGE) {
+            __syncwarp();
+            while (wstaged - wcur >= 32u || (all && wstaged != wcur)) {
+                const uint32_t j = wcur + lane;
+                if (j < wstaged) put_target(j, (uint64_t)lds_t<R>(stage_s + (j & 63u) * (uint32_t)sizeof(R)));
+                wcur = wstaged - wcur >= 32u ? wcur + 32u : wstaged;
+            }
+            __syncwarp();
+        }
+    };
     auto emit = [&](bool f, uint64_t rv) {
         if constexpr (SINK == kTargets) {
             const unsigned m = ballot_all(f);
-            if (f) {
-                const uint32_t tg = (uint32_t)target_of<NARROW, SEED, false, DEG>(rv, p);
-                wout[wcur + __popc(m & ltmask)] = tg;
-                atomicAdd(hist_w + (tg >> a.shift), 1u);
+            if constexpr (PARBA_TARGET_STAGE) {
+                if (f) sts_t<R>(stage_s + ((wstaged + __popc(m & ltmask)) & 63u) * (uint32_t)sizeof(R), (R)rv);
+                wstaged += __popc(m);
+                if (wstaged - wcur >= 32u) drain_stage(false);
+            } else {
+                if (f) put_target(wcur + __popc(m & ltmask), rv);
+                wcur += __popc(m);
             }
-            wcur += __popc(m);
         }
     };
 
@@ -489,6 +518,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
     }
     while (any_act()) step();
     if constexpr (SINK == kTargets) {  // unused slots of the region: empty
+        drain_stage(true);
         PARBA_CHECK(wcur <= a.capw);
         for (uint64_t j = wcur + lane; j < a.capw; j += 32) wout[j] = 0xffffffffu;
         __syncthreads();
