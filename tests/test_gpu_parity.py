@@ -355,6 +355,26 @@ def test_full_partitioned_vs_oracle_small(monkeypatch):
     assert np.array_equal(got.astype(np.int64), want) and probes == wp
 
 
+def test_full_partitioned_random_ranges(monkeypatch):
+    """Forced partition on 24 seeded random (n, d, seed graph, hash, [lo, hi))
+    draws, element-wise against the direct kernel (probes included)."""
+    rng = np.random.default_rng(1602)
+    for _ in range(24):
+        n = int(rng.integers(50, 3_000_000))
+        d = int(rng.integers(1, 12))
+        kw = dict(n=n, d=d)
+        if rng.random() < 0.3:
+            kw.update(n0=3, seed_edges=TRIANGLE)
+        if rng.random() < 0.3:
+            kw.update(hash=HashConfig(kind=HashKind.SIMPLE, seed0=int(rng.integers(0, 1 << 32))))
+        p = pb.GenParams(**kw)
+        lo = int(rng.integers(p.m0, p.m))
+        hi = int(rng.integers(lo, p.m + 1))
+        part, pp = _full_counts(p, lo, hi, "partition", monkeypatch)
+        direct, pd = _full_counts(p, lo, hi, "direct", monkeypatch)
+        assert pp == pd and np.array_equal(part, direct), (kw, lo, hi)
+
+
 def test_full_partition_too_large_falls_back(monkeypatch):
     # n > 2048 * 2^18: a bucket would span 16 slices -> direct atomics
     p = pb.GenParams(n=6 * 10**8, d=2)
