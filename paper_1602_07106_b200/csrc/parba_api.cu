@@ -135,7 +135,7 @@ int nc_for(uint64_t two_hi) {
 struct DevInfo {
     int sms = 0;
     int smem_optin = 0;  // max dynamic shared memory per block
-    bool attr_done[12][4][2] = {};  // [hash variant][sink][seed]
+    bool attr_done[12][5][2] = {};  // [hash variant][sink][seed]
 };
 std::mutex g_mu;
 std::vector<DevInfo> g_dev;
@@ -190,7 +190,7 @@ int launch_tiles_t(const DevParams &dp, uint64_t lo, uint64_t hi, const SinkArgs
         if (grid > need) grid = need;
         SinkArgs ac = a;
         if (SINK == kStore) ac.out = a.out + 2 * (a0 - lo);
-        if (SINK == kTargets) {  // one launch; every warp owns capw slots
+        if (is_targets(SINK)) {  // one launch; every warp owns capw slots
             if (a1 != hi) return fail(PARBA_ECUDA, "targets pass needs one launch");
             const uint64_t nw = grid * warps;
             ac.capw = (ntiles + nw - 1) / nw * kTile;
@@ -293,6 +293,13 @@ int launch_store(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint
 }
 }  // namespace host
 }  // namespace parba
+
+namespace {  // partitioned degree counts, defined below the first C block
+bool use_partitioned(const parba_params_t *p, uint64_t lo, uint64_t hi, uint64_t K);
+template <typename CountT>
+int count_partitioned(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi, uint64_t K,
+                      CountT *counts, unsigned long long *probes, cudaStream_t st);
+}  // namespace
 
 extern "C" {
 
@@ -406,6 +413,11 @@ int parba_degree_window(const parba_params_t *p, uint64_t lo, uint64_t hi, uint6
     cudaStream_t st = (cudaStream_t)stream;
     DevParams dp = make_dev(p, K);
     if (p->flags) return count_nodes_u64(p, dp, lo, hi, K, counts, probes, st);
+    if (use_partitioned(p, lo, hi, K)) {  // large windows: partitioned like the full histogram
+        rc = count_partitioned<unsigned long long>(p, dp, lo, hi, K, counts, probes, st);
+        if (rc) return rc;
+        return launch_sources<unsigned long long>(dp, lo, hi, K, counts, st);
+    }
     if (is_deg(p)) {
         rc = win_rlim_deg(p, dp, K, st);
         if (rc) return rc;
@@ -420,40 +432,47 @@ int parba_degree_window(const parba_params_t *p, uint64_t lo, uint64_t hi, uint6
 
 namespace {
 
-// Partitioned full histogram (parba_hist.cuh) over batches of at most
-// kHistBatch edges.  Applies when every target fits u32 and a bucket spans
-// at most 8 slices (n <= kHistBuckets * 2^18); the source endpoints stay
-// closed-form.
+// Partitioned degree counts (parba_hist.cuh) over batches of at most
+// kHistBatch edges, for the targets below K (full histogram: K = n, u32
+// counts; window: u64 counts).  Applies when targets fit u32 and the domain
+// splits into at most kHistBucketsMax buckets of at most 8 slices
+// (K <= 8192 * 2^18 = 2^31); more than kHistBuckets buckets are scattered
+// in several passes over the batch's targets.  Source endpoints stay
+// closed-form (launch_sources).
 #ifndef PARBA_HIST_BATCH_LG
 #define PARBA_HIST_BATCH_LG 29
 #endif
 constexpr uint64_t kHistBatch = 1ull << PARBA_HIST_BATCH_LG;
 constexpr uint64_t kHistMinEdges = 1ull << 22;
+constexpr int kMaxShift = kSliceLg + kMaxSliceLgPerBucket;
 
-int hist_shift(uint64_t n) {
+// smallest shift with at most kHistBuckets buckets (one scatter pass), capped
+// at 8 slices per bucket; 0 when the domain needs more than kHistBucketsMax
+int hist_shift(uint64_t K) {
     int shift = kSliceLg;
-    while (((n + (1ull << shift) - 1) >> shift) > (uint64_t)kHistBuckets) ++shift;
-    return shift;
+    while (shift < kMaxShift && ((K + (1ull << shift) - 1) >> shift) > (uint64_t)kHistBuckets) ++shift;
+    return ((K + (1ull << shift) - 1) >> shift) <= (uint64_t)kHistBucketsMax ? shift : 0;
 }
 
-bool use_partitioned(const parba_params_t *p, uint64_t lo, uint64_t hi) {
-    const char *e = getenv("PARBA_FULL_MODE");  // "direct" / "partition" (tests, A/B)
+bool use_partitioned(const parba_params_t *p, uint64_t lo, uint64_t hi, uint64_t K) {
+    // PARBA_FULL_MODE = "direct" / "partition" (tests, A/B)
+    const char *e = getenv("PARBA_FULL_MODE");
     const int mode = !e ? 0 : strcmp(e, "direct") == 0 ? 1 : strcmp(e, "partition") == 0 ? 2 : 0;
-    if (p->n >= kEmptyTarget) return false;
-    if (hist_shift(p->n) - kSliceLg > kMaxSliceLgPerBucket) return false;
+    if (p->flags || K == 0 || K >= kEmptyTarget || p->n >= kEmptyTarget) return false;
+    if (!hist_shift(K)) return false;
     if (mode) return mode == 2;
-    // an L2-resident count array (n < 2^25 words) absorbs direct atomics as fast
-    return hi - lo >= kHistMinEdges && p->n >= (1ull << 25);
+    // an L2-resident count array (K < 2^25 words) absorbs direct atomics as fast
+    return hi - lo >= kHistMinEdges && K >= (1ull << 25);
 }
 
-int full_partitioned(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi, uint32_t *counts,
-                     unsigned long long *probes, cudaStream_t st) {
+template <typename CountT>
+int count_partitioned(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi, uint64_t K,
+                      CountT *counts, unsigned long long *probes, cudaStream_t st) {
     DevInfo *di;
     int rc = dev_info(&di);
     if (rc) return rc;
-    const uint32_t n = (uint32_t)p->n;
-    const int shift = hist_shift(n);
-    const int nb = (int)((n + (1ull << shift) - 1) >> shift);
+    const int shift = hist_shift(K);
+    const int nb = (int)((K + (1ull << shift) - 1) >> shift);
     const int spb_lg = shift - kSliceLg;
     const uint64_t batch = hi - lo < kHistBatch ? hi - lo : kHistBatch;
     // a launch fills nw * ceil(ntiles / nw) * kTile slots, nw <= 64 warps per SM
@@ -476,10 +495,12 @@ int full_partitioned(const parba_params_t *p, const DevParams &dp, uint64_t lo, 
         int dev = 0;
         CUDA_TRY(cudaGetDevice(&dev));
         if (dev < 64 && !attr[dev]) {
-            CUDA_TRY(cudaFuncSetAttribute(slice_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            CUDA_TRY(cudaFuncSetAttribute(slice_count_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           kSliceNodes * 4));
-            CUDA_TRY(cudaFuncSetAttribute(bucket_scatter_kernel<kScatterThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          kScatterSmem));
+            CUDA_TRY(cudaFuncSetAttribute(slice_count_kernel<unsigned long long>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kSliceNodes * 4));
+            CUDA_TRY(cudaFuncSetAttribute(bucket_scatter_kernel<kScatterThreads>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kScatterSmem));
             attr[dev] = true;
         }
     }
@@ -492,26 +513,32 @@ int full_partitioned(const parba_params_t *p, const DevParams &dp, uint64_t lo, 
         a.hist = (uint32_t *)H.p;  // the tile launch writes the bucket histogram of each CTA's region
         a.shift = shift;
         a.nb = nb;
+        a.klim = K;
         a.t32_cap = cap;
         a.t32_geom = geom;
-        if ((rc = launch_tiles<kTargets>(p, dp, b0, b1, a, probes, st))) return rc;
+        rc = K >= p->n ? launch_tiles<kTargets>(p, dp, b0, b1, a, probes, st)
+                       : launch_tiles<kTargetsK>(p, dp, b0, b1, a, probes, st);
+        if (rc) return rc;
         const uint64_t len = geom[0], capw = geom[1];
         const uint32_t wpc = (uint32_t)geom[2], used = (uint32_t)geom[3] * kHistGroups;
         if (used > nblk) return fail(PARBA_ECUDA, "targets launch wider than the histogram");
         // H / O: bucket-major, stride `used` (one column per warp group)
         CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, (const uint32_t *)H.p, (uint32_t *)O.p,
                                                (int64_t)nb * used, st));
-        bucket_scatter_kernel<kScatterThreads><<<used, kScatterThreads, kScatterSmem, st>>>(
-            (const uint32_t *)t32.p, len, wpc, kHistGroups, capw, n, shift, nb, (const uint32_t *)O.p,
-            (uint32_t *)srt.p);
-        CUDA_TRY(cudaGetLastError());
+        for (int wb = 0; wb < nb; wb += kHistBuckets) {  // scatter passes
+            const int nbw = nb - wb < kHistBuckets ? nb - wb : kHistBuckets;
+            bucket_scatter_kernel<kScatterThreads><<<used, kScatterThreads, kScatterSmem, st>>>(
+                (const uint32_t *)t32.p, len, wpc, kHistGroups, capw, shift, wb, nbw, (const uint32_t *)O.p,
+                (uint32_t *)srt.p);
+            CUDA_TRY(cudaGetLastError());
+        }
         count_plan_kernel<<<1, kHistThreads, 0, st>>>((const uint32_t *)O.p, (const uint32_t *)H.p, used, nb,
                                                        (uint32_t *)items.p, n_items);
         CUDA_TRY(cudaGetLastError());
         const uint64_t items_ub = nb + len / kCountChunk + 1;  // >= sum of ceil(size_b / chunk)
-        slice_count_kernel<<<(unsigned)(items_ub << spb_lg), kHistThreads, kSliceNodes * 4, st>>>(
+        slice_count_kernel<CountT><<<(unsigned)(items_ub << spb_lg), kHistThreads, kSliceNodes * 4, st>>>(
             (const uint32_t *)srt.p, (const uint32_t *)O.p, (const uint32_t *)H.p, used, nb,
-            (const uint32_t *)items.p, n_items, n, shift, spb_lg, counts);
+            (const uint32_t *)items.p, n_items, (uint32_t)K, shift, spb_lg, counts);
         CUDA_TRY(cudaGetLastError());
         b0 = b1;
     }
@@ -532,8 +559,8 @@ int parba_degree_full(const parba_params_t *p, uint64_t lo, uint64_t hi, uint32_
     cudaStream_t st = (cudaStream_t)stream;
     const DevParams dp = make_dev(p, p->n);
     if (p->flags) return count_nodes_u32(p, dp, lo, hi, p->n, counts, probes, st);
-    if (use_partitioned(p, lo, hi)) {
-        rc = full_partitioned(p, dp, lo, hi, counts, probes, st);
+    if (use_partitioned(p, lo, hi, p->n)) {
+        rc = count_partitioned<uint32_t>(p, dp, lo, hi, p->n, counts, probes, st);
     } else {
         SinkArgs a{nullptr, nullptr, counts};
         rc = launch_tiles<kFull>(p, dp, lo, hi, a, probes, st);

@@ -75,11 +75,13 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t x, uint32_t *w
 // warp group c % groups of tile CTA c / groups: slots
 // [(blk * wpc + w0) * capw, (blk * wpc + w1) * capw) with w0..w1 the group's
 // warps, and writes its bucket-b entries to out[O[b * gridDim.x + c] ...] in
-// sub-tile order.  T threads, kScatterTile entries per sub-tile.
+// sub-tile order.  One pass handles buckets [wb, wb + nbw) (nbw <=
+// kHistBuckets) and skips the others.  T threads, kScatterTile entries per
+// sub-tile.
 template <int T>
 __global__ void __launch_bounds__(T, 1) bucket_scatter_kernel(const uint32_t *__restrict__ t, uint64_t len,
                                                            uint32_t wpc, uint32_t groups, uint64_t capw,
-                                                           uint32_t n, int shift, int nb,
+                                                           int shift, int wb, int nbw,
                                                            const uint32_t *__restrict__ O,
                                                            uint32_t *__restrict__ out) {
     constexpr int BPT = kHistBuckets / T;  // buckets per thread in the scan
@@ -94,7 +96,11 @@ __global__ void __launch_bounds__(T, 1) bucket_scatter_kernel(const uint32_t *__
     __shared__ uint32_t warp_sums[32];
     __shared__ uint32_t total_s;
     const uint32_t c = blockIdx.x, blk = c / groups, g = c % groups;
-    for (int b = threadIdx.x; b < kHistBuckets; b += T) cur[b] = b < nb ? O[(uint64_t)b * gridDim.x + c] : 0u;
+    for (int b = threadIdx.x; b < kHistBuckets; b += T)
+        cur[b] = b < nbw ? O[(uint64_t)(wb + b) * gridDim.x + c] : 0u;
+    // an entry's bucket in this pass: (v >> shift) - wb, kept when < nbw
+    // (empty slots, UINT32_MAX, land above every pass: buckets < 2^(32-shift) - 1)
+    auto wbucket = [&](uint32_t v) -> uint32_t { return (v >> shift) - (uint32_t)wb; };
     const uint64_t s0 = ((uint64_t)blk * wpc + g * wpc / groups) * capw;
     const uint64_t e1 = ((uint64_t)blk * wpc + (g + 1) * wpc / groups) * capw;
     const uint64_t s1 = e1 < len ? e1 : len;
@@ -124,7 +130,7 @@ __global__ void __launch_bounds__(T, 1) bucket_scatter_kernel(const uint32_t *__
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < PER; ++k)
-            if (v[k] < n) rk[k] = atomicAdd(&cnt[v[k] >> shift], 1u);
+            if (v[k] != kEmptyTarget && wbucket(v[k]) < (uint32_t)nbw) rk[k] = atomicAdd(&cnt[wbucket(v[k])], 1u);
         __syncthreads();
         uint32_t cb[BPT], sum = 0;
 #pragma unroll
@@ -145,12 +151,12 @@ __global__ void __launch_bounds__(T, 1) bucket_scatter_kernel(const uint32_t *__
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < PER; ++k)
-            if (v[k] < n) sorted[start[v[k] >> shift] + rk[k]] = v[k];
+            if (v[k] != kEmptyTarget && wbucket(v[k]) < (uint32_t)nbw) sorted[start[wbucket(v[k])] + rk[k]] = v[k];
         __syncthreads();
         const uint32_t total = total_s;
         for (uint32_t k = threadIdx.x; k < total; k += T) {
             const uint32_t x = sorted[k];
-            const uint32_t b = x >> shift;
+            const uint32_t b = wbucket(x);
             PARBA_CHECK(delta[b] + k < len);
             out[delta[b] + k] = x;
         }
@@ -175,28 +181,26 @@ __global__ void __launch_bounds__(kHistThreads) count_plan_kernel(const uint32_t
                                                                   const uint32_t *__restrict__ H, uint32_t nblk,
                                                                   int nb, uint32_t *__restrict__ items,
                                                                   uint32_t *__restrict__ n_items) {
-    constexpr int BPT = kHistBuckets / kHistThreads;
     __shared__ uint32_t warp_sums[32];
-    uint32_t chunks[BPT], sum = 0;
-#pragma unroll
-    for (int i = 0; i < BPT; ++i) {
-        const uint32_t b = threadIdx.x * BPT + i;
-        chunks[i] = 0;
+    __shared__ uint32_t carry_s;
+    if (threadIdx.x == 0) carry_s = 0;
+    __syncthreads();
+    for (int b0 = 0; b0 < nb; b0 += kHistThreads) {
+        const uint32_t b = b0 + threadIdx.x;
+        uint32_t chunks = 0;
         if ((int)b < nb) {
             uint32_t e0, e1;
             bucket_range(O, H, nblk, nb, b, e0, e1);
-            chunks[i] = e1 > e0 ? (e1 - e0 + kCountChunk - 1) / kCountChunk : 0u;
+            chunks = e1 > e0 ? (e1 - e0 + kCountChunk - 1) / kCountChunk : 0u;
         }
-        sum += chunks[i];
+        const uint32_t carry = carry_s;
+        const uint32_t base = carry + block_exclusive_scan(chunks, warp_sums);
+        for (uint32_t c = 0; c < chunks; ++c) items[base + c] = b | (c << kBucketBits);
+        __syncthreads();  // every thread has read carry_s
+        if (threadIdx.x == kHistThreads - 1) carry_s = base + chunks;
+        __syncthreads();
     }
-    uint32_t base = block_exclusive_scan(sum, warp_sums);
-#pragma unroll
-    for (int i = 0; i < BPT; ++i) {
-        const uint32_t b = threadIdx.x * BPT + i;
-        for (uint32_t c = 0; c < chunks[i]; ++c) items[base + c] = b | (c << kBucketBits);
-        base += chunks[i];
-    }
-    if (threadIdx.x == kHistThreads - 1) *n_items = base;
+    if (threadIdx.x == 0) *n_items = carry_s;
 }
 
 // Step 3: CTA (item, s) counts the entries of one chunk of bucket b that fall
@@ -207,18 +211,19 @@ __global__ void __launch_bounds__(kHistThreads) count_plan_kernel(const uint32_t
 // read from HBM about once and from L2 by the others.  (A cluster variant
 // that reads the chunk once and routes each entry to the owning CTA with a
 // distributed-shared-memory red.add measured 3x slower.)
+template <typename CountT>
 __global__ void __launch_bounds__(kHistThreads) slice_count_kernel(const uint32_t *__restrict__ sorted,
                                                                    const uint32_t *__restrict__ O,
                                                                    const uint32_t *__restrict__ H, uint32_t nblk,
                                                                    int nb, const uint32_t *__restrict__ items,
                                                                    const uint32_t *__restrict__ n_items, uint32_t n,
                                                                    int shift, int spb_lg,
-                                                                   uint32_t *__restrict__ counts) {
+                                                                   CountT *__restrict__ counts) {
     extern __shared__ uint32_t c[];
     const uint32_t it = blockIdx.x >> spb_lg;
     if (it >= *n_items) return;
     const uint32_t item = items[it];
-    const uint32_t b = item & (kHistBuckets - 1), chunk = item >> kBucketBits;
+    const uint32_t b = item & ((1u << kBucketBits) - 1), chunk = item >> kBucketBits;
     PARBA_CHECK((int)b < nb);
     const uint32_t s = blockIdx.x & ((1u << spb_lg) - 1);
     for (int k = threadIdx.x; k < kSliceNodes; k += blockDim.x) c[k] = 0;
@@ -263,7 +268,7 @@ __global__ void __launch_bounds__(kHistThreads) slice_count_kernel(const uint32_
         const uint64_t v = v0 + k;
         const uint32_t x = c[k];
         if (v < n && x) {
-            if (split) atomicAdd(counts + v, x);
+            if (split) atomicAdd(counts + v, (CountT)x);
             else counts[v] += x;
         }
     }

@@ -61,13 +61,6 @@ constexpr uint64_t kRyMin = 1ull << 27;
 #ifndef PARBA_ILP_TARGETS
 #define PARBA_ILP_TARGETS 2
 #endif
-// targets sink: finished chain values are staged in a 64-entry per-warp ring
-// and turned into targets 32 at a time with every lane busy (1), or each
-// finishing lane computes and stores its target at once (0; 1 measured 3%
-// slower at C4)
-#ifndef PARBA_TARGET_STAGE
-#define PARBA_TARGET_STAGE 0
-#endif
 #ifndef PARBA_MINB_STREAM
 #define PARBA_MINB_STREAM 1
 #endif
@@ -85,12 +78,20 @@ constexpr int kThreads = kWarps * 32;
 // kTargets: the full histogram's first pass — each warp appends the u32
 // targets it finishes to its own region of a scratch buffer (order is
 // irrelevant to a histogram); parba_hist.cuh partitions and counts them.
-enum SinkKind { kStore = 0, kWindow = 1, kFull = 2, kTargets = 3 };
+// kTargetsK: the same for a window, keeping only targets < klim.
+enum SinkKind { kStore = 0, kWindow = 1, kFull = 2, kTargets = 3, kTargetsK = 4 };
+__host__ __device__ constexpr bool is_targets(int sink) { return sink == kTargets || sink == kTargetsK; }
 #ifndef PARBA_HIST_BUCKETS
 #define PARBA_HIST_BUCKETS 2048
 #endif
-constexpr int kHistBuckets = PARBA_HIST_BUCKETS;  // targets sink: bucket histogram per warp group (parba_hist.cuh)
-constexpr int kBucketBits = kHistBuckets == 1024 ? 10 : kHistBuckets == 2048 ? 11 : 12;
+// buckets one scatter pass handles (parba_hist.cuh); a target domain of up
+// to kHistBucketsMax buckets is scattered in several passes
+constexpr int kHistBuckets = PARBA_HIST_BUCKETS;
+#ifndef PARBA_HIST_BUCKETS_MAX
+#define PARBA_HIST_BUCKETS_MAX 8192
+#endif
+constexpr int kHistBucketsMax = PARBA_HIST_BUCKETS_MAX;  // targets sink: bucket histogram per warp group
+constexpr int kBucketBits = 13;        // bucket field of a count work item
 #ifndef PARBA_HIST_GROUPS
 #define PARBA_HIST_GROUPS 1
 #endif
@@ -113,6 +114,7 @@ struct SinkArgs {
     uint64_t capw;
     uint32_t *hist;                        // targets: H[b * G * gridDim.x + G * blk + group]
     int shift, nb;                         //   (bucket = target >> shift, G = kHistGroups)
+    uint64_t klim;                         // targets: only targets < klim are kept
     uint64_t t32_cap;                      // host side: slots of t32
     uint64_t *t32_geom;                    // host side: {slots filled, capw, warps per CTA, CTAs}
 };
@@ -134,13 +136,11 @@ struct TileLayout {
     static constexpr uint32_t kLgEB = kEB == 8 ? 3u : 2u;
     static constexpr uint32_t kQB = kQueue * kEB;
     static constexpr uint32_t kTB = kTile * (uint32_t)sizeof(R);  // one stage buffer
-    static constexpr uint32_t kStageB = SINK == kStore ? kStageBufs * kTB
-                                        : (SINK == kTargets && PARBA_TARGET_STAGE) ? 64u * (uint32_t)sizeof(R)
-                                                                                   : 0;
+    static constexpr uint32_t kStageB = SINK == kStore ? kStageBufs * kTB : 0;
     static constexpr bool kSlots = SINK == kStore && !Hash::kPack;
     static constexpr uint32_t kSlotB = kSlots ? kQueue * 2 : 0;
     static constexpr size_t kTabB = Hash::kHasCrc ? (Hash::kTableWords + kTile) * 4 : 0;
-    static constexpr size_t kHistB = SINK == kTargets ? kHistGroups * kHistBuckets * 4 : 0;
+    static constexpr size_t kHistB = is_targets(SINK) ? kHistGroups * kHistBucketsMax * 4 : 0;
     static constexpr size_t fixed = kQB /* alignment pad */ + kTabB + kHistB;
     static constexpr size_t per_warp = kQB + kStageB + kSlotB;
 };
@@ -194,7 +194,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
     // areas, i.e. the last kHistB bytes of the layout
     [[maybe_unused]] uint32_t *hist_s = reinterpret_cast<uint32_t *>(
         smem_raw + pad + (size_t)wpc * (L::kQB + L::kStageB + L::kSlotB) + L::kTabB);
-    if constexpr (SINK == kTargets)
+    if constexpr (is_targets(SINK))
         for (int b = threadIdx.x; b < kHistGroups * a.nb; b += blockDim.x) hist_s[b] = 0;
     __syncthreads();
 
@@ -213,7 +213,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
     const uint64_t nw = (uint64_t)gridDim.x * wpc;
 
     // NS chains per lane in phase 2 (independent probes for the scheduler)
-    constexpr int NS = SINK == kStore ? PARBA_ILP_STORE : SINK == kTargets ? PARBA_ILP_TARGETS : PARBA_ILP_STREAM;
+    constexpr int NS = SINK == kStore ? PARBA_ILP_STORE : is_targets(SINK) ? PARBA_ILP_TARGETS : PARBA_ILP_STREAM;
     uint32_t act[NS];               // 1: slot holds a running chain
     R r[NS];
     uint32_t saddr[NS];             // store: smem address of the chain's stage cell
@@ -291,37 +291,30 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
     [[maybe_unused]] uint32_t *wout = nullptr;
     [[maybe_unused]] uint32_t wcur = 0;
     [[maybe_unused]] uint32_t *hist_w = hist_s;  // this warp's group
-    if constexpr (SINK == kTargets) {
+    if constexpr (is_targets(SINK)) {
         wout = a.t32 + gw * a.capw;
         hist_w = hist_s + (uint32_t)(wib * kHistGroups / wpc) * a.nb;
     }
-    auto put_target = [&](uint32_t slot, uint64_t rv) {
-        const uint32_t tg = (uint32_t)target_of<NARROW, SEED, false, DEG>(rv, p);
-        wout[slot] = tg;
-        atomicAdd(hist_w + (tg >> a.shift), 1u);
-    };
-    [[maybe_unused]] uint32_t wstaged = 0;  // staged values (wcur = values written)
-    // stage ring -> targets, 32 (or, at the end, the rest) with every lane busy
-    auto drain_stage = [&](bool all) {
-        if constexpr (SINK == kTargets && PARBA_TARGET_STAGE) {
-            __syncwarp();
-            while (wstaged - wcur >= 32u || (all && wstaged != wcur)) {
-                const uint32_t j = wcur + lane;
-                if (j < wstaged) put_target(j, (uint64_t)lds_t<R>(stage_s + (j & 63u) * (uint32_t)sizeof(R)));
-                wcur = wstaged - wcur >= 32u ? wcur + 32u : wstaged;
-            }
-            __syncwarp();
-        }
-    };
+    // targets >= klim (full: n; window: the K lowest nodes) are dropped
     auto emit = [&](bool f, uint64_t rv) {
-        if constexpr (SINK == kTargets) {
-            const unsigned m = ballot_all(f);
-            if constexpr (PARBA_TARGET_STAGE) {
-                if (f) sts_t<R>(stage_s + ((wstaged + __popc(m & ltmask)) & 63u) * (uint32_t)sizeof(R), (R)rv);
-                wstaged += __popc(m);
-                if (wstaged - wcur >= 32u) drain_stage(false);
+        if constexpr (is_targets(SINK)) {
+            if constexpr (SINK == kTargets) {  // full histogram: every target is kept
+                const unsigned m = ballot_all(f);
+                if (f) {
+                    const uint32_t tg = (uint32_t)target_of<NARROW, SEED, false, DEG>(rv, p);
+                    wout[wcur + __popc(m & ltmask)] = tg;
+                    atomicAdd(hist_w + (tg >> a.shift), 1u);
+                }
+                wcur += __popc(m);
             } else {
-                if (f) put_target(wcur + __popc(m & ltmask), rv);
+                uint64_t tg = 0;
+                if (f) tg = target_of<NARROW, SEED, false, DEG>(rv, p);
+                const bool keep = f && tg < a.klim;
+                const unsigned m = ballot_all(keep);
+                if (keep) {
+                    wout[wcur + __popc(m & ltmask)] = (uint32_t)tg;
+                    atomicAdd(hist_w + ((uint32_t)tg >> a.shift), 1u);
+                }
                 wcur += __popc(m);
             }
         }
@@ -342,7 +335,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
             const uint32_t fin = act[q] & (cont ^ 1u);
             act[q] &= cont;
             r[q] = nr[q];
-            if constexpr (SINK == kTargets) {
+            if constexpr (is_targets(SINK)) {
                 emit(fin != 0, (uint64_t)nr[q]);
             } else if (fin) {
                 if constexpr (SINK == kStore) PARBA_CHECK(saddr[q] - stage_s < L::kStageB);
@@ -425,7 +418,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
             [[maybe_unused]] const uint32_t cell = stage_s + (buf * kTile + j) * (uint32_t)sizeof(R);
             if constexpr (SINK == kStore)  // final unless pending
                 sts_t<R>(cell, r1);
-            if constexpr (SINK == kTargets) emit(valid && done, (uint64_t)r1);
+            if constexpr (is_targets(SINK)) emit(valid && done, (uint64_t)r1);
             else if constexpr (SINK != kStore) if (valid && done) finish<NARROW, SEED, SINK, R, DEG>(0u, (uint64_t)r1, p, a);
             const bool pend = valid && !done;
             const unsigned m = ballot_all(pend);
@@ -517,8 +510,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
         step();
     }
     while (any_act()) step();
-    if constexpr (SINK == kTargets) {  // unused slots of the region: empty
-        drain_stage(true);
+    if constexpr (is_targets(SINK)) {  // unused slots of the region: empty
         PARBA_CHECK(wcur <= a.capw);
         for (uint64_t j = wcur + lane; j < a.capw; j += 32) wout[j] = 0xffffffffu;
         __syncthreads();

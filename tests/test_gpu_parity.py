@@ -375,13 +375,50 @@ def test_full_partitioned_random_ranges(monkeypatch):
         assert pp == pd and np.array_equal(part, direct), (kw, lo, hi)
 
 
-def test_full_partition_too_large_falls_back(monkeypatch):
-    # n > 2048 * 2^18: a bucket would span 16 slices -> direct atomics
+def test_full_partitioned_multi_pass(monkeypatch):
+    # n > 2048 * 2^18: 2289 buckets of 8 slices, scattered in two passes
     p = pb.GenParams(n=6 * 10**8, d=2)
     lo = p.m - (1 << 22)
     part, pp = _full_counts(p, lo, p.m, "partition", monkeypatch)
     direct, pd = _full_counts(p, lo, p.m, "direct", monkeypatch)
     assert pp == pd and np.array_equal(part, direct)
+
+
+def _window_counts(p, K, lo, hi, mode, monkeypatch):
+    import torch
+
+    monkeypatch.setenv("PARBA_FULL_MODE", mode)
+    counts = torch.zeros(K, dtype=torch.int64, device="cuda")
+    probes = torch.zeros(1, dtype=torch.int64, device="cuda")
+    pb.parallel.count_shard_device(p, K, lo, hi, counts=counts, probes=probes)
+    torch.cuda.synchronize()
+    return counts, int(probes.item())
+
+
+@pytest.mark.parametrize(
+    "case",
+    [
+        ("half_window", dict(n=10**6, d=8), 500_000, 777, -3),
+        ("seeded_degseq", dict(n=3 + _RAGGED_DEG.size, n0=3, degrees=_RAGGED_DEG, seed_edges=TRIANGLE), 150_000, 3, 0),
+        ("two_passes_u64", dict(n=10**9, d=10), 10**9, -(1 << 23), 0),
+        ("max_domain_2p31", dict(n=2**31 + 5, d=2), 2**31, -(1 << 22), 0),
+        ("beyond_domain_direct", dict(n=2**31 + 5, d=2), 2**31 + 1, -(1 << 22), 0),
+    ],
+    ids=lambda c: c[0],
+)
+def test_window_partitioned_equals_direct(case, monkeypatch):
+    """u64 degree windows through the partitioned pass (targets < K kept;
+    several scatter passes above 2048 buckets) equal the window kernel."""
+    import torch
+
+    _, kw, K, lo, hi = case
+    p = pb.GenParams(**kw)
+    lo = p.m + lo if lo < 0 else lo
+    hi = p.m + hi if hi <= 0 else hi
+    part, pp = _window_counts(p, K, lo, hi, "partition", monkeypatch)
+    direct, pd = _window_counts(p, K, lo, hi, "direct", monkeypatch)
+    assert pp == pd and torch.equal(part, direct)
+    del part, direct
 
 
 def test_window_large_range_sharding_independent():
