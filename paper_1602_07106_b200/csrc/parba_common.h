@@ -96,7 +96,8 @@ int launch_store(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint
 int win_rlim_deg(const parba_params_t *p, DevParams &dp, uint64_t K, cudaStream_t st);
 int boundary_node(const parba_params_t *p, const DevParams &dp, uint64_t pos, uint64_t *v, cudaStream_t st);
 int generate_nodes(const parba_params_t *p, const DevParams &dp, uint64_t vlo, uint64_t vhi, uint64_t lo,
-                   uint64_t hi, uint64_t *out, unsigned long long *probes, cudaStream_t st);
+                   uint64_t hi, uint64_t *out, unsigned long long *probes, cudaStream_t st,
+                   unsigned long long *fail_ext = nullptr);
 int count_nodes_u64(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi, uint64_t K,
                     unsigned long long *counts, unsigned long long *probes, cudaStream_t st);
 int count_nodes_u32(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi, uint64_t K,

@@ -347,6 +347,30 @@ node_kernel(DevParams p, NodeArgs na, uint64_t vlo, uint64_t vhi, uint64_t lo, u
     node_probes_flush(probes, probes_out);
 }
 
+// Degree counts under no_self_loops alone, fused: node v's dv edges all run
+// the chain from 2*first, so they add dv to v and dv to their common target
+// (both endpoints < K) -- two atomics per node, no edge rows in memory.
+template <bool DEG, typename CountT>
+__global__ void __launch_bounds__(256)
+node_count_kernel(DevParams p, NodeArgs na, uint64_t vlo, uint64_t vhi, uint64_t K, CountT *counts,
+                  unsigned long long *probes_out) {
+    PARBA_NODE_PROLOGUE;
+    for (uint64_t v = vlo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < vhi;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t first, dv;
+        node_span<DEG>(v, p, first, dv);
+        if (dv == 0) continue;
+        uint64_t pr = 0;
+        const Family f0{p.k0, p.k01, p.mult};
+        const uint64_t r = chain_family(tab, 2 * first, f0, simple, p.stop, pr);
+        probes += pr * dv;
+        const uint64_t t = target_of<false, true, false, DEG>(r, p);
+        if (v < K) atomicAdd(counts + v, (CountT)dv);
+        if (t < K) atomicAdd(counts + t, (CountT)dv);
+    }
+    node_probes_flush(probes, probes_out);
+}
+
 // no_parallel_edges for high-degree nodes: one thread per node with an
 // open-addressing set of its targets (and its no_self_loops memo) in global
 // scratch -- O(degree) per node instead of the scan's O(degree^2).  Node k of

@@ -172,8 +172,12 @@ int report_infeasible(const parba_params_t *p, const DevParams &dp, const uint64
 
 // Edges of nodes [vlo, vhi) (first edge lo) into out, honouring the flags;
 // synchronises st to report an infeasible node (InfeasibleTargetsError).
+// fail_ext: a caller-owned failing-edge word (atomicMin, initialised to
+// UINT64_MAX) that the caller reports once after several calls; otherwise
+// the failure is reported here (one device sync).
 int generate_nodes(const parba_params_t *p, const DevParams &dp, uint64_t vlo, uint64_t vhi, uint64_t lo,
-                   uint64_t hi, uint64_t *out, unsigned long long *probes, cudaStream_t st) {
+                   uint64_t hi, uint64_t *out, unsigned long long *probes, cudaStream_t st,
+                   unsigned long long *fail_ext) {
     if (vhi <= vlo) return PARBA_OK;
     NodeArgs na{};
     na.no_self_loops = (p->flags & PARBA_FLAG_NO_SELF_LOOPS) ? 1u : 0u;
@@ -192,9 +196,11 @@ int generate_nodes(const parba_params_t *p, const DevParams &dp, uint64_t vlo, u
         if (rc0) return rc0;
     }
     AsyncBuf fe, need;
-    int rc = fe.alloc(sizeof(unsigned long long), st);
-    if (rc) return rc;
-    CUDA_TRY(cudaMemsetAsync(fe.p, 0xFF, sizeof(unsigned long long), st));
+    int rc = PARBA_OK;
+    if (!fail_ext) {
+        if ((rc = fe.alloc(sizeof(unsigned long long), st))) return rc;
+        CUDA_TRY(cudaMemsetAsync(fe.p, 0xFF, sizeof(unsigned long long), st));
+    }
     const unsigned grid = grid_for(vhi - vlo, 256);
     if (na.pre0) {  // nodes whose attempt-0 targets are already distinct are final
         if ((rc = need.alloc(vhi - vlo, st))) return rc;
@@ -205,7 +211,7 @@ int generate_nodes(const parba_params_t *p, const DevParams &dp, uint64_t vlo, u
         CUDA_TRY(cudaGetLastError());
     }
     const uint64_t big = na.no_parallel_edges ? kBigDegree : UINT64_MAX;
-    unsigned long long *fep = (unsigned long long *)fe.p;
+    unsigned long long *fep = fail_ext ? fail_ext : (unsigned long long *)fe.p;
     const uint8_t *needp = (const uint8_t *)need.p;
     if (is_deg(p))
         node_kernel<true><<<grid, 256, 0, st>>>(dp, na, vlo, vhi, lo, hi - lo, (ulonglong2 *)out, probes, fep, big,
@@ -218,11 +224,14 @@ int generate_nodes(const parba_params_t *p, const DevParams &dp, uint64_t vlo, u
         rc = generate_big_nodes(p, dp, na, vlo, vhi, lo, hi, out, probes, fep, st);
         if (rc) return rc;
     }
-    return report_infeasible(p, dp, (const uint64_t *)fe.p, st);
+    return fail_ext ? PARBA_OK : report_infeasible(p, dp, (const uint64_t *)fe.p, st);
 }
 
 // Degree counts of [lo, hi) with option flags: node-aligned chunks generated
 // into scratch, then counted (both endpoints < K).
+#ifndef PARBA_COUNT_CHUNK_LG
+#define PARBA_COUNT_CHUNK_LG 26
+#endif
 template <typename CountT>
 int count_nodes(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi, uint64_t K,
                 CountT *counts, unsigned long long *probes, cudaStream_t st) {
@@ -230,35 +239,52 @@ int count_nodes(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint6
     int rc = boundary_node(p, dp, lo, &vlo, st);
     if (!rc) rc = boundary_node(p, dp, hi, &vhi, st);
     if (rc) return rc;
-    const uint64_t step = is_deg(p) ? (1ull << 20) : ((1ull << 24) / p->d > 0 ? (1ull << 24) / p->d : 1);
-    for (uint64_t v = vlo; v < vhi;) {
-        const uint64_t v1 = vhi - v > step ? v + step : vhi;
-        uint64_t a, b;
-        if (is_deg(p)) {
-            uint64_t w[2];
-            rc = read_u64s(p->degree_prefix + (v - p->n0), &w[0], 1, st);
-            if (!rc) rc = read_u64s(p->degree_prefix + (v1 - p->n0), &w[1], 1, st);
-            if (rc) return rc;
-            a = w[0];
-            b = w[1];
-        } else {
-            a = node_first_edge(p, v);
-            b = node_first_edge(p, v1);
-        }
-        if (b > a) {
-            AsyncBuf scratch;
-            rc = scratch.alloc((b - a) * 16, st);
-            if (!rc) rc = generate_nodes(p, dp, v, v1, a, b, (uint64_t *)scratch.p, probes, st);
-            if (rc) return rc;
-            if (K > 0) {
-                count_pairs_kernel<CountT><<<grid_for(b - a, 256), 256, 0, st>>>(
-                    (const ulonglong2 *)scratch.p, b - a, K, counts);
-                CUDA_TRY(cudaGetLastError());
-            }
-        }
-        v = v1;
+    if (vhi <= vlo) return PARBA_OK;
+    // node-aligned chunks of about 2^PARBA_COUNT_CHUNK_LG edges (16 B each in
+    // scratch); the chunks' first edges are read in one device sync and a
+    // failing edge is reported once at the end, so the chunks queue back to back
+    if (!(p->flags & PARBA_FLAG_NO_PARALLEL_EDGES)) {  // no_self_loops alone: fused, per node
+        NodeArgs na{};
+        na.no_self_loops = 1u;
+        na.simple = p->hash_kind == PARBA_HASH_SIMPLE ? 1u : 0u;
+        const unsigned grid = grid_for(vhi - vlo, 256);
+        if (is_deg(p))
+            node_count_kernel<true, CountT><<<grid, 256, 0, st>>>(dp, na, vlo, vhi, K, counts, probes);
+        else
+            node_count_kernel<false, CountT><<<grid, 256, 0, st>>>(dp, na, vlo, vhi, K, counts, probes);
+        CUDA_TRY(cudaGetLastError());
+        return PARBA_OK;
     }
-    return PARBA_OK;
+    const uint64_t ce = 1ull << PARBA_COUNT_CHUNK_LG;
+    const uint64_t step = is_deg(p) ? (ce >> 4) : (ce / p->d > 0 ? ce / p->d : 1);
+    const uint64_t nch = (vhi - vlo + step - 1) / step;
+    std::vector<uint64_t> first(nch + 1);
+    for (uint64_t c = 0; c <= nch; ++c) {
+        const uint64_t v = c < nch ? vlo + c * step : vhi;
+        if (is_deg(p))
+            CUDA_TRY(cudaMemcpyAsync(&first[c], p->degree_prefix + (v - p->n0), 8, cudaMemcpyDeviceToHost, st));
+        else
+            first[c] = node_first_edge(p, v);
+    }
+    if (is_deg(p)) CUDA_TRY(cudaStreamSynchronize(st));
+    AsyncBuf fe;
+    if ((rc = fe.alloc(sizeof(unsigned long long), st))) return rc;
+    CUDA_TRY(cudaMemsetAsync(fe.p, 0xFF, sizeof(unsigned long long), st));
+    unsigned long long *fep = (unsigned long long *)fe.p;
+    for (uint64_t c = 0; c < nch; ++c) {
+        const uint64_t v = vlo + c * step, v1 = c + 1 < nch ? v + step : vhi;
+        const uint64_t a = first[c], b = first[c + 1];
+        if (b <= a) continue;
+        AsyncBuf scratch;
+        if ((rc = scratch.alloc((b - a) * 16, st))) return rc;
+        if ((rc = generate_nodes(p, dp, v, v1, a, b, (uint64_t *)scratch.p, probes, st, fep))) return rc;
+        if (K > 0) {
+            count_pairs_kernel<CountT><<<grid_for(b - a, 256), 256, 0, st>>>((const ulonglong2 *)scratch.p, b - a,
+                                                                             K, counts);
+            CUDA_TRY(cudaGetLastError());
+        }
+    }
+    return report_infeasible(p, dp, (const uint64_t *)fe.p, st);
 }
 
 int count_nodes_u64(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi, uint64_t K,

@@ -369,3 +369,19 @@ def test_no_parallel_edges_high_degree_nodes_vs_oracle():
         O.count_block(want_c, seed)
         counter, st = pb.degree_counts(p)
         assert np.array_equal(counter.counts, want_c) and st.hash_probes == wp
+
+
+def test_no_self_loops_fused_counts_match_generated_edges():
+    """no_self_loops alone counts per node (node_count_kernel: dv added to the
+    node and to its one target) instead of materialising edge rows; windows
+    and full counts equal the histogram of the generated edges, probes too."""
+    rng = np.random.default_rng(77)
+    deg = rng.integers(0, 9, size=30_000).astype(np.uint64)
+    for p in (pb.GenParams(n=50_000, d=6, n0=3, seed_edges=TRIANGLE, no_self_loops=True),
+              pb.GenParams(n=3 + deg.size, n0=3, degrees=deg, seed_edges=TRIANGLE, no_self_loops=True)):
+        edges, probes = pb.generate_block(p.m0, p.m, p)
+        seed_hist = np.bincount(np.asarray(p.seed_edges, dtype=np.int64), minlength=p.n)
+        full = np.bincount(edges.astype(np.int64).ravel(), minlength=p.n) + seed_hist
+        for K in (p.n, 1000, 1):
+            counter, stats = pb.degree_counts(p, K=K) if K != p.n else pb.degree_counts(p)
+            assert np.array_equal(counter.counts, full[:K]) and stats.hash_probes == probes, K
