@@ -465,31 +465,27 @@ bool use_partitioned(const parba_params_t *p, uint64_t lo, uint64_t hi, uint64_t
     return hi - lo >= kHistMinEdges && K >= (1ull << 25);
 }
 
-template <typename CountT>
-int count_partitioned(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi, uint64_t K,
-                      CountT *counts, unsigned long long *probes, cudaStream_t st) {
-    DevInfo *di;
-    int rc = dev_info(&di);
-    if (rc) return rc;
-    const int shift = hist_shift(K);
-    const int nb = (int)((K + (1ull << shift) - 1) >> shift);
-    const int spb_lg = shift - kSliceLg;
-    const uint64_t batch = hi - lo < kHistBatch ? hi - lo : kHistBatch;
-    // a launch fills nw * ceil(ntiles / nw) * kTile slots, nw <= 64 warps per SM
-    const uint64_t cap = (batch / kTile + 2) * kTile + (uint64_t)di->sms * 64 * kTile;
-    const uint32_t nblk = (uint32_t)di->sms * 4 * kHistGroups;  // >= warp groups of one tile launch
-    const uint64_t max_items = nb + cap / kCountChunk + 1;
+// Scratch of one partitioned count: targets (t32), targets grouped by
+// bucket (srt), bucket x column histogram (H) and its exclusive scan (O),
+// CUB temp, count work items.
+struct PartScratch {
     AsyncBuf t32, srt, H, O, tmp, items;
-    if ((rc = t32.alloc(cap * 4, st)) || (rc = srt.alloc(cap * 4, st)) ||
-        (rc = H.alloc((size_t)nb * nblk * 4, st)) || (rc = O.alloc((size_t)nb * nblk * 4, st)) ||
-        (rc = items.alloc((max_items + 1) * 4, st)))
-        return rc;
-    uint32_t *n_items = (uint32_t *)items.p + max_items;
     size_t tmp_bytes = 0;
-    CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, (const uint32_t *)H.p, (uint32_t *)O.p,
-                                           (int64_t)nb * nblk, st));
-    if ((rc = tmp.alloc(tmp_bytes, st))) return rc;
-    {
+    uint64_t max_items = 0;
+    int shift = 0, nb = 0, spb_lg = 0;
+    int init(uint64_t K, uint64_t slots, uint32_t cols, cudaStream_t st) {
+        shift = hist_shift(K);
+        nb = (int)((K + (1ull << shift) - 1) >> shift);
+        spb_lg = shift - kSliceLg;
+        max_items = nb + slots / kCountChunk + 1;
+        int rc;
+        if ((rc = t32.alloc(slots * 4, st)) || (rc = srt.alloc(slots * 4, st)) ||
+            (rc = H.alloc((size_t)nb * cols * 4, st)) || (rc = O.alloc((size_t)nb * cols * 4, st)) ||
+            (rc = items.alloc((max_items + 1) * 4, st)))
+            return rc;
+        CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, (const uint32_t *)H.p, (uint32_t *)O.p,
+                                               (int64_t)nb * cols, st));
+        if ((rc = tmp.alloc(tmp_bytes, st))) return rc;
         std::lock_guard<std::mutex> lk(g_mu);
         static bool attr[64] = {};
         int dev = 0;
@@ -503,49 +499,111 @@ int count_partitioned(const parba_params_t *p, const DevParams &dp, uint64_t lo,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, kScatterSmem));
             attr[dev] = true;
         }
+        return PARBA_OK;
     }
+    // t32 / H filled for `cols` columns (column c: slots of warps
+    // [c / groups * wpc + (c % groups) * wpc / groups, ...) of capw each):
+    // scan, scatter passes, plan, slice counts
+    template <typename CountT>
+    int count(uint64_t len, uint64_t capw, uint32_t wpc, uint32_t groups, uint32_t cols, uint64_t K,
+              CountT *counts, cudaStream_t st) {
+        uint32_t *n_items = (uint32_t *)items.p + max_items;
+        CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, (const uint32_t *)H.p, (uint32_t *)O.p,
+                                               (int64_t)nb * cols, st));
+        for (int wb = 0; wb < nb; wb += kHistBuckets) {  // scatter passes
+            const int nbw = nb - wb < kHistBuckets ? nb - wb : kHistBuckets;
+            bucket_scatter_kernel<kScatterThreads><<<cols, kScatterThreads, kScatterSmem, st>>>(
+                (const uint32_t *)t32.p, len, wpc, groups, capw, shift, wb, nbw, (const uint32_t *)O.p,
+                (uint32_t *)srt.p);
+            CUDA_TRY(cudaGetLastError());
+        }
+        count_plan_kernel<<<1, kHistThreads, 0, st>>>((const uint32_t *)O.p, (const uint32_t *)H.p, cols, nb,
+                                                       (uint32_t *)items.p, n_items);
+        CUDA_TRY(cudaGetLastError());
+        const uint64_t items_ub = nb + len / kCountChunk + 1;  // >= sum of ceil(size_b / chunk)
+        slice_count_kernel<CountT><<<(unsigned)(items_ub << spb_lg), kHistThreads, kSliceNodes * 4, st>>>(
+            (const uint32_t *)srt.p, (const uint32_t *)O.p, (const uint32_t *)H.p, cols, nb,
+            (const uint32_t *)items.p, n_items, (uint32_t)K, shift, spb_lg, counts);
+        CUDA_TRY(cudaGetLastError());
+        return PARBA_OK;
+    }
+};
+
+template <typename CountT>
+int count_partitioned(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi, uint64_t K,
+                      CountT *counts, unsigned long long *probes, cudaStream_t st) {
+    DevInfo *di;
+    int rc = dev_info(&di);
+    if (rc) return rc;
+    const uint64_t batch = hi - lo < kHistBatch ? hi - lo : kHistBatch;
+    // a launch fills nw * ceil(ntiles / nw) * kTile slots, nw <= 64 warps per SM
+    const uint64_t cap = (batch / kTile + 2) * kTile + (uint64_t)di->sms * 64 * kTile;
+    const uint32_t nblk = (uint32_t)di->sms * 4 * kHistGroups;  // >= warp groups of one tile launch
+    PartScratch ps;
+    if ((rc = ps.init(K, cap, nblk, st))) return rc;
     for (uint64_t b0 = lo; b0 < hi;) {
         uint64_t b1 = hi - b0 > batch ? (b0 / kTile) * kTile + batch : hi;
         if (b1 > hi) b1 = hi;
         uint64_t geom[4] = {};
         SinkArgs a{};
-        a.t32 = (uint32_t *)t32.p;
-        a.hist = (uint32_t *)H.p;  // the tile launch writes the bucket histogram of each CTA's region
-        a.shift = shift;
-        a.nb = nb;
+        a.t32 = (uint32_t *)ps.t32.p;
+        a.hist = (uint32_t *)ps.H.p;  // the tile launch writes the bucket histogram of each CTA's region
+        a.shift = ps.shift;
+        a.nb = ps.nb;
         a.klim = K;
         a.t32_cap = cap;
         a.t32_geom = geom;
         rc = K >= p->n ? launch_tiles<kTargets>(p, dp, b0, b1, a, probes, st)
                        : launch_tiles<kTargetsK>(p, dp, b0, b1, a, probes, st);
         if (rc) return rc;
-        const uint64_t len = geom[0], capw = geom[1];
-        const uint32_t wpc = (uint32_t)geom[2], used = (uint32_t)geom[3] * kHistGroups;
+        const uint32_t used = (uint32_t)geom[3] * kHistGroups;
         if (used > nblk) return fail(PARBA_ECUDA, "targets launch wider than the histogram");
-        // H / O: bucket-major, stride `used` (one column per warp group)
-        CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, (const uint32_t *)H.p, (uint32_t *)O.p,
-                                               (int64_t)nb * used, st));
-        for (int wb = 0; wb < nb; wb += kHistBuckets) {  // scatter passes
-            const int nbw = nb - wb < kHistBuckets ? nb - wb : kHistBuckets;
-            bucket_scatter_kernel<kScatterThreads><<<used, kScatterThreads, kScatterSmem, st>>>(
-                (const uint32_t *)t32.p, len, wpc, kHistGroups, capw, shift, wb, nbw, (const uint32_t *)O.p,
-                (uint32_t *)srt.p);
-            CUDA_TRY(cudaGetLastError());
-        }
-        count_plan_kernel<<<1, kHistThreads, 0, st>>>((const uint32_t *)O.p, (const uint32_t *)H.p, used, nb,
-                                                       (uint32_t *)items.p, n_items);
-        CUDA_TRY(cudaGetLastError());
-        const uint64_t items_ub = nb + len / kCountChunk + 1;  // >= sum of ceil(size_b / chunk)
-        slice_count_kernel<CountT><<<(unsigned)(items_ub << spb_lg), kHistThreads, kSliceNodes * 4, st>>>(
-            (const uint32_t *)srt.p, (const uint32_t *)O.p, (const uint32_t *)H.p, used, nb,
-            (const uint32_t *)items.p, n_items, (uint32_t)K, shift, spb_lg, counts);
-        CUDA_TRY(cudaGetLastError());
+        if ((rc = ps.count<CountT>(geom[0], geom[1], (uint32_t)geom[2], kHistGroups, used, K, counts, st)))
+            return rc;
         b0 = b1;
     }
     return PARBA_OK;
 }
 
 }  // namespace
+
+namespace parba {
+namespace host {
+// Targets (.y) < K of edge rows already in memory, counted by the partitioned
+// pass (sources are the caller's); returns PARBA_EINVAL-free false via *done
+// when the pass does not apply (the caller counts directly).
+template <typename CountT>
+int count_rows_partitioned_t(const ulonglong2 *rows, uint64_t n_rows, uint64_t K, CountT *counts, bool *done,
+                             cudaStream_t st) {
+    *done = false;
+    const char *e = getenv("PARBA_FULL_MODE");
+    const int mode = !e ? 0 : strcmp(e, "direct") == 0 ? 1 : strcmp(e, "partition") == 0 ? 2 : 0;
+    if (K == 0 || K >= kEmptyTarget || !hist_shift(K) || n_rows == 0) return PARBA_OK;
+    if (mode == 1 || (mode == 0 && (K < (1ull << 25) || n_rows < kHistMinEdges))) return PARBA_OK;
+    DevInfo *di;
+    int rc = dev_info(&di);
+    if (rc) return rc;
+    const uint32_t cols = (uint32_t)di->sms * 2;
+    const uint64_t span = (n_rows + cols - 1) / cols + 255 & ~255ull;  // 256-slot multiple
+    PartScratch ps;
+    if ((rc = ps.init(K, span * cols, cols, st))) return rc;
+    rows_targets_kernel<<<cols, 1024, 0, st>>>(rows, n_rows, span, K, ps.shift, ps.nb, (uint32_t *)ps.t32.p,
+                                               (uint32_t *)ps.H.p);
+    CUDA_TRY(cudaGetLastError());
+    if ((rc = ps.count<CountT>(span * cols, span, 1, 1, cols, K, counts, st))) return rc;
+    *done = true;
+    return PARBA_OK;
+}
+int count_rows_partitioned(const ulonglong2 *rows, uint64_t n_rows, uint64_t K, uint32_t *counts, bool *done,
+                           cudaStream_t st) {
+    return count_rows_partitioned_t<uint32_t>(rows, n_rows, K, counts, done, st);
+}
+int count_rows_partitioned(const ulonglong2 *rows, uint64_t n_rows, uint64_t K, unsigned long long *counts,
+                           bool *done, cudaStream_t st) {
+    return count_rows_partitioned_t<unsigned long long>(rows, n_rows, K, counts, done, st);
+}
+}  // namespace host
+}  // namespace parba
 
 extern "C" {
 

@@ -95,6 +95,10 @@ int launch_store(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint
 // Node-granular paths (parba_nodes_api.cu): option flags and degree sequences.
 int win_rlim_deg(const parba_params_t *p, DevParams &dp, uint64_t K, cudaStream_t st);
 int boundary_node(const parba_params_t *p, const DevParams &dp, uint64_t pos, uint64_t *v, cudaStream_t st);
+int count_rows_partitioned(const ulonglong2 *rows, uint64_t n_rows, uint64_t K, uint32_t *counts, bool *done,
+                           cudaStream_t st);
+int count_rows_partitioned(const ulonglong2 *rows, uint64_t n_rows, uint64_t K, unsigned long long *counts,
+                           bool *done, cudaStream_t st);
 int generate_nodes(const parba_params_t *p, const DevParams &dp, uint64_t vlo, uint64_t vhi, uint64_t lo,
                    uint64_t hi, uint64_t *out, unsigned long long *probes, cudaStream_t st,
                    unsigned long long *fail_ext = nullptr);

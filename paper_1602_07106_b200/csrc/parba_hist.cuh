@@ -46,6 +46,33 @@ __device__ __forceinline__ uint4 ld_stream4(const uint4 *p) {
     return v;
 }
 
+// Generic input (edge rows already in memory, e.g. the option-flag paths):
+// CTA c copies the targets (.y) of rows [c * span, (c + 1) * span) that are
+// < K into slots of the same index (others and slots past n_rows: empty)
+// and writes its bucket histogram H[b * gridDim.x + c] -- the layout the
+// targets sink produces, with one warp group per CTA.
+__global__ void __launch_bounds__(1024) rows_targets_kernel(const ulonglong2 *__restrict__ rows, uint64_t n_rows,
+                                                            uint64_t span, uint64_t K, int shift, int nb,
+                                                            uint32_t *__restrict__ t32, uint32_t *__restrict__ H) {
+    __shared__ uint32_t h[kHistBucketsMax];
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) h[b] = 0;
+    __syncthreads();
+    const uint64_t s0 = (uint64_t)blockIdx.x * span;
+    for (uint64_t k = s0 + threadIdx.x; k < s0 + span; k += blockDim.x) {
+        uint32_t v = kEmptyTarget;
+        if (k < n_rows) {
+            const uint64_t tg = __ldg(&rows[k].y);
+            if (tg < K) {
+                v = (uint32_t)tg;
+                atomicAdd(&h[v >> shift], 1u);
+            }
+        }
+        t32[k] = v;
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) H[(uint64_t)b * gridDim.x + blockIdx.x] = h[b];
+}
+
 // Block-wide exclusive scan of x (one value per thread, <= 1024 threads).
 __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t x, uint32_t *warp_sums) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;

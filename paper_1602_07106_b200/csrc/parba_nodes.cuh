@@ -371,6 +371,17 @@ node_count_kernel(DevParams p, NodeArgs na, uint64_t vlo, uint64_t vhi, uint64_t
     node_probes_flush(probes, probes_out);
 }
 
+// Source endpoints of nodes [vlo, vhi) (all their edges): counts[v] += dv.
+template <bool DEG, typename CountT>
+__global__ void node_sources_kernel(DevParams p, uint64_t vlo, uint64_t vhi, CountT *counts) {
+    for (uint64_t v = vlo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < vhi;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t first, dv;
+        node_span<DEG>(v, p, first, dv);
+        if (dv) counts[v] += (CountT)dv;
+    }
+}
+
 // no_parallel_edges for high-degree nodes: one thread per node with an
 // open-addressing set of its targets (and its no_self_loops memo) in global
 // scratch -- O(degree) per node instead of the scan's O(degree^2).  Node k of

@@ -278,7 +278,20 @@ int count_nodes(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint6
         AsyncBuf scratch;
         if ((rc = scratch.alloc((b - a) * 16, st))) return rc;
         if ((rc = generate_nodes(p, dp, v, v1, a, b, (uint64_t *)scratch.p, probes, st, fep))) return rc;
-        if (K > 0) {
+        if (K == 0) continue;
+        // large K: targets through the partitioned count, sources per node
+        bool done = false;
+        if ((rc = count_rows_partitioned((const ulonglong2 *)scratch.p, b - a, K, counts, &done, st))) return rc;
+        if (done) {
+            const uint64_t s1 = v1 < K ? v1 : K;
+            if (v < s1) {
+                if (is_deg(p))
+                    node_sources_kernel<true, CountT><<<grid_for(s1 - v, 256), 256, 0, st>>>(dp, v, s1, counts);
+                else
+                    node_sources_kernel<false, CountT><<<grid_for(s1 - v, 256), 256, 0, st>>>(dp, v, s1, counts);
+                CUDA_TRY(cudaGetLastError());
+            }
+        } else {
             count_pairs_kernel<CountT><<<grid_for(b - a, 256), 256, 0, st>>>((const ulonglong2 *)scratch.p, b - a,
                                                                              K, counts);
             CUDA_TRY(cudaGetLastError());

@@ -385,3 +385,23 @@ def test_no_self_loops_fused_counts_match_generated_edges():
         for K in (p.n, 1000, 1):
             counter, stats = pb.degree_counts(p, K=K) if K != p.n else pb.degree_counts(p)
             assert np.array_equal(counter.counts, full[:K]) and stats.hash_probes == probes, K
+
+
+@pytest.mark.parametrize("K", [None, 4000])
+def test_no_parallel_edges_counts_partitioned_equals_direct(K, monkeypatch):
+    """no_parallel_edges counts from the materialised edge rows: targets
+    through the partitioned pass (rows_targets_kernel + scatter + slice
+    counts), sources per node, equal to the direct count_pairs_kernel."""
+    deg = np.random.default_rng(5).integers(0, 7, size=40_000).astype(np.uint64)
+    seed = np.array([x for a in range(8) for b in range(a + 1, 8) for x in (a, b)], dtype=np.uint64)
+    for p in (pb.GenParams(n=60_000, d=5, n0=8, seed_edges=seed, no_parallel_edges=True),
+              pb.GenParams(n=8 + deg.size, n0=8, degrees=deg, seed_edges=seed, no_parallel_edges=True,
+                           no_self_loops=True)):
+        kk = p.n if K is None else K
+        got = {}
+        for mode in ("partition", "direct"):
+            monkeypatch.setenv("PARBA_FULL_MODE", mode)
+            counter, stats = pb.degree_counts(p, K=kk) if K else pb.degree_counts(p)
+            got[mode] = (counter.counts.copy(), stats.hash_probes)
+        assert np.array_equal(got["partition"][0], got["direct"][0])
+        assert got["partition"][1] == got["direct"][1]
