@@ -101,6 +101,33 @@ __device__ __forceinline__ uint64_t upper_bound_m1(const uint64_t *W, uint64_t l
     return lo - 1;
 }
 
+// Degree-sequence chunking by edges: out[2k] = the first node v in
+// [vlo, vhi] with W[v - n0] >= e0 + k * ce (k <= nch; the last is vhi),
+// out[2k + 1] = W[v - n0].
+__global__ void deg_chunk_bounds_kernel(const uint64_t *__restrict__ W, uint64_t n0, uint64_t vlo, uint64_t vhi,
+                                        uint64_t e0, uint64_t ce, uint64_t nch, uint64_t *out) {
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k <= nch;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t v;
+        if (k == 0) {
+            v = vlo;
+        } else if (k == nch) {
+            v = vhi;
+        } else {  // lower bound: first index with W >= e
+            const uint64_t e = e0 + k * ce;
+            uint64_t lo = vlo - n0, hi = vhi - n0;
+            while (lo < hi) {
+                const uint64_t mid = lo + (hi - lo) / 2;
+                if (__ldg(W + mid) < e) lo = mid + 1;
+                else hi = mid;
+            }
+            v = lo + n0;
+        }
+        out[2 * k] = v;
+        out[2 * k + 1] = __ldg(W + (v - n0));
+    }
+}
+
 __global__ void node_of_bisect_kernel(DevParams p, const uint64_t *__restrict__ es, uint64_t count,
                                       uint64_t n_nodes, uint64_t *out) {
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count;

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -240,9 +241,6 @@ int count_nodes(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint6
     if (!rc) rc = boundary_node(p, dp, hi, &vhi, st);
     if (rc) return rc;
     if (vhi <= vlo) return PARBA_OK;
-    // node-aligned chunks of about 2^PARBA_COUNT_CHUNK_LG edges (16 B each in
-    // scratch); the chunks' first edges are read in one device sync and a
-    // failing edge is reported once at the end, so the chunks queue back to back
     if (!(p->flags & PARBA_FLAG_NO_PARALLEL_EDGES)) {  // no_self_loops alone: fused, per node
         NodeArgs na{};
         na.no_self_loops = 1u;
@@ -255,25 +253,45 @@ int count_nodes(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint6
         CUDA_TRY(cudaGetLastError());
         return PARBA_OK;
     }
-    const uint64_t ce = 1ull << PARBA_COUNT_CHUNK_LG;
-    const uint64_t step = is_deg(p) ? (ce >> 4) : (ce / p->d > 0 ? ce / p->d : 1);
-    const uint64_t nch = (vhi - vlo + step - 1) / step;
-    std::vector<uint64_t> first(nch + 1);
-    for (uint64_t c = 0; c <= nch; ++c) {
-        const uint64_t v = c < nch ? vlo + c * step : vhi;
-        if (is_deg(p))
-            CUDA_TRY(cudaMemcpyAsync(&first[c], p->degree_prefix + (v - p->n0), 8, cudaMemcpyDeviceToHost, st));
-        else
-            first[c] = node_first_edge(p, v);
+    // node-aligned chunks of about 2^PARBA_COUNT_CHUNK_LG edges (16 B each in
+    // scratch); the chunk bounds cost at most one device sync and a failing
+    // edge is reported once at the end, so the chunks queue back to back.
+    // Chunk c: nodes [bv[c], bv[c + 1]), edges [be[c], be[c + 1]).
+    uint64_t ce = 1ull << PARBA_COUNT_CHUNK_LG;
+    if (const char *e = getenv("PARBA_COUNT_CHUNK_EDGES")) {  // tests: many small chunks
+        const unsigned long long x = strtoull(e, nullptr, 10);
+        if (x > 0) ce = x;
     }
-    if (is_deg(p)) CUDA_TRY(cudaStreamSynchronize(st));
+    std::vector<uint64_t> bv, be;
+    if (is_deg(p)) {  // cut by edges: lower bounds of lo + k * ce in W, one sync
+        const uint64_t nch = (hi - lo + ce - 1) / ce;
+        AsyncBuf bnd;
+        if ((rc = bnd.alloc((nch + 1) * 16, st))) return rc;
+        deg_chunk_bounds_kernel<<<grid_for(nch + 1, 256), 256, 0, st>>>(p->degree_prefix, p->n0, vlo, vhi, lo, ce,
+                                                                        nch, (uint64_t *)bnd.p);
+        CUDA_TRY(cudaGetLastError());
+        std::vector<uint64_t> h(2 * (nch + 1));
+        if ((rc = read_u64s((const uint64_t *)bnd.p, h.data(), h.size(), st))) return rc;
+        for (uint64_t k = 0; k <= nch; ++k)
+            if (bv.empty() || h[2 * k] > bv.back()) {
+                bv.push_back(h[2 * k]);
+                be.push_back(h[2 * k + 1]);
+            }
+    } else {
+        const uint64_t step = ce / p->d > 0 ? ce / p->d : 1;
+        for (uint64_t v = vlo;; v = v + step < vhi ? v + step : vhi) {
+            bv.push_back(v);
+            be.push_back(node_first_edge(p, v));
+            if (v == vhi) break;
+        }
+    }
     AsyncBuf fe;
     if ((rc = fe.alloc(sizeof(unsigned long long), st))) return rc;
     CUDA_TRY(cudaMemsetAsync(fe.p, 0xFF, sizeof(unsigned long long), st));
     unsigned long long *fep = (unsigned long long *)fe.p;
-    for (uint64_t c = 0; c < nch; ++c) {
-        const uint64_t v = vlo + c * step, v1 = c + 1 < nch ? v + step : vhi;
-        const uint64_t a = first[c], b = first[c + 1];
+    for (size_t c = 0; c + 1 < bv.size(); ++c) {
+        const uint64_t v = bv[c], v1 = bv[c + 1];
+        const uint64_t a = be[c], b = be[c + 1];
         if (b <= a) continue;
         AsyncBuf scratch;
         if ((rc = scratch.alloc((b - a) * 16, st))) return rc;

@@ -405,3 +405,19 @@ def test_no_parallel_edges_counts_partitioned_equals_direct(K, monkeypatch):
             got[mode] = (counter.counts.copy(), stats.hash_probes)
         assert np.array_equal(got["partition"][0], got["direct"][0])
         assert got["partition"][1] == got["direct"][1]
+
+
+def test_flag_counts_small_chunks_equal_one_chunk(monkeypatch):
+    """Option-flag counts cut into many node-aligned chunks (degree sequence:
+    chunk bounds by edge lower bounds in W, zero-degree nodes included) equal
+    the single-chunk counts, probes included."""
+    deg = np.random.default_rng(11).integers(0, 9, size=20_000).astype(np.uint64)
+    deg[::7] = 0
+    seed = np.array([x for a in range(9) for b in range(a + 1, 9) for x in (a, b)], dtype=np.uint64)
+    for p in (pb.GenParams(n=9 + deg.size, n0=9, degrees=deg, seed_edges=seed, no_parallel_edges=True),
+              pb.GenParams(n=20_000, d=7, n0=9, seed_edges=seed, no_parallel_edges=True, no_self_loops=True)):
+        whole, wp = pb.degree_counts(p)
+        monkeypatch.setenv("PARBA_COUNT_CHUNK_EDGES", "1001")
+        parts, pp = pb.degree_counts(p)
+        monkeypatch.delenv("PARBA_COUNT_CHUNK_EDGES")
+        assert np.array_equal(whole.counts, parts.counts) and wp.hash_probes == pp.hash_probes
