@@ -352,6 +352,28 @@ __device__ __forceinline__ void build_chunk_tables(uint32_t *tab, int nc, uint32
     }
 }
 
+// Seed-free chunk tables (k0 = 0) by CRC linearity: crc(0, x << s) is the
+// XOR of crc(0, 1 << (s + j)) over the set bits j of x, so the 64 single-bit
+// values are computed once (bitwise) and every entry costs <= 11 XORs -- for
+// kernels with many short-lived CTAs.  bits: 64 words of shared scratch.
+__device__ __forceinline__ void build_chunk_tables_linear(uint32_t *tab, int nc, uint32_t *bits) {
+    if (threadIdx.x < 64) bits[threadIdx.x] = crc32c_u64_bitwise(0u, 1ull << threadIdx.x);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nc * 2048; e += blockDim.x) {
+        const int k = e >> 11;
+        uint32_t x = (uint32_t)(e & 2047), v = 0;
+        if (x < (1u << chunk_width(k))) {
+            const uint32_t *bk = bits + chunk_shift(k);
+            while (x) {
+                const int j = __ffs(x) - 1;
+                v ^= bk[j];
+                x &= x - 1;
+            }
+        }
+        tab[e] = v;
+    }
+}
+
 // Shared-space (32-bit) addressing: the tables are reached through a
 // shared-window address kept in a register, so the compiler does not
 // rematerialise the generic->shared conversion inside the loop.

@@ -213,11 +213,29 @@ __device__ __forceinline__ Family family_of(uint64_t attempt, const DevParams &p
     return f;
 }
 
-// h(r) under family f; tab = seed-free byte tables (crc(0, .)).
+// h(r) under family f; tab = seed-free CRC tables (crc(0, .)): byte tables
+// (8 KB; PARBA_NODE_CHUNKS=1: 5 chunk tables, 42 KB, measured 2x slower for
+// both flags -- fewer resident CTAs), remainder on the FP64 pipe (mod_fp,
+// exact for r < 2^52; the node paths require m <= 2^51; 20% faster than the
+// integer-corrected mod_int for both flags).
+#ifndef PARBA_NODE_CHUNKS
+#define PARBA_NODE_CHUNKS 0
+#endif
+#ifndef PARBA_NODE_MODFP
+#define PARBA_NODE_MODFP 1
+#endif
 __device__ __forceinline__ uint64_t hash_family(uint32_t tab, uint64_t r, const Family &f, bool simple) {
     if (simple) return __umul64hi(r * f.mult, r);
+#if PARBA_NODE_CHUNKS
+    const uint32_t c0 = crc_chunks<5>(tab, r) ^ f.k0;
+#else
     const uint32_t c0 = crc_bytes<8>(tab, r) ^ f.k0;
+#endif
+#if PARBA_NODE_MODFP
+    return mod_fp<uint64_t>(c0, c0 ^ f.k01, __ull2double_rn(r));
+#else
     return mod_int(c0, c0 ^ f.k01, r);
+#endif
 }
 
 // resolve_chain (generator.py:139-154): body at least once.
@@ -310,11 +328,20 @@ __device__ __forceinline__ bool node_npe(uint64_t v, uint64_t first, uint64_t dv
     return true;
 }
 
-// Node-kernel prologue: seed-free CRC byte tables and the retry families.
-#define PARBA_NODE_PROLOGUE                                                                \
+// Node-kernel prologue: seed-free CRC chunk tables and the retry families.
+#if PARBA_NODE_CHUNKS
+#define PARBA_NODE_TABLES                                                                  \
+    __shared__ uint32_t tabs_p[5 * 2048];                                                  \
+    __shared__ uint32_t tab_bits[64];                                                      \
+    build_chunk_tables_linear(tabs_p, 5, tab_bits)
+#else
+#define PARBA_NODE_TABLES                                                                  \
     __shared__ uint32_t tabs_p[8 * 256];                                                   \
+    build_byte_tables(tabs_p, 8, 0u)
+#endif
+#define PARBA_NODE_PROLOGUE                                                                \
+    PARBA_NODE_TABLES;                                                                     \
     __shared__ Family fams[kFamilies];                                                     \
-    build_byte_tables(tabs_p, 8, 0u);                                                      \
     if (na.no_parallel_edges)                                                              \
         for (int a_ = threadIdx.x; a_ < kFamilies; a_ += blockDim.x) fams[a_] = family_of(a_, p, na); \
     __syncthreads();                                                                       \

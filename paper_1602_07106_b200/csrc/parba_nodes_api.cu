@@ -78,6 +78,10 @@ int boundary_node(const parba_params_t *p, const DevParams &dp, uint64_t pos, ui
 }
 
 
+// The node kernels hash chain values < 2m with 5 chunk tables and the FP64
+// remainder (hash_family): every value must stay below 2^52.
+constexpr uint64_t kNodeMaxEdges = 1ull << 51;
+
 // no_parallel_edges nodes of degree > kBigDegree: node_big_kernel with a
 // per-node hash set in scratch, in chunks of at most kBigScratchWords words.
 constexpr uint64_t kBigScratchWords = 1ull << 27;  // 1 GiB per chunk
@@ -180,6 +184,8 @@ int generate_nodes(const parba_params_t *p, const DevParams &dp, uint64_t vlo, u
                    uint64_t hi, uint64_t *out, unsigned long long *probes, cudaStream_t st,
                    unsigned long long *fail_ext) {
     if (vhi <= vlo) return PARBA_OK;
+    if (p->m > kNodeMaxEdges) return fail(PARBA_EINVAL, "option flags support m <= 2^51 edges (m = %llu)",
+                                          (unsigned long long)p->m);
     NodeArgs na{};
     na.no_self_loops = (p->flags & PARBA_FLAG_NO_SELF_LOOPS) ? 1u : 0u;
     na.no_parallel_edges = (p->flags & PARBA_FLAG_NO_PARALLEL_EDGES) ? 1u : 0u;
@@ -236,6 +242,8 @@ int generate_nodes(const parba_params_t *p, const DevParams &dp, uint64_t vlo, u
 template <typename CountT>
 int count_nodes(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi, uint64_t K,
                 CountT *counts, unsigned long long *probes, cudaStream_t st) {
+    if (p->m > kNodeMaxEdges) return fail(PARBA_EINVAL, "option flags support m <= 2^51 edges (m = %llu)",
+                                          (unsigned long long)p->m);
     uint64_t vlo, vhi;
     int rc = boundary_node(p, dp, lo, &vlo, st);
     if (!rc) rc = boundary_node(p, dp, hi, &vhi, st);
