@@ -421,3 +421,12 @@ def test_flag_counts_small_chunks_equal_one_chunk(monkeypatch):
         parts, pp = pb.degree_counts(p)
         monkeypatch.delenv("PARBA_COUNT_CHUNK_EDGES")
         assert np.array_equal(whole.counts, parts.counts) and wp.hash_probes == pp.hash_probes
+
+
+def test_option_flags_reject_beyond_2p51_edges():
+    # the node kernels' FP64 remainder needs chain values < 2^52: m <= 2^51
+    p = pb.GenParams(n=1 << 40, d=1 << 12, n0=3, seed_edges=TRIANGLE, no_self_loops=True)
+    assert p.m > 1 << 51
+    lo = p.m0 + (p.n - p.n0 - 1) * p.d
+    with pytest.raises(pb.ParameterError, match="2\\^51"):
+        pb.generate_block(lo, lo + p.d, p)
