@@ -375,6 +375,26 @@ def test_full_partitioned_random_ranges(monkeypatch):
         assert pp == pd and np.array_equal(part, direct), (kw, lo, hi)
 
 
+def test_partitioned_counts_accumulate(monkeypatch):
+    """parba_degree_full / parba_degree_window add into the caller's counts
+    (+=, the reference's Consumer.merge) on the partitioned path too."""
+    import torch
+
+    monkeypatch.setenv("PARBA_FULL_MODE", "partition")
+    p = pb.GenParams(n=300_000, d=9)
+    lo, hi = 1000, p.m - 1000
+    once, _ = pb.parallel.count_shard_device(p, p.n, lo, hi)
+    pre = torch.arange(p.n, dtype=torch.int32, device="cuda") % 7
+    acc, _ = pb.parallel.count_shard_device(p, p.n, lo, hi, counts=pre.clone())
+    assert torch.equal(acc, once + pre)
+    K = 200_000
+    w_once, _ = _window_counts(p, K, lo, hi, "partition", monkeypatch)
+    base = torch.arange(K, dtype=torch.int64, device="cuda")
+    probes = torch.zeros(1, dtype=torch.int64, device="cuda")
+    w_acc, _ = pb.parallel.count_shard_device(p, K, lo, hi, counts=base.clone(), probes=probes)
+    assert torch.equal(w_acc, w_once + base)
+
+
 def test_full_partitioned_multi_pass(monkeypatch):
     # n > 2048 * 2^18: 2289 buckets of 8 slices, scattered in two passes
     p = pb.GenParams(n=6 * 10**8, d=2)
