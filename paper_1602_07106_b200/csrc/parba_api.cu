@@ -458,7 +458,7 @@ bool use_partitioned(const parba_params_t *p, uint64_t lo, uint64_t hi, uint64_t
     // PARBA_FULL_MODE = "direct" / "partition" (tests, A/B)
     const char *e = getenv("PARBA_FULL_MODE");
     const int mode = !e ? 0 : strcmp(e, "direct") == 0 ? 1 : strcmp(e, "partition") == 0 ? 2 : 0;
-    if (p->flags || K == 0 || K >= kEmptyTarget || p->n >= kEmptyTarget) return false;
+    if (p->flags || K == 0 || K >= kEmptyTarget) return false;  // targets >= K are never stored
     if (!hist_shift(K)) return false;
     if (mode) return mode == 2;
     // an L2-resident count array (K < 2^25 words) absorbs direct atomics as fast

@@ -423,6 +423,7 @@ def _window_counts(p, K, lo, hi, mode, monkeypatch):
         ("two_passes_u64", dict(n=10**9, d=10), 10**9, -(1 << 23), 0),
         ("max_domain_2p31", dict(n=2**31 + 5, d=2), 2**31, -(1 << 22), 0),
         ("beyond_domain_direct", dict(n=2**31 + 5, d=2), 2**31 + 1, -(1 << 22), 0),
+        ("n_above_2p32", dict(n=6 * 10**9, d=2), 10**8, -(1 << 22), 0),
     ],
     ids=lambda c: c[0],
 )
