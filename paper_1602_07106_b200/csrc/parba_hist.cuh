@@ -143,8 +143,11 @@ __global__ void __launch_bounds__(T, 1) bucket_scatter_kernel(const uint32_t *__
         }
     };
     load(s0);
+    for (int b = threadIdx.x; b < kHistBuckets; b += T) cnt[b] = 0;
+    __syncthreads();
+    // five barriers per sub-tile: every shared array is rewritten only after
+    // a barrier that its previous readers must have passed
     for (uint64_t base = s0; base < s1; base += kScatterTile) {
-        for (int b = threadIdx.x; b < kHistBuckets; b += T) cnt[b] = 0;
         uint32_t v[PER], rk[PER];
 #pragma unroll
         for (int h = 0; h < PER / 4; ++h) {
@@ -154,7 +157,6 @@ __global__ void __launch_bounds__(T, 1) bucket_scatter_kernel(const uint32_t *__
             v[4 * h + 3] = nx[h].w;
         }
         load(base + kScatterTile);
-        __syncthreads();
 #pragma unroll
         for (int k = 0; k < PER; ++k)
             if (v[k] != kEmptyTarget && wbucket(v[k]) < (uint32_t)nbw) rk[k] = atomicAdd(&cnt[wbucket(v[k])], 1u);
@@ -163,6 +165,7 @@ __global__ void __launch_bounds__(T, 1) bucket_scatter_kernel(const uint32_t *__
 #pragma unroll
         for (int i = 0; i < BPT; ++i) {
             cb[i] = cnt[threadIdx.x * BPT + i];
+            cnt[threadIdx.x * BPT + i] = 0;  // ready for the next sub-tile
             sum += cb[i];
         }
         uint32_t ex = block_exclusive_scan(sum, warp_sums);
@@ -187,7 +190,6 @@ __global__ void __launch_bounds__(T, 1) bucket_scatter_kernel(const uint32_t *__
             PARBA_CHECK(delta[b] + k < len);
             out[delta[b] + k] = x;
         }
-        __syncthreads();
     }
 }
 
