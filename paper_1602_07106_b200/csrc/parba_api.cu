@@ -298,7 +298,7 @@ namespace {  // partitioned degree counts, defined below the first C block
 bool use_partitioned(const parba_params_t *p, uint64_t lo, uint64_t hi, uint64_t K);
 template <typename CountT>
 int count_partitioned(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi, uint64_t K,
-                      CountT *counts, unsigned long long *probes, cudaStream_t st);
+                      CountT *counts, unsigned long long *probes, cudaStream_t st, bool by_pos = false);
 }  // namespace
 
 extern "C" {
@@ -454,6 +454,15 @@ int hist_shift(uint64_t K) {
     return ((K + (1ull << shift) - 1) >> shift) <= (uint64_t)kHistBucketsMax ? shift : 0;
 }
 
+// The position pass (PARBA_POS_MODE=1) measured slower than resolving owners
+// in the targets pass (f4 full, n=1e8, m=1.29e9: 2.13e10 vs 3.35e10 edges/s:
+// the position domain is 13x the node domain -- 3 scatter passes, 8 slices
+// per bucket, and the whole dense map read per batch), so it is opt-in.
+bool pos_mode_enabled() {
+    const char *e = getenv("PARBA_POS_MODE");
+    return e && strcmp(e, "1") == 0;
+}
+
 bool use_partitioned(const parba_params_t *p, uint64_t lo, uint64_t hi, uint64_t K) {
     // PARBA_FULL_MODE = "direct" / "partition" (tests, A/B)
     const char *e = getenv("PARBA_FULL_MODE");
@@ -495,6 +504,8 @@ struct PartScratch {
                                           kSliceNodes * 4));
             CUDA_TRY(cudaFuncSetAttribute(slice_count_kernel<unsigned long long>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, kSliceNodes * 4));
+            CUDA_TRY(cudaFuncSetAttribute(slice_count_pos_kernel<uint32_t>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kSliceNodes * 4));
             CUDA_TRY(cudaFuncSetAttribute(bucket_scatter_kernel<kScatterThreads>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, kScatterSmem));
             attr[dev] = true;
@@ -504,9 +515,11 @@ struct PartScratch {
     // t32 / H filled for `cols` columns (column c: slots of warps
     // [c / groups * wpc + (c % groups) * wpc / groups, ...) of capw each):
     // scan, scatter passes, plan, slice counts
+    // dense != nullptr: the domain is positions [m0, m) of a degree sequence,
+    // counted into their owners (slice_count_pos_kernel)
     template <typename CountT>
     int count(uint64_t len, uint64_t capw, uint32_t wpc, uint32_t groups, uint32_t cols, uint64_t K,
-              CountT *counts, cudaStream_t st) {
+              CountT *counts, cudaStream_t st, const uint32_t *dense = nullptr, uint64_t m0 = 0) {
         uint32_t *n_items = (uint32_t *)items.p + max_items;
         CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, (const uint32_t *)H.p, (uint32_t *)O.p,
                                                (int64_t)nb * cols, st));
@@ -521,17 +534,26 @@ struct PartScratch {
                                                        (uint32_t *)items.p, n_items);
         CUDA_TRY(cudaGetLastError());
         const uint64_t items_ub = nb + len / kCountChunk + 1;  // >= sum of ceil(size_b / chunk)
-        slice_count_kernel<CountT><<<(unsigned)(items_ub << spb_lg), kHistThreads, kSliceNodes * 4, st>>>(
-            (const uint32_t *)srt.p, (const uint32_t *)O.p, (const uint32_t *)H.p, cols, nb,
-            (const uint32_t *)items.p, n_items, (uint32_t)K, shift, spb_lg, counts);
+        if (dense)
+            slice_count_pos_kernel<CountT><<<(unsigned)(items_ub << spb_lg), kHistThreads, kSliceNodes * 4, st>>>(
+                (const uint32_t *)srt.p, (const uint32_t *)O.p, (const uint32_t *)H.p, cols, nb,
+                (const uint32_t *)items.p, n_items, m0, K, shift, spb_lg, dense, counts);
+        else
+            slice_count_kernel<CountT><<<(unsigned)(items_ub << spb_lg), kHistThreads, kSliceNodes * 4, st>>>(
+                (const uint32_t *)srt.p, (const uint32_t *)O.p, (const uint32_t *)H.p, cols, nb,
+                (const uint32_t *)items.p, n_items, (uint32_t)K, shift, spb_lg, counts);
         CUDA_TRY(cudaGetLastError());
         return PARBA_OK;
     }
 };
 
+// by_pos (full histogram of a degree sequence with the dense owner map): the
+// targets pass emits positions, K becomes the position domain m, and the
+// counts are resolved to owners in order.
 template <typename CountT>
 int count_partitioned(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi, uint64_t K,
-                      CountT *counts, unsigned long long *probes, cudaStream_t st) {
+                      CountT *counts, unsigned long long *probes, cudaStream_t st, bool by_pos) {
+    if (by_pos) K = p->m;
     DevInfo *di;
     int rc = dev_info(&di);
     if (rc) return rc;
@@ -551,6 +573,10 @@ int count_partitioned(const parba_params_t *p, const DevParams &dp, uint64_t lo,
         a.shift = ps.shift;
         a.nb = ps.nb;
         a.klim = K;
+        if constexpr (sizeof(CountT) == 4) {
+            a.by_pos = by_pos ? 1 : 0;
+            a.full = (uint32_t *)counts;  // seed-graph targets of the position pass
+        }
         a.t32_cap = cap;
         a.t32_geom = geom;
         rc = K >= p->n ? launch_tiles<kTargets>(p, dp, b0, b1, a, probes, st)
@@ -558,7 +584,8 @@ int count_partitioned(const parba_params_t *p, const DevParams &dp, uint64_t lo,
         if (rc) return rc;
         const uint32_t used = (uint32_t)geom[3] * kHistGroups;
         if (used > nblk) return fail(PARBA_ECUDA, "targets launch wider than the histogram");
-        if ((rc = ps.count<CountT>(geom[0], geom[1], (uint32_t)geom[2], kHistGroups, used, K, counts, st)))
+        if ((rc = ps.count<CountT>(geom[0], geom[1], (uint32_t)geom[2], kHistGroups, used, K, counts, st,
+                                   by_pos ? dp.dense : nullptr, p->m0)))
             return rc;
         b0 = b1;
     }
@@ -617,8 +644,11 @@ int parba_degree_full(const parba_params_t *p, uint64_t lo, uint64_t hi, uint32_
     cudaStream_t st = (cudaStream_t)stream;
     const DevParams dp = make_dev(p, p->n);
     if (p->flags) return count_nodes_u32(p, dp, lo, hi, p->n, counts, probes, st);
-    if (use_partitioned(p, lo, hi, p->n)) {
-        rc = count_partitioned<uint32_t>(p, dp, lo, hi, p->n, counts, probes, st);
+    // degree sequence with the dense owner map: partition positions instead
+    // of owners (no random owner lookups in the targets pass)
+    const bool by_pos = is_deg(p) && dp.dense && p->m < (1ull << 31) && pos_mode_enabled();
+    if (by_pos ? use_partitioned(p, lo, hi, p->m) : use_partitioned(p, lo, hi, p->n)) {
+        rc = count_partitioned<uint32_t>(p, dp, lo, hi, p->n, counts, probes, st, by_pos);
     } else {
         SinkArgs a{nullptr, nullptr, counts};
         rc = launch_tiles<kFull>(p, dp, lo, hi, a, probes, st);

@@ -303,4 +303,52 @@ __global__ void __launch_bounds__(kHistThreads) slice_count_kernel(const uint32_
     }
 }
 
+// Step 3 for positions (degree sequences): like slice_count_kernel over the
+// position domain, then each slice's position counts are summed per owning
+// node (dense owner map, read in order; owners are non-decreasing in the
+// position, so a warp reduces runs of equal owners with shuffles) and the
+// run totals are added to counts with atomics (a node's positions may span
+// slices).  Positions >= m are never stored; positions < m0 never occur.
+template <typename CountT>
+__global__ void __launch_bounds__(kHistThreads) slice_count_pos_kernel(
+    const uint32_t *__restrict__ sorted, const uint32_t *__restrict__ O, const uint32_t *__restrict__ H,
+    uint32_t nblk, int nb, const uint32_t *__restrict__ items, const uint32_t *__restrict__ n_items, uint64_t m0,
+    uint64_t m, int shift, int spb_lg, const uint32_t *__restrict__ dense, CountT *__restrict__ counts) {
+    extern __shared__ uint32_t c[];
+    const uint32_t it = blockIdx.x >> spb_lg;
+    if (it >= *n_items) return;
+    const uint32_t item = items[it];
+    const uint32_t b = item & ((1u << kBucketBits) - 1), chunk = item >> kBucketBits;
+    const uint32_t s = blockIdx.x & ((1u << spb_lg) - 1);
+    for (int k = threadIdx.x; k < kSliceNodes; k += blockDim.x) c[k] = 0;
+    __syncthreads();
+    uint32_t e0, e1;
+    bucket_range(O, H, nblk, nb, b, e0, e1);
+    const uint32_t k0 = e0 + chunk * kCountChunk;
+    const uint32_t k1 = e1 - k0 > kCountChunk ? k0 + kCountChunk : e1;
+    const uint32_t smask = (1u << spb_lg) - 1;
+    for (uint32_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+        const uint32_t x = __ldg(sorted + k);
+        if (((x >> kSliceLg) & smask) == s) atomicAdd(&c[x & (kSliceNodes - 1)], 1u);
+    }
+    __syncthreads();
+    const uint64_t p0 = ((uint64_t)b << shift) + ((uint64_t)s << kSliceLg);
+    const int lane = threadIdx.x & 31;
+    for (int k = threadIdx.x; k < kSliceNodes; k += blockDim.x) {  // warp-uniform trip count
+        const uint64_t pos = p0 + k;
+        const bool in = pos >= m0 && pos < m;
+        uint32_t x = in ? c[k] : 0u;
+        const uint32_t v = in ? __ldg(dense + (pos - m0)) : 0xffffffffu;
+        // inclusive segmented sum over lanes with the same owner (runs)
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            const uint32_t w = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o && w == v) x += y;
+        }
+        const uint32_t vn = __shfl_down_sync(0xffffffffu, v, 1);
+        if (in && x && (lane == 31 || vn != v)) atomicAdd(counts + v, (CountT)x);
+    }
+}
+
 }  // namespace parba

@@ -115,6 +115,7 @@ struct SinkArgs {
     uint32_t *hist;                        // targets: H[b * G * gridDim.x + G * blk + group]
     int shift, nb;                         //   (bucket = target >> shift, G = kHistGroups)
     uint64_t klim;                         // targets: only targets < klim are kept
+    int by_pos;                            // targets, degree sequence: emit positions (full counts)
     uint64_t t32_cap;                      // host side: slots of t32
     uint64_t *t32_geom;                    // host side: {slots filled, capw, warps per CTA, CTAs}
 };
@@ -298,6 +299,25 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
     // targets >= klim (full: n; window: the K lowest nodes) are dropped
     auto emit = [&](bool f, uint64_t rv) {
         if constexpr (is_targets(SINK)) {
+            if constexpr (SINK == kTargets && DEG) {
+                if (a.by_pos) {
+                    // degree sequence, full histogram by position: the terminal
+                    // position r >> 1 (owner resolved in order by the count
+                    // kernel) instead of a random owner lookup here; seed-graph
+                    // targets (rare) are counted directly
+                    const bool seedt = f && rv < p.stop;
+                    if (seedt) atomicAdd(a.full + __ldg(p.seed + rv), 1u);
+                    const bool keep = f && !seedt;
+                    const unsigned m = ballot_all(keep);
+                    if (keep) {
+                        const uint32_t e = (uint32_t)(rv >> 1);
+                        wout[wcur + __popc(m & ltmask)] = e;
+                        atomicAdd(hist_w + (e >> a.shift), 1u);
+                    }
+                    wcur += __popc(m);
+                    return;
+                }
+            }
             if constexpr (SINK == kTargets) {  // full histogram: every target is kept
                 const unsigned m = ballot_all(f);
                 if (f) {

@@ -430,3 +430,24 @@ def test_option_flags_reject_beyond_2p51_edges():
     lo = p.m0 + (p.n - p.n0 - 1) * p.d
     with pytest.raises(pb.ParameterError, match="2\\^51"):
         pb.generate_block(lo, lo + p.d, p)
+
+
+def test_degree_sequence_full_counts_by_position(monkeypatch):
+    """Degree-sequence full histograms through the opt-in position pass (targets
+    partitioned as positions, owners resolved in order from the dense map,
+    seed-graph targets counted directly) equal the owner-partitioned pass and
+    the direct kernel, probes included; zero degrees and hubs included."""
+    rng = np.random.default_rng(31)
+    deg = np.minimum(rng.zipf(2.0, size=300_000) + rng.integers(0, 3, size=300_000), 5000).astype(np.uint64)
+    deg[::11] = 0
+    p = pb.GenParams(n=3 + deg.size, n0=3, degrees=deg, seed_edges=TRIANGLE)
+    assert p._index()[2] is not None  # the dense owner map exists
+    got = {}
+    for name, mode, pos in (("pos", "partition", "1"), ("owner", "partition", "0"), ("direct", "direct", "0")):
+        monkeypatch.setenv("PARBA_FULL_MODE", mode)
+        monkeypatch.setenv("PARBA_POS_MODE", pos)
+        counter, stats = pb.degree_counts(p)
+        got[name] = (counter.counts.copy(), stats.hash_probes)
+    for name in ("owner", "direct"):
+        assert np.array_equal(got["pos"][0], got[name][0]) and got["pos"][1] == got[name][1], name
+    assert int(got["pos"][0].sum()) == 2 * p.m
