@@ -464,6 +464,29 @@ def test_window_large_range_sharding_independent():
     assert 1.9 <= int(pr.item()) / (hi - lo) <= 2.1
 
 
+@pytest.mark.parametrize("cfg", [("C3", 10**9, 100), ("C5", 10**10, 100)], ids=lambda c: c[0])
+def test_full_baseline_window_independent_of_gpu_count(cfg):
+    """The whole C3 (1e11 edges) and C5 (1e12 edges) windows (K = 1e5): the
+    8-way edge-ID partition's per-shard counts sum to the single-range run,
+    probes included (identical for G in {1, 2, 4, 8}), and the
+    window holds every source of its K*d edges."""
+    import torch
+
+    _, n, d = cfg
+    p = pb.GenParams(n=n, d=d)
+    K = 10**5
+    whole, pr = pb.parallel.count_shard_device(p, K, 0, p.m)
+    acc = torch.zeros_like(whole)
+    prs = torch.zeros_like(pr)
+    for g in range(8):
+        a, b = pb.parallel.shard_range(0, p.m, g, 8)
+        pb.parallel.count_shard_device(p, K, a, b, counts=acc, probes=prs)
+    torch.cuda.synchronize()
+    assert torch.equal(acc, whole) and int(prs.item()) == int(pr.item())
+    c = whole.cpu().numpy()
+    assert (c >= d).all() and 1.99 <= int(pr.item()) / p.m <= 2.01
+
+
 def test_probe_cost_per_edge():
     # acceptance (3): mean probes/edge in [1.8, 2.2]
     for kind in (pb.HashKind.CRC, pb.HashKind.SIMPLE):
