@@ -33,6 +33,7 @@ sys.path.insert(0, ROOT)
 C2 = dict(n=10**8, d=10)          # configs[1]: store mode, m = 1e9
 C3 = dict(n=10**9, d=100, K=10**5)  # configs[2]: streaming window, m = 1e11
 C4 = dict(n=10**8, d=16)          # configs[3]: full histogram, m = 1.6e9
+METRIC = "edges generated/sec (device-timed) at 1/2/4/8 B200; % of HBM/int roofline"  # BASELINE.json metric
 BYTES_PER_EDGE = 16               # algorithmic HBM bytes per stored edge
 E2E_EDGES = 250_000_000  # edges per GPU returned to the host per e2e step (4 GB)
 WRITE_ONLY_GBS = 6867.6  # write-only HBM peak measured by tools/micro.cu on a B200 of this pool
@@ -166,7 +167,7 @@ def run_reference(args) -> None:
         if k >= args.warmup:
             samples.append(cb)
     value = statistics.median(s["value"] for s in samples)
-    line = {"impl": "reference", "metric": "edges generated/sec (device-timed) at 1/2/4/8 B200",
+    line = {"impl": "reference", "metric": METRIC,
             "value": value, "unit": "edges/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1000 * n_edges / value, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
@@ -346,7 +347,7 @@ def main() -> None:
             per_edge = json.load(fh).get("dram_bytes_per_edge")
             traffic = per_edge * shard if per_edge else None
     line = {
-        "metric": "edges generated/sec (device-timed) at 1/2/4/8 B200; % of HBM/int roofline",
+        "metric": METRIC,
         "value": value, "unit": "edges/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000 * elapsed_max / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic (the generator has no input data)",
