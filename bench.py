@@ -155,6 +155,16 @@ def cpu_baseline(sample_edges: int | None = None, budget_s: float = 12.0) -> dic
             "sample_edges": sample_edges, "probes_per_edge": probes / sample_edges}
 
 
+def c2_config(ws: int) -> dict:
+    """The workload both arms report (BASELINE.json configs[1])."""
+    m = C2["n"] * C2["d"]
+    return {"workload": "configs[1]: store mode, n=1e8, d=10, m=1e9 edges -> (m,2) u64 pairs (16 GB) "
+                        "in HBM, contiguous edge-ID shards over the GPUs (total work fixed)",
+            "n": C2["n"], "d": C2["d"], "m": m, "shard_edges": m // ws,
+            "parallelism": f"edge-range shards x{ws} (no collective in store mode)",
+            "l2": "output 16 GB/N >> 126 MB L2: no flush needed between steps"}
+
+
 def run_reference(args) -> None:
     rank, ws, _ = _dist()
     if rank != 0:
@@ -171,8 +181,8 @@ def run_reference(args) -> None:
             "value": value, "unit": "edges/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1000 * n_edges / value, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": {"workload": "configs[1] store mode (n=1e8, d=10, m=1e9); bounded CPU sample per step",
-                       "n": C2["n"], "d": C2["d"], "sample_edges": n_edges},
+            "config": c2_config(ws) | {"sample_edges": n_edges,
+                                       "reference_step": "a bounded CPU sample of the workload per step"},
             "cpu_baseline": {k: samples[-1][k] for k in ("kind", "cores", "sample")} | {"value": value, "unit": "edges/s"},
             "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -351,11 +361,7 @@ def main() -> None:
         "value": value, "unit": "edges/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000 * elapsed_max / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic (the generator has no input data)",
-        "config": {"workload": "configs[1]: store mode, n=1e8, d=10, m=1e9 edges -> (m,2) u64 pairs (16 GB) "
-                               "in HBM, contiguous edge-ID shards over the GPUs (total work fixed)",
-                   "n": p.n, "d": C2["d"], "m": p.m, "shard_edges": shard,
-                   "parallelism": f"edge-range shards x{ws} (no collective in store mode)",
-                   "l2": "output 16 GB/N >> 126 MB L2: no flush needed between steps"},
+        "config": c2_config(ws),
         "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
                      "frac": achieved_gbs / peak, "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": shard * BYTES_PER_EDGE,
