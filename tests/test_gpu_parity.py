@@ -419,6 +419,8 @@ def _window_counts(p, K, lo, hi, mode, monkeypatch):
     "case",
     [
         ("half_window", dict(n=10**6, d=8), 500_000, 777, -3),
+        ("one_node", dict(n=10**6, d=8), 1, 0, 0),
+        ("slice_plus_one", dict(n=10**6, d=3), (1 << 15) + 1, 5, -5),
         ("seeded_degseq", dict(n=3 + _RAGGED_DEG.size, n0=3, degrees=_RAGGED_DEG, seed_edges=TRIANGLE), 150_000, 3, 0),
         ("two_passes_u64", dict(n=10**9, d=10), 10**9, -(1 << 23), 0),
         ("max_domain_2p31", dict(n=2**31 + 5, d=2), 2**31, -(1 << 22), 0),
