@@ -307,6 +307,17 @@ __device__ __forceinline__ bool node_npe(uint64_t v, uint64_t first, uint64_t dv
             }
             if (set) {
                 fresh = set_insert_if_absent(set, lg_cap, t);
+            } else if (nsl && a <= n_memo) {
+                // no_self_loops: every earlier attempt b < a was tried by this
+                // or an earlier edge and is accepted or a repeat of an accepted
+                // target, so t is fresh iff it is the first occurrence in the
+                // memoised attempt sequence (local memory, not the written rows)
+                fresh = true;
+                for (uint64_t b = 0; b < a; ++b)
+                    if (memo_t[b] == t) {
+                        fresh = false;
+                        break;
+                    }
             } else {
                 fresh = true;
                 for (uint64_t j = first; j < i; ++j)  // the node's accepted targets so far
