@@ -272,7 +272,13 @@ __device__ __forceinline__ bool set_insert_if_absent(uint64_t *tab, uint32_t lg_
 // cumulative probe counts are memoised, and edge i starts at the attempt after
 // edge i-1's (earlier ones stay rejected: the accepted set only grows) while
 // adding the probes the reference spends re-walking them.
-template <bool DEG>
+// no_self_loops membership scans of up to kLocalScan attempts read the memo
+// in local memory; longer ones read the node's contiguous output rows (a
+// thread's local array is interleaved across the warp: one cache line per
+// element).
+constexpr uint64_t kLocalScan = 32;
+
+template <bool DEG, bool MEMO_SCAN = false>
 __device__ __forceinline__ bool node_npe(uint64_t v, uint64_t first, uint64_t dv, uint64_t lo, ulonglong2 *out,
                                          uint64_t *set, uint32_t lg_cap, uint64_t *memo_t, uint64_t *memo_c,
                                          uint32_t memo_cap, const Family *fams, uint32_t tab, bool simple,
@@ -307,7 +313,7 @@ __device__ __forceinline__ bool node_npe(uint64_t v, uint64_t first, uint64_t dv
             }
             if (set) {
                 fresh = set_insert_if_absent(set, lg_cap, t);
-            } else if (nsl && a <= n_memo) {
+            } else if (MEMO_SCAN && nsl && a <= n_memo && a <= kLocalScan) {
                 // no_self_loops: every earlier attempt b < a was tried by this
                 // or an earlier edge and is accepted or a repeat of an accepted
                 // target, so t is fresh iff it is the first occurrence in the
@@ -383,7 +389,7 @@ __device__ __forceinline__ void node_span(uint64_t v, const DevParams &p, uint64
 // Under no_parallel_edges nodes of degree > big_deg are skipped here (they
 // run in node_big_kernel with a hash set).  fail_edge receives the smallest
 // edge index that found no fresh target (InfeasibleTargetsError).
-template <bool DEG>
+template <bool DEG, bool MEMO_SCAN = false>  // MEMO_SCAN: both flags (see node_npe)
 __global__ void __launch_bounds__(256)
 node_kernel(DevParams p, NodeArgs na, uint64_t vlo, uint64_t vhi, uint64_t lo, uint64_t n_out, ulonglong2 *out,
             unsigned long long *probes_out, unsigned long long *fail_edge, uint64_t big_deg, const uint8_t *need) {
@@ -406,7 +412,7 @@ node_kernel(DevParams p, NodeArgs na, uint64_t vlo, uint64_t vhi, uint64_t lo, u
             continue;
         }
         if (dv > big_deg || (need && !need[v - vlo])) continue;
-        node_npe<DEG>(v, first, dv, lo, out, nullptr, 0, memo_t, memo_c, kMemo, fams, tab, simple, p, na,
+        node_npe<DEG, MEMO_SCAN>(v, first, dv, lo, out, nullptr, 0, memo_t, memo_c, kMemo, fams, tab, simple, p, na,
                       probes, fail_edge);
     }
     node_probes_flush(probes, probes_out);

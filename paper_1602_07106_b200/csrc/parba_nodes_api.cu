@@ -220,12 +220,12 @@ int generate_nodes(const parba_params_t *p, const DevParams &dp, uint64_t vlo, u
     const uint64_t big = na.no_parallel_edges ? kBigDegree : UINT64_MAX;
     unsigned long long *fep = fail_ext ? fail_ext : (unsigned long long *)fe.p;
     const uint8_t *needp = (const uint8_t *)need.p;
-    if (is_deg(p))
-        node_kernel<true><<<grid, 256, 0, st>>>(dp, na, vlo, vhi, lo, hi - lo, (ulonglong2 *)out, probes, fep, big,
-                                                needp);
-    else
-        node_kernel<false><<<grid, 256, 0, st>>>(dp, na, vlo, vhi, lo, hi - lo, (ulonglong2 *)out, probes, fep, big,
-                                                 needp);
+    const bool both = na.no_self_loops && na.no_parallel_edges;
+    auto args = [&](auto kern) {
+        kern<<<grid, 256, 0, st>>>(dp, na, vlo, vhi, lo, hi - lo, (ulonglong2 *)out, probes, fep, big, needp);
+    };
+    if (is_deg(p)) both ? args(node_kernel<true, true>) : args(node_kernel<true, false>);
+    else both ? args(node_kernel<false, true>) : args(node_kernel<false, false>);
     CUDA_TRY(cudaGetLastError());
     if (na.no_parallel_edges) {
         rc = generate_big_nodes(p, dp, na, vlo, vhi, lo, hi, out, probes, fep, st);
