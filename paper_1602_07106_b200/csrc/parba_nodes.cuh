@@ -418,6 +418,42 @@ node_kernel(DevParams p, NodeArgs na, uint64_t vlo, uint64_t vhi, uint64_t lo, u
     node_probes_flush(probes, probes_out);
 }
 
+// no_self_loops alone, uniform d (<= 2^20): one chain per node (lane), and
+// the warp's 32 nodes' rows written by the whole warp -- consecutive lanes
+// store consecutive 16-byte rows (512-byte coalesced stores) instead of each
+// lane striding through its node's d rows.
+__global__ void __launch_bounds__(256)
+node_nsl_kernel(DevParams p, NodeArgs na, uint64_t vlo, uint64_t vhi, uint64_t lo, ulonglong2 *out,
+                unsigned long long *probes_out) {
+    PARBA_NODE_PROLOGUE;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint32_t d = (uint32_t)p.d;
+    for (uint64_t vb = vlo + warp * 32; vb < vhi; vb += nwarps * 32) {  // warp-uniform trip count
+        const uint64_t v = vb + lane;
+        const uint32_t nact = vhi - vb < 32 ? (uint32_t)(vhi - vb) : 32u;
+        uint64_t t = 0;
+        if (v < vhi) {
+            const uint64_t first = p.m0 + (v - p.n0) * p.d;
+            uint64_t pr = 0;
+            const Family f0{p.k0, p.k01, p.mult};
+            const uint64_t r = chain_family(tab, 2 * first, f0, simple, p.stop, pr);
+            probes += pr * p.d;
+            t = target_of<false, true, false, false>(r, p);
+        }
+        ulonglong2 *o = out + (p.m0 + (vb - p.n0) * p.d - lo);
+        const uint32_t nrows = nact * d;
+        for (uint32_t b = 0; b < nrows; b += 32) {
+            const uint32_t rr = b + lane;
+            const uint32_t k = magic_div32(rr < nrows ? rr : nrows - 1, p.div32);  // node of row rr
+            const uint64_t tv = __shfl_sync(0xffffffffu, t, k);
+            if (rr < nrows) __stcs(o + rr, make_ulonglong2(vb + k, tv));
+        }
+    }
+    node_probes_flush(probes, probes_out);
+}
+
 // Degree counts under no_self_loops alone, fused: node v's dv edges all run
 // the chain from 2*first, so they add dv to v and dv to their common target
 // (both endpoints < K) -- two atomics per node, no edge rows in memory.

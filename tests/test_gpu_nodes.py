@@ -451,3 +451,19 @@ def test_degree_sequence_full_counts_by_position(monkeypatch):
     for name in ("owner", "direct"):
         assert np.array_equal(got["pos"][0], got[name][0]) and got["pos"][1] == got[name][1], name
     assert int(got["pos"][0].sum()) == 2 * p.m
+
+
+@pytest.mark.parametrize("d", [1, 3, 33, 300])
+def test_no_self_loops_warp_rows_vs_oracle(d):
+    """no_self_loops alone with uniform d runs node_nsl_kernel (one chain per
+    node, the warp's rows stored cooperatively); node ranges that start and
+    end off a 32-node boundary, bit-exact with probes vs the oracle."""
+    k = 5
+    seed = np.array([x for a in range(k) for b in range(a + 1, k) for x in (a, b)], dtype=np.uint64)
+    p = pb.GenParams(n=3000 + 77, d=d, n0=k, seed_edges=seed, no_self_loops=True)
+    op = O.OParams(n=p.n, d=d, n0=k, seed_edges=tuple(int(x) for x in seed), no_self_loops=True)
+    for lo_node, hi_node in ((k, p.n), (k + 13, p.n - 7), (k + 40, k + 41)):
+        lo, hi = p.m0 + (lo_node - k) * d, p.m0 + (hi_node - k) * d
+        got, pr = pb.generate_block(lo, hi, p)
+        want, wp = O.generate_block(op, lo, hi)
+        assert np.array_equal(got, want) and pr == wp, (lo_node, hi_node)
