@@ -356,6 +356,13 @@ __device__ __forceinline__ bool node_npe(uint64_t v, uint64_t first, uint64_t dv
     __shared__ uint32_t tabs_p[8 * 256];                                                   \
     build_byte_tables(tabs_p, 8, 0u)
 #endif
+// no_self_loops-only kernels: no retry families
+#define PARBA_NODE_PROLOGUE_NSL                                                            \
+    PARBA_NODE_TABLES;                                                                     \
+    __syncthreads();                                                                       \
+    const uint32_t tab = opaque(smem_addr(tabs_p));                                        \
+    const bool simple = na.simple != 0;                                                    \
+    uint64_t probes = 0
 #define PARBA_NODE_PROLOGUE                                                                \
     PARBA_NODE_TABLES;                                                                     \
     __shared__ Family fams[kFamilies];                                                     \
@@ -412,6 +419,19 @@ node_kernel(DevParams p, NodeArgs na, uint64_t vlo, uint64_t vhi, uint64_t lo, u
             continue;
         }
         if (dv > big_deg || (need && !need[v - vlo])) continue;
+        if (!MEMO_SCAN && na.pre0 && !need && dv <= 16) {  // (not compiled into the both-flags kernel)
+            // attempt-0 targets (the plain pass's rows) pairwise distinct:
+            // the node is final (npe_dup_kernel's rule, checked inline)
+            uint64_t t[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) t[k] = (uint64_t)k < dv ? out[first - lo + k].y : ~(uint64_t)k;
+            bool dup = false;
+#pragma unroll
+            for (int a = 1; a < 16; ++a)
+#pragma unroll
+                for (int b = 0; b < a; ++b) dup |= t[a] == t[b];
+            if (!dup) continue;
+        }
         node_npe<DEG, MEMO_SCAN>(v, first, dv, lo, out, nullptr, 0, memo_t, memo_c, kMemo, fams, tab, simple, p, na,
                       probes, fail_edge);
     }
@@ -425,7 +445,7 @@ node_kernel(DevParams p, NodeArgs na, uint64_t vlo, uint64_t vhi, uint64_t lo, u
 __global__ void __launch_bounds__(256)
 node_nsl_kernel(DevParams p, NodeArgs na, uint64_t vlo, uint64_t vhi, uint64_t lo, ulonglong2 *out,
                 unsigned long long *probes_out) {
-    PARBA_NODE_PROLOGUE;
+    PARBA_NODE_PROLOGUE_NSL;
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -461,7 +481,7 @@ template <bool DEG, typename CountT>
 __global__ void __launch_bounds__(256)
 node_count_kernel(DevParams p, NodeArgs na, uint64_t vlo, uint64_t vhi, uint64_t K, CountT *counts,
                   unsigned long long *probes_out) {
-    PARBA_NODE_PROLOGUE;
+    PARBA_NODE_PROLOGUE_NSL;
     for (uint64_t v = vlo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < vhi;
          v += (uint64_t)gridDim.x * blockDim.x) {
         uint64_t first, dv;

@@ -180,6 +180,9 @@ int report_infeasible(const parba_params_t *p, const DevParams &dp, const uint64
 // fail_ext: a caller-owned failing-edge word (atomicMin, initialised to
 // UINT64_MAX) that the caller reports once after several calls; otherwise
 // the failure is reported here (one device sync).
+#ifndef PARBA_INLINE_DUP
+#define PARBA_INLINE_DUP 1
+#endif
 int generate_nodes(const parba_params_t *p, const DevParams &dp, uint64_t vlo, uint64_t vhi, uint64_t lo,
                    uint64_t hi, uint64_t *out, unsigned long long *probes, cudaStream_t st,
                    unsigned long long *fail_ext) {
@@ -209,7 +212,10 @@ int generate_nodes(const parba_params_t *p, const DevParams &dp, uint64_t vlo, u
         CUDA_TRY(cudaMemsetAsync(fe.p, 0xFF, sizeof(unsigned long long), st));
     }
     const unsigned grid = grid_for(vhi - vlo, 256);
-    if (na.pre0) {  // nodes whose attempt-0 targets are already distinct are final
+    // PARBA_INLINE_DUP: the node kernel checks the attempt-0 rows of nodes of
+    // degree <= 16 itself (one pass over the rows instead of npe_dup_kernel +
+    // the node kernel); larger nodes always re-run
+    if (na.pre0 && !PARBA_INLINE_DUP) {  // nodes whose attempt-0 targets are already distinct are final
         if ((rc = need.alloc(vhi - vlo, st))) return rc;
         if (is_deg(p))
             npe_dup_kernel<true><<<grid, 256, 0, st>>>(dp, vlo, vhi, lo, (const ulonglong2 *)out, (uint8_t *)need.p);
