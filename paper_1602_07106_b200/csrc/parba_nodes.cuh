@@ -438,10 +438,14 @@ node_kernel(DevParams p, NodeArgs na, uint64_t vlo, uint64_t vhi, uint64_t lo, u
     node_probes_flush(probes, probes_out);
 }
 
-// no_self_loops alone, uniform d (<= 2^20): one chain per node (lane), and
-// the warp's 32 nodes' rows written by the whole warp -- consecutive lanes
-// store consecutive 16-byte rows (512-byte coalesced stores) instead of each
-// lane striding through its node's d rows.
+// no_self_loops alone: one chain per node (lane), and the warp's 32 nodes'
+// rows written by the whole warp -- consecutive lanes store consecutive
+// 16-byte rows (512-byte coalesced stores) instead of each lane striding
+// through its own node's rows.  Row -> node: uniform d (<= 2^20) by the
+// magic division; degree sequences by a binary search over the lanes'
+// exclusive degree prefix (zero-degree lanes share the next lane's prefix,
+// so the search lands on the owning lane).
+template <bool DEG>
 __global__ void __launch_bounds__(256)
 node_nsl_kernel(DevParams p, NodeArgs na, uint64_t vlo, uint64_t vhi, uint64_t lo, ulonglong2 *out,
                 unsigned long long *probes_out) {
@@ -449,26 +453,58 @@ node_nsl_kernel(DevParams p, NodeArgs na, uint64_t vlo, uint64_t vhi, uint64_t l
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    const uint32_t d = (uint32_t)p.d;
     for (uint64_t vb = vlo + warp * 32; vb < vhi; vb += nwarps * 32) {  // warp-uniform trip count
         const uint64_t v = vb + lane;
         const uint32_t nact = vhi - vb < 32 ? (uint32_t)(vhi - vb) : 32u;
-        uint64_t t = 0;
-        if (v < vhi) {
-            const uint64_t first = p.m0 + (v - p.n0) * p.d;
+        uint64_t first = 0, dv = 0, t = 0;
+        if (v < vhi) node_span<DEG>(v, p, first, dv);
+        if (DEG ? dv != 0 : v < vhi) {
             uint64_t pr = 0;
             const Family f0{p.k0, p.k01, p.mult};
             const uint64_t r = chain_family(tab, 2 * first, f0, simple, p.stop, pr);
-            probes += pr * p.d;
-            t = target_of<false, true, false, false>(r, p);
+            probes += pr * dv;
+            t = target_of<false, true, false, DEG>(r, p);
         }
-        ulonglong2 *o = out + (p.m0 + (vb - p.n0) * p.d - lo);
-        const uint32_t nrows = nact * d;
-        for (uint32_t b = 0; b < nrows; b += 32) {
-            const uint32_t rr = b + lane;
-            const uint32_t k = magic_div32(rr < nrows ? rr : nrows - 1, p.div32);  // node of row rr
-            const uint64_t tv = __shfl_sync(0xffffffffu, t, k);
-            if (rr < nrows) __stcs(o + rr, make_ulonglong2(vb + k, tv));
+        uint64_t first_b;  // first edge of the warp's first node
+        uint64_t nrows;
+        uint64_t excl = 0;  // DEG: rows of the lanes before this one
+        if constexpr (DEG) {
+            uint64_t inc = dv;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint64_t y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= (uint32_t)o) inc += y;
+            }
+            excl = inc - dv;
+            nrows = __shfl_sync(0xffffffffu, inc, 31);
+            first_b = __shfl_sync(0xffffffffu, first, 0);
+            if (v >= vhi) excl = nrows;  // inactive lanes sit past the end
+        } else {
+            nrows = (uint64_t)nact * p.d;
+            first_b = p.m0 + (vb - p.n0) * p.d;
+        }
+        ulonglong2 *o = out + (first_b - lo);
+        if constexpr (DEG) {
+            for (uint64_t b = 0; b < nrows; b += 32) {
+                const uint64_t rr = b + lane;
+                const uint64_t rq = rr < nrows ? rr : nrows - 1;
+                uint32_t k = 0;
+#pragma unroll
+                for (uint32_t st = 16; st > 0; st >>= 1) {
+                    const uint64_t e = __shfl_sync(0xffffffffu, excl, k + st);
+                    if (e <= rq) k += st;
+                }
+                const uint64_t tv = __shfl_sync(0xffffffffu, t, k);
+                if (rr < nrows) __stcs(o + rr, make_ulonglong2(vb + k, tv));
+            }
+        } else {
+            const uint32_t nr = (uint32_t)nrows;  // <= 32 * 2^20
+            for (uint32_t b = 0; b < nr; b += 32) {
+                const uint32_t rr = b + lane;
+                const uint32_t k = magic_div32(rr < nr ? rr : nr - 1, p.div32);  // node of row rr
+                const uint64_t tv = __shfl_sync(0xffffffffu, t, k);
+                if (rr < nr) __stcs(o + rr, make_ulonglong2(vb + k, tv));
+            }
         }
     }
     node_probes_flush(probes, probes_out);

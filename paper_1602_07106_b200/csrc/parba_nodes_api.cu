@@ -226,8 +226,11 @@ int generate_nodes(const parba_params_t *p, const DevParams &dp, uint64_t vlo, u
     const uint64_t big = na.no_parallel_edges ? kBigDegree : UINT64_MAX;
     unsigned long long *fep = fail_ext ? fail_ext : (unsigned long long *)fe.p;
     const uint8_t *needp = (const uint8_t *)need.p;
-    if (na.no_self_loops && !na.no_parallel_edges && !is_deg(p) && p->d <= (1u << 20)) {
-        node_nsl_kernel<<<grid, 256, 0, st>>>(dp, na, vlo, vhi, lo, (ulonglong2 *)out, probes);
+    if (na.no_self_loops && !na.no_parallel_edges && (is_deg(p) || p->d <= (1u << 20))) {
+        if (is_deg(p))
+            node_nsl_kernel<true><<<grid, 256, 0, st>>>(dp, na, vlo, vhi, lo, (ulonglong2 *)out, probes);
+        else
+            node_nsl_kernel<false><<<grid, 256, 0, st>>>(dp, na, vlo, vhi, lo, (ulonglong2 *)out, probes);
         CUDA_TRY(cudaGetLastError());
         return fail_ext ? PARBA_OK : report_infeasible(p, dp, (const uint64_t *)fe.p, st);
     }

@@ -467,3 +467,24 @@ def test_no_self_loops_warp_rows_vs_oracle(d):
         got, pr = pb.generate_block(lo, hi, p)
         want, wp = O.generate_block(op, lo, hi)
         assert np.array_equal(got, want) and pr == wp, (lo_node, hi_node)
+
+
+def test_no_self_loops_degree_sequence_warp_rows_vs_oracle():
+    """node_nsl_kernel on a degree sequence (zeros, hubs, runs of zero-degree
+    nodes, ragged node ranges): rows mapped to nodes by the warp's degree
+    prefix, bit-exact with probes vs the oracle."""
+    rng = np.random.default_rng(17)
+    deg = np.minimum(rng.zipf(1.8, size=4000), 700).astype(np.uint64)
+    deg[::5] = 0
+    deg[100:170] = 0  # a whole warp of zero-degree nodes
+    k = 6
+    seed = np.array([x for a in range(k) for b in range(a + 1, k) for x in (a, b)], dtype=np.uint64)
+    p = pb.GenParams(n=k + deg.size, n0=k, degrees=deg, seed_edges=seed, no_self_loops=True)
+    op = O.OParams(n=p.n, d=None, n0=k, seed_edges=tuple(int(x) for x in seed),
+                   degrees=tuple(int(x) for x in deg), no_self_loops=True)
+    W = np.concatenate([[p.m0], p.m0 + np.cumsum(deg.astype(np.int64))])
+    for a, b in ((0, deg.size), (33, deg.size - 9), (101, 168), (7, 8)):
+        lo, hi = int(W[a]), int(W[b])
+        got, pr = pb.generate_block(lo, hi, p)
+        want, wp = O.generate_block(op, lo, hi)
+        assert np.array_equal(got, want) and pr == wp, (a, b)
