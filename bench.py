@@ -5,15 +5,20 @@ n=1e8, d=10, m=1e9 int64 pairs written to HBM), the fixed graph's edge-ID
 range sharded over the GPUs as configs[1] prescribes (strong scaling).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-    torchrun --nproc-per-node N bench.py --gpus N ...
+
+With --gpus N > 1 and no torchrun environment, bench.py re-launches itself
+under torch.distributed.run with N ranks (one per GPU, NCCL).
 
 One JSON line on rank 0.  `value` = whole-job edges/s with the output
 resident in HBM; `e2e` = the same metric through the reference-facing API
-`generate_block(lo, hi, p)` returning a host array (device->host copy inside
-the timed region); `roofline` = the store kernel's algorithmic 16 B/edge
-write rate against the measured HBM peak; `cpu_baseline` = the CPU oracle
-port (reference algorithm in C) on a bounded sample, all host cores.
-`--impl reference` times that CPU implementation alone.
+`generate_block(lo, hi, p)` returning a host array (its device->host traffic
+inside the timed region); `roofline` = the store kernel's algorithmic
+16 B/edge write rate against the measured HBM peak; `modes` = the streaming
+configs (C3 window, C4 full histogram, C5 the paper's demo), each with its
+own device time, NCCL reduce included, and an integer roofline against the
+INT32 peak measured in the same run; `cpu_baseline` = the reference itself
+(parba + numba from baseline/_ref) on all host cores, with the C port of the
+oracle beside it.  `--impl reference` times the reference alone.
 """
 
 from __future__ import annotations
@@ -33,10 +38,10 @@ sys.path.insert(0, ROOT)
 C2 = dict(n=10**8, d=10)          # configs[1]: store mode, m = 1e9
 C3 = dict(n=10**9, d=100, K=10**5)  # configs[2]: streaming window, m = 1e11
 C4 = dict(n=10**8, d=16)          # configs[3]: full histogram, m = 1.6e9
+C5 = dict(n=10**10, d=100, K=10**5)  # configs[4]: the paper's demo, m = 1e12
 METRIC = "edges generated/sec (device-timed) at 1/2/4/8 B200; % of HBM/int roofline"  # BASELINE.json metric
 BYTES_PER_EDGE = 16               # algorithmic HBM bytes per stored edge
 E2E_EDGES = 250_000_000  # edges per GPU returned to the host per e2e step (4 GB)
-WRITE_ONLY_GBS = 6867.6  # write-only HBM peak measured by tools/micro.cu on a B200 of this pool
 INT_OPS_PER_PROBE = 32            # SURVEY 8d convention (64 per edge)
 
 
@@ -155,6 +160,104 @@ def cpu_baseline(sample_edges: int | None = None, budget_s: float = 12.0) -> dic
             "sample_edges": sample_edges, "probes_per_edge": probes / sample_edges}
 
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+REF_CFG = {"store": (C2["n"], C2["d"], 0), "window": (C3["n"], C3["d"], C3["K"]),
+           "full": (C4["n"], C4["d"], C4["n"])}
+
+
+def _ref_worker(args):
+    """One forked worker of the reference's own driver loop (parba/driver.py
+    _work_loop: claim a 2^16-edge batch, generate_block, accept_block)."""
+    wid, mode, n, d, K, batches, cursor, out_q = args
+    try:
+        import parba.driver as rd
+        from parba.analytics import DegreeCountConsumer
+        from parba.generator import GenParams
+
+        p = GenParams(n=n, d=d)
+        consumer = rd.DiscardConsumer() if mode == "store" else DegreeCountConsumer(K)
+        blist = [rd.Batch(a, b) for a, b in batches]
+
+        def claim():
+            with cursor.get_lock():
+                k = cursor.value
+                cursor.value = k + 1
+                return k
+
+        ctx, st = rd._work_loop(wid, p, consumer, blist, claim, None, "rank")
+        out_q.put(("ok", wid, st.edges, st.probes, int(ctx.sum()) if mode != "store" else int(ctx)))
+    except BaseException as e:  # surfaced by the parent
+        out_q.put(("error", wid, repr(e), 0, 0))
+
+
+def reference_numba(mode: str = "store", sample_edges: int | None = None, budget_s: float = 10.0,
+                    threads: int | None = None) -> dict:
+    """The reference itself (parba from baseline/_ref: numba kernels, its
+    own generate_block / consumers / batch loop, fork workers like
+    driver.run) on all host cores over the top `sample_edges` edge IDs of
+    the config's range.  Returns a cpu_baseline dict (kind "reference")."""
+    import multiprocessing as mp
+
+    if not os.path.isdir(os.path.join(REF_DIR, "parba")):
+        raise RuntimeError("baseline/_ref is not installed")
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/parba_numba_cache")
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import parba._kernels as rk
+    from parba.generator import GenParams, generate_block
+
+    rk.warmup()  # compile before the fork, as driver.run does
+    threads = threads or len(os.sched_getaffinity(0))
+    n, d, K = REF_CFG[mode]
+    m = n * d
+    bs = 1 << 16  # driver.DEFAULT_BATCH_SIZE
+    if sample_edges is None:  # calibrate one core on the top of the range
+        p = GenParams(n=n, d=d)
+        t0 = time.perf_counter()
+        for k in range(8):
+            generate_block(m - (k + 1) * bs, m - k * bs, p)
+        rate = 8 * bs / (time.perf_counter() - t0)
+        sample_edges = int(min(m, max(rate * threads * budget_s, threads * bs)))
+        sample_edges -= sample_edges % bs
+    lo = m - sample_edges
+    batches = [(a, min(a + bs, m)) for a in range(lo, m, bs)]
+    ctx = mp.get_context("fork")
+    cursor = ctx.Value("q", 0)
+    out_q = ctx.Queue()
+    t0 = time.perf_counter()
+    procs = [ctx.Process(target=_ref_worker, args=((w, mode, n, d, K, batches, cursor, out_q),))
+             for w in range(threads)]
+    for pr in procs:
+        pr.start()
+    msgs = [out_q.get() for _ in procs]
+    for pr in procs:
+        pr.join()
+    dt = time.perf_counter() - t0
+    bad = [mm for mm in msgs if mm[0] != "ok"]
+    if bad:
+        raise RuntimeError(f"reference worker failed: {bad[0]}")
+    edges = sum(mm[2] for mm in msgs)
+    assert edges == sample_edges, (edges, sample_edges)
+    what = {"store": "generate_block per 2^16-edge batch into fresh host arrays (DiscardConsumer)",
+            "window": f"generate_block + count_block, K={K} (DegreeCountConsumer)",
+            "full": "generate_block + count_block, K=n (DegreeCountConsumer)"}[mode]
+    return {"value": sample_edges / dt, "unit": "edges/s", "cores": threads, "kind": "reference",
+            "sample": f"the reference parba (baseline/_ref, numba {_numba_version()}) on edge IDs "
+                      f"[{lo}, {m}) of n={n:.0e}, d={d}: {what}, its own batch loop "
+                      f"(driver._work_loop) in {threads} forked workers, {dt:.2f} s",
+            "sample_edges": sample_edges, "probes_per_edge": sum(mm[3] for mm in msgs) / sample_edges,
+            "seconds": dt}
+
+
+def _numba_version() -> str:
+    try:
+        import numba
+
+        return numba.__version__
+    except Exception:  # pragma: no cover
+        return "?"
+
+
 def c2_config(ws: int) -> dict:
     """The workload both arms report (BASELINE.json configs[1])."""
     m = C2["n"] * C2["d"]
@@ -165,25 +268,49 @@ def c2_config(ws: int) -> dict:
             "l2": "output 16 GB/N >> 126 MB L2: no flush needed between steps"}
 
 
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _relaunch(n: int) -> int:
+    """bench.py --gpus N without a torchrun environment: run N ranks."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def run_reference(args) -> None:
+    """The reference arm: parba itself (baseline/_ref, numba) on all host
+    cores, store mode on C2, one bounded sample per step; rank 0 only."""
     rank, ws, _ = _dist()
     if rank != 0:
         return
+    try:
+        first = reference_numba("store", budget_s=3.0)
+        measure = lambda n: reference_numba("store", sample_edges=n)  # noqa: E731
+    except Exception as e:  # no baseline/_ref: the oracle's C port instead
+        print(f"reference parba unavailable ({e!r}); timing the C port", file=sys.stderr)
+        first = cpu_baseline(budget_s=3.0)
+        measure = lambda n: cpu_baseline(sample_edges=n)  # noqa: E731
+    n_edges = first["sample_edges"]
     samples = []
-    n_edges = None
     for k in range(args.warmup + args.steps):
-        cb = cpu_baseline(sample_edges=n_edges, budget_s=4.0)
-        n_edges = n_edges or cb["sample_edges"]
+        cb = first if k == 0 else measure(n_edges)
         if k >= args.warmup:
             samples.append(cb)
     value = statistics.median(s["value"] for s in samples)
     line = {"impl": "reference", "metric": METRIC,
-            "value": value, "unit": "edges/s", "n_gpus": args.gpus, "steps": args.steps,
+            "value": value, "unit": "edges/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1000 * n_edges / value, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": c2_config(ws) | {"sample_edges": n_edges,
                                        "reference_step": "a bounded CPU sample of the workload per step"},
-            "cpu_baseline": {k: samples[-1][k] for k in ("kind", "cores", "sample")} | {"value": value, "unit": "edges/s"},
+            "cpu_baseline": {k: samples[-1][k] for k in ("kind", "cores", "sample")} | {"value": value,
+                                                                                        "unit": "edges/s"},
             "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -198,30 +325,54 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra-modes", action="store_true")
     ap.add_argument("--profile", action="store_true", help="store kernel only (for ncu)")
+    ap.add_argument("--only", default=None, help="one streaming mode only (window_c3|full_c4|window_c5), for ncu")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="control-flow check of the N-rank path on ONE GPU (gloo, every rank on cuda:0); "
+                         "its numbers are not measurements")
     args = ap.parse_args()
-    args.warmup = max(args.warmup, 3) if not args.profile else args.warmup
+    args.warmup = max(args.warmup, 3) if not (args.profile or args.only) else args.warmup
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_relaunch(args.gpus))
     if args.impl == "reference":
         run_reference(args)
         return
 
     rank, ws, local = _dist()
-    # CPU baseline first: the oracle is plain C, but keep it out of the
-    # timed GPU region and before CUDA work on rank 0 (N=1 only).
+    if ws != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}")
+    # host threads of the e2e pipeline: this rank's share of the host cores
+    lws = int(os.environ.get("LOCAL_WORLD_SIZE", str(ws)))
+    os.environ.setdefault("PARBA_HOST_THREADS", str(max(1, len(os.sched_getaffinity(0)) // lws)))
+    # CPU baselines first (N=1, rank 0), before any CUDA work
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline and not args.profile:
-        cpu = cpu_baseline()
+    if rank == 0 and ws == 1 and not (args.no_cpu_baseline or args.profile or args.only):
+        port = cpu_baseline(budget_s=6.0)
+        try:
+            cpu = reference_numba("store", budget_s=8.0)
+            cpu["port"] = {k: port[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as e:  # baseline/_ref missing
+            cpu = port | {"reference_unavailable": repr(e)}
 
+    import ctypes
+
+    import numpy as np
     import torch
     import torch.distributed as dist
 
     import paper_1602_07106_b200 as pb
 
+    if args.share_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.share_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     L = pb._lib.load()
+    stream = torch.cuda.current_stream(dev)
 
     def barrier():
         if ws > 1:
@@ -234,6 +385,26 @@ def main() -> None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    def gather(x: float) -> list[float]:
+        if ws == 1:
+            return [x]
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        out = [torch.zeros_like(t) for _ in range(ws)]
+        dist.all_gather(out, t)
+        return [float(o.item()) for o in out]
+
+    def timed(fn, reps: int = 3) -> float:
+        """best device time (s) of fn() over reps, CUDA events on `stream`."""
+        best = 1e30
+        for _ in range(reps + 1):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            b.synchronize()
+            best = min(best, a.elapsed_time(b) / 1000.0)
+        return best
+
     # ---------------- store mode, C2 (headline): BASELINE.json configs[1] is
     # one fixed graph (n=1e8, d=10) "sharded by contiguous edge-ID ranges over
     # 1/2/4/8 GPUs", so total work is fixed as N grows (strong scaling).
@@ -243,111 +414,158 @@ def main() -> None:
     out = torch.empty((shard, 2), dtype=torch.int64, device=dev)
     probes = torch.zeros(1, dtype=torch.int64, device=dev)
     cp = p._device_params(dev)
-    stream = torch.cuda.current_stream(dev)
+
+    # roofline denominators measured here, on this GPU, before the kernels
+    peaks = {}
+    if not args.profile:
+        wsec = timed(lambda: pb._lib.check(L.parba_peak_write(out.data_ptr(), shard * 16, stream.cuda_stream)))
+        scratch = torch.zeros(1, dtype=torch.int32, device=dev)
+        ops = ctypes.c_double(0.0)
+        isec = timed(lambda: pb._lib.check(L.parba_peak_int32(scratch.data_ptr(), ctypes.byref(ops),
+                                                              stream.cuda_stream)))
+        peaks = {"write_only_gbs": shard * 16 / wsec / 1e9, "int32_lane_ops_per_s": ops.value / isec,
+                 "how": "in this run on this GPU: 16-byte streaming stores over the store buffer "
+                        "(parba_peak_write); LOP3+IADD3 chains (parba_peak_int32), best of 3"}
 
     def store_step():
         pb._lib.check(L.parba_generate(cp, lo, hi, out.data_ptr(), probes.data_ptr(), stream.cuda_stream))
 
-    for _ in range(args.warmup):
-        store_step()
-    torch.cuda.synchronize(dev)
-    probes.zero_()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    barrier()
-    torch.cuda.synchronize(dev)
-    with ClockSampler(local) as clk:
-        t_all0 = torch.cuda.Event(enable_timing=True)
-        t_all1 = torch.cuda.Event(enable_timing=True)
-        t_all0.record(stream)
-        for k in range(args.steps):
-            ev[k][0].record(stream)
+    kern_ms: list[float] = []
+    value = elapsed_max = 0.0
+    clk = None
+    if not args.only:
+        for _ in range(args.warmup):
             store_step()
-            ev[k][1].record(stream)
-        t_all1.record(stream)
         torch.cuda.synchronize(dev)
+        probes.zero_()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
         barrier()
-    elapsed = t_all0.elapsed_time(t_all1) / 1000.0
-    kern_ms = [a.elapsed_time(b) for a, b in ev]
-    elapsed_max = max_over_ranks(elapsed)
-    value = p.m * args.steps / elapsed_max
-    probes_per_edge = int(probes.item()) / (shard * args.steps)
-    peak, peak_src = _peaks()
-    avg_kernel_s = statistics.mean(kern_ms) / 1000.0
-    achieved_gbs = shard * BYTES_PER_EDGE / avg_kernel_s / 1e9
-    # spot-check the stored array against the sampled-ID kernel (no oracle on this path)
-    if rank == 0:
-        import numpy as np
-
-        ids = np.random.default_rng(1).integers(lo, hi, size=4096, dtype=np.uint64)
-        want, _ = pb.edges_at(ids, p, device=dev)
-        got = out[torch.from_numpy((ids - np.uint64(lo)).view(np.int64)).to(dev)].cpu().numpy().view(np.uint64)
-        assert np.array_equal(got, want), "stored edges disagree with edges_at"
-    if args.profile:
+        torch.cuda.synchronize(dev)
+        with ClockSampler(local) as clk:
+            t_all0 = torch.cuda.Event(enable_timing=True)
+            t_all1 = torch.cuda.Event(enable_timing=True)
+            t_all0.record(stream)
+            for k in range(args.steps):
+                ev[k][0].record(stream)
+                store_step()
+                ev[k][1].record(stream)
+            t_all1.record(stream)
+            torch.cuda.synchronize(dev)
+            barrier()
+        elapsed = t_all0.elapsed_time(t_all1) / 1000.0
+        kern_ms = [a.elapsed_time(b) for a, b in ev]
+        elapsed_max = max_over_ranks(elapsed)
+        value = p.m * args.steps / elapsed_max
+        probes_per_edge = int(probes.item()) / (shard * args.steps)
+        # spot-check the stored array against the sampled-ID kernel
         if rank == 0:
-            print(json.dumps({"profile": True, "value": value, "kernel_ms": kern_ms}))
-        return
+            ids = np.random.default_rng(1).integers(lo, hi, size=4096, dtype=np.uint64)
+            want, _ = pb.edges_at(ids, p, device=dev)
+            got = out[torch.from_numpy((ids - np.uint64(lo)).view(np.int64)).to(dev)].cpu().numpy().view(np.uint64)
+            assert np.array_equal(got, want), "stored edges disagree with edges_at"
+        if args.profile:
+            if rank == 0:
+                print(json.dumps({"profile": True, "value": value, "kernel_ms": kern_ms}))
+            return
     del out
     torch.cuda.empty_cache()
 
     # ---------------- e2e: reference-facing API, host array out.  Each rank
     # returns E2E_EDGES of its shard as a fresh host array (4 GB; bounded so
     # that 8 ranks do not pin 128 GB of host memory); the edges/s metric is
-    # the same.
-    barrier()
-    e2e_n = min(shard, E2E_EDGES)
-    e2e_times = []
-    for k in range(1 + args.e2e_steps):
+    # the same.  The native pipeline moves the u32 targets (4 B per edge)
+    # over PCIe and fills the (source, target) rows with host threads.
+    e2e = None
+    if not args.only:
         barrier()
-        torch.cuda.synchronize(dev)
-        t0 = time.perf_counter()
-        arr, _ = pb.generate_block(lo, lo + e2e_n, p, device=dev)
-        dt = time.perf_counter() - t0
-        if k:
-            e2e_times.append(dt)
-        del arr
-    e2e_s = max_over_ranks(statistics.median(e2e_times))
-    e2e = {"value": e2e_n * ws / e2e_s, "unit": "edges/s", "h2d_bytes_per_step": 0,
-           "d2h_bytes_per_step": e2e_n * 16, "edges_per_step_per_gpu": e2e_n,
-           "api": "paper_1602_07106_b200.generate_block(lo, hi, p) -> host (hi-lo,2) uint64 (pinned), "
-           "chunked device generation overlapped with D2H",
-           "h2d_note": "the generator has no input data: only (n, d, seed, range) scalars cross by value"}
-
-    # ---------------- extra modes: C3 streaming window, C4 full histogram
-    extra = {}
-    if not args.no_extra_modes:
-        for name, cfg, K in (("window_c3", C3, C3["K"]), ("full_c4", C4, C4["n"])):
-            q = pb.GenParams(n=cfg["n"], d=cfg["d"])
-            a, b = pb.parallel.shard_range(0, q.m, rank, ws)
-            counts = torch.zeros(K, dtype=torch.int32 if name == "full_c4" else torch.int64, device=dev)
-            prb = torch.zeros(1, dtype=torch.int64, device=dev)
-            steps = 2 if name == "window_c3" else 5
-            pb.parallel.count_shard_device(q, K, a, b, counts=counts, probes=prb, device=dev)
-            torch.cuda.synchronize(dev)
+        e2e_n = min(shard, E2E_EDGES)
+        e2e_times = []
+        for k in range(1 + args.e2e_steps):
             barrier()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            for _ in range(steps):
-                counts.zero_()
-                pb.parallel.count_shard_device(q, K, a, b, counts=counts, probes=prb, device=dev)
-                pb.parallel.reduce_counts(counts, op="reduce")  # u32 words for the full histogram
-            e1.record(stream)
             torch.cuda.synchronize(dev)
-            c64 = pb.parallel.widen_counts(torch, counts, K)  # C4's counts are u32 in HBM; widened for the check
-            t = max_over_ranks(e0.elapsed_time(e1) / 1000.0)
-            if name == "full_c4" and rank == 0:
-                assert int(c64.sum().item()) == 2 * q.m
-            extra[name] = {"edges_per_s": q.m * steps / t, "ms_per_step": 1000 * t / steps,
-                           "n": cfg["n"], "d": cfg["d"], "K": K, "m": q.m,
-                           "int_ops_per_s_convention": q.m * steps / t * 2 * INT_OPS_PER_PROBE}
-            if name == "full_c4":
-                extra[name]["path"] = ("partitioned: targets pass with per-CTA bucket histogram, bucket "
-                                       "sort in shared memory, shared-memory slice counts (parba_hist.cuh); "
-                                       "no per-edge global atomics")
-            del counts
+            t0 = time.perf_counter()
+            arr, _ = pb.generate_block(lo, lo + e2e_n, p, device=dev)
+            dt = time.perf_counter() - t0
+            if k:
+                e2e_times.append(dt)
+            del arr
+        e2e_s = max_over_ranks(statistics.median(e2e_times))
+        e2e = {"value": e2e_n * ws / e2e_s, "unit": "edges/s", "h2d_bytes_per_step": 0,
+               "d2h_bytes_per_step": e2e_n * 4 * ws, "edges_per_step_per_gpu": e2e_n,
+               "host_threads_per_gpu": int(os.environ["PARBA_HOST_THREADS"]),
+               "api": "paper_1602_07106_b200.generate_block(lo, hi, p) -> fresh host (hi-lo,2) uint64 array: "
+                      "device generates u32 targets, 4 B/edge over PCIe into pinned staging, host threads "
+                      "fill (source, target) rows (C ABI parba_generate_host)",
+               "h2d_note": "the generator has no input data: only (n, d, seed, range) scalars cross by value"}
 
+    # ---------------- streaming modes: C3 window, C4 full histogram, C5 the
+    # paper's demo (1e12 edges).  Device time per step includes the NCCL
+    # reduce of the histogram (N > 1); max over ranks.
+    extra = {}
+    int_peak = peaks.get("int32_lane_ops_per_s")
+    if not args.no_extra_modes:
+        todo = [("window_c3", C3, C3["K"], 2), ("full_c4", C4, C4["n"], 5), ("window_c5", C5, C5["K"], 1)]
+        if args.only:
+            todo = [t for t in todo if t[0] == args.only]
+        with ClockSampler(local) as clk_modes:
+            for name, cfg, K, steps in todo:
+                q = pb.GenParams(n=cfg["n"], d=cfg["d"])
+                a, b = pb.parallel.shard_range(0, q.m, rank, ws)
+                full = name == "full_c4"
+                counts = torch.zeros(K, dtype=torch.int32 if full else torch.int64, device=dev)
+                prb = torch.zeros(1, dtype=torch.int64, device=dev)
+                # warm-up on a slice (attributes, tables, allocator)
+                w = min(b - a, 10**9 if not full else b - a)
+                pb.parallel.count_shard_device(q, K, b - w, b, counts=counts, probes=prb, device=dev)
+                torch.cuda.synchronize(dev)
+                prb.zero_()
+                barrier()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for _ in range(steps):
+                    counts.zero_()
+                    pb.parallel.count_shard_device(q, K, a, b, counts=counts, probes=prb, device=dev)
+                    pb.parallel.reduce_counts(counts, op="reduce")  # u32 words for the full histogram
+                e1.record(stream)
+                torch.cuda.synchronize(dev)
+                t_rank = e0.elapsed_time(e1) / 1000.0
+                t = max_over_ranks(t_rank)
+                c64 = pb.parallel.widen_counts(torch, counts, K)
+                if full and rank == 0:
+                    assert int(c64.sum().item()) == 2 * q.m
+                eps = q.m * steps / t
+                ppe = int(prb.item()) / ((b - a) * steps)
+                extra[name] = {"edges_per_s": eps, "ms_per_step": 1000 * t / steps,
+                               "per_rank_ms_per_step": [1000 * x / steps for x in gather(t_rank)],
+                               "n": cfg["n"], "d": cfg["d"], "K": K, "m": q.m, "probes_per_edge": ppe,
+                               "steps": steps}
+                if int_peak:
+                    ach = eps / ws * 2 * INT_OPS_PER_PROBE  # per GPU, SURVEY 8d convention: 64 lane-ops/edge
+                    extra[name]["roofline"] = {
+                        "bound": "int", "achieved": ach, "peak": int_peak, "unit": "int32 lane-ops/s per GPU",
+                        "frac": ach / int_peak, "traffic": None,
+                        "convention": "32 int32 lane-ops per hash probe, 2 probes per edge (SURVEY 8d)",
+                        "peak_source": "measured in this run (parba_peak_int32)"}
+                if full:
+                    extra[name]["path"] = ("partitioned: targets pass with per-CTA bucket histogram, bucket "
+                                           "sort in shared memory, shared-memory slice counts (parba_hist.cuh)")
+                del counts
+        if extra:
+            extra["clocks"] = clk_modes.summary()
+    if args.only:
+        if rank == 0:
+            print(json.dumps({"only": args.only, "modes": extra}), flush=True)
+        if ws > 1:
+            dist.destroy_process_group()
+        return
+
+    kms = gather(statistics.mean(kern_ms))
     if rank != 0:
         dist.destroy_process_group() if ws > 1 else None
         return
+    peak, peak_src = _peaks()
+    avg_kernel_s = kms[0] / 1000.0
+    achieved_gbs = shard * BYTES_PER_EDGE / avg_kernel_s / 1e9
     # DRAM bytes per launch from the committed `ncu --set full` capture of this
     # kernel (profiles/store_traffic.json: dram__bytes_read+write per edge)
     traffic = None
@@ -356,6 +574,7 @@ def main() -> None:
         with open(tpath) as fh:
             per_edge = json.load(fh).get("dram_bytes_per_edge")
             traffic = per_edge * shard if per_edge else None
+    wo = peaks.get("write_only_gbs")
     line = {
         "metric": METRIC,
         "value": value, "unit": "edges/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
@@ -365,13 +584,15 @@ def main() -> None:
         "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
                      "frac": achieved_gbs / peak, "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": shard * BYTES_PER_EDGE,
-                     # also against a write-only peak measured on this pool
-                     # (tools/micro.cu, profiles/r01_micro.json: 6867.6 GB/s)
-                     "frac_of_write_only_peak": achieved_gbs / WRITE_ONLY_GBS,
-                     "avg_kernel_ms": statistics.mean(kern_ms)},
+                     "avg_kernel_ms": kms[0], "per_rank_avg_kernel_ms": kms,
+                     # also against the write-only peak measured in this run
+                     "write_only_peak_gbs": wo, "frac_of_write_only_peak": achieved_gbs / wo if wo else None},
+        "peaks_measured": peaks,
         "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": args.steps,
-        "clocks": clk.summary(), "probes_per_edge": probes_per_edge, "modes": extra,
+        "clocks": clk.summary() if clk else None, "probes_per_edge": probes_per_edge, "modes": extra,
     }
+    if args.share_gpu:
+        line["debug"] = "share-gpu control-flow check: all ranks on cuda:0 over gloo; not a measurement"
     print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()

@@ -116,6 +116,14 @@ int parba_resolve_chains(const parba_params_t *p, const uint64_t *r0, uint64_t c
 int parba_generate(const parba_params_t *p, uint64_t lo, uint64_t hi, uint64_t *out_pairs,
                    unsigned long long *probes, void *stream);
 
+/* Store mode, targets column only: targets[i - lo] = (uint32) target of
+ * edge i for lo <= i < hi (the source is the closed form (i - m0) / d + n0,
+ * generator.py:163-169).  4 B per edge instead of 16: the host-array path
+ * (parba_generate_host) moves this over PCIe and fills the pairs on the
+ * host.  CRC hash, uniform degree, no option flags, n <= 2^32. */
+int parba_generate_targets(const parba_params_t *p, uint64_t lo, uint64_t hi, uint32_t *targets,
+                           unsigned long long *probes, void *stream);
+
 /* generate_edge on an arbitrary ID list (generator.py:172-181):
  * out_pairs[2k], out_pairs[2k+1] = edge ids[k].  Every id in [m0, m). */
 int parba_edges_at(const parba_params_t *p, const uint64_t *ids, uint64_t count,
@@ -185,21 +193,62 @@ int parba_degree_window_host(const parba_params_t *p_host_seed, uint64_t lo, uin
                              uint64_t K, int64_t *counts_host, uint64_t *probes_host, int device);
 
 /* Single-process multi-GPU run over [m0, m) (parba_multi_run;
- * the fork workers + Consumer.merge of driver.py:210-270): contiguous shards
- * on devs[0..ndev), one host thread per device (a device may repeat).
+ * the fork workers + Consumer.merge of driver.py:210-270, analytics.py:78-99):
+ * equal contiguous shards on devs[0..ndev), one host thread per distinct
+ * device (a device may repeat: its shards run back to back into one
+ * histogram).
  *   PARBA_MULTI_STORE   out_host = host u64 pairs [2*(m - m0)] (edge i at row i - m0)
  *   PARBA_MULTI_WINDOW  out_host = host int64 counts[K], +=
  *   PARBA_MULTI_FULL    out_host = host int64 counts[n], += (needs 2m < 2^32)
  *   PARBA_MULTI_DISCARD out_host unused (probes and time only)
- * Counts are summed on devs[0] (peer copies + an add kernel).  probes_host
- * and device_seconds (max shard device time + the reduction) are optional.
- * Uniform degree only (host entry point); option flags cut at node boundaries. */
+ * The distinct devices' histograms are summed by one ncclReduce (SUM, root
+ * devs[0]; NCCL loaded at run time) -- the DegreeCountConsumer.merge of
+ * analytics.py:78-82.  probes_host and device_seconds (max over devices of
+ * generation + reduction) are optional.  Uniform degree only (host entry
+ * point); option flags cut at node boundaries. */
 #define PARBA_MULTI_STORE 0
 #define PARBA_MULTI_WINDOW 1
 #define PARBA_MULTI_FULL 2
 #define PARBA_MULTI_DISCARD 3
 int parba_multi_run(const parba_params_t *p_host_seed, int ndev, const int *devs, int mode, uint64_t K,
                     void *out_host, uint64_t *probes_host, double *device_seconds);
+/* The same with explicit shards: shard s = edges [los[s], his[s]) on device
+ * devs[s] (driver.run's worker batches, driver.py:161-207);
+ * probes_per_shard[s] (optional) = that shard's hash probes
+ * (WorkerStats.probes, driver.py:41-47).  Under option flags every cut must
+ * be a node boundary. */
+int parba_multi_run_shards(const parba_params_t *p_host_seed, int nshards, const int *devs,
+                           const uint64_t *los, const uint64_t *his, int mode, uint64_t K, void *out_host,
+                           uint64_t *probes_per_shard, double *device_seconds);
+
+/* ---- Remainder self-test (h % r, _kernels.py:32-42) --------------------
+ * The exact-remainder routines of the tile kernels, callable on arbitrary
+ * inputs so tests can pin them against integer division.  Methods: */
+#define PARBA_MOD_FP31 0              /* r < 2^31 (chain values of 2-chunk launches) */
+#define PARBA_MOD_FP_NARROW 1         /* r < 2^32                                  */
+#define PARBA_MOD_FP_WIDE 2           /* r < 2^52 (4- and 5-chunk launches)         */
+#define PARBA_MOD_INT 3               /* any r >= 1 (6 chunks, generic kernels)     */
+#define PARBA_MOD_FP31_SERIES 4       /* the same three with 1/r from phase 1's     */
+#define PARBA_MOD_FP_NARROW_SERIES 5  /* per-tile reciprocal series (r >= 2^27 + 224) */
+#define PARBA_MOD_FP_WIDE_SERIES 6
+/* out[k] = (hhi[k] * 2^32 + hlo[k]) mod r[k] by `method` (device buffers). */
+int parba_debug_mod(int method, const uint32_t *hhi, const uint32_t *hlo, const uint64_t *r, uint64_t count,
+                    uint64_t *out, void *stream);
+/* `count` (h, r) pairs drawn on the device from `seed` (r log-uniform in
+ * [rmin, rmax]; h uniform, next to a multiple of r, with an all-ones half,
+ * or below 2r), each compared with exact u64 %: *mismatches += failures,
+ * first_bad[0..2] = (h, r, result) of one failure.  Device buffers. */
+int parba_debug_mod_check(int method, uint64_t seed, uint64_t count, uint64_t rmin, uint64_t rmax,
+                          unsigned long long *mismatches, unsigned long long *first_bad, void *stream);
+
+/* ---- Roofline denominators (measured next to the kernels, bench.py) ----
+ * parba_peak_int32: launch an INT32 issue-rate kernel (LOP3 + IADD3 chains)
+ * on `stream`; *lane_ops = the lane-operations it executes (time it with
+ * events around the call).  scratch: one device u32.
+ * parba_peak_write: 16-byte streaming stores over buf[0, bytes) (write-only
+ * HBM bandwidth). */
+int parba_peak_int32(uint32_t *scratch, double *lane_ops, void *stream);
+int parba_peak_write(void *buf, uint64_t bytes, void *stream);
 
 #ifdef __cplusplus
 }

@@ -28,11 +28,13 @@ FLAG_NO_SELF_LOOPS, FLAG_NO_PARALLEL_EDGES = 1, 2
 # Every symbol include/parba_b200.h declares (checked by tests/test_boundary.py).
 EXPORTS = (
     "parba_version", "parba_last_error", "parba_device_count", "parba_hash",
-    "parba_resolve_chains", "parba_generate", "parba_edges_at", "parba_degree_window",
+    "parba_resolve_chains", "parba_generate", "parba_generate_targets", "parba_edges_at", "parba_degree_window",
     "parba_degree_full", "parba_count_ids", "parba_generate_host", "parba_degree_window_host",
     "parba_degseq_prefix", "parba_degseq_rank", "parba_rank1", "parba_node_of_edges", "parba_count_pairs",
-    "parba_multi_run", "parba_crc32c", "parba_mulhi_u64", "parba_degseq_dense",
+    "parba_multi_run", "parba_multi_run_shards", "parba_crc32c", "parba_mulhi_u64", "parba_degseq_dense",
+    "parba_peak_int32", "parba_peak_write", "parba_debug_mod", "parba_debug_mod_check",
 )
+MOD_FP31, MOD_FP_NARROW, MOD_FP_WIDE, MOD_INT, MOD_FP31_SERIES, MOD_FP_NARROW_SERIES, MOD_FP_WIDE_SERIES = range(7)
 MULTI_STORE, MULTI_WINDOW, MULTI_FULL, MULTI_DISCARD = 0, 1, 2, 3
 
 
@@ -89,6 +91,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
             "parba_hash": ([P, vp, u64, vp, vp], i32),
             "parba_resolve_chains": ([P, vp, u64, u64, vp, vp, vp], i32),
             "parba_generate": ([P, u64, u64, vp, vp, vp], i32),
+            "parba_generate_targets": ([P, u64, u64, vp, vp, vp], i32),
             "parba_edges_at": ([P, vp, u64, vp, vp, vp], i32),
             "parba_degree_window": ([P, u64, u64, u64, vp, vp, vp], i32),
             "parba_degree_full": ([P, u64, u64, vp, vp, vp], i32),
@@ -105,6 +108,11 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
             "parba_degseq_dense": ([vp, u64, u64, u64, vp, vp], i32),
             "parba_multi_run": ([P, i32, vp, i32, u64, vp, ctypes.POINTER(u64), ctypes.POINTER(ctypes.c_double)],
                                 i32),
+            "parba_debug_mod": ([i32, vp, vp, vp, u64, vp, vp], i32),
+            "parba_debug_mod_check": ([i32, u64, u64, u64, u64, vp, vp, vp], i32),
+            "parba_peak_int32": ([vp, ctypes.POINTER(ctypes.c_double), vp], i32),
+            "parba_peak_write": ([vp, u64, vp], i32),
+            "parba_multi_run_shards": ([P, i32, vp, vp, vp, i32, u64, vp, vp, ctypes.POINTER(ctypes.c_double)], i32),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name, None)

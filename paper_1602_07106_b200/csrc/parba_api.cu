@@ -135,7 +135,7 @@ int nc_for(uint64_t two_hi) {
 struct DevInfo {
     int sms = 0;
     int smem_optin = 0;  // max dynamic shared memory per block
-    bool attr_done[12][5][2] = {};  // [hash variant][sink][seed]
+    bool attr_done[12][kSinkKinds][2] = {};  // [hash variant][sink][seed]
 };
 std::mutex g_mu;
 std::vector<DevInfo> g_dev;
@@ -190,6 +190,7 @@ int launch_tiles_t(const DevParams &dp, uint64_t lo, uint64_t hi, const SinkArgs
         if (grid > need) grid = need;
         SinkArgs ac = a;
         if (SINK == kStore) ac.out = a.out + 2 * (a0 - lo);
+        if (SINK == kStoreT) ac.t32 = a.t32 + (a0 - lo);
         if (is_targets(SINK)) {  // one launch; every warp owns capw slots
             if (a1 != hi) return fail(PARBA_ECUDA, "targets pass needs one launch");
             const uint64_t nw = grid * warps;
@@ -236,6 +237,23 @@ int launch_tiles(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint
         case 4: return launch_tiles_s<HashCrc<4>, SINK>(p, dp, lo, hi, a, probes, st, 1);
         case 5: return launch_tiles_s<HashCrc<5>, SINK>(p, dp, lo, hi, a, probes, st, 2);
         default: return launch_tiles_s<HashCrc<6>, SINK>(p, dp, lo, hi, a, probes, st, 3);
+    }
+}
+
+// Targets-only store (kStoreT): CRC families with uniform degree and n <= 2^32
+// (callers check; parba_host.cu's host-array path).
+int launch_store_targets(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi, uint32_t *t32,
+                         unsigned long long *probes, cudaStream_t st) {
+    SinkArgs a{};
+    a.t32 = t32;
+    int nc = nc_for(2 * hi);
+    if (nc <= 3 && p->d >= (1ull << 31)) nc = 4;
+    switch (nc) {
+        case 2: return launch_tiles_s<HashCrc<2>, kStoreT>(p, dp, lo, hi, a, probes, st, 6);
+        case 3: return launch_tiles_s<HashCrc<3>, kStoreT>(p, dp, lo, hi, a, probes, st, 0);
+        case 4: return launch_tiles_s<HashCrc<4>, kStoreT>(p, dp, lo, hi, a, probes, st, 1);
+        case 5: return launch_tiles_s<HashCrc<5>, kStoreT>(p, dp, lo, hi, a, probes, st, 2);
+        default: return launch_tiles_s<HashCrc<6>, kStoreT>(p, dp, lo, hi, a, probes, st, 3);
     }
 }
 
@@ -290,6 +308,10 @@ int launch_store(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint
                  unsigned long long *probes, cudaStream_t st) {
     SinkArgs a{out, nullptr, nullptr};
     return launch_tiles<kStore>(p, dp, lo, hi, a, probes, st);
+}
+int launch_store_t32(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi, uint32_t *t32,
+                     unsigned long long *probes, cudaStream_t st) {
+    return launch_store_targets(p, dp, lo, hi, t32, probes, st);
 }
 }  // namespace host
 }  // namespace parba
@@ -388,6 +410,20 @@ int parba_generate(const parba_params_t *p, uint64_t lo, uint64_t hi, uint64_t *
     }
     SinkArgs a{out_pairs, nullptr, nullptr};
     return launch_tiles<kStore>(p, dp, lo, hi, a, probes, st);
+}
+
+int parba_generate_targets(const parba_params_t *p, uint64_t lo, uint64_t hi, uint32_t *targets,
+                           unsigned long long *probes, void *stream) {
+    int rc = validate(p);
+    if (!rc) rc = check_range(p, lo, hi);
+    if (rc) return rc;
+    if (!targets_only_ok(p))
+        return fail(PARBA_EINVAL, "targets-only store needs the CRC hash, a uniform degree, no option flags "
+                                  "and n <= 2^32");
+    if (hi == lo) return PARBA_OK;
+    if (!targets) return fail(PARBA_EINVAL, "targets is NULL");
+    if (((uintptr_t)targets) & 3) return fail(PARBA_EINVAL, "targets must be 4-byte aligned");
+    return launch_store_t32(p, make_dev(p), lo, hi, targets, probes, (cudaStream_t)stream);
 }
 
 int parba_edges_at(const parba_params_t *p, const uint64_t *ids, uint64_t count, uint64_t *out_pairs,
@@ -665,5 +701,69 @@ int parba_count_ids(const uint64_t *ids, uint64_t count, uint64_t K, unsigned lo
     return PARBA_OK;
 }
 
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Roofline denominators measured in the same run as the kernels they judge
+// (bench.py): an INT32 issue peak and a write-only HBM peak.
+
+namespace {
+
+constexpr int kPeakIters = 2048;  // x 8 unrolled x 8 chains x 2 ops
+
+__global__ void __launch_bounds__(256) int_peak_kernel(uint32_t *out, uint32_t seed) {
+    uint32_t a[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = seed + threadIdx.x * 7u + (uint32_t)k;
+    const uint32_t c = 0x9E3779B9u;
+    for (int i = 0; i < kPeakIters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                // one LOP3 and one IADD3 per step, emitted as written
+                asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(a[k]) : "r"(c), "r"((uint32_t)u));
+                asm volatile("add.u32 %0, %0, %1;" : "+r"(a[k]) : "r"(c));
+            }
+        }
+    }
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s ^= a[k];
+    if (s == 0x12345678u) out[0] = s;
+}
+
+__global__ void write_peak_kernel(ulonglong2 *out, uint64_t n) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        __stcs(out + i, make_ulonglong2(i, i ^ 0x5555ull));
+}
+
+}  // namespace
+
+extern "C" {
+
+int parba_peak_int32(uint32_t *scratch, double *lane_ops, void *stream) {
+    if (!scratch || !lane_ops) return fail(PARBA_EINVAL, "NULL buffer");
+    DevInfo *di;
+    int rc = dev_info(&di);
+    if (rc) return rc;
+    const unsigned blocks = (unsigned)di->sms * 8, threads = 256;
+    int_peak_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(scratch, 1u);
+    CUDA_TRY(cudaGetLastError());
+    *lane_ops = (double)blocks * threads * kPeakIters * 8.0 * 8.0 * 2.0;
+    return PARBA_OK;
+}
+
+int parba_peak_write(void *buf, uint64_t bytes, void *stream) {
+    if (!buf) return fail(PARBA_EINVAL, "NULL buffer");
+    if (((uintptr_t)buf) & 15) return fail(PARBA_EINVAL, "buffer must be 16-byte aligned");
+    DevInfo *di;
+    int rc = dev_info(&di);
+    if (rc) return rc;
+    write_peak_kernel<<<(unsigned)di->sms * 8, 512, 0, (cudaStream_t)stream>>>((ulonglong2 *)buf, bytes / 16);
+    CUDA_TRY(cudaGetLastError());
+    return PARBA_OK;
+}
 
 }  // extern "C"

@@ -92,6 +92,14 @@ int read_u64s(const uint64_t *dptr, uint64_t *out, size_t n, cudaStream_t st);
 int launch_store(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi, uint64_t *out,
                  unsigned long long *probes, cudaStream_t st);
 
+// Targets-only store (the u32 target of each edge in edge order): CRC,
+// uniform degree, no option flags, n <= 2^32 (see targets_only_ok).
+int launch_store_t32(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi, uint32_t *t32,
+                     unsigned long long *probes, cudaStream_t st);
+inline bool targets_only_ok(const parba_params_t *p) {
+    return !is_deg(p) && !p->flags && p->hash_kind == PARBA_HASH_CRC && p->n <= (1ull << 32);
+}
+
 // Node-granular paths (parba_nodes_api.cu): option flags and degree sequences.
 int win_rlim_deg(const parba_params_t *p, DevParams &dp, uint64_t K, cudaStream_t st);
 int boundary_node(const parba_params_t *p, const DevParams &dp, uint64_t pos, uint64_t *v, cudaStream_t st);

@@ -311,8 +311,11 @@ __device__ __forceinline__ uint64_t mod_int(uint32_t hhi, uint32_t hlo, uint64_t
     int64_t x = (int64_t)((uint64_t)hhi - (uint64_t)qa * r);
     x += (x < 0) ? (int64_t)r : 0;                     // x = hhi mod r < 2^32
     const uint64_t v = ((uint64_t)x << 32) | hlo;      // < r * 2^32, no overflow
-    const uint32_t qb = (uint32_t)__double2loint(fma(u64_halves_to_f64((uint32_t)x, hlo), y, 0x1p52));
-    int64_t t = (int64_t)(v - (uint64_t)qb * r);       // in [-r, r): fits for r <= 2^63
+    // qb = round(v / r) may be 2^32 itself (x = r - 1, hlo near 2^32 - 1, r <=
+    // 2^32): read all of it from the mantissa of 2^52 + qb, not its low word
+    const uint64_t qb = (uint64_t)__double_as_longlong(fma(u64_halves_to_f64((uint32_t)x, hlo), y, 0x1p52)) -
+                        0x4330000000000000ull;
+    int64_t t = (int64_t)(v - qb * r);                 // in [-r, r) (mod 2^64 arithmetic), r <= 2^63
     t += (t < 0) ? (int64_t)r : 0;
     return (uint64_t)t;
 }

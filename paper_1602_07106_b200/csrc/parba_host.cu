@@ -3,7 +3,17 @@
 // single-process multi-GPU driver parba_multi_run.
 #include <cuda_runtime.h>
 
+#include <emmintrin.h>
+#include <sched.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
 #include <cstdint>
+#include <cstdlib>
+#include <map>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -47,8 +57,13 @@ int parba_generate_host(const parba_params_t *ph, uint64_t lo, uint64_t hi, uint
 
 namespace {
 
-// generate_block into host memory on one device; *ms (optional) = device
-// time from the first launch to the last copy.
+// generate_block into host memory on one device; *ms (optional) = time
+// from the first launch to the last row in host memory.
+int generate_host_pairs(const parba_params_t *ph, uint64_t lo, uint64_t hi, uint64_t *out_host,
+                        uint64_t *probes_host, int device, float *ms);
+int generate_host_targets(const parba_params_t *ph, uint64_t lo, uint64_t hi, uint64_t *out_host,
+                          uint64_t *probes_host, int device, float *ms);
+
 int generate_host_impl(const parba_params_t *ph, uint64_t lo, uint64_t hi, uint64_t *out_host,
                        uint64_t *probes_host, int device, float *ms) {
     if (ph && is_deg(ph)) return fail(PARBA_EINVAL, "host entry points take uniform-degree families only");
@@ -59,10 +74,22 @@ int generate_host_impl(const parba_params_t *ph, uint64_t lo, uint64_t hi, uint6
     if (ms) *ms = 0.f;
     if (hi == lo) return PARBA_OK;
     if (!out_host) return fail(PARBA_EINVAL, "out_pairs_host is NULL");
+    const char *mode = getenv("PARBA_HOST_PAIRS");  // A/B: 16-byte rows over PCIe
+    if (targets_only_ok(ph) && !(mode && mode[0] == '1'))
+        return generate_host_targets(ph, lo, hi, out_host, probes_host, device, ms);
+    return generate_host_pairs(ph, lo, hi, out_host, probes_host, device, ms);
+}
+
+// ---- pairs pipeline (SIMPLE hash, option flags, n > 2^32): 16-byte rows
+// generated on the device in chunks, copied straight into the caller's
+// array while the next chunk is generated.  *ms = device time from the
+// first launch to the last copy.
+int generate_host_pairs(const parba_params_t *ph, uint64_t lo, uint64_t hi, uint64_t *out_host,
+                        uint64_t *probes_host, int device, float *ms) {
     CUDA_TRY(cudaSetDevice(device));
     parba_params_t pd;
     DevBuf seed, bufs, prb;
-    rc = upload_seed(ph, &pd, seed);
+    int rc = upload_seed(ph, &pd, seed);
     if (rc) return rc;
     // Two chunk buffers: the kernel fills one while the other drains over PCIe.
     const uint64_t total = hi - lo;
@@ -107,6 +134,179 @@ int generate_host_impl(const parba_params_t *ph, uint64_t lo, uint64_t hi, uint6
     return PARBA_OK;
 }
 
+
+// ---- targets-only pipeline: the device writes the u32 target of every edge
+// (4 B instead of 16), the copy engine moves it into pinned staging, and a
+// team of host threads expands each staged chunk into (source, target) rows
+// of the caller's array -- the source is the closed form (i - m0) / d + n0
+// (generator.py:163-169), counted up edge by edge, and the rows are written
+// with 16-byte streaming stores.  GPU, PCIe and host memory overlap over a
+// ring of kSlots staging buffers; the host write (16 B per edge + 4 B read)
+// is the bound (tools/host_probe.cu).
+
+constexpr int kSlots = 3;
+constexpr uint64_t kTgtChunk = 1ull << 24;  // edges per chunk (64 MiB of targets)
+
+// Staging per device, kept for the life of the process (pinned allocation
+// costs more than a chunk's work); one host-array call per device at a time.
+struct Staging {
+    std::mutex use;
+    uint32_t *host = nullptr;  // kSlots * kTgtChunk, pinned
+    uint32_t *dev = nullptr;   // 2 * kTgtChunk on the device
+};
+
+Staging &staging_for(int device) {
+    static std::mutex mu;
+    static std::map<int, Staging *> all;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = all.find(device);
+    if (it == all.end()) it = all.emplace(device, new Staging).first;
+    return *it->second;
+}
+
+int host_threads() {
+    if (const char *e = getenv("PARBA_HOST_THREADS")) {
+        const int t = atoi(e);
+        if (t > 0) return t;
+    }
+    cpu_set_t cs;
+    CPU_ZERO(&cs);
+    int n = 0;
+    if (sched_getaffinity(0, sizeof(cs), &cs) == 0) n = CPU_COUNT(&cs);
+    if (n <= 0) n = (int)std::thread::hardware_concurrency();
+    return n > 0 ? n : 1;
+}
+
+// rows[k] = ((lo0 + k - m0) / d + n0, tgt[k]) for k in [a, b)
+void expand_rows(uint64_t *rows, const uint32_t *tgt, uint64_t i0, uint64_t a, uint64_t b, const parba_params_t *p,
+                 bool nt) {
+    if (b <= a) return;
+    const uint64_t e = i0 + a - p->m0;
+    uint64_t src = e / p->d + p->n0, rem = e % p->d;
+    const uint64_t d = p->d;
+    if (nt) {
+        __m128i *o = reinterpret_cast<__m128i *>(rows);
+        for (uint64_t k = a; k < b; ++k) {
+            _mm_stream_si128(o + k, _mm_set_epi64x((long long)tgt[k], (long long)src));
+            if (++rem == d) {
+                rem = 0;
+                ++src;
+            }
+        }
+        _mm_sfence();
+    } else {
+        for (uint64_t k = a; k < b; ++k) {
+            rows[2 * k] = src;
+            rows[2 * k + 1] = tgt[k];
+            if (++rem == d) {
+                rem = 0;
+                ++src;
+            }
+        }
+    }
+}
+
+int generate_host_targets(const parba_params_t *ph, uint64_t lo, uint64_t hi, uint64_t *out_host,
+                          uint64_t *probes_host, int device, float *ms) {
+    const auto w0 = std::chrono::steady_clock::now();
+    CUDA_TRY(cudaSetDevice(device));
+    Staging &sg = staging_for(device);
+    std::lock_guard<std::mutex> use(sg.use);
+    if (!sg.host) CUDA_TRY(cudaHostAlloc((void **)&sg.host, kSlots * kTgtChunk * 4, cudaHostAllocPortable));
+    if (!sg.dev) CUDA_TRY(cudaMalloc((void **)&sg.dev, 2 * kTgtChunk * 4));
+    parba_params_t pd;
+    DevBuf seed, prb;
+    int rc = upload_seed(ph, &pd, seed);
+    if (rc) return rc;
+    const DevParams dp = make_dev(&pd);
+    CUDA_TRY(cudaMalloc(&prb.p, sizeof(unsigned long long)));
+    StreamGuard sc, sx;
+    CUDA_TRY(cudaStreamCreateWithFlags(&sc.s, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&sx.s, cudaStreamNonBlocking));
+    CUDA_TRY(cudaMemsetAsync(prb.p, 0, sizeof(unsigned long long), sc.s));
+    EventGuard made[2], copied[kSlots];
+    for (auto &e : made) CUDA_TRY(cudaEventCreateWithFlags(&e.e, cudaEventDisableTiming));
+    for (auto &e : copied) CUDA_TRY(cudaEventCreateWithFlags(&e.e, cudaEventDisableTiming | cudaEventBlockingSync));
+    const uint64_t total = hi - lo;
+    const int64_t nchunks = (int64_t)((total + kTgtChunk - 1) / kTgtChunk);
+    const bool nt = (((uintptr_t)out_host) & 15) == 0;
+    auto chunk_lo = [&](int64_t k) { return lo + (uint64_t)k * kTgtChunk; };
+    auto chunk_n = [&](int64_t k) { return std::min(kTgtChunk, hi - chunk_lo(k)); };
+
+    // GPU side of chunk k: targets into device buffer k % 2, then into slot k % kSlots
+    auto enqueue = [&](int64_t k) -> int {
+        const int d = (int)(k & 1), s = (int)(k % kSlots);
+        uint32_t *dbuf = sg.dev + (uint64_t)d * kTgtChunk;
+        if (k >= 2) CUDA_TRY(cudaStreamWaitEvent(sc.s, copied[(k - 2) % kSlots].e, 0));  // device buffer free
+        int r = launch_store_t32(&pd, dp, chunk_lo(k), chunk_lo(k) + chunk_n(k), dbuf,
+                                 (unsigned long long *)prb.p, sc.s);
+        if (r) return r;
+        CUDA_TRY(cudaEventRecord(made[d].e, sc.s));
+        CUDA_TRY(cudaStreamWaitEvent(sx.s, made[d].e, 0));
+        CUDA_TRY(cudaMemcpyAsync(sg.host + (uint64_t)s * kTgtChunk, dbuf, chunk_n(k) * 4, cudaMemcpyDeviceToHost,
+                                 sx.s));
+        CUDA_TRY(cudaEventRecord(copied[s].e, sx.s));
+        return PARBA_OK;
+    };
+
+    // host team: worker w expands slice w of every chunk, in chunk order
+    const int T = host_threads();
+    std::mutex mu;
+    std::condition_variable cv_work, cv_main;
+    int64_t enq = 0;                  // chunks enqueued (guarded by mu)
+    int finished[kSlots] = {};        // workers done with the slot's current chunk (mu)
+    bool abort = false;               // (mu)
+    std::atomic<int> werr{0};
+    auto worker = [&](int w) {
+        for (int64_t k = 0; k < nchunks; ++k) {
+            {
+                std::unique_lock<std::mutex> lk(mu);
+                cv_work.wait(lk, [&] { return enq > k || abort; });
+                if (abort) return;
+            }
+            const int s = (int)(k % kSlots);
+            if (cudaEventSynchronize(copied[s].e) != cudaSuccess) werr = 1;
+            const uint64_t n = chunk_n(k);
+            uint64_t a = n * (uint64_t)w / T, b = n * (uint64_t)(w + 1) / T;
+            if (!werr) expand_rows(out_host + 2 * (chunk_lo(k) - lo), sg.host + (uint64_t)s * kTgtChunk, chunk_lo(k),
+                                   a, b, ph, nt);
+            std::lock_guard<std::mutex> lk(mu);
+            if (++finished[s] == T) cv_main.notify_one();
+        }
+    };
+    for (int64_t k = 0; k < std::min<int64_t>(kSlots, nchunks); ++k) {
+        if ((rc = enqueue(k))) return rc;
+        enq = k + 1;  // no worker runs yet
+    }
+    std::vector<std::thread> team;
+    for (int w = 0; w < T; ++w) team.emplace_back(worker, w);
+    for (int64_t k = 0; k < nchunks && !rc; ++k) {
+        const int s = (int)(k % kSlots);
+        std::unique_lock<std::mutex> lk(mu);
+        cv_main.wait(lk, [&] { return finished[s] == T; });
+        finished[s] = 0;
+        if (k + kSlots < nchunks) {
+            lk.unlock();
+            rc = enqueue(k + kSlots);
+            lk.lock();
+            if (rc) abort = true;
+            else enq = k + kSlots + 1;
+        }
+        lk.unlock();
+        cv_work.notify_all();
+    }
+    for (auto &t : team) t.join();
+    if (rc) return rc;
+    if (werr) return fail(PARBA_ECUDA, "waiting for a staged chunk failed");
+    unsigned long long pr = 0;
+    CUDA_TRY(cudaMemcpyAsync(&pr, prb.p, sizeof(pr), cudaMemcpyDeviceToHost, sc.s));
+    CUDA_TRY(cudaStreamSynchronize(sc.s));
+    CUDA_TRY(cudaStreamSynchronize(sx.s));
+    if (probes_host) *probes_host = pr;
+    if (ms) *ms = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - w0).count();
+    return PARBA_OK;
+}
+
 }  // namespace
 
 int parba_degree_window_host(const parba_params_t *ph, uint64_t lo, uint64_t hi, uint64_t K,
@@ -141,103 +341,285 @@ int parba_degree_window_host(const parba_params_t *ph, uint64_t lo, uint64_t hi,
     return PARBA_OK;
 }
 
-// ---------------------------------------------------------------------------
-// Single-process multi-GPU driver (SURVEY.md 8b parba_multi_run): contiguous
-// shards on `ndev` devices driven by one host thread each; degree counts are
-// summed on devs[0] (peer copies over NVLink + an add kernel) and returned
-// once.  torch.distributed / NCCL serve the one-process-per-GPU path
-// (paper_1602_07106_b200.parallel); this entry point serves C / FFI callers.
-
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Single-process multi-GPU driver (SURVEY.md 8b parba_multi_run; the fork
+// workers + Consumer.merge of driver.py:210-270 / analytics.py:78-82).
+//
+// Shards are contiguous edge ranges, each bound to a device.  One host thread
+// per distinct device runs that device's shards back to back on one stream,
+// accumulating degree counts into ONE device histogram (counts are +=), so a
+// device that appears several times costs no extra reduction.  The distinct
+// devices' histograms are then summed by one NCCL reduce (SUM, root = the
+// first device) over NVLink -- the only collective on this path -- and the
+// root's histogram is added into the caller's host array.  NCCL is loaded at
+// run time (dlopen: the copy torch already loaded, else the system one), so
+// the library has no link-time NCCL dependency.
+
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <map>
+#include <mutex>
 
 namespace {
 
-template <typename T>
-__global__ void add_counts_kernel(T *acc, const T *__restrict__ x, uint64_t n) {
-    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x)
-        acc[k] += x[k];
-}
-
-struct ShardRun {
-    int dev = 0;
-    uint64_t a = 0, b = 0;
-    int rc = PARBA_OK;
-    std::string err;
-    uint64_t probes = 0;
-    float ms = 0.f;
-    void *counts = nullptr;  // device counts of this shard (modes 1, 2)
+struct NcclApi {
+    decltype(&ncclCommInitAll) init_all = nullptr;
+    decltype(&ncclReduce) reduce = nullptr;
+    decltype(&ncclGroupStart) group_start = nullptr;
+    decltype(&ncclGroupEnd) group_end = nullptr;
+    decltype(&ncclGetErrorString) error_string = nullptr;
+    decltype(&ncclGetVersion) get_version = nullptr;
+    std::string why;  // non-empty when NCCL could not be loaded
 };
 
-void run_shard(const parba_params_t *ph, int mode, uint64_t K, ShardRun &s, void *out_host) {
-    auto done = [&](int rc) {
-        s.rc = rc;
-        if (rc) s.err = g_err;
-    };
-    if (mode == PARBA_MULTI_STORE) {
-        done(generate_host_impl(ph, s.a, s.b, (uint64_t *)out_host + 2 * (s.a - ph->m0), &s.probes, s.dev, &s.ms));
-        return;
-    }
-    if (cudaSetDevice(s.dev) != cudaSuccess) return done(fail(PARBA_ECUDA, "cudaSetDevice(%d) failed", s.dev));
-    parba_params_t pd;
-    DevBuf seed, prb;
-    int rc = upload_seed(ph, &pd, seed);
-    if (rc) return done(rc);
-    StreamGuard st;
-    EventGuard t0, t1;
-    if (cudaStreamCreateWithFlags(&st.s, cudaStreamNonBlocking) != cudaSuccess || cudaEventCreate(&t0.e) ||
-        cudaEventCreate(&t1.e) || cudaMalloc(&prb.p, 8) || cudaMemsetAsync(prb.p, 0, 8, st.s))
-        return done(fail(PARBA_ECUDA, "shard setup on device %d failed", s.dev));
-    const size_t bytes = mode == PARBA_MULTI_FULL ? (size_t)ph->n * 4 : (size_t)(K ? K : 1) * 8;
-    if (mode != PARBA_MULTI_DISCARD) {
-        if (cudaMalloc(&s.counts, bytes) || cudaMemsetAsync(s.counts, 0, bytes, st.s))
-            return done(fail(PARBA_ENOMEM, "count buffer of %zu bytes on device %d", bytes, s.dev));
-    }
-    cudaEventRecord(t0.e, st.s);
-    if (mode == PARBA_MULTI_FULL)
-        rc = parba_degree_full(&pd, s.a, s.b, (uint32_t *)s.counts, (unsigned long long *)prb.p, st.s);
-    else
-        rc = parba_degree_window(&pd, s.a, s.b, mode == PARBA_MULTI_DISCARD ? 0 : K,
-                                 (unsigned long long *)s.counts, (unsigned long long *)prb.p, st.s);
-    if (rc) return done(rc);
-    cudaEventRecord(t1.e, st.s);
-    unsigned long long pr = 0;
-    if (cudaMemcpyAsync(&pr, prb.p, 8, cudaMemcpyDeviceToHost, st.s) || cudaStreamSynchronize(st.s) ||
-        cudaEventElapsedTime(&s.ms, t0.e, t1.e))
-        return done(fail(PARBA_ECUDA, "shard on device %d: %s", s.dev, cudaGetErrorString(cudaGetLastError())));
-    s.probes = pr;
-    done(PARBA_OK);
+const NcclApi &nccl_api() {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        const char *names[] = {getenv("PARBA_NCCL_LIB"), "libnccl.so.2", "libnccl.so"};
+        void *h = nullptr;
+        for (const char *nm : names)  // a copy already in the process (torch's) first
+            if (nm && (h = dlopen(nm, RTLD_NOW | RTLD_NOLOAD))) break;
+        for (const char *nm : names)
+            if (!h && nm) h = dlopen(nm, RTLD_NOW | RTLD_LOCAL);
+        if (!h) {
+            const char *e = dlerror();
+            api.why = e ? e : "libnccl.so.2 not found";
+            return;
+        }
+        api.init_all = (decltype(api.init_all))dlsym(h, "ncclCommInitAll");
+        api.reduce = (decltype(api.reduce))dlsym(h, "ncclReduce");
+        api.group_start = (decltype(api.group_start))dlsym(h, "ncclGroupStart");
+        api.group_end = (decltype(api.group_end))dlsym(h, "ncclGroupEnd");
+        api.error_string = (decltype(api.error_string))dlsym(h, "ncclGetErrorString");
+        api.get_version = (decltype(api.get_version))dlsym(h, "ncclGetVersion");
+        if (!api.init_all || !api.reduce || !api.group_start || !api.group_end || !api.error_string)
+            api.why = "libnccl is missing ncclCommInitAll / ncclReduce / ncclGroupStart / ncclGroupEnd";
+    });
+    return api;
 }
 
-// Sum the shards' device counts on devs[0] and add them into the host array.
-template <typename T>
-int reduce_shards(std::vector<ShardRun> &sh, uint64_t n, int64_t *out_host, float *ms) {
-    const int d0 = sh[0].dev;
-    CUDA_TRY(cudaSetDevice(d0));
-    StreamGuard st;
-    EventGuard t0, t1;
-    CUDA_TRY(cudaStreamCreateWithFlags(&st.s, cudaStreamNonBlocking));
-    CUDA_TRY(cudaEventCreate(&t0.e));
-    CUDA_TRY(cudaEventCreate(&t1.e));
-    CUDA_TRY(cudaEventRecord(t0.e, st.s));
-    DevBuf stage;
-    if (sh.size() > 1) CUDA_TRY(cudaMalloc(&stage.p, n * sizeof(T)));
-    for (size_t g = 1; g < sh.size(); ++g) {
-        CUDA_TRY(cudaMemcpyPeerAsync(stage.p, d0, sh[g].counts, sh[g].dev, n * sizeof(T), st.s));
-        add_counts_kernel<T><<<grid_for(n, 256), 256, 0, st.s>>>((T *)sh[0].counts, (const T *)stage.p, n);
-        CUDA_TRY(cudaGetLastError());
+#define NCCL_TRY(api, expr)                                                                              \
+    do {                                                                                                 \
+        ncclResult_t r_ = (expr);                                                                        \
+        if (r_ != ncclSuccess) return fail(PARBA_ECUDA, "%s failed: %s", #expr, (api).error_string(r_)); \
+    } while (0)
+
+// One communicator clique per distinct device list, created once per process
+// (ncclCommInitAll costs 0.1-1 s); a mutex per clique serialises its use.
+struct Clique {
+    std::vector<ncclComm_t> comms;
+    std::mutex use;
+};
+
+int get_clique(const std::vector<int> &devs, Clique **out) {
+    static std::mutex mu;
+    static std::map<std::vector<int>, Clique *> cache;
+    const NcclApi &api = nccl_api();
+    if (!api.why.empty()) return fail(PARBA_ECUDA, "NCCL unavailable: %s", api.why.c_str());
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(devs);
+    if (it == cache.end()) {
+        auto *c = new Clique;
+        c->comms.resize(devs.size());
+        ncclResult_t r = api.init_all(c->comms.data(), (int)devs.size(), devs.data());
+        if (r != ncclSuccess) {
+            delete c;
+            return fail(PARBA_ECUDA, "ncclCommInitAll(%zu devices) failed: %s", devs.size(), api.error_string(r));
+        }
+        it = cache.emplace(devs, c).first;  // kept for the life of the process
     }
-    std::vector<T> tmp(n);
-    CUDA_TRY(cudaMemcpyAsync(tmp.data(), sh[0].counts, n * sizeof(T), cudaMemcpyDeviceToHost, st.s));
-    CUDA_TRY(cudaEventRecord(t1.e, st.s));
-    CUDA_TRY(cudaStreamSynchronize(st.s));
-    CUDA_TRY(cudaEventElapsedTime(ms, t0.e, t1.e));
-    for (uint64_t v = 0; v < n; ++v) out_host[v] += (int64_t)tmp[v];
+    *out = it->second;
     return PARBA_OK;
+}
+
+// All shards of one distinct device.
+struct DeviceRun {
+    int dev = 0;
+    std::vector<int> shards;  // indices into the caller's shard arrays
+    int rc = PARBA_OK;
+    std::string err;
+    void *counts = nullptr;         // this device's histogram (count modes)
+    unsigned long long *prb = nullptr;  // one probe counter per shard
+    cudaStream_t st = nullptr;
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    float ms = 0.f;  // store mode: summed generate_host_impl device time
+    DevBuf seed;     // seed graph on this device (alive until the run ends)
+    DeviceRun() = default;
+    DeviceRun(const DeviceRun &) = delete;
+    DeviceRun &operator=(const DeviceRun &) = delete;
+    ~DeviceRun() {
+        if (counts || prb || st || t0 || t1 || seed.p) cudaSetDevice(dev);
+        if (counts) cudaFree(counts);
+        if (prb) cudaFree(prb);
+        if (t0) cudaEventDestroy(t0);
+        if (t1) cudaEventDestroy(t1);
+        if (st) cudaStreamDestroy(st);
+    }
+};
+
+size_t count_bytes(const parba_params_t *ph, int mode, uint64_t K) {
+    return mode == PARBA_MULTI_FULL ? (size_t)ph->n * 4 : (size_t)(K ? K : 1) * 8;
+}
+
+// Run every shard of `r` on its device; counts stay on the device.
+int run_device(const parba_params_t *ph, int mode, uint64_t K, const uint64_t *los, const uint64_t *his,
+               void *out_host, uint64_t *shard_probes, DeviceRun &r) {
+    if (mode == PARBA_MULTI_STORE) {
+        for (int s : r.shards) {
+            float ms = 0.f;
+            uint64_t pr = 0;
+            int rc = generate_host_impl(ph, los[s], his[s], (uint64_t *)out_host + 2 * (los[s] - ph->m0), &pr,
+                                        r.dev, &ms);
+            if (rc) return rc;
+            shard_probes[s] = pr;
+            r.ms += ms;
+        }
+        return PARBA_OK;
+    }
+    CUDA_TRY(cudaSetDevice(r.dev));
+    parba_params_t pd;
+    int rc = upload_seed(ph, &pd, r.seed);
+    if (rc) return rc;
+    CUDA_TRY(cudaStreamCreateWithFlags(&r.st, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreate(&r.t0));
+    CUDA_TRY(cudaEventCreate(&r.t1));
+    const size_t ns = r.shards.size();
+    CUDA_TRY(cudaMalloc((void **)&r.prb, ns * 8));
+    CUDA_TRY(cudaMemsetAsync(r.prb, 0, ns * 8, r.st));
+    const bool counted = mode != PARBA_MULTI_DISCARD && (mode == PARBA_MULTI_FULL || K > 0);
+    if (counted) {
+        const size_t bytes = count_bytes(ph, mode, K);
+        if (cudaMalloc(&r.counts, bytes) != cudaSuccess)
+            return fail(PARBA_ENOMEM, "count buffer of %zu bytes on device %d", bytes, r.dev);
+        CUDA_TRY(cudaMemsetAsync(r.counts, 0, bytes, r.st));
+    }
+    CUDA_TRY(cudaEventRecord(r.t0, r.st));
+    for (size_t j = 0; j < ns; ++j) {
+        const int s = r.shards[j];
+        if (mode == PARBA_MULTI_FULL)
+            rc = parba_degree_full(&pd, los[s], his[s], (uint32_t *)r.counts, r.prb + j, r.st);
+        else
+            rc = parba_degree_window(&pd, los[s], his[s], counted ? K : 0, (unsigned long long *)r.counts,
+                                     r.prb + j, r.st);
+        if (rc) return rc;
+    }
+    return PARBA_OK;  // probes are read after the reduction
+}
+
+template <typename T>
+void add_into(int64_t *out, const std::vector<T> &x, uint64_t n) {
+    for (uint64_t v = 0; v < n; ++v) out[v] += (int64_t)x[v];
 }
 
 }  // namespace
 
 extern "C" {
+
+int parba_multi_run_shards(const parba_params_t *ph, int nshards, const int *devs, const uint64_t *los,
+                           const uint64_t *his, int mode, uint64_t K, void *out_host, uint64_t *probes_per_shard,
+                           double *device_seconds) {
+    if (ph && is_deg(ph)) return fail(PARBA_EINVAL, "host entry points take uniform-degree families only");
+    int rc = validate(ph);
+    if (rc) return rc;
+    if (nshards < 1 || !devs || !los || !his) return fail(PARBA_EINVAL, "need nshards >= 1 shards with devices");
+    if (mode < PARBA_MULTI_STORE || mode > PARBA_MULTI_DISCARD) return fail(PARBA_EINVAL, "unknown mode %d", mode);
+    if (mode == PARBA_MULTI_FULL) K = ph->n;
+    if (!out_host && (mode == PARBA_MULTI_STORE || ((mode == PARBA_MULTI_WINDOW || mode == PARBA_MULTI_FULL) && K)))
+        return fail(PARBA_EINVAL, "out_host is NULL");
+    if (mode == PARBA_MULTI_FULL && 2 * (unsigned __int128)ph->m >= ((unsigned __int128)1 << 32))
+        return fail(PARBA_EINVAL, "full histogram needs 2m < 2^32 (uint32 counters); use the window mode");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess) ndev = 0;
+    for (int s = 0; s < nshards; ++s) {
+        if ((rc = check_range(ph, los[s], his[s]))) return rc;
+        if (devs[s] < 0 || devs[s] >= ndev) return fail(PARBA_EINVAL, "device %d of shard %d not visible", devs[s], s);
+    }
+    // group shards by distinct device, in order of first appearance
+    std::vector<int> udev;
+    for (int s = 0; s < nshards; ++s)
+        if (std::find(udev.begin(), udev.end(), devs[s]) == udev.end()) udev.push_back(devs[s]);
+    std::vector<DeviceRun> runs(udev.size());  // never resized: DeviceRun owns device memory
+    for (int s = 0; s < nshards; ++s) {
+        const size_t g = (size_t)(std::find(udev.begin(), udev.end(), devs[s]) - udev.begin());
+        runs[g].dev = devs[s];
+        runs[g].shards.push_back(s);
+    }
+    std::vector<uint64_t> probes(nshards, 0);
+    {
+        std::vector<std::thread> th;
+        for (auto &r : runs)
+            th.emplace_back([&, rp = &r] {
+                rp->rc = run_device(ph, mode, K, los, his, out_host, probes.data(), *rp);
+                if (rp->rc) rp->err = g_err;
+            });
+        for (auto &t : th) t.join();
+    }
+    for (auto &r : runs)
+        if (r.rc) return fail(r.rc, "device %d: %s", r.dev, r.err.c_str());
+    double secs = 0.0;
+    if (mode == PARBA_MULTI_STORE) {
+        for (auto &r : runs) secs = std::max(secs, (double)r.ms / 1000.0);
+    } else {
+        const bool counted = runs[0].counts != nullptr;
+        const char *force = getenv("PARBA_MULTI_NCCL");  // tests: NCCL even for one device
+        if (counted && (runs.size() > 1 || (force && force[0] == '1'))) {
+            Clique *cq = nullptr;
+            if ((rc = get_clique(udev, &cq))) return rc;
+            const NcclApi &api = nccl_api();
+            std::lock_guard<std::mutex> lk(cq->use);
+            const size_t n = mode == PARBA_MULTI_FULL ? ph->n : K;
+            const ncclDataType_t ty = mode == PARBA_MULTI_FULL ? ncclUint32 : ncclUint64;
+            NCCL_TRY(api, api.group_start());
+            for (size_t g = 0; g < runs.size(); ++g) {
+                CUDA_TRY(cudaSetDevice(runs[g].dev));
+                ncclResult_t r = api.reduce(runs[g].counts, runs[g].counts, n, ty, ncclSum, 0, cq->comms[g],
+                                            runs[g].st);
+                if (r != ncclSuccess) {
+                    api.group_end();
+                    return fail(PARBA_ECUDA, "ncclReduce failed: %s", api.error_string(r));
+                }
+            }
+            NCCL_TRY(api, api.group_end());
+        }
+        for (auto &r : runs) {
+            CUDA_TRY(cudaSetDevice(r.dev));
+            CUDA_TRY(cudaEventRecord(r.t1, r.st));
+        }
+        for (auto &r : runs) {
+            CUDA_TRY(cudaSetDevice(r.dev));
+            CUDA_TRY(cudaStreamSynchronize(r.st));
+            float ms = 0.f;
+            CUDA_TRY(cudaEventElapsedTime(&ms, r.t0, r.t1));
+            secs = std::max(secs, (double)ms / 1000.0);
+            std::vector<unsigned long long> pr(r.shards.size());
+            CUDA_TRY(cudaMemcpy(pr.data(), r.prb, pr.size() * 8, cudaMemcpyDeviceToHost));
+            for (size_t j = 0; j < pr.size(); ++j) probes[r.shards[j]] = pr[j];
+        }
+        if (counted) {  // the root's histogram (= the sum) into the caller's array
+            DeviceRun &r0 = runs[0];
+            CUDA_TRY(cudaSetDevice(r0.dev));
+            if (mode == PARBA_MULTI_FULL) {
+                std::vector<uint32_t> tmp(ph->n);
+                CUDA_TRY(cudaMemcpy(tmp.data(), r0.counts, ph->n * 4, cudaMemcpyDeviceToHost));
+                add_into((int64_t *)out_host, tmp, ph->n);
+            } else {
+                std::vector<unsigned long long> tmp(K);
+                CUDA_TRY(cudaMemcpy(tmp.data(), r0.counts, K * 8, cudaMemcpyDeviceToHost));
+                add_into((int64_t *)out_host, tmp, K);
+            }
+        }
+    }
+    if (probes_per_shard)
+        for (int s = 0; s < nshards; ++s) probes_per_shard[s] = probes[s];
+    if (device_seconds) *device_seconds = secs;
+    return PARBA_OK;
+}
 
 int parba_multi_run(const parba_params_t *ph, int ndev, const int *devs, int mode, uint64_t K, void *out_host,
                     uint64_t *probes_host, double *device_seconds) {
@@ -245,51 +627,23 @@ int parba_multi_run(const parba_params_t *ph, int ndev, const int *devs, int mod
     int rc = validate(ph);
     if (rc) return rc;
     if (ndev < 1 || !devs) return fail(PARBA_EINVAL, "need ndev >= 1 devices");
-    if (mode < PARBA_MULTI_STORE || mode > PARBA_MULTI_DISCARD) return fail(PARBA_EINVAL, "unknown mode %d", mode);
-    if (mode == PARBA_MULTI_FULL) K = ph->n;
-    if (!out_host && (mode == PARBA_MULTI_STORE || ((mode == PARBA_MULTI_WINDOW || mode == PARBA_MULTI_FULL) && K)))
-        return fail(PARBA_EINVAL, "out_host is NULL");
-    if (mode == PARBA_MULTI_FULL && 2 * (unsigned __int128)ph->m >= ((unsigned __int128)1 << 32))
-        return fail(PARBA_EINVAL, "full histogram needs 2m < 2^32 (uint32 counters); use the window mode");
     const uint64_t total = ph->m - ph->m0;
-    std::vector<ShardRun> sh(ndev);
+    std::vector<uint64_t> lo(ndev), hi(ndev), pr(ndev);
     for (int g = 0; g < ndev; ++g) {
-        sh[g].dev = devs[g];
-        sh[g].a = ph->m0 + (uint64_t)(((unsigned __int128)total * g) / ndev);
-        sh[g].b = ph->m0 + (uint64_t)(((unsigned __int128)total * (g + 1)) / ndev);
+        lo[g] = ph->m0 + (uint64_t)(((unsigned __int128)total * g) / ndev);
+        hi[g] = ph->m0 + (uint64_t)(((unsigned __int128)total * (g + 1)) / ndev);
         if (ph->flags) {  // node-granular: cut at node boundaries (uniform d)
-            if (g > 0) sh[g].a = node_first_edge(ph, ph->n0 + (sh[g].a - ph->m0) / ph->d);
-            if (g < ndev - 1) sh[g].b = node_first_edge(ph, ph->n0 + (sh[g].b - ph->m0) / ph->d);
+            if (g > 0) lo[g] = node_first_edge(ph, ph->n0 + (lo[g] - ph->m0) / ph->d);
+            if (g < ndev - 1) hi[g] = node_first_edge(ph, ph->n0 + (hi[g] - ph->m0) / ph->d);
         }
     }
-    std::vector<std::thread> th;
-    for (int g = 0; g < ndev; ++g) th.emplace_back(run_shard, ph, mode, K, std::ref(sh[g]), out_host);
-    for (auto &t : th) t.join();
-    rc = PARBA_OK;
-    std::string err;
-    uint64_t probes = 0;
-    float worst = 0.f;
-    for (auto &s : sh) {
-        if (s.rc && !rc) {
-            rc = s.rc;
-            err = s.err;
-        }
-        probes += s.probes;
-        worst = s.ms > worst ? s.ms : worst;
+    rc = parba_multi_run_shards(ph, ndev, devs, lo.data(), hi.data(), mode, K, out_host, pr.data(), device_seconds);
+    if (rc) return rc;
+    if (probes_host) {
+        uint64_t s = 0;
+        for (uint64_t x : pr) s += x;
+        *probes_host = s;
     }
-    float red_ms = 0.f;
-    if (!rc && mode == PARBA_MULTI_WINDOW && K)
-        rc = reduce_shards<unsigned long long>(sh, K, (int64_t *)out_host, &red_ms);
-    else if (!rc && mode == PARBA_MULTI_FULL)
-        rc = reduce_shards<uint32_t>(sh, K, (int64_t *)out_host, &red_ms);
-    for (auto &s : sh)
-        if (s.counts) {
-            cudaSetDevice(s.dev);
-            cudaFree(s.counts);
-        }
-    if (rc) return err.empty() ? rc : fail(rc, "%s", err.c_str());
-    if (probes_host) *probes_host = probes;
-    if (device_seconds) *device_seconds = (worst + red_ms) / 1000.0;
     return PARBA_OK;
 }
 

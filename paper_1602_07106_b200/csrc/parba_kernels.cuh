@@ -79,8 +79,14 @@ constexpr int kThreads = kWarps * 32;
 // targets it finishes to its own region of a scratch buffer (order is
 // irrelevant to a histogram); parba_hist.cuh partitions and counts them.
 // kTargetsK: the same for a window, keeping only targets < klim.
-enum SinkKind { kStore = 0, kWindow = 1, kFull = 2, kTargets = 3, kTargetsK = 4 };
+// kStoreT: store mode emitting only the u32 target of each edge, in edge
+// order (tgt[i - lo]); the source is a closed form the host fills in
+// (parba_host.cu: the end-to-end host-array path moves 4 B per edge over
+// PCIe instead of 16).
+enum SinkKind { kStore = 0, kWindow = 1, kFull = 2, kTargets = 3, kTargetsK = 4, kStoreT = 5 };
+constexpr int kSinkKinds = 6;
 __host__ __device__ constexpr bool is_targets(int sink) { return sink == kTargets || sink == kTargetsK; }
+__host__ __device__ constexpr bool is_store(int sink) { return sink == kStore || sink == kStoreT; }
 #ifndef PARBA_HIST_BUCKETS
 #define PARBA_HIST_BUCKETS 2048
 #endif
@@ -133,12 +139,12 @@ struct SinkArgs {
 template <class Hash, int SINK>
 struct TileLayout {
     using R = typename Hash::R;
-    static constexpr uint32_t kEB = SINK == kStore ? 8u : (uint32_t)sizeof(R);
+    static constexpr uint32_t kEB = is_store(SINK) ? 8u : (uint32_t)sizeof(R);
     static constexpr uint32_t kLgEB = kEB == 8 ? 3u : 2u;
     static constexpr uint32_t kQB = kQueue * kEB;
     static constexpr uint32_t kTB = kTile * (uint32_t)sizeof(R);  // one stage buffer
-    static constexpr uint32_t kStageB = SINK == kStore ? kStageBufs * kTB : 0;
-    static constexpr bool kSlots = SINK == kStore && !Hash::kPack;
+    static constexpr uint32_t kStageB = is_store(SINK) ? kStageBufs * kTB : 0;
+    static constexpr bool kSlots = is_store(SINK) && !Hash::kPack;
     static constexpr uint32_t kSlotB = kSlots ? kQueue * 2 : 0;
     static constexpr size_t kTabB = Hash::kHasCrc ? (Hash::kTableWords + kTile) * 4 : 0;
     static constexpr size_t kHistB = is_targets(SINK) ? kHistGroups * kHistBucketsMax * 4 : 0;
@@ -153,7 +159,7 @@ constexpr uint64_t kLaunchEdgesPerWarp = 1ull << 27;
 // A chain finished with terminal value r: hand its target to the sink.
 template <bool NARROW, bool SEED, int SINK, class R, bool DEG = false>
 __device__ __forceinline__ void finish(uint32_t saddr, uint64_t r, const DevParams &p, const SinkArgs &a) {
-    if constexpr (SINK == kStore) {
+    if constexpr (is_store(SINK)) {
         sts_t<R>(saddr, (R)r);  // stage cell; the target is computed at flush
     } else if constexpr (SINK == kWindow) {
         if (SEED && r < p.stop) {
@@ -169,7 +175,7 @@ __device__ __forceinline__ void finish(uint32_t saddr, uint64_t r, const DevPara
 }
 
 template <class Hash, int SINK, bool SEED, bool DEG = false>
-__global__ void __launch_bounds__(kThreads, SINK == kStore ? PARBA_MINB_STORE : PARBA_MINB_STREAM)
+__global__ void __launch_bounds__(kThreads, is_store(SINK) ? PARBA_MINB_STORE : PARBA_MINB_STREAM)
 tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntiles,
             SinkArgs a, unsigned long long *probes_out) {
     using R = typename Hash::R;
@@ -214,7 +220,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
     const uint64_t nw = (uint64_t)gridDim.x * wpc;
 
     // NS chains per lane in phase 2 (independent probes for the scheduler)
-    constexpr int NS = SINK == kStore ? PARBA_ILP_STORE : is_targets(SINK) ? PARBA_ILP_TARGETS : PARBA_ILP_STREAM;
+    constexpr int NS = is_store(SINK) ? PARBA_ILP_STORE : is_targets(SINK) ? PARBA_ILP_TARGETS : PARBA_ILP_STREAM;
     uint32_t act[NS];               // 1: slot holds a running chain
     R r[NS];
     uint32_t saddr[NS];             // store: smem address of the chain's stage cell
@@ -246,7 +252,18 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
     // Interior tiles (all but the range ends) skip the per-edge bounds test.
     auto flush_t = [&](auto full_c, uint32_t b, uint64_t base) {
         [[maybe_unused]] constexpr bool FULL = decltype(full_c)::value;
-        if constexpr (SINK == kStore) {
+        if constexpr (SINK == kStoreT) {
+            // targets only (n < 2^32): 4 B per edge, 128 B per warp store
+            uint32_t *o = a.t32 + (int64_t)(base - lo);
+#pragma unroll
+            for (int k = 0; k < kEpl; ++k) {
+                const uint32_t j = lane + 32u * k;
+                const uint64_t i = base + j;
+                if (FULL || (i >= lo && i < hi))
+                    __stcs(o + j, (uint32_t)target_of<NARROW, SEED, Hash::kR31, false>(
+                                      (uint64_t)lds_t<R>(stage_s + (b * kTile + j) * (uint32_t)sizeof(R)), p));
+            }
+        } else if constexpr (SINK == kStore) {
             ulonglong2 *o = reinterpret_cast<ulonglong2 *>(a.out) + (int64_t)(base - lo);
             if constexpr (FULL && !NARROW && !DEG) {
                 // 64-bit positions: one 64-bit division per lane and tile, then
@@ -279,7 +296,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
         }
     };
     auto flush = [&](uint32_t b, uint64_t base) {
-        if constexpr (SINK == kStore) {
+        if constexpr (is_store(SINK)) {
             __syncwarp();
             if (base >= lo && base + kTile <= hi) flush_t(std::true_type{}, b, base);
             else flush_t(std::false_type{}, b, base);
@@ -358,7 +375,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
             if constexpr (is_targets(SINK)) {
                 emit(fin != 0, (uint64_t)nr[q]);
             } else if (fin) {
-                if constexpr (SINK == kStore) PARBA_CHECK(saddr[q] - stage_s < L::kStageB);
+                if constexpr (is_store(SINK)) PARBA_CHECK(saddr[q] - stage_s < L::kStageB);
                 finish<NARROW, SEED, SINK, R, DEG>(saddr[q], (uint64_t)nr[q], p, a);
             }
         }
@@ -374,7 +391,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
         const uint32_t availb = tailb - headb;
         if (!act[Q] && (FULLQ || (rank << L::kLgEB) < availb)) {
             const uint32_t cur = headb + (rank << L::kLgEB);
-            if constexpr (SINK == kStore) {
+            if constexpr (is_store(SINK)) {
                 const uint64_t e = lds_u64(qaddr(cur));
                 if constexpr (NARROW) {
                     r[Q] = (R)(uint32_t)e;
@@ -436,14 +453,14 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
             }
             const bool done = is_done(r1);
             [[maybe_unused]] const uint32_t cell = stage_s + (buf * kTile + j) * (uint32_t)sizeof(R);
-            if constexpr (SINK == kStore)  // final unless pending
+            if constexpr (is_store(SINK))  // final unless pending
                 sts_t<R>(cell, r1);
             if constexpr (is_targets(SINK)) emit(valid && done, (uint64_t)r1);
-            else if constexpr (SINK != kStore) if (valid && done) finish<NARROW, SEED, SINK, R, DEG>(0u, (uint64_t)r1, p, a);
+            else if constexpr (!is_store(SINK)) if (valid && done) finish<NARROW, SEED, SINK, R, DEG>(0u, (uint64_t)r1, p, a);
             const bool pend = valid && !done;
             const unsigned m = ballot_all(pend);
             const uint32_t cur = tailb + (__popc(m & ltmask) << L::kLgEB);
-            if constexpr (SINK == kStore) {
+            if constexpr (is_store(SINK)) {
                 if constexpr (NARROW) {
                     sts_u64_if(pend, qaddr(cur), ((uint64_t)cell << 32) | (uint64_t)r1);
                 } else if constexpr (Hash::kPack) {
@@ -489,7 +506,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
             } while (headb <= lim);
         }
         // ---- store: flush the oldest tile in flight once none of its chains runs
-        if constexpr (SINK == kStore) {
+        if constexpr (is_store(SINK)) {
             if (have_prev) {
                 // oldest tile: t-1 (2 buffers) or t-2 (3 buffers)
                 const uint32_t pb = kStageBufs == 2 ? (buf ^ 1u) : (buf == 2 ? 0u : buf + 1);
@@ -539,7 +556,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
             a.hist[(uint64_t)b * kHistGroups * gridDim.x + (uint64_t)kHistGroups * blockIdx.x + g] = hist_s[i];
         }
     }
-    if constexpr (SINK == kStore) {
+    if constexpr (is_store(SINK)) {
         if constexpr (kStageBufs == 2) {
             if (have_prev) flush(buf ^ 1u, prev_base);
         } else {

@@ -126,16 +126,16 @@ class CollectConsumer(Consumer):
 def _round_down_to_node(p: GenParams, pos: int) -> int:
     if p.d is not None:
         return p.m0 + ((pos - p.m0) // p.d) * p.d
-    W = p.m0 + np.concatenate([[0], np.cumsum(p.degrees.astype(np.int64))])
-    k = int(np.searchsorted(W, pos, side="right")) - 1
+    W = p._host_W()  # cached prefix (the reference reuses p.prefix.W, driver.py:125-128)
+    k = int(np.searchsorted(W, np.uint64(pos), side="right")) - 1
     return int(W[k])
 
 
 def _next_node_boundary(p: GenParams, lo: int) -> int:
     if p.d is not None:
         return lo + p.d
-    W = p.m0 + np.concatenate([[0], np.cumsum(p.degrees.astype(np.int64))])
-    k = int(np.searchsorted(W, lo, side="right")) - 1
+    W = p._host_W()
+    k = int(np.searchsorted(W, np.uint64(lo), side="right")) - 1
     return lo + int(p.degrees[k])
 
 
@@ -164,9 +164,19 @@ def plan_batches(p: GenParams, batch_size: int, granularity: Granularity | None 
 
 def run(p: GenParams, consumer: Consumer, workers: int = 1, batch_size: int = DEFAULT_BATCH_SIZE,
         resolution: Resolution = "rank", device=None) -> tuple[Any, RunStats]:
-    """Generate every edge of [m0, m) exactly once into a fused consumer.
+    """Generate every edge of [m0, m) exactly once into a consumer.
 
-    Returns (merged consumer result, RunStats) like driver.py:210-270."""
+    Returns (merged consumer result, RunStats) like driver.py:210-270.  The
+    plan is the reference's (``plan_batches(p, batch_size)``); worker w takes
+    the contiguous group of batches [w*B//W, (w+1)*B//W) and runs it as one
+    fused launch on its GPU -- ``workers`` is a GPU count: the visible
+    devices round-robin from the current one, or all on ``device`` when
+    given (a device running several workers' groups runs them back to back).
+    Several GPUs in one process go through the C ABI's multi-device driver
+    (one NCCL reduce of the histograms).  Under an initialised
+    ``torch.distributed`` world each rank is one worker instead (its group of
+    batches on its GPU, histograms summed over NCCL).  ``RunStats.per_worker``
+    has one entry per worker whose batch and edge counts add up to the plan."""
     from . import analytics, io, parallel
     from .generator import generate_block
 
@@ -178,38 +188,110 @@ def run(p: GenParams, consumer: Consumer, workers: int = 1, batch_size: int = DE
     kind = type(consumer)
     if kind not in (analytics.DegreeCountConsumer, DiscardConsumer, io.EdgeFileWriter, CollectConsumer):
         return _run_generic(p, consumer, workers, batch_size, resolution, device, t0)
+    batches = plan_batches(p, batch_size)
+    rank, ws = parallel.world()
+    if ws > 1:
+        return _run_fused_ranks(p, consumer, batches, rank, ws, resolution, device, t0)
+    groups = parallel.split_batches(len(batches), workers)
+    ranges = parallel.group_ranges(p, batches, groups)
+    devices = parallel.worker_devices(workers, device)
     if isinstance(consumer, analytics.DegreeCountConsumer):
-        counts, probes, per = parallel.degree_counts_sharded(p, consumer.K, p.m0, p.m, device=device)
+        counts, probes = parallel.run_shards(p, "window", consumer.K, ranges, devices)
         merged = analytics.DegreeCounter(K=consumer.K, counts=counts)
     elif isinstance(consumer, DiscardConsumer):
-        _, probes, per = parallel.degree_counts_sharded(p, 0, p.m0, p.m, device=device)
+        _, probes = parallel.run_shards(p, "discard", 0, ranges, devices)
         merged = p.m - p.m0
     elif isinstance(consumer, io.EdgeFileWriter):
-        rank, ws = parallel.world()
-        a, b = parallel.shard_range_for(p, p.m0, p.m, rank, ws)
-        if ws > 1:
-            import torch.distributed as dist
-
-            dist.barrier()  # every rank has opened (and rank 0 sized) the file
-        nbytes, probes = consumer.write_range(p, a, b, device=device)
-        per = [(rank, b - a, probes)]
-        merged = nbytes
-        if ws > 1:
-            from .generator import _device
-
-            torch, dev = _device(device)
-            t = torch.tensor([nbytes, b - a, probes], dtype=torch.int64, device=dev)
-            gathered = [torch.zeros_like(t) for _ in range(ws)]
-            dist.all_gather(gathered, t)
-            per = [(r, int(g[1].item()), int(g[2].item())) for r, g in enumerate(gathered)]
-            merged = sum(int(g[0].item()) for g in gathered)
-            probes = sum(pr for _, _, pr in per)
-            dist.barrier()  # the file is complete on return
-    else:  # CollectConsumer
-        merged, probes = generate_block(p.m0, p.m, p, resolution=resolution, device=device)
-        per = [(0, p.m - p.m0, probes)]
+        probes = _write_file_shards(p, consumer, ranges, devices)
+        merged = 16 * (p.m - p.m0)
+    elif workers == 1:  # CollectConsumer on one GPU: the host-array block path
+        merged, pr = generate_block(p.m0, p.m, p, resolution=resolution, device=devices[0])
+        probes = [pr]
+    else:
+        merged, probes = parallel.run_shards(p, "store", 0, ranges, devices)
     elapsed = time.perf_counter() - t0
-    per_worker = tuple(WorkerStats(w, 1 if e else 0, e, pr, elapsed) for w, e, pr in per)
+    per_worker = tuple(WorkerStats(w, b - a, r1 - r0, pr, elapsed)
+                       for w, ((a, b), (r0, r1), pr) in enumerate(zip(groups, ranges, probes)))
+    return merged, RunStats(edges_emitted=sum(w.edges for w in per_worker),
+                            hash_probes=sum(w.probes for w in per_worker),
+                            elapsed=elapsed, per_worker=per_worker)
+
+
+def _write_file_shards(p: GenParams, consumer, ranges, devices) -> list[int]:
+    """EdgeFileWriter: each worker's range written from its device (a host
+    thread per distinct device; positional writes, so any order)."""
+    probes = [0] * len(ranges)
+    errors: list = []
+
+    def work(dv):
+        try:
+            for k, (a, b) in enumerate(ranges):
+                if devices[k] == dv and b > a:
+                    probes[k] = consumer.write_range(p, a, b, device=dv)[1]
+        except BaseException as e:  # re-raised below
+            errors.append(e)
+
+    udev = list(dict.fromkeys(devices))
+    if len(udev) == 1:
+        work(udev[0])
+    else:
+        ths = [threading.Thread(target=work, args=(dv,)) for dv in udev]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+    if errors:
+        raise errors[0]
+    return probes
+
+
+def _run_fused_ranks(p: GenParams, consumer, batches, rank: int, ws: int, resolution, device, t0):
+    """One worker per torch.distributed rank: this rank's group of batches on
+    its GPU; histograms summed over NCCL, stats all-gathered."""
+    import torch.distributed as dist
+
+    from . import analytics, io, parallel
+    from .generator import _device, generate_block
+
+    torch, dev = _device(device)
+    groups = parallel.split_batches(len(batches), ws)
+    a, b = parallel.group_ranges(p, batches, [groups[rank]])[0]
+    counts = None
+    if isinstance(consumer, (analytics.DegreeCountConsumer, DiscardConsumer)):
+        K = consumer.K if isinstance(consumer, analytics.DegreeCountConsumer) else 0
+        prb = torch.zeros(1, dtype=torch.int64, device=dev)
+        if K:
+            full = parallel._counts_kind(p, K) == "full"
+            counts = torch.zeros(K, dtype=torch.int32 if full else torch.int64, device=dev)
+        if b > a:
+            counts, _ = parallel.count_shard_device(p, K, a, b, counts=counts, probes=prb, device=dev)
+        if K:
+            # full histograms travel as 32-bit words (2m < 2^32, so the wrapped
+            # int32 sum has the exact bits): half the bytes of an int64 reduce
+            parallel.reduce_counts(counts)
+        probes = int(prb.item())
+        merged = (analytics.DegreeCounter(K=K, counts=parallel.widen_counts(torch, counts, K)[:K].cpu().numpy())
+                  if isinstance(consumer, analytics.DegreeCountConsumer) else p.m - p.m0)
+    elif isinstance(consumer, io.EdgeFileWriter):
+        dist.barrier()  # every rank has opened (and rank 0 sized) the file
+        probes = consumer.write_range(p, a, b, device=dev)[1] if b > a else 0
+        dist.barrier()  # the file is complete on return
+        merged = 16 * (p.m - p.m0)
+    else:  # CollectConsumer: the merged array is the whole graph on every rank;
+        # this rank's stats are its own group's share of the plan
+        parts, probes = [], 0
+        for x, y in ((p.m0, a), (a, b), (b, p.m)):
+            if y > x:
+                arr, pr = generate_block(x, y, p, resolution=resolution, device=dev)
+                parts.append(arr)
+                probes += pr if (x, y) == (a, b) else 0
+        merged = np.concatenate(parts) if parts else np.empty((0, 2), dtype=np.uint64)
+    elapsed = time.perf_counter() - t0
+    t = torch.tensor([groups[rank][1] - groups[rank][0], b - a, probes], dtype=torch.int64, device=dev)
+    gathered = [torch.zeros_like(t) for _ in range(ws)]
+    dist.all_gather(gathered, t)
+    per_worker = tuple(WorkerStats(r, int(g[0].item()), int(g[1].item()), int(g[2].item()), elapsed)
+                       for r, g in enumerate(gathered))
     return merged, RunStats(edges_emitted=sum(w.edges for w in per_worker),
                             hash_probes=sum(w.probes for w in per_worker),
                             elapsed=elapsed, per_worker=per_worker)

@@ -59,9 +59,9 @@ class GenParams:
 
     Exactly one of d (uniform out-degree) and degrees must be given; the seed
     graph is a flat array of 2*m0 node IDs, all < n0.  Validation and derived
-    quantities follow the reference.  The B200 path generates uniform-d,
-    flag-free families; the others validate here but are rejected at
-    generation time.
+    quantities follow the reference.  Every family runs on the device:
+    uniform degree and degree sequences (f4), with or without the option
+    flags (f3), CRC or SIMPLE hash, salted or not.
     """
 
     n: int
@@ -179,6 +179,16 @@ class GenParams:
         return self.no_self_loops or self.no_parallel_edges
 
     # -- device plumbing -----------------------------------------------------
+    def _host_params(self):
+        """(parba_params_t, keep-alive) with the seed graph in HOST memory, for
+        the C ABI's host-buffer entry points (uniform degree only)."""
+        seed = np.ascontiguousarray(self.seed_edges, dtype=np.uint64)
+        cp = c_params(self.hash, self.n, self.d, self.n0, self.m0, seed.ctypes.data if seed.size else None)
+        cp.flags = ((_lib.FLAG_NO_SELF_LOOPS if self.no_self_loops else 0)
+                    | (_lib.FLAG_NO_PARALLEL_EDGES if self.no_parallel_edges else 0))
+        cp.max_attempts = self.max_attempts or 0
+        return cp, seed
+
     def _device_params(self, device) -> _lib.CParams:
         """parba_params_t with the seed graph (and a degree sequence's index)
         resident on `device` (cached)."""
@@ -369,22 +379,36 @@ def generate_block_device(lo: int, hi: int, p: GenParams, out=None, probes=None,
 def generate_block(lo: int, hi: int, p: GenParams, resolution: Resolution = "rank",
                    device=None) -> tuple[np.ndarray, int]:
     """Edges lo..hi-1 as a fresh (hi-lo, 2) uint64 host array plus total
-    probes (generator.py:258-325).  The device generates in chunks while the
-    previous chunk streams into pinned host memory."""
+    probes (generator.py:258-325).
+
+    Uniform degree: the C ABI's native host pipeline (``parba_generate_host``):
+    the device generates only the u32 targets (CRC, no flags, n <= 2^32),
+    they cross PCIe at 4 B per edge, and a team of host threads fills the
+    (source, target) rows; other families stream 16-byte rows.  Degree
+    sequences (their index lives on the device): device chunks streamed into
+    pinned host memory while the next chunk is generated."""
     _check_block(lo, hi, p)
     _check_resolution(resolution)
     if lo == hi:
         return np.empty((0, 2), dtype=np.uint64), 0
     torch, dev = _device(device)
     total = hi - lo
-    try:  # pinned: the D2H copies run at full PCIe speed and overlap generation
+    try:  # pinned (torch's caching host allocator: reused, already faulted in)
         out_host = torch.empty(2 * total, dtype=torch.int64, pin_memory=True)
-    except RuntimeError:  # pinning refused (host limits): pageable array, staged copies
+    except RuntimeError:  # pinning refused (host limits): pageable array
         out_host = torch.empty(2 * total, dtype=torch.int64)
+    L = _lib.load()
+    if p.d is not None:
+        import ctypes
+
+        cp, _keep = p._host_params()
+        probes = ctypes.c_uint64(0)
+        idx = dev.index if dev.index is not None else torch.cuda.current_device()
+        _lib.check(L.parba_generate_host(ctypes.byref(cp), lo, hi, out_host.data_ptr(), ctypes.byref(probes), idx))
+        return out_host.numpy().view(np.uint64).reshape(-1, 2), int(probes.value)
     cuts = _cuts(p, lo, hi, min(total, HOST_CHUNK_EDGES))
     spans = list(zip(cuts, cuts[1:]))
     chunk = max(b - a for a, b in spans)
-    L = _lib.load()
     with torch.cuda.device(dev):
         comp = torch.cuda.current_stream(dev)
         copy = torch.cuda.Stream(dev)

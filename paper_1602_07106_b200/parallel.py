@@ -112,60 +112,163 @@ def widen_counts(torch, counts, K: int):
     return counts[:K]
 
 
-def degree_counts_sharded(p, K: int, lo: int, hi: int, device=None):
-    """This rank's shard of [lo, hi) counted on its GPU, summed over ranks.
-
-    Returns (int64 numpy counts[K], total probes, per-rank [(rank, edges, probes)])."""
-    from .generator import _device
-
-    torch, dev = _device(device)
-    rank, ws = world()
-    a, b = shard_range_for(p, lo, hi, rank, ws)
-    counts, probes = count_shard_device(p, K, a, b, device=dev)
-    stats = torch.tensor([b - a, 0], dtype=torch.int64, device=dev)
-    stats[1:2].copy_(probes)
-    if ws > 1:
-        # full histograms travel as 32-bit words (2m < 2^32, so the wrapped
-        # int32 sum has the exact bits): half the bytes of an int64 reduce
-        reduce_counts(counts)
-        gathered = [torch.zeros_like(stats) for _ in range(ws)]
-        import torch.distributed as dist
-
-        dist.all_gather(gathered, stats)
-        per = [(r, int(g[0].item()), int(g[1].item())) for r, g in enumerate(gathered)]
-    else:
-        per = [(0, b - a, int(probes.item()))]
-    c64 = widen_counts(torch, counts, K)
-    out = c64[:K].cpu().numpy() if K else np.zeros(0, dtype=np.int64)
-    return out.astype(np.int64, copy=False), sum(pr for _, _, pr in per), per
+def split_batches(n_batches: int, parts: int) -> list[tuple[int, int]]:
+    """Contiguous groups of batch indices, one per worker / rank:
+    group w = batches [w*B//W, (w+1)*B//W) (empty when W > B).  The
+    reference's workers claim batches from a shared cursor
+    (driver.py:200-207); a contiguous static split keeps every worker's
+    edges one range, so it runs as one fused launch."""
+    return [(n_batches * w // parts, n_batches * (w + 1) // parts) for w in range(parts)]
 
 
-_MULTI_MODES = {"store": _lib.MULTI_STORE, "window": _lib.MULTI_WINDOW, "full": _lib.MULTI_FULL,
-                "discard": _lib.MULTI_DISCARD}
+def group_ranges(p, batches, groups) -> list[tuple[int, int]]:
+    """Edge range [lo, hi) covered by each group of batches (empty: (m0, m0))."""
+    return [(batches[a].lo, batches[b - 1].hi) if b > a else (p.m0, p.m0) for a, b in groups]
+
+
+def worker_devices(workers: int, device=None) -> list[int]:
+    """Device index of each worker: `device` for all of them when given,
+    else the visible devices round-robin from the current one -- the
+    reference's ``workers`` becomes a GPU count."""
+    torch = _lib.torch_cuda()
+    if device is not None:
+        dev = torch.device(device)
+        idx = dev.index if dev.index is not None else torch.cuda.current_device()
+        return [idx] * workers
+    n = torch.cuda.device_count()
+    cur = torch.cuda.current_device()
+    return [(cur + w) % n for w in range(workers)]
+
+
+def _counts_kind(p, K: int) -> str:
+    return "full" if (K == p.n and K > 0 and 2 * p.m < (1 << 32)) else "window"
+
+
+def _run_one_device(p, mode: str, K: int, ranges, dev):
+    """Every range on one device, back to back into one histogram (or one
+    host array for 'store').  Returns (result, per-range probes)."""
+    from .generator import _device, generate_block
+
+    torch, dev = _device(dev)
+    live = [(k, a, b) for k, (a, b) in enumerate(ranges) if b > a]
+    probes = [0] * len(ranges)
+    if mode == "store":
+        parts = []
+        for k, a, b in live:
+            arr, probes[k] = generate_block(a, b, p, device=dev)
+            parts.append(arr)
+        if len(parts) == 1:
+            return parts[0], probes
+        return (np.concatenate(parts) if parts else np.empty((0, 2), dtype=np.uint64)), probes
+    Kc = K if mode != "discard" else 0
+    counts = None
+    prb = torch.zeros(max(len(ranges), 1), dtype=torch.int64, device=dev)
+    for k, a, b in live:
+        counts, _ = count_shard_device(p, Kc, a, b, counts=counts, probes=prb[k:k + 1], device=dev)
+    probes = [int(x) for x in prb.cpu().tolist()][: len(ranges)]
+    if mode == "discard" or Kc == 0:
+        return None, probes
+    if counts is None:
+        return np.zeros(Kc, dtype=np.int64), probes
+    c64 = widen_counts(torch, counts, Kc)
+    return c64[:Kc].cpu().numpy().astype(np.int64, copy=False), probes
+
+
+def run_shards(p, mode: str, K: int, ranges, devices):
+    """Run shard k = edges ranges[k] on device devices[k] (single process).
+
+    mode: 'window' (int64 counts[K]; K == n selects the u32 full-histogram
+    kernels), 'discard', or 'store' ((sum, 2) uint64 rows of the ranges, in
+    order -- the ranges must be contiguous).  Returns (result, per-shard
+    probes).  One distinct device: the device path directly.  Several
+    devices, uniform degree: the C ABI ``parba_multi_run_shards`` (a host
+    thread per device, one NCCL reduce of the histograms).  Several devices
+    with a degree sequence (its index lives on each device): a host thread per
+    device, histograms summed on the host."""
+    import ctypes
+
+    if len(ranges) != len(devices):
+        raise ParameterError("one device per shard")
+    udev = list(dict.fromkeys(devices))
+    if len(udev) == 1:
+        return _run_one_device(p, mode, K, ranges, udev[0])
+    if p.d is not None:
+        cp, _keep = p._host_params()
+        kind = {"store": _lib.MULTI_STORE, "discard": _lib.MULTI_DISCARD}.get(mode)
+        if kind is None:
+            kind = _lib.MULTI_FULL if _counts_kind(p, K) == "full" else _lib.MULTI_WINDOW
+        lo_all = min(a for a, _ in ranges)
+        hi_all = max(b for _, b in ranges)
+        if kind == _lib.MULTI_STORE:
+            out = np.empty((p.m - p.m0, 2), dtype=np.uint64)  # the C ABI writes edge i at row i - m0
+        elif kind in (_lib.MULTI_WINDOW, _lib.MULTI_FULL):
+            out = np.zeros(max(K, 1), dtype=np.int64)
+        else:
+            out = None
+        devs = np.ascontiguousarray(devices, dtype=np.int32)
+        los = np.ascontiguousarray([a for a, _ in ranges], dtype=np.uint64)
+        his = np.ascontiguousarray([b for _, b in ranges], dtype=np.uint64)
+        prs = np.zeros(len(ranges), dtype=np.uint64)
+        secs = ctypes.c_double(0.0)
+        L = _lib.load()
+        _lib.check(L.parba_multi_run_shards(ctypes.byref(cp), len(ranges), devs.ctypes.data, los.ctypes.data,
+                                            his.ctypes.data, kind, K if kind == _lib.MULTI_WINDOW else 0,
+                                            out.ctypes.data if out is not None else None, prs.ctypes.data,
+                                            ctypes.byref(secs)))
+        if kind == _lib.MULTI_STORE:
+            out = out[lo_all - p.m0: hi_all - p.m0]
+        elif out is not None:
+            out = out[:K]
+        return out, [int(x) for x in prs]
+    # degree sequence on several devices: a host thread per device, each
+    # running its shards one by one (results kept per shard)
+    import threading
+
+    per: dict = {}
+    errors: list = []
+
+    def work(dv):
+        try:
+            for k, x in enumerate(devices):
+                if x == dv:
+                    res, pr = _run_one_device(p, mode, K, [ranges[k]], dv)
+                    per[k] = (res, pr[0])
+        except BaseException as e:  # re-raised below
+            errors.append(e)
+
+    ths = [threading.Thread(target=work, args=(dv,)) for dv in udev]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    if errors:
+        raise errors[0]
+    probes = [per[k][1] for k in range(len(ranges))]
+    if mode == "store":
+        return np.concatenate([per[k][0] for k in range(len(ranges))]), probes
+    if mode == "discard" or K == 0:
+        return None, probes
+    return sum(per[k][0] for k in range(len(ranges))), probes
 
 
 def multi_run(p, devices, mode: str = "window", K: int | None = None):
-    """Whole graph [m0, m) on several GPUs from ONE process (C ABI
-    ``parba_multi_run``: a host thread per device, counts summed on
-    devices[0] over peer copies).  Returns (result, probes, device_seconds):
+    """Whole graph [m0, m) on several GPUs from ONE process through the C ABI
+    ``parba_multi_run`` (equal contiguous shards, a host thread per distinct
+    device, one NCCL reduce).  Returns (result, probes, device_seconds):
     result = (m - m0, 2) uint64 edges ('store'), int64 counts[K] ('window'),
     int64 counts[n] ('full') or None ('discard').  Uniform degree only."""
     import ctypes
 
-    from .hashing import c_params
-
-    if mode not in _MULTI_MODES:
+    modes = {"store": _lib.MULTI_STORE, "window": _lib.MULTI_WINDOW, "full": _lib.MULTI_FULL,
+             "discard": _lib.MULTI_DISCARD}
+    if mode not in modes:
         raise ParameterError(f"unknown mode {mode!r}")
     if p.d is None:
         raise ParameterError("multi_run takes uniform-degree families (degree sequences: one process per GPU)")
     devs = np.ascontiguousarray(np.asarray(list(devices), dtype=np.int32))
     if devs.size < 1:
         raise ParameterError("need at least one device")
-    seed = np.ascontiguousarray(p.seed_edges, dtype=np.uint64)
-    cp = c_params(p.hash, p.n, p.d, p.n0, p.m0, seed.ctypes.data if seed.size else None)
-    cp.flags = ((_lib.FLAG_NO_SELF_LOOPS if p.no_self_loops else 0)
-                | (_lib.FLAG_NO_PARALLEL_EDGES if p.no_parallel_edges else 0))
-    cp.max_attempts = p.max_attempts or 0
+    cp, _keep = p._host_params()
     if mode == "window":
         K = p.n if K is None else K
         out = np.zeros(max(K, 1), dtype=np.int64)
@@ -180,7 +283,7 @@ def multi_run(p, devices, mode: str = "window", K: int | None = None):
     probes = ctypes.c_uint64(0)
     secs = ctypes.c_double(0.0)
     L = _lib.load()
-    _lib.check(L.parba_multi_run(ctypes.byref(cp), int(devs.size), devs.ctypes.data, _MULTI_MODES[mode], K,
+    _lib.check(L.parba_multi_run(ctypes.byref(cp), int(devs.size), devs.ctypes.data, modes[mode], K,
                                  out.ctypes.data if out is not None else None, ctypes.byref(probes),
                                  ctypes.byref(secs)))
     if mode in ("window", "full"):

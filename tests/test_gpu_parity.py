@@ -64,8 +64,10 @@ def test_hash_frozen_values_and_edges():
 
 
 def test_hash_dense_small_r_vs_oracle():
-    # every r in [1, 70000) -- covers the exact slow path (r < 2^13) and the
-    # fp64-reciprocal fast path on both sides of the switch
+    # every r in [1, 70000) through hash_many (the generic hash kernel:
+    # byte-table CRC + mod_int).  The tile kernels' FP64 remainders (mod_fp31,
+    # mod_fp, the per-tile reciprocal series) are pinned directly in
+    # tests/test_gpu_remainder.py.
     rs = np.arange(1, 70000, dtype=np.uint64)
     for cfg in (pb.HashConfig(), pb.HashConfig(seed0=7, seed1=9, attempt_salt=11)):
         p = O.OParams(n=1, d=1, seed0=cfg.seed0, seed1=cfg.seed1, salt=cfg.attempt_salt)
