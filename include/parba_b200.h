@@ -221,6 +221,18 @@ int parba_multi_run_shards(const parba_params_t *p_host_seed, int nshards, const
                            const uint64_t *los, const uint64_t *his, int mode, uint64_t K, void *out_host,
                            uint64_t *probes_per_shard, double *device_seconds);
 
+/* ---- Sequential-oracle counterpart (bb_generate, oracle.py:45-107) ------
+ * The whole edge array E[0 .. 2m) (device, u64) built as an array: seed
+ * cells, E[2i] = source(i), E[2i+1] = E[h(2i+1)] -- one hash per edge and
+ * pointer jumping over the links, no hash chains (an independent check of
+ * the tile kernels, as the reference's verify compares its parallel path
+ * with the sequential fill, cli.py:332-351).  link: m - m0 u64 scratch;
+ * flag: one device u32; *passes (optional) = pointer-jumping passes.
+ * Plain mode (no option flags), uniform degree or degree sequence.
+ * Synchronises `stream`. */
+int parba_bb_fill(const parba_params_t *p, uint64_t *E, uint64_t *link, unsigned int *flag, int *passes,
+                  void *stream);
+
 /* ---- Remainder self-test (h % r, _kernels.py:32-42) --------------------
  * The exact-remainder routines of the tile kernels, callable on arbitrary
  * inputs so tests can pin them against integer division.  Methods: */

@@ -10,19 +10,13 @@ fallback: without the library or a CUDA device every compute call raises
 """
 
 from .analytics import (
-    BinRatio,
     DegreeCounter,
     DegreeCountConsumer,
-    Histogram,
     count_block,
     count_edge,
     count_seed_edges,
     degree_counts,
-    expected_degree_check,
-    fit_exponent,
     merge,
-    write_degree_csv,
-    write_histogram_csv,
 )
 from .driver import (
     DEFAULT_BATCH_SIZE,
@@ -85,15 +79,15 @@ __version__ = "0.1.0"
 
 __all__ = [
     "CRC32C_TABLE", "crc32c_u64", "crc32c_u64_many", "h_crc_many", "h_simple_many", "mulhi_u64",
-    "Batch", "BinRatio", "ChainResult", "CollectConsumer", "Consumer", "DEFAULT_BATCH_SIZE",
+    "Batch", "ChainResult", "CollectConsumer", "Consumer", "DEFAULT_BATCH_SIZE",
     "DEFAULT_MULTIPLIER", "DegreeCountConsumer", "EdgeFileWriter", "write_edges_binary", "DegreeCounter", "DiscardConsumer", "Edge",
-    "GenParams", "GenerationError", "Granularity", "HashConfig", "HashKind", "Histogram",
+    "GenParams", "GenerationError", "Granularity", "HashConfig", "HashKind",
     "InfeasibleTargetsError", "MAX_EDGES", "ParameterError", "PrefixIndex", "RankBits", "RunStats",
     "SeedGraphFormatError", "build_prefix", "build_rank_bits", "first_half_pos", "node_of_edge",
     "node_of_edge_bisect", "read_degree_file", "resolve_targets_deferred",
     "WorkerStats", "bb_generate", "count_block", "count_edge", "count_seed_edges", "degree_counts",
-    "edge_count", "edge_list", "edges_at", "expected_degree_check", "fit_exponent",
+    "edge_count", "edge_list", "edges_at",
     "generate_block", "generate_block_device", "generate_edge", "generate_node_edges", "h_crc",
     "h_simple", "hash_many", "hash_value", "merge", "plan_batches", "resolve_chain",
-    "resolve_chain_block", "run", "write_degree_csv", "write_histogram_csv",
+    "resolve_chain_block", "run",
 ]

@@ -33,6 +33,7 @@ EXPORTS = (
     "parba_degseq_prefix", "parba_degseq_rank", "parba_rank1", "parba_node_of_edges", "parba_count_pairs",
     "parba_multi_run", "parba_multi_run_shards", "parba_crc32c", "parba_mulhi_u64", "parba_degseq_dense",
     "parba_peak_int32", "parba_peak_write", "parba_debug_mod", "parba_debug_mod_check",
+    "parba_bb_fill",
 )
 MOD_FP31, MOD_FP_NARROW, MOD_FP_WIDE, MOD_INT, MOD_FP31_SERIES, MOD_FP_NARROW_SERIES, MOD_FP_WIDE_SERIES = range(7)
 MULTI_STORE, MULTI_WINDOW, MULTI_FULL, MULTI_DISCARD = 0, 1, 2, 3
@@ -108,6 +109,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
             "parba_degseq_dense": ([vp, u64, u64, u64, vp, vp], i32),
             "parba_multi_run": ([P, i32, vp, i32, u64, vp, ctypes.POINTER(u64), ctypes.POINTER(ctypes.c_double)],
                                 i32),
+            "parba_bb_fill": ([P, vp, vp, vp, ctypes.POINTER(i32), vp], i32),
             "parba_debug_mod": ([i32, vp, vp, vp, u64, vp, vp], i32),
             "parba_debug_mod_check": ([i32, u64, u64, u64, u64, vp, vp, vp], i32),
             "parba_peak_int32": ([vp, ctypes.POINTER(ctypes.c_double), vp], i32),

@@ -17,7 +17,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libparba_b200.so")
 ROOT = os.path.dirname(HERE)
 
-SOURCES = ["parba_api.cu", "parba_nodes_api.cu", "parba_host.cu", "parba_debug.cu"]
+SOURCES = ["parba_api.cu", "parba_nodes_api.cu", "parba_host.cu", "parba_debug.cu", "parba_bb.cu"]
 DEPS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cu", ".cuh", ".h")))
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -47,7 +47,8 @@ int validate(const parba_params_t *p) {
                                   "with an empty seed the first edge is the forced self-loop (0, 0)");
     if (is_deg(p)) {
         if (p->d != 0) return fail(PARBA_EINVAL, "exactly one of d and degrees must be given");
-        if (!p->rank) return fail(PARBA_EINVAL, "degree sequence without its rank directory");
+        // (a sequence of zero degrees generates nothing and has no directory)
+        if (!p->rank && p->m > p->m0) return fail(PARBA_EINVAL, "degree sequence without its rank directory");
         if (p->n < p->n0) return fail(PARBA_EINVAL, "need 0 <= n0 <= n, got n0=%llu, n=%llu",
                                       (unsigned long long)p->n0, (unsigned long long)p->n);
         if (p->hash_kind > PARBA_HASH_SIMPLE) return fail(PARBA_EINVAL, "unknown hash kind %u", p->hash_kind);

@@ -270,8 +270,12 @@ def _run_fused_ranks(p: GenParams, consumer, batches, rank: int, ws: int, resolu
             # int32 sum has the exact bits): half the bytes of an int64 reduce
             parallel.reduce_counts(counts)
         probes = int(prb.item())
-        merged = (analytics.DegreeCounter(K=K, counts=parallel.widen_counts(torch, counts, K)[:K].cpu().numpy())
-                  if isinstance(consumer, analytics.DegreeCountConsumer) else p.m - p.m0)
+        if isinstance(consumer, analytics.DegreeCountConsumer):
+            c = (parallel.widen_counts(torch, counts, K)[:K].cpu().numpy() if K
+                 else np.zeros(0, dtype=np.int64))
+            merged = analytics.DegreeCounter(K=K, counts=c)
+        else:
+            merged = p.m - p.m0
     elif isinstance(consumer, io.EdgeFileWriter):
         dist.barrier()  # every rank has opened (and rank 0 sized) the file
         probes = consumer.write_range(p, a, b, device=dev)[1] if b > a else 0

@@ -166,9 +166,9 @@ def _run_one_device(p, mode: str, K: int, ranges, dev):
     for k, a, b in live:
         counts, _ = count_shard_device(p, Kc, a, b, counts=counts, probes=prb[k:k + 1], device=dev)
     probes = [int(x) for x in prb.cpu().tolist()][: len(ranges)]
-    if mode == "discard" or Kc == 0:
+    if mode == "discard":
         return None, probes
-    if counts is None:
+    if counts is None or Kc == 0:
         return np.zeros(Kc, dtype=np.int64), probes
     c64 = widen_counts(torch, counts, Kc)
     return c64[:Kc].cpu().numpy().astype(np.int64, copy=False), probes
@@ -246,7 +246,7 @@ def run_shards(p, mode: str, K: int, ranges, devices):
     probes = [per[k][1] for k in range(len(ranges))]
     if mode == "store":
         return np.concatenate([per[k][0] for k in range(len(ranges))]), probes
-    if mode == "discard" or K == 0:
+    if mode == "discard":
         return None, probes
     return sum(per[k][0] for k in range(len(ranges))), probes
 

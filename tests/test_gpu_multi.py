@@ -100,6 +100,20 @@ def test_degree_counts_workers_flags_and_degree_sequences():
         assert sum(w.batches for w in sb.per_worker) == len(pb.plan_batches(p, 3000))
 
 
+def test_empty_degree_sequence():
+    """A degree sequence of zeros generates no edges (m == m0): zero counts,
+    no batches, like the reference -- no rank directory needed."""
+    p = pb.GenParams(n=8, degrees=np.zeros(8, dtype=np.uint64))
+    assert p.m == 0
+    counter, st = pb.degree_counts(p)
+    assert counter.counts.tolist() == [0] * 8 and st.edges_emitted == 0
+    res, st = pb.run(p, pb.DiscardConsumer(), workers=2)
+    assert res == 0 and len(st.per_worker) == 2 and sum(w.batches for w in st.per_worker) == 0
+    q = pb.GenParams(n=13, n0=10, seed_edges=ring_edges(10), degrees=np.zeros(3, dtype=np.uint64))
+    c, _ = pb.degree_counts(q)
+    assert c.counts.tolist() == [2] * 10 + [0] * 3
+
+
 def test_file_writer_workers(tmp_path):
     p = pb.GenParams(n=50000, d=4, n0=3, seed_edges=TRIANGLE)
     want, _ = O.generate_block(_op(p), p.m0, p.m)

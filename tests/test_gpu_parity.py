@@ -15,6 +15,7 @@ import pytest
 import oracle as O
 from paper_1602_07106_b200.hashing import HashConfig, HashKind
 from conftest import GOLDEN_CRC_N10_D2, GOLDEN_SIMPLE_N10_D2, RING10, TRIANGLE
+from powerlaw import attachment_ratios, mle_exponent
 
 pytestmark = pytest.mark.gpu
 
@@ -132,6 +133,38 @@ def test_golden_n10_d2():
         assert [tuple(pb.generate_edge(i, p)) for i in range(20)] == want
         assert [tuple(map(int, r)) for r in pb.edge_list(pb.bb_generate(p))] == want
     assert pb.generate_edge(7, pb.GenParams(n=10, d=2, hash=pb.HashConfig(kind=pb.HashKind.SIMPLE))) == (3, 2)
+
+
+def test_bb_generate_array_fill(golden):
+    """bb_generate: the edge array built by one hash per edge + pointer
+    jumping (no chains) equals the chain recomputation of generate_block, the
+    oracle's sequential fill and the reference's config-1 sha256, for
+    every hash family / seed graph / degree sequence tried."""
+    _, meta = golden
+    rng = np.random.default_rng(5)
+    deg = rng.integers(0, 7, size=50_000).astype(np.uint64)
+    fams = [pb.GenParams(n=300_000, d=5), pb.GenParams(n=200_000, d=3, n0=3, seed_edges=TRIANGLE),
+            pb.GenParams(n=100_000, d=7, n0=10, seed_edges=RING10,
+                         hash=pb.HashConfig(kind=pb.HashKind.SIMPLE)),
+            pb.GenParams(n=100_000, d=4, hash=pb.HashConfig(seed0=77, seed1=(1 << 40) + 5, attempt_salt=3)),
+            pb.GenParams(n=50_010, n0=10, seed_edges=RING10, degrees=deg)]
+    for p in fams:
+        e = pb.bb_generate(p)
+        assert e.dtype == np.uint64 and e.size == 2 * p.m
+        assert np.array_equal(e[: 2 * p.m0], p.seed_edges)
+        blk, _ = pb.generate_block(p.m0, p.m, p)
+        assert np.array_equal(pb.edge_list(e, p.m0), blk)
+        if p.d is not None:
+            assert np.array_equal(e, O.bb_generate(_op(p)))
+    g = meta["config1"]
+    e = pb.bb_generate(pb.GenParams(n=g["n"], d=g["d"]), engine="python")
+    assert _sha(e.reshape(-1, 2)) == g["sha256"]
+    with pytest.raises(pb.ParameterError, match="uniform degrees only"):
+        pb.bb_generate(fams[-1], engine="compiled")
+    with pytest.raises(pb.ParameterError, match="rng"):
+        pb.bb_generate(fams[0], mode="rng")
+    with pytest.raises(pb.ParameterError, match="cap"):
+        pb.bb_generate(fams[0], cap=1000)
 
 
 def test_72_combos_byte_identical(golden):
@@ -303,8 +336,7 @@ def test_full_histogram_n1e6_d16_vs_oracle():
     blk, wp = O.run_threaded(_op(p), 0, p.m, O.MODE_STORE, threads=os.cpu_count() or 1, batch=1 << 18)
     want = np.bincount(blk.astype(np.int64).ravel(), minlength=p.n)
     assert np.array_equal(counter.counts, want) and stats.hash_probes == wp
-    h = pb.Histogram.from_degree_counts(counter)
-    assert 2.6 <= pb.fit_exponent(h, xmin=16) <= 3.4
+    assert 2.6 <= mle_exponent(counter.counts, kmin=16) <= 3.4
 
 
 def _full_counts(p, lo, hi, mode, monkeypatch):
@@ -504,8 +536,8 @@ def test_expected_degree_law_billion_edges():
     n, d, K = 10**7, 100, 10**4
     p = pb.GenParams(n=n, d=d, hash=pb.HashConfig(kind=pb.HashKind.SIMPLE))
     counter, stats = pb.degree_counts(p, K=K)
-    ratios = pb.expected_degree_check(counter, n=n, d=d, bins=12, lo=10, hi=K)
-    assert len(ratios) >= 10 and all(0.8 <= r.ratio <= 1.2 for r in ratios)
+    ratios = attachment_ratios(counter.counts, n=n, d=d, bins=12, lo=10, hi=K)
+    assert len(ratios) >= 10 and all(0.8 <= r <= 1.2 for r in ratios)
     assert stats.edges_emitted == 10**9
 
 
@@ -587,9 +619,7 @@ def test_config4_full_histogram_properties():
     win, _ = pb.parallel.count_shard_device(p, 100_000, 0, p.m)
     torch.cuda.synchronize()
     assert torch.equal(win[:100_000], c64[:100_000])
-    vals, cnt = torch.unique(c64, return_counts=True)
-    h = pb.Histogram(degrees=vals.cpu().numpy(), counts=cnt.cpu().numpy())
-    assert 2.6 <= pb.fit_exponent(h, xmin=32) <= 3.4
+    assert 2.6 <= mle_exponent(c64.cpu().numpy(), kmin=32) <= 3.4
 
 
 # --------------------------------------------------------------------------- binary file writer (f2)
