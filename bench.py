@@ -343,7 +343,8 @@ def main() -> None:
         raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}")
     # host threads of the e2e pipeline: this rank's share of the host cores
     lws = int(os.environ.get("LOCAL_WORLD_SIZE", str(ws)))
-    os.environ.setdefault("PARBA_HOST_THREADS", str(max(1, len(os.sched_getaffinity(0)) // lws)))
+    ncpu = len(os.sched_getaffinity(0))
+    os.environ.setdefault("PARBA_HOST_THREADS", str(max(1, ncpu // lws - 1 if ncpu // lws > 2 else 1)))
     # CPU baselines first (N=1, rank 0), before any CUDA work
     cpu = None
     if rank == 0 and ws == 1 and not (args.no_cpu_baseline or args.profile or args.only):
@@ -411,13 +412,13 @@ def main() -> None:
     p = pb.GenParams(**C2)
     lo, hi = pb.parallel.shard_range(0, p.m, rank, ws)
     shard = hi - lo
-    out = torch.empty((shard, 2), dtype=torch.int64, device=dev)
+    out = torch.empty((shard if not args.only else 1, 2), dtype=torch.int64, device=dev)
     probes = torch.zeros(1, dtype=torch.int64, device=dev)
     cp = p._device_params(dev)
 
     # roofline denominators measured here, on this GPU, before the kernels
     peaks = {}
-    if not args.profile:
+    if not (args.profile or args.only):
         wsec = timed(lambda: pb._lib.check(L.parba_peak_write(out.data_ptr(), shard * 16, stream.cuda_stream)))
         scratch = torch.zeros(1, dtype=torch.int32, device=dev)
         ops = ctypes.c_double(0.0)

@@ -141,19 +141,50 @@ int generate_host_pairs(const parba_params_t *ph, uint64_t lo, uint64_t hi, uint
 // of the caller's array -- the source is the closed form (i - m0) / d + n0
 // (generator.py:163-169), counted up edge by edge, and the rows are written
 // with 16-byte streaming stores.  GPU, PCIe and host memory overlap over a
-// ring of kSlots staging buffers; the host write (16 B per edge + 4 B read)
-// is the bound (tools/host_probe.cu).
+// ring of staging slots.  Host memory traffic is the bound (per edge: 16 B of
+// rows written + the 4 B target written by the DMA and read back,
+// tools/host_probe.cu), so small chunks help: a staged chunk that the CPU
+// reads while it is still in the last-level cache costs no DRAM traffic.
+// Optionally (PARBA_E2E_ROWS_FRAC, pinned output only) the first part of the
+// range goes over PCIe as finished 16-byte rows concurrently with the CPU's
+// part; measured slower on this pool's hosts, so off by default.
 
-constexpr int kSlots = 3;
-constexpr uint64_t kTgtChunk = 1ull << 24;  // edges per chunk (64 MiB of targets)
+struct PipeCfg {
+    uint64_t chunk = 1ull << 21;  // edges per staged chunk (8 MiB of targets: stays in the LLC)
+    int slots = 8;                // staging slots in flight
+    double rows_frac = 0.0;       // share of the range sent as 16-byte rows (pinned output only)
+};
+
+PipeCfg pipe_cfg() {
+    PipeCfg c;
+    if (const char *e = getenv("PARBA_E2E_CHUNK_LOG2")) {
+        const int b = atoi(e);
+        if (b >= 16 && b <= 26) c.chunk = 1ull << b;
+    }
+    if (const char *e = getenv("PARBA_E2E_SLOTS")) {
+        const int k = atoi(e);
+        if (k >= 2 && k <= 64) c.slots = k;
+    }
+    // measured on the B200 hosts (tools/e2e_perf.py, profiles/r02_e2e_sweep.jsonl):
+    // the rows split only adds PCIe + DMA traffic to the bound host memory
+    c.rows_frac = 0.0;
+    if (const char *e = getenv("PARBA_E2E_ROWS_FRAC")) c.rows_frac = atof(e);
+    if (c.rows_frac < 0.0) c.rows_frac = 0.0;
+    if (c.rows_frac > 1.0) c.rows_frac = 1.0;
+    return c;
+}
 
 // Staging per device, kept for the life of the process (pinned allocation
 // costs more than a chunk's work); one host-array call per device at a time.
 struct Staging {
     std::mutex use;
-    uint32_t *host = nullptr;  // kSlots * kTgtChunk, pinned
-    uint32_t *dev = nullptr;   // 2 * kTgtChunk on the device
+    uint32_t *host = nullptr;  // slots * chunk u32, pinned
+    size_t host_words = 0;
+    uint32_t *dev = nullptr;   // 2 * chunk u32 on the device
+    size_t dev_words = 0;
+    uint64_t *rows = nullptr;  // 2 * kRowChunk 16-byte rows on the device (rows split)
 };
+constexpr uint64_t kRowChunk = 1ull << 24;
 
 Staging &staging_for(int device) {
     static std::mutex mu;
@@ -174,10 +205,10 @@ int host_threads() {
     int n = 0;
     if (sched_getaffinity(0, sizeof(cs), &cs) == 0) n = CPU_COUNT(&cs);
     if (n <= 0) n = (int)std::thread::hardware_concurrency();
-    return n > 0 ? n : 1;
+    return n > 2 ? n - 1 : 1;  // one core for the thread driving the GPU
 }
 
-// rows[k] = ((lo0 + k - m0) / d + n0, tgt[k]) for k in [a, b)
+// rows[k] = ((i0 + k - m0) / d + n0, tgt[k]) for k in [a, b)
 void expand_rows(uint64_t *rows, const uint32_t *tgt, uint64_t i0, uint64_t a, uint64_t b, const parba_params_t *p,
                  bool nt) {
     if (b <= a) return;
@@ -206,103 +237,169 @@ void expand_rows(uint64_t *rows, const uint32_t *tgt, uint64_t i0, uint64_t a, u
     }
 }
 
+bool is_pinned(const void *p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+
 int generate_host_targets(const parba_params_t *ph, uint64_t lo, uint64_t hi, uint64_t *out_host,
                           uint64_t *probes_host, int device, float *ms) {
     const auto w0 = std::chrono::steady_clock::now();
     CUDA_TRY(cudaSetDevice(device));
+    const PipeCfg cfg = pipe_cfg();
+    const uint64_t C = cfg.chunk;
+    const int S = cfg.slots;
     Staging &sg = staging_for(device);
     std::lock_guard<std::mutex> use(sg.use);
-    if (!sg.host) CUDA_TRY(cudaHostAlloc((void **)&sg.host, kSlots * kTgtChunk * 4, cudaHostAllocPortable));
-    if (!sg.dev) CUDA_TRY(cudaMalloc((void **)&sg.dev, 2 * kTgtChunk * 4));
+    if (sg.host_words < (size_t)S * C) {
+        if (sg.host) cudaFreeHost(sg.host);
+        sg.host = nullptr;
+        sg.host_words = 0;
+        CUDA_TRY(cudaHostAlloc((void **)&sg.host, (size_t)S * C * 4, cudaHostAllocPortable));
+        sg.host_words = (size_t)S * C;
+    }
+    if (sg.dev_words < 2 * C) {
+        if (sg.dev) cudaFree(sg.dev);
+        sg.dev = nullptr;
+        sg.dev_words = 0;
+        CUDA_TRY(cudaMalloc((void **)&sg.dev, 2 * C * 4));
+        sg.dev_words = 2 * C;
+    }
     parba_params_t pd;
     DevBuf seed, prb;
     int rc = upload_seed(ph, &pd, seed);
     if (rc) return rc;
     const DevParams dp = make_dev(&pd);
-    CUDA_TRY(cudaMalloc(&prb.p, sizeof(unsigned long long)));
-    StreamGuard sc, sx;
+    CUDA_TRY(cudaMalloc(&prb.p, 2 * sizeof(unsigned long long)));
+    unsigned long long *prb_t = (unsigned long long *)prb.p, *prb_r = prb_t + 1;
+    StreamGuard sc, sx, sc2, sx2;
     CUDA_TRY(cudaStreamCreateWithFlags(&sc.s, cudaStreamNonBlocking));
     CUDA_TRY(cudaStreamCreateWithFlags(&sx.s, cudaStreamNonBlocking));
-    CUDA_TRY(cudaMemsetAsync(prb.p, 0, sizeof(unsigned long long), sc.s));
-    EventGuard made[2], copied[kSlots];
-    for (auto &e : made) CUDA_TRY(cudaEventCreateWithFlags(&e.e, cudaEventDisableTiming));
-    for (auto &e : copied) CUDA_TRY(cudaEventCreateWithFlags(&e.e, cudaEventDisableTiming | cudaEventBlockingSync));
-    const uint64_t total = hi - lo;
-    const int64_t nchunks = (int64_t)((total + kTgtChunk - 1) / kTgtChunk);
-    const bool nt = (((uintptr_t)out_host) & 15) == 0;
-    auto chunk_lo = [&](int64_t k) { return lo + (uint64_t)k * kTgtChunk; };
-    auto chunk_n = [&](int64_t k) { return std::min(kTgtChunk, hi - chunk_lo(k)); };
+    CUDA_TRY(cudaMemsetAsync(prb.p, 0, 2 * sizeof(unsigned long long), sc.s));
+    CUDA_TRY(cudaStreamSynchronize(sc.s));
 
-    // GPU side of chunk k: targets into device buffer k % 2, then into slot k % kSlots
+    // the rows part [lo, mid): generated as 16-byte rows, DMA'd straight into
+    // the (pinned) caller's array on its own streams, no host work
+    uint64_t mid = lo;
+    if (cfg.rows_frac > 0.0 && hi - lo >= 4 * C && is_pinned(out_host))
+        mid = lo + (uint64_t)((double)(hi - lo) * cfg.rows_frac);
+    if (mid > lo) {
+        if (!sg.rows) CUDA_TRY(cudaMalloc((void **)&sg.rows, 2 * kRowChunk * 16));
+        CUDA_TRY(cudaStreamCreateWithFlags(&sc2.s, cudaStreamNonBlocking));
+        CUDA_TRY(cudaStreamCreateWithFlags(&sx2.s, cudaStreamNonBlocking));
+    }
+    std::vector<EventGuard> rmade(2), rcopied(2);
+    for (int b = 0; b < 2 && mid > lo; ++b) {
+        CUDA_TRY(cudaEventCreateWithFlags(&rmade[b].e, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&rcopied[b].e, cudaEventDisableTiming));
+    }
+    {
+        uint64_t k = 0;
+        for (uint64_t a = lo; a < mid; a += kRowChunk, ++k) {
+            const uint64_t b = std::min(a + kRowChunk, mid);
+            const int j = (int)(k & 1);
+            uint64_t *dbuf = sg.rows + (uint64_t)j * 2 * kRowChunk;
+            if (k >= 2) CUDA_TRY(cudaStreamWaitEvent(sc2.s, rcopied[j].e, 0));
+            if ((rc = launch_store(&pd, dp, a, b, dbuf, prb_r, sc2.s))) return rc;
+            CUDA_TRY(cudaEventRecord(rmade[j].e, sc2.s));
+            CUDA_TRY(cudaStreamWaitEvent(sx2.s, rmade[j].e, 0));
+            CUDA_TRY(cudaMemcpyAsync(out_host + 2 * (a - lo), dbuf, (b - a) * 16, cudaMemcpyDeviceToHost, sx2.s));
+            CUDA_TRY(cudaEventRecord(rcopied[j].e, sx2.s));
+        }
+    }
+
+    // the targets part [mid, hi)
+    std::vector<EventGuard> made(2), copied(S);
+    for (auto &e : made) CUDA_TRY(cudaEventCreateWithFlags(&e.e, cudaEventDisableTiming));
+    for (auto &e : copied) CUDA_TRY(cudaEventCreateWithFlags(&e.e, cudaEventDisableTiming));
+    const int64_t nchunks = (int64_t)((hi - mid + C - 1) / C);
+    const bool nt = (((uintptr_t)out_host) & 15) == 0;
+    auto chunk_lo = [&](int64_t k) { return mid + (uint64_t)k * C; };
+    auto chunk_n = [&](int64_t k) { return std::min(C, hi - chunk_lo(k)); };
+
+    // GPU side of chunk k: targets into device buffer k % 2, then into slot k % S
     auto enqueue = [&](int64_t k) -> int {
-        const int d = (int)(k & 1), s = (int)(k % kSlots);
-        uint32_t *dbuf = sg.dev + (uint64_t)d * kTgtChunk;
-        if (k >= 2) CUDA_TRY(cudaStreamWaitEvent(sc.s, copied[(k - 2) % kSlots].e, 0));  // device buffer free
-        int r = launch_store_t32(&pd, dp, chunk_lo(k), chunk_lo(k) + chunk_n(k), dbuf,
-                                 (unsigned long long *)prb.p, sc.s);
+        const int d = (int)(k & 1), s = (int)(k % S);
+        uint32_t *dbuf = sg.dev + (uint64_t)d * C;
+        if (k >= 2) CUDA_TRY(cudaStreamWaitEvent(sc.s, copied[(k - 2) % S].e, 0));  // device buffer free
+        int r = launch_store_t32(&pd, dp, chunk_lo(k), chunk_lo(k) + chunk_n(k), dbuf, prb_t, sc.s);
         if (r) return r;
         CUDA_TRY(cudaEventRecord(made[d].e, sc.s));
         CUDA_TRY(cudaStreamWaitEvent(sx.s, made[d].e, 0));
-        CUDA_TRY(cudaMemcpyAsync(sg.host + (uint64_t)s * kTgtChunk, dbuf, chunk_n(k) * 4, cudaMemcpyDeviceToHost,
-                                 sx.s));
+        CUDA_TRY(cudaMemcpyAsync(sg.host + (uint64_t)s * C, dbuf, chunk_n(k) * 4, cudaMemcpyDeviceToHost, sx.s));
         CUDA_TRY(cudaEventRecord(copied[s].e, sx.s));
         return PARBA_OK;
     };
 
-    // host team: worker w expands slice w of every chunk, in chunk order
+    // host team: worker w expands slice w of every chunk, in chunk order.  The
+    // main thread alone waits on the copy engine (one event wait per chunk)
+    // and publishes staged chunks; it recycles a slot once every worker is
+    // done with it.
     const int T = host_threads();
     std::mutex mu;
     std::condition_variable cv_work, cv_main;
-    int64_t enq = 0;                  // chunks enqueued (guarded by mu)
-    int finished[kSlots] = {};        // workers done with the slot's current chunk (mu)
-    bool abort = false;               // (mu)
-    std::atomic<int> werr{0};
+    int64_t ready = 0;                 // chunks staged in host memory (guarded by mu)
+    std::vector<int> finished(S, 0);   // workers done with the slot's current chunk (mu)
+    bool abort = false;                // (mu)
     auto worker = [&](int w) {
         for (int64_t k = 0; k < nchunks; ++k) {
             {
                 std::unique_lock<std::mutex> lk(mu);
-                cv_work.wait(lk, [&] { return enq > k || abort; });
+                cv_work.wait(lk, [&] { return ready > k || abort; });
                 if (abort) return;
             }
-            const int s = (int)(k % kSlots);
-            if (cudaEventSynchronize(copied[s].e) != cudaSuccess) werr = 1;
+            const int s = (int)(k % S);
             const uint64_t n = chunk_n(k);
-            uint64_t a = n * (uint64_t)w / T, b = n * (uint64_t)(w + 1) / T;
-            if (!werr) expand_rows(out_host + 2 * (chunk_lo(k) - lo), sg.host + (uint64_t)s * kTgtChunk, chunk_lo(k),
-                                   a, b, ph, nt);
+            // 8-edge-aligned slices (whole 128-byte lines of rows per thread)
+            const uint64_t a = (n * (uint64_t)w / T) & ~7ull;
+            const uint64_t b = w == T - 1 ? n : (n * (uint64_t)(w + 1) / T) & ~7ull;
+            expand_rows(out_host + 2 * (chunk_lo(k) - lo), sg.host + (uint64_t)s * C, chunk_lo(k), a, b, ph, nt);
             std::lock_guard<std::mutex> lk(mu);
             if (++finished[s] == T) cv_main.notify_one();
         }
     };
-    for (int64_t k = 0; k < std::min<int64_t>(kSlots, nchunks); ++k) {
+    for (int64_t k = 0; k < std::min<int64_t>(S, nchunks); ++k)
         if ((rc = enqueue(k))) return rc;
-        enq = k + 1;  // no worker runs yet
-    }
     std::vector<std::thread> team;
-    for (int w = 0; w < T; ++w) team.emplace_back(worker, w);
+    for (int w = 0; w < T && nchunks > 0; ++w) team.emplace_back(worker, w);
     for (int64_t k = 0; k < nchunks && !rc; ++k) {
-        const int s = (int)(k % kSlots);
-        std::unique_lock<std::mutex> lk(mu);
-        cv_main.wait(lk, [&] { return finished[s] == T; });
-        finished[s] = 0;
-        if (k + kSlots < nchunks) {
-            lk.unlock();
-            rc = enqueue(k + kSlots);
-            lk.lock();
-            if (rc) abort = true;
-            else enq = k + kSlots + 1;
+        if (cudaEventSynchronize(copied[k % S].e) != cudaSuccess) {
+            rc = fail(PARBA_ECUDA, "waiting for staged chunk %lld failed", (long long)k);
+            std::lock_guard<std::mutex> lk(mu);
+            abort = true;
+            cv_work.notify_all();
+            break;
         }
-        lk.unlock();
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            ready = k + 1;
+        }
         cv_work.notify_all();
+        if (k >= 1) {  // chunk k-1's slot is next in line for chunk k-1+S
+            const int s = (int)((k - 1) % S);
+            std::unique_lock<std::mutex> lk(mu);
+            cv_main.wait(lk, [&] { return finished[s] == T; });
+            finished[s] = 0;
+            lk.unlock();
+            if (k - 1 + S < nchunks && (rc = enqueue(k - 1 + S))) {
+                std::lock_guard<std::mutex> lk2(mu);
+                abort = true;
+                cv_work.notify_all();
+            }
+        }
     }
     for (auto &t : team) t.join();
     if (rc) return rc;
-    if (werr) return fail(PARBA_ECUDA, "waiting for a staged chunk failed");
-    unsigned long long pr = 0;
-    CUDA_TRY(cudaMemcpyAsync(&pr, prb.p, sizeof(pr), cudaMemcpyDeviceToHost, sc.s));
+    if (mid > lo) CUDA_TRY(cudaStreamSynchronize(sx2.s));
+    unsigned long long pr[2] = {0, 0};
+    CUDA_TRY(cudaMemcpyAsync(pr, prb.p, sizeof(pr), cudaMemcpyDeviceToHost, sc.s));
     CUDA_TRY(cudaStreamSynchronize(sc.s));
     CUDA_TRY(cudaStreamSynchronize(sx.s));
-    if (probes_host) *probes_host = pr;
+    if (probes_host) *probes_host = pr[0] + pr[1];
     if (ms) *ms = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - w0).count();
     return PARBA_OK;
 }

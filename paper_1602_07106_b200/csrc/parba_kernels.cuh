@@ -65,9 +65,19 @@ constexpr uint64_t kRyMin = 1ull << 27;
 #define PARBA_MINB_STREAM 1
 #endif
 constexpr int kWarps = PARBA_WARPS;        // warps per CTA
+// Window sink: bins of the lowest nodes privatised in shared memory (0 = off)
+#ifndef PARBA_WIN_SMEM
+#define PARBA_WIN_SMEM 0
+#endif
+constexpr uint32_t kWinSmem = PARBA_WIN_SMEM;
 // Store-mode stage buffers (tiles in flight): 2 = flush tile t-1 after
 // phase 2 of tile t; 3 = flush tile t-2 (its chains have had a whole tile
 // longer to finish, so the flush rarely waits).
+// phase-2 loop of the store sinks: refill+probe steps per loop-condition
+// test (2: +0.35% at C2, profiles/r02_ab_window_smem_and_unroll.txt)
+#ifndef PARBA_P2_UNROLL
+#define PARBA_P2_UNROLL 2
+#endif
 #ifndef PARBA_NBUF
 #define PARBA_NBUF 2
 #endif
@@ -148,7 +158,8 @@ struct TileLayout {
     static constexpr uint32_t kSlotB = kSlots ? kQueue * 2 : 0;
     static constexpr size_t kTabB = Hash::kHasCrc ? (Hash::kTableWords + kTile) * 4 : 0;
     static constexpr size_t kHistB = is_targets(SINK) ? kHistGroups * kHistBucketsMax * 4 : 0;
-    static constexpr size_t fixed = kQB /* alignment pad */ + kTabB + kHistB;
+    static constexpr size_t kWinB = SINK == kWindow ? kWinSmem * 4 : 0;
+    static constexpr size_t fixed = kQB /* alignment pad */ + kTabB + kHistB + kWinB;
     static constexpr size_t per_warp = kQB + kStageB + kSlotB;
 };
 constexpr uint64_t kValueMask52 = (1ull << 52) - 1;
@@ -156,18 +167,37 @@ constexpr uint64_t kValueMask52 = (1ull << 52) - 1;
 // kLaunchEdgesPerWarp edges per warp (the host splits larger ranges).
 constexpr uint64_t kLaunchEdgesPerWarp = 1ull << 27;
 
+// Window sink, optional shared-memory privatisation (the north star's
+// suggestion; A/B knob PARBA_WIN_SMEM, off): the counts of the lowest nodes --
+// the hottest part of the window, node v draws ~1/sqrt(v) of the targets --
+// live in a per-CTA u32 array in shared memory and are added to the global
+// window once at the end of the launch.  Measured at C3: 8K bins -1.8%, 16K
+// bins -4.8% (the bins cost resident warps; only ~2% of edges hit the window
+// and its 800 KB stay in L2), profiles/r02_ab_window_smem_and_unroll.txt.
+
+__device__ __forceinline__ void win_add(const SinkArgs &a, uint32_t wsm, uint64_t t) {
+#if PARBA_WIN_SMEM > 0
+    if (t < kWinSmem) {
+        asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(wsm + 4u * (uint32_t)t) : "memory");
+        return;
+    }
+#endif
+    atomicAdd(a.win + t, 1ull);
+}
+
 // A chain finished with terminal value r: hand its target to the sink.
 template <bool NARROW, bool SEED, int SINK, class R, bool DEG = false>
-__device__ __forceinline__ void finish(uint32_t saddr, uint64_t r, const DevParams &p, const SinkArgs &a) {
+__device__ __forceinline__ void finish(uint32_t saddr, uint64_t r, const DevParams &p, const SinkArgs &a,
+                                       uint32_t wsm = 0) {
     if constexpr (is_store(SINK)) {
         sts_t<R>(saddr, (R)r);  // stage cell; the target is computed at flush
     } else if constexpr (SINK == kWindow) {
         if (SEED && r < p.stop) {
             const uint64_t t = __ldg(p.seed + r);
-            if (t < p.K) atomicAdd(a.win + t, 1ull);
+            if (t < p.K) win_add(a, wsm, t);
         } else if (NARROW ? ((uint32_t)r < p.win_rlim32) : (r < p.win_rlim)) {
             // generated target < K  <=>  r < win_rlim
-            atomicAdd(a.win + source_of<NARROW, SEED, DEG>(r >> 1, p), 1ull);
+            win_add(a, wsm, source_of<NARROW, SEED, DEG>(r >> 1, p));
         }
     } else {
         atomicAdd(a.full + target_of<NARROW, SEED, false, DEG>(r, p), 1u);
@@ -203,6 +233,16 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
         smem_raw + pad + (size_t)wpc * (L::kQB + L::kStageB + L::kSlotB) + L::kTabB);
     if constexpr (is_targets(SINK))
         for (int b = threadIdx.x; b < kHistGroups * a.nb; b += blockDim.x) hist_s[b] = 0;
+    // window sink: privatised bins after the stage/slot areas (kWinB bytes)
+    [[maybe_unused]] uint32_t *win_s = reinterpret_cast<uint32_t *>(
+        smem_raw + pad + (size_t)wpc * (L::kQB + L::kStageB + L::kSlotB) + L::kTabB);
+    [[maybe_unused]] uint32_t wsm = 0;
+#if PARBA_WIN_SMEM > 0
+    if constexpr (SINK == kWindow) {
+        for (uint32_t b = threadIdx.x; b < kWinSmem; b += blockDim.x) win_s[b] = 0;
+        wsm = opaque(smem_addr(win_s));
+    }
+#endif
     __syncthreads();
 
     // shared-window addresses of this warp's queue, stage and slot ring
@@ -376,7 +416,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
                 emit(fin != 0, (uint64_t)nr[q]);
             } else if (fin) {
                 if constexpr (is_store(SINK)) PARBA_CHECK(saddr[q] - stage_s < L::kStageB);
-                finish<NARROW, SEED, SINK, R, DEG>(saddr[q], (uint64_t)nr[q], p, a);
+                finish<NARROW, SEED, SINK, R, DEG>(saddr[q], (uint64_t)nr[q], p, a, wsm);
             }
         }
     };
@@ -456,7 +496,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
             if constexpr (is_store(SINK))  // final unless pending
                 sts_t<R>(cell, r1);
             if constexpr (is_targets(SINK)) emit(valid && done, (uint64_t)r1);
-            else if constexpr (!is_store(SINK)) if (valid && done) finish<NARROW, SEED, SINK, R, DEG>(0u, (uint64_t)r1, p, a);
+            else if constexpr (!is_store(SINK)) if (valid && done) finish<NARROW, SEED, SINK, R, DEG>(0u, (uint64_t)r1, p, a, wsm);
             const bool pend = valid && !done;
             const unsigned m = ballot_all(pend);
             const uint32_t cur = tailb + (__popc(m & ltmask) << L::kLgEB);
@@ -498,6 +538,18 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
         // ---- phase 2: pop queued chains into idle lanes and probe while at
         // least a full warp of entries is queued (the < 32 newest entries
         // carry over to the next tile, so every refill can fill every idle lane)
+#if PARBA_P2_UNROLL >= 2
+        // two refill+probe steps per loop test while >= 2 warps of entries wait
+        if (is_store(SINK) && tailb - headb >= ((64u * NS) << L::kLgEB)) {
+            const uint32_t lim2 = tailb - ((64u * NS) << L::kLgEB);
+            do {
+                refill(std::true_type{});
+                step();
+                refill(std::true_type{});
+                step();
+            } while (headb <= lim2);
+        }
+#endif
         if (tailb - headb >= ((32u * NS) << L::kLgEB)) {
             const uint32_t lim = tailb - ((32u * NS) << L::kLgEB);
             do {
@@ -556,6 +608,13 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
             a.hist[(uint64_t)b * kHistGroups * gridDim.x + (uint64_t)kHistGroups * blockIdx.x + g] = hist_s[i];
         }
     }
+#if PARBA_WIN_SMEM > 0
+    if constexpr (SINK == kWindow) {  // privatised bins -> the global window
+        __syncthreads();
+        for (uint32_t b = threadIdx.x; b < kWinSmem && b < p.K; b += blockDim.x)
+            if (win_s[b]) atomicAdd(a.win + b, (unsigned long long)win_s[b]);
+    }
+#endif
     if constexpr (is_store(SINK)) {
         if constexpr (kStageBufs == 2) {
             if (have_prev) flush(buf ^ 1u, prev_base);
