@@ -164,14 +164,16 @@ int launch_tiles_t(const DevParams &dp, uint64_t lo, uint64_t hi, const SinkArgs
     auto kern = tile_kernel<Hash, SINK, SEED, DEG>;
     // as many warps per CTA (<= kWarps) as the shared memory allows
     const size_t fixed = TileLayout<Hash, SINK>::fixed, per_warp = TileLayout<Hash, SINK>::per_warp;
-    int warps = kWarps;
+    int warps = warps_for(SINK);
     while (warps > 1 && fixed + warps * per_warp > (size_t)di->smem_optin) --warps;
     const size_t smem = fixed + warps * per_warp;
     int per_sm = 0;
     {
         std::lock_guard<std::mutex> lk(g_mu);
         if (!di->attr_done[variant][SINK][SEED]) {
-            CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(fixed + kWarps * per_warp > (size_t)di->smem_optin ? di->smem_optin : fixed + kWarps * per_warp)));
+            const size_t want = fixed + (size_t)warps_for(SINK) * per_warp;
+            CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)(want > (size_t)di->smem_optin ? di->smem_optin : want)));
             di->attr_done[variant][SINK][SEED] = true;
         }
     }

@@ -84,6 +84,11 @@ constexpr uint32_t kWinSmem = PARBA_WIN_SMEM;
 constexpr int kStageBufs = PARBA_NBUF;
 
 constexpr int kThreads = kWarps * 32;
+// Warps per CTA of the streaming sinks (window, full, targets); with
+// PARBA_MINB_STREAM = 2 two such CTAs share an SM (A/B knob).
+#ifndef PARBA_WARPS_STREAM
+#define PARBA_WARPS_STREAM 32
+#endif
 
 // kTargets: the full histogram's first pass — each warp appends the u32
 // targets it finishes to its own region of a scratch buffer (order is
@@ -97,6 +102,7 @@ enum SinkKind { kStore = 0, kWindow = 1, kFull = 2, kTargets = 3, kTargetsK = 4,
 constexpr int kSinkKinds = 6;
 __host__ __device__ constexpr bool is_targets(int sink) { return sink == kTargets || sink == kTargetsK; }
 __host__ __device__ constexpr bool is_store(int sink) { return sink == kStore || sink == kStoreT; }
+__host__ __device__ constexpr int warps_for(int sink) { return is_store(sink) ? kWarps : PARBA_WARPS_STREAM; }
 #ifndef PARBA_HIST_BUCKETS
 #define PARBA_HIST_BUCKETS 2048
 #endif
@@ -205,7 +211,7 @@ __device__ __forceinline__ void finish(uint32_t saddr, uint64_t r, const DevPara
 }
 
 template <class Hash, int SINK, bool SEED, bool DEG = false>
-__global__ void __launch_bounds__(kThreads, is_store(SINK) ? PARBA_MINB_STORE : PARBA_MINB_STREAM)
+__global__ void __launch_bounds__(32 * warps_for(SINK), is_store(SINK) ? PARBA_MINB_STORE : PARBA_MINB_STREAM)
 tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntiles,
             SinkArgs a, unsigned long long *probes_out) {
     using R = typename Hash::R;

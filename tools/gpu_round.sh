@@ -35,3 +35,14 @@ echo "ncu window full rc=$?"
 ncu --set full --clock-control none --import-source on -c 12 \
     -o $OUT/${TAG}_full_c4 python bench.py --only full_c4 --steps 1 --warmup 0 > $OUT/${TAG}_ncu_c4.log 2>&1
 echo "ncu c4 rc=$?"
+# reports -> text on the box (gpurun brings back at most 64 MiB)
+for R in $OUT/${TAG}_*.ncu-rep; do
+  [ -f "$R" ] || continue
+  B=${R%.ncu-rep}
+  ncu -i "$R" --page raw --csv > ${B}_raw.csv 2>/dev/null
+  ncu -i "$R" --page details --csv > ${B}_details.csv 2>/dev/null
+  ncu -i "$R" --page source --csv --print-source sass > ${B}_sass.csv 2>/dev/null
+  gzip -f ${B}_sass.csv
+  [ "${KEEP_REPS:-0}" = "1" ] || rm -f "$R"
+done
+ls -la $OUT/ | tail -30
