@@ -504,6 +504,11 @@ def main() -> None:
     # reduce of the histogram (N > 1); max over ranks.
     extra = {}
     int_peak = peaks.get("int32_lane_ops_per_s")
+    mode_traffic = {}
+    mpath = os.path.join(ROOT, "profiles", "r02_mode_traffic.json")
+    if os.path.exists(mpath):
+        with open(mpath) as fh:
+            mode_traffic = json.load(fh)
     if not args.no_extra_modes:
         todo = [("window_c3", C3, C3["K"], 2), ("full_c4", C4, C4["n"], 5), ("window_c5", C5, C5["K"], 1)]
         if args.only:
@@ -542,9 +547,13 @@ def main() -> None:
                                "steps": steps}
                 if int_peak:
                     ach = eps / ws * 2 * INT_OPS_PER_PROBE  # per GPU, SURVEY 8d convention: 64 lane-ops/edge
+                    tb = mode_traffic.get("full_c4_first_batch" if full else "window_c5", {}).get("dram_bytes_per_edge")
                     extra[name]["roofline"] = {
                         "bound": "int", "achieved": ach, "peak": int_peak, "unit": "int32 lane-ops/s per GPU",
-                        "frac": ach / int_peak, "traffic": None,
+                        "frac": ach / int_peak,
+                        "traffic": tb * (b - a) if tb is not None else None,
+                        "traffic_note": "DRAM bytes of one step on this rank, scaled from the committed ncu capture "
+                                        "(profiles/r02_mode_traffic.json: bytes per edge)",
                         "convention": "32 int32 lane-ops per hash probe, 2 probes per edge (SURVEY 8d)",
                         "peak_source": "measured in this run (parba_peak_int32)"}
                 if full:
