@@ -633,10 +633,10 @@ int parba_multi_run_shards(const parba_params_t *ph, int nshards, const int *dev
         return fail(PARBA_EINVAL, "full histogram needs 2m < 2^32 (uint32 counters); use the window mode");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess) ndev = 0;
-    for (int s = 0; s < nshards; ++s) {
+    for (int s = 0; s < nshards; ++s)
         if ((rc = check_range(ph, los[s], his[s]))) return rc;
+    for (int s = 0; s < nshards; ++s)
         if (devs[s] < 0 || devs[s] >= ndev) return fail(PARBA_EINVAL, "device %d of shard %d not visible", devs[s], s);
-    }
     // group shards by distinct device, in order of first appearance
     std::vector<int> udev;
     for (int s = 0; s < nshards; ++s)

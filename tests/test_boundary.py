@@ -107,6 +107,53 @@ def test_abi_option_flag_and_degree_sequence_validation(lib_path):
     assert L.parba_node_of_edges(ctypes.byref(u), fake, 1, fake, 7, None) == _lib.PARBA_EINVAL
 
 
+def test_abi_round2_entry_points_validation(lib_path):
+    """The round-2 entry points reject bad input on the host, before CUDA."""
+    from paper_1602_07106_b200 import _lib, hashing
+
+    L = _lib.load(lib_path)
+    fake = ctypes.c_void_p(256)
+    simple = hashing.c_params(hashing.HashConfig(kind=hashing.HashKind.SIMPLE), n=10, d=2)
+    assert L.parba_generate_targets(ctypes.byref(simple), 0, 4, fake, None, None) == _lib.PARBA_EINVAL
+    assert b"targets-only" in L.parba_last_error()
+    crc = hashing.c_params(hashing.HashConfig(), n=10, d=2)
+    assert L.parba_generate_targets(ctypes.byref(crc), 3, 1, fake, None, None) == _lib.PARBA_EINVAL
+    flagged = hashing.c_params(hashing.HashConfig(), n=10, d=3, n0=3, m0=3, seed_ptr=512)
+    flagged.flags = _lib.FLAG_NO_SELF_LOOPS
+    assert L.parba_bb_fill(ctypes.byref(flagged), fake, fake, fake, None, None) == _lib.PARBA_EINVAL
+    assert b"plain mode only" in L.parba_last_error()
+    assert L.parba_debug_mod(99, fake, fake, fake, 1, fake, None) == _lib.PARBA_EINVAL
+    assert L.parba_debug_mod_check(0, 1, 10, 0, 5, fake, fake, None) == _lib.PARBA_EINVAL
+    devs = np.zeros(2, dtype=np.int32)
+    los = np.array([0, 5], dtype=np.uint64)
+    his = np.array([5, 21], dtype=np.uint64)  # 21 > m = 20
+    assert L.parba_multi_run_shards(ctypes.byref(crc), 2, devs.ctypes.data, los.ctypes.data, his.ctypes.data,
+                                    _lib.MULTI_DISCARD, 0, None, None, None) == _lib.PARBA_EINVAL
+    assert b"out of range" in L.parba_last_error()
+    assert L.parba_multi_run_shards(ctypes.byref(crc), 2, devs.ctypes.data, los.ctypes.data, his.ctypes.data,
+                                    9, 0, None, None, None) == _lib.PARBA_EINVAL
+    assert L.parba_multi_run_shards(ctypes.byref(crc), 0, None, None, None, _lib.MULTI_DISCARD, 0, None, None,
+                                    None) == _lib.PARBA_EINVAL
+
+
+def test_worker_groups_cover_the_plan():
+    """driver.run's split of the reference plan over workers / ranks."""
+    import paper_1602_07106_b200 as pb
+    from paper_1602_07106_b200 import parallel
+
+    p = pb.GenParams(n=40, d=3, n0=3, seed_edges=np.array([0, 1, 1, 2, 2, 0], dtype=np.uint64))
+    plan = pb.plan_batches(p, 10)
+    for workers in (1, 2, 3, 5, 12, 20):
+        groups = parallel.split_batches(len(plan), workers)
+        assert len(groups) == workers and groups[0][0] == 0 and groups[-1][1] == len(plan)
+        assert all(a <= b for a, b in groups) and all(groups[k][1] == groups[k + 1][0] for k in range(workers - 1))
+        ranges = parallel.group_ranges(p, plan, groups)
+        live = [(a, b) for a, b in ranges if b > a]
+        assert live[0][0] == p.m0 and live[-1][1] == p.m
+        assert all(live[k][1] == live[k + 1][0] for k in range(len(live) - 1))
+        assert sum(b - a for a, b in ranges) == p.m - p.m0
+
+
 def test_product_never_imports_the_oracle():
     for dirpath, _, files in os.walk(PKG):
         for f in files:
