@@ -150,8 +150,8 @@ int generate_host_pairs(const parba_params_t *ph, uint64_t lo, uint64_t hi, uint
 // part; measured slower on this pool's hosts, so off by default.
 
 struct PipeCfg {
-    uint64_t chunk = 1ull << 21;  // edges per staged chunk (8 MiB of targets: stays in the LLC)
-    int slots = 8;                // staging slots in flight
+    uint64_t chunk = 1ull << 20;  // edges per staged chunk (4 MiB of targets: stays in the LLC)
+    int slots = 4;                // staging slots in flight
     double rows_frac = 0.0;       // share of the range sent as 16-byte rows (pinned output only)
 };
 
@@ -335,37 +335,44 @@ int generate_host_targets(const parba_params_t *ph, uint64_t lo, uint64_t hi, ui
         return PARBA_OK;
     };
 
-    // host team: worker w expands slice w of every chunk, in chunk order.  The
-    // main thread alone waits on the copy engine (one event wait per chunk)
-    // and publishes staged chunks; it recycles a slot once every worker is
-    // done with it.
+    // host team: the staged chunks are cut into pieces of kPiece edges that
+    // the workers claim in order from one atomic cursor (a descheduled thread
+    // delays one piece, not a whole chunk).  The main thread alone waits on
+    // the copy engine (one event per chunk), publishes staged chunks, and
+    // recycles a slot once all of its pieces are done.
     const int T = host_threads();
+    constexpr uint64_t kPiece = 1ull << 16;
+    const uint64_t P = (C + kPiece - 1) / kPiece;  // pieces per chunk (the last chunk may use fewer)
     std::mutex mu;
     std::condition_variable cv_work, cv_main;
-    int64_t ready = 0;                 // chunks staged in host memory (guarded by mu)
-    std::vector<int> finished(S, 0);   // workers done with the slot's current chunk (mu)
-    bool abort = false;                // (mu)
-    auto worker = [&](int w) {
-        for (int64_t k = 0; k < nchunks; ++k) {
+    int64_t ready = 0;                    // chunks staged in host memory (guarded by mu)
+    std::vector<uint64_t> done(S, 0);     // pieces finished of the slot's current chunk (mu)
+    bool abort = false;                   // (mu)
+    std::atomic<uint64_t> next{0};
+    const uint64_t total_pieces = nchunks ? (uint64_t)(nchunks - 1) * P + (chunk_n(nchunks - 1) + kPiece - 1) / kPiece : 0;
+    auto pieces_of = [&](int64_t k) { return (chunk_n(k) + kPiece - 1) / kPiece; };
+    auto worker = [&]() {
+        for (;;) {
+            const uint64_t q = next.fetch_add(1, std::memory_order_relaxed);
+            if (q >= total_pieces) return;
+            const int64_t k = (int64_t)(q / P);
+            const uint64_t j = q % P;
             {
                 std::unique_lock<std::mutex> lk(mu);
                 cv_work.wait(lk, [&] { return ready > k || abort; });
                 if (abort) return;
             }
             const int s = (int)(k % S);
-            const uint64_t n = chunk_n(k);
-            // 8-edge-aligned slices (whole 128-byte lines of rows per thread)
-            const uint64_t a = (n * (uint64_t)w / T) & ~7ull;
-            const uint64_t b = w == T - 1 ? n : (n * (uint64_t)(w + 1) / T) & ~7ull;
+            const uint64_t a = j * kPiece, b = std::min(a + kPiece, chunk_n(k));
             expand_rows(out_host + 2 * (chunk_lo(k) - lo), sg.host + (uint64_t)s * C, chunk_lo(k), a, b, ph, nt);
             std::lock_guard<std::mutex> lk(mu);
-            if (++finished[s] == T) cv_main.notify_one();
+            if (++done[s] == pieces_of(k)) cv_main.notify_one();
         }
     };
     for (int64_t k = 0; k < std::min<int64_t>(S, nchunks); ++k)
         if ((rc = enqueue(k))) return rc;
     std::vector<std::thread> team;
-    for (int w = 0; w < T && nchunks > 0; ++w) team.emplace_back(worker, w);
+    for (int w = 0; w < T && nchunks > 0; ++w) team.emplace_back(worker);
     for (int64_t k = 0; k < nchunks && !rc; ++k) {
         if (cudaEventSynchronize(copied[k % S].e) != cudaSuccess) {
             rc = fail(PARBA_ECUDA, "waiting for staged chunk %lld failed", (long long)k);
@@ -382,8 +389,8 @@ int generate_host_targets(const parba_params_t *ph, uint64_t lo, uint64_t hi, ui
         if (k >= 1) {  // chunk k-1's slot is next in line for chunk k-1+S
             const int s = (int)((k - 1) % S);
             std::unique_lock<std::mutex> lk(mu);
-            cv_main.wait(lk, [&] { return finished[s] == T; });
-            finished[s] = 0;
+            cv_main.wait(lk, [&] { return done[s] == pieces_of(k - 1); });
+            done[s] = 0;
             lk.unlock();
             if (k - 1 + S < nchunks && (rc = enqueue(k - 1 + S))) {
                 std::lock_guard<std::mutex> lk2(mu);
