@@ -900,3 +900,23 @@ def test_config3_window_subranges_1e8_vs_oracle():
         torch.cuda.synchronize()
         want, wp = O.run_threaded(_op(p), lo, hi, O.MODE_WINDOW, K=K, threads=threads, batch=1 << 20)
         assert np.array_equal(c.cpu().numpy()[:K], want) and int(prb.item()) == wp, lo
+
+
+@pytest.mark.parametrize("seeded", [False, True])
+def test_wide_store_vs_oracle(seeded):
+    """Wide store launches (chain values >= 2^32, 64-bit stage and queue
+    entries) on ragged ranges, with and without a seed graph, vs the oracle;
+    also a range straddling 2^31 positions (two launch widths)."""
+    import torch
+
+    if seeded:
+        p = pb.GenParams(n=8 * 10**8 + 3, d=10, n0=3, seed_edges=TRIANGLE)
+    else:
+        p = pb.GenParams(n=8 * 10**8, d=10)
+    dev = torch.device("cuda", 0)
+    for lo, hi in ((7 * 10**9 + 11, 7 * 10**9 + 3_000_013), (p.m - 2_000_001, p.m),
+                   ((1 << 31) - 777, (1 << 31) + 1_000_000)):
+        got, prb = pb.generate_block_device(lo, hi, p, device=dev)
+        g = got.cpu().numpy().view(np.uint64)
+        want, wp = O.generate_block(_op(p), lo, hi)
+        assert np.array_equal(g, want) and int(prb.item()) == wp
