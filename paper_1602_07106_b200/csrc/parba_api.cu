@@ -193,7 +193,15 @@ int launch_tiles_t(const DevParams &dp, uint64_t lo, uint64_t hi, const SinkArgs
         if (grid > need) grid = need;
         SinkArgs ac = a;
         if (SINK == kStore) ac.out = a.out + 2 * (a0 - lo);
-        if (SINK == kStoreT) ac.t32 = a.t32 + (a0 - lo);
+        if (SINK == kStoreT && !a.hist) ac.t32 = a.t32 + (a0 - lo);
+        if (SINK == kStoreT && a.hist) {  // one launch; tile-order slots, every nw-th run per CTA
+            if (a1 != hi) return fail(PARBA_ECUDA, "targets pass needs one launch");
+            if (ntiles * kTile > a.t32_cap) return fail(PARBA_ECUDA, "targets scratch too small");
+            a.t32_geom[0] = ntiles * kTile;
+            a.t32_geom[1] = 0;
+            a.t32_geom[2] = (uint64_t)warps;
+            a.t32_geom[3] = grid;
+        }
         if (is_targets(SINK)) {  // one launch; every warp owns capw slots
             if (a1 != hi) return fail(PARBA_ECUDA, "targets pass needs one launch");
             const uint64_t nw = grid * warps;
@@ -245,10 +253,8 @@ int launch_tiles(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint
 
 // Targets-only store (kStoreT): CRC families with uniform degree and n <= 2^32
 // (callers check; parba_host.cu's host-array path).
-int launch_store_targets(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi, uint32_t *t32,
+int launch_store_targets(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi, const SinkArgs &a,
                          unsigned long long *probes, cudaStream_t st) {
-    SinkArgs a{};
-    a.t32 = t32;
     int nc = nc_for(2 * hi);
     if (nc <= 3 && p->d >= (1ull << 31)) nc = 4;
     switch (nc) {
@@ -314,7 +320,9 @@ int launch_store(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint
 }
 int launch_store_t32(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi, uint32_t *t32,
                      unsigned long long *probes, cudaStream_t st) {
-    return launch_store_targets(p, dp, lo, hi, t32, probes, st);
+    SinkArgs a{};
+    a.t32 = t32;
+    return launch_store_targets(p, dp, lo, hi, a, probes, st);
 }
 }  // namespace host
 }  // namespace parba
@@ -493,6 +501,13 @@ int hist_shift(uint64_t K) {
     return ((K + (1ull << shift) - 1) >> shift) <= (uint64_t)kHistBucketsMax ? shift : 0;
 }
 
+// PARBA_STT=0: the full histogram's targets pass by the per-step targets
+// sink (kTargets) instead of the store-targets sink (A/B)
+bool stt_enabled() {
+    const char *e = getenv("PARBA_STT");
+    return !(e && e[0] == '0');
+}
+
 // The position pass (PARBA_POS_MODE=1) measured slower than resolving owners
 // in the targets pass (f4 full, n=1e8, m=1.29e9: 2.13e10 vs 3.35e10 edges/s:
 // the position domain is 13x the node domain -- 3 scatter passes, 8 slices
@@ -519,6 +534,7 @@ bool use_partitioned(const parba_params_t *p, uint64_t lo, uint64_t hi, uint64_t
 struct PartScratch {
     AsyncBuf t32, srt, H, O, tmp, items;
     size_t tmp_bytes = 0;
+    uint64_t stride_nw = 0, stride_ntiles = 0;  // store-targets input: tile-order slots (bucket_scatter_kernel)
     uint64_t max_items = 0;
     int shift = 0, nb = 0, spb_lg = 0;
     int init(uint64_t K, uint64_t slots, uint32_t cols, cudaStream_t st) {
@@ -566,7 +582,7 @@ struct PartScratch {
             const int nbw = nb - wb < kHistBuckets ? nb - wb : kHistBuckets;
             bucket_scatter_kernel<kScatterThreads><<<cols, kScatterThreads, kScatterSmem, st>>>(
                 (const uint32_t *)t32.p, len, wpc, groups, capw, shift, wb, nbw, (const uint32_t *)O.p,
-                (uint32_t *)srt.p);
+                (uint32_t *)srt.p, stride_nw, stride_ntiles);
             CUDA_TRY(cudaGetLastError());
         }
         count_plan_kernel<<<1, kHistThreads, 0, st>>>((const uint32_t *)O.p, (const uint32_t *)H.p, cols, nb,
@@ -618,8 +634,18 @@ int count_partitioned(const parba_params_t *p, const DevParams &dp, uint64_t lo,
         }
         a.t32_cap = cap;
         a.t32_geom = geom;
-        rc = K >= p->n ? launch_tiles<kTargets>(p, dp, b0, b1, a, probes, st)
-                       : launch_tiles<kTargetsK>(p, dp, b0, b1, a, probes, st);
+        // the full histogram of a plain CRC family: the store-targets sink
+        // (terminal values staged per tile, targets written in tile order with
+        // all lanes busy, the bucket histogram counted at the flush)
+        ps.stride_nw = ps.stride_ntiles = 0;
+        if (K >= p->n && !by_pos && targets_only_ok(p) && ps.nb <= kHistBuckets && stt_enabled()) {
+            rc = launch_store_targets(p, dp, b0, b1, a, probes, st);
+            ps.stride_nw = geom[2] * geom[3];                       // warps of the launch
+            ps.stride_ntiles = (b1 - 1) / kTile - b0 / kTile + 1;   // tiles of the batch
+        } else {
+            rc = K >= p->n ? launch_tiles<kTargets>(p, dp, b0, b1, a, probes, st)
+                           : launch_tiles<kTargetsK>(p, dp, b0, b1, a, probes, st);
+        }
         if (rc) return rc;
         const uint32_t used = (uint32_t)geom[3] * kHistGroups;
         if (used > nblk) return fail(PARBA_ECUDA, "targets launch wider than the histogram");

@@ -105,12 +105,16 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t x, uint32_t *w
 // sub-tile order.  One pass handles buckets [wb, wb + nbw) (nbw <=
 // kHistBuckets) and skips the others.  T threads, kScatterTile entries per
 // sub-tile.
+// Strided input (nw > 0: the store-targets sink's tile-order slots): tile
+// CTA c owns tiles k*nw + c*wpc + [0, wpc) for k = 0, 1, ... below ntiles,
+// i.e. its k-th block of wpc*kTile entries starts at slot (k*nw + c*wpc)*kTile.
 template <int T>
 __global__ void __launch_bounds__(T, 1) bucket_scatter_kernel(const uint32_t *__restrict__ t, uint64_t len,
                                                            uint32_t wpc, uint32_t groups, uint64_t capw,
                                                            int shift, int wb, int nbw,
                                                            const uint32_t *__restrict__ O,
-                                                           uint32_t *__restrict__ out) {
+                                                           uint32_t *__restrict__ out, uint64_t nw,
+                                                           uint64_t ntiles) {
     constexpr int BPT = kHistBuckets / T;  // buckets per thread in the scan
     constexpr int PER = kScatterTile / T;  // entries per thread and sub-tile
     static_assert(BPT * T == kHistBuckets && PER % 4 == 0, "scatter shape");
@@ -128,18 +132,35 @@ __global__ void __launch_bounds__(T, 1) bucket_scatter_kernel(const uint32_t *__
     // an entry's bucket in this pass: (v >> shift) - wb, kept when < nbw
     // (empty slots, UINT32_MAX, land above every pass: buckets < 2^(32-shift) - 1)
     auto wbucket = [&](uint32_t v) -> uint32_t { return (v >> shift) - (uint32_t)wb; };
-    const uint64_t s0 = ((uint64_t)blk * wpc + g * wpc / groups) * capw;
+    const uint64_t c0 = (uint64_t)c * wpc;  // strided input: first tile of this CTA
+    uint64_t s0 = ((uint64_t)blk * wpc + g * wpc / groups) * capw;
     const uint64_t e1 = ((uint64_t)blk * wpc + (g + 1) * wpc / groups) * capw;
-    const uint64_t s1 = e1 < len ? e1 : len;
+    uint64_t s1 = e1 < len ? e1 : len;
+    if (nw) {  // strided: logical entries [0, rounds * wpc * kTile) of this CTA (groups == 1)
+        s0 = 0;
+        s1 = ntiles > c0 ? (ntiles - c0 + nw - 1) / nw * wpc * kTile : 0;
+    }
     // coalesced: thread i takes 16-byte words i, i + T, ... of a sub-tile; the
     // next sub-tile's loads are issued before this one is sorted
     uint4 nx[PER / 4];
+    // strided input: logical entry e of this CTA -> block k = e / (wpc*kTile),
+    // offset within the block; k by a float reciprocal of wpc on e / kTile
+    // (< 2^24, the +1/2 margin keeps the rounding exact)
+    const float inv_wpc = 1.0f / (float)wpc;
     auto load = [&](uint64_t base) {
 #pragma unroll
         for (int h = 0; h < PER / 4; ++h) {
             const uint64_t e = base + 4ull * (threadIdx.x + (uint64_t)h * T);
             nx[h] = make_uint4(kEmptyTarget, kEmptyTarget, kEmptyTarget, kEmptyTarget);
-            if (e < s1) nx[h] = ld_stream4(reinterpret_cast<const uint4 *>(t + e));
+            if (nw) {
+                const uint32_t x = (uint32_t)(e / kTile);  // logical tile of this CTA
+                const uint32_t k = __float2uint_rz(__fmaf_rn((float)x, inv_wpc, 0.5f * inv_wpc));
+                const uint64_t tile = (uint64_t)k * nw + c0 + (x - k * wpc);
+                if (e < s1 && tile < ntiles)
+                    nx[h] = ld_stream4(reinterpret_cast<const uint4 *>(t + tile * kTile + (e & (kTile - 1))));
+            } else if (e < s1) {
+                nx[h] = ld_stream4(reinterpret_cast<const uint4 *>(t + e));
+            }
         }
     };
     load(s0);

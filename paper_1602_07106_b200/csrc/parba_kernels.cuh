@@ -163,7 +163,9 @@ struct TileLayout {
     static constexpr bool kSlots = is_store(SINK) && !Hash::kPack;
     static constexpr uint32_t kSlotB = kSlots ? kQueue * 2 : 0;
     static constexpr size_t kTabB = Hash::kHasCrc ? (Hash::kTableWords + kTile) * 4 : 0;
-    static constexpr size_t kHistB = is_targets(SINK) ? kHistGroups * kHistBucketsMax * 4 : 0;
+    static constexpr size_t kHistB = is_targets(SINK)   ? kHistGroups * kHistBucketsMax * 4
+                                     : SINK == kStoreT ? kHistBuckets * 4
+                                                       : 0;
     static constexpr size_t kWinB = SINK == kWindow ? kWinSmem * 4 : 0;
     static constexpr size_t fixed = kQB /* alignment pad */ + kTabB + kHistB + kWinB;
     static constexpr size_t per_warp = kQB + kStageB + kSlotB;
@@ -239,6 +241,9 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
         smem_raw + pad + (size_t)wpc * (L::kQB + L::kStageB + L::kSlotB) + L::kTabB);
     if constexpr (is_targets(SINK))
         for (int b = threadIdx.x; b < kHistGroups * a.nb; b += blockDim.x) hist_s[b] = 0;
+    if constexpr (SINK == kStoreT)
+        if (a.hist)
+            for (int b = threadIdx.x; b < a.nb; b += blockDim.x) hist_s[b] = 0;
     // window sink: privatised bins after the stage/slot areas (kWinB bytes)
     [[maybe_unused]] uint32_t *win_s = reinterpret_cast<uint32_t *>(
         smem_raw + pad + (size_t)wpc * (L::kQB + L::kStageB + L::kSlotB) + L::kTabB);
@@ -299,7 +304,29 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
     auto flush_t = [&](auto full_c, uint32_t b, uint64_t base) {
         [[maybe_unused]] constexpr bool FULL = decltype(full_c)::value;
         if constexpr (SINK == kStoreT) {
-            // targets only (n < 2^32): 4 B per edge, 128 B per warp store
+            // targets only (n < 2^32): 4 B per edge, 128 B per warp store.
+            // Histogram mode (a.hist, the full-histogram count): slot i -
+            // tile0*kTile (tile order, grid-stride tiles as always, so every
+            // CTA sees a representative mix of the batch), empty slots for
+            // positions outside [lo, hi), and bucket = target >> shift
+            // counted in the CTA's histogram; the scatter reads a CTA's tiles
+            // as every nw-th run of wpc tiles.
+            if (a.hist) {
+                uint32_t *o = a.t32 + (int64_t)(base - tile0 * kTile);
+#pragma unroll
+                for (int k = 0; k < kEpl; ++k) {
+                    const uint32_t j = lane + 32u * k;
+                    const uint64_t i = base + j;
+                    uint32_t tg = 0xffffffffu;
+                    if (FULL || (i >= lo && i < hi)) {
+                        tg = (uint32_t)target_of<NARROW, SEED, Hash::kR31, false>(
+                            (uint64_t)lds_t<R>(stage_s + (b * kTile + j) * (uint32_t)sizeof(R)), p);
+                        atomicAdd(hist_s + (tg >> a.shift), 1u);
+                    }
+                    __stcs(o + j, tg);
+                }
+                return;
+            }
             uint32_t *o = a.t32 + (int64_t)(base - lo);
 #pragma unroll
             for (int k = 0; k < kEpl; ++k) {
@@ -630,6 +657,13 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
             const uint32_t b2 = b1 == 0 ? 2u : b1 - 1;
             if (n_inflight == 2) flush(b2, prev_base);
             if (n_inflight >= 1) flush(b1, mid_base);
+        }
+    }
+    if constexpr (SINK == kStoreT) {
+        if (a.hist) {  // the CTA's bucket histogram (its tiles: every nw-th run of wpc tiles)
+            __syncthreads();
+            for (int b = threadIdx.x; b < a.nb; b += blockDim.x)
+                a.hist[(uint64_t)b * gridDim.x + blockIdx.x] = hist_s[b];
         }
     }
 #if PARBA_WARP_TIMES
