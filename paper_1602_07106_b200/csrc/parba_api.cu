@@ -501,6 +501,12 @@ int hist_shift(uint64_t K) {
     return ((K + (1ull << shift) - 1) >> shift) <= (uint64_t)kHistBucketsMax ? shift : 0;
 }
 
+// PARBA_ONE_SLICE=0: power-of-two bucket widths on the store-targets path too (A/B)
+bool one_slice_enabled() {
+    const char *e = getenv("PARBA_ONE_SLICE");
+    return !(e && e[0] == '0');
+}
+
 // PARBA_STT=0: the full histogram's targets pass by the per-step targets
 // sink (kTargets) instead of the store-targets sink (A/B)
 bool stt_enabled() {
@@ -537,10 +543,22 @@ struct PartScratch {
     uint64_t stride_nw = 0, stride_ntiles = 0;  // store-targets input: tile-order slots (bucket_scatter_kernel)
     uint64_t max_items = 0;
     int shift = 0, nb = 0, spb_lg = 0;
-    int init(uint64_t K, uint64_t slots, uint32_t cols, cudaStream_t st) {
+    uint32_t bw = 0;   // bucket width (nodes)
+    Magic32 bdiv{};    // bucket = target / bw
+    // one_slice: buckets of any width <= kSliceMax, each counted by one CTA
+    // (the store-targets path; every other path uses power-of-two widths)
+    int init(uint64_t K, uint64_t slots, uint32_t cols, cudaStream_t st, bool one_slice = false) {
         shift = hist_shift(K);
         nb = (int)((K + (1ull << shift) - 1) >> shift);
         spb_lg = shift - kSliceLg;
+        bw = 1u << shift;
+        bdiv = Magic32{1u, (uint32_t)shift};
+        if (one_slice && spb_lg > 0 && K < (1ull << 31) && (K + kHistBuckets - 1) / kHistBuckets <= kSliceMax) {
+            bw = (uint32_t)((K + kHistBuckets - 1) / kHistBuckets);
+            nb = (int)((K + bw - 1) / bw);
+            spb_lg = 0;
+            bdiv = make_magic32(bw);
+        }
         max_items = nb + slots / kCountChunk + 1;
         int rc;
         if ((rc = t32.alloc(slots * 4, st)) || (rc = srt.alloc(slots * 4, st)) ||
@@ -556,9 +574,9 @@ struct PartScratch {
         CUDA_TRY(cudaGetDevice(&dev));
         if (dev < 64 && !attr[dev]) {
             CUDA_TRY(cudaFuncSetAttribute(slice_count_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          kSliceNodes * 4));
+                                          kSliceMax * 4));
             CUDA_TRY(cudaFuncSetAttribute(slice_count_kernel<unsigned long long>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kSliceNodes * 4));
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kSliceMax * 4));
             CUDA_TRY(cudaFuncSetAttribute(slice_count_pos_kernel<uint32_t>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, kSliceNodes * 4));
             CUDA_TRY(cudaFuncSetAttribute(bucket_scatter_kernel<kScatterThreads>,
@@ -581,7 +599,7 @@ struct PartScratch {
         for (int wb = 0; wb < nb; wb += kHistBuckets) {  // scatter passes
             const int nbw = nb - wb < kHistBuckets ? nb - wb : kHistBuckets;
             bucket_scatter_kernel<kScatterThreads><<<cols, kScatterThreads, kScatterSmem, st>>>(
-                (const uint32_t *)t32.p, len, wpc, groups, capw, shift, wb, nbw, (const uint32_t *)O.p,
+                (const uint32_t *)t32.p, len, wpc, groups, capw, bdiv, wb, nbw, (const uint32_t *)O.p,
                 (uint32_t *)srt.p, stride_nw, stride_ntiles);
             CUDA_TRY(cudaGetLastError());
         }
@@ -594,9 +612,10 @@ struct PartScratch {
                 (const uint32_t *)srt.p, (const uint32_t *)O.p, (const uint32_t *)H.p, cols, nb,
                 (const uint32_t *)items.p, n_items, m0, K, shift, spb_lg, dense, counts);
         else
-            slice_count_kernel<CountT><<<(unsigned)(items_ub << spb_lg), kHistThreads, kSliceNodes * 4, st>>>(
+            slice_count_kernel<CountT><<<(unsigned)(items_ub << spb_lg), kHistThreads,
+                                         (spb_lg ? (size_t)kSliceNodes : (size_t)bw) * 4, st>>>(
                 (const uint32_t *)srt.p, (const uint32_t *)O.p, (const uint32_t *)H.p, cols, nb,
-                (const uint32_t *)items.p, n_items, (uint32_t)K, shift, spb_lg, counts);
+                (const uint32_t *)items.p, n_items, (uint32_t)K, bw, spb_lg, counts);
         CUDA_TRY(cudaGetLastError());
         return PARBA_OK;
     }
@@ -617,7 +636,8 @@ int count_partitioned(const parba_params_t *p, const DevParams &dp, uint64_t lo,
     const uint64_t cap = (batch / kTile + 2) * kTile + (uint64_t)di->sms * 64 * kTile;
     const uint32_t nblk = (uint32_t)di->sms * 4 * kHistGroups;  // >= warp groups of one tile launch
     PartScratch ps;
-    if ((rc = ps.init(K, cap, nblk, st))) return rc;
+    const bool stt = K >= p->n && !by_pos && targets_only_ok(p) && stt_enabled();
+    if ((rc = ps.init(K, cap, nblk, st, stt && one_slice_enabled()))) return rc;
     for (uint64_t b0 = lo; b0 < hi;) {
         uint64_t b1 = hi - b0 > batch ? (b0 / kTile) * kTile + batch : hi;
         if (b1 > hi) b1 = hi;
@@ -627,6 +647,7 @@ int count_partitioned(const parba_params_t *p, const DevParams &dp, uint64_t lo,
         a.hist = (uint32_t *)ps.H.p;  // the tile launch writes the bucket histogram of each CTA's region
         a.shift = ps.shift;
         a.nb = ps.nb;
+        a.bdiv = ps.bdiv;
         a.klim = K;
         if constexpr (sizeof(CountT) == 4) {
             a.by_pos = by_pos ? 1 : 0;
@@ -638,7 +659,7 @@ int count_partitioned(const parba_params_t *p, const DevParams &dp, uint64_t lo,
         // (terminal values staged per tile, targets written in tile order with
         // all lanes busy, the bucket histogram counted at the flush)
         ps.stride_nw = ps.stride_ntiles = 0;
-        if (K >= p->n && !by_pos && targets_only_ok(p) && ps.nb <= kHistBuckets && stt_enabled()) {
+        if (stt && ps.nb <= kHistBuckets) {
             rc = launch_store_targets(p, dp, b0, b1, a, probes, st);
             ps.stride_nw = geom[2] * geom[3];                       // warps of the launch
             ps.stride_ntiles = (b1 - 1) / kTile - b0 / kTile + 1;   // tiles of the batch

@@ -26,6 +26,7 @@ namespace parba {
 constexpr int kSliceLg = 15;                // level-2 slice: 2^15 counters
 constexpr int kSliceNodes = 1 << kSliceLg;  // 128 KB of u32 in shared memory
 constexpr int kMaxSliceLgPerBucket = 3;     // <= 8 slices per bucket
+constexpr uint32_t kSliceMax = 57344;       // one-slice buckets (any width): 224 KB of u32
 constexpr int kHistThreads = 1024;
 #ifndef PARBA_SCATTER_TILE
 #define PARBA_SCATTER_TILE 16384
@@ -111,7 +112,7 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t x, uint32_t *w
 template <int T>
 __global__ void __launch_bounds__(T, 1) bucket_scatter_kernel(const uint32_t *__restrict__ t, uint64_t len,
                                                            uint32_t wpc, uint32_t groups, uint64_t capw,
-                                                           int shift, int wb, int nbw,
+                                                           Magic32 bdiv, int wb, int nbw,
                                                            const uint32_t *__restrict__ O,
                                                            uint32_t *__restrict__ out, uint64_t nw,
                                                            uint64_t ntiles) {
@@ -131,7 +132,11 @@ __global__ void __launch_bounds__(T, 1) bucket_scatter_kernel(const uint32_t *__
         cur[b] = b < nbw ? O[(uint64_t)(wb + b) * gridDim.x + c] : 0u;
     // an entry's bucket in this pass: (v >> shift) - wb, kept when < nbw
     // (empty slots, UINT32_MAX, land above every pass: buckets < 2^(32-shift) - 1)
-    auto wbucket = [&](uint32_t v) -> uint32_t { return (v >> shift) - (uint32_t)wb; };
+    // (bucket = v / width: {1, shift} for a power-of-two width, else a
+    // multiply-high -- exact for v < 2^31; empty slots map far above nbw)
+    auto wbucket = [&](uint32_t v) -> uint32_t {
+        return (uint32_t)(((uint64_t)v * bdiv.mul) >> bdiv.shift) - (uint32_t)wb;
+    };
     const uint64_t c0 = (uint64_t)c * wpc;  // strided input: first tile of this CTA
     uint64_t s0 = ((uint64_t)blk * wpc + g * wpc / groups) * capw;
     const uint64_t e1 = ((uint64_t)blk * wpc + (g + 1) * wpc / groups) * capw;
@@ -267,7 +272,7 @@ __global__ void __launch_bounds__(kHistThreads) slice_count_kernel(const uint32_
                                                                    const uint32_t *__restrict__ H, uint32_t nblk,
                                                                    int nb, const uint32_t *__restrict__ items,
                                                                    const uint32_t *__restrict__ n_items, uint32_t n,
-                                                                   int shift, int spb_lg,
+                                                                   uint32_t bw, int spb_lg,
                                                                    CountT *__restrict__ counts) {
     extern __shared__ uint32_t c[];
     const uint32_t it = blockIdx.x >> spb_lg;
@@ -276,7 +281,7 @@ __global__ void __launch_bounds__(kHistThreads) slice_count_kernel(const uint32_
     const uint32_t b = item & ((1u << kBucketBits) - 1), chunk = item >> kBucketBits;
     PARBA_CHECK((int)b < nb);
     const uint32_t s = blockIdx.x & ((1u << spb_lg) - 1);
-    for (int k = threadIdx.x; k < kSliceNodes; k += blockDim.x) c[k] = 0;
+    for (uint32_t k = threadIdx.x; k < (spb_lg ? (uint32_t)kSliceNodes : bw); k += blockDim.x) c[k] = 0;
     __syncthreads();
     uint32_t e0, e1;
     bucket_range(O, H, nblk, nb, b, e0, e1);
@@ -284,8 +289,13 @@ __global__ void __launch_bounds__(kHistThreads) slice_count_kernel(const uint32_
     const uint32_t k0 = e0 + chunk * kCountChunk;
     const uint32_t k1 = e1 - k0 > kCountChunk ? k0 + kCountChunk : e1;
     const uint32_t smask = (1u << spb_lg) - 1;
+    // bucket width bw: 2^(15 + spb_lg) (slices of 2^15 nodes) or, with
+    // spb_lg = 0, any width up to kSliceMax held in one slice
+    const uint32_t base_b = b * bw;
+    const uint32_t imask = spb_lg ? (uint32_t)(kSliceNodes - 1) : 0xffffffffu;
     auto count = [&](uint32_t x) {
-        if (((x >> kSliceLg) & smask) == s) atomicAdd(&c[x & (kSliceNodes - 1)], 1u);
+        const uint32_t l = x - base_b;
+        if (((l >> kSliceLg) & smask) == s) atomicAdd(&c[l & imask], 1u);
     };
     auto count4 = [&](const uint4 &w) {
         count(w.x);
@@ -313,8 +323,9 @@ __global__ void __launch_bounds__(kHistThreads) slice_count_kernel(const uint32_
     const uint32_t t0 = a0 + 4 * nv;
     if (t0 + threadIdx.x < k1) count(__ldg(sorted + t0 + threadIdx.x));
     __syncthreads();
-    const uint64_t v0 = ((uint64_t)b << shift) + ((uint64_t)s << kSliceLg);
-    for (int k = threadIdx.x; k < kSliceNodes; k += blockDim.x) {
+    const uint64_t v0 = (uint64_t)base_b + ((uint64_t)s << kSliceLg);
+    const uint32_t sw = spb_lg ? (uint32_t)kSliceNodes : bw;
+    for (uint32_t k = threadIdx.x; k < sw; k += blockDim.x) {
         const uint64_t v = v0 + k;
         const uint32_t x = c[k];
         if (v < n && x) {

@@ -136,6 +136,7 @@ struct SinkArgs {
     uint64_t capw;
     uint32_t *hist;                        // targets: H[b * G * gridDim.x + G * blk + group]
     int shift, nb;                         //   (bucket = target >> shift, G = kHistGroups)
+    Magic32 bdiv;                          // store-targets histogram: bucket = target / bucket width
     uint64_t klim;                         // targets: only targets < klim are kept
     int by_pos;                            // targets, degree sequence: emit positions (full counts)
     uint64_t t32_cap;                      // host side: slots of t32
@@ -321,7 +322,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
                     if (FULL || (i >= lo && i < hi)) {
                         tg = (uint32_t)target_of<NARROW, SEED, Hash::kR31, false>(
                             (uint64_t)lds_t<R>(stage_s + (b * kTile + j) * (uint32_t)sizeof(R)), p);
-                        atomicAdd(hist_s + (tg >> a.shift), 1u);
+                        atomicAdd(hist_s + (uint32_t)(((uint64_t)tg * a.bdiv.mul) >> a.bdiv.shift), 1u);
                     }
                     __stcs(o + j, tg);
                 }

@@ -360,6 +360,10 @@ _RAGGED_DEG = np.random.default_rng(7).integers(1, 40, size=200_000)
         ("all_buckets_one_slice", dict(n=1 << 26, d=2), (1 << 26) - (1 << 22) - 5, 0),
         ("four_slices", dict(n=10**8, d=3), 3 * 10**8 - (1 << 23) - 99, 0),
         ("eight_slices", dict(n=5 * 10**8, d=2), 2 * (5 * 10**8) - (1 << 23) - 99, 0),
+        # one-slice buckets (width K / 2048, not a power of two) of the
+        # store-targets path: the whole C4 graph, and a seeded ragged range
+        ("c4_whole_one_slice", dict(n=10**8, d=16), 0, 0),
+        ("one_slice_seeded", dict(n=10**8 + 3, d=2, n0=3, seed_edges=TRIANGLE), 7 * 10**7 + 13, -12345),
         ("simple_hash", dict(n=500_000, d=4, hash=HashConfig(kind=HashKind.SIMPLE, seed0=5)), 0, 0),
         ("degree_sequence", dict(n=3 + _RAGGED_DEG.size, n0=3, degrees=_RAGGED_DEG, seed_edges=TRIANGLE), 3, 0),
     ],
@@ -369,7 +373,8 @@ def test_full_partitioned_equals_direct(case, monkeypatch):
     """The partitioned full histogram (targets -> bucket sort -> shared-memory
     slices, parba_hist.cuh) equals the direct-atomic kernel element-wise,
     probes included, on ragged ranges, seeds, degree sequences, a single
-    bucket, every bucket (2048) of one slice, and 4 or 8 slices per bucket."""
+    bucket, every bucket (2048) of one slice, 4 or 8 slices per bucket, and
+    the one-slice buckets of the store-targets path (C4)."""
     _, kw, lo, hi = case
     p = pb.GenParams(**kw)
     hi = p.m + hi if hi <= 0 else hi
@@ -378,6 +383,10 @@ def test_full_partitioned_equals_direct(case, monkeypatch):
     assert pp == pd
     assert np.array_equal(part, direct)
     assert int(part.astype(np.int64).sum()) == 2 * (hi - lo)
+    if case[0] in ("four_slices", "c4_whole_one_slice"):  # the per-step targets sink and 2^k buckets too
+        monkeypatch.setenv("PARBA_STT", "0")
+        legacy, pl = _full_counts(p, lo, hi, "partition", monkeypatch)
+        assert pl == pd and np.array_equal(legacy, direct)
 
 
 def test_full_partitioned_vs_oracle_small(monkeypatch):
