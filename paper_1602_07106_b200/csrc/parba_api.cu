@@ -111,6 +111,11 @@ DevParams make_dev(const parba_params_t *p, uint64_t K) {
     }
     // narrow launches hold r < 2^32; 2^32-1 is odd, so never a terminal value
     d.win_rlim32 = d.win_rlim > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)d.win_rlim;
+    // wide launches: targets by the FP64 reciprocal (target_fp's bounds);
+    // PARBA_TGT_FP=0 keeps the 64-bit integer division (A/B)
+    const char *tf = getenv("PARBA_TGT_FP");
+    d.tgt_fp = (!is_deg(p) && p->d >= 1 && p->d < 174762 && p->n <= (1ull << 32) && !(tf && tf[0] == '0')) ? 1u : 0u;
+    d.inv2d = 1.0 / (2.0 * (double)dd);
     return d;
 }
 

@@ -106,6 +106,8 @@ struct DevParams {
     Magic32 div32_2d;      // by 2d (every r < 2^31: target = (r - 2m0) / 2d + n0)
     uint64_t win_rlim;     // window mode: generated target < K  <=>  r < win_rlim
     uint32_t win_rlim32;   // min(win_rlim, 2^32 - 1) for narrow launches
+    uint32_t tgt_fp;       // wide launches: targets by the FP64 reciprocal (target_fp)
+    double inv2d;          // RN(1 / (2d))
     uint64_t K;
     // degree sequences (f4): node of a position by rank (degreeseq.py:145-178)
     const uint64_t *W;         // W[k] = first edge of node n0+k, W[n-n0] = m
@@ -175,6 +177,29 @@ __device__ __forceinline__ uint64_t target_of(uint64_t r, const DevParams &p) {
         else return (uint64_t)magic_div32((uint32_t)r, p.div32_2d);
     }
     return source_of<NARROW, SEED>(r >> 1, p);
+}
+
+// Target of a terminal value r < 2^52 (wide launches) without a 64-bit
+// integer division: q = floor((r - 2m0) / 2d) + n0 (generator.py:163-169) as
+// round(x * RN(1/2d) - 1/2 + 2^-19) with x = r - 2m0 exact in a double (the
+// rounding by the 1.5*2^52 magic addition).  For
+// q < 2^32 the product and the first rounding err by at most 2^-20, so the
+// value lies in [Q + phi - 1/2 + 2^-20, Q + phi - 1/2 + 3*2^-20] (phi = the
+// fraction, 0 <= phi <= 1 - 1/2d) and rounds to Q whenever 3*2^-20 < 1/2d,
+// i.e. d < 174762 (the host checks that and n <= 2^32: DevParams.tgt_fp).
+template <bool SEED>
+__device__ __forceinline__ uint64_t target_fp(uint64_t r, const DevParams &p) {
+    if constexpr (SEED) {
+        if (r < p.stop) return __ldg(p.seed + r);
+        r -= p.stop;
+    }
+    const double x = __longlong_as_double((long long)(r | 0x4330000000000000ull)) - 0x1p52;  // exact, r < 2^52
+    // + 1.5*2^52 keeps every sum (>= -1/2) in [2^52, 2^53), where the spacing
+    // is 1: the addition rounds to the integer floor(x / 2d) in the low word
+    const double q = fma(x, p.inv2d, -0.5 + 0x1p-19) + 0x1.8p52;
+    const uint64_t t = (uint64_t)(uint32_t)__double2loint(q);  // floor(x / 2d) < 2^32
+    if constexpr (SEED) return t + p.n0;
+    else return t;
 }
 
 // ---------------------------------------------------------------------------

@@ -347,13 +347,21 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
                     const uint64_t i0 = base + lane - (SEED ? p.m0 : 0);
                     const uint64_t q0 = magic_div(i0, p.div64) + (SEED ? p.n0 : 0);
                     const uint32_t r0 = (uint32_t)(i0 - (q0 - (SEED ? p.n0 : 0)) * p.d);
+                    // targets: FP64 reciprocal (target_fp: one DFMA instead of
+                    // a 64-bit multiply-high division) when the host allows it
+                    auto rows = [&](auto fp_c) {
 #pragma unroll
-                    for (int k = 0; k < kEpl; ++k) {
-                        const uint32_t j = lane + 32u * k;
-                        const uint64_t tgt = target_of<NARROW, SEED, false, false>(
-                            (uint64_t)lds_t<R>(stage_s + (b * kTile + j) * (uint32_t)sizeof(R)), p);
-                        __stcs(o + j, make_ulonglong2(q0 + magic_div32(r0 + 32u * k, p.div32), tgt));
-                    }
+                        for (int k = 0; k < kEpl; ++k) {
+                            const uint32_t j = lane + 32u * k;
+                            const uint64_t r = (uint64_t)lds_t<R>(stage_s + (b * kTile + j) * (uint32_t)sizeof(R));
+                            uint64_t tgt;
+                            if constexpr (decltype(fp_c)::value) tgt = target_fp<SEED>(r, p);
+                            else tgt = target_of<NARROW, SEED, false, false>(r, p);
+                            __stcs(o + j, make_ulonglong2(q0 + magic_div32(r0 + 32u * k, p.div32), tgt));
+                        }
+                    };
+                    if (p.tgt_fp) rows(std::true_type{});
+                    else rows(std::false_type{});
                     return;
                 }
             }

@@ -929,3 +929,25 @@ def test_wide_store_vs_oracle(seeded):
         g = got.cpu().numpy().view(np.uint64)
         want, wp = O.generate_block(_op(p), lo, hi)
         assert np.array_equal(g, want) and int(prb.item()) == wp
+
+
+@pytest.mark.parametrize("n,d,seeded", [((1 << 32), 174761, False), ((1 << 32) - 1, 3, True),
+                                        (10**9, 174761, True), (3 * 10**9, 1000, False), (10**9, 174762, False)])
+def test_wide_store_fp64_targets_at_the_bounds(n, d, seeded, monkeypatch):
+    """Wide store targets by the FP64 reciprocal (target_fp: n <= 2^32,
+    d < 174762) at the edges of its range, and d = 174762 (integer path),
+    vs the oracle and vs the 64-bit integer division (PARBA_TGT_FP=0)."""
+    import torch
+
+    kw = dict(n0=3, seed_edges=TRIANGLE) if seeded else {}
+    p = pb.GenParams(n=n, d=d, **kw)
+    dev = torch.device("cuda", 0)
+    for lo, hi in ((p.m - 600_017, p.m), (p.m // 2 - 300_000, p.m // 2 + 300_001)):
+        got, prb = pb.generate_block_device(lo, hi, p, device=dev)
+        g = got.cpu().numpy().view(np.uint64)
+        want, wp = O.generate_block(_op(p), lo, hi)
+        assert np.array_equal(g, want) and int(prb.item()) == wp, (lo, hi)
+        monkeypatch.setenv("PARBA_TGT_FP", "0")
+        alt, _ = pb.generate_block_device(lo, hi, p, device=dev)
+        monkeypatch.delenv("PARBA_TGT_FP")
+        assert np.array_equal(alt.cpu().numpy().view(np.uint64), g)
