@@ -312,31 +312,38 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
             // positions outside [lo, hi), and bucket = target >> shift
             // counted in the CTA's histogram; the scatter reads a CTA's tiles
             // as every nw-th run of wpc tiles.
-            if (a.hist) {
-                uint32_t *o = a.t32 + (int64_t)(base - tile0 * kTile);
+            // wide launches: targets by the FP64 reciprocal when allowed
+            auto tgt_at = [&](auto fp_c, uint32_t j) -> uint32_t {
+                const uint64_t r = (uint64_t)lds_t<R>(stage_s + (b * kTile + j) * (uint32_t)sizeof(R));
+                if constexpr (!NARROW && decltype(fp_c)::value) return (uint32_t)target_fp<SEED>(r, p);
+                else return (uint32_t)target_of<NARROW, SEED, Hash::kR31, false>(r, p);
+            };
+            auto rows = [&](auto fp_c) {
+                if (a.hist) {
+                    uint32_t *o = a.t32 + (int64_t)(base - tile0 * kTile);
+#pragma unroll
+                    for (int k = 0; k < kEpl; ++k) {
+                        const uint32_t j = lane + 32u * k;
+                        const uint64_t i = base + j;
+                        uint32_t tg = 0xffffffffu;
+                        if (FULL || (i >= lo && i < hi)) {
+                            tg = tgt_at(fp_c, j);
+                            atomicAdd(hist_s + (uint32_t)(((uint64_t)tg * a.bdiv.mul) >> a.bdiv.shift), 1u);
+                        }
+                        __stcs(o + j, tg);
+                    }
+                    return;
+                }
+                uint32_t *o = a.t32 + (int64_t)(base - lo);
 #pragma unroll
                 for (int k = 0; k < kEpl; ++k) {
                     const uint32_t j = lane + 32u * k;
                     const uint64_t i = base + j;
-                    uint32_t tg = 0xffffffffu;
-                    if (FULL || (i >= lo && i < hi)) {
-                        tg = (uint32_t)target_of<NARROW, SEED, Hash::kR31, false>(
-                            (uint64_t)lds_t<R>(stage_s + (b * kTile + j) * (uint32_t)sizeof(R)), p);
-                        atomicAdd(hist_s + (uint32_t)(((uint64_t)tg * a.bdiv.mul) >> a.bdiv.shift), 1u);
-                    }
-                    __stcs(o + j, tg);
+                    if (FULL || (i >= lo && i < hi)) __stcs(o + j, tgt_at(fp_c, j));
                 }
-                return;
-            }
-            uint32_t *o = a.t32 + (int64_t)(base - lo);
-#pragma unroll
-            for (int k = 0; k < kEpl; ++k) {
-                const uint32_t j = lane + 32u * k;
-                const uint64_t i = base + j;
-                if (FULL || (i >= lo && i < hi))
-                    __stcs(o + j, (uint32_t)target_of<NARROW, SEED, Hash::kR31, false>(
-                                      (uint64_t)lds_t<R>(stage_s + (b * kTile + j) * (uint32_t)sizeof(R)), p));
-            }
+            };
+            if (!NARROW && p.tgt_fp) rows(std::true_type{});
+            else rows(std::false_type{});
         } else if constexpr (SINK == kStore) {
             ulonglong2 *o = reinterpret_cast<ulonglong2 *>(a.out) + (int64_t)(base - lo);
             if constexpr (FULL && !NARROW && !DEG) {

@@ -158,7 +158,8 @@ def test_multi_run_two_devices():
 # --------------------------------------------------------------------------- host-array pipeline
 
 
-@pytest.mark.parametrize("n,d,n0,lo_frac", [(10**5, 4, 0, 0.0), (3 * 10**6, 11, 3, 0.3), (10**8, 10, 0, 0.9)])
+@pytest.mark.parametrize("n,d,n0,lo_frac", [(10**5, 4, 0, 0.0), (3 * 10**6, 11, 3, 0.3), (10**8, 10, 0, 0.9),
+                                            (8 * 10**8, 10, 3, 0.9)])
 def test_generate_block_host_pipeline(n, d, n0, lo_frac, monkeypatch):
     """Targets-only pipeline == 16-byte-row path == the oracle (several
     chunks, unaligned range starts, seeds)."""
