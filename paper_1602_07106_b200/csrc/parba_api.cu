@@ -116,6 +116,8 @@ DevParams make_dev(const parba_params_t *p, uint64_t K) {
     const char *tf = getenv("PARBA_TGT_FP");
     d.tgt_fp = (!is_deg(p) && p->d >= 1 && p->d < 174762 && p->n <= (1ull << 32) && !(tf && tf[0] == '0')) ? 1u : 0u;
     d.inv2d = 1.0 / (2.0 * (double)dd);
+    // the window sink only resolves targets < K: the same bound holds for any n
+    d.win_fp = (!is_deg(p) && p->d >= 1 && p->d < 174762 && K <= (1ull << 32) && !(tf && tf[0] == '0')) ? 1u : 0u;
     return d;
 }
 

@@ -107,6 +107,7 @@ struct DevParams {
     uint64_t win_rlim;     // window mode: generated target < K  <=>  r < win_rlim
     uint32_t win_rlim32;   // min(win_rlim, 2^32 - 1) for narrow launches
     uint32_t tgt_fp;       // wide launches: targets by the FP64 reciprocal (target_fp)
+    uint32_t win_fp;       // window hits (targets < K <= 2^32) by target_fp
     double inv2d;          // RN(1 / (2d))
     uint64_t K;
     // degree sequences (f4): node of a position by rank (degreeseq.py:145-178)

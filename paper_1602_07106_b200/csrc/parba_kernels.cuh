@@ -205,7 +205,14 @@ __device__ __forceinline__ void finish(uint32_t saddr, uint64_t r, const DevPara
             const uint64_t t = __ldg(p.seed + r);
             if (t < p.K) win_add(a, wsm, t);
         } else if (NARROW ? ((uint32_t)r < p.win_rlim32) : (r < p.win_rlim)) {
-            // generated target < K  <=>  r < win_rlim
+            // generated target < K  <=>  r < win_rlim (wide: the FP64 reciprocal
+            // instead of a 64-bit division when the host allows it)
+            if constexpr (!NARROW && !DEG) {
+                if (p.win_fp) {
+                    win_add(a, wsm, target_fp<SEED>(r, p));
+                    return;
+                }
+            }
             win_add(a, wsm, source_of<NARROW, SEED, DEG>(r >> 1, p));
         }
     } else {
