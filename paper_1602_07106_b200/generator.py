@@ -38,6 +38,7 @@ HOST_CHUNK_EDGES = 1 << 25
 # one load per owner lookup instead of a rank entry + owners gather) when it
 # fits in this many bytes and in a quarter of the free device memory.
 DENSE_OWNER_MAX_BYTES = 1 << 34
+DENSE_FORCE = False  # A/B (tools/degseq_lookup_ab.py): build the map without zero-degree nodes too
 
 
 class Edge(NamedTuple):
@@ -138,7 +139,13 @@ class GenParams:
             rb = degreeseq.build_rank_bits(pi, device=dev)
             dense = None
             nbytes = 4 * (self.m - self.m0)
-            if self.n < (1 << 32) and 0 < nbytes <= DENSE_OWNER_MAX_BYTES:
+            # without zero-degree nodes a rank entry gives the owner directly
+            # (one 16-byte load, with the skewed targets' low positions
+            # L2-resident: 3.37e10 vs 2.94e10 edges/s through the dense map,
+            # tools/degseq_lookup_ab.py); with zeros the rank path needs a
+            # second (owners) gather and the dense map wins (2.96e10 vs 1.67e10)
+            if ((rb.owners_dev is not None or DENSE_FORCE) and self.n < (1 << 32)
+                    and 0 < nbytes <= DENSE_OWNER_MAX_BYTES):
                 free, _ = torch.cuda.mem_get_info(dev)
                 if nbytes <= free // 4:
                     dense = torch.empty(self.m - self.m0, dtype=torch.int32, device=dev)
