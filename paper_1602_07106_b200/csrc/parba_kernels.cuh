@@ -39,6 +39,9 @@ namespace parba {
 
 constexpr int kTile = 256;                 // edges per warp tile (power of two)
 constexpr int kQueue = 512;                // per-warp pending ring (>= kTile + 31)
+#ifndef PARBA_WIDE_SPLIT
+#define PARBA_WIDE_SPLIT 1
+#endif
 constexpr int kEpl = kTile / 32;           // edges per lane in phase 1
 // first probes use the per-tile reciprocal series from 2*base >= 2^27 on
 constexpr uint64_t kRyMin = 1ull << 27;
@@ -158,7 +161,12 @@ struct TileLayout {
     using R = typename Hash::R;
     static constexpr uint32_t kEB = is_store(SINK) ? 8u : (uint32_t)sizeof(R);
     static constexpr uint32_t kLgEB = kEB == 8 ? 3u : 2u;
-    static constexpr uint32_t kQB = kQueue * kEB;
+    // wide store (64-bit values, packed entries): a 256-entry queue, with
+    // phase 1 split in two halves and a drain between them (at most 31 + 128
+    // entries are ever queued), so 32 warps fit instead of 23
+    static constexpr bool kSplit = is_store(SINK) && !Hash::kNarrow && Hash::kPack && PARBA_WIDE_SPLIT;
+    static constexpr uint32_t kQ = kSplit ? 256u : (uint32_t)kQueue;
+    static constexpr uint32_t kQB = kQ * kEB;
     static constexpr uint32_t kTB = kTile * (uint32_t)sizeof(R);  // one stage buffer
     static constexpr uint32_t kStageB = is_store(SINK) ? kStageBufs * kTB : 0;
     static constexpr bool kSlots = is_store(SINK) && !Hash::kPack;
@@ -522,17 +530,19 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
     // multiples of 64, so 1/r0 comes from one reciprocal per lane and tile,
     // c = 1/rc at the centre rc, and the first-order series
     // 1/(rc + e) ~ c - e*c^2 (relative error (e/rc)^2 < 2^-38 for |e| <= 224).
-    auto phase1 = [&](auto full_c, auto ry_c, uint64_t base, uint32_t cb) {
+    [[maybe_unused]] double rc = 0.0, c = 0.0, s64 = 0.0;  // RY: this lane's series of the current tile
+    auto ry_setup = [&](uint64_t base) {
+        rc = u52_to_f64(2 * base + 2 * lane + 1 + 224);
+        c = recip_approx(rc);
+        s64 = 64.0 * c * c;
+    };
+    // first probes of the lane's edges k in [KB, KE) of the tile
+    auto phase1 = [&](auto full_c, auto ry_c, uint64_t base, uint32_t cb, auto kb_c, auto ke_c) {
         constexpr bool FULL = decltype(full_c)::value;
         constexpr bool RY = decltype(ry_c)::value;
-        [[maybe_unused]] double rc = 0.0, c = 0.0, s64 = 0.0;
-        if constexpr (RY) {
-            rc = u52_to_f64(2 * base + 2 * lane + 1 + 224);
-            c = recip_approx(rc);
-            s64 = 64.0 * c * c;
-        }
+        constexpr int KB = decltype(kb_c)::value, KE = decltype(ke_c)::value;
 #pragma unroll
-        for (int k = 0; k < kEpl; ++k) {
+        for (int k = KB; k < KE; ++k) {
             const uint32_t j = lane + 32u * k;
             const uint64_t i = base + j;
             const bool valid = FULL || ((i >= lo) && (i < hi));
@@ -580,39 +590,56 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
         tile_q0 = tailb;  // queue position where this tile's entries start
         uint32_t cb = 0;
         if constexpr (Hash::kHasCrc) cb = Hash::crc(tabs, 2 * base, p);
+        // ---- phase 2 body: pop queued chains into idle lanes and probe while
+        // at least a full warp of entries is queued (the < 32 newest entries
+        // carry over, so every refill can fill every idle lane)
+        auto drain = [&]() {
+#if PARBA_P2_UNROLL >= 2
+            // two refill+probe steps per loop test while >= 2 warps of entries wait
+            if (is_store(SINK) && tailb - headb >= ((64u * NS) << L::kLgEB)) {
+                const uint32_t lim2 = tailb - ((64u * NS) << L::kLgEB);
+                do {
+                    refill(std::true_type{});
+                    step();
+                    refill(std::true_type{});
+                    step();
+                } while (headb <= lim2);
+            }
+#endif
+            if (tailb - headb >= ((32u * NS) << L::kLgEB)) {
+                const uint32_t lim = tailb - ((32u * NS) << L::kLgEB);
+                do {
+                    refill(std::true_type{});
+                    step();
+                } while (headb <= lim);
+            }
+        };
+        // phase 1 over all 8 edges per lane, or in two halves with a drain
+        // between them (the 256-entry queue of the wide store)
+        auto run_phase1 = [&](auto full_c, auto ry_c) {
+            if constexpr (decltype(ry_c)::value) ry_setup(base);
+            if constexpr (L::kSplit) {
+                phase1(full_c, ry_c, base, cb, std::integral_constant<int, 0>{}, std::integral_constant<int, kEpl / 2>{});
+                __syncwarp();
+                drain();
+                phase1(full_c, ry_c, base, cb, std::integral_constant<int, kEpl / 2>{},
+                       std::integral_constant<int, kEpl>{});
+            } else {
+                phase1(full_c, ry_c, base, cb, std::integral_constant<int, 0>{}, std::integral_constant<int, kEpl>{});
+            }
+        };
         if (base >= lo && base + kTile <= hi) {
             if constexpr (Hash::kHasRy) {
-                if (2 * base >= kRyMin) phase1(std::true_type{}, std::true_type{}, base, cb);
-                else phase1(std::true_type{}, std::false_type{}, base, cb);
+                if (2 * base >= kRyMin) run_phase1(std::true_type{}, std::true_type{});
+                else run_phase1(std::true_type{}, std::false_type{});
             } else {
-                phase1(std::true_type{}, std::false_type{}, base, cb);
+                run_phase1(std::true_type{}, std::false_type{});
             }
         } else {
-            phase1(std::false_type{}, std::false_type{}, base, cb);
+            run_phase1(std::false_type{}, std::false_type{});
         }
         __syncwarp();
-        // ---- phase 2: pop queued chains into idle lanes and probe while at
-        // least a full warp of entries is queued (the < 32 newest entries
-        // carry over to the next tile, so every refill can fill every idle lane)
-#if PARBA_P2_UNROLL >= 2
-        // two refill+probe steps per loop test while >= 2 warps of entries wait
-        if (is_store(SINK) && tailb - headb >= ((64u * NS) << L::kLgEB)) {
-            const uint32_t lim2 = tailb - ((64u * NS) << L::kLgEB);
-            do {
-                refill(std::true_type{});
-                step();
-                refill(std::true_type{});
-                step();
-            } while (headb <= lim2);
-        }
-#endif
-        if (tailb - headb >= ((32u * NS) << L::kLgEB)) {
-            const uint32_t lim = tailb - ((32u * NS) << L::kLgEB);
-            do {
-                refill(std::true_type{});
-                step();
-            } while (headb <= lim);
-        }
+        drain();
         // ---- store: flush the oldest tile in flight once none of its chains runs
         if constexpr (is_store(SINK)) {
             if (have_prev) {
