@@ -42,6 +42,9 @@ constexpr int kQueue = 512;                // per-warp pending ring (>= kTile + 
 #ifndef PARBA_WIDE_SPLIT
 #define PARBA_WIDE_SPLIT 1
 #endif
+#ifndef PARBA_NARROW_SPLIT
+#define PARBA_NARROW_SPLIT 0  // A/B: the split phase 1 and 256-entry queue for narrow store kernels too
+#endif
 constexpr int kEpl = kTile / 32;           // edges per lane in phase 1
 // first probes use the per-tile reciprocal series from 2*base >= 2^27 on
 constexpr uint64_t kRyMin = 1ull << 27;
@@ -164,7 +167,8 @@ struct TileLayout {
     // wide store (64-bit values, packed entries): a 256-entry queue, with
     // phase 1 split in two halves and a drain between them (at most 31 + 128
     // entries are ever queued), so 32 warps fit instead of 23
-    static constexpr bool kSplit = is_store(SINK) && !Hash::kNarrow && Hash::kPack && PARBA_WIDE_SPLIT;
+    static constexpr bool kSplit =
+        is_store(SINK) && ((!Hash::kNarrow && Hash::kPack && PARBA_WIDE_SPLIT) || (Hash::kNarrow && PARBA_NARROW_SPLIT));
     static constexpr uint32_t kQ = kSplit ? 256u : (uint32_t)kQueue;
     static constexpr uint32_t kQB = kQ * kEB;
     static constexpr uint32_t kTB = kTile * (uint32_t)sizeof(R);  // one stage buffer
