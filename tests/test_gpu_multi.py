@@ -203,3 +203,35 @@ def test_generate_targets_entry_point():
     with pytest.raises(pb.ParameterError, match="targets-only"):
         pb._lib.check(L.parba_generate_targets(s._device_params(dev), 0, 10, t.data_ptr(), None,
                                                pb._lib.stream_ptr(torch, dev)))
+
+
+def test_run_workers_with_option_flags_collect_and_file(tmp_path):
+    """Node-granular plans (option flags) split over workers: Collect and the
+    positional file equal the single-worker result; bb_generate refuses flags."""
+    p = pb.GenParams(n=20_000, d=4, n0=10, seed_edges=ring_edges(10), no_self_loops=True, no_parallel_edges=True)
+    one, s1 = pb.run(p, pb.CollectConsumer(), workers=1, batch_size=5001)
+    three, s3 = pb.run(p, pb.CollectConsumer(), workers=3, batch_size=5001)
+    assert np.array_equal(one, three) and s1.hash_probes == s3.hash_probes
+    plan = pb.plan_batches(p, 5001)
+    assert all((b.lo - p.m0) % 4 == 0 for b in plan)  # node-aligned batches, so node-aligned groups
+    path = str(tmp_path / "f.bin")
+    with pb.EdgeFileWriter(path, p.m0, p.m - p.m0) as w:
+        pb.run(p, w, workers=2, batch_size=3000)
+    assert np.array_equal(np.fromfile(path, dtype="<u8").reshape(-1, 2), one)
+    with pytest.raises(pb.ParameterError, match="plain mode"):
+        pb.bb_generate(p)
+
+
+def test_multi_run_shards_flags_node_cuts():
+    """parba_multi_run_shards with option flags: explicit node-aligned shards
+    on one device (repeated) equal the single-range generation and counts."""
+    p = pb.GenParams(n=30_000, d=5, n0=3, seed_edges=TRIANGLE, no_self_loops=True)
+    want, wp = pb.generate_block(p.m0, p.m, p)
+    cuts = [p.m0, p.first_edge_of(10_000), p.first_edge_of(20_001), p.m]
+    ranges = list(zip(cuts, cuts[1:]))
+    rows, prs = pb.parallel.run_shards(p, "store", 0, ranges, [0, 0, 0])
+    assert np.array_equal(rows, want) and sum(prs) == wp
+    counts, _ = pb.parallel.run_shards(p, "window", 777, ranges, [0, 0, 0])
+    ref = np.zeros(777, dtype=np.int64)
+    O.count_block(ref, want)
+    assert np.array_equal(counts, ref)
