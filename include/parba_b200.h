@@ -257,8 +257,8 @@ int parba_debug_mod_check(int method, uint64_t seed, uint64_t count, uint64_t rm
  * parba_peak_int32: launch an INT32 issue-rate kernel (LOP3 + IADD3 chains)
  * on `stream`; *lane_ops = the lane-operations it executes (time it with
  * events around the call).  scratch: one device u32.
- * parba_peak_write: 16-byte streaming stores over buf[0, bytes) (write-only
- * HBM bandwidth). */
+ * parba_peak_write: 32-byte stores over buf[0, bytes) from many CTAs
+ * (write-only HBM bandwidth; buf 32-byte aligned). */
 int parba_peak_int32(uint32_t *scratch, double *lane_ops, void *stream);
 int parba_peak_write(void *buf, uint64_t bytes, void *stream);
 

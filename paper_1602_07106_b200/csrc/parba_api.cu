@@ -791,9 +791,14 @@ __global__ void __launch_bounds__(256) int_peak_kernel(uint32_t *out, uint32_t s
     if (s == 0x12345678u) out[0] = s;
 }
 
-__global__ void write_peak_kernel(ulonglong2 *out, uint64_t n) {
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-        __stcs(out + i, make_ulonglong2(i, i ^ 0x5555ull));
+// 32-byte stores (st.global.v4.b64, sm_100), many CTAs in flight: the
+// write-only HBM rate rises with outstanding stores (tools/write_probe.cu:
+// 6.1 / 6.9 / 7.2 TB/s with 4 / 8 / 16 CTAs of 512 threads per SM)
+__global__ void __launch_bounds__(512) write_peak_kernel(uint64_t *out, uint64_t n32) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n32; i += (uint64_t)gridDim.x * blockDim.x)
+        asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(out + 4 * i), "l"(i), "l"(i ^ 1ull),
+                     "l"(i ^ 2ull), "l"(i ^ 3ull)
+                     : "memory");
 }
 
 }  // namespace
@@ -818,7 +823,8 @@ int parba_peak_write(void *buf, uint64_t bytes, void *stream) {
     DevInfo *di;
     int rc = dev_info(&di);
     if (rc) return rc;
-    write_peak_kernel<<<(unsigned)di->sms * 8, 512, 0, (cudaStream_t)stream>>>((ulonglong2 *)buf, bytes / 16);
+    if (((uintptr_t)buf) & 31) return fail(PARBA_EINVAL, "buffer must be 32-byte aligned");
+    write_peak_kernel<<<(unsigned)di->sms * 32, 512, 0, (cudaStream_t)stream>>>((uint64_t *)buf, bytes / 32);
     CUDA_TRY(cudaGetLastError());
     return PARBA_OK;
 }

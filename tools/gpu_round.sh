@@ -46,3 +46,7 @@ for R in $OUT/${TAG}_*.ncu-rep; do
   [ "${KEEP_REPS:-0}" = "1" ] || rm -f "$R"
 done
 ls -la $OUT/ | tail -30
+# bench repeats (spread of the default line on one box)
+if [ "${REPEATS:-0}" -gt 0 ]; then
+  for i in $(seq 1 $REPEATS); do timeout 900 python bench.py > $OUT/${TAG}_bench_rep$i.json 2>/dev/null; done
+fi
