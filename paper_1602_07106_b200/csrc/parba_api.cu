@@ -144,6 +144,7 @@ struct DevInfo {
     int sms = 0;
     int smem_optin = 0;  // max dynamic shared memory per block
     bool attr_done[12][kSinkKinds][2] = {};  // [hash variant][sink][seed]
+    int per_sm[12][kSinkKinds][2] = {};      // resident CTAs per SM (0: not queried yet)
 };
 std::mutex g_mu;
 std::vector<DevInfo> g_dev;
@@ -184,8 +185,16 @@ int launch_tiles_t(const DevParams &dp, uint64_t lo, uint64_t hi, const SinkArgs
             di->attr_done[variant][SINK][SEED] = true;
         }
     }
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem));
-    if (per_sm < 1) per_sm = 1;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        per_sm = di->per_sm[variant][SINK][SEED];
+    }
+    if (!per_sm) {  // once per kernel and device (a launch of a small chunk should not pay for it)
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem));
+        if (per_sm < 1) per_sm = 1;
+        std::lock_guard<std::mutex> lk(g_mu);
+        di->per_sm[variant][SINK][SEED] = per_sm;
+    }
     // launches of at most kLaunchEdgesPerWarp edges per warp (tile-aligned
     // cuts), so the kernel's 32-bit queue cursors never wrap
     const uint64_t max_grid = (uint64_t)di->sms * per_sm;

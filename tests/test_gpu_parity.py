@@ -367,6 +367,8 @@ _RAGGED_DEG = np.random.default_rng(7).integers(1, 40, size=200_000)
         # all-node counts of a graph with 2m >= 2^32 (u64 window, K = n): the
         # wide store-targets pass with FP64 targets, 8 slices per bucket
         ("wide_u64_all_nodes", dict(n=10**9, d=10), (1 << 32) + 5, (1 << 32) + 5 + (1 << 23)),
+        # ... and with one scatter pass: the wide store-targets pass (FP64 targets)
+        ("wide_u64_store_targets", dict(n=4 * 10**8, d=16), (1 << 32) + 5, (1 << 32) + 5 + (1 << 23)),
         ("simple_hash", dict(n=500_000, d=4, hash=HashConfig(kind=HashKind.SIMPLE, seed0=5)), 0, 0),
         ("degree_sequence", dict(n=3 + _RAGGED_DEG.size, n0=3, degrees=_RAGGED_DEG, seed_edges=TRIANGLE), 3, 0),
     ],
