@@ -1,4 +1,6 @@
-"""A/B of the hot-low-node split of the partitioned full histogram
+"""(Record of a dropped experiment: the PARBA_LOW_DIV knob is not in the shipped
+library; see profiles/r02_ab_c4_scatter_lean.txt.)
+A/B of the hot-low-node split of the partitioned full histogram
 (PARBA_LOW_DIV = D: targets below ~K/D counted by direct L2 atomics in the
 store-targets pass, the rest bucket-sorted).  C4 (n=1e8, d=16) and two other
 shapes; every setting is checked element-wise against D = 0.  One JSON line."""

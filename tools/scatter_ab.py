@@ -1,4 +1,6 @@
-"""A/B of the full-histogram scatter (C4 and two other shapes): libraries
+"""(Record of a dropped experiment: the PARBA_SCATTER2 knob is not in the shipped
+library; see profiles/r02_ab_c4_scatter_lean.txt.)
+A/B of the full-histogram scatter (C4 and two other shapes): libraries
 given on the command line, and for the current one the env knob
 PARBA_SCATTER2 (1: lean scatter, 0: first form).  Counts checked equal to
 the direct-atomic kernel.  CUDA-event timed, median of 5."""
