@@ -128,11 +128,13 @@ namespace {
 
 int bits_of(uint64_t x) { return x ? 64 - __builtin_clzll(x) : 0; }
 
-// CRC chunk tables needed to cover every chain value of a launch (r < 2*hi):
-// 2 -> r < 2^31 (narrow, 32-bit remainder), 3 -> r < 2^32, 4 -> < 2^43,
-// 5 -> < 2^52, 6 -> any.
-int nc_for(uint64_t two_hi) {
-    const int b = bits_of(two_hi);
+// CRC chunk tables needed to cover every chain value of a launch (r <= 2*hi-1,
+// the largest first value): 2 -> r < 2^31 (narrow, 32-bit remainder),
+// 3 -> r < 2^32, 4 -> < 2^43, 5 -> < 2^52, 6 -> any.  (Classing by 2*hi
+// itself put a range ending at exactly 2^30 edges -- C4's second batch --
+// on the slower 3-chunk kernel.)
+int nc_for(uint64_t max_r) {
+    const int b = bits_of(max_r);
     if (b <= 31) return 2;
     if (b <= 32) return 3;
     if (b <= 43) return 4;
@@ -245,7 +247,7 @@ int launch_tiles_s(const parba_params_t *p, const DevParams &dp, uint64_t lo, ui
 template <int SINK>
 int launch_tiles(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi,
                  const SinkArgs &a, unsigned long long *probes, cudaStream_t st) {
-    int nc = nc_for(2 * hi);
+    int nc = nc_for(2 * hi - 1);
     if (is_deg(p)) {  // degree sequence: owner lookups instead of closed forms
         if (p->hash_kind == PARBA_HASH_SIMPLE)
             return launch_tiles_t<HashSimple<false>, SINK, true, true>(dp, lo, hi, a, probes, st, 8);
@@ -271,7 +273,7 @@ int launch_tiles(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint
 // (callers check; parba_host.cu's host-array path).
 int launch_store_targets(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi, const SinkArgs &a,
                          unsigned long long *probes, cudaStream_t st) {
-    int nc = nc_for(2 * hi);
+    int nc = nc_for(2 * hi - 1);
     if (nc <= 3 && p->d >= (1ull << 31)) nc = 4;
     switch (nc) {
         case 2: return launch_tiles_s<HashCrc<2>, kStoreT>(p, dp, lo, hi, a, probes, st, 6);

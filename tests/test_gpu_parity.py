@@ -956,3 +956,29 @@ def test_wide_store_fp64_targets_at_the_bounds(n, d, seeded, monkeypatch):
         alt, _ = pb.generate_block_device(lo, hi, p, device=dev)
         monkeypatch.delenv("PARBA_TGT_FP")
         assert np.array_equal(alt.cpu().numpy().view(np.uint64), g)
+
+
+@pytest.mark.parametrize("hi", [1 << 30, (1 << 30) + 1, (1 << 30) + 100, 1 << 31, (1 << 31) + 1, (1 << 31) + 77])
+def test_chunk_class_boundaries(hi):
+    """The launch's kernel class follows its largest chain value 2*hi-1:
+    ranges ending at exactly 2^30 / 2^31 edges run the 2- / 3-chunk kernels
+    (r < 2^31 / r < 2^32), one edge more the next class.  Store, window and
+    full counts of [hi - 300017, hi) vs the oracle, ragged top tiles included."""
+    import torch
+
+    p = pb.GenParams(n=27 * 10**7, d=8)
+    op = _op(p)
+    dev = torch.device("cuda", 0)
+    lo = hi - 300_017
+    got, prb = pb.generate_block_device(lo, hi, p, device=dev)
+    want, wp = O.generate_block(op, lo, hi)
+    assert np.array_equal(got.cpu().numpy().view(np.uint64), want) and int(prb.item()) == wp
+    K = 10**5
+    counts, cprb = pb.parallel.count_shard_device(p, K, lo, hi, device=dev)
+    w, _ = O.degree_block(op, lo, hi, K)
+    assert np.array_equal(counts.cpu().numpy(), w) and int(cprb.item()) == wp
+    # all nodes (2m >= 2^32 here: the u64 window kernel with K = n)
+    full, _ = pb.parallel.count_shard_device(p, p.n, lo, hi, device=dev)
+    nodes, cnt = np.unique(want.reshape(-1), return_counts=True)
+    idx = torch.from_numpy(nodes.astype(np.int64)).to(dev)
+    assert np.array_equal(full[idx].cpu().numpy(), cnt) and int(full.sum().item()) == 2 * (hi - lo)
