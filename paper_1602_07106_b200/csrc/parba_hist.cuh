@@ -35,6 +35,9 @@ constexpr int kHistThreads = 1024;
 #define PARBA_SCATTER_THREADS 1024
 #endif
 constexpr int kScatterThreads = PARBA_SCATTER_THREADS;
+#ifndef PARBA_FLUSH_UNROLL
+#define PARBA_FLUSH_UNROLL 4
+#endif
 constexpr int kScatterTile = PARBA_SCATTER_TILE;  // entries per sorted sub-tile (dynamic smem)
 constexpr int kScatterSmem = (4 * kHistBuckets + kScatterTile) * 4;
 constexpr uint32_t kEmptyTarget = 0xffffffffu;
@@ -325,14 +328,28 @@ __global__ void __launch_bounds__(kHistThreads) slice_count_kernel(const uint32_
     __syncthreads();
     const uint64_t v0 = (uint64_t)base_b + ((uint64_t)s << kSliceLg);
     const uint32_t sw = spb_lg ? (uint32_t)kSliceNodes : bw;
-    for (uint32_t k = threadIdx.x; k < sw; k += blockDim.x) {
-        const uint64_t v = v0 + k;
-        const uint32_t x = c[k];
-        if (v < n && x) {
-            if (split) atomicAdd(counts + v, (CountT)x);
-            else counts[v] += x;
+    if (split) {
+        for (uint32_t k = threadIdx.x; k < sw; k += blockDim.x) {
+            const uint64_t v = v0 + k;
+            const uint32_t x = c[k];
+            if (v < n && x) atomicAdd(counts + v, (CountT)x);
         }
+        return;
     }
+    // the CTA owns these counters: read-modify-write, PARBA_FLUSH_UNROLL
+    // independent loads in flight per thread (one round trip per group
+    // instead of one per counter)
+    const uint32_t lim = v0 >= n ? 0u : (uint64_t)sw < n - v0 ? sw : (uint32_t)(n - v0);
+    constexpr int U = PARBA_FLUSH_UNROLL;
+    uint32_t k = threadIdx.x;
+    for (; k + (U - 1) * blockDim.x < lim; k += U * blockDim.x) {
+        CountT old[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) old[u] = counts[v0 + k + u * blockDim.x];
+#pragma unroll
+        for (int u = 0; u < U; ++u) counts[v0 + k + u * blockDim.x] = old[u] + c[k + u * blockDim.x];
+    }
+    for (; k < lim; k += blockDim.x) counts[v0 + k] += c[k];
 }
 
 // Step 3 for positions (degree sequences): like slice_count_kernel over the
