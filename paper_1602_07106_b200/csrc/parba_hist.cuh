@@ -35,6 +35,9 @@ constexpr int kHistThreads = 1024;
 #define PARBA_SCATTER_THREADS 1024
 #endif
 constexpr int kScatterThreads = PARBA_SCATTER_THREADS;
+#ifndef PARBA_COUNT_LOADS
+#define PARBA_COUNT_LOADS 8  // 16-byte loads in flight per thread in the slice count
+#endif
 #ifndef PARBA_FLUSH_UNROLL
 #define PARBA_FLUSH_UNROLL 4
 #endif
@@ -314,13 +317,13 @@ __global__ void __launch_bounds__(kHistThreads) slice_count_kernel(const uint32_
     const uint4 *s4 = reinterpret_cast<const uint4 *>(sorted + a0);
     const uint32_t bd = blockDim.x;
     uint32_t j = threadIdx.x;
-    for (; j + 3 * bd < nv; j += 4 * bd) {
-        const uint4 w0 = __ldg(s4 + j), w1 = __ldg(s4 + j + bd), w2 = __ldg(s4 + j + 2 * bd),
-                    w3 = __ldg(s4 + j + 3 * bd);
-        count4(w0);
-        count4(w1);
-        count4(w2);
-        count4(w3);
+    constexpr int NL = PARBA_COUNT_LOADS;
+    for (; j + (NL - 1) * bd < nv; j += NL * bd) {
+        uint4 w[NL];
+#pragma unroll
+        for (int u = 0; u < NL; ++u) w[u] = __ldg(s4 + j + u * bd);
+#pragma unroll
+        for (int u = 0; u < NL; ++u) count4(w[u]);
     }
     for (; j < nv; j += bd) count4(__ldg(s4 + j));
     const uint32_t t0 = a0 + 4 * nv;
