@@ -349,7 +349,8 @@ namespace {  // partitioned degree counts, defined below the first C block
 bool use_partitioned(const parba_params_t *p, uint64_t lo, uint64_t hi, uint64_t K);
 template <typename CountT>
 int count_partitioned(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi, uint64_t K,
-                      CountT *counts, unsigned long long *probes, cudaStream_t st, bool by_pos = false);
+                      CountT *counts, unsigned long long *probes, cudaStream_t st, bool by_pos = false,
+                      bool *sources_done = nullptr);
 }  // namespace
 
 extern "C" {
@@ -479,8 +480,9 @@ int parba_degree_window(const parba_params_t *p, uint64_t lo, uint64_t hi, uint6
     DevParams dp = make_dev(p, K);
     if (p->flags) return count_nodes_u64(p, dp, lo, hi, K, counts, probes, st);
     if (use_partitioned(p, lo, hi, K)) {  // large windows: partitioned like the full histogram
-        rc = count_partitioned<unsigned long long>(p, dp, lo, hi, K, counts, probes, st);
-        if (rc) return rc;
+        bool src_done = false;
+        rc = count_partitioned<unsigned long long>(p, dp, lo, hi, K, counts, probes, st, false, &src_done);
+        if (rc || src_done) return rc;
         return launch_sources<unsigned long long>(dp, lo, hi, K, counts, st);
     }
     if (is_deg(p)) {
@@ -536,6 +538,12 @@ bool stt_enabled() {
 // in the targets pass (f4 full, n=1e8, m=1.29e9: 2.13e10 vs 3.35e10 edges/s:
 // the position domain is 13x the node domain -- 3 scatter passes, 8 slices
 // per bucket, and the whole dense map read per batch), so it is opt-in.
+// PARBA_FOLD_SOURCES=0: closed-form sources by their own kernel (A/B)
+bool fold_enabled() {
+    const char *e = getenv("PARBA_FOLD_SOURCES");
+    return !(e && e[0] == '0');
+}
+
 bool pos_mode_enabled() {
     const char *e = getenv("PARBA_POS_MODE");
     return e && strcmp(e, "1") == 0;
@@ -610,7 +618,8 @@ struct PartScratch {
     // counted into their owners (slice_count_pos_kernel)
     template <typename CountT>
     int count(uint64_t len, uint64_t capw, uint32_t wpc, uint32_t groups, uint32_t cols, uint64_t K,
-              CountT *counts, cudaStream_t st, const uint32_t *dense = nullptr, uint64_t m0 = 0) {
+              CountT *counts, cudaStream_t st, const uint32_t *dense = nullptr, uint64_t m0 = 0,
+              SrcFold fold = SrcFold{}) {
         uint32_t *n_items = (uint32_t *)items.p + max_items;
         CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, (const uint32_t *)H.p, (uint32_t *)O.p,
                                                (int64_t)nb * cols, st));
@@ -622,7 +631,7 @@ struct PartScratch {
             CUDA_TRY(cudaGetLastError());
         }
         count_plan_kernel<<<1, kHistThreads, 0, st>>>((const uint32_t *)O.p, (const uint32_t *)H.p, cols, nb,
-                                                       (uint32_t *)items.p, n_items);
+                                                       (uint32_t *)items.p, n_items, fold.on);
         CUDA_TRY(cudaGetLastError());
         const uint64_t items_ub = nb + len / kCountChunk + 1;  // >= sum of ceil(size_b / chunk)
         if (dense)
@@ -633,7 +642,7 @@ struct PartScratch {
             slice_count_kernel<CountT><<<(unsigned)(items_ub << spb_lg), kHistThreads,
                                          (spb_lg ? (size_t)kSliceNodes : (size_t)bw) * 4, st>>>(
                 (const uint32_t *)srt.p, (const uint32_t *)O.p, (const uint32_t *)H.p, cols, nb,
-                (const uint32_t *)items.p, n_items, (uint32_t)K, bw, spb_lg, counts);
+                (const uint32_t *)items.p, n_items, (uint32_t)K, bw, spb_lg, counts, fold);
         CUDA_TRY(cudaGetLastError());
         return PARBA_OK;
     }
@@ -644,8 +653,13 @@ struct PartScratch {
 // counts are resolved to owners in order.
 template <typename CountT>
 int count_partitioned(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi, uint64_t K,
-                      CountT *counts, unsigned long long *probes, cudaStream_t st, bool by_pos) {
+                      CountT *counts, unsigned long long *probes, cudaStream_t st, bool by_pos,
+                      bool *sources_done) {
     if (by_pos) K = p->m;
+    // uniform degree: the closed-form sources ride along with the last
+    // batch's slice count (no separate pass over the counts)
+    const bool fold_src = sources_done && !is_deg(p) && !by_pos && p->d >= 1 && fold_enabled();
+    if (sources_done) *sources_done = false;
     DevInfo *di;
     int rc = dev_info(&di);
     if (rc) return rc;
@@ -688,9 +702,12 @@ int count_partitioned(const parba_params_t *p, const DevParams &dp, uint64_t lo,
         if (rc) return rc;
         const uint32_t used = (uint32_t)geom[3] * kHistGroups;
         if (used > nblk) return fail(PARBA_ECUDA, "targets launch wider than the histogram");
+        SrcFold fold{};
+        if (fold_src && b1 == hi) fold = SrcFold{lo, hi, p->m0, p->n0, p->d, 1};
         if ((rc = ps.count<CountT>(geom[0], geom[1], (uint32_t)geom[2], kHistGroups, used, K, counts, st,
-                                   by_pos ? dp.dense : nullptr, p->m0)))
+                                   by_pos ? dp.dense : nullptr, p->m0, fold)))
             return rc;
+        if (fold.on) *sources_done = true;
         b0 = b1;
     }
     return PARBA_OK;
@@ -751,13 +768,14 @@ int parba_degree_full(const parba_params_t *p, uint64_t lo, uint64_t hi, uint32_
     // degree sequence with the dense owner map: partition positions instead
     // of owners (no random owner lookups in the targets pass)
     const bool by_pos = is_deg(p) && dp.dense && p->m < (1ull << 31) && pos_mode_enabled();
+    bool src_done = false;
     if (by_pos ? use_partitioned(p, lo, hi, p->m) : use_partitioned(p, lo, hi, p->n)) {
-        rc = count_partitioned<uint32_t>(p, dp, lo, hi, p->n, counts, probes, st, by_pos);
+        rc = count_partitioned<uint32_t>(p, dp, lo, hi, p->n, counts, probes, st, by_pos, &src_done);
     } else {
         SinkArgs a{nullptr, nullptr, counts};
         rc = launch_tiles<kFull>(p, dp, lo, hi, a, probes, st);
     }
-    if (rc) return rc;
+    if (rc || src_done) return rc;
     return launch_sources<uint32_t>(dp, lo, hi, p->n, counts, st);
 }
 

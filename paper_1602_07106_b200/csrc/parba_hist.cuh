@@ -238,10 +238,24 @@ __device__ __forceinline__ void bucket_range(const uint32_t *O, const uint32_t *
     e1 = (int)b + 1 < nb ? O[(uint64_t)(b + 1) * nblk] : O[last] + H[last];
 }
 
+// Closed-form source counts folded into the last batch's slice count
+// (uniform degree): node v's edges [m0 + (v - n0) d, + d) overlap [lo, hi).
+// Every bucket then gets at least one work item, so every node is visited.
+struct SrcFold {
+    uint64_t lo, hi, m0, n0, d;
+    int on;
+};
+__device__ __forceinline__ uint64_t src_overlap(const SrcFold &f, uint64_t v) {
+    if (v < f.n0) return 0u;
+    const uint64_t a = f.m0 + (v - f.n0) * f.d, b = a + f.d;
+    const uint64_t x = a > f.lo ? a : f.lo, y = b < f.hi ? b : f.hi;
+    return y > x ? y - x : 0u;
+}
+
 __global__ void __launch_bounds__(kHistThreads) count_plan_kernel(const uint32_t *__restrict__ O,
                                                                   const uint32_t *__restrict__ H, uint32_t nblk,
                                                                   int nb, uint32_t *__restrict__ items,
-                                                                  uint32_t *__restrict__ n_items) {
+                                                                  uint32_t *__restrict__ n_items, int all_buckets) {
     __shared__ uint32_t warp_sums[32];
     __shared__ uint32_t carry_s;
     if (threadIdx.x == 0) carry_s = 0;
@@ -252,7 +266,7 @@ __global__ void __launch_bounds__(kHistThreads) count_plan_kernel(const uint32_t
         if ((int)b < nb) {
             uint32_t e0, e1;
             bucket_range(O, H, nblk, nb, b, e0, e1);
-            chunks = e1 > e0 ? (e1 - e0 + kCountChunk - 1) / kCountChunk : 0u;
+            chunks = e1 > e0 ? (e1 - e0 + kCountChunk - 1) / kCountChunk : (all_buckets ? 1u : 0u);
         }
         const uint32_t carry = carry_s;
         const uint32_t base = carry + block_exclusive_scan(chunks, warp_sums);
@@ -279,7 +293,7 @@ __global__ void __launch_bounds__(kHistThreads) slice_count_kernel(const uint32_
                                                                    int nb, const uint32_t *__restrict__ items,
                                                                    const uint32_t *__restrict__ n_items, uint32_t n,
                                                                    uint32_t bw, int spb_lg,
-                                                                   CountT *__restrict__ counts) {
+                                                                   CountT *__restrict__ counts, SrcFold fold) {
     extern __shared__ uint32_t c[];
     const uint32_t it = blockIdx.x >> spb_lg;
     if (it >= *n_items) return;
@@ -331,10 +345,11 @@ __global__ void __launch_bounds__(kHistThreads) slice_count_kernel(const uint32_
     __syncthreads();
     const uint64_t v0 = (uint64_t)base_b + ((uint64_t)s << kSliceLg);
     const uint32_t sw = spb_lg ? (uint32_t)kSliceNodes : bw;
-    if (split) {
+    if (split) {  // the bucket's first chunk also adds the folded sources
+        const bool addsrc = fold.on && chunk == 0;
         for (uint32_t k = threadIdx.x; k < sw; k += blockDim.x) {
             const uint64_t v = v0 + k;
-            const uint32_t x = c[k];
+            const uint64_t x = c[k] + (addsrc && v < n ? src_overlap(fold, v) : 0u);
             if (v < n && x) atomicAdd(counts + v, (CountT)x);
         }
         return;
@@ -345,6 +360,19 @@ __global__ void __launch_bounds__(kHistThreads) slice_count_kernel(const uint32_
     const uint32_t lim = v0 >= n ? 0u : (uint64_t)sw < n - v0 ? sw : (uint32_t)(n - v0);
     constexpr int U = PARBA_FLUSH_UNROLL;
     uint32_t k = threadIdx.x;
+    if (fold.on) {
+        for (; k + (U - 1) * blockDim.x < lim; k += U * blockDim.x) {
+            CountT old[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) old[u] = counts[v0 + k + u * blockDim.x];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                counts[v0 + k + u * blockDim.x] =
+                    old[u] + c[k + u * blockDim.x] + (CountT)src_overlap(fold, v0 + k + u * blockDim.x);
+        }
+        for (; k < lim; k += blockDim.x) counts[v0 + k] += c[k] + (CountT)src_overlap(fold, v0 + k);
+        return;
+    }
     for (; k + (U - 1) * blockDim.x < lim; k += U * blockDim.x) {
         CountT old[U];
 #pragma unroll
