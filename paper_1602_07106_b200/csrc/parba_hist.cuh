@@ -177,10 +177,10 @@ __global__ void __launch_bounds__(T, 1) bucket_scatter_kernel(const uint32_t *__
     load(s0);
     for (int b = threadIdx.x; b < kHistBuckets; b += T) cnt[b] = 0;
     __syncthreads();
-    // five barriers per sub-tile: every shared array is rewritten only after
-    // a barrier that its previous readers must have passed
-    for (uint64_t base = s0; base < s1; base += kScatterTile) {
-        uint32_t v[PER], rk[PER];
+    uint32_t v[PER], rk[PER];
+    // rank of every entry of the sub-tile in nx within its bucket (shared
+    // atomics on cnt), prefetching the sub-tile after it
+    auto rank = [&]() {
 #pragma unroll
         for (int h = 0; h < PER / 4; ++h) {
             v[4 * h] = nx[h].x;
@@ -188,10 +188,19 @@ __global__ void __launch_bounds__(T, 1) bucket_scatter_kernel(const uint32_t *__
             v[4 * h + 2] = nx[h].z;
             v[4 * h + 3] = nx[h].w;
         }
-        load(base + kScatterTile);
 #pragma unroll
         for (int k = 0; k < PER; ++k)
             if (v[k] != kEmptyTarget && wbucket(v[k]) < (uint32_t)nbw) rk[k] = atomicAdd(&cnt[wbucket(v[k])], 1u);
+    };
+    if (s0 < s1) {
+        rank();
+        load(s0 + kScatterTile);
+    }
+    // five barriers per sub-tile: every shared array is rewritten only after
+    // a barrier that its previous readers must have passed.  The next
+    // sub-tile's ranks (cnt) are taken while this one's sorted runs are
+    // written out (sorted, delta): disjoint arrays, so the two overlap.
+    for (uint64_t base = s0; base < s1; base += kScatterTile) {
         __syncthreads();
         uint32_t cb[BPT], sum = 0;
 #pragma unroll
@@ -215,6 +224,8 @@ __global__ void __launch_bounds__(T, 1) bucket_scatter_kernel(const uint32_t *__
         for (int k = 0; k < PER; ++k)
             if (v[k] != kEmptyTarget && wbucket(v[k]) < (uint32_t)nbw) sorted[start[wbucket(v[k])] + rk[k]] = v[k];
         __syncthreads();
+        const bool more = base + kScatterTile < s1;
+        if (more) rank();
         const uint32_t total = total_s;
         for (uint32_t k = threadIdx.x; k < total; k += T) {
             const uint32_t x = sorted[k];
@@ -222,6 +233,7 @@ __global__ void __launch_bounds__(T, 1) bucket_scatter_kernel(const uint32_t *__
             PARBA_CHECK(delta[b] + k < len);
             out[delta[b] + k] = x;
         }
+        if (more) load(base + 2 * kScatterTile);
     }
 }
 
