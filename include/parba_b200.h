@@ -188,6 +188,15 @@ int parba_count_pairs(const uint64_t *pairs, uint64_t count, uint64_t K, unsigne
  * stream back over PCIe (pinned host memory gets full DMA speed). */
 int parba_generate_host(const parba_params_t *p_host_seed, uint64_t lo, uint64_t hi,
                         uint64_t *out_pairs_host, uint64_t *probes_host, int device);
+/* Positional binary edge file (EdgeFileWriter / _pwrite_all, cli.py:109-145):
+ * rows (source, target) of edges lo..hi-1 written into the open file `fd`
+ * at byte offset 16*(i - base_edge) (base_edge = the file's first edge, the
+ * reference's m0).  The file must already span the range (ftruncate).  The
+ * range is mapped (MAP_SHARED) and filled by the host-array pipeline of
+ * parba_generate_host, so rows go straight into the page cache from many
+ * host threads instead of through one pwrite copy.  Blocking. */
+int parba_write_binary(const parba_params_t *p_host_seed, uint64_t lo, uint64_t hi, int fd,
+                       uint64_t base_edge, uint64_t *probes_host, int device);
 /* degree_counts for [lo,hi) into host int64 counts[K] (+=). */
 int parba_degree_window_host(const parba_params_t *p_host_seed, uint64_t lo, uint64_t hi,
                              uint64_t K, int64_t *counts_host, uint64_t *probes_host, int device);

@@ -29,7 +29,7 @@ FLAG_NO_SELF_LOOPS, FLAG_NO_PARALLEL_EDGES = 1, 2
 EXPORTS = (
     "parba_version", "parba_last_error", "parba_device_count", "parba_hash",
     "parba_resolve_chains", "parba_generate", "parba_generate_targets", "parba_edges_at", "parba_degree_window",
-    "parba_degree_full", "parba_count_ids", "parba_generate_host", "parba_degree_window_host",
+    "parba_degree_full", "parba_count_ids", "parba_generate_host", "parba_write_binary", "parba_degree_window_host",
     "parba_degseq_prefix", "parba_degseq_rank", "parba_rank1", "parba_node_of_edges", "parba_count_pairs",
     "parba_multi_run", "parba_multi_run_shards", "parba_crc32c", "parba_mulhi_u64", "parba_degseq_dense",
     "parba_peak_int32", "parba_peak_write", "parba_debug_mod", "parba_debug_mod_check",
@@ -98,6 +98,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
             "parba_degree_full": ([P, u64, u64, vp, vp, vp], i32),
             "parba_count_ids": ([vp, u64, u64, vp, vp], i32),
             "parba_generate_host": ([P, u64, u64, vp, vp, i32], i32),
+            "parba_write_binary": ([P, u64, u64, i32, u64, vp, i32], i32),
             "parba_degree_window_host": ([P, u64, u64, u64, vp, vp, i32], i32),
             "parba_degseq_prefix": ([vp, u64, u64, vp, vp], i32),
             "parba_degseq_rank": ([vp, u64, u64, u64, vp, vp, ctypes.POINTER(u64), vp], i32),

@@ -5,6 +5,12 @@
 
 #include <emmintrin.h>
 #include <sched.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <sys/vfs.h>
+#include <unistd.h>
+#include <cerrno>
+#include <cstring>
 
 #include <algorithm>
 #include <atomic>
@@ -53,6 +59,98 @@ int generate_host_impl(const parba_params_t *ph, uint64_t lo, uint64_t hi, uint6
 int parba_generate_host(const parba_params_t *ph, uint64_t lo, uint64_t hi, uint64_t *out_host,
                         uint64_t *probes_host, int device) {
     return generate_host_impl(ph, lo, hi, out_host, probes_host, device, nullptr);
+}
+
+namespace {
+// pwrite every byte of [buf, buf + len) at `off` (cli.py:109-118)
+int pwrite_all(int fd, const char *buf, uint64_t len, uint64_t off) {
+    while (len) {
+        const ssize_t k = pwrite(fd, buf, len, (off_t)off);
+        if (k < 0) {
+            if (errno == EINTR) continue;
+            return fail(PARBA_EINVAL, "write failed at byte offset %llu: %s", (unsigned long long)off,
+                        strerror(errno));
+        }
+        buf += k;
+        off += (uint64_t)k;
+        len -= (uint64_t)k;
+    }
+    return PARBA_OK;
+}
+
+// Files not in memory (a disk file system): rows generated into host
+// buffers of 2^23 edges by the host pipeline while a writer thread pwrites
+// the previous buffer (mapped writes there pay a page fault and a block
+// allocation per page: 0.9 vs 2.4 GB/s measured into /tmp).
+int write_binary_staged(const parba_params_t *ph, uint64_t lo, uint64_t hi, int fd, uint64_t off,
+                        uint64_t *probes_host, int device) {
+    constexpr uint64_t kChunk = 1ull << 23;
+    const uint64_t C = hi - lo < kChunk ? hi - lo : kChunk;
+    std::vector<uint64_t *> bufs(2, nullptr);
+    for (auto &b : bufs)
+        if (posix_memalign((void **)&b, 4096, C * 16) != 0) {
+            for (auto &x : bufs) free(x);
+            return fail(PARBA_EINVAL, "out of host memory for the file staging buffers");
+        }
+    int rc = PARBA_OK, wrc = PARBA_OK;
+    std::thread writer;
+    uint64_t probes = 0;
+    std::string werr;
+    int k = 0;
+    for (uint64_t a = lo; a < hi && !rc; a += C, k ^= 1) {
+        const uint64_t b = hi - a < C ? hi : a + C;
+        uint64_t pr = 0;
+        rc = generate_host_impl(ph, a, b, bufs[k], &pr, device, nullptr);
+        probes += pr;
+        if (writer.joinable()) writer.join();
+        if (wrc) break;
+        if (rc) break;
+        writer = std::thread([&, k, a, b] {
+            wrc = pwrite_all(fd, reinterpret_cast<const char *>(bufs[k]), 16 * (b - a), off + 16 * (a - lo));
+            if (wrc) werr = parba_last_error();
+        });
+    }
+    if (writer.joinable()) writer.join();
+    for (auto &x : bufs) free(x);
+    if (!rc && wrc) rc = fail(wrc, "%s", werr.c_str());
+    if (!rc && probes_host) *probes_host = probes;
+    return rc;
+}
+}  // namespace
+
+int parba_write_binary(const parba_params_t *ph, uint64_t lo, uint64_t hi, int fd, uint64_t base_edge,
+                       uint64_t *probes_host, int device) {
+    if (probes_host) *probes_host = 0;
+    if (ph && is_deg(ph)) return fail(PARBA_EINVAL, "host entry points take uniform-degree families only");
+    int rc = validate(ph);
+    if (!rc) rc = check_range(ph, lo, hi);
+    if (rc) return rc;
+    if (lo < base_edge) return fail(PARBA_EINVAL, "lo (%llu) is below the file's first edge (%llu)",
+                                    (unsigned long long)lo, (unsigned long long)base_edge);
+    if (hi == lo) return PARBA_OK;
+    struct stat sb;
+    if (fd < 0 || fstat(fd, &sb) != 0) return fail(PARBA_EINVAL, "bad file descriptor %d", fd);
+    const uint64_t off = 16 * (lo - base_edge), len = 16 * (hi - lo);
+    if ((uint64_t)sb.st_size < off + len)
+        return fail(PARBA_EINVAL, "file has %lld bytes, the range needs %llu", (long long)sb.st_size,
+                    (unsigned long long)(off + len));
+    // memory file systems (tmpfs, ramfs): map the range and fill it in place
+    // (7.3 vs 3.6 GB/s for one pwrite thread into /dev/shm); anything else:
+    // staged buffers + pwrite.  PARBA_WRITER_MMAP=0/1 forces either.
+    struct statfs fs;
+    const char *wm = getenv("PARBA_WRITER_MMAP");
+    const bool in_memory = fstatfs(fd, &fs) == 0 && (fs.f_type == 0x01021994 /* TMPFS_MAGIC */ ||
+                                                     fs.f_type == 0x858458f6 /* RAMFS_MAGIC */);
+    if (wm ? wm[0] != '1' : !in_memory) return write_binary_staged(ph, lo, hi, fd, off, probes_host, device);
+    const uint64_t pg = (uint64_t)sysconf(_SC_PAGESIZE);
+    const uint64_t moff = off / pg * pg, mlen = len + (off - moff);
+    // (MAP_POPULATE measured slower: 2.6 GB/s, the kernel faults the pages in on one thread)
+    void *map = mmap(nullptr, mlen, PROT_READ | PROT_WRITE, MAP_SHARED, fd, (off_t)moff);
+    if (map == MAP_FAILED) return fail(PARBA_EINVAL, "mmap of the file failed: %s", strerror(errno));
+    uint64_t *rows = reinterpret_cast<uint64_t *>(static_cast<char *>(map) + (off - moff));
+    rc = generate_host_impl(ph, lo, hi, rows, probes_host, device, nullptr);
+    if (munmap(map, mlen) != 0 && !rc) rc = fail(PARBA_ECUDA, "munmap failed: %s", strerror(errno));
+    return rc;
 }
 
 namespace {

@@ -5,10 +5,13 @@ is stored as two little-endian u64 at byte offset 16*(i - m0), so any range
 of edges can be written by any worker in any order and the file is
 byte-identical for every schedule.
 
-Here a range is generated on the GPU in chunks (the store kernel), each chunk
-is copied into a pinned host buffer while the next one is generated, and a
-writer thread ``pwrite``s the pinned buffer at the edge's file offset --
-device generation, PCIe and the file system overlap.
+Uniform-degree families go through the C ABI's ``parba_write_binary``: the
+file range is mapped and filled by the host-array pipeline (the device
+generates u32 targets, they cross PCIe at 4 B per edge, host threads write
+the (source, target) rows straight into the page cache).  Degree sequences
+are generated on the GPU in chunks (the store kernel), each chunk copied
+into a pinned host buffer while the next one is generated, and a writer
+thread ``pwrite``s it at the edge's file offset.
 """
 
 from __future__ import annotations
@@ -69,12 +72,27 @@ class EdgeFileWriter(driver.Consumer):
 
     def write_range(self, p: GenParams, lo: int, hi: int, device=None) -> tuple[int, int]:
         """Generate edges lo..hi-1 on the GPU and write them at their file
-        offsets.  Returns (bytes written, hash probes)."""
+        offsets.  Returns (bytes written, hash probes).
+
+        Uniform degree: the C ABI's ``parba_write_binary`` maps the file range
+        and fills it with the host-array pipeline (u32 targets over PCIe, rows
+        written into the page cache by a team of host threads).  Degree
+        sequences: device chunks, pinned buffers, one ``pwrite`` thread."""
         _check_block(lo, hi, p)
         if lo == hi:
             return 0, 0
         torch, dev = _device(device)
         L = _lib.load()
+        if p.d is not None and os.environ.get("PARBA_WRITER_PWRITE") != "1":
+            import ctypes
+
+            if lo < self.m0 or 16 * (hi - self.m0) > os.fstat(self.fd).st_size:
+                raise ParameterError(f"edges [{lo}, {hi}) fall outside the file's range")
+            cp, _keep = p._host_params()
+            probes = ctypes.c_uint64(0)
+            idx = dev.index if dev.index is not None else torch.cuda.current_device()
+            _lib.check(L.parba_write_binary(ctypes.byref(cp), lo, hi, self.fd, self.m0, ctypes.byref(probes), idx))
+            return 16 * (hi - lo), int(probes.value)
         total = hi - lo
         cuts = _cuts(p, lo, hi, min(total, FILE_CHUNK_EDGES))  # node-aligned under option flags
         spans = list(zip(cuts, cuts[1:]))

@@ -674,6 +674,54 @@ def test_binary_file_equals_oracle_and_is_schedule_independent(tmp_path):
     assert path.read_bytes() == np.ascontiguousarray(blk, dtype="<u8").tobytes()
 
 
+def test_binary_file_native_writer_vs_pwrite(tmp_path, monkeypatch):
+    """parba_write_binary (the file range mapped and filled by the host
+    pipeline) writes the same bytes as the pinned-buffer pwrite path, for the
+    targets pipeline (CRC) and the 16-byte-row pipeline (SIMPLE hash, option
+    flags), at page-misaligned offsets, and refuses ranges outside the file."""
+    import ctypes
+
+    from paper_1602_07106_b200 import _lib
+
+    fams = [pb.GenParams(n=3 * 10**6, d=7),
+            pb.GenParams(n=2 * 10**5, d=5, hash=HashConfig(kind=HashKind.SIMPLE, seed0=77)),
+            pb.GenParams(n=10**5, d=4, n0=3, seed_edges=TRIANGLE, no_self_loops=True)]
+    for k, p in enumerate(fams):
+        a = p.m0 + 12345 if p.d is not None and not p.no_self_loops else p.m0
+        b = p.m - 777 if not p.no_self_loops else p.m
+        paths = []
+        # mapped range, staged buffers + pwrite (native), pinned buffers + pwrite (Python)
+        for mode, mm in (("0", "1"), ("0", "0"), ("1", None)):
+            monkeypatch.setenv("PARBA_WRITER_PWRITE", mode)
+            if mm is None:
+                monkeypatch.delenv("PARBA_WRITER_MMAP", raising=False)
+            else:
+                monkeypatch.setenv("PARBA_WRITER_MMAP", mm)
+            path = tmp_path / f"w{k}_{mode}{mm}.bin"
+            with pb.EdgeFileWriter(str(path), p.m0, p.m - p.m0) as w:
+                nb, pr = w.write_range(p, a, b)
+            assert nb == 16 * (b - a)
+            paths.append((path, pr))
+        assert len({q.read_bytes() for q, _ in paths}) == 1 and len({pr for _, pr in paths}) == 1
+        op = _op(p)
+        if p.no_self_loops:
+            op = O.OParams(n=p.n, d=p.d, n0=p.n0, seed_edges=tuple(int(x) for x in p.seed_edges),
+                           no_self_loops=True)
+        want, wp = O.generate_block(op, a, b)
+        got = np.fromfile(paths[0][0], dtype="<u8").reshape(-1, 2)[a - p.m0: b - p.m0]
+        assert np.array_equal(got, want) and paths[0][1] == wp
+    monkeypatch.delenv("PARBA_WRITER_PWRITE")
+    monkeypatch.delenv("PARBA_WRITER_MMAP", raising=False)
+    p = fams[0]
+    path = tmp_path / "short.bin"
+    with pb.EdgeFileWriter(str(path), p.m0, 1000) as w:
+        with pytest.raises(pb.ParameterError):
+            w.write_range(p, 0, 2000)
+        cp, _keep = p._host_params()
+        rc = _lib.load().parba_write_binary(ctypes.byref(cp), 0, 2000, w.fd, 0, None, 0)
+        assert rc != 0 and b"range needs" in _lib.load().parba_last_error()
+
+
 # --------------------------------------------------------------------------- C ABI, host-buffer entry points
 
 def test_c_abi_host_entry_points():

@@ -15,6 +15,8 @@ from paper_1602_07106_b200 import io as pio
 
 p = pb.GenParams(n=10**8, d=2)
 res = {"edges": p.m, "bytes": 16 * p.m}
+mode = os.environ.get("PARBA_WRITER_PWRITE", "0")
+res["path"] = "pinned buffers + one pwrite thread" if mode == "1" else "parba_write_binary (mapped range, host pipeline)"
 for name, d in (("dev_shm", "/dev/shm"), ("tmp", "/tmp")):
     free = shutil.disk_usage(d).free
     if free < 2 * 16 * p.m:
