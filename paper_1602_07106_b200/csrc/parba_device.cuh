@@ -385,7 +385,7 @@ __device__ __forceinline__ void build_chunk_tables(uint32_t *tab, int nc, uint32
 // XOR of crc(0, 1 << (s + j)) over the set bits j of x, so the 64 single-bit
 // values are computed once (bitwise) and every entry costs <= 11 XORs -- for
 // kernels with many short-lived CTAs.  bits: 64 words of shared scratch.
-__device__ __forceinline__ void build_chunk_tables_linear(uint32_t *tab, int nc, uint32_t *bits) {
+__device__ __forceinline__ void build_chunk_tables_linear(uint32_t *tab, int nc, uint32_t *bits, uint32_t k0 = 0u) {
     if (threadIdx.x < 64) bits[threadIdx.x] = crc32c_u64_bitwise(0u, 1ull << threadIdx.x);
     __syncthreads();
     for (int e = threadIdx.x; e < nc * 2048; e += blockDim.x) {
@@ -398,6 +398,7 @@ __device__ __forceinline__ void build_chunk_tables_linear(uint32_t *tab, int nc,
                 v ^= bk[j];
                 x &= x - 1;
             }
+            if (k == 0) v ^= k0;  // the seed's crc(s0, 0), folded into table 0
         }
         tab[e] = v;
     }
@@ -518,6 +519,12 @@ struct HashCrc {
     static constexpr int kTableWords = kChunks * 2048;
     using R = typename std::conditional<kNarrow, uint32_t, uint64_t>::type;
     __device__ __forceinline__ static void build(uint32_t *tab, uint32_t k0) { build_chunk_tables(tab, kChunks, k0); }
+    // the same tables from the 64 single-bit CRCs (bits: 64 words of shared
+    // scratch; includes a __syncthreads): <= 11 XORs per entry instead of a
+    // 64-step bitwise CRC
+    __device__ __forceinline__ static void build_linear(uint32_t *tab, uint32_t *bits, uint32_t k0) {
+        build_chunk_tables_linear(tab, kChunks, bits, k0);
+    }
     __device__ __forceinline__ static R from_crc(uint32_t c0, R r, const DevParams &p) {
         if constexpr (NC == 2) return mod_fp31(c0, c0 ^ p.k01, r);
         else if constexpr (kNarrow) return mod_fp<R>(c0, c0 ^ p.k01, u32_to_f64(r));

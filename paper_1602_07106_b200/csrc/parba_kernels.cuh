@@ -251,9 +251,18 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
     uint32_t *clow_s = tabs_p + Hash::kTableWords;  // crc(0, 2j+1), j < kTile (2j+1 < 512)
     const uint32_t tabs = opaque(smem_addr(tabs_p));
     if constexpr (Hash::kHasCrc) {
-        Hash::build(tabs_p, p.k0);
-        for (int j = threadIdx.x; j < kTile; j += blockDim.x)
-            clow_s[j] = crc32c_u64_bitwise(0u, 2u * (uint32_t)j + 1u);
+        // the 64 single-bit CRCs in queue 0's space (unused until phase 1);
+        // every table entry and crc(0, 2j+1) is an XOR of them
+        uint32_t *bits = reinterpret_cast<uint32_t *>(smem_raw + pad);
+        Hash::build_linear(tabs_p, bits, p.k0);
+        for (int j = threadIdx.x; j < kTile; j += blockDim.x) {
+            uint32_t x = 2u * (uint32_t)j + 1u, v = 0u;
+            while (x) {
+                v ^= bits[__ffs(x) - 1];
+                x &= x - 1;
+            }
+            clow_s[j] = v;
+        }
     }
     // targets sink: the CTA's bucket histograms follow the stage and slot
     // areas, i.e. the last kHistB bytes of the layout
