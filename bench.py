@@ -528,6 +528,27 @@ def main() -> None:
                 w = min(b - a, 10**9 if not full else b - a)
                 pb.parallel.count_shard_device(q, K, b - w, b, counts=counts, probes=prb, device=dev)
                 torch.cuda.synchronize(dev)
+                balance = None
+                if ws > 1:
+                    # counting modes: the per-edge cost varies along the ID
+                    # space (window hits are denser at low IDs; C4's upper
+                    # targets spread over more buckets), so one measured step
+                    # on equal shards re-cuts the range into equal-cost
+                    # contiguous shards (parallel.balanced_cuts); the counts
+                    # do not depend on the cuts
+                    cuts0 = [pb.parallel.shard_range(0, q.m, r, ws)[0] for r in range(ws)] + [q.m]
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    pb.parallel.count_shard_device(q, K, a, b, counts=counts, probes=prb, device=dev)
+                    e1.record(stream)
+                    torch.cuda.synchronize(dev)
+                    t_eq = gather(e0.elapsed_time(e1))
+                    cuts = pb.parallel.balanced_cuts(cuts0, t_eq)
+                    a, b = cuts[rank], cuts[rank + 1]
+                    balance = {"partition": "contiguous shards cut to equal cost from one measured step on equal "
+                                            "shards (parallel.balanced_cuts)",
+                               "equal_shard_ms": t_eq, "cuts": cuts}
+                counts.zero_()
                 prb.zero_()
                 barrier()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -549,6 +570,8 @@ def main() -> None:
                                "per_rank_ms_per_step": [1000 * x / steps for x in gather(t_rank)],
                                "n": cfg["n"], "d": cfg["d"], "K": K, "m": q.m, "probes_per_edge": ppe,
                                "steps": steps}
+                if balance:
+                    extra[name]["balance"] = balance
                 if int_peak:
                     ach = eps / ws * 2 * INT_OPS_PER_PROBE  # per GPU, SURVEY 8d convention: 64 lane-ops/edge
                     tb = mode_traffic.get("full_c4_first_batch" if full else "window_c5", {}).get("dram_bytes_per_edge")

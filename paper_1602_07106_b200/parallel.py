@@ -42,6 +42,40 @@ def shard_range(lo: int, hi: int, rank: int, world_size: int) -> tuple[int, int]
     return lo + (rank * n) // world_size, lo + ((rank + 1) * n) // world_size
 
 
+def balanced_cuts(cuts, times, align: int = 256) -> list[int]:
+    """Cut points of a contiguous partition re-balanced by measured cost.
+
+    `cuts` (c_0 < ... <= c_N) is the partition a step ran with and `times`
+    the N per-part device times.  The cost is taken as uniform inside each
+    part (density t_k / (c_{k+1} - c_k)); the new cuts put 1/N of the total
+    cost in every part (interior cuts rounded to multiples of `align`, the
+    tile size).  The reference balances its workers dynamically (batches
+    claimed from a shared cursor, driver.py:200-207); ranks of one
+    collective need their ranges up front, so the balance is taken from a
+    measured warm-up step instead.  Any cover of [c_0, c_N) gives the same
+    counts."""
+    n = len(times)
+    if len(cuts) != n + 1 or n < 1:
+        raise ParameterError("need N + 1 cuts for N times")
+    lo, hi = int(cuts[0]), int(cuts[-1])
+    if n == 1 or hi <= lo or min(times) <= 0:
+        return [int(c) for c in cuts]
+    total = float(sum(times))
+    out = [lo]
+    k, acc = 0, 0.0  # part k, cost before it
+    for j in range(1, n):
+        target = total * j / n
+        while k < n - 1 and acc + times[k] < target:
+            acc += times[k]
+            k += 1
+        a, b = int(cuts[k]), int(cuts[k + 1])
+        x = a + (b - a) * min(1.0, max(0.0, (target - acc) / times[k]))
+        x = int(round(x / align)) * align if align > 1 else int(round(x))
+        out.append(min(hi, max(out[-1], x)))
+    out.append(hi)
+    return out
+
+
 def node_floor(p, x: int) -> int:
     """Largest node boundary <= x (x in [m0, m]); m is a boundary."""
     if x >= p.m:

@@ -206,3 +206,36 @@ def test_node_aligned_cuts_and_shards():
 def test_crc_table_constant_matches_reference(golden):
     arrays, _ = golden
     assert np.array_equal(np.array(pb.CRC32C_TABLE, dtype=np.uint32), arrays["crc_table"])
+
+
+def test_balanced_cuts():
+    """parallel.balanced_cuts: equal-cost contiguous parts under the
+    piecewise-constant density the measured step implies; a cover of the
+    range with monotone, tile-aligned interior cuts."""
+    from paper_1602_07106_b200 import parallel as P
+
+    def cost(cuts, times, a, b):
+        tot = 0.0
+        for k in range(len(times)):
+            lo, hi = max(a, cuts[k]), min(b, cuts[k + 1])
+            if hi > lo:
+                tot += times[k] * (hi - lo) / (cuts[k + 1] - cuts[k])
+        return tot
+
+    rng = np.random.default_rng(5)
+    for _ in range(200):
+        n = int(rng.integers(1, 9))
+        lo = int(rng.integers(0, 1 << 20))
+        hi = lo + int(rng.integers(n, 1 << 34))
+        cuts = [P.shard_range(lo, hi, r, n)[0] for r in range(n)] + [hi]
+        times = list(rng.uniform(0.5, 3.0, size=n))
+        new = P.balanced_cuts(cuts, times, align=1)
+        assert new[0] == lo and new[-1] == hi and all(x <= y for x, y in zip(new, new[1:]))
+        parts = [cost(cuts, times, new[i], new[i + 1]) for i in range(n)]
+        assert max(parts) - min(parts) <= 1e-6 * sum(times) + max(times) * n / max(1, hi - lo) * 4
+        al = P.balanced_cuts(cuts, times)
+        assert all(x % 256 == 0 for x in al[1:-1]) and al[0] == lo and al[-1] == hi
+    assert P.balanced_cuts([0, 5, 10], [1.0, 1.0], align=1) == [0, 5, 10]
+    assert P.balanced_cuts([0, 100, 200, 300, 400], [1, 1, 2, 4], align=1) == [0, 200, 300, 350, 400]
+    with pytest.raises(pb.ParameterError):
+        P.balanced_cuts([0, 1], [1.0, 2.0])
