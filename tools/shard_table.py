@@ -34,7 +34,8 @@ def timed(fn, reps):
 
 
 res = {"note": "per-shard device ms measured sequentially on one B200; max = projected N-GPU step before the "
-               "NCCL reduce; eff = T(N=1) / (N * max)"}
+               "NCCL reduce; eff = T(N=1) / (N * max); 'balanced' = the counting modes' shards re-cut to equal "
+               "cost from the equal-shard times (parallel.balanced_cuts, as bench.py does at N > 1)"}
 modes = [("store_c2", dict(n=10**8, d=10), None, 5), ("window_c3", dict(n=10**9, d=100), 10**5, 1),
          ("full_c4", dict(n=10**8, d=16), 10**8, 3), ("window_c5", dict(n=10**10, d=100), 10**5, 1)]
 only = sys.argv[1:]
@@ -62,6 +63,16 @@ for name, kw, K, reps in modes:
         t1 = t1 if t1 is not None else ms[0]
         rows[N] = {"shard_ms": [round(x, 3) for x in ms], "max_ms": round(max(ms), 3),
                    "edges_per_s_projected": p.m / max(ms) * 1e3, "eff": t1 / (N * max(ms))}
+        if K is not None and N > 1:  # the bench's counting modes: cuts re-balanced by the measured step
+            cuts = pb.parallel.balanced_cuts([pb.parallel.shard_range(0, p.m, r, N)[0] for r in range(N)] + [p.m], ms)
+            bms = []
+            for r in range(N):
+                lo, hi = cuts[r], cuts[r + 1]
+                counts = torch.zeros(K, dtype=torch.int32 if K == p.n else torch.int64, device=dev)
+                f = lambda: pb.parallel.count_shard_device(p, K, lo, hi, counts=counts, probes=prb, device=dev)
+                bms.append(timed(f, reps))
+            rows[N]["balanced"] = {"shard_ms": [round(x, 3) for x in bms], "max_ms": round(max(bms), 3),
+                                   "eff": t1 / (N * max(bms))}
         print(name, N, rows[N], flush=True)
     res[name] = rows
     del out
