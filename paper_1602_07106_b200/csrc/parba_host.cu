@@ -146,7 +146,8 @@ int parba_write_binary(const parba_params_t *ph, uint64_t lo, uint64_t hi, int f
     const uint64_t moff = off / pg * pg, mlen = len + (off - moff);
     // (MAP_POPULATE measured slower: 2.6 GB/s, the kernel faults the pages in on one thread)
     void *map = mmap(nullptr, mlen, PROT_READ | PROT_WRITE, MAP_SHARED, fd, (off_t)moff);
-    if (map == MAP_FAILED) return fail(PARBA_EINVAL, "mmap of the file failed: %s", strerror(errno));
+    if (map == MAP_FAILED)  // e.g. a write-only descriptor: staged buffers + pwrite instead
+        return write_binary_staged(ph, lo, hi, fd, off, probes_host, device);
     uint64_t *rows = reinterpret_cast<uint64_t *>(static_cast<char *>(map) + (off - moff));
     rc = generate_host_impl(ph, lo, hi, rows, probes_host, device, nullptr);
     if (munmap(map, mlen) != 0 && !rc) rc = fail(PARBA_ECUDA, "munmap failed: %s", strerror(errno));

@@ -713,6 +713,20 @@ def test_binary_file_native_writer_vs_pwrite(tmp_path, monkeypatch):
     monkeypatch.delenv("PARBA_WRITER_PWRITE")
     monkeypatch.delenv("PARBA_WRITER_MMAP", raising=False)
     p = fams[0]
+    # a write-only descriptor cannot be mapped: the staged pwrite path takes over
+    import os as _os
+
+    path = tmp_path / "wo.bin"
+    fd = _os.open(str(path), _os.O_WRONLY | _os.O_CREAT | _os.O_TRUNC, 0o644)
+    _os.ftruncate(fd, 16 * 100_000)
+    cp, _keep = p._host_params()
+    pr = ctypes.c_uint64(0)
+    monkeypatch.setenv("PARBA_WRITER_MMAP", "1")  # the mapped path is asked for and refused
+    assert _lib.load().parba_write_binary(ctypes.byref(cp), 0, 100_000, fd, 0, ctypes.byref(pr), 0) == 0
+    monkeypatch.delenv("PARBA_WRITER_MMAP")
+    _os.close(fd)
+    want, wp = O.generate_block(_op(p), 0, 100_000)
+    assert np.array_equal(np.fromfile(path, dtype="<u8").reshape(-1, 2), want) and pr.value == wp
     path = tmp_path / "short.bin"
     with pb.EdgeFileWriter(str(path), p.m0, 1000) as w:
         with pytest.raises(pb.ParameterError):
