@@ -4,5 +4,6 @@
 # check traps) and run the GPU parity suite against it.  On the GPU box:
 #   bash tools/check_build.sh
 set -eu
+mkdir -p build_ab
 python -c "from paper_1602_07106_b200 import build; build.build(out='build_ab/lib_checks.so', defines={'PARBA_DEBUG_CHECKS': 1})"
 PARBA_LIB=build_ab/lib_checks.so python -m pytest tests -m gpu -q -x
