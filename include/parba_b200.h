@@ -252,6 +252,8 @@ int parba_bb_fill(const parba_params_t *p, uint64_t *E, uint64_t *link, unsigned
 #define PARBA_MOD_FP31_SERIES 4       /* the same three with 1/r from phase 1's     */
 #define PARBA_MOD_FP_NARROW_SERIES 5  /* per-tile reciprocal series (r >= 2^27 + 224) */
 #define PARBA_MOD_FP_WIDE_SERIES 6
+#define PARBA_MOD_FP31_SERIES1 7      /* the series + one-stage remainder, r in [2^28 + 224, 2^31) */
+#define PARBA_MOD_FP_WIDE_SERIES1 8   /* the same in 64 bits, r in [2^28 + 224, 2^52)              */
 /* out[k] = (hhi[k] * 2^32 + hlo[k]) mod r[k] by `method` (device buffers). */
 int parba_debug_mod(int method, const uint32_t *hhi, const uint32_t *hlo, const uint64_t *r, uint64_t count,
                     uint64_t *out, void *stream);
@@ -261,6 +263,12 @@ int parba_debug_mod(int method, const uint32_t *hhi, const uint32_t *hlo, const 
  * first_bad[0..2] = (h, r, result) of one failure.  Device buffers. */
 int parba_debug_mod_check(int method, uint64_t seed, uint64_t count, uint64_t rmin, uint64_t rmax,
                           unsigned long long *mismatches, unsigned long long *first_bad, void *stream);
+/* Exact relative-error bound of rcp.approx.ftz.f64 (it reads only the high
+ * word of its operand, so 2^21 operands per exponent cover it): out[0] =
+ * max |y0*x - 1| over biased exponents [e0, e0+ne), out[1] = the same after
+ * the Newton step of the tile kernels' recip_approx.  Device buffer of 2
+ * doubles. */
+int parba_debug_rcp_bound(int e0, int ne, double *out, void *stream);
 
 /* ---- Roofline denominators (measured next to the kernels, bench.py) ----
  * parba_peak_int32: launch an INT32 issue-rate kernel (LOP3 + IADD3 chains)

@@ -32,10 +32,11 @@ EXPORTS = (
     "parba_degree_full", "parba_count_ids", "parba_generate_host", "parba_write_binary", "parba_degree_window_host",
     "parba_degseq_prefix", "parba_degseq_rank", "parba_rank1", "parba_node_of_edges", "parba_count_pairs",
     "parba_multi_run", "parba_multi_run_shards", "parba_crc32c", "parba_mulhi_u64", "parba_degseq_dense",
-    "parba_peak_int32", "parba_peak_write", "parba_debug_mod", "parba_debug_mod_check",
+    "parba_peak_int32", "parba_peak_write", "parba_debug_mod", "parba_debug_mod_check", "parba_debug_rcp_bound",
     "parba_bb_fill",
 )
-MOD_FP31, MOD_FP_NARROW, MOD_FP_WIDE, MOD_INT, MOD_FP31_SERIES, MOD_FP_NARROW_SERIES, MOD_FP_WIDE_SERIES = range(7)
+MOD_FP31, MOD_FP_NARROW, MOD_FP_WIDE, MOD_INT, MOD_FP31_SERIES, MOD_FP_NARROW_SERIES, MOD_FP_WIDE_SERIES, \
+    MOD_FP31_SERIES1, MOD_FP_WIDE_SERIES1 = range(9)
 MULTI_STORE, MULTI_WINDOW, MULTI_FULL, MULTI_DISCARD = 0, 1, 2, 3
 
 
@@ -113,6 +114,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
             "parba_bb_fill": ([P, vp, vp, vp, ctypes.POINTER(i32), vp], i32),
             "parba_debug_mod": ([i32, vp, vp, vp, u64, vp, vp], i32),
             "parba_debug_mod_check": ([i32, u64, u64, u64, u64, vp, vp, vp], i32),
+            "parba_debug_rcp_bound": ([i32, i32, vp, vp], i32),
             "parba_peak_int32": ([vp, ctypes.POINTER(ctypes.c_double), vp], i32),
             "parba_peak_write": ([vp, u64, vp], i32),
             "parba_multi_run_shards": ([P, i32, vp, vp, vp, i32, u64, vp, vp, ctypes.POINTER(ctypes.c_double)], i32),

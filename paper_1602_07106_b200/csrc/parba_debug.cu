@@ -11,6 +11,10 @@
 //                        per-tile reciprocal series (tile_kernel, 2*base >= 2^27):
 //                        element k plays lane-slot k % 8 of a lane whose centre
 //                        is rc = r - (64*(k % 8) - 224).
+//   PARBA_MOD_FP31_SERIES1  the series with phase 1's one-stage remainder
+//                        (mod_fp31_y1: 2-chunk tiles with 2*base >= 2^28)
+//   PARBA_MOD_FP_WIDE_SERIES1  the same for 3- to 5-chunk tiles (mod_fp_y1w)
+//   parba_debug_rcp_bound   the exact error bound of rcp.approx.ftz.f64
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -40,6 +44,8 @@ __device__ __forceinline__ uint64_t eval_mod(int method, uint32_t hhi, uint32_t 
     const double y = fma(-(slot - 3.5), s64, c);
     const double rd = rc + e;
     switch (method) {
+        case PARBA_MOD_FP31_SERIES1: return mod_fp31_y1(hhi, hlo, (uint32_t)r, y);
+        case PARBA_MOD_FP_WIDE_SERIES1: return mod_fp_y1w(hhi, hlo, r, y);
         case PARBA_MOD_FP31_SERIES: return mod_fp31_y(hhi, hlo, (uint32_t)r, rd, y);
         case PARBA_MOD_FP_NARROW_SERIES: return mod_fp_y<uint32_t>(hhi, hlo, rd, y);
         default: return mod_fp_y<uint64_t>(hhi, hlo, rd, y);
@@ -98,7 +104,30 @@ __global__ void mod_check_kernel(int method, uint64_t seed, uint64_t count, uint
     }
 }
 
-bool method_ok(int m) { return m >= PARBA_MOD_FP31 && m <= PARBA_MOD_FP_WIDE_SERIES; }
+bool method_ok(int m) { return m >= PARBA_MOD_FP31 && m <= PARBA_MOD_FP_WIDE_SERIES1; }
+
+// rcp.approx.ftz.f64 (MUFU.RCP64H) reads only the high word of its operand:
+// for one high word (sign 0, biased exponent E, top 20 mantissa bits M) the
+// result y0 is one value, and |y0*x - 1| over the 2^32 operands sharing that
+// high word is largest at the two ends of the low word.  So the maximum over
+// all 2^20 values of M at both ends is the exact bound of the instruction's
+// relative error for exponent E (out[0]); out[1] is the same for the
+// Newton-refined recip_approx at those operands.  Exponents E0 .. E0+ne-1.
+__global__ void rcp_bound_kernel(int e0, int ne, unsigned long long *out) {
+    double m0 = 0.0, m1 = 0.0;
+    const uint32_t total = (uint32_t)ne << 21;
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < total; k += gridDim.x * blockDim.x) {
+        const uint32_t E = (uint32_t)e0 + (k >> 21), M = (k >> 1) & 0xFFFFFu, lo = (k & 1u) ? 0xFFFFFFFFu : 0u;
+        const double x = __hiloint2double((int)((E << 20) | M), (int)lo);
+        double y0;
+        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(x));
+        m0 = fmax(m0, fabs(fma(y0, x, -1.0)));
+        m1 = fmax(m1, fabs(fma(recip_approx(x), x, -1.0)));
+    }
+    // non-negative doubles order like their bit patterns
+    atomicMax(out, (unsigned long long)__double_as_longlong(m0));
+    atomicMax(out + 1, (unsigned long long)__double_as_longlong(m1));
+}
 
 }  // namespace
 
@@ -122,6 +151,15 @@ int parba_debug_mod_check(int method, uint64_t seed, uint64_t count, uint64_t rm
     if (count == 0) return PARBA_OK;
     mod_check_kernel<<<148 * 16, 256, 0, (cudaStream_t)stream>>>(method, seed, count, rmin, rmax, mismatches,
                                                                    first_bad);
+    CUDA_TRY(cudaGetLastError());
+    return PARBA_OK;
+}
+
+int parba_debug_rcp_bound(int e0, int ne, double *out, void *stream) {
+    if (e0 < 1 || ne < 1 || e0 + ne > 2047) return fail(PARBA_EINVAL, "exponents must lie in [1, 2046]");
+    if (!out) return fail(PARBA_EINVAL, "NULL buffer");
+    CUDA_TRY(cudaMemsetAsync(out, 0, 2 * sizeof(double), (cudaStream_t)stream));
+    rcp_bound_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(e0, ne, (unsigned long long *)out);
     CUDA_TRY(cudaGetLastError());
     return PARBA_OK;
 }

@@ -322,6 +322,45 @@ __device__ __forceinline__ uint32_t mod_fp31_y(uint32_t hhi, uint32_t hlo, uint3
     const uint32_t t = hlo + nqb * r;                           // exact mod 2^32
     return min(t, t + r);
 }
+#ifndef PARBA_ONESTAGE
+#define PARBA_ONESTAGE 1
+#endif
+// 4- and 5-chunk tiles too (A/B: C3 window -2.6%, the integer correction
+// costs more than the FP64 stages it saves there; off)
+#ifndef PARBA_ONESTAGE_WIDE
+#define PARBA_ONESTAGE_WIDE 0
+#endif
+constexpr uint64_t kOneStageMin = 1ull << 28;
+// One-stage form for 2^28 <= r < 2^31 (phase 1 of 2-chunk tiles with 2*base
+// >= kOneStageMin): q = round(v), v = hd*y, from h rounded to a double hd
+// (|hd - h| <= 2^11, i.e. <= 2^-17 in v) and y ~ 1/r with relative error
+// eps: |v - h/r| <= (h/r)*eps + 2^-17 with h/r < 2^36.  The tile series gives
+// eps < 2^-38.6: Newton on an rcp.approx whose relative error is < 2^-19.5
+// (2^-39 after the step; the raw bound is checked exhaustively over the
+// instruction's 2^21 operands per exponent by parba_debug_rcp_bound) plus the
+// series truncation (224/2^28)^2 = 2^-40.4.  So |v - h/r| < 0.17 < 1/2 and q
+// is floor(h/r) or floor(h/r) + 1: t = hlo - q*r (mod 2^32) lies in [-r, r)
+// and min(t, t + r) is the remainder, as in mod_fp31_y.  4 FP64 instructions
+// instead of 7 (and no rd).
+__device__ __forceinline__ uint32_t mod_fp31_y1(uint32_t hhi, uint32_t hlo, uint32_t r, double y) {
+    const double hd = fma(u32_to_f64_magic(hhi), 0x1p32, u32_to_f64_magic(hlo));  // h, one rounding
+    const uint32_t nq = (uint32_t)__double2loint(fma(-hd, y, 0x1.8p52));             // -q mod 2^32
+    const uint32_t t = hlo + nq * r;
+    return min(t, t + r);
+}
+// The one-stage form for 2^28 <= r < 2^52 (phase 1 of 3-chunk tiles with
+// 2*base >= kOneStageMin; 4- and 5-chunk tiles with PARBA_ONESTAGE_WIDE): q = round(hd*y) as above (h/r < 2^36,
+// |q - h/r| < 0.17 + 1/2), read whole from the mantissa of 2^52 + q, and t =
+// h - q*r in 64-bit integer arithmetic (its true value lies in [-r, r), so
+// the wrapping product is harmless); one correction.  4 FP64 instructions
+// and ~8 integer ones instead of ~13 FP64 ones.
+__device__ __forceinline__ uint64_t mod_fp_y1w(uint32_t hhi, uint32_t hlo, uint64_t r, double y) {
+    const double hd = fma(u32_to_f64_magic(hhi), 0x1p32, u32_to_f64_magic(hlo));
+    const uint64_t q = (uint64_t)__double_as_longlong(fma(hd, y, 0x1p52)) - 0x4330000000000000ull;
+    int64_t t = (int64_t)((((uint64_t)hhi << 32) | hlo) - q * r);
+    t += (t < 0) ? (int64_t)r : 0;
+    return (uint64_t)t;
+}
 __device__ __forceinline__ uint32_t mod_fp31(uint32_t hhi, uint32_t hlo, uint32_t r) {
     const double rd = cvt31<0>(r);
     return mod_fp31_y(hhi, hlo, r, rd, recip_approx(rd));
@@ -539,6 +578,13 @@ struct HashCrc {
         if constexpr (NC == 2) return mod_fp31_y(c0, c0 ^ p.k01, r, rd, y);
         else return mod_fp_y<R>(c0, c0 ^ p.k01, rd, y);
     }
+    // One-stage remainder (mod_fp31_y1 / mod_fp_y1w) for first probes of
+    // tiles with 2*base >= kOneStageMin (every r >= 2^28): needs no rd
+    static constexpr bool kHasRy1 = PARBA_ONESTAGE && (NC <= 3 || (NC <= 5 && PARBA_ONESTAGE_WIDE));
+    __device__ __forceinline__ static R from_crc_ry1(uint32_t c0, R r, double y, const DevParams &p) {
+        if constexpr (NC == 2) return mod_fp31_y1(c0, c0 ^ p.k01, r, y);
+        else return (R)mod_fp_y1w(c0, c0 ^ p.k01, (uint64_t)r, y);
+    }
     __device__ __forceinline__ static uint32_t crc(uint32_t tab, uint64_t w, const DevParams &p) {
         return crc_chunks<kChunks>(tab, w);
     }
@@ -553,6 +599,9 @@ struct HashCrcBytes {
     static constexpr bool kHasRy = false;
     template <class T>
     __device__ __forceinline__ static T from_crc_ry(uint32_t, T r, double, double, const DevParams &) { return r; }
+    static constexpr bool kHasRy1 = false;
+    template <class T>
+    __device__ __forceinline__ static T from_crc_ry1(uint32_t, T r, double, const DevParams &) { return r; }
     static constexpr bool kNarrow = false;
     static constexpr bool kR31 = false;
     static constexpr bool kPack = false;
@@ -571,6 +620,9 @@ struct HashSimple {
     static constexpr bool kHasRy = false;
     template <class T>
     __device__ __forceinline__ static T from_crc_ry(uint32_t, T r, double, double, const DevParams &) { return r; }
+    static constexpr bool kHasRy1 = false;
+    template <class T>
+    __device__ __forceinline__ static T from_crc_ry1(uint32_t, T r, double, const DevParams &) { return r; }
     static constexpr bool kNarrow = NARROW;
     static constexpr bool kR31 = false;
     static constexpr bool kPack = NARROW;

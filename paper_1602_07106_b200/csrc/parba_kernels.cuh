@@ -539,10 +539,13 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
         return __any_sync(0xffffffffu, x);
     };
 
-    // RY: large tile (2*base >= kRyMin): the lane's 8 start values differ by
+    // RY = 1: large tile (2*base >= kRyMin): the lane's 8 start values differ by
     // multiples of 64, so 1/r0 comes from one reciprocal per lane and tile,
     // c = 1/rc at the centre rc, and the first-order series
     // 1/(rc + e) ~ c - e*c^2 (relative error (e/rc)^2 < 2^-38 for |e| <= 224).
+    // RY = 2: 2-chunk tiles with 2*base >= kOneStageMin take the same series
+    // into the one-stage remainder (mod_fp31_y1: no rd, 4 FP64 instructions
+    // instead of 7 per first probe).
     [[maybe_unused]] double rc = 0.0, c = 0.0, s64 = 0.0;  // RY: this lane's series of the current tile
     auto ry_setup = [&](uint64_t base) {
         rc = u52_to_f64(2 * base + 2 * lane + 1 + 224);
@@ -552,7 +555,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
     // first probes of the lane's edges k in [KB, KE) of the tile
     auto phase1 = [&](auto full_c, auto ry_c, uint64_t base, uint32_t cb, auto kb_c, auto ke_c) {
         constexpr bool FULL = decltype(full_c)::value;
-        constexpr bool RY = decltype(ry_c)::value;
+        constexpr int RY = decltype(ry_c)::value;  // 0: none, 1: series, 2: series + one-stage remainder
         constexpr int KB = decltype(kb_c)::value, KE = decltype(ke_c)::value;
 #pragma unroll
         for (int k = KB; k < KE; ++k) {
@@ -561,9 +564,11 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
             const bool valid = FULL || ((i >= lo) && (i < hi));
             const R r0 = (R)(2 * base) + (R)(2 * j + 1);
             R r1;
-            if constexpr (RY) {
+            if constexpr (RY == 2) {
+                if constexpr (Hash::kHasRy1) r1 = Hash::from_crc_ry1(cb ^ clow_s[j], r0, fma(-(k - 3.5), s64, c), p);
+            } else if constexpr (RY == 1) {
                 static_assert(kEpl == 8, "series centre assumes 8 edges per lane");
-            const double e = 64.0 * k - 224.0;
+                const double e = 64.0 * k - 224.0;
                 r1 = Hash::from_crc_ry(cb ^ clow_s[j], r0, rc + e, fma(-(k - 3.5), s64, c), p);
             } else if constexpr (Hash::kHasCrc) {
                 r1 = Hash::from_crc(cb ^ clow_s[j], r0, p);
@@ -630,7 +635,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
         // phase 1 over all 8 edges per lane, or in two halves with a drain
         // between them (the 256-entry queue of the wide store)
         auto run_phase1 = [&](auto full_c, auto ry_c) {
-            if constexpr (decltype(ry_c)::value) ry_setup(base);
+            if constexpr (decltype(ry_c)::value != 0) ry_setup(base);
             if constexpr (L::kSplit) {
                 phase1(full_c, ry_c, base, cb, std::integral_constant<int, 0>{}, std::integral_constant<int, kEpl / 2>{});
                 __syncwarp();
@@ -642,14 +647,21 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
             }
         };
         if (base >= lo && base + kTile <= hi) {
-            if constexpr (Hash::kHasRy) {
-                if (2 * base >= kRyMin) run_phase1(std::true_type{}, std::true_type{});
-                else run_phase1(std::true_type{}, std::false_type{});
+            using I0 = std::integral_constant<int, 0>;
+            using I1 = std::integral_constant<int, 1>;
+            using I2 = std::integral_constant<int, 2>;
+            if constexpr (Hash::kHasRy1) {
+                if (2 * base >= kOneStageMin) run_phase1(std::true_type{}, I2{});
+                else if (2 * base >= kRyMin) run_phase1(std::true_type{}, I1{});
+                else run_phase1(std::true_type{}, I0{});
+            } else if constexpr (Hash::kHasRy) {
+                if (2 * base >= kRyMin) run_phase1(std::true_type{}, I1{});
+                else run_phase1(std::true_type{}, I0{});
             } else {
-                run_phase1(std::true_type{}, std::false_type{});
+                run_phase1(std::true_type{}, I0{});
             }
         } else {
-            run_phase1(std::false_type{}, std::false_type{});
+            run_phase1(std::false_type{}, std::integral_constant<int, 0>{});
         }
         __syncwarp();
         drain();

@@ -31,6 +31,7 @@ pb = pytest.importorskip("paper_1602_07106_b200")
 L_ = pb._lib
 
 RY_MIN = (1 << 27) + 224  # the series path runs for tiles with 2*base >= 2^27
+ONESTAGE_MIN = (1 << 28) + 224  # 2-chunk tiles with 2*base >= 2^28: one-stage remainder
 
 # (method, rmin, rmax): each routine over the r range of the launches that use it
 CLASSES = [
@@ -43,6 +44,9 @@ CLASSES = [
     (L_.MOD_FP_NARROW_SERIES, RY_MIN, (1 << 32) - 1),
     (L_.MOD_FP_WIDE_SERIES, RY_MIN, (1 << 52) - 1),
     (L_.MOD_FP_WIDE_SERIES, 1 << 44, (1 << 52) - 1),
+    (L_.MOD_FP31_SERIES1, ONESTAGE_MIN, (1 << 31) - 1),
+    (L_.MOD_FP_WIDE_SERIES1, ONESTAGE_MIN, (1 << 52) - 1),
+    (L_.MOD_FP_WIDE_SERIES1, 1 << 44, (1 << 52) - 1),
 ]
 
 
@@ -66,11 +70,12 @@ def test_remainder_random_1e8(method, rmin, rmax):
 
 def _adversarial(rmin: int, rmax: int):
     rs = {1, 2, 3, (1 << 31) - 1, (1 << 32) - 1, 1 << 32, (1 << 32) + 1, 1 << 44, (1 << 52) - 1,
-          (1 << 63) + 1, (1 << 64) - 1, RY_MIN, RY_MIN + 1}
+          (1 << 63) + 1, (1 << 64) - 1, RY_MIN, RY_MIN + 1, ONESTAGE_MIN, ONESTAGE_MIN + 1}
     for k in range(1, 64):
         rs |= {(1 << k) - 1, 1 << k, (1 << k) + 1}
     rng = np.random.default_rng(160207106)
     rs |= {int(x) for x in rng.integers(1, 1 << 62, 64)}
+    rs |= {rmin + int(x) % (rmax - rmin + 1) for x in rng.integers(0, 1 << 62, 16)}  # inside every class
     rs = sorted(r for r in rs if rmin <= r <= rmax)
     hs, rr = [], []
     M = (1 << 64) - 1
@@ -102,6 +107,22 @@ def test_remainder_adversarial(method, rmin, rmax):
     bad = np.nonzero(got != want)[0]
     assert bad.size == 0, [(int(h[k]), int(r[k]), int(got[k]), int(want[k])) for k in bad[:5]]
     assert h.size > 200
+
+
+def test_rcp_approx_bound_exhaustive():
+    """rcp.approx.ftz.f64 reads only the high word of its operand, so its
+    relative error over every operand in [1, 2^64) is the maximum over 2^20
+    mantissa prefixes x 64 exponents x both ends of the low word.  The
+    remainder analysis (parba_device.cuh: mod_fp_y, mod_fp31_y1) assumes
+    < 2^-19.5 raw and < 2^-38 after the Newton step."""
+    import torch
+
+    dev = torch.device("cuda", 0)
+    out = torch.zeros(2, dtype=torch.float64, device=dev)
+    pb._lib.check(pb._lib.load().parba_debug_rcp_bound(1023, 64, out.data_ptr(), pb._lib.stream_ptr(torch, dev)))
+    raw, newton = out.cpu().tolist()
+    assert 0 < raw < 2.0 ** -19.5, raw
+    assert newton < 2.0 ** -38, newton
 
 
 def _op(p):
