@@ -544,6 +544,13 @@ bool fold_enabled() {
     return !(e && e[0] == '0');
 }
 
+// PARBA_OFF16=0: one-slice buckets keep u32 targets in the sorted array
+// instead of u16 offsets (A/B)
+bool off16_enabled() {
+    const char *e = getenv("PARBA_OFF16");
+    return !(e && e[0] == '0');
+}
+
 bool pos_mode_enabled() {
     const char *e = getenv("PARBA_POS_MODE");
     return e && strcmp(e, "1") == 0;
@@ -607,6 +614,12 @@ struct PartScratch {
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, kSliceNodes * 4));
             CUDA_TRY(cudaFuncSetAttribute(bucket_scatter_kernel<kScatterThreads>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, kScatterSmem));
+            CUDA_TRY(cudaFuncSetAttribute(bucket_scatter_kernel<kScatterThreads, true>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kScatterSmem));
+            CUDA_TRY(cudaFuncSetAttribute(slice_count_kernel<uint32_t, true>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kSliceMax * 4));
+            CUDA_TRY(cudaFuncSetAttribute(slice_count_kernel<unsigned long long, true>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kSliceMax * 4));
             attr[dev] = true;
         }
         return PARBA_OK;
@@ -623,11 +636,18 @@ struct PartScratch {
         uint32_t *n_items = (uint32_t *)items.p + max_items;
         CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, (const uint32_t *)H.p, (uint32_t *)O.p,
                                                (int64_t)nb * cols, st));
+        // one-slice buckets narrower than 2^16 nodes: u16 offsets in the sorted array
+        const bool off16 = !dense && spb_lg == 0 && bw <= 0xffffu && off16_enabled();
         for (int wb = 0; wb < nb; wb += kHistBuckets) {  // scatter passes
             const int nbw = nb - wb < kHistBuckets ? nb - wb : kHistBuckets;
-            bucket_scatter_kernel<kScatterThreads><<<cols, kScatterThreads, kScatterSmem, st>>>(
-                (const uint32_t *)t32.p, len, wpc, groups, capw, bdiv, wb, nbw, (const uint32_t *)O.p,
-                (uint32_t *)srt.p, stride_nw, stride_ntiles);
+            if (off16)
+                bucket_scatter_kernel<kScatterThreads, true><<<cols, kScatterThreads, kScatterSmem, st>>>(
+                    (const uint32_t *)t32.p, len, wpc, groups, capw, bdiv, wb, nbw, (const uint32_t *)O.p,
+                    (uint32_t *)srt.p, stride_nw, stride_ntiles, bw);
+            else
+                bucket_scatter_kernel<kScatterThreads><<<cols, kScatterThreads, kScatterSmem, st>>>(
+                    (const uint32_t *)t32.p, len, wpc, groups, capw, bdiv, wb, nbw, (const uint32_t *)O.p,
+                    (uint32_t *)srt.p, stride_nw, stride_ntiles);
             CUDA_TRY(cudaGetLastError());
         }
         count_plan_kernel<<<1, kHistThreads, 0, st>>>((const uint32_t *)O.p, (const uint32_t *)H.p, cols, nb,
@@ -638,6 +658,10 @@ struct PartScratch {
             slice_count_pos_kernel<CountT><<<(unsigned)(items_ub << spb_lg), kHistThreads, kSliceNodes * 4, st>>>(
                 (const uint32_t *)srt.p, (const uint32_t *)O.p, (const uint32_t *)H.p, cols, nb,
                 (const uint32_t *)items.p, n_items, m0, K, shift, spb_lg, dense, counts);
+        else if (off16)
+            slice_count_kernel<CountT, true><<<(unsigned)items_ub, kHistThreads, (size_t)bw * 4, st>>>(
+                (const uint32_t *)srt.p, (const uint32_t *)O.p, (const uint32_t *)H.p, cols, nb,
+                (const uint32_t *)items.p, n_items, (uint32_t)K, bw, 0, counts, fold);
         else
             slice_count_kernel<CountT><<<(unsigned)(items_ub << spb_lg), kHistThreads,
                                          (spb_lg ? (size_t)kSliceNodes : (size_t)bw) * 4, st>>>(

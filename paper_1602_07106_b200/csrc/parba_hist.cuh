@@ -115,13 +115,16 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t x, uint32_t *w
 // Strided input (nw > 0: the store-targets sink's tile-order slots): tile
 // CTA c owns tiles k*nw + c*wpc + [0, wpc) for k = 0, 1, ... below ntiles,
 // i.e. its k-th block of wpc*kTile entries starts at slot (k*nw + c*wpc)*kTile.
-template <int T>
+// OFF16: one-slice buckets of width bw < 2^16 -- each entry is written as
+// its u16 offset in the bucket (target - bucket * bw), half the bytes of the
+// scatter's writes and of the count's reads.
+template <int T, bool OFF16 = false>
 __global__ void __launch_bounds__(T, 1) bucket_scatter_kernel(const uint32_t *__restrict__ t, uint64_t len,
                                                            uint32_t wpc, uint32_t groups, uint64_t capw,
                                                            Magic32 bdiv, int wb, int nbw,
                                                            const uint32_t *__restrict__ O,
                                                            uint32_t *__restrict__ out, uint64_t nw,
-                                                           uint64_t ntiles) {
+                                                           uint64_t ntiles, uint32_t bw = 0) {
     constexpr int BPT = kHistBuckets / T;  // buckets per thread in the scan
     constexpr int PER = kScatterTile / T;  // entries per thread and sub-tile
     static_assert(BPT * T == kHistBuckets && PER % 4 == 0, "scatter shape");
@@ -231,7 +234,12 @@ __global__ void __launch_bounds__(T, 1) bucket_scatter_kernel(const uint32_t *__
             const uint32_t x = sorted[k];
             const uint32_t b = wbucket(x);
             PARBA_CHECK(delta[b] + k < len);
-            out[delta[b] + k] = x;
+            if constexpr (OFF16) {
+                PARBA_CHECK(x - (wb + b) * bw < bw);
+                reinterpret_cast<uint16_t *>(out)[delta[b] + k] = (uint16_t)(x - (wb + b) * bw);
+            } else {
+                out[delta[b] + k] = x;
+            }
         }
         if (more) load(base + 2 * kScatterTile);
     }
@@ -298,7 +306,8 @@ __global__ void __launch_bounds__(kHistThreads) count_plan_kernel(const uint32_t
 // read from HBM about once and from L2 by the others.  (A cluster variant
 // that reads the chunk once and routes each entry to the owning CTA with a
 // distributed-shared-memory red.add measured 3x slower.)
-template <typename CountT>
+// OFF16: the entries are u16 offsets within one-slice buckets (spb_lg = 0).
+template <typename CountT, bool OFF16 = false>
 __global__ void __launch_bounds__(kHistThreads) slice_count_kernel(const uint32_t *__restrict__ sorted,
                                                                    const uint32_t *__restrict__ O,
                                                                    const uint32_t *__restrict__ H, uint32_t nblk,
@@ -335,15 +344,51 @@ __global__ void __launch_bounds__(kHistThreads) slice_count_kernel(const uint32_
         count(w.z);
         count(w.w);
     };
+    constexpr int NL = PARBA_COUNT_LOADS;
+    const uint32_t bd = blockDim.x;
+    if constexpr (OFF16) {
+        // u16 offsets: scalar head to a 16-byte boundary, 8 entries per
+        // 16-byte word, tail
+        PARBA_CHECK(spb_lg == 0);
+        const uint16_t *s16 = reinterpret_cast<const uint16_t *>(sorted);
+        auto c2 = [&](uint32_t w) {
+            atomicAdd(&c[w & 0xffffu], 1u);
+            atomicAdd(&c[w >> 16], 1u);
+        };
+        const uint32_t h0 = ((k0 + 7u) & ~7u) < k1 ? ((k0 + 7u) & ~7u) : k1;
+        if (k0 + threadIdx.x < h0) atomicAdd(&c[__ldg(s16 + k0 + threadIdx.x)], 1u);
+        const uint32_t nv8 = (k1 - h0) / 8;
+        const uint4 *w4 = reinterpret_cast<const uint4 *>(s16 + h0);
+        uint32_t j = threadIdx.x;
+        for (; j + (NL - 1) * bd < nv8; j += NL * bd) {
+            uint4 w[NL];
+#pragma unroll
+            for (int u = 0; u < NL; ++u) w[u] = __ldg(w4 + j + u * bd);
+#pragma unroll
+            for (int u = 0; u < NL; ++u) {
+                c2(w[u].x);
+                c2(w[u].y);
+                c2(w[u].z);
+                c2(w[u].w);
+            }
+        }
+        for (; j < nv8; j += bd) {
+            const uint4 w = __ldg(w4 + j);
+            c2(w.x);
+            c2(w.y);
+            c2(w.z);
+            c2(w.w);
+        }
+        const uint32_t t8 = h0 + 8 * nv8;
+        if (t8 + threadIdx.x < k1) atomicAdd(&c[__ldg(s16 + t8 + threadIdx.x)], 1u);
+    } else {
     // scalar head to a 16-byte boundary, then 16-byte words with four loads in
     // flight per thread (the reads are latency-bound), tail
     const uint32_t a0 = ((k0 + 3u) & ~3u) < k1 ? ((k0 + 3u) & ~3u) : k1;
     if (k0 + threadIdx.x < a0) count(__ldg(sorted + k0 + threadIdx.x));
     const uint32_t nv = (k1 - a0) / 4;
     const uint4 *s4 = reinterpret_cast<const uint4 *>(sorted + a0);
-    const uint32_t bd = blockDim.x;
     uint32_t j = threadIdx.x;
-    constexpr int NL = PARBA_COUNT_LOADS;
     for (; j + (NL - 1) * bd < nv; j += NL * bd) {
         uint4 w[NL];
 #pragma unroll
@@ -354,6 +399,7 @@ __global__ void __launch_bounds__(kHistThreads) slice_count_kernel(const uint32_
     for (; j < nv; j += bd) count4(__ldg(s4 + j));
     const uint32_t t0 = a0 + 4 * nv;
     if (t0 + threadIdx.x < k1) count(__ldg(sorted + t0 + threadIdx.x));
+    }
     __syncthreads();
     const uint64_t v0 = (uint64_t)base_b + ((uint64_t)s << kSliceLg);
     const uint32_t sw = spb_lg ? (uint32_t)kSliceNodes : bw;
