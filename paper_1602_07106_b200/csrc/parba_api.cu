@@ -579,7 +579,8 @@ struct PartScratch {
     uint32_t bw = 0;   // bucket width (nodes)
     Magic32 bdiv{};    // bucket = target / bw
     // one_slice: buckets of any width <= kSliceMax, each counted by one CTA
-    // (the store-targets path; every other path uses power-of-two widths)
+    // (the tile-kernel targets passes; rows input and positions use
+    // power-of-two widths)
     int init(uint64_t K, uint64_t slots, uint32_t cols, cudaStream_t st, bool one_slice = false) {
         shift = hist_shift(K);
         nb = (int)((K + (1ull << shift) - 1) >> shift);
@@ -693,7 +694,9 @@ int count_partitioned(const parba_params_t *p, const DevParams &dp, uint64_t lo,
     const uint32_t nblk = (uint32_t)di->sms * 4 * kHistGroups;  // >= warp groups of one tile launch
     PartScratch ps;
     const bool stt = K >= p->n && !by_pos && targets_only_ok(p) && stt_enabled();
-    if ((rc = ps.init(K, cap, nblk, st, stt && one_slice_enabled()))) return rc;
+    // one-slice buckets (width K/2048, counted by one CTA each) for every
+    // tile-kernel targets pass but the position pass (power-of-two slices)
+    if ((rc = ps.init(K, cap, nblk, st, !by_pos && one_slice_enabled()))) return rc;
     for (uint64_t b0 = lo; b0 < hi;) {
         uint64_t b1 = hi - b0 > batch ? (b0 / kTile) * kTile + batch : hi;
         if (b1 > hi) b1 = hi;

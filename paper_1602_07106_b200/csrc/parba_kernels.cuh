@@ -142,7 +142,7 @@ struct SinkArgs {
     uint64_t capw;
     uint32_t *hist;                        // targets: H[b * G * gridDim.x + G * blk + group]
     int shift, nb;                         //   (bucket = target >> shift, G = kHistGroups)
-    Magic32 bdiv;                          // store-targets histogram: bucket = target / bucket width
+    Magic32 bdiv;                          // targets / store-targets histogram: bucket = target / bucket width
     uint64_t klim;                         // targets: only targets < klim are kept
     int by_pos;                            // targets, degree sequence: emit positions (full counts)
     uint64_t t32_cap;                      // host side: slots of t32
@@ -457,7 +457,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
                 if (f) {
                     const uint32_t tg = (uint32_t)target_of<NARROW, SEED, false, DEG>(rv, p);
                     wout[wcur + __popc(m & ltmask)] = tg;
-                    atomicAdd(hist_w + (tg >> a.shift), 1u);
+                    atomicAdd(hist_w + (uint32_t)(((uint64_t)tg * a.bdiv.mul) >> a.bdiv.shift), 1u);
                 }
                 wcur += __popc(m);
             } else {
@@ -467,7 +467,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
                 const unsigned m = ballot_all(keep);
                 if (keep) {
                     wout[wcur + __popc(m & ltmask)] = (uint32_t)tg;
-                    atomicAdd(hist_w + ((uint32_t)tg >> a.shift), 1u);
+                    atomicAdd(hist_w + (uint32_t)(((uint64_t)(uint32_t)tg * a.bdiv.mul) >> a.bdiv.shift), 1u);
                 }
                 wcur += __popc(m);
             }

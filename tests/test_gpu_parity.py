@@ -388,10 +388,13 @@ def test_full_partitioned_equals_direct(case, monkeypatch):
     assert pp == pd
     assert np.array_equal(part, direct)
     assert int(part.astype(np.int64).sum()) == 2 * (hi - lo)
-    if case[0] in ("four_slices", "c4_whole_one_slice"):  # the per-step targets sink and 2^k buckets too
-        monkeypatch.setenv("PARBA_STT", "0")
-        legacy, pl = _full_counts(p, lo, hi, "partition", monkeypatch)
-        assert pl == pd and np.array_equal(legacy, direct)
+    if case[0] in ("four_slices", "c4_whole_one_slice"):
+        # the per-step targets sink (one-slice buckets, u16 offsets), then
+        # with 2^k buckets, then with u32 entries in the sorted array
+        for env in (("PARBA_STT", "0"), ("PARBA_ONE_SLICE", "0"), ("PARBA_OFF16", "0")):
+            monkeypatch.setenv(*env)
+            legacy, pl = _full_counts(p, lo, hi, "partition", monkeypatch)
+            assert pl == pd and np.array_equal(legacy, direct), env
 
 
 def test_full_partitioned_vs_oracle_small(monkeypatch):
