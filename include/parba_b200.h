@@ -212,7 +212,11 @@ int parba_degree_window_host(const parba_params_t *p_host_seed, uint64_t lo, uin
  *   PARBA_MULTI_DISCARD out_host unused (probes and time only)
  * The distinct devices' histograms are summed by one ncclReduce (SUM, root
  * devs[0]; NCCL loaded at run time) -- the DegreeCountConsumer.merge of
- * analytics.py:78-82.  probes_host and device_seconds (max over devices of
+ * analytics.py:78-82.  PARBA_MULTI_FULL on several devices with peer access
+ * takes the owner-routed count instead (parba_degree_full_routed: device g
+ * owns nodes [g * slice, (g + 1) * slice), the count kernels add into the
+ * owners over NVLink, every device copies its own slice to the host), when
+ * it applies to every shard; PARBA_MULTI_ROUTED=0 keeps the ncclReduce.  probes_host and device_seconds (max over devices of
  * generation + reduction) are optional.  Uniform degree only (host entry
  * point); option flags cut at node boundaries. */
 #define PARBA_MULTI_STORE 0
@@ -229,6 +233,36 @@ int parba_multi_run(const parba_params_t *p_host_seed, int ndev, const int *devs
 int parba_multi_run_shards(const parba_params_t *p_host_seed, int nshards, const int *devs,
                            const uint64_t *los, const uint64_t *his, int mode, uint64_t K, void *out_host,
                            uint64_t *probes_per_shard, double *device_seconds);
+
+/* ---- Owner-routed full histogram: the histogram reduce fused into the count
+ * (the N-GPU form of analytics.py:78-99: every worker counts its edge range,
+ * DegreeCountConsumer.merge sums the arrays).  Node v's uint32 counter lives
+ * on owner g = v / slice_nodes at slices[g][v - g * slice_nodes]; slices[g]
+ * is a device pointer valid on the CURRENT device -- local memory, a peer
+ * mapping (cudaDeviceEnablePeerAccess) or an IPC mapping (parba_ipc_open) of
+ * owner g's memory over NVLink.  The count kernels add each bucket's
+ * counters (closed-form sources included) straight into the owners' slices
+ * with red.add as the bucket is counted, so the reduce-scatter of the
+ * histograms overlaps the counting and no n-word array per GPU is summed
+ * afterwards.  All workers call this with the same slice table; the owners
+ * zero their slices before any worker starts and read them after every
+ * worker's stream has drained (the caller's barriers).  slice_nodes: a
+ * multiple of 65536 with nowners * slice_nodes >= n; nowners <= 16.
+ * parba_degree_full_routed_ok = 1 when the path applies to [lo, hi) (plain
+ * uniform-degree family, n >= 2^25, a shard of >= 2^22 edges): otherwise use
+ * parba_degree_full and a reduce. */
+int parba_degree_full_routed_ok(const parba_params_t *p, uint64_t lo, uint64_t hi);
+int parba_degree_full_routed(const parba_params_t *p, uint64_t lo, uint64_t hi, int nowners,
+                             uint32_t *const *slices, uint64_t slice_nodes, unsigned long long *probes,
+                             void *stream);
+/* Slices another process can map (one process per GPU, torch.distributed):
+ * parba_ipc_alloc = cudaMalloc on the current device + cudaIpcGetMemHandle
+ * (handle64: 64 bytes to send to the peers); parba_ipc_open maps a peer's
+ * handle on the current device; parba_ipc_close / parba_ipc_free undo them. */
+int parba_ipc_alloc(uint64_t bytes, void **dev_ptr, void *handle64);
+int parba_ipc_open(const void *handle64, void **dev_ptr);
+int parba_ipc_close(void *dev_ptr);
+int parba_ipc_free(void *dev_ptr);
 
 /* ---- Sequential-oracle counterpart (bb_generate, oracle.py:45-107) ------
  * The whole edge array E[0 .. 2m) (device, u64) built as an array: seed

@@ -33,7 +33,8 @@ EXPORTS = (
     "parba_degseq_prefix", "parba_degseq_rank", "parba_rank1", "parba_node_of_edges", "parba_count_pairs",
     "parba_multi_run", "parba_multi_run_shards", "parba_crc32c", "parba_mulhi_u64", "parba_degseq_dense",
     "parba_peak_int32", "parba_peak_write", "parba_debug_mod", "parba_debug_mod_check", "parba_debug_rcp_bound",
-    "parba_bb_fill",
+    "parba_bb_fill", "parba_degree_full_routed_ok", "parba_degree_full_routed", "parba_ipc_alloc", "parba_ipc_open",
+    "parba_ipc_close", "parba_ipc_free",
 )
 MOD_FP31, MOD_FP_NARROW, MOD_FP_WIDE, MOD_INT, MOD_FP31_SERIES, MOD_FP_NARROW_SERIES, MOD_FP_WIDE_SERIES, \
     MOD_FP31_SERIES1, MOD_FP_WIDE_SERIES1 = range(9)
@@ -118,6 +119,12 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
             "parba_peak_int32": ([vp, ctypes.POINTER(ctypes.c_double), vp], i32),
             "parba_peak_write": ([vp, u64, vp], i32),
             "parba_multi_run_shards": ([P, i32, vp, vp, vp, i32, u64, vp, vp, ctypes.POINTER(ctypes.c_double)], i32),
+            "parba_degree_full_routed_ok": ([P, u64, u64], i32),
+            "parba_degree_full_routed": ([P, u64, u64, i32, vp, u64, vp, vp], i32),
+            "parba_ipc_alloc": ([u64, ctypes.POINTER(vp), vp], i32),
+            "parba_ipc_open": ([vp, ctypes.POINTER(vp)], i32),
+            "parba_ipc_close": ([vp], i32),
+            "parba_ipc_free": ([vp], i32),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name, None)

@@ -350,7 +350,7 @@ bool use_partitioned(const parba_params_t *p, uint64_t lo, uint64_t hi, uint64_t
 template <typename CountT>
 int count_partitioned(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi, uint64_t K,
                       CountT *counts, unsigned long long *probes, cudaStream_t st, bool by_pos = false,
-                      bool *sources_done = nullptr);
+                      bool *sources_done = nullptr, const Route *route = nullptr);
 }  // namespace
 
 extern "C" {
@@ -621,6 +621,10 @@ struct PartScratch {
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, kSliceMax * 4));
             CUDA_TRY(cudaFuncSetAttribute(slice_count_kernel<unsigned long long, true>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, kSliceMax * 4));
+            CUDA_TRY(cudaFuncSetAttribute(slice_count_kernel<uint32_t, false, true>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kSliceMax * 4));
+            CUDA_TRY(cudaFuncSetAttribute(slice_count_kernel<uint32_t, true, true>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kSliceMax * 4));
             attr[dev] = true;
         }
         return PARBA_OK;
@@ -633,7 +637,7 @@ struct PartScratch {
     template <typename CountT>
     int count(uint64_t len, uint64_t capw, uint32_t wpc, uint32_t groups, uint32_t cols, uint64_t K,
               CountT *counts, cudaStream_t st, const uint32_t *dense = nullptr, uint64_t m0 = 0,
-              SrcFold fold = SrcFold{}) {
+              SrcFold fold = SrcFold{}, const Route *route = nullptr) {
         uint32_t *n_items = (uint32_t *)items.p + max_items;
         CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, (const uint32_t *)H.p, (uint32_t *)O.p,
                                                (int64_t)nb * cols, st));
@@ -655,6 +659,22 @@ struct PartScratch {
                                                        (uint32_t *)items.p, n_items, fold.on);
         CUDA_TRY(cudaGetLastError());
         const uint64_t items_ub = nb + len / kCountChunk + 1;  // >= sum of ceil(size_b / chunk)
+        if constexpr (sizeof(CountT) == 4) {
+            if (route && route->n > 0) {  // counters added straight into their owners' slices
+                if (dense) return fail(PARBA_EINVAL, "routed counts do not take the position pass");
+                if (off16)
+                    slice_count_kernel<CountT, true, true><<<(unsigned)items_ub, kHistThreads, (size_t)bw * 4, st>>>(
+                        (const uint32_t *)srt.p, (const uint32_t *)O.p, (const uint32_t *)H.p, cols, nb,
+                        (const uint32_t *)items.p, n_items, (uint32_t)K, bw, 0, nullptr, fold, *route);
+                else
+                    slice_count_kernel<CountT, false, true><<<(unsigned)(items_ub << spb_lg), kHistThreads,
+                                                              (spb_lg ? (size_t)kSliceNodes : (size_t)bw) * 4, st>>>(
+                        (const uint32_t *)srt.p, (const uint32_t *)O.p, (const uint32_t *)H.p, cols, nb,
+                        (const uint32_t *)items.p, n_items, (uint32_t)K, bw, spb_lg, nullptr, fold, *route);
+                CUDA_TRY(cudaGetLastError());
+                return PARBA_OK;
+            }
+        }
         if (dense)
             slice_count_pos_kernel<CountT><<<(unsigned)(items_ub << spb_lg), kHistThreads, kSliceNodes * 4, st>>>(
                 (const uint32_t *)srt.p, (const uint32_t *)O.p, (const uint32_t *)H.p, cols, nb,
@@ -679,7 +699,7 @@ struct PartScratch {
 template <typename CountT>
 int count_partitioned(const parba_params_t *p, const DevParams &dp, uint64_t lo, uint64_t hi, uint64_t K,
                       CountT *counts, unsigned long long *probes, cudaStream_t st, bool by_pos,
-                      bool *sources_done) {
+                      bool *sources_done, const Route *route) {
     if (by_pos) K = p->m;
     // uniform degree: the closed-form sources ride along with the last
     // batch's slice count (no separate pass over the counts)
@@ -732,7 +752,7 @@ int count_partitioned(const parba_params_t *p, const DevParams &dp, uint64_t lo,
         SrcFold fold{};
         if (fold_src && b1 == hi) fold = SrcFold{lo, hi, p->m0, p->n0, p->d, 1};
         if ((rc = ps.count<CountT>(geom[0], geom[1], (uint32_t)geom[2], kHistGroups, used, K, counts, st,
-                                   by_pos ? dp.dense : nullptr, p->m0, fold)))
+                                   by_pos ? dp.dense : nullptr, p->m0, fold, route)))
             return rc;
         if (fold.on) *sources_done = true;
         b0 = b1;
@@ -804,6 +824,48 @@ int parba_degree_full(const parba_params_t *p, uint64_t lo, uint64_t hi, uint32_
     }
     if (rc || src_done) return rc;
     return launch_sources<uint32_t>(dp, lo, hi, p->n, counts, st);
+}
+
+// Routed counts apply where the partitioned pass with folded sources does:
+// plain uniform-degree CRC/SIMPLE families (no option flags) with n >= 2^25
+// nodes and a shard of at least kHistMinEdges edges.
+static bool routed_ok(const parba_params_t *p, uint64_t lo, uint64_t hi) {
+    return !is_deg(p) && !p->flags && p->d >= 1 && fold_enabled() && use_partitioned(p, lo, hi, p->n);
+}
+
+int parba_degree_full_routed_ok(const parba_params_t *p, uint64_t lo, uint64_t hi) {
+    if (validate(p) || check_range(p, lo, hi)) return 0;
+    return routed_ok(p, lo, hi) ? 1 : 0;
+}
+
+int parba_degree_full_routed(const parba_params_t *p, uint64_t lo, uint64_t hi, int nowners,
+                             uint32_t *const *slices, uint64_t slice_nodes, unsigned long long *probes,
+                             void *stream) {
+    int rc = validate(p);
+    if (!rc) rc = check_range(p, lo, hi);
+    if (rc) return rc;
+    if (nowners < 1 || nowners > kMaxOwners || !slices)
+        return fail(PARBA_EINVAL, "routed counts take 1..%d owner slices", kMaxOwners);
+    if (slice_nodes == 0 || (slice_nodes & 0xffffu) || slice_nodes >= (1ull << 32) ||
+        (unsigned __int128)slice_nodes * (unsigned)nowners < p->n)
+        return fail(PARBA_EINVAL, "slice_nodes must be a multiple of 65536 with nowners * slice_nodes >= n");
+    for (int g = 0; g < nowners; ++g)
+        if (!slices[g] && (uint64_t)g * slice_nodes < p->n) return fail(PARBA_EINVAL, "slice %d is NULL", g);
+    if (hi == lo) return PARBA_OK;
+    if (!routed_ok(p, lo, hi))
+        return fail(PARBA_EINVAL,
+                    "routed counts need the partitioned full histogram (uniform degree, no option flags, "
+                    "n >= 2^25, a shard of >= 2^22 edges); use parba_degree_full and a reduce");
+    Route route{};
+    for (int g = 0; g < nowners; ++g) route.ptr[g] = slices[g];
+    route.slice = (uint32_t)slice_nodes;
+    route.n = nowners;
+    const DevParams dp = make_dev(p, p->n);
+    bool src_done = false;
+    rc = count_partitioned<uint32_t>(p, dp, lo, hi, p->n, nullptr, probes, (cudaStream_t)stream, false, &src_done,
+                                     &route);
+    if (!rc && !src_done) return fail(PARBA_ECUDA, "routed counts: sources were not folded");
+    return rc;
 }
 
 int parba_count_ids(const uint64_t *ids, uint64_t count, uint64_t K, unsigned long long *counts, void *stream) {

@@ -272,6 +272,22 @@ __device__ __forceinline__ uint64_t src_overlap(const SrcFold &f, uint64_t v) {
     return y > x ? y - x : 0u;
 }
 
+// Owner-routed counts (multi-GPU full histogram): instead of a local n-word
+// array summed by a collective afterwards, node v's counter lives on owner
+// g = v / slice at ptr[g][v - g * slice] -- the owner's own memory or a peer
+// mapping of it (NVLink) -- and every count CTA adds its bucket's counters
+// there with red.add as soon as the bucket is counted: the reduce-scatter of
+// the histograms (analytics.py:78-82, Consumer.merge) fused into the count
+// kernel, its traffic overlapped with the counting of the other buckets.
+// slice is a multiple of 2^16 >= kSliceMax, so one CTA's nodes have at most
+// two owners.
+constexpr int kMaxOwners = 16;
+struct Route {
+    uint32_t *ptr[kMaxOwners];
+    uint32_t slice;  // nodes per owner
+    int n;           // owners (0: local counts)
+};
+
 __global__ void __launch_bounds__(kHistThreads) count_plan_kernel(const uint32_t *__restrict__ O,
                                                                   const uint32_t *__restrict__ H, uint32_t nblk,
                                                                   int nb, uint32_t *__restrict__ items,
@@ -307,14 +323,17 @@ __global__ void __launch_bounds__(kHistThreads) count_plan_kernel(const uint32_t
 // that reads the chunk once and routes each entry to the owning CTA with a
 // distributed-shared-memory red.add measured 3x slower.)
 // OFF16: the entries are u16 offsets within one-slice buckets (spb_lg = 0).
-template <typename CountT, bool OFF16 = false>
+// ROUTED: counts is unused, every non-zero counter (folded sources included)
+// goes to its owner through `route` with one red.add.
+template <typename CountT, bool OFF16 = false, bool ROUTED = false>
 __global__ void __launch_bounds__(kHistThreads) slice_count_kernel(const uint32_t *__restrict__ sorted,
                                                                    const uint32_t *__restrict__ O,
                                                                    const uint32_t *__restrict__ H, uint32_t nblk,
                                                                    int nb, const uint32_t *__restrict__ items,
                                                                    const uint32_t *__restrict__ n_items, uint32_t n,
                                                                    uint32_t bw, int spb_lg,
-                                                                   CountT *__restrict__ counts, SrcFold fold) {
+                                                                   CountT *__restrict__ counts, SrcFold fold,
+                                                                   Route route = Route{}) {
     extern __shared__ uint32_t c[];
     const uint32_t it = blockIdx.x >> spb_lg;
     if (it >= *n_items) return;
@@ -403,6 +422,24 @@ __global__ void __launch_bounds__(kHistThreads) slice_count_kernel(const uint32_
     __syncthreads();
     const uint64_t v0 = (uint64_t)base_b + ((uint64_t)s << kSliceLg);
     const uint32_t sw = spb_lg ? (uint32_t)kSliceNodes : bw;
+    if constexpr (ROUTED) {
+        static_assert(sizeof(CountT) == 4, "routed counts are u32");
+        // nodes [v0, v0 + lim) of this CTA: owner g0 below bnd, g0 + 1 from there
+        const uint32_t lim = v0 >= n ? 0u : (uint64_t)sw < n - v0 ? sw : (uint32_t)(n - v0);
+        const bool addsrc = fold.on && (!split || chunk == 0);
+        const uint32_t g0 = (uint32_t)(v0 / route.slice);
+        const uint64_t bnd = (uint64_t)(g0 + 1) * route.slice;
+        PARBA_CHECK(lim == 0 || (int)g0 < route.n);
+        uint32_t *const p0 = route.ptr[g0];
+        uint32_t *const p1 = (int)g0 + 1 < route.n ? route.ptr[g0 + 1] : nullptr;
+        const uint32_t o0 = (uint32_t)(v0 - (uint64_t)g0 * route.slice);
+        for (uint32_t k = threadIdx.x; k < lim; k += blockDim.x) {
+            const uint64_t v = v0 + k;
+            const uint32_t x = c[k] + (addsrc ? (uint32_t)src_overlap(fold, v) : 0u);
+            if (x) atomicAdd(v < bnd ? p0 + o0 + k : p1 + (v - bnd), x);  // RED.ADD (local or peer)
+        }
+        return;
+    }
     if (split) {  // the bucket's first chunk also adds the folded sources
         const bool addsrc = fold.on && chunk == 0;
         for (uint32_t k = threadIdx.x; k < sw; k += blockDim.x) {

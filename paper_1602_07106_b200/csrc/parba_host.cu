@@ -653,6 +653,10 @@ struct DeviceRun {
     cudaEvent_t t0 = nullptr, t1 = nullptr;
     float ms = 0.f;  // store mode: summed generate_host_impl device time
     DevBuf seed;     // seed graph on this device (alive until the run ends)
+    // owner-routed full histogram: the slices this device owns (index into the
+    // run's owner list) and the event recorded after they were zeroed
+    std::vector<int> owned;
+    cudaEvent_t zeroed = nullptr;
     DeviceRun() = default;
     DeviceRun(const DeviceRun &) = delete;
     DeviceRun &operator=(const DeviceRun &) = delete;
@@ -662,9 +666,45 @@ struct DeviceRun {
         if (prb) cudaFree(prb);
         if (t0) cudaEventDestroy(t0);
         if (t1) cudaEventDestroy(t1);
+        if (zeroed) cudaEventDestroy(zeroed);
         if (st) cudaStreamDestroy(st);
     }
 };
+
+// Owner-routed full histogram of one multi-device run: owner k holds nodes
+// [k * slice, (k + 1) * slice) on device dev[k] (parba_degree_full_routed).
+struct RoutedRun {
+    std::vector<uint32_t *> ptr;  // one allocation per owner
+    std::vector<int> dev;
+    uint64_t slice = 0;
+    ~RoutedRun() {
+        for (size_t k = 0; k < ptr.size(); ++k)
+            if (ptr[k]) {
+                cudaSetDevice(dev[k]);
+                cudaFree(ptr[k]);
+            }
+    }
+};
+
+// Every device of the run can map every other one's memory (enabled here).
+bool peers_ok(const std::vector<int> &udev) {
+    for (int a : udev)
+        for (int b : udev) {
+            if (a == b) continue;
+            int can = 0;
+            if (cudaDeviceCanAccessPeer(&can, a, b) != cudaSuccess || !can) return false;
+        }
+    for (int a : udev) {
+        if (cudaSetDevice(a) != cudaSuccess) return false;
+        for (int b : udev) {
+            if (a == b) continue;
+            const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+            else if (e != cudaSuccess) return false;
+        }
+    }
+    return true;
+}
 
 size_t count_bytes(const parba_params_t *ph, int mode, uint64_t K) {
     return mode == PARBA_MULTI_FULL ? (size_t)ph->n * 4 : (size_t)(K ? K : 1) * 8;
@@ -672,7 +712,8 @@ size_t count_bytes(const parba_params_t *ph, int mode, uint64_t K) {
 
 // Run every shard of `r` on its device; counts stay on the device.
 int run_device(const parba_params_t *ph, int mode, uint64_t K, const uint64_t *los, const uint64_t *his,
-               void *out_host, uint64_t *shard_probes, DeviceRun &r) {
+               void *out_host, uint64_t *shard_probes, DeviceRun &r, const RoutedRun *routed = nullptr,
+               const std::vector<DeviceRun> *all = nullptr) {
     if (mode == PARBA_MULTI_STORE) {
         for (int s : r.shards) {
             float ms = 0.f;
@@ -696,6 +737,20 @@ int run_device(const parba_params_t *ph, int mode, uint64_t K, const uint64_t *l
     CUDA_TRY(cudaMalloc((void **)&r.prb, ns * 8));
     CUDA_TRY(cudaMemsetAsync(r.prb, 0, ns * 8, r.st));
     const bool counted = mode != PARBA_MULTI_DISCARD && (mode == PARBA_MULTI_FULL || K > 0);
+    if (routed) {
+        // the slices this device owns were zeroed on its stream (event
+        // `zeroed`, recorded before the worker threads started): wait for
+        // every owner's, then count straight into the owners' slices
+        for (const DeviceRun &o : *all) CUDA_TRY(cudaStreamWaitEvent(r.st, o.zeroed, 0));
+        CUDA_TRY(cudaEventRecord(r.t0, r.st));
+        for (size_t j = 0; j < ns; ++j) {
+            const int s = r.shards[j];
+            rc = parba_degree_full_routed(&pd, los[s], his[s], (int)routed->ptr.size(), routed->ptr.data(),
+                                          routed->slice, r.prb + j, r.st);
+            if (rc) return rc;
+        }
+        return PARBA_OK;
+    }
     if (counted) {
         const size_t bytes = count_bytes(ph, mode, K);
         if (cudaMalloc(&r.counts, bytes) != cudaSuccess)
@@ -754,11 +809,51 @@ int parba_multi_run_shards(const parba_params_t *ph, int nshards, const int *dev
         runs[g].shards.push_back(s);
     }
     std::vector<uint64_t> probes(nshards, 0);
+    // Full histogram on several devices with peer access: owner-routed counts
+    // (the reduce fused into the count kernels) when the path applies to
+    // every non-empty shard.  PARBA_MULTI_ROUTED: 0 = keep the ncclReduce, 1 =
+    // routed even on one device; PARBA_MULTI_OWNERS = k: at least k owner
+    // slices, dealt round-robin over the devices (tests of the routing).
+    RoutedRun routed;
+    bool use_routed = false;
+    if (mode == PARBA_MULTI_FULL) {
+        const char *e = getenv("PARBA_MULTI_ROUTED");
+        const bool off = e && e[0] == '0', force = e && e[0] == '1';
+        use_routed = !off && (runs.size() > 1 || force) && ph->n < (1ull << 32);
+        for (int s = 0; use_routed && s < nshards; ++s)
+            if (his[s] > los[s] && !parba_degree_full_routed_ok(ph, los[s], his[s])) use_routed = false;
+        if (use_routed && runs.size() > 1 && !peers_ok(udev)) use_routed = false;
+    }
+    if (use_routed) {
+        size_t owners = runs.size();
+        if (const char *e = getenv("PARBA_MULTI_OWNERS")) owners = std::max(owners, (size_t)atoi(e));
+        if (owners > 16) owners = 16;
+        routed.slice = ((ph->n + owners - 1) / owners + 0xffffull) & ~0xffffull;
+        routed.ptr.assign(owners, nullptr);
+        routed.dev.assign(owners, 0);
+        for (size_t k = 0; k < owners; ++k) {
+            DeviceRun &r = runs[k % runs.size()];
+            routed.dev[k] = r.dev;
+            r.owned.push_back((int)k);
+        }
+        for (auto &r : runs) {
+            CUDA_TRY(cudaSetDevice(r.dev));
+            for (int k : r.owned) {
+                if (cudaMalloc((void **)&routed.ptr[k], routed.slice * 4) != cudaSuccess)
+                    return fail(PARBA_ENOMEM, "owner slice of %llu bytes on device %d",
+                                (unsigned long long)routed.slice * 4, r.dev);
+                CUDA_TRY(cudaMemsetAsync(routed.ptr[k], 0, routed.slice * 4, 0));
+            }
+            CUDA_TRY(cudaEventCreateWithFlags(&r.zeroed, cudaEventDisableTiming));
+            CUDA_TRY(cudaEventRecord(r.zeroed, 0));
+        }
+    }
     {
         std::vector<std::thread> th;
         for (auto &r : runs)
             th.emplace_back([&, rp = &r] {
-                rp->rc = run_device(ph, mode, K, los, his, out_host, probes.data(), *rp);
+                rp->rc = run_device(ph, mode, K, los, his, out_host, probes.data(), *rp,
+                                    use_routed ? &routed : nullptr, &runs);
                 if (rp->rc) rp->err = g_err;
             });
         for (auto &t : th) t.join();
@@ -768,6 +863,47 @@ int parba_multi_run_shards(const parba_params_t *ph, int nshards, const int *dev
     double secs = 0.0;
     if (mode == PARBA_MULTI_STORE) {
         for (auto &r : runs) secs = std::max(secs, (double)r.ms / 1000.0);
+    } else if (use_routed) {
+        for (auto &r : runs) {
+            CUDA_TRY(cudaSetDevice(r.dev));
+            CUDA_TRY(cudaEventRecord(r.t1, r.st));
+        }
+        for (auto &r : runs) {  // every stream drained: the owners' slices are complete
+            CUDA_TRY(cudaSetDevice(r.dev));
+            CUDA_TRY(cudaStreamSynchronize(r.st));
+            float ms = 0.f;
+            CUDA_TRY(cudaEventElapsedTime(&ms, r.t0, r.t1));
+            secs = std::max(secs, (double)ms / 1000.0);
+            std::vector<unsigned long long> pr(r.shards.size());
+            CUDA_TRY(cudaMemcpy(pr.data(), r.prb, pr.size() * 8, cudaMemcpyDeviceToHost));
+            for (size_t j = 0; j < pr.size(); ++j) probes[r.shards[j]] = pr[j];
+        }
+        // every device copies its own slices to the host (one thread per
+        // device: the copies run on all PCIe links at once)
+        std::vector<std::thread> th;
+        std::vector<int> rcs(runs.size(), PARBA_OK);
+        for (size_t g = 0; g < runs.size(); ++g)
+            th.emplace_back([&, g] {
+                DeviceRun &r = runs[g];
+                if (cudaSetDevice(r.dev) != cudaSuccess) {
+                    rcs[g] = PARBA_ECUDA;
+                    return;
+                }
+                for (int k : r.owned) {
+                    const uint64_t v0 = (uint64_t)k * routed.slice;
+                    if (v0 >= ph->n) continue;
+                    const uint64_t cnt = std::min<uint64_t>(routed.slice, ph->n - v0);
+                    std::vector<uint32_t> tmp(cnt);
+                    if (cudaMemcpy(tmp.data(), routed.ptr[k], cnt * 4, cudaMemcpyDeviceToHost) != cudaSuccess) {
+                        rcs[g] = PARBA_ECUDA;
+                        return;
+                    }
+                    add_into((int64_t *)out_host + v0, tmp, cnt);
+                }
+            });
+        for (auto &t : th) t.join();
+        for (int c : rcs)
+            if (c) return fail(c, "copy of an owner slice to the host failed");
     } else {
         const bool counted = runs[0].counts != nullptr;
         const char *force = getenv("PARBA_MULTI_NCCL");  // tests: NCCL even for one device
@@ -821,6 +957,46 @@ int parba_multi_run_shards(const parba_params_t *ph, int nshards, const int *dev
     if (probes_per_shard)
         for (int s = 0; s < nshards; ++s) probes_per_shard[s] = probes[s];
     if (device_seconds) *device_seconds = secs;
+    return PARBA_OK;
+}
+
+// Owner slices shared between processes (one process per GPU): plain
+// cudaMalloc memory (the IPC handle of a pooled or sub-allocated block would
+// name the whole block) and its 64-byte handle.
+int parba_ipc_alloc(uint64_t bytes, void **dev_ptr, void *handle64) {
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    if (!dev_ptr || !handle64 || bytes == 0) return fail(PARBA_EINVAL, "ipc_alloc needs a size and two outputs");
+    void *ptr = nullptr;
+    if (cudaMalloc(&ptr, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(PARBA_ENOMEM, "owner slice of %llu bytes", (unsigned long long)bytes);
+    }
+    cudaIpcMemHandle_t h;
+    const cudaError_t e = cudaIpcGetMemHandle(&h, ptr);
+    if (e != cudaSuccess) {
+        cudaFree(ptr);
+        return fail(PARBA_ECUDA, "cudaIpcGetMemHandle failed: %s", cudaGetErrorString(e));
+    }
+    memcpy(handle64, &h, 64);
+    *dev_ptr = ptr;
+    return PARBA_OK;
+}
+
+int parba_ipc_open(const void *handle64, void **dev_ptr) {
+    if (!handle64 || !dev_ptr) return fail(PARBA_EINVAL, "ipc_open needs a handle and an output");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle64, 64);
+    CUDA_TRY(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return PARBA_OK;
+}
+
+int parba_ipc_close(void *dev_ptr) {
+    if (dev_ptr) CUDA_TRY(cudaIpcCloseMemHandle(dev_ptr));
+    return PARBA_OK;
+}
+
+int parba_ipc_free(void *dev_ptr) {
+    if (dev_ptr) CUDA_TRY(cudaFree(dev_ptr));
     return PARBA_OK;
 }
 

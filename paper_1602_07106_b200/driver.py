@@ -29,6 +29,7 @@ reference (driver.py:1-9).
 from __future__ import annotations
 
 import enum
+import os
 import threading
 import time
 import traceback
@@ -260,15 +261,30 @@ def _run_fused_ranks(p: GenParams, consumer, batches, rank: int, ws: int, resolu
     if isinstance(consumer, (analytics.DegreeCountConsumer, DiscardConsumer)):
         K = consumer.K if isinstance(consumer, analytics.DegreeCountConsumer) else 0
         prb = torch.zeros(1, dtype=torch.int64, device=dev)
-        if K:
-            full = parallel._counts_kind(p, K) == "full"
-            counts = torch.zeros(K, dtype=torch.int32 if full else torch.int64, device=dev)
-        if b > a:
-            counts, _ = parallel.count_shard_device(p, K, a, b, counts=counts, probes=prb, device=dev)
-        if K:
-            # full histograms travel as 32-bit words (2m < 2^32, so the wrapped
-            # int32 sum has the exact bits): half the bytes of an int64 reduce
-            parallel.reduce_counts(counts)
+        full = bool(K) and parallel._counts_kind(p, K) == "full"
+        routed = None
+        if full and os.environ.get("PARBA_ROUTED", "1") != "0":
+            # full histogram: the reduce fused into the count kernels (every
+            # rank adds into the owners' slices over peer memory) when the
+            # path applies to every rank's shard and the GPUs can map each other
+            ok = torch.tensor([1 if (b == a or parallel.routed_ok(p, a, b, dev)) else 0], dtype=torch.int32,
+                              device=dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if int(ok.item()):
+                routed = parallel.RoutedCounts.try_create(p, device=dev)
+        if routed is not None:
+            with routed:
+                routed.run(a, b, probes=prb)
+                counts = routed.gather()  # int64, the whole histogram on every rank
+        else:
+            if K:
+                counts = torch.zeros(K, dtype=torch.int32 if full else torch.int64, device=dev)
+            if b > a:
+                counts, _ = parallel.count_shard_device(p, K, a, b, counts=counts, probes=prb, device=dev)
+            if K:
+                # full histograms travel as 32-bit words (2m < 2^32, so the wrapped
+                # int32 sum has the exact bits): half the bytes of an int64 reduce
+                parallel.reduce_counts(counts)
         probes = int(prb.item())
         if isinstance(consumer, analytics.DegreeCountConsumer):
             c = (parallel.widen_counts(torch, counts, K)[:K].cpu().numpy() if K

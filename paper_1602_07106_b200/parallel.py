@@ -15,6 +15,8 @@ world size.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 from . import _lib
@@ -137,6 +139,180 @@ def count_shard_device(p, K: int, lo: int, hi: int, counts=None, probes=None, de
             _lib.check(L.parba_degree_window(cp, lo, hi, K, counts.data_ptr() if K else None,
                                              probes.data_ptr(), st))
     return counts, probes
+
+
+# --------------------------------------------------------------------------
+# Owner-routed full histogram: the histogram reduce fused into the count
+# kernels (include/parba_b200.h, parba_degree_full_routed).
+
+MAX_OWNERS = 16
+
+
+def routed_slice_nodes(n: int, owners: int) -> int:
+    """Nodes per owner: ceil(n / owners) rounded up to a multiple of 2^16."""
+    return ((n + owners - 1) // owners + 0xFFFF) & ~0xFFFF
+
+
+def routed_ok(p, lo: int, hi: int, device=None) -> bool:
+    """True when edges [lo, hi) can be counted straight into owner slices
+    (plain uniform-degree family, n >= 2^25, a shard of >= 2^22 edges)."""
+    from .generator import _device
+
+    if p.d is None or p.has_flags or not (p.n < (1 << 32) and 2 * p.m < (1 << 32)):
+        return False
+    torch, dev = _device(device)
+    with torch.cuda.device(dev):
+        return bool(_lib.load().parba_degree_full_routed_ok(p._device_params(dev), lo, hi))
+
+
+def count_shard_routed(p, lo: int, hi: int, slice_ptrs, slice_nodes: int, probes=None, device=None):
+    """Generate edges [lo, hi) on this GPU and add the degree of every node v
+    into owner v // slice_nodes's uint32 slice (``slice_ptrs[g]``: a device
+    address valid on this GPU -- local, peer-mapped or IPC-mapped).  Returns
+    the probes tensor.  The owners zero their slices before any caller starts
+    and read them after every caller's stream has drained."""
+    import ctypes
+
+    from .generator import _device
+
+    torch, dev = _device(device)
+    if probes is None:
+        probes = torch.zeros(1, dtype=torch.int64, device=dev)
+    ptrs = (ctypes.c_void_p * len(slice_ptrs))(*[int(x) if x else None for x in slice_ptrs])
+    with torch.cuda.device(dev):
+        _lib.check(_lib.load().parba_degree_full_routed(p._device_params(dev), lo, hi, len(slice_ptrs), ptrs,
+                                                        slice_nodes, probes.data_ptr(), _lib.stream_ptr(torch, dev)))
+    return probes
+
+
+class _RawU32:
+    """A raw device allocation seen by torch (``torch.as_tensor``) without a copy."""
+
+    def __init__(self, ptr: int, count: int):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": "<i4", "data": (ptr, False), "version": 2}
+
+
+class RoutedCounts:
+    """The full degree histogram reduce-scattered over the ranks of the
+    default process group, one process per GPU: rank g owns the uint32
+    counters of nodes [g*S, (g+1)*S) in plain device memory mapped into every
+    other rank by CUDA IPC (NVLink peer memory), and every rank's count
+    kernels add into the owners' slices as they go (no collective over an
+    n-word array afterwards -- analytics.py:78-82's merge fused into the
+    count).  ``run(lo, hi)``: zero -> barrier -> count -> drain + barrier;
+    afterwards ``own`` (an int32 torch view of this rank's slice, bits of
+    uint32 counts) is complete.  ``gather()`` returns the whole int64
+    histogram on every rank (NCCL/gloo all-gather of the slices)."""
+
+    def __init__(self, p, device=None, group=None):
+        import ctypes
+
+        import torch.distributed as dist
+
+        from .generator import _device
+
+        self.p, self.group = p, group
+        self.torch, self.dev = _device(device)
+        self.rank, self.ws = dist.get_rank(group), dist.get_world_size(group)
+        if self.ws > MAX_OWNERS:
+            raise ParameterError(f"routed counts take at most {MAX_OWNERS} owners")
+        self.S = routed_slice_nodes(p.n, self.ws)
+        L = _lib.load()
+        self._ptr = ctypes.c_void_p()
+        self._opened: list[int] = []
+        self.ptrs: list[int] = []
+        self.own = None
+        self.error: str | None = None
+        handle = ctypes.create_string_buffer(64)
+        # every rank reaches every collective below even when a step failed
+        # on it; `error` is then set on all ranks and the object is unusable
+        try:
+            with self.torch.cuda.device(self.dev):
+                _lib.check(L.parba_ipc_alloc(self.S * 4, ctypes.byref(self._ptr), handle))
+        except Exception as e:
+            self.error = str(e)
+        handles: list = [None] * self.ws
+        dist.all_gather_object(handles, None if self.error else bytes(handle.raw), group=group)
+        if self.error is None and all(h is not None for h in handles):
+            try:
+                with self.torch.cuda.device(self.dev):
+                    for g, h in enumerate(handles):
+                        if g == self.rank:
+                            self.ptrs.append(self._ptr.value)
+                            continue
+                        q = ctypes.c_void_p()
+                        _lib.check(L.parba_ipc_open(ctypes.create_string_buffer(h, 64), ctypes.byref(q)))
+                        self._opened.append(q.value)
+                        self.ptrs.append(q.value)
+                self.own = self.torch.as_tensor(_RawU32(self._ptr.value, self.S), device=self.dev)
+            except Exception as e:
+                self.error = str(e)
+        elif self.error is None:
+            self.error = "a peer could not allocate its slice"
+        errs: list = [None] * self.ws
+        dist.all_gather_object(errs, self.error, group=group)
+        bad = [f"rank {g}: {e}" for g, e in enumerate(errs) if e]
+        if bad:
+            self.error = "; ".join(bad)
+            self.close()
+        self.lo_node = self.rank * self.S
+        self.count = max(0, min(self.S, p.n - self.lo_node))  # nodes of this rank's slice below n
+
+    @classmethod
+    def try_create(cls, p, device=None, group=None):
+        """A RoutedCounts, or None on every rank when any rank could not set
+        it up (no IPC / peer access between the GPUs): callers then reduce."""
+        rc = cls(p, device=device, group=group)
+        return None if rc.error else rc
+
+    def run(self, lo: int, hi: int, probes=None):
+        """Count edges [lo, hi) of this rank into the owners' slices.  Every
+        rank of the group calls this (collective: two barriers)."""
+        import torch.distributed as dist
+
+        torch = self.torch
+        self.own.zero_()
+        torch.cuda.synchronize(self.dev)
+        dist.barrier(group=self.group)  # every slice is zero before anyone adds
+        probes = count_shard_routed(self.p, lo, hi, self.ptrs, self.S, probes=probes, device=self.dev)
+        torch.cuda.synchronize(self.dev)
+        dist.barrier(group=self.group)  # every rank's adds have landed
+        return probes
+
+    def gather(self):
+        """int64 counts[n] on every rank."""
+        import torch.distributed as dist
+
+        own = self.own
+        if dist.get_backend(self.group) == "gloo":  # gloo gathers host tensors only
+            own = own.cpu()
+        parts = [self.torch.empty_like(own) for _ in range(self.ws)]
+        dist.all_gather(parts, own, group=self.group)
+        c = self.torch.cat(parts)[: self.p.n].to(self.dev)
+        return c.to(self.torch.int64) & 0xFFFFFFFF
+
+    def close(self) -> None:
+        import ctypes
+
+        import torch.distributed as dist
+
+        L = _lib.load()
+        self.own = None
+        with self.torch.cuda.device(self.dev):
+            self.torch.cuda.synchronize(self.dev)
+            for q in self._opened:
+                L.parba_ipc_close(q)
+            self._opened = []
+            dist.barrier(group=self.group)  # no peer still maps this rank's slice
+            if self._ptr:
+                L.parba_ipc_free(self._ptr)
+                self._ptr = ctypes.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
 
 
 def widen_counts(torch, counts, K: int):

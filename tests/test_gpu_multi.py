@@ -141,6 +141,107 @@ def test_multi_run_shards_nccl_path(monkeypatch):
     assert np.array_equal(res, ref[:999]) and sum(prs) == wp and prs[1] == 0
 
 
+# --------------------------------------------------------------------------- owner-routed full histogram
+
+
+def _routed_full(p, ranges, owners, dev="cuda:0"):
+    """Counts of the ranges through parba_degree_full_routed into `owners`
+    separately allocated slices on one device; returns (int64 counts[n], probes)."""
+    import torch
+
+    S = pb.parallel.routed_slice_nodes(p.n, owners)
+    slices = [torch.zeros(S, dtype=torch.int32, device=dev) for _ in range(owners)]
+    prb = torch.zeros(1, dtype=torch.int64, device=dev)
+    for a, b in ranges:
+        pb.parallel.count_shard_routed(p, a, b, [t.data_ptr() for t in slices], S, probes=prb, device=dev)
+    torch.cuda.synchronize()
+    c = torch.cat(slices)
+    assert int((c[p.n:] != 0).sum()) == 0  # nothing lands past node n - 1
+    return (c[: p.n].to(torch.int64) & 0xFFFFFFFF), int(prb.item())
+
+
+def _direct_full(p, ranges, dev="cuda:0"):
+    import torch
+
+    counts = None
+    prb = torch.zeros(1, dtype=torch.int64, device=dev)
+    for a, b in ranges:
+        counts, _ = pb.parallel.count_shard_device(p, p.n, a, b, counts=counts, probes=prb, device=dev)
+    torch.cuda.synchronize()
+    return (counts.to(torch.int64) & 0xFFFFFFFF), int(prb.item())
+
+
+@pytest.mark.parametrize("owners", [1, 2, 5])
+def test_routed_counts_small_vs_oracle(monkeypatch, owners):
+    """The routed count (forced onto the partitioned pass at small n) against
+    the oracle: seed graph, ragged ranges, nodes split over 1 / 2 / 5 owners."""
+    monkeypatch.setenv("PARBA_FULL_MODE", "partition")
+    p = pb.GenParams(n=300_000, d=7, n0=3, seed_edges=TRIANGLE)
+    ref = np.zeros(p.n, dtype=np.int64)
+    blk, wp = O.generate_block(_op(p), p.m0, p.m)
+    O.count_block(ref, blk)
+    ranges = [(p.m0, 700_001), (700_001, 700_001), (700_001, p.m)]
+    got, pr = _routed_full(p, ranges, owners)
+    assert np.array_equal(got.cpu().numpy(), ref) and pr == wp
+
+
+@pytest.mark.parametrize("env", [{}, {"PARBA_OFF16": "0"}, {"PARBA_ONE_SLICE": "0"}])
+def test_routed_counts_large_vs_local(monkeypatch, env):
+    """n >= 2^25 (the partitioned pass by default): routed slices over 8
+    owners == the local n-word histogram, for the u16-offset, u32-entry and
+    multi-slice bucket layouts."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    n = 70_000_000 if env.get("PARBA_ONE_SLICE") == "0" else (1 << 25) + 12_345
+    p = pb.GenParams(n=n, d=3)
+    cut = p.m // 3 + 17
+    assert pb.parallel.routed_ok(p, 0, cut) and pb.parallel.routed_ok(p, cut, p.m)
+    got, pr = _routed_full(p, [(0, cut), (cut, p.m)], 8)
+    monkeypatch.setenv("PARBA_FULL_MODE", "direct")
+    want, wp = _direct_full(p, [(0, p.m)])
+    assert bool((got == want).all()) and pr == wp
+    assert int(got.sum()) == 2 * p.m
+
+
+def test_routed_counts_validation():
+    import torch
+
+    small = pb.GenParams(n=10_000, d=4)
+    assert not pb.parallel.routed_ok(small, 0, small.m)
+    p = pb.GenParams(n=(1 << 25) + 5, d=2)
+    assert pb.parallel.routed_ok(p, 0, p.m) and not pb.parallel.routed_ok(p, 0, 1000)
+    S = pb.parallel.routed_slice_nodes(p.n, 2)
+    t = [torch.zeros(S, dtype=torch.int32, device="cuda:0") for _ in range(2)]
+    ptrs = [x.data_ptr() for x in t]
+    with pytest.raises(pb.ParameterError):  # slices too small for n
+        pb.parallel.count_shard_routed(p, 0, p.m, ptrs[:1], S)
+    with pytest.raises(pb.ParameterError):  # not a multiple of 2^16
+        pb.parallel.count_shard_routed(p, 0, p.m, ptrs, S + 1)
+    with pytest.raises(pb.ParameterError):  # a shard the partitioned pass does not take
+        pb.parallel.count_shard_routed(p, 0, 1000, ptrs, S)
+    with pytest.raises(pb.ParameterError):
+        pb.parallel.count_shard_routed(p, 0, p.m, [ptrs[0], 0], S)
+    pb.parallel.count_shard_routed(p, 5, 5, ptrs, S)  # empty range: nothing to do
+    assert int(t[0].sum()) == 0
+
+
+def test_multi_run_routed_path(monkeypatch):
+    """parba_multi_run_shards' owner-routed full histogram, forced on one
+    device with three owner slices: equal to the oracle and to the reduce."""
+    monkeypatch.setenv("PARBA_FULL_MODE", "partition")
+    monkeypatch.setenv("PARBA_MULTI_ROUTED", "1")
+    monkeypatch.setenv("PARBA_MULTI_OWNERS", "3")
+    p = pb.GenParams(n=200_000, d=6, n0=3, seed_edges=TRIANGLE)
+    ref = np.zeros(p.n, dtype=np.int64)
+    blk, wp = O.generate_block(_op(p), p.m0, p.m)
+    O.count_block(ref, blk)
+    got, pr, secs = pb.parallel.multi_run(p, [0, 0, 0], mode="full")
+    assert np.array_equal(got, ref) and pr == wp and secs > 0
+    monkeypatch.setenv("PARBA_MULTI_ROUTED", "0")
+    got2, pr2, _ = pb.parallel.multi_run(p, [0, 0, 0], mode="full")
+    assert np.array_equal(got2, ref) and pr2 == wp
+
+
 def test_multi_run_two_devices():
     import torch
 
