@@ -550,10 +550,25 @@ def main() -> None:
                                "equal_shard_ms": t_eq, "cuts": cuts}
                 counts.zero_()
                 prb.zero_()
+                # full histogram on N > 1 GPUs: the reduce fused into the count
+                # kernels (every rank adds into the owners' slices over peer
+                # memory, parallel.RoutedCounts) when the GPUs can map each
+                # other; else count locally + one NCCL reduce of the u32 words
+                routed = None
+                if full and ws > 1 and os.environ.get("PARBA_ROUTED", "1") != "0":
+                    ok = torch.tensor([1 if pb.parallel.routed_ok(q, a, b, dev) else 0], dtype=torch.int32, device=dev)
+                    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+                    if int(ok.item()):
+                        routed = pb.parallel.RoutedCounts.try_create(q, device=dev)
+                    if routed is not None:
+                        routed.run(a, b)  # warm-up of the routed kernels and the peer mappings
                 barrier()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
                 for _ in range(steps):
+                    if routed is not None:
+                        routed.run(a, b, probes=prb)  # zero, barrier, count into the owners, drain + barrier
+                        continue
                     counts.zero_()
                     pb.parallel.count_shard_device(q, K, a, b, counts=counts, probes=prb, device=dev)
                     pb.parallel.reduce_counts(counts, op="reduce")  # u32 words for the full histogram
@@ -561,9 +576,15 @@ def main() -> None:
                 torch.cuda.synchronize(dev)
                 t_rank = e0.elapsed_time(e1) / 1000.0
                 t = max_over_ranks(t_rank)
-                c64 = pb.parallel.widen_counts(torch, counts, K)
-                if full and rank == 0:
-                    assert int(c64.sum().item()) == 2 * q.m
+                if routed is not None:
+                    tot = (routed.own[: routed.count].to(torch.int64) & 0xFFFFFFFF).sum().reshape(1)
+                    dist.all_reduce(tot)
+                    assert int(tot.item()) == 2 * q.m
+                    routed.close()
+                else:
+                    c64 = pb.parallel.widen_counts(torch, counts, K)
+                    if full and rank == 0:
+                        assert int(c64.sum().item()) == 2 * q.m
                 eps = q.m * steps / t
                 ppe = int(prb.item()) / ((b - a) * steps)
                 extra[name] = {"edges_per_s": eps, "ms_per_step": 1000 * t / steps,
@@ -586,6 +607,11 @@ def main() -> None:
                 if full:
                     extra[name]["path"] = ("partitioned: targets pass with per-CTA bucket histogram, bucket "
                                            "sort in shared memory, shared-memory slice counts (parba_hist.cuh)")
+                    if ws > 1:
+                        extra[name]["reduce"] = (
+                            "fused: count kernels red.add into the owners' slices over peer memory "
+                            "(reduce-scatter, parba_degree_full_routed)" if routed is not None
+                            else "one reduce of the u32 histogram over the process group")
                 del counts
         if extra:
             extra["clocks"] = clk_modes.summary()
