@@ -288,6 +288,8 @@ int parba_bb_fill(const parba_params_t *p, uint64_t *E, uint64_t *link, unsigned
 #define PARBA_MOD_FP_WIDE_SERIES 6
 #define PARBA_MOD_FP31_SERIES1 7      /* the series + one-stage remainder, r in [2^28 + 224, 2^31) */
 #define PARBA_MOD_FP_WIDE_SERIES1 8   /* the same in 64 bits, r in [2^28 + 224, 2^52)              */
+#define PARBA_MOD_FP32 9              /* r <= 0xF0000000 (chain values of 3-chunk launches): 32-bit tail */
+#define PARBA_MOD_FP32_SERIES 10      /* the same with the series reciprocal                       */
 /* out[k] = (hhi[k] * 2^32 + hlo[k]) mod r[k] by `method` (device buffers). */
 int parba_debug_mod(int method, const uint32_t *hhi, const uint32_t *hlo, const uint64_t *r, uint64_t count,
                     uint64_t *out, void *stream);

@@ -37,7 +37,7 @@ EXPORTS = (
     "parba_ipc_close", "parba_ipc_free",
 )
 MOD_FP31, MOD_FP_NARROW, MOD_FP_WIDE, MOD_INT, MOD_FP31_SERIES, MOD_FP_NARROW_SERIES, MOD_FP_WIDE_SERIES, \
-    MOD_FP31_SERIES1, MOD_FP_WIDE_SERIES1 = range(9)
+    MOD_FP31_SERIES1, MOD_FP_WIDE_SERIES1, MOD_FP32, MOD_FP32_SERIES = range(11)
 MULTI_STORE, MULTI_WINDOW, MULTI_FULL, MULTI_DISCARD = 0, 1, 2, 3
 
 

@@ -130,13 +130,13 @@ int bits_of(uint64_t x) { return x ? 64 - __builtin_clzll(x) : 0; }
 
 // CRC chunk tables needed to cover every chain value of a launch (r <= 2*hi-1,
 // the largest first value): 2 -> r < 2^31 (narrow, 32-bit remainder),
-// 3 -> r < 2^32, 4 -> < 2^43, 5 -> < 2^52, 6 -> any.  (Classing by 2*hi
+// 3 -> r <= kR32Max (0.9375 * 2^32), 4 -> < 2^43, 5 -> < 2^52, 6 -> any.  (Classing by 2*hi
 // itself put a range ending at exactly 2^30 edges -- C4's second batch --
 // on the slower 3-chunk kernel.)
 int nc_for(uint64_t max_r) {
     const int b = bits_of(max_r);
     if (b <= 31) return 2;
-    if (b <= 32) return 3;
+    if (PARBA_R32 ? max_r <= kR32Max : b <= 32) return 3;  // the 32-bit tail of mod_fp32_y
     if (b <= 43) return 4;
     if (b <= 52) return 5;
     return 6;

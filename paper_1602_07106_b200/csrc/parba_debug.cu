@@ -4,7 +4,9 @@
 // (hhi, hlo, r) -- not only on the values a CRC happens to produce.
 //
 //   PARBA_MOD_FP31       mod_fp31 (HashCrc<2>: r < 2^31)
-//   PARBA_MOD_FP_NARROW  mod_fp<u32> with I2F of r (HashCrc<3>: r < 2^32)
+//   PARBA_MOD_FP_NARROW  mod_fp<u32> with I2F of r (r < 2^32; HashCrc<3> before mod_fp32_y)
+//   PARBA_MOD_FP32       mod_fp32_y (HashCrc<3>: r <= kR32Max = 0xF0000000), and its
+//                        series form PARBA_MOD_FP32_SERIES
 //   PARBA_MOD_FP_WIDE    mod_fp<u64> with the wide conversion (HashCrc<4,5>: r < 2^52)
 //   PARBA_MOD_INT        mod_int (HashCrc<6>, HashCrcBytes: any r >= 1)
 //   PARBA_MOD_*_SERIES   the same remainders with 1/r taken from phase 1's
@@ -33,6 +35,10 @@ __device__ __forceinline__ uint64_t eval_mod(int method, uint32_t hhi, uint32_t 
         case PARBA_MOD_FP_NARROW: return mod_fp<uint32_t>(hhi, hlo, u32_to_f64((uint32_t)r));
         case PARBA_MOD_FP_WIDE: return mod_fp<uint64_t>(hhi, hlo, r_to_f64w(r));
         case PARBA_MOD_INT: return mod_int(hhi, hlo, r);
+        case PARBA_MOD_FP32: {
+            const double rd = u32_to_f64((uint32_t)r);
+            return mod_fp32_y(hhi, hlo, (uint32_t)r, rd, recip_approx(rd));
+        }
         default: break;
     }
     // series: the lane's centre rc, c = 1/rc, y_k = c - (k - 3.5) * 64 c^2
@@ -48,6 +54,7 @@ __device__ __forceinline__ uint64_t eval_mod(int method, uint32_t hhi, uint32_t 
         case PARBA_MOD_FP_WIDE_SERIES1: return mod_fp_y1w(hhi, hlo, r, y);
         case PARBA_MOD_FP31_SERIES: return mod_fp31_y(hhi, hlo, (uint32_t)r, rd, y);
         case PARBA_MOD_FP_NARROW_SERIES: return mod_fp_y<uint32_t>(hhi, hlo, rd, y);
+        case PARBA_MOD_FP32_SERIES: return mod_fp32_y(hhi, hlo, (uint32_t)r, rd, y);
         default: return mod_fp_y<uint64_t>(hhi, hlo, rd, y);
     }
 }
@@ -104,7 +111,7 @@ __global__ void mod_check_kernel(int method, uint64_t seed, uint64_t count, uint
     }
 }
 
-bool method_ok(int m) { return m >= PARBA_MOD_FP31 && m <= PARBA_MOD_FP_WIDE_SERIES1; }
+bool method_ok(int m) { return m >= PARBA_MOD_FP31 && m <= PARBA_MOD_FP32_SERIES; }
 
 // rcp.approx.ftz.f64 (MUFU.RCP64H) reads only the high word of its operand:
 // for one high word (sign 0, biased exponent E, top 20 mantissa bits M) the

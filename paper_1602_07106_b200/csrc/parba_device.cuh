@@ -322,6 +322,27 @@ __device__ __forceinline__ uint32_t mod_fp31_y(uint32_t hhi, uint32_t hlo, uint3
     const uint32_t t = hlo + nqb * r;                           // exact mod 2^32
     return min(t, t + r);
 }
+// The same for 1 <= r <= kR32Max (3-chunk launches: chain values < 2^32).
+// With y ~ 1/r to a relative error < 2^-37.6 (recip_approx: 2^-39; the tile
+// series adds (224/2^27)^2) and v = RN(V), V = x*2^32 + hlo (|v - V| < r*2^-21):
+// |v*y - V/r| < 2^32 * 2^-37.6 + 2^-21 < 0.0207, so qb = round(v*y) gives
+// t = V - qb*r with |t| <= 0.5207 r < 2^31 for r <= kR32Max = 0.9375 * 2^32:
+// t = hlo - qb*r (mod 2^32) read as int32 is exact, and t < 0 ? t + r : t is
+// the remainder.  3 integer instructions instead of mod_fp's ~9 FP64 ones
+// for the second stage (PARBA_R32=0: 3-chunk launches keep mod_fp, A/B).
+#ifndef PARBA_R32
+#define PARBA_R32 1
+#endif
+constexpr uint32_t kR32Max = 0xF0000000u;
+__device__ __forceinline__ uint32_t mod_fp32_y(uint32_t hhi, uint32_t hlo, uint32_t r, double rd, double y) {
+    const double ha = cvt31<1>(hhi);
+    const double qa = fma(ha, y, 0x1.8p52) - 0x1.8p52;
+    const double x = fma(-qa, rd, ha);                          // exact, in [-r, r)
+    const double v = fma(x, 0x1p32, cvt31<2>(hlo));
+    const uint32_t nqb = (uint32_t)__double2loint(fma(-v, y, 0x1.8p52));  // -qb mod 2^32
+    const uint32_t t = hlo + nqb * r;                           // t mod 2^32, |t| < 2^31
+    return t + (r & (uint32_t)((int32_t)t >> 31));
+}
 #ifndef PARBA_ONESTAGE
 #define PARBA_ONESTAGE 1
 #endif
@@ -546,8 +567,8 @@ __device__ __forceinline__ uint32_t crc_chunks(uint32_t tab, uint64_t w) {
 // Hash policies.  R is the chain-value type (u32 when every position < 2^32).
 // probe(tab, r) = h(r); from_crc(c0, r) finishes h from c0 = crc(s0, r).
 
-// Tile kernels: chunk tables; NC = 2 (every r < 2^31; 3 tables), 3 (< 2^32),
-// 4 (< 2^43), 5 (< 2^52), 6 (any).
+// Tile kernels: chunk tables; NC = 2 (every r < 2^31; 3 tables), 3 (<= kR32Max,
+// just below 2^32), 4 (< 2^43), 5 (< 2^52), 6 (any).
 template <int NC>
 struct HashCrc {
     static constexpr bool kHasCrc = true;
@@ -566,7 +587,10 @@ struct HashCrc {
     }
     __device__ __forceinline__ static R from_crc(uint32_t c0, R r, const DevParams &p) {
         if constexpr (NC == 2) return mod_fp31(c0, c0 ^ p.k01, r);
-        else if constexpr (kNarrow) return mod_fp<R>(c0, c0 ^ p.k01, u32_to_f64(r));
+        else if constexpr (kNarrow && PARBA_R32) {
+            const double rd = u32_to_f64(r);
+            return mod_fp32_y(c0, c0 ^ p.k01, r, rd, recip_approx(rd));
+        } else if constexpr (kNarrow) return mod_fp<R>(c0, c0 ^ p.k01, u32_to_f64(r));
         else if constexpr (NC <= 5) return mod_fp<R>(c0, c0 ^ p.k01, r_to_f64w(r));
         else return mod_int(c0, c0 ^ p.k01, r);
     }
@@ -576,6 +600,7 @@ struct HashCrc {
     __device__ __forceinline__ static R from_crc_ry(uint32_t c0, R r, double rd, double y,
                                                     const DevParams &p) {
         if constexpr (NC == 2) return mod_fp31_y(c0, c0 ^ p.k01, r, rd, y);
+        else if constexpr (kNarrow && PARBA_R32) return mod_fp32_y(c0, c0 ^ p.k01, r, rd, y);
         else return mod_fp_y<R>(c0, c0 ^ p.k01, rd, y);
     }
     // One-stage remainder (mod_fp31_y1 / mod_fp_y1w) for first probes of

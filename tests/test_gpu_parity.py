@@ -1023,11 +1023,13 @@ def test_wide_store_fp64_targets_at_the_bounds(n, d, seeded, monkeypatch):
         assert np.array_equal(alt.cpu().numpy().view(np.uint64), g)
 
 
-@pytest.mark.parametrize("hi", [1 << 30, (1 << 30) + 1, (1 << 30) + 100, 1 << 31, (1 << 31) + 1, (1 << 31) + 77])
+@pytest.mark.parametrize("hi", [1 << 30, (1 << 30) + 1, (1 << 30) + 100, 0x78000000, 0x78000000 + 1, 1 << 31,
+                                (1 << 31) + 1, (1 << 31) + 77])
 def test_chunk_class_boundaries(hi):
     """The launch's kernel class follows its largest chain value 2*hi-1:
-    ranges ending at exactly 2^30 / 2^31 edges run the 2- / 3-chunk kernels
-    (r < 2^31 / r < 2^32), one edge more the next class.  Store, window and
+    ranges ending at exactly 2^30 / 0x78000000 edges run the 2- / 3-chunk
+    kernels (r < 2^31 / r <= 0xF0000000, the 32-bit-tail remainder's range),
+    one edge more the next class.  Store, window and
     full counts of [hi - 300017, hi) vs the oracle, ragged top tiles included."""
     import torch
 

@@ -47,6 +47,10 @@ CLASSES = [
     (L_.MOD_FP31_SERIES1, ONESTAGE_MIN, (1 << 31) - 1),
     (L_.MOD_FP_WIDE_SERIES1, ONESTAGE_MIN, (1 << 52) - 1),
     (L_.MOD_FP_WIDE_SERIES1, 1 << 44, (1 << 52) - 1),
+    (L_.MOD_FP32, 1, 0xF0000000),            # 3-chunk launches: the 32-bit tail
+    (L_.MOD_FP32, 0xE0000000, 0xF0000000),   # at the top of its range, |t| closest to 2^31
+    (L_.MOD_FP32_SERIES, RY_MIN, 0xF0000000),
+    (L_.MOD_FP32_SERIES, 0xE0000000, 0xF0000000),
 ]
 
 
