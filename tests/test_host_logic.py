@@ -239,3 +239,15 @@ def test_balanced_cuts():
     assert P.balanced_cuts([0, 100, 200, 300, 400], [1, 1, 2, 4], align=1) == [0, 200, 300, 350, 400]
     with pytest.raises(pb.ParameterError):
         P.balanced_cuts([0, 1], [1.0, 2.0])
+
+
+def test_routed_slice_nodes():
+    """Owner slices of the routed full histogram: multiples of 2^16 (>= the
+    57344 nodes one count CTA holds, so a CTA's nodes have at most two
+    owners) that cover [0, n) with the last owner possibly short or empty."""
+    for n in (1, 65_536, 65_537, 10**8, (1 << 25) + 12_345, (1 << 31) - 1):  # 2m < 2^32 bounds n
+        for owners in (1, 2, 3, 8, 16):
+            S = pb.parallel.routed_slice_nodes(n, owners)
+            assert S % 65_536 == 0 and S >= 65_536 and S * owners >= n
+            assert S - 65_536 < (n + owners - 1) // owners  # no more padding than one 2^16 block
+            assert S < (1 << 32)
