@@ -260,6 +260,9 @@ int parba_degree_full_routed(const parba_params_t *p, uint64_t lo, uint64_t hi, 
  * (handle64: 64 bytes to send to the peers); parba_ipc_open maps a peer's
  * handle on the current device; parba_ipc_close / parba_ipc_free undo them. */
 int parba_ipc_alloc(uint64_t bytes, void **dev_ptr, void *handle64);
+/* 1 when kernels on `dev` can map `peer`'s memory and add into it with native
+ * atomics (red.add over NVLink); routed counts need it of every pair. */
+int parba_peer_atomics_ok(int dev, int peer);
 int parba_ipc_open(const void *handle64, void **dev_ptr);
 int parba_ipc_close(void *dev_ptr);
 int parba_ipc_free(void *dev_ptr);

@@ -34,7 +34,7 @@ EXPORTS = (
     "parba_multi_run", "parba_multi_run_shards", "parba_crc32c", "parba_mulhi_u64", "parba_degseq_dense",
     "parba_peak_int32", "parba_peak_write", "parba_debug_mod", "parba_debug_mod_check", "parba_debug_rcp_bound",
     "parba_bb_fill", "parba_degree_full_routed_ok", "parba_degree_full_routed", "parba_ipc_alloc", "parba_ipc_open",
-    "parba_ipc_close", "parba_ipc_free",
+    "parba_ipc_close", "parba_ipc_free", "parba_peer_atomics_ok",
 )
 MOD_FP31, MOD_FP_NARROW, MOD_FP_WIDE, MOD_INT, MOD_FP31_SERIES, MOD_FP_NARROW_SERIES, MOD_FP_WIDE_SERIES, \
     MOD_FP31_SERIES1, MOD_FP_WIDE_SERIES1, MOD_FP32, MOD_FP32_SERIES = range(11)
@@ -125,6 +125,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
             "parba_ipc_open": ([vp, ctypes.POINTER(vp)], i32),
             "parba_ipc_close": ([vp], i32),
             "parba_ipc_free": ([vp], i32),
+            "parba_peer_atomics_ok": ([i32, i32], i32),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name, None)

@@ -686,13 +686,15 @@ struct RoutedRun {
     }
 };
 
-// Every device of the run can map every other one's memory (enabled here).
+// Every device of the run can map every other one's memory (enabled here)
+// and add into it with native atomics (NVLink; not every PCIe path).
 bool peers_ok(const std::vector<int> &udev) {
     for (int a : udev)
         for (int b : udev) {
             if (a == b) continue;
             int can = 0;
             if (cudaDeviceCanAccessPeer(&can, a, b) != cudaSuccess || !can) return false;
+            if (!parba_peer_atomics_ok(a, b)) return false;
         }
     for (int a : udev) {
         if (cudaSetDevice(a) != cudaSuccess) return false;
@@ -980,6 +982,20 @@ int parba_ipc_alloc(uint64_t bytes, void **dev_ptr, void *handle64) {
     memcpy(handle64, &h, 64);
     *dev_ptr = ptr;
     return PARBA_OK;
+}
+
+int parba_peer_atomics_ok(int dev, int peer) {
+    if (dev == peer) return 1;
+    int can = 0, native = 0;
+    if (cudaDeviceCanAccessPeer(&can, dev, peer) != cudaSuccess || !can) {
+        cudaGetLastError();
+        return 0;
+    }
+    if (cudaDeviceGetP2PAttribute(&native, cudaDevP2PAttrNativeAtomicSupported, dev, peer) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return native ? 1 : 0;
 }
 
 int parba_ipc_open(const void *handle64, void **dev_ptr) {

@@ -20,7 +20,7 @@ import os
 import numpy as np
 
 from . import _lib
-from .errors import ParameterError
+from .errors import GenerationError, ParameterError
 
 
 def world() -> tuple[int, int]:
@@ -232,14 +232,18 @@ class RoutedCounts:
         except Exception as e:
             self.error = str(e)
         handles: list = [None] * self.ws
-        dist.all_gather_object(handles, None if self.error else bytes(handle.raw), group=group)
+        mine = self.dev.index if self.dev.index is not None else self.torch.cuda.current_device()
+        dist.all_gather_object(handles, None if self.error else (bytes(handle.raw), mine), group=group)
         if self.error is None and all(h is not None for h in handles):
             try:
                 with self.torch.cuda.device(self.dev):
-                    for g, h in enumerate(handles):
+                    for g, (h, peer) in enumerate(handles):
                         if g == self.rank:
                             self.ptrs.append(self._ptr.value)
                             continue
+                        # (ranks see the same device numbering under torchrun)
+                        if peer != mine and not L.parba_peer_atomics_ok(mine, peer):
+                            raise GenerationError(f"no native peer atomics between GPUs {mine} and {peer}")
                         q = ctypes.c_void_p()
                         _lib.check(L.parba_ipc_open(ctypes.create_string_buffer(h, 64), ctypes.byref(q)))
                         self._opened.append(q.value)
