@@ -507,6 +507,11 @@ __device__ __forceinline__ void sts_t_if(bool pred, uint32_t addr, T v) {
 __device__ __forceinline__ void sts_u16(uint32_t addr, uint16_t v) {
     asm volatile("st.shared.u16 [%0], %1;" :: "r"(addr), "h"(v) : "memory");
 }
+// 32 bytes (two edge rows) with one streaming store (sm_100: STG.256); the
+// address must be 32-byte aligned.
+__device__ __forceinline__ void stcs_256(void *ptr, uint64_t a, uint64_t b, uint64_t c, uint64_t d) {
+    asm volatile("st.global.cs.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(ptr), "l"(a), "l"(b), "l"(c), "l"(d) : "memory");
+}
 // Loop-invariant value the compiler must keep in a register (it would
 // otherwise rematerialise shared-window bases inside the hot loop).
 __device__ __forceinline__ uint32_t opaque(uint32_t x) {

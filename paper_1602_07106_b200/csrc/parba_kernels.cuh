@@ -87,6 +87,11 @@ constexpr uint32_t kWinSmem = PARBA_WIN_SMEM;
 #ifndef PARBA_NBUF
 #define PARBA_NBUF 2
 #endif
+// narrow store flush of interior tiles: 256-bit stores of edge pairs (A/B
+// knob; measured 2.1% slower at C2 than 128-bit rows, profiles/r02_ab_st256.txt: off)
+#ifndef PARBA_ST256
+#define PARBA_ST256 0
+#endif
 constexpr int kStageBufs = PARBA_NBUF;
 
 constexpr int kThreads = kWarps * 32;
@@ -400,6 +405,26 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
                     return;
                 }
             }
+#if PARBA_ST256
+            if constexpr (FULL && NARROW && !DEG) {
+                // interior tile, 32-byte aligned rows: each lane writes pairs of
+                // consecutive edges (2*lane + 64k, +1) with one 256-bit store,
+                // their two staged values read by one 8-byte load
+                if ((reinterpret_cast<uintptr_t>(o) & 31u) == 0) {
+#pragma unroll
+                    for (int k = 0; k < kEpl / 2; ++k) {
+                        const uint32_t j = 2u * lane + 64u * k;
+                        const uint64_t i = base + j;
+                        const uint64_t rr = lds_u64(stage_s + (b * kTile + j) * 4u);
+                        const uint64_t t0 = target_of<NARROW, SEED, Hash::kR31, false>((uint64_t)(uint32_t)rr, p);
+                        const uint64_t t1 = target_of<NARROW, SEED, Hash::kR31, false>(rr >> 32, p);
+                        stcs_256(o + j, source_of<NARROW, SEED, false>(i, p), t0,
+                                 source_of<NARROW, SEED, false>(i + 1, p), t1);
+                    }
+                    return;
+                }
+            }
+#endif
 #pragma unroll
             for (int k = 0; k < kEpl; ++k) {
                 const uint32_t j = lane + 32u * k;
