@@ -172,6 +172,7 @@ int launch_tiles_t(const DevParams &dp, uint64_t lo, uint64_t hi, const SinkArgs
     int rc = dev_info(&di);
     if (rc) return rc;
     auto kern = tile_kernel<Hash, SINK, SEED, DEG>;
+    constexpr uint64_t kTile = TileLayout<Hash, SINK>::kTileE;  // this kernel's tile (shadows the default)
     // as many warps per CTA (<= kWarps) as the shared memory allows
     const size_t fixed = TileLayout<Hash, SINK>::fixed, per_warp = TileLayout<Hash, SINK>::per_warp;
     int warps = warps_for(SINK);

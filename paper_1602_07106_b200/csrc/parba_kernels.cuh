@@ -46,6 +46,13 @@ constexpr int kQueue = 512;                // per-warp pending ring (>= kTile + 
 #define PARBA_NARROW_SPLIT 0  // A/B: the split phase 1 and 256-entry queue for narrow store kernels too
 #endif
 constexpr int kEpl = kTile / 32;           // edges per lane in phase 1
+// Narrow CRC store launches: 512-edge tiles (16 edges per lane, phase 1 in
+// four 128-edge pieces with a drain between them and a 256-entry queue), so
+// the per-tile work -- crc(2*base), bounds, the flush hand-over -- is paid
+// once per 512 edges (A/B knob).
+#ifndef PARBA_TILE512
+#define PARBA_TILE512 1
+#endif
 // first probes use the per-tile reciprocal series from 2*base >= 2^27 on
 constexpr uint64_t kRyMin = 1ull << 27;
 #ifndef PARBA_WARPS
@@ -172,15 +179,20 @@ struct TileLayout {
     // wide store (64-bit values, packed entries): a 256-entry queue, with
     // phase 1 split in two halves and a drain between them (at most 31 + 128
     // entries are ever queued), so 32 warps fit instead of 23
+    static constexpr bool kBig = PARBA_TILE512 && SINK == kStore && Hash::kNarrow && Hash::kHasCrc;
+    static constexpr int kTileE = kBig ? 2 * kTile : kTile;  // edges per warp tile of this kernel
+    static constexpr int kEplE = kTileE / 32;                 // edges per lane in phase 1
     static constexpr bool kSplit =
-        is_store(SINK) && ((!Hash::kNarrow && Hash::kPack && PARBA_WIDE_SPLIT) || (Hash::kNarrow && PARBA_NARROW_SPLIT));
+        kBig || (is_store(SINK) &&
+                 ((!Hash::kNarrow && Hash::kPack && PARBA_WIDE_SPLIT) || (Hash::kNarrow && PARBA_NARROW_SPLIT)));
+    static constexpr int kPieceEpl = kSplit ? 4 : kEplE;     // edges per lane between two drains
     static constexpr uint32_t kQ = kSplit ? 256u : (uint32_t)kQueue;
     static constexpr uint32_t kQB = kQ * kEB;
-    static constexpr uint32_t kTB = kTile * (uint32_t)sizeof(R);  // one stage buffer
+    static constexpr uint32_t kTB = kTileE * (uint32_t)sizeof(R);  // one stage buffer
     static constexpr uint32_t kStageB = is_store(SINK) ? kStageBufs * kTB : 0;
     static constexpr bool kSlots = is_store(SINK) && !Hash::kPack;
     static constexpr uint32_t kSlotB = kSlots ? kQueue * 2 : 0;
-    static constexpr size_t kTabB = Hash::kHasCrc ? (Hash::kTableWords + kTile) * 4 : 0;
+    static constexpr size_t kTabB = Hash::kHasCrc ? (Hash::kTableWords + kTileE) * 4 : 0;
     static constexpr size_t kHistB = is_targets(SINK)   ? kHistGroups * kHistBucketsMax * 4
                                      : SINK == kStoreT ? kHistBuckets * 4
                                                        : 0;
@@ -244,6 +256,8 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
     using R = typename Hash::R;
     constexpr bool NARROW = Hash::kNarrow;
     using L = TileLayout<Hash, SINK>;
+    constexpr int kTile = L::kTileE;  // this kernel's tile (shadows the default)
+    constexpr int kEpl = L::kEplE;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
@@ -572,8 +586,8 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
     // into the one-stage remainder (mod_fp31_y1: no rd, 4 FP64 instructions
     // instead of 7 per first probe).
     [[maybe_unused]] double rc = 0.0, c = 0.0, s64 = 0.0;  // RY: this lane's series of the current tile
-    auto ry_setup = [&](uint64_t base) {
-        rc = u52_to_f64(2 * base + 2 * lane + 1 + 224);
+    auto ry_setup = [&](uint64_t base, int half) {  // half: the lane's edges 8*half .. 8*half + 7
+        rc = u52_to_f64(2 * base + 2 * lane + 1 + 224 + 512 * half);
         c = recip_approx(rc);
         s64 = 64.0 * c * c;
     };
@@ -590,11 +604,12 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
             const R r0 = (R)(2 * base) + (R)(2 * j + 1);
             R r1;
             if constexpr (RY == 2) {
-                if constexpr (Hash::kHasRy1) r1 = Hash::from_crc_ry1(cb ^ clow_s[j], r0, fma(-(k - 3.5), s64, c), p);
+                if constexpr (Hash::kHasRy1)
+                    r1 = Hash::from_crc_ry1(cb ^ clow_s[j], r0, fma(-((k & 7) - 3.5), s64, c), p);
             } else if constexpr (RY == 1) {
-                static_assert(kEpl == 8, "series centre assumes 8 edges per lane");
-                const double e = 64.0 * k - 224.0;
-                r1 = Hash::from_crc_ry(cb ^ clow_s[j], r0, rc + e, fma(-(k - 3.5), s64, c), p);
+                static_assert(kEpl % 8 == 0, "one series centre per 8 edges of a lane");
+                const double e = 64.0 * (k & 7) - 224.0;
+                r1 = Hash::from_crc_ry(cb ^ clow_s[j], r0, rc + e, fma(-((k & 7) - 3.5), s64, c), p);
             } else if constexpr (Hash::kHasCrc) {
                 r1 = Hash::from_crc(cb ^ clow_s[j], r0, p);
             } else {
@@ -660,16 +675,26 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
         // phase 1 over all 8 edges per lane, or in two halves with a drain
         // between them (the 256-entry queue of the wide store)
         auto run_phase1 = [&](auto full_c, auto ry_c) {
-            if constexpr (decltype(ry_c)::value != 0) ry_setup(base);
-            if constexpr (L::kSplit) {
-                phase1(full_c, ry_c, base, cb, std::integral_constant<int, 0>{}, std::integral_constant<int, kEpl / 2>{});
-                __syncwarp();
-                drain();
-                phase1(full_c, ry_c, base, cb, std::integral_constant<int, kEpl / 2>{},
-                       std::integral_constant<int, kEpl>{});
-            } else {
-                phase1(full_c, ry_c, base, cb, std::integral_constant<int, 0>{}, std::integral_constant<int, kEpl>{});
-            }
+            constexpr int PE = L::kPieceEpl, NP = kEpl / PE;
+            static_assert(NP * PE == kEpl && NP <= 4 && (8 % PE == 0 || PE % 8 == 0), "phase-1 pieces");
+            // piece P: the lane's edges [P*PE, (P+1)*PE); a new reciprocal
+            // series at every 8th edge; a drain between pieces
+            auto piece = [&](auto p_c) {
+                constexpr int P = decltype(p_c)::value;
+                if constexpr (P < NP) {
+                    if constexpr (decltype(ry_c)::value != 0 && (P * PE) % 8 == 0) ry_setup(base, (P * PE) / 8);
+                    if constexpr (P > 0) {
+                        __syncwarp();
+                        drain();
+                    }
+                    phase1(full_c, ry_c, base, cb, std::integral_constant<int, P * PE>{},
+                           std::integral_constant<int, (P + 1) * PE>{});
+                }
+            };
+            piece(std::integral_constant<int, 0>{});
+            piece(std::integral_constant<int, 1>{});
+            piece(std::integral_constant<int, 2>{});
+            piece(std::integral_constant<int, 3>{});
         };
         if (base >= lo && base + kTile <= hi) {
             using I0 = std::integral_constant<int, 0>;
