@@ -711,7 +711,8 @@ int count_partitioned(const parba_params_t *p, const DevParams &dp, uint64_t lo,
     if (rc) return rc;
     const uint64_t batch = hi - lo < kHistBatch ? hi - lo : kHistBatch;
     // a launch fills nw * ceil(ntiles / nw) * kTile slots, nw <= 64 warps per SM
-    const uint64_t cap = (batch / kTile + 2) * kTile + (uint64_t)di->sms * 64 * kTile;
+    // (tiles of up to 2 * kTile edges: the streaming sinks' 512-edge tiles)
+    const uint64_t cap = (batch / kTile + 4) * kTile + (uint64_t)di->sms * 64 * 2 * kTile;
     const uint32_t nblk = (uint32_t)di->sms * 4 * kHistGroups;  // >= warp groups of one tile launch
     PartScratch ps;
     const bool stt = K >= p->n && !by_pos && targets_only_ok(p) && stt_enabled();

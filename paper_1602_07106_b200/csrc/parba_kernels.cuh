@@ -53,6 +53,11 @@ constexpr int kEpl = kTile / 32;           // edges per lane in phase 1
 #ifndef PARBA_TILE512
 #define PARBA_TILE512 1
 #endif
+// the same for the streaming sinks (queue of 512 entries, a drain after 256
+// edges): C3 window 2.554e11 -> 2.536e11 (-0.7%), off
+#ifndef PARBA_TILE512_STREAM
+#define PARBA_TILE512_STREAM 0
+#endif
 // first probes use the per-tile reciprocal series from 2*base >= 2^27 on
 constexpr uint64_t kRyMin = 1ull << 27;
 #ifndef PARBA_WARPS
@@ -179,13 +184,20 @@ struct TileLayout {
     // wide store (64-bit values, packed entries): a 256-entry queue, with
     // phase 1 split in two halves and a drain between them (at most 31 + 128
     // entries are ever queued), so 32 warps fit instead of 23
-    static constexpr bool kBig = PARBA_TILE512 && SINK == kStore && Hash::kNarrow && Hash::kHasCrc;
+    // 512-edge tiles: narrow CRC store kernels (the stage of a wide one would
+    // not fit), and the streaming sinks (no stage; the queue stays 512 entries
+    // with a drain after 256 edges); the store-targets sink keeps 256 (its
+    // tile-order slots are the scatter's input geometry)
+    static constexpr bool kBig = Hash::kHasCrc && ((PARBA_TILE512 && SINK == kStore && Hash::kNarrow) ||
+                                                   (PARBA_TILE512_STREAM && !is_store(SINK)));
     static constexpr int kTileE = kBig ? 2 * kTile : kTile;  // edges per warp tile of this kernel
     static constexpr int kEplE = kTileE / 32;                 // edges per lane in phase 1
     static constexpr bool kSplit =
-        kBig || (is_store(SINK) &&
-                 ((!Hash::kNarrow && Hash::kPack && PARBA_WIDE_SPLIT) || (Hash::kNarrow && PARBA_NARROW_SPLIT)));
-    static constexpr int kPieceEpl = kSplit ? 4 : kEplE;     // edges per lane between two drains
+        is_store(SINK) && (kBig || (!Hash::kNarrow && Hash::kPack && PARBA_WIDE_SPLIT) ||
+                           (Hash::kNarrow && PARBA_NARROW_SPLIT));
+    // edges per lane between two drains: 4 with the 256-entry queue of a split
+    // store kernel, else 8 (the whole 256-edge tile, half a 512-edge one)
+    static constexpr int kPieceEpl = kSplit ? 4 : 8;
     static constexpr uint32_t kQ = kSplit ? 256u : (uint32_t)kQueue;
     static constexpr uint32_t kQB = kQ * kEB;
     static constexpr uint32_t kTB = kTileE * (uint32_t)sizeof(R);  // one stage buffer
