@@ -55,6 +55,9 @@ constexpr int kEpl = kTile / 32;           // edges per lane in phase 1
 #endif
 // the same for the streaming sinks (queue of 512 entries, a drain after 256
 // edges): C3 window 2.554e11 -> 2.536e11 (-0.7%), off
+#ifndef PARBA_LAZY_DRAIN
+#define PARBA_LAZY_DRAIN 1
+#endif
 #ifndef PARBA_TILE512_STREAM
 #define PARBA_TILE512_STREAM 0
 #endif
@@ -696,8 +699,15 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
                 if constexpr (P < NP) {
                     if constexpr (decltype(ry_c)::value != 0 && (P * PE) % 8 == 0) ry_setup(base, (P * PE) / 8);
                     if constexpr (P > 0) {
+                        // the next piece pushes at most 32 * PE entries: drain only
+                        // when the ring could not take them (larger drains run more
+                        // of their steps in the unrolled loop)
                         __syncwarp();
+#if PARBA_LAZY_DRAIN
+                        if (tailb - headb > ((L::kQ - 32u * PE) << L::kLgEB)) drain();
+#else
                         drain();
+#endif
                     }
                     phase1(full_c, ry_c, base, cb, std::integral_constant<int, P * PE>{},
                            std::integral_constant<int, (P + 1) * PE>{});
