@@ -220,6 +220,7 @@ int launch_tiles_t(const DevParams &dp, uint64_t lo, uint64_t hi, const SinkArgs
             a.t32_geom[1] = 0;
             a.t32_geom[2] = (uint64_t)warps;
             a.t32_geom[3] = grid;
+            a.t32_geom[4] = kTile;
         }
         if (is_targets(SINK)) {  // one launch; every warp owns capw slots
             if (a1 != hi) return fail(PARBA_ECUDA, "targets pass needs one launch");
@@ -575,6 +576,7 @@ struct PartScratch {
     AsyncBuf t32, srt, H, O, tmp, items;
     size_t tmp_bytes = 0;
     uint64_t stride_nw = 0, stride_ntiles = 0;  // store-targets input: tile-order slots (bucket_scatter_kernel)
+    int stride_tlg = 8;                         //   log2 of that launch's tile edges
     uint64_t max_items = 0;
     int shift = 0, nb = 0, spb_lg = 0;
     uint32_t bw = 0;   // bucket width (nodes)
@@ -649,11 +651,11 @@ struct PartScratch {
             if (off16)
                 bucket_scatter_kernel<kScatterThreads, true><<<cols, kScatterThreads, kScatterSmem, st>>>(
                     (const uint32_t *)t32.p, len, wpc, groups, capw, bdiv, wb, nbw, (const uint32_t *)O.p,
-                    (uint32_t *)srt.p, stride_nw, stride_ntiles, bw);
+                    (uint32_t *)srt.p, stride_nw, stride_ntiles, bw, stride_tlg);
             else
                 bucket_scatter_kernel<kScatterThreads><<<cols, kScatterThreads, kScatterSmem, st>>>(
                     (const uint32_t *)t32.p, len, wpc, groups, capw, bdiv, wb, nbw, (const uint32_t *)O.p,
-                    (uint32_t *)srt.p, stride_nw, stride_ntiles);
+                    (uint32_t *)srt.p, stride_nw, stride_ntiles, 0, stride_tlg);
             CUDA_TRY(cudaGetLastError());
         }
         count_plan_kernel<<<1, kHistThreads, 0, st>>>((const uint32_t *)O.p, (const uint32_t *)H.p, cols, nb,
@@ -722,7 +724,7 @@ int count_partitioned(const parba_params_t *p, const DevParams &dp, uint64_t lo,
     for (uint64_t b0 = lo; b0 < hi;) {
         uint64_t b1 = hi - b0 > batch ? (b0 / kTile) * kTile + batch : hi;
         if (b1 > hi) b1 = hi;
-        uint64_t geom[4] = {};
+        uint64_t geom[5] = {};
         SinkArgs a{};
         a.t32 = (uint32_t *)ps.t32.p;
         a.hist = (uint32_t *)ps.H.p;  // the tile launch writes the bucket histogram of each CTA's region
@@ -743,7 +745,9 @@ int count_partitioned(const parba_params_t *p, const DevParams &dp, uint64_t lo,
         if (stt && ps.nb <= kHistBuckets) {
             rc = launch_store_targets(p, dp, b0, b1, a, probes, st);
             ps.stride_nw = geom[2] * geom[3];                       // warps of the launch
-            ps.stride_ntiles = (b1 - 1) / kTile - b0 / kTile + 1;   // tiles of the batch
+            const uint64_t te = geom[4];                            // its tile (256 or 512 edges)
+            ps.stride_tlg = te == 512 ? 9 : 8;
+            ps.stride_ntiles = (b1 - 1) / te - b0 / te + 1;         // tiles of the batch
         } else {
             rc = K >= p->n ? launch_tiles<kTargets>(p, dp, b0, b1, a, probes, st)
                            : launch_tiles<kTargetsK>(p, dp, b0, b1, a, probes, st);

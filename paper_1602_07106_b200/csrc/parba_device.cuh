@@ -431,8 +431,8 @@ __device__ __forceinline__ void build_byte_tables(uint32_t *tab, int nb, uint32_
     }
 }
 
-__device__ __forceinline__ void build_chunk_tables(uint32_t *tab, int nc, uint32_t k0) {
-    for (int e = threadIdx.x; e < nc * 2048; e += blockDim.x) {
+__device__ __forceinline__ void build_chunk_tables(uint32_t *tab, int nc, uint32_t k0, int words = 1 << 30) {
+    for (int e = threadIdx.x; e < nc * 2048 && e < words; e += blockDim.x) {
         const int k = e >> 11, x = e & 2047;
         uint32_t v = 0;
         if ((uint32_t)x < (1u << chunk_width(k)))
@@ -445,10 +445,11 @@ __device__ __forceinline__ void build_chunk_tables(uint32_t *tab, int nc, uint32
 // XOR of crc(0, 1 << (s + j)) over the set bits j of x, so the 64 single-bit
 // values are computed once (bitwise) and every entry costs <= 11 XORs -- for
 // kernels with many short-lived CTAs.  bits: 64 words of shared scratch.
-__device__ __forceinline__ void build_chunk_tables_linear(uint32_t *tab, int nc, uint32_t *bits, uint32_t k0 = 0u) {
+__device__ __forceinline__ void build_chunk_tables_linear(uint32_t *tab, int nc, uint32_t *bits, uint32_t k0 = 0u,
+                                                          int words = 1 << 30) {
     if (threadIdx.x < 64) bits[threadIdx.x] = crc32c_u64_bitwise(0u, 1ull << threadIdx.x);
     __syncthreads();
-    for (int e = threadIdx.x; e < nc * 2048; e += blockDim.x) {
+    for (int e = threadIdx.x; e < nc * 2048 && e < words; e += blockDim.x) {
         const int k = e >> 11;
         uint32_t x = (uint32_t)(e & 2047), v = 0;
         if (x < (1u << chunk_width(k))) {
@@ -581,14 +582,18 @@ struct HashCrc {
     static constexpr bool kNarrow = NC <= 3;
     static constexpr bool kR31 = NC == 2;
     static constexpr bool kPack = NC <= 5;       // every value < 2^52
-    static constexpr int kTableWords = kChunks * 2048;
+    // 2048 entries per table; the last table of the 3-table (32-bit) layout
+    // holds a 10-bit chunk, so it is 1024 entries
+    static constexpr int kTableWords = kChunks == 3 ? 2 * 2048 + 1024 : kChunks * 2048;
     using R = typename std::conditional<kNarrow, uint32_t, uint64_t>::type;
-    __device__ __forceinline__ static void build(uint32_t *tab, uint32_t k0) { build_chunk_tables(tab, kChunks, k0); }
+    __device__ __forceinline__ static void build(uint32_t *tab, uint32_t k0) {
+        build_chunk_tables(tab, kChunks, k0, kTableWords);
+    }
     // the same tables from the 64 single-bit CRCs (bits: 64 words of shared
     // scratch; includes a __syncthreads): <= 11 XORs per entry instead of a
     // 64-step bitwise CRC
     __device__ __forceinline__ static void build_linear(uint32_t *tab, uint32_t *bits, uint32_t k0) {
-        build_chunk_tables_linear(tab, kChunks, bits, k0);
+        build_chunk_tables_linear(tab, kChunks, bits, k0, kTableWords);
     }
     __device__ __forceinline__ static R from_crc(uint32_t c0, R r, const DevParams &p) {
         if constexpr (NC == 2) return mod_fp31(c0, c0 ^ p.k01, r);

@@ -124,7 +124,8 @@ __global__ void __launch_bounds__(T, 1) bucket_scatter_kernel(const uint32_t *__
                                                            Magic32 bdiv, int wb, int nbw,
                                                            const uint32_t *__restrict__ O,
                                                            uint32_t *__restrict__ out, uint64_t nw,
-                                                           uint64_t ntiles, uint32_t bw = 0) {
+                                                           uint64_t ntiles, uint32_t bw = 0, int tlg = 8) {
+    const uint32_t kTile = 1u << tlg;  // strided input: edges per tile of the targets launch (256 or 512)
     constexpr int BPT = kHistBuckets / T;  // buckets per thread in the scan
     constexpr int PER = kScatterTile / T;  // entries per thread and sub-tile
     static_assert(BPT * T == kHistBuckets && PER % 4 == 0, "scatter shape");
@@ -167,7 +168,7 @@ __global__ void __launch_bounds__(T, 1) bucket_scatter_kernel(const uint32_t *__
             const uint64_t e = base + 4ull * (threadIdx.x + (uint64_t)h * T);
             nx[h] = make_uint4(kEmptyTarget, kEmptyTarget, kEmptyTarget, kEmptyTarget);
             if (nw) {
-                const uint32_t x = (uint32_t)(e / kTile);  // logical tile of this CTA
+                const uint32_t x = (uint32_t)(e >> tlg);  // logical tile of this CTA
                 const uint32_t k = __float2uint_rz(__fmaf_rn((float)x, inv_wpc, 0.5f * inv_wpc));
                 const uint64_t tile = (uint64_t)k * nw + c0 + (x - k * wpc);
                 if (e < s1 && tile < ntiles)

@@ -55,6 +55,11 @@ constexpr int kEpl = kTile / 32;           // edges per lane in phase 1
 #endif
 // the same for the streaming sinks (queue of 512 entries, a drain after 256
 // edges): C3 window 2.554e11 -> 2.536e11 (-0.7%), off
+// the store-targets sink (the full histogram's targets pass, the host-array
+// pipeline) on 512-edge tiles too; the scatter takes the tile size as a parameter
+#ifndef PARBA_TILE512_ST
+#define PARBA_TILE512_ST 1
+#endif
 #ifndef PARBA_LAZY_DRAIN
 #define PARBA_LAZY_DRAIN 1
 #endif
@@ -166,7 +171,7 @@ struct SinkArgs {
     uint64_t klim;                         // targets: only targets < klim are kept
     int by_pos;                            // targets, degree sequence: emit positions (full counts)
     uint64_t t32_cap;                      // host side: slots of t32
-    uint64_t *t32_geom;                    // host side: {slots filled, capw, warps per CTA, CTAs}
+    uint64_t *t32_geom;                    // host side: {slots filled, capw, warps per CTA, CTAs, tile edges}
 };
 
 // Shared-memory layout of a tile CTA (dynamic smem, W warps):
@@ -187,12 +192,13 @@ struct TileLayout {
     // wide store (64-bit values, packed entries): a 256-entry queue, with
     // phase 1 split in two halves and a drain between them (at most 31 + 128
     // entries are ever queued), so 32 warps fit instead of 23
-    // 512-edge tiles: narrow CRC store kernels (the stage of a wide one would
-    // not fit), and the streaming sinks (no stage; the queue stays 512 entries
-    // with a drain after 256 edges); the store-targets sink keeps 256 (its
-    // tile-order slots are the scatter's input geometry)
-    static constexpr bool kBig = Hash::kHasCrc && ((PARBA_TILE512 && SINK == kStore && Hash::kNarrow) ||
-                                                   (PARBA_TILE512_STREAM && !is_store(SINK)));
+    // 512-edge tiles: narrow CRC store and store-targets kernels (the stage of
+    // a wide one would not fit), optionally the streaming sinks (no stage; the
+    // queue stays 512 entries with a drain after 256 edges)
+    static constexpr bool kBig =
+        Hash::kHasCrc && ((PARBA_TILE512 && SINK == kStore && Hash::kNarrow) ||
+                          (PARBA_TILE512_ST && SINK == kStoreT && Hash::kNarrow) ||
+                          (PARBA_TILE512_STREAM && !is_store(SINK)));
     static constexpr int kTileE = kBig ? 2 * kTile : kTile;  // edges per warp tile of this kernel
     static constexpr int kEplE = kTileE / 32;                 // edges per lane in phase 1
     static constexpr bool kSplit =
