@@ -60,6 +60,10 @@ constexpr int kEpl = kTile / 32;           // edges per lane in phase 1
 #ifndef PARBA_TILE512_ST
 #define PARBA_TILE512_ST 1
 #endif
+// edges per lane of a phase-1 piece in the split store kernels (A/B knob)
+#ifndef PARBA_PIECE
+#define PARBA_PIECE 4
+#endif
 #ifndef PARBA_LAZY_DRAIN
 #define PARBA_LAZY_DRAIN 1
 #endif
@@ -103,6 +107,9 @@ constexpr uint32_t kWinSmem = PARBA_WIN_SMEM;
 // test (2: +0.35% at C2, profiles/r02_ab_window_smem_and_unroll.txt)
 #ifndef PARBA_P2_UNROLL
 #define PARBA_P2_UNROLL 2
+#endif
+#ifndef PARBA_P2_UNROLL_STREAM
+#define PARBA_P2_UNROLL_STREAM 0  // the same for the streaming sinks (A/B)
 #endif
 #ifndef PARBA_NBUF
 #define PARBA_NBUF 2
@@ -206,7 +213,7 @@ struct TileLayout {
                            (Hash::kNarrow && PARBA_NARROW_SPLIT));
     // edges per lane between two drains: 4 with the 256-entry queue of a split
     // store kernel, else 8 (the whole 256-edge tile, half a 512-edge one)
-    static constexpr int kPieceEpl = kSplit ? 4 : 8;
+    static constexpr int kPieceEpl = kSplit ? PARBA_PIECE : 8;
     static constexpr uint32_t kQ = kSplit ? 256u : (uint32_t)kQueue;
     static constexpr uint32_t kQB = kQ * kEB;
     static constexpr uint32_t kTB = kTileE * (uint32_t)sizeof(R);  // one stage buffer
@@ -675,7 +682,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
         auto drain = [&]() {
 #if PARBA_P2_UNROLL >= 2
             // two refill+probe steps per loop test while >= 2 warps of entries wait
-            if (is_store(SINK) && tailb - headb >= ((64u * NS) << L::kLgEB)) {
+            if ((is_store(SINK) || PARBA_P2_UNROLL_STREAM) && tailb - headb >= ((64u * NS) << L::kLgEB)) {
                 const uint32_t lim2 = tailb - ((64u * NS) << L::kLgEB);
                 do {
                     refill(std::true_type{});
@@ -697,7 +704,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
         // between them (the 256-entry queue of the wide store)
         auto run_phase1 = [&](auto full_c, auto ry_c) {
             constexpr int PE = L::kPieceEpl, NP = kEpl / PE;
-            static_assert(NP * PE == kEpl && NP <= 4 && (8 % PE == 0 || PE % 8 == 0), "phase-1 pieces");
+            static_assert(NP * PE == kEpl && NP <= 8 && (8 % PE == 0 || PE % 8 == 0), "phase-1 pieces");
             // piece P: the lane's edges [P*PE, (P+1)*PE); a new reciprocal
             // series at every 8th edge; a drain between pieces
             auto piece = [&](auto p_c) {
@@ -723,6 +730,10 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
             piece(std::integral_constant<int, 1>{});
             piece(std::integral_constant<int, 2>{});
             piece(std::integral_constant<int, 3>{});
+            piece(std::integral_constant<int, 4>{});
+            piece(std::integral_constant<int, 5>{});
+            piece(std::integral_constant<int, 6>{});
+            piece(std::integral_constant<int, 7>{});
         };
         if (base >= lo && base + kTile <= hi) {
             using I0 = std::integral_constant<int, 0>;
