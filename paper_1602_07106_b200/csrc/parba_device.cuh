@@ -363,8 +363,20 @@ constexpr uint64_t kOneStageMin = 1ull << 28;
 // is floor(h/r) or floor(h/r) + 1: t = hlo - q*r (mod 2^32) lies in [-r, r)
 // and min(t, t + r) is the remainder, as in mod_fp31_y.  4 FP64 instructions
 // instead of 7 (and no rd).
+// PARBA_Y1_I2F: hd by one 64-bit I2F (XU pipe) instead of two magic-exponent
+// conversions and an FMA (2 MOV + 2 DADD + DFMA): same single rounding (A/B)
+#ifndef PARBA_Y1_I2F
+#define PARBA_Y1_I2F 1
+#endif
+__device__ __forceinline__ double h_to_f64(uint32_t hhi, uint32_t hlo) {
+#if PARBA_Y1_I2F
+    return __ull2double_rn(((uint64_t)hhi << 32) | hlo);
+#else
+    return fma(u32_to_f64_magic(hhi), 0x1p32, u32_to_f64_magic(hlo));
+#endif
+}
 __device__ __forceinline__ uint32_t mod_fp31_y1(uint32_t hhi, uint32_t hlo, uint32_t r, double y) {
-    const double hd = fma(u32_to_f64_magic(hhi), 0x1p32, u32_to_f64_magic(hlo));  // h, one rounding
+    const double hd = h_to_f64(hhi, hlo);  // h, one rounding
     const uint32_t nq = (uint32_t)__double2loint(fma(-hd, y, 0x1.8p52));             // -q mod 2^32
     const uint32_t t = hlo + nq * r;
     return min(t, t + r);
@@ -376,7 +388,7 @@ __device__ __forceinline__ uint32_t mod_fp31_y1(uint32_t hhi, uint32_t hlo, uint
 // the wrapping product is harmless); one correction.  4 FP64 instructions
 // and ~8 integer ones instead of ~13 FP64 ones.
 __device__ __forceinline__ uint64_t mod_fp_y1w(uint32_t hhi, uint32_t hlo, uint64_t r, double y) {
-    const double hd = fma(u32_to_f64_magic(hhi), 0x1p32, u32_to_f64_magic(hlo));
+    const double hd = h_to_f64(hhi, hlo);
     const uint64_t q = (uint64_t)__double_as_longlong(fma(hd, y, 0x1p52)) - 0x4330000000000000ull;
     int64_t t = (int64_t)((((uint64_t)hhi << 32) | hlo) - q * r);
     t += (t < 0) ? (int64_t)r : 0;
