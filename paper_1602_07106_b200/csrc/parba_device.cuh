@@ -351,6 +351,9 @@ __device__ __forceinline__ uint32_t mod_fp32_y(uint32_t hhi, uint32_t hlo, uint3
 #ifndef PARBA_ONESTAGE_WIDE
 #define PARBA_ONESTAGE_WIDE 0
 #endif
+#ifndef PARBA_ONESTAGE_WIDE_STORE
+#define PARBA_ONESTAGE_WIDE_STORE 1
+#endif
 constexpr uint64_t kOneStageMin = 1ull << 28;
 // One-stage form for 2^28 <= r < 2^31 (phase 1 of 2-chunk tiles with 2*base
 // >= kOneStageMin): q = round(v), v = hd*y, from h rounded to a double hd
@@ -628,6 +631,8 @@ struct HashCrc {
     // One-stage remainder (mod_fp31_y1 / mod_fp_y1w) for first probes of
     // tiles with 2*base >= kOneStageMin (every r >= 2^28): needs no rd
     static constexpr bool kHasRy1 = PARBA_ONESTAGE && (NC <= 3 || (NC <= 5 && PARBA_ONESTAGE_WIDE));
+    // 4- and 5-chunk store kernels take it too (wide store +1.4%; the window -0.55%)
+    static constexpr bool kHasRy1Store = PARBA_ONESTAGE && NC <= 5 && PARBA_ONESTAGE_WIDE_STORE;
     __device__ __forceinline__ static R from_crc_ry1(uint32_t c0, R r, double y, const DevParams &p) {
         if constexpr (NC == 2) return mod_fp31_y1(c0, c0 ^ p.k01, r, y);
         else return (R)mod_fp_y1w(c0, c0 ^ p.k01, (uint64_t)r, y);
@@ -647,6 +652,7 @@ struct HashCrcBytes {
     template <class T>
     __device__ __forceinline__ static T from_crc_ry(uint32_t, T r, double, double, const DevParams &) { return r; }
     static constexpr bool kHasRy1 = false;
+    static constexpr bool kHasRy1Store = false;
     template <class T>
     __device__ __forceinline__ static T from_crc_ry1(uint32_t, T r, double, const DevParams &) { return r; }
     static constexpr bool kNarrow = false;
@@ -668,6 +674,7 @@ struct HashSimple {
     template <class T>
     __device__ __forceinline__ static T from_crc_ry(uint32_t, T r, double, double, const DevParams &) { return r; }
     static constexpr bool kHasRy1 = false;
+    static constexpr bool kHasRy1Store = false;
     template <class T>
     __device__ __forceinline__ static T from_crc_ry1(uint32_t, T r, double, const DevParams &) { return r; }
     static constexpr bool kNarrow = NARROW;

@@ -285,6 +285,8 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
     constexpr bool NARROW = Hash::kNarrow;
     using L = TileLayout<Hash, SINK>;
     constexpr int kTile = L::kTileE;  // this kernel's tile (shadows the default)
+    // one-stage first probes: per hash class, and for every store kernel up to 5 chunks
+    constexpr bool kRy1 = Hash::kHasRy1 || (is_store(SINK) && Hash::kHasRy1Store);
     constexpr int kEpl = L::kEplE;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
@@ -632,7 +634,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
             const R r0 = (R)(2 * base) + (R)(2 * j + 1);
             R r1;
             if constexpr (RY == 2) {
-                if constexpr (Hash::kHasRy1)
+                if constexpr (kRy1)
                     r1 = Hash::from_crc_ry1(cb ^ clow_s[j], r0, fma(-((k & 7) - 3.5), s64, c), p);
             } else if constexpr (RY == 1) {
                 static_assert(kEpl % 8 == 0, "one series centre per 8 edges of a lane");
@@ -739,7 +741,7 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
             using I0 = std::integral_constant<int, 0>;
             using I1 = std::integral_constant<int, 1>;
             using I2 = std::integral_constant<int, 2>;
-            if constexpr (Hash::kHasRy1) {
+            if constexpr (kRy1) {
                 if (2 * base >= kOneStageMin) run_phase1(std::true_type{}, I2{});
                 else if (2 * base >= kRyMin) run_phase1(std::true_type{}, I1{});
                 else run_phase1(std::true_type{}, I0{});
