@@ -67,6 +67,9 @@ constexpr int kEpl = kTile / 32;           // edges per lane in phase 1
 #ifndef PARBA_LAZY_DRAIN
 #define PARBA_LAZY_DRAIN 1
 #endif
+#ifndef PARBA_LAZY_END
+#define PARBA_LAZY_END 0
+#endif
 #ifndef PARBA_TILE512_STREAM
 #define PARBA_TILE512_STREAM 0
 #endif
@@ -755,7 +758,14 @@ tile_kernel(DevParams p, uint64_t lo, uint64_t hi, uint64_t tile0, uint64_t ntil
             run_phase1(std::false_type{}, std::integral_constant<int, 0>{});
         }
         __syncwarp();
-        drain();
+        // the end-of-tile drain is lazy too (PARBA_LAZY_END; bit 0: store
+        // sinks, bit 1: streaming sinks): entries stay queued while the ring
+        // can still take the next tile's first piece
+        if constexpr (((PARBA_LAZY_END & 1) && is_store(SINK) && L::kSplit) || ((PARBA_LAZY_END & 2) && !is_store(SINK))) {
+            if (tailb - headb > ((L::kQ - 32u * L::kPieceEpl) << L::kLgEB)) drain();
+        } else {
+            drain();
+        }
         // ---- store: flush the oldest tile in flight once none of its chains runs
         if constexpr (is_store(SINK)) {
             if (have_prev) {
