@@ -582,6 +582,12 @@ def main() -> None:
                         routed = pb.parallel.RoutedCounts.try_create(q, device=dev)
                     if routed is not None:
                         routed.run(a, b)  # warm-up of the routed kernels and the peer mappings
+                        # the slices must hold every endpoint before the path is timed
+                        tot = (routed.own[: routed.count].to(torch.int64) & 0xFFFFFFFF).sum().reshape(1)
+                        dist.all_reduce(tot)
+                        if int(tot.item()) != 2 * q.m:  # (the same on every rank) count locally + reduce instead
+                            routed.close()
+                            routed = None
                 barrier()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
