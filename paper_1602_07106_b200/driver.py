@@ -276,6 +276,9 @@ def _run_fused_ranks(p: GenParams, consumer, batches, rank: int, ws: int, resolu
             with routed:
                 routed.run(a, b, probes=prb)
                 counts = routed.gather()  # int64, the whole histogram on every rank
+            if int(counts.sum().item()) != 2 * (p.m - p.m0):  # every endpoint landed in a slice
+                raise GenerationError("owner-routed degree counts lost endpoints (peer atomics); "
+                                      "set PARBA_ROUTED=0 to count locally and reduce")
         else:
             if K:
                 counts = torch.zeros(K, dtype=torch.int32 if full else torch.int64, device=dev)
