@@ -7,7 +7,9 @@
 // engine here is warp-centric:
 //
 //   phase 1  every lane takes the first probe of 8 edges of a 256-edge,
-//            256-aligned warp tile.  r0 = 2i+1 = 2B + (2j+1), so by CRC
+//            256-aligned warp tile (16 edges of a 512-edge tile in the narrow
+//            CRC store and store-targets kernels, in four pieces with lazy
+//            drains between them: TileLayout::kBig).  r0 = 2i+1 = 2B + (2j+1), so by CRC
 //            linearity crc(0,r0) = crc(0,2B) ^ crc(0,2j+1): a warp-uniform
 //            value per tile XOR a constant read from a 1 KB smem table
 //            (conflict-free, lane-consecutive) -- the first probe (half of
